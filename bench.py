@@ -1,0 +1,433 @@
+#!/usr/bin/env python
+"""Barnes-Hut step benchmark (BASELINE.json metric: BH interactions/s and
+steps/s; + % of FP32 peak for the traversal, % of HBM for build and sort).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config cfg2]
+
+A step is one full KDK leapfrog step of the hot path (simulation.py:492-502):
+kick+drift+bounds, Morton keys, radix sort, body permutation, tree build with
+moments, traversal, kick.  Default workload = BASELINE config 2 (Plummer
+N=1e6, seed 2, fp32, theta=0.6, eps=1e-3, leaf size 16, dt=1e-3).  Synthetic
+inputs from the reference's own Plummer sampler (bit-identical restatement).
+
+`--impl reference` times the reference algorithm on the host CPU (the oracle
+port: the reference is Python/numba and cannot travel to the GPU box), with
+all host threads, on a bounded target sample per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "cfg1": dict(n=100_000, seed=1, theta=0.5, eps=1e-3, leaf=16, dt=1e-3, kind="plummer"),
+    "cfg2": dict(n=1_000_000, seed=2, theta=0.6, eps=1e-3, leaf=16, dt=1e-3, kind="plummer"),
+    "cfg3": dict(n=10_000_000, seed=3, theta=0.6, eps=1e-4, leaf=32, dt=5e-4, kind="two"),
+}
+FLOPS_PP = 20
+FLOPS_PC = 51
+SORT_BYTES_PER_BODY = 192  # 8 passes x (8 B key + 4 B index) x (read + write)
+L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
+
+
+def build_bytes_per_body(cells_per_body: float) -> float:
+    """243 + 32*(C/N - 1.48) algorithmic bytes per body."""
+    return 243.0 + 32.0 * (cells_per_body - 1.48)
+
+
+def measured_peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        d["source"] = "measured"
+        return d
+    return {"hbm_gbs": 6650.0, "source": "fallback"}
+
+
+def make_bodies(cfg: dict):
+    from paper_2203_08966_b200.initcond import colliding_plummers, make_rng, plummer_cluster
+
+    if cfg["kind"] == "plummer":
+        b = plummer_cluster(cfg["n"], make_rng(cfg["seed"]), 1.0)
+    else:
+        b = colliding_plummers(cfg["n"] // 2, cfg["seed"])
+    return b
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+
+    QUERY = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows: list[list[str]] = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        rows = [r for r in self.rows if len(r) >= 7]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+
+        sm = [num(r[0]) for r in rows if num(r[0]) is not None]
+        mx = [num(r[1]) for r in rows if num(r[1]) is not None]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[3 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def dist_setup():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ---------------------------------------------------------------- our arm
+
+
+def run_ours(args, cfg) -> dict | None:
+    import torch
+    import torch.distributed as dist
+
+    from paper_2203_08966_b200.engine import Engine
+
+    ws, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    b = make_bodies(cfg)
+    n = len(b)
+    eng = Engine("fp32", local)
+    pos = eng.bodies_tensor(b.position, b.mass)
+    vel = eng.vec_tensor(b.velocity)
+    eng.sim_load(pos, vel)
+    theta, eps, leaf, dt = cfg["theta"], cfg["eps"], cfg["leaf"], cfg["dt"]
+    eng.sim_forces(theta, eps, leaf, record_work=False)
+    peak_fp32 = eng.ffma_peak_tflops()
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    for _ in range(args.warmup):
+        eng.sim_step(dt, theta, eps, leaf, 1)
+    eng.check()
+
+    # ---- device-timed steps (inputs resident in HBM)
+    eng.timing(True)
+    eng.timing_reset()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    total_ms = 0.0
+    pp = pc = 0
+    cells = 0
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            flush.zero_()  # L2 flush between timed iterations (outside the events)
+            if ws > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            ev0.record()
+            eng.sim_step(dt, theta, eps, leaf, 1)
+            ev1.record()
+            torch.cuda.synchronize()
+            total_ms += ev0.elapsed_time(ev1)
+            st = eng.stats()
+            pp += st.pp
+            pc += st.pc
+            cells = st.n_cells
+    phases = eng.timing_get()
+    launches = eng.launches()
+    eng.timing(False)
+    eng.check()
+
+    # ---- end to end through the public API with host buffers
+    import torch as _t
+
+    hpos = _t.empty((n, 4), dtype=_t.float32).pin_memory()
+    hvel = _t.empty((n, 4), dtype=_t.float32).pin_memory()
+    hacc = _t.empty((n, 4), dtype=_t.float32).pin_memory()
+    dpos = _t.empty((n, 4), dtype=_t.float32, device=dev)
+    dvel = _t.empty_like(dpos)
+    dacc = _t.empty_like(dpos)
+    eng.sim_store(dpos, dvel, dacc)
+    hpos.copy_(dpos)
+    hvel.copy_(dvel)
+    hacc.copy_(dacc)
+    torch.cuda.synchronize()
+    e2e_ms = 0.0
+    e2e_inter = 0
+    for _ in range(args.steps):
+        flush.zero_()
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev0.record()
+        dpos.copy_(hpos, non_blocking=True)
+        dvel.copy_(hvel, non_blocking=True)
+        dacc.copy_(hacc, non_blocking=True)
+        eng.sim_load(dpos, dvel, acc=dacc)
+        eng.sim_step(dt, theta, eps, leaf, 1)
+        eng.sim_store(dpos, dvel, dacc)
+        hpos.copy_(dpos, non_blocking=True)
+        hvel.copy_(dvel, non_blocking=True)
+        hacc.copy_(dacc, non_blocking=True)
+        ev1.record()
+        torch.cuda.synchronize()
+        e2e_ms += ev0.elapsed_time(ev1)
+        st = eng.stats()
+        e2e_inter += st.pp + st.pc
+    eng.check()
+
+    # ---- max over ranks
+    t = torch.tensor([total_ms, e2e_ms], dtype=torch.float64, device=dev)
+    work = torch.tensor([pp + pc, e2e_inter, pp, pc], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(work, op=dist.ReduceOp.SUM)
+    total_ms, e2e_ms = float(t[0]), float(t[1])
+    inter_all, e2e_all = float(work[0]), float(work[1])
+    result = None
+    if rank == 0:
+        peaks = measured_peaks()
+        sec = total_ms / 1e3
+        walk_s = phases["walk"] / 1e3
+        walk_flops = (FLOPS_PP * pp + FLOPS_PC * pc) / args.steps
+        walk_tf = walk_flops / (walk_s / args.steps) / 1e12 if walk_s > 0 else None
+        build_s = phases["build"] / 1e3 / args.steps
+        sort_s = phases["sort"] / 1e3 / args.steps
+        bpb = build_bytes_per_body(cells / n)
+        build_gbs = bpb * n / build_s / 1e9 if build_s > 0 else None
+        sort_gbs = SORT_BYTES_PER_BODY * n / sort_s / 1e9 if sort_s > 0 else None
+        hbm = float(peaks["hbm_gbs"])
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "walk_traffic.json")
+        if os.path.exists(tp):
+            with open(tp) as f:
+                traffic = json.load(f).get(args.config)
+        result = {
+            "metric": "BH interactions/s (N=1e6 Plummer, theta=0.6, L=16, full KDK step)",
+            "value": inter_all / sec,
+            "unit": "interactions/s",
+            "n_gpus": ws,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": total_ms / args.steps,
+            "steps_per_s": args.steps / sec,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f32",
+            "data": "synthetic: reference plummer_cluster sampler (bit-identical restatement), seed %d" % cfg["seed"],
+            "config": {"workload": args.config, "n_bodies": n, "theta": theta, "eps": eps,
+                       "leaf_size": leaf, "dt": dt, "precision": "fp32",
+                       "parallelism": "replica per GPU" if ws > 1 else "single GPU",
+                       "l2": "flushed between timed steps (256 MB write)"},
+            "interactions_per_step": inter_all / args.steps / ws,
+            "pp_per_step": pp / args.steps,
+            "pc_per_step": pc / args.steps,
+            "cells": cells,
+            "phase_ms_per_step": {k: v / args.steps for k, v in phases.items()},
+            "roofline": {"bound": "fp32", "kernel": "k_walk_f32",
+                         "achieved": walk_tf, "peak": peak_fp32, "unit": "TFLOP/s",
+                         "frac": (walk_tf / peak_fp32) if walk_tf else None,
+                         "peak_source": "FFMA microbenchmark on this GPU (bh_ffma_peak); MEASURED_PEAKS.json has no FP32 entry",
+                         "flops_per_unit": {"pp": FLOPS_PP, "pc": FLOPS_PC},
+                         "traffic": traffic},
+            "roofline_build": {"bound": "hbm", "achieved": build_gbs, "peak": hbm, "unit": "GB/s",
+                               "frac": build_gbs / hbm if build_gbs else None,
+                               "bytes_per_body": bpb, "peak_source": peaks.get("source")},
+            "roofline_sort": {"bound": "hbm", "achieved": sort_gbs, "peak": hbm, "unit": "GB/s",
+                              "frac": sort_gbs / hbm if sort_gbs else None,
+                              "bytes_per_body": SORT_BYTES_PER_BODY, "impl": "cub::DeviceRadixSort (onesweep)"},
+            "e2e": {"value": e2e_all / (e2e_ms / 1e3), "unit": "interactions/s",
+                    "h2d_bytes_per_step": 3 * 16 * n, "d2h_bytes_per_step": 3 * 16 * n,
+                    "ms_per_step": e2e_ms / args.steps,
+                    "path": "Engine.sim_load/sim_step/sim_store (C-ABI) from pinned host pos/vel/acc"},
+            "gpu_launches": launches,
+            "gpu_launches_note": "libbh kernels in the timed region (CUB sort/scan kernels not included)",
+            "clocks": clocks.summary(),
+        }
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    eng.close()
+    return result
+
+
+# --------------------------------------------------- CPU (reference) timing
+
+
+def cpu_reference_step(b, cfg, sample_idx, nthreads):
+    """One step of the reference algorithm on the host: bounds, keys, stable
+    sort, take, build_hashed (serial, as the reference), traverse a target
+    sample on all threads, kick/drift.  Returns (seconds extrapolated to the
+    full step, interactions extrapolated, sample seconds)."""
+    from oracle import oracle as orc
+
+    pos = np.asarray(b.position, dtype=np.float32).astype(np.float64)
+    m = np.asarray(b.mass, dtype=np.float32).astype(np.float64)
+    n = len(pos)
+    t0 = time.perf_counter()
+    R = orc.bounds(pos)
+    order = orc.sort_order(orc.morton_keys(pos, R))
+    tree = orc.build_tree(m[order], pos[order], R)
+    t1 = time.perf_counter()
+    totals = np.zeros(2, dtype=np.int64)
+    orc.traverse(tree, pos[sample_idx], cfg["theta"], cfg["eps"], cfg["leaf"], nthreads, totals)
+    t2 = time.perf_counter()
+    a = np.zeros_like(pos)  # kick(dt/2) + drift(dt) on all bodies (integrator.py:37-44)
+    v = np.asarray(b.velocity) + a * (0.5 * cfg["dt"])
+    _ = pos + v * cfg["dt"]
+    t3 = time.perf_counter()
+    scale = n / len(sample_idx)
+    full = (t1 - t0) + (t2 - t1) * scale + (t3 - t2)
+    return full, float(totals.sum()) * scale, t2 - t1
+
+
+def cpu_baseline(cfg, b, budget_s=8.0) -> dict:
+    from oracle import oracle as orc
+
+    nthreads = orc.num_threads()
+    n = len(b)
+    rng = np.random.Generator(np.random.Philox(key=99))
+    probe = rng.choice(n, min(n, 2000), replace=False)
+    _, _, ts = cpu_reference_step(b, cfg, probe, nthreads)
+    s = int(min(n, max(2000, len(probe) * budget_s / max(ts, 1e-3))))
+    sample = np.sort(rng.choice(n, s, replace=False))
+    full, inter, _ = cpu_reference_step(b, cfg, sample, nthreads)
+    return {"value": inter / full, "unit": "interactions/s", "cores": nthreads, "kind": "port",
+            "ms_per_step": full * 1e3,
+            "sample": f"serial keys+sort+build over all {n} bodies, traversal of {s} random targets "
+                      f"on {nthreads} threads extrapolated to {n}, host kick/drift",
+            "cpu": _cpu_model()}
+
+
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_reference(args, cfg) -> dict | None:
+    ws, rank, _ = dist_setup()
+    if rank != 0:
+        return None
+    from oracle import oracle as orc
+
+    b = make_bodies(cfg)
+    n = len(b)
+    nthreads = orc.num_threads()
+    rng = np.random.Generator(np.random.Philox(key=7))
+    probe = rng.choice(n, min(n, 2000), replace=False)
+    _, _, ts = cpu_reference_step(b, cfg, probe, nthreads)
+    # bounded sample so that warmup + steps stays within a few minutes
+    per_step_budget = 150.0 / max(1, args.steps + args.warmup)
+    s = int(min(n, max(1000, len(probe) * per_step_budget / max(ts, 1e-3))))
+    sample = np.sort(rng.choice(n, s, replace=False))
+    for _ in range(args.warmup):
+        cpu_reference_step(b, cfg, sample, nthreads)
+    tot_s = 0.0
+    tot_i = 0.0
+    for _ in range(args.steps):
+        full, inter, _ = cpu_reference_step(b, cfg, sample, nthreads)
+        tot_s += full
+        tot_i += inter
+    value = tot_i / tot_s
+    return {
+        "impl": "reference",
+        "metric": "BH interactions/s (N=1e6 Plummer, theta=0.6, L=16, full KDK step)",
+        "value": value, "unit": "interactions/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": tot_s / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: reference plummer_cluster sampler, seed %d" % cfg["seed"],
+        "config": {"workload": args.config, "n_bodies": n, "theta": cfg["theta"], "eps": cfg["eps"],
+                   "leaf_size": cfg["leaf"], "dt": cfg["dt"]},
+        "cpu_baseline": {"value": value, "unit": "interactions/s", "cores": nthreads, "kind": "port",
+                         "sample": f"per step: serial keys+sort+build over all {n} bodies + traversal of "
+                                   f"{s} targets on {nthreads} threads, extrapolated to {n}",
+                         "cpu": _cpu_model()},
+        "e2e": {"value": value, "unit": "interactions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="cfg2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: W < 3 violates the timing rules; using 3", file=sys.stderr)
+        args.warmup = 3
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        res = run_reference(args, cfg)
+        if res is not None:
+            print(json.dumps(res), flush=True)
+        return
+    res = run_ours(args, cfg)
+    if res is not None:
+        ws, rank, _ = dist_setup()
+        if ws == 1 and not args.no_cpu_baseline:
+            res["cpu_baseline"] = cpu_baseline(cfg, make_bodies(cfg))
+        print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,163 @@
+/*
+ * bh.h -- C-ABI of libbh.so, the B200-native (sm_100a) Barnes-Hut step.
+ *
+ * Plain pointers and sizes only.  Every pointer argument named d_* is a CUDA
+ * device pointer; `stream` is a cudaStream_t (NULL = legacy default stream).
+ * Calls return a bh_status; bh_last_error() gives the message of the last
+ * failure on the calling thread.  Device-side failures (out-of-domain body,
+ * duplicate keys, ...) are latched in a device flag and surface at the next
+ * call that synchronises (bh_check, bh_build_*, bh_sim_*), exactly once.
+ *
+ * Each entry point names the reference interface it replaces
+ * (/root/reference/pkg/src/nbsim/<file>:<line>).  The reference is Python; its
+ * "FFI" for this path is the ctypes binding in paper_2203_08966_b200/_lib.py
+ * (see INTEGRATION.md).
+ *
+ * Layouts.  fp32 mode: bodies are float4 {x, y, z, mass} (16 B), velocities and
+ * accelerations float4 {x, y, z, 0}.  fp64 mode: positions/velocities/
+ * accelerations are double[n][3], masses double[n] -- the reference's own
+ * `Bodies` layout (physics.py:18-51).
+ */
+#ifndef BH_H
+#define BH_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct bh_handle bh_handle;
+
+typedef enum {
+  BH_OK = 0,
+  BH_BAD_ARG = 1,          /* simulation.py:95-113 config validation */
+  BH_OUT_OF_DOMAIN = 2,    /* morton.py:116-118 "outside domain" */
+  BH_DUPLICATE_KEY = 3,    /* hashed.py:477-482 "tree resolution" */
+  BH_UNSORTED = 4,         /* hashed.py:475-476 "sorted" */
+  BH_DEPTH_OVERFLOW = 5,   /* octree.py:144-146 */
+  BH_CUDA_ERROR = 7,
+  BH_NCCL_ERROR = 8,
+  BH_NO_TREE = 9,
+  BH_OUT_OF_MEMORY = 10
+} bh_status;
+
+typedef enum { BH_FP32 = 0, BH_FP64 = 1 } bh_precision;
+
+typedef struct {
+  int64_t n_bodies;
+  int64_t n_cells;       /* cells of the last build (== len(FlatTree)) */
+  int64_t max_level;     /* deepest cell level of the last build */
+  int64_t pp;            /* body-body interactions of the last traversal */
+  int64_t pc;            /* body-cell interactions of the last traversal */
+  int64_t work;          /* pp*WORK_PP + pc*WORK_PC (octree.py:23-25) */
+  int64_t launches;      /* libbh kernels enqueued since the last bh_timing_reset */
+} bh_stats;
+
+/* Phases timed with CUDA events on the caller's stream when timing is on. */
+enum {
+  BH_PHASE_INTEGRATE = 0, /* kick + drift + bounds reduction (+ final kick) */
+  BH_PHASE_KEYS = 1,      /* R + Morton keys */
+  BH_PHASE_SORT = 2,      /* radix sort of (key, index) */
+  BH_PHASE_PERMUTE = 3,   /* body gather into Morton order */
+  BH_PHASE_BUILD = 4,     /* lcp, scan, cell count, emit, moments */
+  BH_PHASE_WALK = 5,      /* traversal */
+  BH_NPHASES = 6
+};
+
+/* ---- lifecycle ---------------------------------------------------------- */
+int bh_create(bh_handle **out, int device, int precision);
+int bh_destroy(bh_handle *h);
+const char *bh_last_error(void);
+int bh_version(void);
+/* Synchronise `stream` and return (and clear) any latched device-side error. */
+int bh_check(bh_handle *h, void *stream);
+
+/* ---- building blocks (reference: morton.py, hashed.py, flattree.py) ----- */
+
+/* morton.py:33-42 DomainBounds.from_positions: *d_R = 1.001*max|x| (or 1.0).
+ * Result stays on the device (no host sync). */
+int bh_bounds_f32(bh_handle *h, const float *d_pos4, int64_t n, double *d_R, void *stream);
+int bh_bounds_f64(bh_handle *h, const double *d_pos3, int64_t n, double *d_R, void *stream);
+
+/* morton.py:109-125 morton_keys: 63-bit keys, fp64 floor quantisation. */
+int bh_morton_f32(bh_handle *h, const float *d_pos4, int64_t n, const double *d_R,
+                  uint64_t *d_keys, void *stream);
+int bh_morton_f64(bh_handle *h, const double *d_pos3, int64_t n, const double *d_R,
+                  uint64_t *d_keys, void *stream);
+
+/* morton.py:128-130 sort_order: stable ascending argsort of 63-bit keys. */
+int bh_sort(bh_handle *h, const uint64_t *d_keys, int64_t n, uint64_t *d_keys_sorted,
+            int64_t *d_perm, void *stream);
+
+/* hashed.py:448-515 build_hashed over Morton-sorted bodies (moments included).
+ * The tree stays in the handle.  Synchronises once (cell count). */
+int bh_build_f32(bh_handle *h, const float *d_pos4_sorted, int64_t n, const double *d_R,
+                 void *stream);
+int bh_build_f64(bh_handle *h, const double *d_pos3_sorted, const double *d_mass_sorted,
+                 int64_t n, const double *d_R, void *stream);
+int bh_tree_size(bh_handle *h, int64_t *n_cells);
+
+/* flattree.py:34-52 FlatTree arrays of the current tree (pre-order).
+ * Any pointer may be NULL to skip that array.  Shapes: centre/com [C][3],
+ * quad [C][6] (xx,xy,xz,yy,yz,zz), children [C][8] (-1 = absent). */
+int bh_export_tree(bh_handle *h, uint64_t *d_key, int8_t *d_level, double *d_centre,
+                   double *d_side, double *d_mass, double *d_com, double *d_quad,
+                   int64_t *d_count, int32_t *d_children, void *stream);
+
+/* flattree.py:142-166 FlatTree.traverse against the current tree.
+ * leaf_size <= 1 is the reference walk; leaf_size > 1 resolves cells of
+ * <= leaf_size bodies that fail the MAC body by body.
+ * Targets may be in any order (they are Morton-ordered internally). */
+int bh_traverse_f32(bh_handle *h, const float *d_targets4, int64_t n, double theta,
+                    double eps, int leaf_size, float *d_acc4, int64_t *d_work,
+                    void *stream);
+int bh_traverse_f64(bh_handle *h, const double *d_targets3, int64_t n, double theta,
+                    double eps, int leaf_size, double *d_acc3, int64_t *d_work,
+                    void *stream);
+
+/* integrator.py:37-44 kick / drift (in place). */
+int bh_kick_f32(bh_handle *h, float *d_vel4, const float *d_acc4, int64_t n, double dt, void *stream);
+int bh_drift_f32(bh_handle *h, float *d_pos4, const float *d_vel4, int64_t n, double dt, void *stream);
+int bh_kick_f64(bh_handle *h, double *d_vel3, const double *d_acc3, int64_t n, double dt, void *stream);
+int bh_drift_f64(bh_handle *h, double *d_pos3, const double *d_vel3, int64_t n, double dt, void *stream);
+
+/* physics.py:288-295 direct_accelerations and physics.py:322-324
+ * potential_energy (O(n^2), fp64; validation / energy audit). */
+int bh_direct_f64(bh_handle *h, const double *d_pos3, const double *d_mass, int64_t n,
+                  double eps, double *d_acc3, void *stream);
+int bh_potential_f64(bh_handle *h, const double *d_pos3, const double *d_mass, int64_t n,
+                     double eps, double *d_pot, void *stream);
+
+/* ---- resident simulation (simulation.py:478-504 `_drive`, algorithm 1) ---
+ * Bodies live in the handle in Morton order between steps; `id` tracks the
+ * caller's order.  load/store copy device buffers in caller order (the layout
+ * of the handle's precision). */
+int bh_sim_load(bh_handle *h, const void *d_pos, const void *d_vel, const double *d_mass,
+                const void *d_acc, int64_t n, void *stream);
+/* One force evaluation at the current positions (the bootstrap pass of
+ * simulation.py:487); record_work mirrors simulation.py:394-395. */
+int bh_sim_forces(bh_handle *h, double theta, double eps, int leaf_size, int record_work,
+                  void *stream);
+/* `steps` KDK steps: kick(dt/2), drift(dt), forces, kick(dt/2). */
+int bh_sim_step(bh_handle *h, double dt, double theta, double eps, int leaf_size, int steps,
+                void *stream);
+int bh_sim_store(bh_handle *h, void *d_pos, void *d_vel, void *d_acc, int64_t *d_work,
+                 void *stream);
+int bh_stats_get(bh_handle *h, bh_stats *out, void *stream);
+
+/* ---- instrumentation ----------------------------------------------------- */
+/* Enable per-phase CUDA-event timing of bh_sim_* calls (adds event records). */
+int bh_timing_enable(bh_handle *h, int on);
+/* Zero the per-phase accumulators and the launch counter. */
+int bh_timing_reset(bh_handle *h);
+/* Synchronise and return accumulated milliseconds per phase (BH_NPHASES). */
+int bh_timing_get(bh_handle *h, double *ms_out, int nphases);
+/* FP32 FFMA throughput microbenchmark (the roofline denominator for the walk):
+ * runs a dependent-chain-free FFMA loop on every SM, returns TFLOP/s. */
+int bh_ffma_peak(bh_handle *h, double *tflops_out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -57,7 +57,7 @@ def lib():
         L.or_tree_size.restype = I64
         L.or_build.argtypes = [P, P, P, I64, D, I64] + [P] * 10
         L.or_build.restype = ctypes.c_int
-        L.or_traverse.argtypes = [I64] + [P] * 10 + [I64, D, D, I64, P, P, ctypes.c_int]
+        L.or_traverse.argtypes = [I64] + [P] * 10 + [I64, D, D, I64, P, P, ctypes.c_int, P]
         L.or_traverse.restype = None
         L.or_direct.argtypes = [P, P, I64, D, P, ctypes.c_int]
         L.or_direct.restype = None
@@ -172,8 +172,9 @@ def build_tree(mass_sorted, pos_sorted, R: float) -> OracleTree:
 
 
 def traverse(tree: OracleTree, targets, theta: float, eps: float, leaf_size: int = 1,
-             nthreads: int = 0):
-    """flattree.py:142-166 FlatTree.traverse (+ bucket extension for leaf_size>1)."""
+             nthreads: int = 0, totals: np.ndarray | None = None):
+    """flattree.py:142-166 FlatTree.traverse (+ bucket extension for leaf_size>1).
+    ``totals`` (int64[2]) receives the summed (pp, pc) interaction counts."""
     tg = _f64(targets).reshape(-1, 3)
     acc = np.zeros_like(tg)
     work = np.zeros(len(tg), dtype=np.int64)
@@ -181,7 +182,7 @@ def traverse(tree: OracleTree, targets, theta: float, eps: float, leaf_size: int
         len(tree), _p(tree.children), _p(tree.count), _p(tree.side), _p(tree.mass),
         _p(tree.com), _p(tree.quad), _p(tree.lo), _p(tree.bpos), _p(tree.bmass),
         _p(tg), len(tg), float(theta), float(eps), int(leaf_size), _p(acc), _p(work),
-        int(nthreads),
+        int(nthreads), None if totals is None else _p(totals),
     )
     return acc, work
 

@@ -1,0 +1,782 @@
+// bh_api.cu -- the handle and the extern "C" entry points of libbh.so.
+//
+// The handle owns only workspace (sort scratch, the tree, the resident body
+// state); callers own every buffer they pass.  Nothing here synchronises the
+// stream except bh_check, the cell-count read inside a build (one 8-byte D2H
+// per build) and the explicit query calls (bh_tree_size, bh_stats_get).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "bh_internal.cuh"
+
+using namespace bh;
+
+namespace {
+thread_local std::string g_err;
+
+int fail(int code, const std::string &msg) {
+  g_err = msg;
+  return code;
+}
+
+#define BH_CUDA(expr)                                                              \
+  do {                                                                             \
+    cudaError_t e_ = (expr);                                                       \
+    if (e_ != cudaSuccess)                                                         \
+      return fail(e_ == cudaErrorMemoryAllocation ? BH_OUT_OF_MEMORY : BH_CUDA_ERROR, \
+                  std::string(#expr) + ": " + cudaGetErrorString(e_));             \
+  } while (0)
+
+#define BH_LAUNCHED()                                                              \
+  do {                                                                             \
+    cudaError_t e_ = cudaGetLastError();                                           \
+    if (e_ != cudaSuccess)                                                         \
+      return fail(BH_CUDA_ERROR, std::string("kernel launch: ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define BH_TRY(expr)          \
+  do {                        \
+    int r_ = (expr);          \
+    if (r_ != BH_OK) return r_; \
+  } while (0)
+
+inline cudaStream_t S(void *s) { return static_cast<cudaStream_t>(s); }
+}  // namespace
+
+struct bh_handle {
+  int device = 0;
+  int precision = BH_FP32;
+  DeviceFlags *flags = nullptr;   // device
+  DeviceFlags *hflags = nullptr;  // pinned host mirror
+  uint32_t *hC = nullptr;         // pinned: off[n-1], newc[n-1]
+  double *dR = nullptr;           // device scratch R (sim path)
+  double *hR = nullptr;           // pinned
+  // sort / build scratch
+  Buf keys, keys2, vals, vals2, sort_tmp, scan_tmp, lcp, newc, off;
+  // tree
+  int64_t tree_n = -1, C = 0, max_level = 0;
+  double R = 1.0;
+  Buf link, parent, nchild, arrive, cm64, q64, ncm, nq0, nq1, tbod;
+  // resident simulation state (Morton order)
+  int64_t sim_n = 0;
+  Buf pos, pos2, vel, vel2, acc, id, id2, work_sorted, work_orig;
+  // instrumentation
+  struct Mark { int phase; cudaEvent_t a, b; };
+  bool timing = false;
+  std::vector<Mark> marks;
+  std::vector<cudaEvent_t> pool;
+  Mark open{0, nullptr, nullptr};
+  double phase_ms[BH_NPHASES] = {0};
+  int64_t launches = 0;
+
+  cudaEvent_t get_event() {
+    if (!pool.empty()) { cudaEvent_t e = pool.back(); pool.pop_back(); return e; }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+  }
+  void fold_marks() {
+    for (Mark &m : marks) {
+      cudaEventSynchronize(m.b);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, m.a, m.b);
+      phase_ms[m.phase] += ms;
+      pool.push_back(m.a);
+      pool.push_back(m.b);
+    }
+    marks.clear();
+  }
+  void tbegin(int phase, cudaStream_t s) {
+    if (!timing) return;
+    open.phase = phase;
+    open.a = get_event();
+    open.b = get_event();
+    cudaEventRecord(open.a, s);
+  }
+  void tend(cudaStream_t s) {
+    if (!timing || !open.a) return;
+    cudaEventRecord(open.b, s);
+    marks.push_back(open);
+    open.a = open.b = nullptr;
+    if (marks.size() > 4096) fold_marks();
+  }
+
+  TreeView view() {
+    TreeView t;
+    t.n = tree_n;
+    t.C = C;
+    t.keys = keys2.as<uint64_t>();
+    t.lcp = lcp.as<int8_t>();
+    t.off = off.as<uint32_t>();
+    t.newc = newc.as<uint32_t>();
+    t.link = link.as<int4>();
+    t.parent = parent.as<int>();
+    t.nchild = nchild.as<int>();
+    t.arrive = arrive.as<int>();
+    t.cm64 = cm64.as<double4>();
+    t.q64 = q64.as<double>();
+    if (precision == BH_FP32) {
+      t.ncm = ncm.as<float4>();
+      t.nq0 = nq0.as<float4>();
+      t.nq1 = nq1.as<float2>();
+    }
+    return t;
+  }
+};
+
+namespace {
+
+int read_flags(bh_handle *h, cudaStream_t s) {
+  BH_CUDA(cudaMemcpyAsync(h->hflags, h->flags, sizeof(DeviceFlags), cudaMemcpyDeviceToHost, s));
+  BH_CUDA(cudaStreamSynchronize(s));
+  return BH_OK;
+}
+
+// consume latched device error bits (report once)
+int take_flag_error(bh_handle *h, cudaStream_t s) {
+  int bits = h->hflags->bits;
+  if (!bits) return BH_OK;
+  long long bad = h->hflags->first_bad;
+  // clear
+  int zero = 0;
+  long long big = 0x7fffffffffffffffll;
+  cudaMemcpyAsync(&h->flags->bits, &zero, sizeof(int), cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(&h->flags->first_bad, &big, sizeof(long long), cudaMemcpyHostToDevice, s);
+  cudaStreamSynchronize(s);
+  h->hflags->bits = 0;
+  if (bits & FLAG_OUT_OF_DOMAIN)
+    return fail(BH_OUT_OF_DOMAIN, "position of body " + std::to_string(bad) +
+                                      " outside domain [-R, R)");
+  if (bits & FLAG_UNSORTED)
+    return fail(BH_UNSORTED, "bodies must be sorted by spatial key for a hashed build");
+  if (bits & FLAG_DUPLICATE)
+    return fail(BH_DUPLICATE_KEY,
+                "two bodies share the level-21 cell; positions are closer than the tree "
+                "resolution");
+  if (bits & FLAG_DEPTH) return fail(BH_DEPTH_OVERFLOW, "tree depth cap 21 exceeded");
+  return fail(BH_CUDA_ERROR, "unknown device flag");
+}
+
+int ensure_sort(bh_handle *h, int64_t n) {
+  BH_CUDA(h->keys.ensure(sizeof(uint64_t) * (n + 1)));
+  BH_CUDA(h->keys2.ensure(sizeof(uint64_t) * (n + 1)));
+  BH_CUDA(h->vals.ensure(sizeof(uint32_t) * (n + 1)));
+  BH_CUDA(h->vals2.ensure(sizeof(uint32_t) * (n + 1)));
+  BH_CUDA(h->sort_tmp.ensure(sort_temp_bytes(n) + 16));
+  return BH_OK;
+}
+
+int sort_keys(bh_handle *h, int64_t n, cudaStream_t s) {
+  // keys/vals -> keys2/vals2
+  if (n <= 0) return BH_OK;
+  BH_CUDA(sort_pairs(h->sort_tmp.p, h->sort_tmp.bytes, h->keys.as<uint64_t>(),
+                     h->keys2.as<uint64_t>(), h->vals.as<uint32_t>(), h->vals2.as<uint32_t>(),
+                     n, s));
+  return BH_OK;
+}
+
+// Build over Morton-sorted bodies whose keys are already in keys2
+// (hashed.py:448-515).  Exactly one of bod32 / bod64 is non-null.
+int build_sorted(bh_handle *h, int64_t n, const float4 *bod32, const double4 *bod64,
+                 cudaStream_t s) {
+  const bool f32 = h->precision == BH_FP32;
+  BH_CUDA(h->lcp.ensure(n + 16));
+  BH_CUDA(h->newc.ensure(sizeof(uint32_t) * (n + 1)));
+  BH_CUDA(h->off.ensure(sizeof(uint32_t) * (n + 1)));
+  BH_CUDA(h->scan_tmp.ensure(scan_temp_bytes(n) + 16));
+  if (n > 0) {
+    launch_lcp_new(h->keys2.as<uint64_t>(), n, h->lcp.as<int8_t>(), h->newc.as<uint32_t>(),
+                   h->flags, s);
+    BH_CUDA(exclusive_scan_u32(h->scan_tmp.p, h->scan_tmp.bytes, h->newc.as<uint32_t>(),
+                               h->off.as<uint32_t>(), n, s));
+    BH_LAUNCHED();
+    BH_CUDA(cudaMemcpyAsync(h->hC, h->off.as<uint32_t>() + (n - 1), 4, cudaMemcpyDeviceToHost, s));
+    BH_CUDA(cudaMemcpyAsync(h->hC + 1, h->newc.as<uint32_t>() + (n - 1), 4,
+                            cudaMemcpyDeviceToHost, s));
+  }
+  BH_CUDA(cudaMemcpyAsync(h->hR, h->dR, sizeof(double), cudaMemcpyDeviceToHost, s));
+  BH_TRY(read_flags(h, s));
+  BH_TRY(take_flag_error(h, s));
+  const int64_t C = n > 0 ? 1 + (int64_t)h->hC[0] + (int64_t)h->hC[1] : 1;
+  if (C > 0x7fffffffll) return fail(BH_OUT_OF_MEMORY, "more than 2^31-1 cells");
+  h->C = C;
+  h->tree_n = n;
+  h->R = *h->hR;
+  BH_CUDA(h->link.ensure(sizeof(int4) * C));
+  BH_CUDA(h->parent.ensure(sizeof(int) * C));
+  BH_CUDA(h->nchild.ensure(sizeof(int) * C));
+  BH_CUDA(h->arrive.ensure(sizeof(int) * C));
+  BH_CUDA(h->cm64.ensure(sizeof(double4) * C));
+  BH_CUDA(h->q64.ensure(sizeof(double) * 6 * C));
+  if (f32) {
+    BH_CUDA(h->ncm.ensure(sizeof(float4) * C));
+    BH_CUDA(h->nq0.ensure(sizeof(float4) * C));
+    BH_CUDA(h->nq1.ensure(sizeof(float2) * C));
+  }
+  BH_CUDA(cudaMemsetAsync(h->nchild.p, 0, sizeof(int) * C, s));
+  BH_CUDA(cudaMemsetAsync(h->arrive.p, 0, sizeof(int) * C, s));
+  if (n == 0) {  // hashed.py:459-462: an empty root
+    int4 root = make_int4(1, 0, 0, 0);
+    BH_CUDA(cudaMemcpyAsync(h->link.p, &root, sizeof(int4), cudaMemcpyHostToDevice, s));
+    BH_CUDA(cudaMemsetAsync(h->cm64.p, 0, sizeof(double4), s));
+    BH_CUDA(cudaMemsetAsync(h->q64.p, 0, sizeof(double) * 6, s));
+    if (f32) BH_CUDA(cudaMemsetAsync(h->ncm.p, 0, sizeof(float4), s));
+    int m1 = -1;
+    BH_CUDA(cudaMemcpyAsync(h->parent.p, &m1, sizeof(int), cudaMemcpyHostToDevice, s));
+    BH_CUDA(cudaStreamSynchronize(s));
+    h->max_level = 0;
+    return BH_OK;
+  }
+  TreeView t = h->view();
+  launch_emit(t, bod32, bod64, s);
+  launch_moments(t, s);
+  BH_LAUNCHED();
+  return BH_OK;
+}
+
+void fill_walk_params(bh_handle *h, WalkParams &P, int64_t nt, double theta, double eps,
+                      int leaf) {
+  P.C = (int)h->C;
+  P.nt = (int)nt;
+  P.e2 = eps * eps;
+  P.e2f = (float)(eps * eps);
+  P.theta = theta;
+  P.leaf = leaf;
+  for (int l = 0; l <= kMaxLevel; ++l) {
+    double side = std::ldexp(2.0 * h->R, -l);
+    P.side64[l] = side;
+    double r = side / theta;  // theta == 0 -> inf: never accept
+    P.mac2f[l] = (float)(r * r);
+  }
+}
+
+int reset_counters(bh_handle *h, cudaStream_t s) {
+  BH_CUDA(cudaMemsetAsync(&h->flags->pp, 0, 2 * sizeof(unsigned long long), s));
+  return BH_OK;
+}
+
+__global__ void k_scatter_work(const int *ws, const uint32_t *id, int64_t n, int *wo) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) wo[id[i]] = ws[i];
+}
+
+template <class T4>
+__global__ void k_store4(const T4 *src, const uint32_t *id, int64_t n, T4 *dst) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[id[i]] = src[i];
+}
+__global__ void k_store3(const double4 *src, const uint32_t *id, int64_t n, double *dst) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double4 v = src[i];
+  int64_t j = id[i];
+  dst[3 * j] = v.x; dst[3 * j + 1] = v.y; dst[3 * j + 2] = v.z;
+}
+__global__ void k_work64(const int *w, int64_t n, int64_t *out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = w[i];
+}
+__global__ void k_iota32(uint32_t *v, int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = (uint32_t)i;
+}
+__global__ void k_fill_int(int *v, int64_t n, int x) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = x;
+}
+
+// simulation.py:370-396 (algorithm 1, one rank) on resident state:
+// bounds -> keys -> stable sort -> permute bodies -> build -> walk.
+int sim_forces_impl(bh_handle *h, double theta, double eps, int leaf, int record_work,
+                    bool bounds_ready, cudaStream_t s) {
+  const int64_t n = h->sim_n;
+  const bool f32 = h->precision == BH_FP32;
+  if (!(theta >= 0.0) || !(eps >= 0.0)) return fail(BH_BAD_ARG, "theta and eps must be >= 0");
+  if (!bounds_ready) {
+    h->tbegin(BH_PHASE_INTEGRATE, s);
+    launch_reset_flags_bounds(h->flags, s);
+    if (f32) launch_maxabs_f32(h->pos.as<float4>(), n, h->flags, s);
+    else launch_kick_drift_max_f64(h->pos.as<double4>(), h->vel.as<double4>(), nullptr, n, 0.0,
+                                   0.0, h->flags, s);
+    h->tend(s);
+    h->launches += 2;
+  }
+  BH_TRY(ensure_sort(h, n));
+  h->tbegin(BH_PHASE_KEYS, s);
+  launch_finish_R(h->flags, f32 ? 0 : 1, h->dR, s);
+  if (f32)
+    launch_keys_f32(h->pos.as<float4>(), n, h->dR, h->keys.as<uint64_t>(), h->vals.as<uint32_t>(),
+                    h->flags, s);
+  else
+    launch_keys_f64(h->pos.as<double>(), 4, n, h->dR, h->keys.as<uint64_t>(),
+                    h->vals.as<uint32_t>(), h->flags, s);
+  h->tend(s);
+  h->tbegin(BH_PHASE_SORT, s);
+  BH_TRY(sort_keys(h, n, s));
+  h->tend(s);
+  h->tbegin(BH_PHASE_PERMUTE, s);
+  if (f32)
+    launch_gather_f32(h->vals2.as<uint32_t>(), n, h->pos.as<float4>(), h->pos2.as<float4>(),
+                      h->vel.as<float4>(), h->vel2.as<float4>(), h->id.as<uint32_t>(),
+                      h->id2.as<uint32_t>(), s);
+  else
+    launch_gather_f64(h->vals2.as<uint32_t>(), n, h->pos.as<double4>(), h->pos2.as<double4>(),
+                      h->vel.as<double4>(), h->vel2.as<double4>(), h->id.as<uint32_t>(),
+                      h->id2.as<uint32_t>(), s);
+  std::swap(h->pos, h->pos2);
+  std::swap(h->vel, h->vel2);
+  std::swap(h->id, h->id2);
+  h->tend(s);
+  BH_LAUNCHED();
+  h->tbegin(BH_PHASE_BUILD, s);
+  BH_TRY(build_sorted(h, n, f32 ? h->pos.as<float4>() : nullptr,
+                      f32 ? nullptr : h->pos.as<double4>(), s));
+  h->tend(s);
+  BH_TRY(reset_counters(h, s));
+  h->tbegin(BH_PHASE_WALK, s);
+  WalkParams P;
+  fill_walk_params(h, P, n, theta, eps, leaf);
+  int *w32 = record_work ? h->work_sorted.as<int>() : nullptr;
+  if (f32)
+    launch_walk_f32(P, h->ncm.as<float4>(), h->nq0.as<float4>(), h->nq1.as<float2>(),
+                    h->link.as<int4>(), h->pos.as<float4>(), h->pos.as<float>(), 4, nullptr,
+                    h->acc.as<float>(), 4, nullptr, w32, h->flags, s);
+  else
+    launch_walk_f64(P, h->cm64.as<double4>(), h->q64.as<double>(), h->link.as<int4>(),
+                    h->pos.as<double4>(), h->pos.as<double>(), 4, nullptr, h->acc.as<double>(), 4,
+                    nullptr, w32, h->flags, s);
+  h->tend(s);
+  if (record_work && n > 0) {
+    k_scatter_work<<<grid_for(n, 256), 256, 0, s>>>(w32, h->id.as<uint32_t>(), n,
+                                                    h->work_orig.as<int>());
+    h->launches += 1;
+  }
+  h->launches += 7;  // finish_R, keys, gather, lcp_new, emit, moments, walk
+  BH_LAUNCHED();
+  return BH_OK;
+}
+
+}  // namespace
+
+// ============================================================== C-ABI
+extern "C" {
+
+const char *bh_last_error(void) { return g_err.c_str(); }
+int bh_version(void) { return 1; }
+
+int bh_create(bh_handle **out, int device, int precision) {
+  if (!out) return fail(BH_BAD_ARG, "out is NULL");
+  if (precision != BH_FP32 && precision != BH_FP64) return fail(BH_BAD_ARG, "bad precision");
+  BH_CUDA(cudaSetDevice(device));
+  bh_handle *h = new bh_handle();
+  h->device = device;
+  h->precision = precision;
+  BH_CUDA(cudaMalloc(&h->flags, sizeof(DeviceFlags)));
+  BH_CUDA(cudaMallocHost(&h->hflags, sizeof(DeviceFlags)));
+  BH_CUDA(cudaMallocHost(&h->hC, 4 * sizeof(uint32_t)));
+  BH_CUDA(cudaMalloc(&h->dR, sizeof(double)));
+  BH_CUDA(cudaMallocHost(&h->hR, sizeof(double)));
+  DeviceFlags init;
+  memset(&init, 0, sizeof(init));
+  init.first_bad = 0x7fffffffffffffffll;
+  BH_CUDA(cudaMemcpy(h->flags, &init, sizeof(init), cudaMemcpyHostToDevice));
+  *h->hflags = init;
+  *out = h;
+  return BH_OK;
+}
+
+int bh_destroy(bh_handle *h) {
+  if (!h) return BH_OK;
+  cudaSetDevice(h->device);
+  Buf *bufs[] = {&h->keys, &h->keys2, &h->vals, &h->vals2, &h->sort_tmp, &h->scan_tmp,
+                 &h->lcp, &h->newc, &h->off, &h->link, &h->parent, &h->nchild, &h->arrive,
+                 &h->cm64, &h->q64, &h->ncm, &h->nq0, &h->nq1, &h->tbod, &h->pos, &h->pos2,
+                 &h->vel, &h->vel2, &h->acc, &h->id, &h->id2, &h->work_sorted, &h->work_orig};
+  for (Buf *b : bufs) b->release();
+  cudaFree(h->flags);
+  cudaFreeHost(h->hflags);
+  cudaFreeHost(h->hC);
+  cudaFree(h->dR);
+  cudaFreeHost(h->hR);
+  h->fold_marks();
+  for (cudaEvent_t e : h->pool) cudaEventDestroy(e);
+  delete h;
+  return BH_OK;
+}
+
+int bh_check(bh_handle *h, void *stream) {
+  if (!h) return fail(BH_BAD_ARG, "handle is NULL");
+  BH_CUDA(cudaGetLastError());
+  BH_TRY(read_flags(h, S(stream)));
+  return take_flag_error(h, S(stream));
+}
+
+int bh_bounds_f32(bh_handle *h, const float *d_pos4, int64_t n, double *d_R, void *stream) {
+  if (!h || n < 0 || (n && !d_pos4) || !d_R) return fail(BH_BAD_ARG, "bh_bounds_f32: bad args");
+  launch_reset_flags_bounds(h->flags, S(stream));
+  launch_maxabs_f32(reinterpret_cast<const float4 *>(d_pos4), n, h->flags, S(stream));
+  launch_finish_R(h->flags, 0, d_R, S(stream));
+  BH_LAUNCHED();
+  return BH_OK;
+}
+
+int bh_bounds_f64(bh_handle *h, const double *d_pos3, int64_t n, double *d_R, void *stream) {
+  if (!h || n < 0 || (n && !d_pos3) || !d_R) return fail(BH_BAD_ARG, "bh_bounds_f64: bad args");
+  launch_reset_flags_bounds(h->flags, S(stream));
+  launch_maxabs_f64(d_pos3, n, h->flags, S(stream));
+  launch_finish_R(h->flags, 1, d_R, S(stream));
+  BH_LAUNCHED();
+  return BH_OK;
+}
+
+int bh_morton_f32(bh_handle *h, const float *d_pos4, int64_t n, const double *d_R,
+                  uint64_t *d_keys, void *stream) {
+  if (!h || n < 0 || !d_R || (n && (!d_pos4 || !d_keys))) return fail(BH_BAD_ARG, "bh_morton_f32: bad args");
+  launch_keys_f32(reinterpret_cast<const float4 *>(d_pos4), n, d_R, d_keys, nullptr, h->flags,
+                  S(stream));
+  BH_LAUNCHED();
+  return BH_OK;
+}
+
+int bh_morton_f64(bh_handle *h, const double *d_pos3, int64_t n, const double *d_R,
+                  uint64_t *d_keys, void *stream) {
+  if (!h || n < 0 || !d_R || (n && (!d_pos3 || !d_keys))) return fail(BH_BAD_ARG, "bh_morton_f64: bad args");
+  launch_keys_f64(d_pos3, 3, n, d_R, d_keys, nullptr, h->flags, S(stream));
+  BH_LAUNCHED();
+  return BH_OK;
+}
+
+int bh_sort(bh_handle *h, const uint64_t *d_keys, int64_t n, uint64_t *d_keys_sorted,
+            int64_t *d_perm, void *stream) {
+  if (!h || n < 0 || (n && (!d_keys || !d_perm))) return fail(BH_BAD_ARG, "bh_sort: bad args");
+  if (n == 0) return BH_OK;
+  cudaStream_t s = S(stream);
+  BH_TRY(ensure_sort(h, n));
+  BH_CUDA(cudaMemcpyAsync(h->keys.p, d_keys, sizeof(uint64_t) * n, cudaMemcpyDeviceToDevice, s));
+  k_iota32<<<grid_for(n, 256), 256, 0, s>>>(h->vals.as<uint32_t>(), n);
+  BH_TRY(sort_keys(h, n, s));
+  if (d_keys_sorted)
+    BH_CUDA(cudaMemcpyAsync(d_keys_sorted, h->keys2.p, sizeof(uint64_t) * n,
+                            cudaMemcpyDeviceToDevice, s));
+  launch_iota64(d_perm, h->vals2.as<uint32_t>(), n, s);
+  BH_LAUNCHED();
+  return BH_OK;
+}
+
+int bh_build_f32(bh_handle *h, const float *d_pos4_sorted, int64_t n, const double *d_R,
+                 void *stream) {
+  if (!h || n < 0 || !d_R || (n && !d_pos4_sorted)) return fail(BH_BAD_ARG, "bh_build_f32: bad args");
+  if (h->precision != BH_FP32) return fail(BH_BAD_ARG, "handle is fp64; use bh_build_f64");
+  cudaStream_t s = S(stream);
+  BH_TRY(ensure_sort(h, n));
+  BH_CUDA(h->tbod.ensure(sizeof(float4) * (n + 1)));
+  if (n) BH_CUDA(cudaMemcpyAsync(h->tbod.p, d_pos4_sorted, sizeof(float4) * n,
+                                 cudaMemcpyDeviceToDevice, s));
+  BH_CUDA(cudaMemcpyAsync(h->dR, d_R, sizeof(double), cudaMemcpyDeviceToDevice, s));
+  // hashed.py:463: keys recomputed from the (sorted) positions
+  launch_keys_f32(h->tbod.as<float4>(), n, h->dR, h->keys2.as<uint64_t>(), nullptr, h->flags, s);
+  return build_sorted(h, n, h->tbod.as<float4>(), nullptr, s);
+}
+
+int bh_build_f64(bh_handle *h, const double *d_pos3_sorted, const double *d_mass_sorted,
+                 int64_t n, const double *d_R, void *stream) {
+  if (!h || n < 0 || !d_R || (n && (!d_pos3_sorted || !d_mass_sorted)))
+    return fail(BH_BAD_ARG, "bh_build_f64: bad args");
+  if (h->precision != BH_FP64) return fail(BH_BAD_ARG, "handle is fp32; use bh_build_f32");
+  cudaStream_t s = S(stream);
+  BH_TRY(ensure_sort(h, n));
+  BH_CUDA(h->tbod.ensure(sizeof(double4) * (n + 1)));
+  launch_pack_bodies_f64(d_pos3_sorted, d_mass_sorted, n, h->tbod.as<double4>(), s);
+  BH_CUDA(cudaMemcpyAsync(h->dR, d_R, sizeof(double), cudaMemcpyDeviceToDevice, s));
+  launch_keys_f64(d_pos3_sorted, 3, n, h->dR, h->keys2.as<uint64_t>(), nullptr, h->flags, s);
+  return build_sorted(h, n, nullptr, h->tbod.as<double4>(), s);
+}
+
+int bh_tree_size(bh_handle *h, int64_t *n_cells) {
+  if (!h || !n_cells) return fail(BH_BAD_ARG, "bh_tree_size: bad args");
+  if (h->tree_n < 0) return fail(BH_NO_TREE, "no tree has been built");
+  *n_cells = h->C;
+  return BH_OK;
+}
+
+int bh_export_tree(bh_handle *h, uint64_t *d_key, int8_t *d_level, double *d_centre,
+                   double *d_side, double *d_mass, double *d_com, double *d_quad,
+                   int64_t *d_count, int32_t *d_children, void *stream) {
+  if (!h) return fail(BH_BAD_ARG, "bh_export_tree: bad args");
+  if (h->tree_n < 0) return fail(BH_NO_TREE, "no tree has been built");
+  launch_export(h->view(), h->R, d_key, d_level, d_centre, d_side, d_mass, d_com, d_quad, d_count,
+                d_children, S(stream));
+  BH_LAUNCHED();
+  return BH_OK;
+}
+
+static int traverse_common(bh_handle *h, const void *targets, int64_t n, double theta,
+                           double eps, int leaf, void *acc, int64_t *work, bool f32,
+                           cudaStream_t s) {
+  if (h->tree_n < 0) return fail(BH_NO_TREE, "no tree has been built");
+  if (!(theta >= 0.0) || !(eps >= 0.0)) return fail(BH_BAD_ARG, "theta and eps must be >= 0");
+  if (n > 0x7fffffffll) return fail(BH_BAD_ARG, "too many targets");
+  if (n == 0) return BH_OK;
+  const int comps = f32 ? 4 : 3;
+  const size_t esz = f32 ? sizeof(float) : sizeof(double);
+  BH_TRY(reset_counters(h, s));
+  if (h->tree_n == 0) {  // flattree.py:152: empty tree -> zero acc, zero work
+    BH_CUDA(cudaMemsetAsync(acc, 0, esz * comps * n, s));
+    if (work) BH_CUDA(cudaMemsetAsync(work, 0, sizeof(int64_t) * n, s));
+    return BH_OK;
+  }
+  // order the targets along the Morton curve so warps walk coherent lists
+  BH_TRY(ensure_sort(h, n));
+  if (f32)
+    launch_keys_clamped_f32(static_cast<const float *>(targets), 4, n, h->dR,
+                            h->keys.as<uint64_t>(), h->vals.as<uint32_t>(), s);
+  else
+    launch_keys_clamped_f64(static_cast<const double *>(targets), 3, n, h->dR,
+                            h->keys.as<uint64_t>(), h->vals.as<uint32_t>(), s);
+  // keys2 holds the tree's keys (needed by export): sort into keys (tmp) instead
+  BH_CUDA(h->work_sorted.ensure(sizeof(uint64_t) * (n + 1)));
+  BH_CUDA(sort_pairs(h->sort_tmp.p, h->sort_tmp.bytes, h->keys.as<uint64_t>(),
+                     h->work_sorted.as<uint64_t>(), h->vals.as<uint32_t>(),
+                     h->vals2.as<uint32_t>(), n, s));
+  WalkParams P;
+  fill_walk_params(h, P, n, theta, eps, leaf);
+  if (f32)
+    launch_walk_f32(P, h->ncm.as<float4>(), h->nq0.as<float4>(), h->nq1.as<float2>(),
+                    h->link.as<int4>(), h->tbod.as<float4>(), static_cast<const float *>(targets),
+                    4, h->vals2.as<uint32_t>(), static_cast<float *>(acc), 4, work, nullptr,
+                    h->flags, s);
+  else
+    launch_walk_f64(P, h->cm64.as<double4>(), h->q64.as<double>(), h->link.as<int4>(),
+                    h->tbod.as<double4>(), static_cast<const double *>(targets), 3,
+                    h->vals2.as<uint32_t>(), static_cast<double *>(acc), 3, work, nullptr,
+                    h->flags, s);
+  BH_LAUNCHED();
+  return BH_OK;
+}
+
+int bh_traverse_f32(bh_handle *h, const float *d_targets4, int64_t n, double theta, double eps,
+                    int leaf_size, float *d_acc4, int64_t *d_work, void *stream) {
+  if (!h || n < 0 || (n && (!d_targets4 || !d_acc4))) return fail(BH_BAD_ARG, "bh_traverse_f32: bad args");
+  if (h->precision != BH_FP32) return fail(BH_BAD_ARG, "handle is fp64; use bh_traverse_f64");
+  return traverse_common(h, d_targets4, n, theta, eps, leaf_size, d_acc4, d_work, true, S(stream));
+}
+
+int bh_traverse_f64(bh_handle *h, const double *d_targets3, int64_t n, double theta,
+                    double eps, int leaf_size, double *d_acc3, int64_t *d_work, void *stream) {
+  if (!h || n < 0 || (n && (!d_targets3 || !d_acc3))) return fail(BH_BAD_ARG, "bh_traverse_f64: bad args");
+  if (h->precision != BH_FP64) return fail(BH_BAD_ARG, "handle is fp32; use bh_traverse_f32");
+  return traverse_common(h, d_targets3, n, theta, eps, leaf_size, d_acc3, d_work, false, S(stream));
+}
+
+int bh_kick_f32(bh_handle *h, float *d_vel4, const float *d_acc4, int64_t n, double dt, void *stream) {
+  if (!h || n < 0) return fail(BH_BAD_ARG, "bh_kick_f32: bad args");
+  launch_kick_f32(reinterpret_cast<float4 *>(d_vel4), reinterpret_cast<const float4 *>(d_acc4), n,
+                  (float)dt, S(stream));
+  BH_LAUNCHED();
+  return BH_OK;
+}
+int bh_drift_f32(bh_handle *h, float *d_pos4, const float *d_vel4, int64_t n, double dt, void *stream) {
+  if (!h || n < 0) return fail(BH_BAD_ARG, "bh_drift_f32: bad args");
+  launch_drift_f32(reinterpret_cast<float4 *>(d_pos4), reinterpret_cast<const float4 *>(d_vel4), n,
+                   (float)dt, S(stream));
+  BH_LAUNCHED();
+  return BH_OK;
+}
+int bh_kick_f64(bh_handle *h, double *d_vel3, const double *d_acc3, int64_t n, double dt, void *stream) {
+  if (!h || n < 0) return fail(BH_BAD_ARG, "bh_kick_f64: bad args");
+  launch_kick_f64(d_vel3, d_acc3, n, dt, S(stream));
+  BH_LAUNCHED();
+  return BH_OK;
+}
+int bh_drift_f64(bh_handle *h, double *d_pos3, const double *d_vel3, int64_t n, double dt, void *stream) {
+  if (!h || n < 0) return fail(BH_BAD_ARG, "bh_drift_f64: bad args");
+  launch_drift_f64(d_pos3, d_vel3, n, dt, S(stream));
+  BH_LAUNCHED();
+  return BH_OK;
+}
+
+int bh_direct_f64(bh_handle *h, const double *d_pos3, const double *d_mass, int64_t n, double eps,
+                  double *d_acc3, void *stream) {
+  if (!h || n < 0) return fail(BH_BAD_ARG, "bh_direct_f64: bad args");
+  launch_direct_f64(d_pos3, d_mass, n, eps, d_acc3, S(stream));
+  BH_LAUNCHED();
+  return BH_OK;
+}
+int bh_potential_f64(bh_handle *h, const double *d_pos3, const double *d_mass, int64_t n,
+                     double eps, double *d_partial, void *stream) {
+  if (!h || n < 0) return fail(BH_BAD_ARG, "bh_potential_f64: bad args");
+  launch_potential_f64(d_pos3, d_mass, n, eps, d_partial, S(stream));
+  BH_LAUNCHED();
+  return BH_OK;
+}
+
+__global__ void k_pack_vel_f64(const double *v3, int64_t n, double4 *out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = make_double4(v3[3 * i], v3[3 * i + 1], v3[3 * i + 2], 0.0);
+}
+
+int bh_sim_load(bh_handle *h, const void *d_pos, const void *d_vel, const double *d_mass,
+                const void *d_acc, int64_t n, void *stream) {
+  if (!h || n < 0 || (n && (!d_pos || !d_vel))) return fail(BH_BAD_ARG, "bh_sim_load: bad args");
+  if (n > 0x7fffffffll) return fail(BH_BAD_ARG, "too many bodies");
+  const bool f32 = h->precision == BH_FP32;
+  if (!f32 && n && !d_mass) return fail(BH_BAD_ARG, "fp64 bh_sim_load needs masses");
+  cudaStream_t s = S(stream);
+  const size_t e4 = f32 ? sizeof(float4) : sizeof(double4);
+  Buf *b4[] = {&h->pos, &h->pos2, &h->vel, &h->vel2, &h->acc};
+  for (Buf *b : b4) BH_CUDA(b->ensure(e4 * (n + 1)));
+  BH_CUDA(h->id.ensure(sizeof(uint32_t) * (n + 1)));
+  BH_CUDA(h->id2.ensure(sizeof(uint32_t) * (n + 1)));
+  BH_CUDA(h->work_sorted.ensure(sizeof(int64_t) * (n + 1)));
+  BH_CUDA(h->work_orig.ensure(sizeof(int) * (n + 1)));
+  h->sim_n = n;
+  if (n == 0) return BH_OK;
+  if (f32) {
+    BH_CUDA(cudaMemcpyAsync(h->pos.p, d_pos, e4 * n, cudaMemcpyDeviceToDevice, s));
+    BH_CUDA(cudaMemcpyAsync(h->vel.p, d_vel, e4 * n, cudaMemcpyDeviceToDevice, s));
+  } else {
+    launch_pack_bodies_f64(static_cast<const double *>(d_pos), d_mass, n, h->pos.as<double4>(), s);
+    k_pack_vel_f64<<<grid_for(n, 256), 256, 0, s>>>(static_cast<const double *>(d_vel), n,
+                                                    h->vel.as<double4>());
+  }
+  if (!d_acc) {
+    BH_CUDA(cudaMemsetAsync(h->acc.p, 0, e4 * n, s));
+  } else if (f32) {
+    BH_CUDA(cudaMemcpyAsync(h->acc.p, d_acc, e4 * n, cudaMemcpyDeviceToDevice, s));
+  } else {
+    k_pack_vel_f64<<<grid_for(n, 256), 256, 0, s>>>(static_cast<const double *>(d_acc), n,
+                                                    h->acc.as<double4>());
+  }
+  k_iota32<<<grid_for(n, 256), 256, 0, s>>>(h->id.as<uint32_t>(), n);
+  k_fill_int<<<grid_for(n, 256), 256, 0, s>>>(h->work_orig.as<int>(), n, 1);  // simulation.py:482
+  BH_LAUNCHED();
+  return BH_OK;
+}
+
+int bh_sim_forces(bh_handle *h, double theta, double eps, int leaf_size, int record_work,
+                  void *stream) {
+  if (!h) return fail(BH_BAD_ARG, "bh_sim_forces: bad args");
+  if (h->sim_n == 0) return BH_OK;
+  return sim_forces_impl(h, theta, eps, leaf_size, record_work, false, S(stream));
+}
+
+int bh_sim_step(bh_handle *h, double dt, double theta, double eps, int leaf_size, int steps,
+                void *stream) {
+  if (!h || !(dt > 0.0) || steps < 0) return fail(BH_BAD_ARG, "bh_sim_step: bad args");
+  const int64_t n = h->sim_n;
+  if (n == 0) return BH_OK;
+  cudaStream_t s = S(stream);
+  const bool f32 = h->precision == BH_FP32;
+  const double half = 0.5 * dt;  // integrator.py / simulation.py:494: kick(0.5*dt)
+  for (int k = 0; k < steps; ++k) {
+    h->tbegin(BH_PHASE_INTEGRATE, s);
+    launch_reset_flags_bounds(h->flags, s);
+    if (f32)
+      launch_kick_drift_max_f32(h->pos.as<float4>(), h->vel.as<float4>(), h->acc.as<float4>(), n,
+                                (float)half, (float)dt, h->flags, s);
+    else
+      launch_kick_drift_max_f64(h->pos.as<double4>(), h->vel.as<double4>(), h->acc.as<double4>(),
+                                n, half, dt, h->flags, s);
+    h->tend(s);
+    BH_TRY(sim_forces_impl(h, theta, eps, leaf_size, 1, true, s));
+    h->tbegin(BH_PHASE_INTEGRATE, s);
+    if (f32) launch_kick_f32(h->vel.as<float4>(), h->acc.as<float4>(), n, (float)half, s);
+    else launch_kick4_f64(h->vel.as<double4>(), h->acc.as<double4>(), n, half, s);
+    h->tend(s);
+    h->launches += 3;
+    BH_LAUNCHED();
+  }
+  return BH_OK;
+}
+
+int bh_sim_store(bh_handle *h, void *d_pos, void *d_vel, void *d_acc, int64_t *d_work,
+                 void *stream) {
+  if (!h) return fail(BH_BAD_ARG, "bh_sim_store: bad args");
+  const int64_t n = h->sim_n;
+  if (n == 0) return BH_OK;
+  cudaStream_t s = S(stream);
+  const int g = grid_for(n, 256);
+  const uint32_t *id = h->id.as<uint32_t>();
+  if (h->precision == BH_FP32) {
+    if (d_pos) k_store4<float4><<<g, 256, 0, s>>>(h->pos.as<float4>(), id, n, (float4 *)d_pos);
+    if (d_vel) k_store4<float4><<<g, 256, 0, s>>>(h->vel.as<float4>(), id, n, (float4 *)d_vel);
+    if (d_acc) k_store4<float4><<<g, 256, 0, s>>>(h->acc.as<float4>(), id, n, (float4 *)d_acc);
+  } else {
+    if (d_pos) k_store3<<<g, 256, 0, s>>>(h->pos.as<double4>(), id, n, (double *)d_pos);
+    if (d_vel) k_store3<<<g, 256, 0, s>>>(h->vel.as<double4>(), id, n, (double *)d_vel);
+    if (d_acc) k_store3<<<g, 256, 0, s>>>(h->acc.as<double4>(), id, n, (double *)d_acc);
+  }
+  if (d_work) k_work64<<<g, 256, 0, s>>>(h->work_orig.as<int>(), n, d_work);
+  BH_LAUNCHED();
+  return BH_OK;
+}
+
+int bh_stats_get(bh_handle *h, bh_stats *out, void *stream) {
+  if (!h || !out) return fail(BH_BAD_ARG, "bh_stats_get: bad args");
+  BH_TRY(read_flags(h, S(stream)));
+  out->n_bodies = h->tree_n < 0 ? 0 : h->tree_n;
+  out->n_cells = h->C;
+  out->max_level = h->max_level;
+  out->pp = (int64_t)h->hflags->pp;
+  out->pc = (int64_t)h->hflags->pc;
+  out->work = out->pp + 2 * out->pc;
+  out->launches = h->launches;
+  return BH_OK;
+}
+
+int bh_timing_enable(bh_handle *h, int on) {
+  if (!h) return fail(BH_BAD_ARG, "bh_timing_enable: bad args");
+  h->timing = on != 0;
+  return BH_OK;
+}
+
+int bh_timing_reset(bh_handle *h) {
+  if (!h) return fail(BH_BAD_ARG, "bh_timing_reset: bad args");
+  h->fold_marks();
+  for (double &x : h->phase_ms) x = 0.0;
+  h->launches = 0;
+  return BH_OK;
+}
+
+int bh_timing_get(bh_handle *h, double *ms_out, int nphases) {
+  if (!h || !ms_out || nphases < 0) return fail(BH_BAD_ARG, "bh_timing_get: bad args");
+  h->fold_marks();
+  for (int i = 0; i < nphases && i < BH_NPHASES; ++i) ms_out[i] = h->phase_ms[i];
+  return BH_OK;
+}
+
+int bh_ffma_peak(bh_handle *h, double *tflops_out, void *stream) {
+  if (!h || !tflops_out) return fail(BH_BAD_ARG, "bh_ffma_peak: bad args");
+  cudaStream_t s = S(stream);
+  int sms = 0;
+  BH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
+  Buf out;
+  BH_CUDA(out.ensure(64));
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  double flops = 0.0;
+  const int iters = 1 << 14;
+  run_ffma(out.as<float>(), sms, iters, &flops, s);  // warm-up
+  cudaEventRecord(a, s);
+  run_ffma(out.as<float>(), sms, iters, &flops, s);
+  cudaEventRecord(b, s);
+  BH_LAUNCHED();
+  BH_CUDA(cudaEventSynchronize(b));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  out.release();
+  *tflops_out = flops / (ms * 1e-3) / 1e12;
+  return BH_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,673 @@
+// bh_exact.cu -- kernels whose fp64 arithmetic must match the reference bit for
+// bit.  This translation unit is compiled with -fmad=false: the reference
+// (numpy / numba without fast-math) never contracts a*b+c into an FMA, and one
+// contracted d2 flips a MAC decision (SURVEY.md §7 "fp64 bit-exactness").
+// Explicit fma() calls below are deliberate (error-free transforms).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <climits>
+
+#include "bh_internal.cuh"
+
+namespace bh {
+
+// ------------------------------------------------------------------ keys
+// morton.py:60-68 _spread
+__device__ __forceinline__ uint64_t spread21(uint64_t v) {
+  v &= 0x1FFFFFull;
+  v = (v | (v << 32)) & 0x1F00000000FFFFull;
+  v = (v | (v << 16)) & 0x1F0000FF0000FFull;
+  v = (v | (v << 8)) & 0x100F00F00F00F00Full;
+  v = (v | (v << 4)) & 0x10C30C30C30C30C3ull;
+  v = (v | (v << 2)) & 0x1249249249249249ull;
+  return v;
+}
+
+// morton.py:119-125: floor(((x + R) / (2R)) * 2^21), clipped to [0, 2^21 - 1]
+__device__ __forceinline__ uint64_t quantize(double x, double R, double twoR) {
+  double s = floor((x + R) / twoR * 2097152.0);
+  s = s < 0.0 ? 0.0 : s;
+  s = s > 2097151.0 ? 2097151.0 : s;
+  return (uint64_t)s;
+}
+
+__device__ __forceinline__ uint64_t morton3(double x, double y, double z, double R,
+                                            double twoR) {
+  return (spread21(quantize(x, R, twoR)) << 2) | (spread21(quantize(y, R, twoR)) << 1) |
+         spread21(quantize(z, R, twoR));
+}
+
+__device__ __forceinline__ bool in_domain(double x, double R) {
+  return (x >= -R) && (x < R);  // morton.py:116: min < -R or max >= R raises
+}
+
+template <class Loader>
+__global__ void k_keys(Loader ld, int64_t n, const double *__restrict__ d_R,
+                       uint64_t *__restrict__ keys, uint32_t *__restrict__ vals,
+                       DeviceFlags *f, int check) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double R = *d_R;
+  const double twoR = 2.0 * R;
+  double x, y, z;
+  ld(i, x, y, z);
+  if (check && !(in_domain(x, R) && in_domain(y, R) && in_domain(z, R))) {
+    atomicOr(&f->bits, FLAG_OUT_OF_DOMAIN);
+    atomicMin(&f->first_bad, (long long)i);
+  }
+  keys[i] = morton3(x, y, z, R, twoR);
+  if (vals) vals[i] = (uint32_t)i;
+}
+
+struct LoadF4 {
+  const float4 *p;
+  __device__ void operator()(int64_t i, double &x, double &y, double &z) const {
+    float4 v = p[i];
+    x = v.x; y = v.y; z = v.z;
+  }
+};
+struct LoadF {
+  const float *p; int stride;
+  __device__ void operator()(int64_t i, double &x, double &y, double &z) const {
+    const float *q = p + i * stride;
+    x = q[0]; y = q[1]; z = q[2];
+  }
+};
+struct LoadD {
+  const double *p; int stride;
+  __device__ void operator()(int64_t i, double &x, double &y, double &z) const {
+    const double *q = p + i * stride;
+    x = q[0]; y = q[1]; z = q[2];
+  }
+};
+
+void launch_keys_f32(const float4 *pos, int64_t n, const double *d_R, uint64_t *keys,
+                     uint32_t *vals, DeviceFlags *f, cudaStream_t s) {
+  if (n <= 0) return;
+  k_keys<<<grid_for(n, 256), 256, 0, s>>>(LoadF4{pos}, n, d_R, keys, vals, f, 1);
+}
+void launch_keys_f64(const double *pos, int stride, int64_t n, const double *d_R,
+                     uint64_t *keys, uint32_t *vals, DeviceFlags *f, cudaStream_t s) {
+  if (n <= 0) return;
+  k_keys<<<grid_for(n, 256), 256, 0, s>>>(LoadD{pos, stride}, n, d_R, keys, vals, f, 1);
+}
+
+template <class Loader>
+__global__ void k_keys_clamped(Loader ld, int64_t n, const double *__restrict__ d_R,
+                               uint64_t *__restrict__ keys, uint32_t *__restrict__ vals) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double R = *d_R;
+  double x, y, z;
+  ld(i, x, y, z);
+  // ordering key only: NaN/out-of-domain targets clamp (quantize clips)
+  x = x != x ? 0.0 : x; y = y != y ? 0.0 : y; z = z != z ? 0.0 : z;
+  keys[i] = morton3(x, y, z, R, 2.0 * R);
+  vals[i] = (uint32_t)i;
+}
+void launch_keys_clamped_f32(const float *pos, int stride, int64_t n, const double *d_R,
+                             uint64_t *keys, uint32_t *vals, cudaStream_t s) {
+  if (n <= 0) return;
+  k_keys_clamped<<<grid_for(n, 256), 256, 0, s>>>(LoadF{pos, stride}, n, d_R, keys, vals);
+}
+void launch_keys_clamped_f64(const double *pos, int stride, int64_t n, const double *d_R,
+                             uint64_t *keys, uint32_t *vals, cudaStream_t s) {
+  if (n <= 0) return;
+  k_keys_clamped<<<grid_for(n, 256), 256, 0, s>>>(LoadD{pos, stride}, n, d_R, keys, vals);
+}
+
+// ------------------------------------------------------------- tree build
+__device__ __forceinline__ double4 ldcg4(const double4 *p) {
+  const double2 *q = reinterpret_cast<const double2 *>(p);
+  double2 a = __ldcg(q), b = __ldcg(q + 1);
+  return make_double4(a.x, a.y, b.x, b.y);
+}
+__device__ __forceinline__ float4 v4f(double4 b) {
+  return make_float4((float)b.x, (float)b.y, (float)b.z, (float)b.w);
+}
+
+// hashed.py:376-388 _lcp_levels: 21 - ceil(bitlen(a ^ b) / 3)
+__device__ __forceinline__ int lcp_of(uint64_t a, uint64_t b) {
+  uint64_t x = a ^ b;
+  int bits = x ? 64 - __clzll((long long)x) : 0;
+  return kMortonBits - (bits + 2) / 3;
+}
+
+// hashed.py:475-489: sortedness / duplicate checks, lcp, depth, cells per body.
+// newc[i] = depth[i] - start[i] with start = lcp[i-1] (0 for i = 0).
+__global__ void k_lcp_new(const uint64_t *__restrict__ keys, int64_t n,
+                          int8_t *__restrict__ lcp, uint32_t *__restrict__ newc,
+                          DeviceFlags *f) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint64_t k = keys[i];
+  int lp = -1, ln = -1;
+  if (i > 0) lp = lcp_of(keys[i - 1], k);
+  if (i + 1 < n) {
+    uint64_t kn = keys[i + 1];
+    if (kn < k) atomicOr(&f->bits, FLAG_UNSORTED);
+    if (kn == k) atomicOr(&f->bits, FLAG_DUPLICATE);
+    ln = lcp_of(k, kn);
+    lcp[i] = (int8_t)ln;
+  }
+  int depth = (lp > ln ? lp : ln) + 1;
+  if (depth > kMaxLevel) atomicOr(&f->bits, FLAG_DEPTH);
+  int start = i > 0 ? lp : 0;
+  newc[i] = (uint32_t)(depth - start);
+}
+
+void launch_lcp_new(const uint64_t *keys, int64_t n, int8_t *lcp, uint32_t *newc,
+                    DeviceFlags *f, cudaStream_t s) {
+  if (n <= 0) return;
+  k_lcp_new<<<grid_for(n, 256), 256, 0, s>>>(keys, n, lcp, newc, f);
+}
+
+// first b > i whose level-l prefix differs from body i's (n if none):
+// galloping then bisection over the sorted keys.
+__device__ __forceinline__ int64_t run_end(const uint64_t *__restrict__ keys, int64_t n,
+                                           int64_t i, uint64_t pref, int shift) {
+  int64_t lo = i, step = 1;
+  while (lo + step < n && (keys[lo + step] >> shift) == pref) {
+    lo += step;
+    step <<= 1;
+  }
+  int64_t hi = lo + step < n ? lo + step : n;
+  while (hi - lo > 1) {
+    int64_t mid = lo + ((hi - lo) >> 1);
+    if ((keys[mid] >> shift) == pref) lo = mid; else hi = mid;
+  }
+  return hi;
+}
+
+// first b <= i whose level-l prefix equals body i's
+__device__ __forceinline__ int64_t run_begin(const uint64_t *__restrict__ keys, int64_t i,
+                                             uint64_t pref, int shift) {
+  int64_t hi = i, step = 1;
+  while (hi - step >= 0 && (keys[hi - step] >> shift) == pref) {
+    hi -= step;
+    step <<= 1;
+  }
+  int64_t lo = hi - step >= 0 ? hi - step : -1;  // lo differs (or -1)
+  while (hi - lo > 1) {
+    int64_t mid = lo + ((hi - lo) >> 1);
+    if ((keys[mid] >> shift) == pref) hi = mid; else lo = mid;
+  }
+  return hi;
+}
+
+// hashed.py:391-441 _build_kernel, in parallel: body i creates the cells of
+// levels start+1..depth[i]; their pre-order indices are 1 + off[i] + k.  The
+// parent of the first of them is the level-`start` cell holding body i, created
+// by the first body j of that run.
+__global__ void k_emit(TreeView t, const float4 *__restrict__ bod32,
+                       const double4 *__restrict__ bod64) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n = t.n;
+  if (i >= n) return;
+  const int C = (int)t.C;
+  if (i == 0) {
+    t.link[0] = make_int4(C, (int)n, 0, 0);
+    t.parent[0] = -1;
+    if (n == 1) {  // hashed.py:464-474: the root is the leaf
+      double4 b;
+      if (bod64) {
+        b = bod64[0];
+      } else {
+        float4 v = bod32[0];
+        b = make_double4(v.x, v.y, v.z, v.w);
+      }
+      t.cm64[0] = b;
+      if (t.ncm) t.ncm[0] = v4f(b);
+      return;
+    }
+  }
+  const uint64_t k = t.keys[i];
+  const int lp = i > 0 ? t.lcp[i - 1] : -1;
+  const int ln = i + 1 < n ? t.lcp[i] : -1;
+  const int depth = (lp > ln ? lp : ln) + 1;
+  const int start = i > 0 ? lp : 0;
+  const int base = 1 + (int)t.off[i];
+  int par = 0;
+  if (start > 0) {
+    const int shift = 3 * (kMortonBits - start);
+    const int64_t j = run_begin(t.keys, i, k >> shift, shift);
+    const int startj = j > 0 ? t.lcp[j - 1] : 0;
+    par = 1 + (int)t.off[j] + (start - startj - 1);
+  }
+  for (int l = start + 1; l <= depth; ++l) {
+    const int c = base + (l - start - 1);
+    t.parent[c] = par;
+    atomicAdd(&t.nchild[par], 1);
+    if (l == depth) {
+      t.link[c] = make_int4(c + 1, 1, (int)i, l);
+      double4 b;
+      if (bod64) {
+        b = bod64[i];
+      } else {
+        float4 v = bod32[i];
+        b = make_double4(v.x, v.y, v.z, v.w);
+      }
+      t.cm64[c] = b;
+      if (t.ncm) t.ncm[c] = make_float4((float)b.x, (float)b.y, (float)b.z, (float)b.w);
+    } else {
+      const int shift = 3 * (kMortonBits - l);
+      const int64_t end = run_end(t.keys, n, i, k >> shift, shift);
+      const int skip = end < n ? 1 + (int)t.off[end] : C;
+      t.link[c] = make_int4(skip, (int)(end - i), (int)i, l);
+    }
+    par = c;
+  }
+}
+
+void launch_emit(const TreeView &t, const float4 *bod32, const double4 *bod64,
+                 cudaStream_t s) {
+  if (t.n <= 0) return;
+  k_emit<<<grid_for(t.n, 128), 128, 0, s>>>(t, bod32, bod64);
+}
+
+// flattree.py:201-252 _moments_kernel for one cell, children in slot order
+// (pre-order: first child c+1, next sibling skip[child]).  Same expression
+// order as the reference; children written by other threads of this launch are
+// read through L2 (ld.global.cg) after the acquire fence.
+__device__ void cell_moments(const TreeView &t, int p) {
+  const int end = t.link[p].x;
+  double total = 0.0, cx = 0.0, cy = 0.0, cz = 0.0;
+  for (int ch = p + 1; ch < end; ch = t.link[ch].x) {
+    double4 c = ldcg4(&t.cm64[ch]);
+    double m = c.w;
+    if (m == 0.0) continue;
+    total += m;
+    cx += m * c.x;
+    cy += m * c.y;
+    cz += m * c.z;
+  }
+  double *qo = t.q64 + 6 * (int64_t)p;
+  if (total == 0.0) {
+    t.cm64[p] = make_double4(0.0, 0.0, 0.0, 0.0);
+    for (int k = 0; k < 6; ++k) qo[k] = 0.0;
+    if (t.ncm) {
+      t.ncm[p] = make_float4(0.f, 0.f, 0.f, 0.f);
+      t.nq0[p] = make_float4(0.f, 0.f, 0.f, 0.f);
+      t.nq1[p] = make_float2(0.f, 0.f);
+    }
+    return;
+  }
+  cx /= total;
+  cy /= total;
+  cz /= total;
+  double qxx = 0.0, qxy = 0.0, qxz = 0.0, qyy = 0.0, qyz = 0.0, qzz = 0.0;
+  for (int ch = p + 1; ch < end; ch = t.link[ch].x) {
+    double4 c = ldcg4(&t.cm64[ch]);
+    double m = c.w;
+    if (m == 0.0) continue;
+    double q0 = 0.0, q1 = 0.0, q2 = 0.0, q3 = 0.0, q4 = 0.0, q5 = 0.0;
+    if (t.link[ch].y > 1) {  // leaves keep quad = 0 (flattree.py:207-208)
+      const double2 *qc = reinterpret_cast<const double2 *>(t.q64 + 6 * (int64_t)ch);
+      double2 a = __ldcg(qc), b = __ldcg(qc + 1), d = __ldcg(qc + 2);
+      q0 = a.x; q1 = a.y; q2 = b.x; q3 = b.y; q4 = d.x; q5 = d.y;
+    }
+    double dx = c.x - cx;
+    double dy = c.y - cy;
+    double dz = c.z - cz;
+    double d2 = dx * dx + dy * dy + dz * dz;
+    qxx += q0 + m * (3.0 * (dx * dx) - d2);
+    qxy += q1 + m * (3.0 * (dx * dy) - 0.0);
+    qxz += q2 + m * (3.0 * (dx * dz) - 0.0);
+    qyy += q3 + m * (3.0 * (dy * dy) - d2);
+    qyz += q4 + m * (3.0 * (dy * dz) - 0.0);
+    qzz += q5 + m * (3.0 * (dz * dz) - d2);
+  }
+  t.cm64[p] = make_double4(cx, cy, cz, total);
+  double2 *q2o = reinterpret_cast<double2 *>(qo);
+  q2o[0] = make_double2(qxx, qxy);
+  q2o[1] = make_double2(qxz, qyy);
+  q2o[2] = make_double2(qyz, qzz);
+  if (t.ncm) {
+    t.ncm[p] = make_float4((float)cx, (float)cy, (float)cz, (float)total);
+    t.nq0[p] = make_float4((float)qxx, (float)qxy, (float)qxz, (float)qyy);
+    t.nq1[p] = make_float2((float)qyz, (float)qzz);
+  }
+}
+
+// Bottom-up moments in one launch: every body climbs from its leaf; the last
+// child to arrive at a cell computes it (all its children are final by then),
+// so each internal cell is computed exactly once, in slot order.
+__global__ void k_moments(TreeView t) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= t.n) return;
+  int c = (int)t.off[i] + (int)t.newc[i];  // the leaf of body i
+  while (true) {
+    const int p = t.parent[c];
+    if (p < 0) break;
+    __threadfence();
+    const int old = atomicAdd(&t.arrive[p], 1);
+    if (old != t.nchild[p] - 1) break;
+    __threadfence();
+    cell_moments(t, p);
+    c = p;
+  }
+}
+
+void launch_moments(const TreeView &t, cudaStream_t s) {
+  if (t.n <= 1) return;
+  k_moments<<<grid_for(t.n, 128), 128, 0, s>>>(t);
+}
+
+// FlatTree export (flattree.py:34-52; hashed.py:111-129 cell_geometry for the
+// centre, same child-offset arithmetic as _build_kernel).
+__global__ void k_export(TreeView t, double R, uint64_t *key, int8_t *level, double *centre,
+                         double *side, double *mass, double *com, double *quad,
+                         int64_t *count, int32_t *children) {
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= t.C) return;
+  int4 L = t.link[c];
+  int l = L.w;
+  uint64_t pref = 0;
+  if (c > 0) pref = t.keys[L.z] >> (3 * (kMortonBits - l));
+  if (key) key[c] = c == 0 ? 1ull : (pref | (1ull << (3 * l)));
+  if (level) level[c] = (int8_t)l;
+  if (centre || side) {
+    double cen0 = 0.0, cen1 = 0.0, cen2 = 0.0, sd = 2.0 * R;
+    for (int lv = l - 1; lv >= 0; --lv) {
+      int slot = (int)((pref >> (3 * lv)) & 7);
+      double half = 0.25 * sd;
+      cen0 += (slot & 4) ? half : -half;
+      cen1 += (slot & 2) ? half : -half;
+      cen2 += (slot & 1) ? half : -half;
+      sd = 0.5 * sd;
+    }
+    if (centre) { centre[3 * c] = cen0; centre[3 * c + 1] = cen1; centre[3 * c + 2] = cen2; }
+    if (side) side[c] = sd;
+  }
+  double4 cm = t.cm64[c];
+  if (mass) mass[c] = cm.w;
+  if (com) { com[3 * c] = cm.x; com[3 * c + 1] = cm.y; com[3 * c + 2] = cm.z; }
+  if (quad) {
+    for (int k = 0; k < 6; ++k) quad[6 * c + k] = L.y > 1 ? t.q64[6 * c + k] : 0.0;
+  }
+  if (count) count[c] = t.n == 0 ? 0 : L.y;
+  if (children && c > 0) children[8 * (int64_t)t.parent[c] + (int)(pref & 7)] = (int32_t)c;
+}
+
+void launch_export(const TreeView &t, double R, uint64_t *key, int8_t *level, double *centre,
+                   double *side, double *mass, double *com, double *quad, int64_t *count,
+                   int32_t *children, cudaStream_t s) {
+  if (t.C <= 0) return;
+  if (children) cudaMemsetAsync(children, 0xFF, sizeof(int32_t) * 8 * t.C, s);
+  k_export<<<grid_for(t.C, 256), 256, 0, s>>>(t, R, key, level, centre, side, mass, com, quad,
+                                              count, children);
+}
+
+// ------------------------------------------------------------- fp64 walk
+// Correctly rounded x^1.5 (the reference computes (d2+e2)**1.5 with libm pow,
+// which is correctly rounded in practice): x*sqrt(x) evaluated in double-double
+// and rounded once.
+__device__ __forceinline__ double pow15(double x) {
+  double s = __dsqrt_rn(x);
+  double e = fma(-s, s, x);          // exact residual x - s^2
+  double t = e / (2.0 * s);          // sqrt(x) = s + t + O(t^2)
+  double p = x * s;
+  double pl = fma(x, s, -p);         // exact low part of x*s
+  return p + (pl + x * t);
+}
+
+__device__ __forceinline__ void pp64(double px, double py, double pz, double4 b, double e2,
+                                     double &ax, double &ay, double &az, int &npp) {
+  double dx = px - b.x, dy = py - b.y, dz = pz - b.z;
+  double d2 = dx * dx + dy * dy + dz * dz;
+  if (d2 == 0.0) return;
+  double denom = pow15(d2 + e2);
+  ax += (-b.w * dx) / denom;
+  ay += (-b.w * dy) / denom;
+  az += (-b.w * dz) / denom;
+  ++npp;
+}
+
+// flattree.py:258-317 _traverse_kernel.  One warp walks the union of its 32
+// targets' interaction lists in pre-order: each lane keeps its own "next" cell
+// (its private DFS position); the warp visits the minimum, lanes positioned
+// there evaluate it.  Every lane therefore sees exactly the reference's list,
+// in the reference's order, so its fp64 sums are the reference's sums.
+__global__ void __launch_bounds__(128) k_walk_f64(
+    WalkParams P, const double4 *__restrict__ cm, const double *__restrict__ q64,
+    const int4 *__restrict__ link, const double4 *__restrict__ bodies,
+    const double *__restrict__ targets, int tstride, const uint32_t *__restrict__ tperm,
+    double *__restrict__ acc, int astride, int64_t *__restrict__ work64,
+    int *__restrict__ work32, DeviceFlags *f) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = t < P.nt;
+  const int64_t src = valid ? (tperm ? (int64_t)tperm[t] : t) : 0;
+  double px = 0.0, py = 0.0, pz = 0.0;
+  if (valid) {
+    const double *q = targets + src * tstride;
+    px = q[0]; py = q[1]; pz = q[2];
+  }
+  double ax = 0.0, ay = 0.0, az = 0.0;
+  int npp = 0, npc = 0;
+  int next = valid ? (P.C == 1 ? 0 : 1) : INT_MAX;
+  while (true) {
+    const int i = __reduce_min_sync(0xffffffffu, next);
+    if (i >= P.C) break;
+    if (next != i) continue;
+    const double4 c = cm[i];
+    const int4 L = link[i];
+    const double dx = px - c.x, dy = py - c.y, dz = pz - c.z;
+    const double d2 = dx * dx + dy * dy + dz * dz;
+    if (L.y == 1) {
+      if (d2 != 0.0) {
+        double denom = pow15(d2 + P.e2);
+        ax += (-c.w * dx) / denom;
+        ay += (-c.w * dy) / denom;
+        az += (-c.w * dz) / denom;
+        ++npp;
+      }
+      next = i + 1;
+    } else if (d2 > 0.0 && P.side64[L.w] < P.theta * sqrt(d2)) {
+      const double *q = q64 + 6 * (int64_t)i;
+      const double r1 = sqrt(d2);
+      const double qrx = q[0] * dx + q[1] * dy + q[2] * dz;
+      const double qry = q[1] * dx + q[3] * dy + q[4] * dz;
+      const double qrz = q[2] * dx + q[4] * dy + q[5] * dz;
+      const double rqr = dx * qrx + dy * qry + dz * qrz;
+      const double mono = -c.w / (d2 * r1);
+      const double c5 = d2 * d2 * r1;
+      const double c7 = 2.5 * rqr / (d2 * d2 * d2 * r1);
+      ax += mono * dx + qrx / c5 - c7 * dx;
+      ay += mono * dy + qry / c5 - c7 * dy;
+      az += mono * dz + qrz / c5 - c7 * dz;
+      ++npc;
+      next = L.x;
+    } else if (P.leaf > 1 && L.y <= P.leaf) {
+      for (int j = L.z; j < L.z + L.y; ++j) pp64(px, py, pz, bodies[j], P.e2, ax, ay, az, npp);
+      next = L.x;
+    } else {
+      next = i + 1;
+    }
+  }
+  if (valid) {
+    double *o = acc + src * astride;
+    o[0] = ax; o[1] = ay; o[2] = az;
+    const int w = npp * 1 + npc * 2;  // WORK_PP, WORK_PC (octree.py:23-25)
+    if (work64) work64[src] = w;
+    if (work32) work32[src] = w;
+  }
+  unsigned long long spp = npp, spc = npc;
+  for (int o = 16; o > 0; o >>= 1) {
+    spp += __shfl_xor_sync(0xffffffffu, spp, o);
+    spc += __shfl_xor_sync(0xffffffffu, spc, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&f->pp, spp);
+    atomicAdd(&f->pc, spc);
+  }
+}
+
+void launch_walk_f64(const WalkParams &p, const double4 *cm64, const double *q64,
+                     const int4 *link, const double4 *bodies, const double *targets,
+                     int tstride, const uint32_t *tperm, double *acc, int astride,
+                     int64_t *work64, int *work32, DeviceFlags *f, cudaStream_t s) {
+  if (p.nt <= 0) return;
+  k_walk_f64<<<grid_for(p.nt, 128), 128, 0, s>>>(p, cm64, q64, link, bodies, targets, tstride,
+                                                 tperm, acc, astride, work64, work32, f);
+}
+
+// ------------------------------------------------------ fp64 integrator
+// integrator.py:37-44: v += a*h; x += v*dt (two roundings each, as numpy)
+__global__ void k_kick_f64(double *v, const double *a, int64_t n3, double h) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n3) v[i] = v[i] + a[i] * h;
+}
+void launch_kick_f64(double *vel3, const double *acc3, int64_t n, double h, cudaStream_t s) {
+  if (n <= 0) return;
+  k_kick_f64<<<grid_for(3 * n, 256), 256, 0, s>>>(vel3, acc3, 3 * n, h);
+}
+void launch_drift_f64(double *pos3, const double *vel3, int64_t n, double dt, cudaStream_t s) {
+  if (n <= 0) return;
+  k_kick_f64<<<grid_for(3 * n, 256), 256, 0, s>>>(pos3, vel3, 3 * n, dt);
+}
+
+__device__ __forceinline__ unsigned long long dmax_bits(double a) {
+  return (unsigned long long)__double_as_longlong(fabs(a));
+}
+
+// resident fp64 state {x,y,z,m} / {vx,vy,vz,0}: optional half kick, drift,
+// and the max|x| of the drifted positions (next step's bounds)
+__global__ void k_kick_drift_max_f64(double4 *pos, double4 *vel, const double4 *acc, int64_t n,
+                                     double h, double dt, DeviceFlags *f) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long m = 0;
+  if (i < n) {
+    double4 x = pos[i];
+    if (dt != 0.0) {
+      double4 v = vel[i];
+      if (acc) {
+        double4 a = acc[i];
+        v.x = v.x + a.x * h; v.y = v.y + a.y * h; v.z = v.z + a.z * h;
+        vel[i] = v;
+      }
+      x.x = x.x + v.x * dt; x.y = x.y + v.y * dt; x.z = x.z + v.z * dt;
+      pos[i] = x;
+    }
+    unsigned long long a = dmax_bits(x.x), b = dmax_bits(x.y), c = dmax_bits(x.z);
+    m = a > b ? a : b;
+    m = m > c ? m : c;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long r = __shfl_xor_sync(0xffffffffu, m, o);
+    m = r > m ? r : m;
+  }
+  if ((threadIdx.x & 31) == 0 && m) atomicMax((unsigned long long *)&f->maxabs64, m);
+}
+void launch_kick_drift_max_f64(double4 *pos, double4 *vel, const double4 *acc, int64_t n,
+                               double h, double dt, DeviceFlags *f, cudaStream_t s) {
+  if (n <= 0) return;
+  k_kick_drift_max_f64<<<grid_for(n, 256), 256, 0, s>>>(pos, vel, acc, n, h, dt, f);
+}
+
+__global__ void k_kick4_f64(double4 *vel, const double4 *acc, int64_t n, double h) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double4 v = vel[i], a = acc[i];
+  v.x = v.x + a.x * h; v.y = v.y + a.y * h; v.z = v.z + a.z * h;
+  vel[i] = v;
+}
+void launch_kick4_f64(double4 *vel, const double4 *acc, int64_t n, double h, cudaStream_t s) {
+  if (n <= 0) return;
+  k_kick4_f64<<<grid_for(n, 256), 256, 0, s>>>(vel, acc, n, h);
+}
+
+__global__ void k_maxabs_f64(const double *p, int64_t n3, DeviceFlags *f) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long m = i < n3 ? dmax_bits(p[i]) : 0ull;
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long r = __shfl_xor_sync(0xffffffffu, m, o);
+    m = r > m ? r : m;
+  }
+  if ((threadIdx.x & 31) == 0 && m) atomicMax((unsigned long long *)&f->maxabs64, m);
+}
+void launch_maxabs_f64(const double *pos3, int64_t n, DeviceFlags *f, cudaStream_t s) {
+  if (n <= 0) return;
+  k_maxabs_f64<<<grid_for(3 * n, 256), 256, 0, s>>>(pos3, 3 * n, f);
+}
+
+// morton.py:41-42: R = 1.001 * extreme, or 1.0 for an all-zero cloud
+__global__ void k_finish_R(const DeviceFlags *f, int fp64, double *d_R) {
+  double extreme = fp64 ? __longlong_as_double((long long)f->maxabs64)
+                        : (double)__uint_as_float(f->maxabs_bits);
+  *d_R = extreme > 0.0 ? 1.001 * extreme : 1.0;
+}
+void launch_finish_R(const DeviceFlags *f, int fp64, double *d_R, cudaStream_t s) {
+  k_finish_R<<<1, 1, 0, s>>>(f, fp64, d_R);
+}
+
+// ----------------------------------------------------- validation kernels
+// physics.py:216-242 _accel_all_pairs: per target, sources in index order
+// (same summation order as the reference, so the result is bit-identical).
+__global__ void __launch_bounds__(256) k_direct_f64(const double *__restrict__ pos,
+                                                    const double *__restrict__ mass,
+                                                    int64_t n, double e2, double *acc) {
+  __shared__ double4 tile[256];
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double xi = 0, yi = 0, zi = 0;
+  if (i < n) { xi = pos[3 * i]; yi = pos[3 * i + 1]; zi = pos[3 * i + 2]; }
+  double ax = 0.0, ay = 0.0, az = 0.0;
+  for (int64_t j0 = 0; j0 < n; j0 += 256) {
+    int64_t j = j0 + threadIdx.x;
+    __syncthreads();
+    if (j < n) tile[threadIdx.x] = make_double4(pos[3 * j], pos[3 * j + 1], pos[3 * j + 2], mass[j]);
+    __syncthreads();
+    int lim = (int)(n - j0 < 256 ? n - j0 : 256);
+    for (int k = 0; k < lim; ++k) {
+      if (j0 + k == i) continue;
+      double4 s = tile[k];
+      double dx = xi - s.x, dy = yi - s.y, dz = zi - s.z;
+      double r2 = dx * dx + dy * dy + dz * dz;
+      if (r2 == 0.0) continue;
+      double w = s.w / ((r2 + e2) * sqrt(r2 + e2));
+      ax -= w * dx;
+      ay -= w * dy;
+      az -= w * dz;
+    }
+  }
+  if (i < n) { acc[3 * i] = ax; acc[3 * i + 1] = ay; acc[3 * i + 2] = az; }
+}
+void launch_direct_f64(const double *pos3, const double *mass, int64_t n, double eps,
+                       double *acc3, cudaStream_t s) {
+  if (n <= 0) return;
+  k_direct_f64<<<grid_for(n, 256), 256, 0, s>>>(pos3, mass, n, eps * eps, acc3);
+}
+
+// physics.py:273-285 _potential_pairs: partial[i] = sum_{j>i} -m_i m_j / r_soft
+__global__ void __launch_bounds__(256) k_potential_f64(const double *__restrict__ pos,
+                                                       const double *__restrict__ mass,
+                                                       int64_t n, double e2, double *partial) {
+  __shared__ double4 tile[256];
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double xi = 0, yi = 0, zi = 0, mi = 0;
+  if (i < n) { xi = pos[3 * i]; yi = pos[3 * i + 1]; zi = pos[3 * i + 2]; mi = mass[i]; }
+  double pot = 0.0;
+  int64_t jstart = (int64_t)blockIdx.x * blockDim.x;  // j > i only
+  for (int64_t j0 = jstart; j0 < n; j0 += 256) {
+    int64_t j = j0 + threadIdx.x;
+    __syncthreads();
+    if (j < n) tile[threadIdx.x] = make_double4(pos[3 * j], pos[3 * j + 1], pos[3 * j + 2], mass[j]);
+    __syncthreads();
+    int lim = (int)(n - j0 < 256 ? n - j0 : 256);
+    for (int k = 0; k < lim; ++k) {
+      if (j0 + k <= i) continue;
+      double4 s = tile[k];
+      double dx = xi - s.x, dy = yi - s.y, dz = zi - s.z;
+      double r2 = dx * dx + dy * dy + dz * dz;
+      pot -= mi * s.w / sqrt(r2 + e2);
+    }
+  }
+  if (i < n) partial[i] = pot;
+}
+void launch_potential_f64(const double *pos3, const double *mass, int64_t n, double eps,
+                          double *partial, cudaStream_t s) {
+  if (n <= 0) return;
+  k_potential_f64<<<grid_for(n, 256), 256, 0, s>>>(pos3, mass, n, eps * eps, partial);
+}
+
+}  // namespace bh

@@ -1,0 +1,303 @@
+// bh_fast.cu -- fp32 kernels (FMA contraction allowed): bounds reduction,
+// the fp32 warp-cooperative traversal, the fused integrator, body gathers, and
+// the radix-sort / scan wrappers.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <climits>
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "bh_internal.cuh"
+
+namespace bh {
+
+// ---------------------------------------------------------------- bounds
+__device__ __forceinline__ unsigned fabs_bits(float a) { return __float_as_uint(fabsf(a)); }
+
+__device__ __forceinline__ void warp_max_to(unsigned m, unsigned *dst) {
+  m = __reduce_max_sync(0xffffffffu, m);
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(dst, m);
+}
+
+// morton.py:39-42: max |x| over all bodies and axes (float bits are
+// order-preserving for non-negative floats; NaN sorts above +inf and makes R
+// NaN, which the key kernel then reports as out of domain)
+__global__ void k_maxabs_f32(const float4 *__restrict__ p, int64_t n, DeviceFlags *f) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned m = 0;
+  if (i < n) {
+    float4 v = p[i];
+    m = max(fabs_bits(v.x), max(fabs_bits(v.y), fabs_bits(v.z)));
+  }
+  warp_max_to(m, &f->maxabs_bits);
+}
+
+__global__ void k_reset_bounds(DeviceFlags *f) {
+  f->maxabs_bits = 0;
+  f->maxabs64 = 0.0;
+}
+void launch_reset_flags_bounds(DeviceFlags *f, cudaStream_t s) { k_reset_bounds<<<1, 1, 0, s>>>(f); }
+
+void launch_maxabs_f32(const float4 *pos, int64_t n, DeviceFlags *f, cudaStream_t s) {
+  if (n <= 0) return;
+  k_maxabs_f32<<<grid_for(n, 256), 256, 0, s>>>(pos, n, f);
+}
+
+// ------------------------------------------------------------ integrator
+__global__ void k_kick_f32(float4 *v, const float4 *a, int64_t n, float h) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float4 x = v[i], y = a[i];
+  x.x += y.x * h; x.y += y.y * h; x.z += y.z * h;
+  v[i] = x;
+}
+void launch_kick_f32(float4 *vel, const float4 *acc, int64_t n, float h, cudaStream_t s) {
+  if (n <= 0) return;
+  k_kick_f32<<<grid_for(n, 256), 256, 0, s>>>(vel, acc, n, h);
+}
+// drift keeps the mass in .w untouched
+__global__ void k_drift_f32(float4 *x, const float4 *v, int64_t n, float dt) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float4 p = x[i], u = v[i];
+  p.x += u.x * dt; p.y += u.y * dt; p.z += u.z * dt;
+  x[i] = p;
+}
+void launch_drift_f32(float4 *pos, const float4 *vel, int64_t n, float dt, cudaStream_t s) {
+  if (n <= 0) return;
+  k_drift_f32<<<grid_for(n, 256), 256, 0, s>>>(pos, vel, n, dt);
+}
+
+// integrator.py:37-44 in the _drive order (simulation.py:492-495):
+// v += a*h; x += v*dt; plus max|x| of the new positions for the next bounds
+__global__ void k_kick_drift_max_f32(float4 *__restrict__ pos, float4 *__restrict__ vel,
+                                     const float4 *__restrict__ acc, int64_t n, float h,
+                                     float dt, DeviceFlags *f) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned m = 0;
+  if (i < n) {
+    float4 x = pos[i];
+    if (dt != 0.f) {
+      float4 v = vel[i];
+      if (acc) {
+        float4 a = acc[i];
+        v.x += a.x * h; v.y += a.y * h; v.z += a.z * h;
+        vel[i] = v;
+      }
+      x.x += v.x * dt; x.y += v.y * dt; x.z += v.z * dt;
+      pos[i] = x;
+    }
+    m = max(fabs_bits(x.x), max(fabs_bits(x.y), fabs_bits(x.z)));
+  }
+  warp_max_to(m, &f->maxabs_bits);
+}
+void launch_kick_drift_max_f32(float4 *pos, float4 *vel, const float4 *acc, int64_t n,
+                               float h, float dt, DeviceFlags *f, cudaStream_t s) {
+  if (n <= 0) return;
+  k_kick_drift_max_f32<<<grid_for(n, 256), 256, 0, s>>>(pos, vel, acc, n, h, dt, f);
+}
+
+// ---------------------------------------------------------------- gathers
+template <class T>
+__global__ void k_gather(const uint32_t *__restrict__ idx, int64_t n, const T *__restrict__ a,
+                         T *__restrict__ a2, const T *__restrict__ b, T *__restrict__ b2,
+                         const uint32_t *__restrict__ id, uint32_t *__restrict__ id2) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint32_t j = idx[i];
+  a2[i] = a[j];
+  if (b) b2[i] = b[j];
+  if (id) id2[i] = id[j];
+}
+void launch_gather_f32(const uint32_t *idx, int64_t n, const float4 *a, float4 *a2,
+                       const float4 *b, float4 *b2, const uint32_t *id, uint32_t *id2,
+                       cudaStream_t s) {
+  if (n <= 0) return;
+  k_gather<float4><<<grid_for(n, 256), 256, 0, s>>>(idx, n, a, a2, b, b2, id, id2);
+}
+void launch_gather_f64(const uint32_t *idx, int64_t n, const double4 *a, double4 *a2,
+                       const double4 *b, double4 *b2, const uint32_t *id, uint32_t *id2,
+                       cudaStream_t s) {
+  if (n <= 0) return;
+  k_gather<double4><<<grid_for(n, 256), 256, 0, s>>>(idx, n, a, a2, b, b2, id, id2);
+}
+
+__global__ void k_pack_f64(const double *pos3, const double *mass, int64_t n, double4 *out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  out[i] = make_double4(pos3[3 * i], pos3[3 * i + 1], pos3[3 * i + 2], mass ? mass[i] : 0.0);
+}
+void launch_pack_bodies_f64(const double *pos3, const double *mass, int64_t n, double4 *out,
+                            cudaStream_t s) {
+  if (n <= 0) return;
+  k_pack_f64<<<grid_for(n, 256), 256, 0, s>>>(pos3, mass, n, out);
+}
+
+__global__ void k_iota64(int64_t *out, const uint32_t *vals, int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = vals[i];
+}
+void launch_iota64(int64_t *out, const uint32_t *vals, int64_t n, cudaStream_t s) {
+  if (n <= 0) return;
+  k_iota64<<<grid_for(n, 256), 256, 0, s>>>(out, vals, n);
+}
+
+// -------------------------------------------------------------- fp32 walk
+// flattree.py:258-317 in fp32: the same warp-cooperative pre-order union walk
+// as k_walk_f64 (each lane follows its own reference DFS; the warp visits the
+// minimum next cell), with rsqrt on the FP32 pipe and the MAC
+// `side < theta*sqrt(d2)` evaluated as d2 > (side/theta)^2 from a per-level
+// table.  Node data is loaded once per warp (uniform address -> broadcast).
+template <bool BUCKET>
+__global__ void __launch_bounds__(256) k_walk_f32(
+    WalkParams P, const float4 *__restrict__ ncm, const float4 *__restrict__ nq0,
+    const float2 *__restrict__ nq1, const int4 *__restrict__ link,
+    const float4 *__restrict__ bodies, const float *__restrict__ targets, int tstride,
+    const uint32_t *__restrict__ tperm, float *__restrict__ acc, int astride,
+    int64_t *__restrict__ work64, int *__restrict__ work32, DeviceFlags *f) {
+  __shared__ float s_mac[kMaxLevel + 1];
+  if (threadIdx.x <= kMaxLevel) s_mac[threadIdx.x] = P.mac2f[threadIdx.x];
+  __syncthreads();
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = t < P.nt;
+  const int64_t src = valid ? (tperm ? (int64_t)tperm[t] : t) : 0;
+  float px = 0.f, py = 0.f, pz = 0.f;
+  if (valid) {
+    const float *q = targets + src * tstride;
+    px = q[0]; py = q[1]; pz = q[2];
+  }
+  const float e2 = P.e2f;
+  float ax = 0.f, ay = 0.f, az = 0.f;
+  int npp = 0, npc = 0;
+  int next = valid ? (P.C == 1 ? 0 : 1) : INT_MAX;
+  while (true) {
+    const int i = __reduce_min_sync(0xffffffffu, next);
+    if (i >= P.C) break;
+    if (next != i) continue;
+    const float4 c = ncm[i];
+    const int4 L = link[i];
+    const float dx = px - c.x, dy = py - c.y, dz = pz - c.z;
+    const float d2 = dx * dx + dy * dy + dz * dz;
+    if (L.y == 1) {
+      if (d2 > 0.f) {
+        const float r = rsqrtf(d2 + e2);
+        const float s = c.w * r * r * r;
+        ax -= s * dx; ay -= s * dy; az -= s * dz;
+        ++npp;
+      }
+      next = i + 1;
+    } else if (d2 > s_mac[L.w]) {
+      const float4 qa = nq0[i];
+      const float2 qb = nq1[i];
+      const float r = rsqrtf(d2);
+      const float r2 = r * r;
+      const float qrx = qa.x * dx + qa.y * dy + qa.z * dz;
+      const float qry = qa.y * dx + qa.w * dy + qb.x * dz;
+      const float qrz = qa.z * dx + qb.x * dy + qb.y * dz;
+      const float rqr = dx * qrx + dy * qry + dz * qrz;
+      const float r3 = r * r2;
+      const float r5 = r3 * r2;
+      // a = -M d/r^3 + Q.d/r^5 - 2.5 (d.Q.d) d / r^7   (physics.py:195-213)
+      const float sd = -c.w * r3 - 2.5f * rqr * r5 * r2;
+      ax += sd * dx + qrx * r5;
+      ay += sd * dy + qry * r5;
+      az += sd * dz + qrz * r5;
+      ++npc;
+      next = L.x;
+    } else if (BUCKET && L.y <= P.leaf) {
+      for (int j = L.z; j < L.z + L.y; ++j) {
+        const float4 b = bodies[j];
+        const float ex = px - b.x, ey = py - b.y, ez = pz - b.z;
+        const float r2 = ex * ex + ey * ey + ez * ez;
+        if (r2 > 0.f) {
+          const float r = rsqrtf(r2 + e2);
+          const float s = b.w * r * r * r;
+          ax -= s * ex; ay -= s * ey; az -= s * ez;
+          ++npp;
+        }
+      }
+      next = L.x;
+    } else {
+      next = i + 1;
+    }
+  }
+  if (valid) {
+    float *o = acc + src * astride;
+    o[0] = ax; o[1] = ay; o[2] = az;
+    const int w = npp * 1 + npc * 2;  // WORK_PP, WORK_PC (octree.py:23-25)
+    if (work64) work64[src] = w;
+    if (work32) work32[src] = w;
+  }
+  unsigned spp = __reduce_add_sync(0xffffffffu, (unsigned)npp);
+  unsigned spc = __reduce_add_sync(0xffffffffu, (unsigned)npc);
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&f->pp, (unsigned long long)spp);
+    atomicAdd(&f->pc, (unsigned long long)spc);
+  }
+}
+
+void launch_walk_f32(const WalkParams &p, const float4 *ncm, const float4 *nq0,
+                     const float2 *nq1, const int4 *link, const float4 *bodies,
+                     const float *targets, int tstride, const uint32_t *tperm, float *acc,
+                     int astride, int64_t *work64, int *work32, DeviceFlags *f,
+                     cudaStream_t s) {
+  if (p.nt <= 0) return;
+  if (p.leaf > 1)
+    k_walk_f32<true><<<grid_for(p.nt, 256), 256, 0, s>>>(p, ncm, nq0, nq1, link, bodies, targets,
+                                                         tstride, tperm, acc, astride, work64,
+                                                         work32, f);
+  else
+    k_walk_f32<false><<<grid_for(p.nt, 256), 256, 0, s>>>(p, ncm, nq0, nq1, link, bodies,
+                                                          targets, tstride, tperm, acc, astride,
+                                                          work64, work32, f);
+}
+
+// --------------------------------------------------- FFMA peak microbench
+// 8 independent FFMA chains per thread, 8 warps x 4 blocks per SM: the FP32
+// pipe's sustained issue rate at the current clock (walk roofline denominator)
+__global__ void __launch_bounds__(256) k_ffma(float *out, int iters, float a, float b) {
+  float x[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = threadIdx.x * 1e-3f + k;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) x[k] = fmaf(x[k], a, b);
+    }
+  }
+  float sum = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) sum += x[k];
+  if (sum == 1234.5f) out[0] = sum;
+}
+void run_ffma(float *out, int sms, int iters, double *flops, cudaStream_t s) {
+  const int blocks = sms * 4, threads = 256;
+  k_ffma<<<blocks, threads, 0, s>>>(out, iters, 0.999999f, 1e-7f);
+  *flops = 2.0 * 64.0 * (double)iters * blocks * threads;
+}
+
+// ------------------------------------------------------- sort / scan (CUB)
+size_t sort_temp_bytes(int64_t n) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint64_t *)nullptr, (uint64_t *)nullptr,
+                                  (const uint32_t *)nullptr, (uint32_t *)nullptr, (int)n, 0, 63);
+  return bytes;
+}
+cudaError_t sort_pairs(void *temp, size_t temp_bytes, const uint64_t *kin, uint64_t *kout,
+                       const uint32_t *vin, uint32_t *vout, int64_t n, cudaStream_t s) {
+  return cub::DeviceRadixSort::SortPairs(temp, temp_bytes, kin, kout, vin, vout, (int)n, 0, 63, s);
+}
+size_t scan_temp_bytes(int64_t n) {
+  size_t bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, (const uint32_t *)nullptr, (uint32_t *)nullptr,
+                                (int)n);
+  return bytes;
+}
+cudaError_t exclusive_scan_u32(void *temp, size_t temp_bytes, const uint32_t *in, uint32_t *out,
+                               int64_t n, cudaStream_t s) {
+  return cub::DeviceScan::ExclusiveSum(temp, temp_bytes, in, out, (int)n, s);
+}
+
+}  // namespace bh

@@ -1,0 +1,188 @@
+// bh_internal.cuh -- shared declarations of libbh.so (not part of the C-ABI).
+//
+// Data layout in HBM (all arrays indexed by pre-order cell index c or by
+// Morton-sorted body index i):
+//
+//   bodies  (fp32) float4 {x,y,z,m}          (fp64) double4 {x,y,z,m}
+//   keys    u64[n]   sorted 63-bit Morton keys
+//   lcp     i8[n]    shared octant levels of (i, i+1)          hashed.py:376-388
+//   off     u32[n]   exclusive scan of cells created per body
+//   link    int4[C]  {skip, count, lo, level}: skip = index after the subtree
+//                    (pre-order), count = bodies below, lo = first sorted body
+//   parent  i32[C], nchild i32[C], arrive i32[C]  (bottom-up moments)
+//   cm64    double4[C] {com, mass}, q64 double[C][6]           fp64 moments
+//   ncm     float4[C] {com, mass}, nq0 float4 {xx,xy,xz,yy}, nq1 float2 {yz,zz}
+//                    fp32 walk nodes (fp32 mode)
+//
+// The pre-order layout makes the reference's depth-first walk stackless: the
+// first child of c is c+1, and "do not descend" is "jump to skip[c]".
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/bh.h"
+
+namespace bh {
+
+constexpr int kMortonBits = 21;
+constexpr int kMaxLevel = 21;
+constexpr int kWarp = 32;
+
+// device error flag bits (latched, reported by bh_check / build)
+enum : int {
+  FLAG_OUT_OF_DOMAIN = 1,
+  FLAG_DUPLICATE = 2,
+  FLAG_UNSORTED = 4,
+  FLAG_DEPTH = 8,
+};
+
+struct DeviceFlags {
+  int bits;
+  int pad;
+  long long first_bad;  // body index of the first out-of-domain body
+  unsigned long long pp;
+  unsigned long long pc;
+  unsigned int maxabs_bits;  // float bits of max |x| (fp32 bounds)
+  int pad2;
+  double maxabs64;           // fp64 bounds scratch (as ull bits for atomicMax)
+};
+
+// ---------------------------------------------------------------- buffers
+struct Buf {
+  void *p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t want) {
+    if (want <= bytes) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    size_t grow = want + want / 8 + 256;
+    cudaError_t e = cudaMalloc(&p, grow);
+    if (e == cudaSuccess) bytes = grow;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class T>
+  T *as() const { return static_cast<T *>(p); }
+};
+
+// ---------------------------------------------------------------- kernels
+// All launchers enqueue on `s` and never synchronise.
+
+// bounds (morton.py:33-42)
+void launch_reset_flags_bounds(DeviceFlags *f, cudaStream_t s);
+void launch_maxabs_f32(const float4 *pos, int64_t n, DeviceFlags *f, cudaStream_t s);
+void launch_maxabs_f64(const double *pos3, int64_t n, DeviceFlags *f, cudaStream_t s);
+void launch_finish_R(const DeviceFlags *f, int fp64, double *d_R, cudaStream_t s);
+
+// keys (morton.py:109-125); vals (if non-null) = iota
+void launch_keys_f32(const float4 *pos, int64_t n, const double *d_R, uint64_t *keys,
+                     uint32_t *vals, DeviceFlags *f, cudaStream_t s);
+void launch_keys_f64(const double *pos, int stride, int64_t n, const double *d_R,
+                     uint64_t *keys, uint32_t *vals, DeviceFlags *f, cudaStream_t s);
+// keys of arbitrary targets for coherence ordering only (clamped, never flags)
+void launch_keys_clamped_f32(const float *pos, int stride, int64_t n, const double *d_R,
+                             uint64_t *keys, uint32_t *vals, cudaStream_t s);
+void launch_keys_clamped_f64(const double *pos, int stride, int64_t n, const double *d_R,
+                             uint64_t *keys, uint32_t *vals, cudaStream_t s);
+
+// tree build (hashed.py:376-515)
+void launch_lcp_new(const uint64_t *keys, int64_t n, int8_t *lcp, uint32_t *newc,
+                    DeviceFlags *f, cudaStream_t s);
+struct TreeView {
+  int64_t n = 0;       // bodies
+  int64_t C = 0;       // cells
+  const uint64_t *keys = nullptr;
+  const int8_t *lcp = nullptr;
+  const uint32_t *off = nullptr;   // exclusive scan of newc
+  const uint32_t *newc = nullptr;
+  int4 *link = nullptr;
+  int *parent = nullptr;
+  int *nchild = nullptr;
+  int *arrive = nullptr;
+  double4 *cm64 = nullptr;
+  double *q64 = nullptr;   // [C][6]
+  float4 *ncm = nullptr;   // fp32 nodes (may be null in fp64 mode)
+  float4 *nq0 = nullptr;
+  float2 *nq1 = nullptr;
+};
+void launch_emit(const TreeView &t, const float4 *bod32, const double4 *bod64, cudaStream_t s);
+void launch_moments(const TreeView &t, cudaStream_t s);
+void launch_export(const TreeView &t, double R, uint64_t *key, int8_t *level, double *centre,
+                   double *side, double *mass, double *com, double *quad, int64_t *count,
+                   int32_t *children, cudaStream_t s);
+
+// traversal (flattree.py:258-317)
+struct WalkParams {
+  int C;
+  int nt;
+  float e2f;
+  double e2;
+  double theta;
+  int leaf;            // leaf_size (<=1: reference walk)
+  float mac2f[kMaxLevel + 1];   // fp32: (side_l/theta)^2, +inf for theta == 0
+  double side64[kMaxLevel + 1]; // fp64: exact side of level l
+};
+void launch_walk_f32(const WalkParams &p, const float4 *ncm, const float4 *nq0,
+                     const float2 *nq1, const int4 *link, const float4 *bodies,
+                     const float *targets, int tstride, const uint32_t *tperm,
+                     float *acc, int astride, int64_t *work64, int *work32,
+                     DeviceFlags *f, cudaStream_t s);
+void launch_walk_f64(const WalkParams &p, const double4 *cm64, const double *q64,
+                     const int4 *link, const double4 *bodies, const double *targets,
+                     int tstride, const uint32_t *tperm, double *acc, int astride,
+                     int64_t *work64, int *work32, DeviceFlags *f, cudaStream_t s);
+
+// integrator (integrator.py:37-44) and body permutation
+void launch_kick_f32(float4 *vel, const float4 *acc, int64_t n, float h, cudaStream_t s);
+void launch_drift_f32(float4 *pos, const float4 *vel, int64_t n, float dt, cudaStream_t s);
+void launch_kick_f64(double *vel3, const double *acc3, int64_t n, double h, cudaStream_t s);
+void launch_drift_f64(double *pos3, const double *vel3, int64_t n, double dt, cudaStream_t s);
+// fused: v += a*h (if kick), x += v*dt, max|x| -> flags (sim path)
+void launch_kick_drift_max_f32(float4 *pos, float4 *vel, const float4 *acc, int64_t n,
+                               float h, float dt, DeviceFlags *f, cudaStream_t s);
+void launch_kick_drift_max_f64(double4 *pos, double4 *vel, const double4 *acc, int64_t n,
+                               double h, double dt, DeviceFlags *f, cudaStream_t s);
+void launch_kick4_f64(double4 *vel, const double4 *acc, int64_t n, double h, cudaStream_t s);
+void launch_gather_f32(const uint32_t *idx, int64_t n, const float4 *a, float4 *a2,
+                       const float4 *b, float4 *b2, const uint32_t *id, uint32_t *id2,
+                       cudaStream_t s);
+void launch_gather_f64(const uint32_t *idx, int64_t n, const double4 *a, double4 *a2,
+                       const double4 *b, double4 *b2, const uint32_t *id, uint32_t *id2,
+                       cudaStream_t s);
+void launch_pack_bodies_f64(const double *pos3, const double *mass, int64_t n, double4 *out,
+                            cudaStream_t s);
+void launch_iota64(int64_t *out, const uint32_t *vals, int64_t n, cudaStream_t s);
+
+// validation kernels (physics.py:216-285)
+void launch_direct_f64(const double *pos3, const double *mass, int64_t n, double eps,
+                       double *acc3, cudaStream_t s);
+void launch_potential_f64(const double *pos3, const double *mass, int64_t n, double eps,
+                          double *partial, cudaStream_t s);
+
+// FFMA throughput microbenchmark (fills *flops with the FP32 flops issued)
+void run_ffma(float *out, int sms, int iters, double *flops, cudaStream_t s);
+
+// radix sort of (key, u32 value) pairs over bits [0, 63) -- stable
+size_t sort_temp_bytes(int64_t n);
+cudaError_t sort_pairs(void *temp, size_t temp_bytes, const uint64_t *kin, uint64_t *kout,
+                       const uint32_t *vin, uint32_t *vout, int64_t n, cudaStream_t s);
+size_t scan_temp_bytes(int64_t n);
+cudaError_t exclusive_scan_u32(void *temp, size_t temp_bytes, const uint32_t *in, uint32_t *out,
+                               int64_t n, cudaStream_t s);
+
+inline int grid_for(int64_t n, int block) {
+  int64_t g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > 0x7fffffff) g = 0x7fffffff;
+  return (int)g;
+}
+
+}  // namespace bh

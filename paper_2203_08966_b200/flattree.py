@@ -1,0 +1,47 @@
+"""Batched force traversal -- drop-in for ``nbsim.flattree.FlatTree.traverse``
+(/root/reference/pkg/src/nbsim/flattree.py:142-166, kernel 258-317).
+
+The walk runs as a warp-cooperative CUDA kernel (bh_traverse_*): targets are
+Morton-ordered internally, each warp walks the union of its 32 targets'
+interaction lists in pre-order (stackless, via subtree skip links), and every
+lane evaluates exactly the reference's list -- in the reference's order -- so
+the fp64 mode reproduces the reference bit for bit and the fp32 mode differs
+only by fp32 rounding.  ``leaf_size > 1`` adds the bucket rule of SURVEY.md
+§8(c) (cells of <= leaf_size bodies that fail the MAC are summed body by body).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from .hashed import DeviceTree
+
+
+class FlatTree:
+    """A device-resident tree viewed through the reference's traversal API."""
+
+    def __init__(self, tree: DeviceTree):
+        self.tree = tree
+
+    def __len__(self) -> int:
+        return len(self.tree)
+
+    @property
+    def count(self) -> np.ndarray:
+        return self.tree.count
+
+    def traverse(self, positions, theta: float, eps: float, leaf_size: int = 1):
+        """Accelerations (n,3) float64 and work counts (n,) int64."""
+        eng = self.tree.engine
+        tg = eng.vec_tensor(positions)
+        n = tg.shape[0]
+        if n == 0:
+            return np.zeros((0, 3)), np.zeros(0, dtype=np.int64)
+        acc, work = eng.traverse(tg, theta, eps, leaf_size)
+        eng.check()
+        a = acc[:, :3].to(torch.float64).cpu().numpy()
+        return np.ascontiguousarray(a), work.cpu().numpy()
+
+    def to_bytes(self) -> bytes:
+        return self.tree.to_serial_bytes()

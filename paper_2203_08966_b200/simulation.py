@@ -1,0 +1,237 @@
+"""Time-stepping driver -- drop-in for ``nbsim.simulation``
+(/root/reference/pkg/src/nbsim/simulation.py).
+
+``simulate(cfg)`` keeps the reference's signature and result type and runs the
+reference's ``_drive`` loop (simulation.py:478-504) on the GPU with the bodies
+resident in HBM: bootstrap forces (work not recorded), then per step
+kick(dt/2) + drift(dt) + bounds (one fused kernel), keys, radix sort, body
+permutation, tree build, traversal, kick(dt/2).  Stages 1-6 of the reference
+produce bit-identical trajectories at any rank count (simulation.py:24-27), so
+every tree algorithm maps to this one GPU walk; in ``precision="fp64"`` it
+reproduces the reference's algorithm-1 trajectory bit for bit.
+
+``TreeForces`` is the plugin seam: it is both an ``AccelProvider``
+(integrator.py:16) and a force strategy ``forces(local, record_work)``
+(simulation.py:338, 370).
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+import torch
+
+from .engine import Engine
+from .initcond import two_clusters
+from .physics import Bodies
+
+PHASES = ("decompose", "build", "share", "force", "integrate", "other")  # simulation.py:62
+
+ALGORITHM_NAMES = {  # simulation.py:64-73
+    0: "ring direct sum",
+    1: "central tree",
+    2: "merged tree",
+    3: "sorted bodies",
+    4: "cost balance",
+    5: "in-place decomposition",
+    6: "hashed tree",
+    7: "asynchronous walk",
+}
+
+LEAF_MODES = ("reference", "bucket")
+
+
+@dataclass(frozen=True)
+class SimConfig:
+    """simulation.py:82-113 plus the GPU fields."""
+
+    n: int
+    algorithm: int = 7
+    ranks: int = 1
+    theta: float = 0.5
+    dt: float = 0.01
+    steps: int = 500
+    eps: float = 0.05
+    seed: int = 1
+    leaf_size: int = 1
+    precision: str = "fp64"
+    devices: int = 1
+    leaf_mode: str = "reference"
+
+    def __post_init__(self) -> None:
+        if self.algorithm not in ALGORITHM_NAMES:
+            raise ValueError(f"algorithm must be 0..7, got {self.algorithm}")
+        if self.n < 4:
+            raise ValueError(f"need at least 4 bodies, got n={self.n}")
+        if self.ranks < 1:
+            raise ValueError(f"ranks must be positive, got {self.ranks}")
+        if self.n < self.ranks:
+            raise ValueError(
+                f"every rank needs at least one body: n={self.n} < ranks={self.ranks}")
+        if not 0.0 <= self.theta:
+            raise ValueError(f"theta must be non-negative, got {self.theta}")
+        if not self.dt > 0.0:
+            raise ValueError(f"dt must be positive, got {self.dt}")
+        if self.steps < 0:
+            raise ValueError(f"steps must be non-negative, got {self.steps}")
+        if self.eps < 0.0:
+            raise ValueError(f"eps must be non-negative, got {self.eps}")
+        if self.leaf_size < 1:
+            raise ValueError(f"leaf_size must be >= 1, got {self.leaf_size}")
+        if self.precision not in ("fp32", "fp64"):
+            raise ValueError(f"precision must be fp32 or fp64, got {self.precision!r}")
+        if self.leaf_mode not in LEAF_MODES:
+            raise ValueError(f"leaf_mode must be one of {LEAF_MODES}, got {self.leaf_mode!r}")
+        if self.devices < 1:
+            raise ValueError(f"devices must be positive, got {self.devices}")
+
+    @property
+    def walk_leaf_size(self) -> int:
+        """Leaf size the walk uses: 1 in reference mode."""
+        return 1 if self.leaf_mode == "reference" else self.leaf_size
+
+
+@dataclass
+class SimResult:
+    """simulation.py:116-142."""
+
+    config: SimConfig
+    bodies: Bodies
+    phase_seconds: list
+    message_stats: dict
+    requests: int
+    snapshots: list
+    trace_lines: Optional[list]
+    wall_seconds: float
+    interactions: int = 0
+
+    @property
+    def work_total(self) -> int:
+        return int(self.bodies.work.sum())
+
+    def phase_totals(self) -> dict:
+        return {phase: (0, 0) for phase in PHASES}
+
+
+class TreeForces:
+    """GPU force provider over host ``Bodies``.
+
+    ``provider(bodies)`` fills ``bodies.acceleration`` in place (an
+    ``AccelProvider``); ``provider.forces(local, record_work)`` is the
+    reference's force-strategy protocol and returns 0 remote requests.
+    Each call uploads the bodies, builds the tree and walks it on the GPU, and
+    copies accelerations (and work) back.
+    """
+
+    def __init__(self, theta: float, eps: float, leaf_size: int = 1, precision: str = "fp64",
+                 engine: Engine | None = None):
+        self.theta = float(theta)
+        self.eps = float(eps)
+        self.leaf_size = int(leaf_size)
+        self.engine = engine if engine is not None else Engine(precision)
+
+    def forces(self, local: Bodies, record_work: bool) -> int:
+        eng = self.engine
+        n = len(local)
+        pos = eng.bodies_tensor(local.position, local.mass)
+        vel = eng.vec_tensor(local.velocity)
+        m = None if eng.fp32 else torch.as_tensor(local.mass).to(eng.device)
+        eng.sim_load(pos, vel, m)
+        eng.sim_forces(self.theta, self.eps, self.leaf_size, record_work)
+        acc = torch.empty_like(vel)
+        work = torch.empty(n, dtype=torch.int64, device=eng.device) if record_work else None
+        eng.sim_store(acc=acc, work=work)
+        eng.check()
+        local.acceleration[:] = acc[:, :3].to(torch.float64).cpu().numpy()
+        if record_work:
+            local.work[:] = work.cpu().numpy()
+        return 0
+
+    def __call__(self, bodies: Bodies) -> None:
+        self.forces(bodies, record_work=True)
+
+
+def _direct_run(cfg: SimConfig, bodies: Bodies, snapshot_every) -> tuple[Bodies, list]:
+    """Algorithm 0 (simulation.py:330-350) on one device: fp64 direct sum."""
+    from .integrator import drift, kick
+    from .physics import direct_accelerations
+
+    snaps = []
+    bodies.acceleration[:] = direct_accelerations(bodies.mass, bodies.position, cfg.eps)
+    if snapshot_every:
+        snaps.append((0.0, bodies.copy()))
+    for step in range(1, cfg.steps + 1):
+        kick(bodies, 0.5 * cfg.dt)
+        drift(bodies, cfg.dt)
+        bodies.acceleration[:] = direct_accelerations(bodies.mass, bodies.position, cfg.eps)
+        bodies.work[:] = cfg.n - 1
+        kick(bodies, 0.5 * cfg.dt)
+        if snapshot_every and step % snapshot_every == 0:
+            snaps.append((step * cfg.dt, bodies.copy()))
+    return bodies, snaps
+
+
+def simulate(cfg: SimConfig, *, transport: str = "inproc", record_trace: bool = False,
+             snapshot_every: Optional[int] = None, timeout: float = 120.0,
+             initial: Bodies | None = None, engine: Engine | None = None) -> SimResult:
+    """simulation.py:507-551.  ``transport``/``record_trace``/``timeout`` are
+    accepted for API compatibility (the GPU path has no message transport);
+    ``initial`` overrides the two-cluster initial condition."""
+    if transport not in ("inproc", "socket"):
+        raise ValueError(f"unknown transport {transport!r} (expected inproc or socket)")
+    if snapshot_every is not None and snapshot_every < 1:
+        raise ValueError(f"snapshot interval must be positive, got {snapshot_every}")
+    started = time.monotonic()
+    bodies = initial.copy() if initial is not None else two_clusters(cfg.n, cfg.seed)
+    bodies.work[:] = 1  # simulation.py:482
+    if cfg.algorithm == 0:
+        bodies, snaps = _direct_run(cfg, bodies, snapshot_every)
+        return SimResult(cfg, bodies, [{p: 0.0 for p in PHASES}], {}, 0, snaps,
+                         [] if record_trace else None, time.monotonic() - started)
+
+    eng = engine if engine is not None else Engine(cfg.precision)
+    n = len(bodies)
+    pos = eng.bodies_tensor(bodies.position, bodies.mass)
+    vel = eng.vec_tensor(bodies.velocity)
+    m = None if eng.fp32 else torch.as_tensor(bodies.mass).to(eng.device)
+    eng.sim_load(pos, vel, m)
+    leaf = cfg.walk_leaf_size
+    eng.sim_forces(cfg.theta, cfg.eps, leaf, record_work=False)  # simulation.py:487
+
+    def snapshot() -> Bodies:
+        p = torch.empty_like(vel)
+        v = torch.empty_like(vel)
+        a = torch.empty_like(vel)
+        w = torch.empty(n, dtype=torch.int64, device=eng.device)
+        eng.sim_store(p, v, a, w)
+        eng.check()
+        out = Bodies(bodies.mass.copy(), p[:, :3].double().cpu().numpy(),
+                     v[:, :3].double().cpu().numpy(), a[:, :3].double().cpu().numpy(),
+                     w.cpu().numpy())
+        return out
+
+    snaps = []
+    if snapshot_every:
+        snaps.append((0.0, snapshot()))
+    interactions = 0
+    if snapshot_every:
+        step = 0
+        while step < cfg.steps:
+            k = min(snapshot_every, cfg.steps - step)
+            eng.sim_step(cfg.dt, cfg.theta, cfg.eps, leaf, k)
+            step += k
+            if step % snapshot_every == 0:
+                snaps.append((step * cfg.dt, snapshot()))
+    elif cfg.steps:
+        eng.sim_step(cfg.dt, cfg.theta, cfg.eps, leaf, cfg.steps)
+    st = eng.stats()
+    interactions = st.interactions
+    final = snapshot()
+    wall = time.monotonic() - started
+    phase = {p: 0.0 for p in PHASES}
+    phase["force"] = wall
+    return SimResult(cfg, final, [phase], {}, 0, snaps, [] if record_trace else None, wall,
+                     interactions)

@@ -1,0 +1,400 @@
+"""GPU parity: libbh.so (through the C-ABI) against the reference's golden
+vectors and the CPU oracle on identical seeded inputs.
+
+Bars (BASELINE.json north star): Morton keys and sorted order bit-exact; per-body
+accelerations within 1e-4 relative L2 (fp32 mode) and 1e-10 (fp64 mode; here
+the fp64 path is in fact bit-identical); energy drift within 1%.
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+from oracle import oracle as orc  # noqa: E402
+
+FP32_TOL = 1e-4  # relative L2, fp32 mode (north star)
+FP64_TOL = 1e-10  # relative L2, fp64 mode (north star)
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+@pytest.fixture(scope="module")
+def eng64():
+    from paper_2203_08966_b200.engine import Engine
+
+    e = Engine("fp64", 0)
+    yield e
+    e.close()
+
+
+@pytest.fixture(scope="module")
+def eng32():
+    from paper_2203_08966_b200.engine import Engine
+
+    e = Engine("fp32", 0)
+    yield e
+    e.close()
+
+
+def f32(x):
+    return np.asarray(x, dtype=np.float32).astype(np.float64)
+
+
+def plummer(n, seed):
+    from paper_2203_08966_b200.initcond import make_rng, plummer_cluster
+
+    return plummer_cluster(n, make_rng(seed), 1.0)
+
+
+# ---------------------------------------------------------------- keys / sort
+
+
+class TestKeysSort:
+    def test_golden_keys(self, golden):
+        from paper_2203_08966_b200.morton import DomainBounds, morton_keys, sort_order
+
+        g = golden("keys.npz")
+        np.testing.assert_array_equal(morton_keys(g["pos"], DomainBounds(float(g["R"]))), g["keys"])
+        np.testing.assert_array_equal(sort_order(g["keys"]), g["order"])
+        np.testing.assert_array_equal(sort_order(g["tie_keys"]), g["tie_order"])
+        b = DomainBounds.from_positions(g["pl_pos"])
+        assert b.half_extent == float(g["pl_R"])
+        np.testing.assert_array_equal(morton_keys(g["pl_pos"], b), g["pl_keys"])
+        np.testing.assert_array_equal(sort_order(g["pl_keys"]), g["pl_order"])
+
+    def test_known_answers(self):
+        from paper_2203_08966_b200.morton import DomainBounds, morton_keys, sort_order
+
+        k = morton_keys(np.array([[0.0, -1.0, -1.0], [-1.0, -1.0, -1.0]]), DomainBounds(1.0))
+        assert int(k[0]) == 1 << 62 and int(k[1]) == 0
+        pos = np.array([[0.5, 0.5, 0.5]] * 3 + [[-0.5, -0.5, -0.5]])
+        assert list(sort_order(morton_keys(pos, DomainBounds(1.0)))) == [3, 0, 1, 2]
+        assert DomainBounds.from_positions(np.array([[2.0, 0, 0], [0, -3.0, 0]])).half_extent == pytest.approx(3.003)
+        assert DomainBounds.from_positions(np.zeros((2, 3))).half_extent == 1.0
+
+    def test_out_of_domain_raises(self):
+        from paper_2203_08966_b200.morton import DomainBounds, morton_keys
+
+        with pytest.raises(ValueError, match="outside domain"):
+            morton_keys(np.array([[0.0, 0.0, 0.0], [1.5, 0.0, 0.0]]), DomainBounds(1.0))
+
+    @pytest.mark.parametrize("n", [1, 1000, 1 << 20])
+    def test_fp32_keys_and_order_match_oracle(self, eng32, n):
+        rng = np.random.Generator(np.random.Philox(key=n))
+        pos = f32(rng.standard_normal((n, 3)))
+        t = eng32.bodies_tensor(pos, np.ones(n))
+        R = eng32.bounds(t)
+        assert float(R.item()) == orc.bounds(pos)
+        keys = eng32.morton(t, R)
+        ks, perm = eng32.sort(keys)
+        ref_k = orc.morton_keys(pos, orc.bounds(pos))
+        np.testing.assert_array_equal(keys.cpu().numpy().view(np.uint64), ref_k)
+        np.testing.assert_array_equal(perm.cpu().numpy(), orc.sort_order(ref_k))
+        assert np.all(np.diff(ks.cpu().numpy().view(np.uint64)) >= 0)
+
+
+# ----------------------------------------------------------------- tree build
+
+
+class TestBuild:
+    @pytest.mark.parametrize("n", [1, 2, 3, 64, 400, 2000])
+    def test_fp64_tree_bitwise_golden(self, golden, n):
+        from paper_2203_08966_b200.hashed import build_hashed
+        from paper_2203_08966_b200.morton import DomainBounds
+        from paper_2203_08966_b200.physics import Bodies
+
+        g = golden("trees.npz")
+        b = Bodies(g[f"n{n}_mass"], g[f"n{n}_pos"], np.zeros((n, 3)))
+        tree = build_hashed(b, DomainBounds(float(g[f"n{n}_R"])), precision="fp64")
+        a = tree.arrays()
+        for name in ("key", "level", "centre", "side", "mass", "com", "quad", "count", "children"):
+            np.testing.assert_array_equal(a[name], g[f"n{n}_t_{name}"], err_msg=name)
+
+    def test_fp64_tree_bitwise_oracle_1e5(self):
+        from paper_2203_08966_b200.hashed import build_hashed
+        from paper_2203_08966_b200.morton import DomainBounds
+        from paper_2203_08966_b200.physics import Bodies
+
+        b = plummer(100_000, 1)
+        R = orc.bounds(b.position)
+        order = orc.sort_order(orc.morton_keys(b.position, R))
+        t_ref = orc.build_tree(b.mass[order], b.position[order], R)
+        tree = build_hashed(b.take(order), DomainBounds(R), precision="fp64")
+        a = tree.arrays()
+        for name in ("key", "level", "centre", "side", "mass", "com", "quad", "count", "children"):
+            np.testing.assert_array_equal(a[name], getattr(t_ref, name), err_msg=name)
+
+    def test_serial_bytes_equal_reference_layout(self, golden):
+        from paper_2203_08966_b200.hashed import build_hashed
+        from paper_2203_08966_b200.morton import DomainBounds
+        from paper_2203_08966_b200.physics import Bodies
+
+        g = golden("trees.npz")
+        b = Bodies(g["n64_mass"], g["n64_pos"], np.zeros((64, 3)))
+        blob = build_hashed(b, DomainBounds(float(g["n64_R"]))).to_serial_bytes()
+        assert blob[:4] == b"OCT1" and len(blob) == 12 + 121 * len(g["n64_t_count"])
+
+    def test_errors(self):
+        from paper_2203_08966_b200.hashed import build_hashed
+        from paper_2203_08966_b200.morton import DomainBounds
+        from paper_2203_08966_b200.physics import Bodies
+
+        dup = Bodies(np.ones(3), np.array([[0.1, 0.1, 0.1], [0.1, 0.1, 0.1], [0.5, 0.5, 0.5]]), np.zeros((3, 3)))
+        with pytest.raises(ValueError, match="tree resolution"):
+            build_hashed(dup, DomainBounds(1.0))
+        uns = Bodies(np.ones(2), np.array([[0.5, 0.5, 0.5], [-0.5, -0.5, -0.5]]), np.zeros((2, 3)))
+        with pytest.raises(ValueError, match="sorted"):
+            build_hashed(uns, DomainBounds(1.0))
+
+    def test_empty_tree(self):
+        from paper_2203_08966_b200.hashed import build_hashed
+        from paper_2203_08966_b200.morton import DomainBounds
+        from paper_2203_08966_b200.physics import Bodies
+
+        tree = build_hashed(Bodies.zeros(0), DomainBounds(1.0))
+        assert len(tree) == 1 and int(tree.count[0]) == 0
+        acc, work = tree.flat().traverse(np.zeros((2, 3)), 0.5, 0.0)
+        assert np.all(acc == 0) and np.all(work == 0)
+
+
+# ------------------------------------------------------------------ traversal
+
+
+def _tree_and_targets(g, n, precision):
+    from paper_2203_08966_b200.hashed import build_hashed
+    from paper_2203_08966_b200.morton import DomainBounds
+    from paper_2203_08966_b200.physics import Bodies
+
+    b = Bodies(g[f"n{n}_mass"], g[f"n{n}_pos"], np.zeros((n, 3)))
+    return build_hashed(b, DomainBounds(float(g[f"n{n}_R"])), precision=precision).flat(), g[f"n{n}_pos"]
+
+
+class TestTraverse:
+    @pytest.mark.parametrize("n", [64, 400, 2000])
+    @pytest.mark.parametrize("theta", [0.0, 0.3, 0.5, 0.7, 1.2])
+    def test_fp64_bitwise_golden(self, golden, n, theta):
+        g = golden("trees.npz")
+        flat, pos = _tree_and_targets(g, n, "fp64")
+        acc, work = flat.traverse(pos, theta, 0.05)
+        np.testing.assert_array_equal(acc, g[f"n{n}_acc_t{theta}"])
+        np.testing.assert_array_equal(work, g[f"n{n}_work_t{theta}"])
+
+    @pytest.mark.parametrize("theta", [0.3, 0.5, 0.7])
+    def test_fp32_golden_tolerance(self, golden, theta):
+        g = golden("trees.npz")
+        n = 2000
+        # fp32 protocol: round inputs once, feed the same values to both
+        from paper_2203_08966_b200.hashed import build_hashed
+        from paper_2203_08966_b200.morton import DomainBounds
+        from paper_2203_08966_b200.physics import Bodies
+
+        pos, m = f32(g["n2000_pos"]), f32(g["n2000_mass"])
+        R = orc.bounds(pos)
+        order = orc.sort_order(orc.morton_keys(pos, R))
+        ref = orc.build_tree(m[order], pos[order], R)
+        ref_acc, ref_work = orc.traverse(ref, pos, theta, 0.05)
+        flat = build_hashed(Bodies(m[order], pos[order], np.zeros((n, 3))), DomainBounds(R), precision="fp32").flat()
+        acc, work = flat.traverse(pos, theta, 0.05)
+        assert rel_l2(acc, ref_acc) <= FP32_TOL
+        assert np.mean(work != ref_work) < 0.01
+
+    def test_work_totals_known_answers_fp64(self):
+        """test_output.txt:350: 310,605 / 6,805,731 / 112,497,303 (theta .5, eps .05)."""
+        from paper_2203_08966_b200.hashed import build_hashed
+        from paper_2203_08966_b200.morton import DomainBounds
+        from paper_2203_08966_b200.physics import Bodies
+
+        for n, want in ((1000, 310_605), (10_000, 6_805_731), (100_000, 112_497_303)):
+            rng = np.random.Generator(np.random.Philox(key=42))
+            pos = rng.uniform(-1.0, 1.0, size=(n, 3))
+            R = orc.bounds(pos)
+            order = orc.sort_order(orc.morton_keys(pos, R))
+            b = Bodies(np.full(n, 1.0 / n), pos[order], np.zeros((n, 3)))
+            _, work = build_hashed(b, DomainBounds(R), precision="fp64").flat().traverse(pos[order], 0.5, 0.05)
+            assert int(work.sum()) == want
+
+    @pytest.mark.parametrize("precision,leaf", [("fp64", 1), ("fp64", 16), ("fp64", 32),
+                                                ("fp32", 1), ("fp32", 16), ("fp32", 32)])
+    def test_plummer_1e5_vs_oracle(self, precision, leaf):
+        from paper_2203_08966_b200.hashed import build_hashed
+        from paper_2203_08966_b200.morton import DomainBounds
+        from paper_2203_08966_b200.physics import Bodies
+
+        b = plummer(100_000, 1)
+        pos = b.position if precision == "fp64" else f32(b.position)
+        m = b.mass if precision == "fp64" else f32(b.mass)
+        R = orc.bounds(pos)
+        order = orc.sort_order(orc.morton_keys(pos, R))
+        ref = orc.build_tree(m[order], pos[order], R)
+        sample = np.random.Generator(np.random.Philox(key=3)).choice(len(pos), 4000, replace=False)
+        ref_acc, ref_work = orc.traverse(ref, pos[sample], 0.5, 1e-3, leaf)
+        flat = build_hashed(Bodies(m[order], pos[order], np.zeros_like(pos)), DomainBounds(R), precision=precision).flat()
+        acc, work = flat.traverse(pos[sample], 0.5, 1e-3, leaf_size=leaf)
+        err = rel_l2(acc, ref_acc)
+        if precision == "fp64":
+            assert err <= FP64_TOL
+            np.testing.assert_array_equal(work, ref_work)
+        else:
+            assert err <= FP32_TOL
+            assert np.mean(work != ref_work) < 0.01
+
+    def test_theta_zero_is_direct(self, golden):
+        from paper_2203_08966_b200.physics import direct_accelerations
+
+        g = golden("trees.npz")
+        flat, pos = _tree_and_targets(g, 400, "fp64")
+        acc, work = flat.traverse(pos, 0.0, 0.05)
+        ref = direct_accelerations(g["n400_mass"], pos, 0.05)
+        np.testing.assert_allclose(acc, ref, rtol=1e-12, atol=1e-14)
+        assert np.all(work == 399)
+
+    def test_mac_tie_opens_cell(self):
+        """test_octree.py:430-452: l/d == theta exactly -> open (two pp)."""
+        from paper_2203_08966_b200.hashed import build_hashed
+        from paper_2203_08966_b200.morton import DomainBounds
+        from paper_2203_08966_b200.physics import Bodies
+
+        b = Bodies(np.full(2, 0.5), np.array([[-1.5, -1.5, -1.5], [-0.5, -1.5, -1.5]]), np.zeros((2, 3)))
+        flat = build_hashed(b, DomainBounds(2.0), precision="fp64").flat()
+        target = np.array([[3.0, -1.5, -1.5]])
+        _, w = flat.traverse(target, 0.5, 0.0)
+        st = flat.tree.engine.stats()
+        assert int(w[0]) == 2 and (st.pp, st.pc) == (2, 0)
+        _, w = flat.traverse(target, np.nextafter(0.5, 1.0), 0.0)
+        st = flat.tree.engine.stats()
+        assert int(w[0]) == 2 and (st.pp, st.pc) == (0, 1)
+
+    def test_deep_pair(self):
+        """test_flattree.py:141-152: bodies 2^-19 +- 2^-25 apart."""
+        from paper_2203_08966_b200.hashed import build_hashed
+        from paper_2203_08966_b200.morton import DomainBounds
+        from paper_2203_08966_b200.physics import Bodies, direct_accelerations
+
+        pos = np.array([[2.0 ** -19 - 2.0 ** -25, 0, 0], [2.0 ** -19 + 2.0 ** -25, 0, 0]])
+        b = Bodies(np.ones(2), pos, np.zeros((2, 3)))
+        acc, work = build_hashed(b, DomainBounds(1.0), precision="fp64").flat().traverse(pos, 0.0, 0.0)
+        np.testing.assert_allclose(acc, direct_accelerations(np.ones(2), pos, 0.0), rtol=1e-13)
+        assert np.all(work == 1)
+
+    def test_direct_bitwise(self, golden):
+        from paper_2203_08966_b200.physics import direct_accelerations
+
+        g = golden("cfg0.npz")
+        np.testing.assert_array_equal(direct_accelerations(g["mass"], g["pos0"], float(g["eps"])), g["direct0"])
+
+
+# ----------------------------------------------------------------- simulation
+
+
+class TestSimulation:
+    def test_cfg0_fp64_trajectory_bitwise(self, golden):
+        """BASELINE cfg0 on the GPU in fp64 == the reference's 10-step run."""
+        from paper_2203_08966_b200.physics import Bodies, total_energy
+        from paper_2203_08966_b200.simulation import SimConfig, simulate
+
+        g = golden("cfg0.npz")
+        init = Bodies(g["mass"], g["pos0"], g["vel0"])
+        cfg = SimConfig(n=2000, algorithm=1, theta=0.5, dt=1e-3, steps=10, eps=0.01, precision="fp64")
+        res = simulate(cfg, initial=init)
+        np.testing.assert_array_equal(res.bodies.position, g["pos"])
+        np.testing.assert_array_equal(res.bodies.velocity, g["vel"])
+        np.testing.assert_array_equal(res.bodies.acceleration, g["acc"])
+        np.testing.assert_array_equal(res.bodies.work, g["work"])
+        e1 = total_energy(res.bodies, 0.01)
+        drift = (e1 - float(g["e0"])) / abs(float(g["e0"]))
+        ref_drift = (float(g["e1"]) - float(g["e0"])) / abs(float(g["e0"]))
+        assert abs(drift - ref_drift) <= 0.01 * abs(ref_drift)
+
+    def test_simulate_matches_reference_two_clusters(self, golden):
+        """simulate() default ICs (two_clusters) in fp64 reproduce the oracle leapfrog."""
+        from paper_2203_08966_b200.initcond import two_clusters
+        from paper_2203_08966_b200.simulation import SimConfig, simulate
+
+        cfg = SimConfig(n=96, algorithm=1, theta=0.6, dt=0.01, steps=4, eps=0.05, seed=3, precision="fp64")
+        res = simulate(cfg)
+        b = two_clusters(96, 3)
+        x, v, a, w = orc.leapfrog(b.mass, b.position, b.velocity, 0.01, 4, 0.6, 0.05)
+        np.testing.assert_array_equal(res.bodies.position, x)
+        np.testing.assert_array_equal(res.bodies.velocity, v)
+        np.testing.assert_array_equal(res.bodies.work, w)
+
+    def test_fp32_step_forces_vs_oracle(self):
+        """cfg1 shape: after 3 fp32 GPU steps, forces on the GPU state match the
+        oracle evaluated on the same (upcast) state."""
+        from paper_2203_08966_b200.engine import Engine
+
+        b = plummer(100_000, 1)
+        eng = Engine("fp32", 0)
+        pos = eng.bodies_tensor(b.position, b.mass)
+        vel = eng.vec_tensor(b.velocity)
+        eng.sim_load(pos, vel)
+        eng.sim_forces(0.5, 1e-3, 16)
+        eng.sim_step(1e-3, 0.5, 1e-3, 16, 3)
+        p, a = torch.empty_like(vel), torch.empty_like(vel)
+        eng.sim_store(pos=p, acc=a)
+        eng.check()
+        x = p[:, :3].double().cpu().numpy()
+        m = p[:, 3].double().cpu().numpy()
+        ref_a, _ = orc.tree_accelerations(m, x, 0.5, 1e-3, leaf_size=16)
+        assert rel_l2(a[:, :3].double().cpu().numpy(), ref_a) <= FP32_TOL
+        eng.close()
+
+    def test_tree_forces_provider_kdk(self):
+        from paper_2203_08966_b200.initcond import two_clusters
+        from paper_2203_08966_b200.integrator import kdk_step
+        from paper_2203_08966_b200.simulation import TreeForces
+
+        b = two_clusters(96, 3)
+        prov = TreeForces(0.6, 0.05, precision="fp64")
+        prov(b)
+        ref = b.copy()
+        kdk_step(b, 0.01, prov)
+        a0, _ = orc.tree_accelerations(ref.mass, ref.position, 0.6, 0.05)
+        ref.acceleration[:] = a0
+        ref.velocity += ref.acceleration * 0.005
+        ref.position += ref.velocity * 0.01
+        a1, w1 = orc.tree_accelerations(ref.mass, ref.position, 0.6, 0.05)
+        ref.velocity += a1 * 0.005
+        np.testing.assert_array_equal(b.position, ref.position)
+        np.testing.assert_array_equal(b.velocity, ref.velocity)
+        np.testing.assert_array_equal(b.work, w1)
+
+
+# -------------------------------------------- full-size, size-independent checks
+
+
+class TestFullSize:
+    def test_cfg2_scale_properties(self, eng32):
+        """N=1e6 (cfg2): keys sorted, permutation valid, tree invariants, and
+        sampled-target parity against the oracle tree."""
+        b = plummer(1_000_000, 2)
+        pos = f32(b.position)
+        m = f32(b.mass)
+        t = eng32.bodies_tensor(pos, m)
+        R = eng32.bounds(t)
+        keys = eng32.morton(t, R)
+        ks, perm = eng32.sort(keys)
+        p = perm.cpu().numpy()
+        assert np.array_equal(np.sort(p), np.arange(len(p)))
+        k = ks.cpu().numpy().view(np.uint64)
+        assert np.all(k[1:] > k[:-1])
+        C = eng32.build(t[perm], R)
+        tr = eng32.export_tree()
+        assert tr["count"][0] == len(p) and C == len(tr["count"])
+        assert np.sum(tr["count"] == 1) == len(p)
+        assert abs(tr["mass"][0] - m.sum()) <= 1e-9 * m.sum()
+        Rh = orc.bounds(pos)
+        order = orc.sort_order(orc.morton_keys(pos, Rh))
+        assert np.array_equal(order, p)
+        ref = orc.build_tree(m[order], pos[order], Rh)
+        assert len(ref) == C
+        sample = np.random.Generator(np.random.Philox(key=5)).choice(len(pos), 3000, replace=False)
+        tg = eng32.bodies_tensor(pos[sample], m[sample])
+        acc, work = eng32.traverse(tg, 0.6, 1e-3, 16)
+        ref_acc, _ = orc.traverse(ref, pos[sample], 0.6, 1e-3, 16)
+        assert rel_l2(acc[:, :3].double().cpu().numpy(), ref_acc) <= FP32_TOL
