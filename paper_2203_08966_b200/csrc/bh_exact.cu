@@ -593,8 +593,8 @@ void launch_maxabs_f64(const double *pos3, int64_t n, DeviceFlags *f, cudaStream
 
 // morton.py:41-42: R = 1.001 * extreme, or 1.0 for an all-zero cloud
 __global__ void k_finish_R(const DeviceFlags *f, int fp64, double *d_R) {
-  double extreme = fp64 ? __longlong_as_double((long long)f->maxabs64)
-                        : (double)__uint_as_float(f->maxabs_bits);
+  // maxabs64 holds the bits of a non-negative double (atomicMax on its bits)
+  double extreme = fp64 ? f->maxabs64 : (double)__uint_as_float(f->maxabs_bits);
   *d_R = extreme > 0.0 ? 1.001 * extreme : 1.0;
 }
 void launch_finish_R(const DeviceFlags *f, int fp64, double *d_R, cudaStream_t s) {
