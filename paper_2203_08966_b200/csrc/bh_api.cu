@@ -63,7 +63,13 @@ struct bh_handle {
   // tree
   int64_t tree_n = -1, C = 0, max_level = 0;
   double R = 1.0;
-  Buf link, parent, nchild, arrive, cm64, q64, ncm, nq0, nq1, tbod;
+  Buf link, parent, nchild, arrive, cm64, q64, tbod;
+  // fp32 walk tree (compacted per (theta, leaf size))
+  Buf keep, widx, wnodes, wscan_tmp;
+  int *dCp = nullptr;
+  double walk_theta = -1.0;
+  int walk_leaf = -1;
+  bool walk_valid = false;
   // resident simulation state (Morton order)
   int64_t sim_n = 0;
   Buf pos, pos2, vel, vel2, acc, id, id2, work_sorted, work_orig;
@@ -122,11 +128,6 @@ struct bh_handle {
     t.arrive = arrive.as<int>();
     t.cm64 = cm64.as<double4>();
     t.q64 = q64.as<double>();
-    if (precision == BH_FP32) {
-      t.ncm = ncm.as<float4>();
-      t.nq0 = nq0.as<float4>();
-      t.nq1 = nq1.as<float2>();
-    }
     return t;
   }
 };
@@ -186,7 +187,6 @@ int sort_keys(bh_handle *h, int64_t n, cudaStream_t s) {
 // (hashed.py:448-515).  Exactly one of bod32 / bod64 is non-null.
 int build_sorted(bh_handle *h, int64_t n, const float4 *bod32, const double4 *bod64,
                  cudaStream_t s) {
-  const bool f32 = h->precision == BH_FP32;
   BH_CUDA(h->lcp.ensure(n + 16));
   BH_CUDA(h->newc.ensure(sizeof(uint32_t) * (n + 1)));
   BH_CUDA(h->off.ensure(sizeof(uint32_t) * (n + 1)));
@@ -215,11 +215,7 @@ int build_sorted(bh_handle *h, int64_t n, const float4 *bod32, const double4 *bo
   BH_CUDA(h->arrive.ensure(sizeof(int) * C));
   BH_CUDA(h->cm64.ensure(sizeof(double4) * C));
   BH_CUDA(h->q64.ensure(sizeof(double) * 6 * C));
-  if (f32) {
-    BH_CUDA(h->ncm.ensure(sizeof(float4) * C));
-    BH_CUDA(h->nq0.ensure(sizeof(float4) * C));
-    BH_CUDA(h->nq1.ensure(sizeof(float2) * C));
-  }
+  h->walk_valid = false;
   BH_CUDA(cudaMemsetAsync(h->nchild.p, 0, sizeof(int) * C, s));
   BH_CUDA(cudaMemsetAsync(h->arrive.p, 0, sizeof(int) * C, s));
   if (n == 0) {  // hashed.py:459-462: an empty root
@@ -227,7 +223,6 @@ int build_sorted(bh_handle *h, int64_t n, const float4 *bod32, const double4 *bo
     BH_CUDA(cudaMemcpyAsync(h->link.p, &root, sizeof(int4), cudaMemcpyHostToDevice, s));
     BH_CUDA(cudaMemsetAsync(h->cm64.p, 0, sizeof(double4), s));
     BH_CUDA(cudaMemsetAsync(h->q64.p, 0, sizeof(double) * 6, s));
-    if (f32) BH_CUDA(cudaMemsetAsync(h->ncm.p, 0, sizeof(float4), s));
     int m1 = -1;
     BH_CUDA(cudaMemcpyAsync(h->parent.p, &m1, sizeof(int), cudaMemcpyHostToDevice, s));
     BH_CUDA(cudaStreamSynchronize(s));
@@ -255,6 +250,34 @@ void fill_walk_params(bh_handle *h, WalkParams &P, int64_t nt, double theta, dou
     double r = side / theta;  // theta == 0 -> inf: never accept
     P.mac2f[l] = (float)(r * r);
   }
+}
+
+// (Re)build the compact fp32 walk tree for (theta, leaf) -- bh_walk.cu
+int ensure_walk_tree(bh_handle *h, double theta, int leaf, cudaStream_t s) {
+  if (leaf < 1) leaf = 1;
+  if (h->walk_valid && h->walk_theta == theta && h->walk_leaf == leaf) return BH_OK;
+  const int64_t C = h->C;
+  BH_CUDA(h->keep.ensure(sizeof(uint32_t) * C));
+  BH_CUDA(h->widx.ensure(sizeof(uint32_t) * C));
+  BH_CUDA(h->wnodes.ensure(sizeof(WalkNode) * C));
+  BH_CUDA(h->wscan_tmp.ensure(scan_temp_bytes(C) + 16));
+  TreeView t = h->view();
+  WalkTable tab;
+  for (int l = 0; l <= kMaxLevel; ++l) {
+    double r = std::ldexp(2.0 * h->R, -l) / theta;  // theta == 0 -> inf: never accept
+    tab.mac2[l] = (float)(r * r);
+  }
+  launch_keep(t, leaf, h->keep.as<uint32_t>(), s);
+  BH_CUDA(exclusive_scan_u32(h->wscan_tmp.p, h->wscan_tmp.bytes, h->keep.as<uint32_t>(),
+                             h->widx.as<uint32_t>(), C, s));
+  launch_compact(t, tab, leaf, h->keep.as<uint32_t>(), h->widx.as<uint32_t>(),
+                 h->wnodes.as<WalkNode>(), h->dCp, s);
+  h->launches += 2;
+  BH_LAUNCHED();
+  h->walk_valid = true;
+  h->walk_theta = theta;
+  h->walk_leaf = leaf;
+  return BH_OK;
 }
 
 int reset_counters(bh_handle *h, cudaStream_t s) {
@@ -344,11 +367,12 @@ int sim_forces_impl(bh_handle *h, double theta, double eps, int leaf, int record
   WalkParams P;
   fill_walk_params(h, P, n, theta, eps, leaf);
   int *w32 = record_work ? h->work_sorted.as<int>() : nullptr;
-  if (f32)
-    launch_walk_f32(P, h->ncm.as<float4>(), h->nq0.as<float4>(), h->nq1.as<float2>(),
-                    h->link.as<int4>(), h->pos.as<float4>(), h->pos.as<float>(), 4, nullptr,
-                    h->acc.as<float>(), 4, nullptr, w32, h->flags, s);
-  else
+  if (f32) {
+    BH_TRY(ensure_walk_tree(h, theta, leaf, s));
+    launch_walk2_f32(h->wnodes.as<WalkNode>(), h->dCp, h->pos.as<float4>(), h->pos.as<float>(), 4,
+                     nullptr, (int)n, (float)(eps * eps), leaf, h->acc.as<float>(), 4, nullptr,
+                     w32, h->flags, s);
+  } else
     launch_walk_f64(P, h->cm64.as<double4>(), h->q64.as<double>(), h->link.as<int4>(),
                     h->pos.as<double4>(), h->pos.as<double>(), 4, nullptr, h->acc.as<double>(), 4,
                     nullptr, w32, h->flags, s);
@@ -382,6 +406,7 @@ int bh_create(bh_handle **out, int device, int precision) {
   BH_CUDA(cudaMallocHost(&h->hflags, sizeof(DeviceFlags)));
   BH_CUDA(cudaMallocHost(&h->hC, 4 * sizeof(uint32_t)));
   BH_CUDA(cudaMalloc(&h->dR, sizeof(double)));
+  BH_CUDA(cudaMalloc(&h->dCp, sizeof(int)));
   BH_CUDA(cudaMallocHost(&h->hR, sizeof(double)));
   DeviceFlags init;
   memset(&init, 0, sizeof(init));
@@ -397,13 +422,14 @@ int bh_destroy(bh_handle *h) {
   cudaSetDevice(h->device);
   Buf *bufs[] = {&h->keys, &h->keys2, &h->vals, &h->vals2, &h->sort_tmp, &h->scan_tmp,
                  &h->lcp, &h->newc, &h->off, &h->link, &h->parent, &h->nchild, &h->arrive,
-                 &h->cm64, &h->q64, &h->ncm, &h->nq0, &h->nq1, &h->tbod, &h->pos, &h->pos2,
+                 &h->cm64, &h->q64, &h->keep, &h->widx, &h->wnodes, &h->wscan_tmp, &h->tbod, &h->pos, &h->pos2,
                  &h->vel, &h->vel2, &h->acc, &h->id, &h->id2, &h->work_sorted, &h->work_orig};
   for (Buf *b : bufs) b->release();
   cudaFree(h->flags);
   cudaFreeHost(h->hflags);
   cudaFreeHost(h->hC);
   cudaFree(h->dR);
+  cudaFree(h->dCp);
   cudaFreeHost(h->hR);
   h->fold_marks();
   for (cudaEvent_t e : h->pool) cudaEventDestroy(e);
@@ -547,12 +573,13 @@ static int traverse_common(bh_handle *h, const void *targets, int64_t n, double 
                      h->vals2.as<uint32_t>(), n, s));
   WalkParams P;
   fill_walk_params(h, P, n, theta, eps, leaf);
-  if (f32)
-    launch_walk_f32(P, h->ncm.as<float4>(), h->nq0.as<float4>(), h->nq1.as<float2>(),
-                    h->link.as<int4>(), h->tbod.as<float4>(), static_cast<const float *>(targets),
-                    4, h->vals2.as<uint32_t>(), static_cast<float *>(acc), 4, work, nullptr,
-                    h->flags, s);
-  else
+  if (f32) {
+    BH_TRY(ensure_walk_tree(h, theta, leaf, s));
+    launch_walk2_f32(h->wnodes.as<WalkNode>(), h->dCp, h->tbod.as<float4>(),
+                     static_cast<const float *>(targets), 4, h->vals2.as<uint32_t>(), (int)n,
+                     (float)(eps * eps), leaf, static_cast<float *>(acc), 4, work, nullptr,
+                     h->flags, s);
+  } else
     launch_walk_f64(P, h->cm64.as<double4>(), h->q64.as<double>(), h->link.as<int4>(),
                     h->tbod.as<double4>(), static_cast<const double *>(targets), 3,
                     h->vals2.as<uint32_t>(), static_cast<double *>(acc), 3, work, nullptr,

@@ -123,9 +123,6 @@ __device__ __forceinline__ double4 ldcg4(const double4 *p) {
   double2 a = __ldcg(q), b = __ldcg(q + 1);
   return make_double4(a.x, a.y, b.x, b.y);
 }
-__device__ __forceinline__ float4 v4f(double4 b) {
-  return make_float4((float)b.x, (float)b.y, (float)b.z, (float)b.w);
-}
 
 // hashed.py:376-388 _lcp_levels: 21 - ceil(bitlen(a ^ b) / 3)
 __device__ __forceinline__ int lcp_of(uint64_t a, uint64_t b) {
@@ -218,7 +215,6 @@ __global__ void k_emit(TreeView t, const float4 *__restrict__ bod32,
         b = make_double4(v.x, v.y, v.z, v.w);
       }
       t.cm64[0] = b;
-      if (t.ncm) t.ncm[0] = v4f(b);
       return;
     }
   }
@@ -249,7 +245,6 @@ __global__ void k_emit(TreeView t, const float4 *__restrict__ bod32,
         b = make_double4(v.x, v.y, v.z, v.w);
       }
       t.cm64[c] = b;
-      if (t.ncm) t.ncm[c] = make_float4((float)b.x, (float)b.y, (float)b.z, (float)b.w);
     } else {
       const int shift = 3 * (kMortonBits - l);
       const int64_t end = run_end(t.keys, n, i, k >> shift, shift);
@@ -286,11 +281,6 @@ __device__ void cell_moments(const TreeView &t, int p) {
   if (total == 0.0) {
     t.cm64[p] = make_double4(0.0, 0.0, 0.0, 0.0);
     for (int k = 0; k < 6; ++k) qo[k] = 0.0;
-    if (t.ncm) {
-      t.ncm[p] = make_float4(0.f, 0.f, 0.f, 0.f);
-      t.nq0[p] = make_float4(0.f, 0.f, 0.f, 0.f);
-      t.nq1[p] = make_float2(0.f, 0.f);
-    }
     return;
   }
   cx /= total;
@@ -323,11 +313,6 @@ __device__ void cell_moments(const TreeView &t, int p) {
   q2o[0] = make_double2(qxx, qxy);
   q2o[1] = make_double2(qxz, qyy);
   q2o[2] = make_double2(qyz, qzz);
-  if (t.ncm) {
-    t.ncm[p] = make_float4((float)cx, (float)cy, (float)cz, (float)total);
-    t.nq0[p] = make_float4((float)qxx, (float)qxy, (float)qxz, (float)qyy);
-    t.nq1[p] = make_float2((float)qyz, (float)qzz);
-  }
 }
 
 // Bottom-up moments in one launch: every body climbs from its leaf; the last

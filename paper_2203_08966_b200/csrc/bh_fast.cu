@@ -143,116 +143,6 @@ void launch_iota64(int64_t *out, const uint32_t *vals, int64_t n, cudaStream_t s
   k_iota64<<<grid_for(n, 256), 256, 0, s>>>(out, vals, n);
 }
 
-// -------------------------------------------------------------- fp32 walk
-// flattree.py:258-317 in fp32: the same warp-cooperative pre-order union walk
-// as k_walk_f64 (each lane follows its own reference DFS; the warp visits the
-// minimum next cell), with rsqrt on the FP32 pipe and the MAC
-// `side < theta*sqrt(d2)` evaluated as d2 > (side/theta)^2 from a per-level
-// table.  Node data is loaded once per warp (uniform address -> broadcast).
-template <bool BUCKET>
-__global__ void __launch_bounds__(256) k_walk_f32(
-    WalkParams P, const float4 *__restrict__ ncm, const float4 *__restrict__ nq0,
-    const float2 *__restrict__ nq1, const int4 *__restrict__ link,
-    const float4 *__restrict__ bodies, const float *__restrict__ targets, int tstride,
-    const uint32_t *__restrict__ tperm, float *__restrict__ acc, int astride,
-    int64_t *__restrict__ work64, int *__restrict__ work32, DeviceFlags *f) {
-  __shared__ float s_mac[kMaxLevel + 1];
-  if (threadIdx.x <= kMaxLevel) s_mac[threadIdx.x] = P.mac2f[threadIdx.x];
-  __syncthreads();
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool valid = t < P.nt;
-  const int64_t src = valid ? (tperm ? (int64_t)tperm[t] : t) : 0;
-  float px = 0.f, py = 0.f, pz = 0.f;
-  if (valid) {
-    const float *q = targets + src * tstride;
-    px = q[0]; py = q[1]; pz = q[2];
-  }
-  const float e2 = P.e2f;
-  float ax = 0.f, ay = 0.f, az = 0.f;
-  int npp = 0, npc = 0;
-  int next = valid ? (P.C == 1 ? 0 : 1) : INT_MAX;
-  while (true) {
-    const int i = __reduce_min_sync(0xffffffffu, next);
-    if (i >= P.C) break;
-    if (next != i) continue;
-    const float4 c = ncm[i];
-    const int4 L = link[i];
-    const float dx = px - c.x, dy = py - c.y, dz = pz - c.z;
-    const float d2 = dx * dx + dy * dy + dz * dz;
-    if (L.y == 1) {
-      if (d2 > 0.f) {
-        const float r = rsqrtf(d2 + e2);
-        const float s = c.w * r * r * r;
-        ax -= s * dx; ay -= s * dy; az -= s * dz;
-        ++npp;
-      }
-      next = i + 1;
-    } else if (d2 > s_mac[L.w]) {
-      const float4 qa = nq0[i];
-      const float2 qb = nq1[i];
-      const float r = rsqrtf(d2);
-      const float r2 = r * r;
-      const float qrx = qa.x * dx + qa.y * dy + qa.z * dz;
-      const float qry = qa.y * dx + qa.w * dy + qb.x * dz;
-      const float qrz = qa.z * dx + qb.x * dy + qb.y * dz;
-      const float rqr = dx * qrx + dy * qry + dz * qrz;
-      const float r3 = r * r2;
-      const float r5 = r3 * r2;
-      // a = -M d/r^3 + Q.d/r^5 - 2.5 (d.Q.d) d / r^7   (physics.py:195-213)
-      const float sd = -c.w * r3 - 2.5f * rqr * r5 * r2;
-      ax += sd * dx + qrx * r5;
-      ay += sd * dy + qry * r5;
-      az += sd * dz + qrz * r5;
-      ++npc;
-      next = L.x;
-    } else if (BUCKET && L.y <= P.leaf) {
-      for (int j = L.z; j < L.z + L.y; ++j) {
-        const float4 b = bodies[j];
-        const float ex = px - b.x, ey = py - b.y, ez = pz - b.z;
-        const float r2 = ex * ex + ey * ey + ez * ez;
-        if (r2 > 0.f) {
-          const float r = rsqrtf(r2 + e2);
-          const float s = b.w * r * r * r;
-          ax -= s * ex; ay -= s * ey; az -= s * ez;
-          ++npp;
-        }
-      }
-      next = L.x;
-    } else {
-      next = i + 1;
-    }
-  }
-  if (valid) {
-    float *o = acc + src * astride;
-    o[0] = ax; o[1] = ay; o[2] = az;
-    const int w = npp * 1 + npc * 2;  // WORK_PP, WORK_PC (octree.py:23-25)
-    if (work64) work64[src] = w;
-    if (work32) work32[src] = w;
-  }
-  unsigned spp = __reduce_add_sync(0xffffffffu, (unsigned)npp);
-  unsigned spc = __reduce_add_sync(0xffffffffu, (unsigned)npc);
-  if ((threadIdx.x & 31) == 0) {
-    atomicAdd(&f->pp, (unsigned long long)spp);
-    atomicAdd(&f->pc, (unsigned long long)spc);
-  }
-}
-
-void launch_walk_f32(const WalkParams &p, const float4 *ncm, const float4 *nq0,
-                     const float2 *nq1, const int4 *link, const float4 *bodies,
-                     const float *targets, int tstride, const uint32_t *tperm, float *acc,
-                     int astride, int64_t *work64, int *work32, DeviceFlags *f,
-                     cudaStream_t s) {
-  if (p.nt <= 0) return;
-  if (p.leaf > 1)
-    k_walk_f32<true><<<grid_for(p.nt, 256), 256, 0, s>>>(p, ncm, nq0, nq1, link, bodies, targets,
-                                                         tstride, tperm, acc, astride, work64,
-                                                         work32, f);
-  else
-    k_walk_f32<false><<<grid_for(p.nt, 256), 256, 0, s>>>(p, ncm, nq0, nq1, link, bodies,
-                                                          targets, tstride, tperm, acc, astride,
-                                                          work64, work32, f);
-}
-
 // --------------------------------------------------- FFMA peak microbench
 // 8 independent FFMA chains per thread, 8 warps x 4 blocks per SM: the FP32
 // pipe's sustained issue rate at the current clock (walk roofline denominator)

@@ -11,8 +11,8 @@
 //                    (pre-order), count = bodies below, lo = first sorted body
 //   parent  i32[C], nchild i32[C], arrive i32[C]  (bottom-up moments)
 //   cm64    double4[C] {com, mass}, q64 double[C][6]           fp64 moments
-//   ncm     float4[C] {com, mass}, nq0 float4 {xx,xy,xz,yy}, nq1 float2 {yz,zz}
-//                    fp32 walk nodes (fp32 mode)
+//   wnodes  WalkNode[C'] 64-byte fp32 walk records of the cells a walk with
+//                    leaf size L can reach (bh_walk.cu)
 //
 // The pre-order layout makes the reference's depth-first walk stackless: the
 // first child of c is c+1, and "do not descend" is "jump to skip[c]".
@@ -109,9 +109,6 @@ struct TreeView {
   int *arrive = nullptr;
   double4 *cm64 = nullptr;
   double *q64 = nullptr;   // [C][6]
-  float4 *ncm = nullptr;   // fp32 nodes (may be null in fp64 mode)
-  float4 *nq0 = nullptr;
-  float2 *nq1 = nullptr;
 };
 void launch_emit(const TreeView &t, const float4 *bod32, const double4 *bod64, cudaStream_t s);
 void launch_moments(const TreeView &t, cudaStream_t s);
@@ -130,11 +127,24 @@ struct WalkParams {
   float mac2f[kMaxLevel + 1];   // fp32: (side_l/theta)^2, +inf for theta == 0
   double side64[kMaxLevel + 1]; // fp64: exact side of level l
 };
-void launch_walk_f32(const WalkParams &p, const float4 *ncm, const float4 *nq0,
-                     const float2 *nq1, const int4 *link, const float4 *bodies,
-                     const float *targets, int tstride, const uint32_t *tperm,
-                     float *acc, int astride, int64_t *work64, int *work32,
-                     DeviceFlags *f, cudaStream_t s);
+// fp32 walk tree (bh_walk.cu): compact pre-order records of the cells the
+// walk can reach for a given leaf size, MAC threshold baked per level
+struct __align__(16) WalkNode {
+  float4 a;  // com.x, com.y, com.z, mac2 = (side/theta)^2
+  float4 b;  // qxx, qxy, qxy, qyy
+  float4 c;  // qxz, qyz, mass, qzz
+  int4 d;    // skip (index after subtree), count, lo (first sorted body), level
+};
+struct WalkTable {
+  float mac2[kMaxLevel + 1];
+};
+void launch_keep(const TreeView &t, int leaf, uint32_t *keep, cudaStream_t s);
+void launch_compact(const TreeView &t, const WalkTable &tab, int leaf, const uint32_t *keep,
+                    const uint32_t *widx, WalkNode *out, int *dCp, cudaStream_t s);
+void launch_walk2_f32(const WalkNode *T, const int *dCp, const float4 *bodies,
+                      const float *targets, int tstride, const uint32_t *tperm, int nt, float e2,
+                      int leaf, float *acc, int astride, int64_t *work64, int *work32,
+                      DeviceFlags *f, cudaStream_t s);
 void launch_walk_f64(const WalkParams &p, const double4 *cm64, const double *q64,
                      const int4 *link, const double4 *bodies, const double *targets,
                      int tstride, const uint32_t *tperm, double *acc, int astride,
