@@ -65,7 +65,7 @@ struct bh_handle {
   double R = 1.0;
   Buf link, parent, nchild, arrive, cm64, q64, tbod;
   // fp32 walk tree (compacted per (theta, leaf size))
-  Buf keep, widx, wnodes, wscan_tmp;
+  Buf smask, nck, wbase, wnodes, wscan_tmp;
   int *dCp = nullptr;
   double walk_theta = -1.0;
   int walk_leaf = -1;
@@ -257,8 +257,9 @@ int ensure_walk_tree(bh_handle *h, double theta, int leaf, cudaStream_t s) {
   if (leaf < 1) leaf = 1;
   if (h->walk_valid && h->walk_theta == theta && h->walk_leaf == leaf) return BH_OK;
   const int64_t C = h->C;
-  BH_CUDA(h->keep.ensure(sizeof(uint32_t) * C));
-  BH_CUDA(h->widx.ensure(sizeof(uint32_t) * C));
+  BH_CUDA(h->smask.ensure(sizeof(uint32_t) * C));
+  BH_CUDA(h->nck.ensure(sizeof(uint32_t) * C));
+  BH_CUDA(h->wbase.ensure(sizeof(uint32_t) * C));
   BH_CUDA(h->wnodes.ensure(sizeof(WalkNode) * C));
   BH_CUDA(h->wscan_tmp.ensure(scan_temp_bytes(C) + 16));
   TreeView t = h->view();
@@ -267,12 +268,10 @@ int ensure_walk_tree(bh_handle *h, double theta, int leaf, cudaStream_t s) {
     double r = std::ldexp(2.0 * h->R, -l) / theta;  // theta == 0 -> inf: never accept
     tab.mac2[l] = (float)(r * r);
   }
-  launch_keep(t, leaf, h->keep.as<uint32_t>(), s);
-  BH_CUDA(exclusive_scan_u32(h->wscan_tmp.p, h->wscan_tmp.bytes, h->keep.as<uint32_t>(),
-                             h->widx.as<uint32_t>(), C, s));
-  launch_compact(t, tab, leaf, h->keep.as<uint32_t>(), h->widx.as<uint32_t>(),
-                 h->wnodes.as<WalkNode>(), h->dCp, s);
-  h->launches += 2;
+  launch_walk_tree(t, tab, leaf, h->smask.as<uint32_t>(), h->nck.as<uint32_t>(),
+                   h->wbase.as<uint32_t>(), h->wscan_tmp.p, h->wscan_tmp.bytes,
+                   h->wnodes.as<WalkNode>(), h->dCp, s);
+  h->launches += 3;
   BH_LAUNCHED();
   h->walk_valid = true;
   h->walk_theta = theta;
@@ -369,9 +368,9 @@ int sim_forces_impl(bh_handle *h, double theta, double eps, int leaf, int record
   int *w32 = record_work ? h->work_sorted.as<int>() : nullptr;
   if (f32) {
     BH_TRY(ensure_walk_tree(h, theta, leaf, s));
-    launch_walk2_f32(h->wnodes.as<WalkNode>(), h->dCp, h->pos.as<float4>(), h->pos.as<float>(), 4,
-                     nullptr, (int)n, (float)(eps * eps), leaf, h->acc.as<float>(), 4, nullptr,
-                     w32, h->flags, s);
+    launch_walk_f32(h->wnodes.as<WalkNode>(), h->pos.as<float4>(), h->pos.as<float>(), 4, nullptr,
+                    (int)n, (float)(eps * eps), leaf, h->acc.as<float>(), 4, nullptr, w32,
+                    h->flags, s);
   } else
     launch_walk_f64(P, h->cm64.as<double4>(), h->q64.as<double>(), h->link.as<int4>(),
                     h->pos.as<double4>(), h->pos.as<double>(), 4, nullptr, h->acc.as<double>(), 4,
@@ -422,7 +421,7 @@ int bh_destroy(bh_handle *h) {
   cudaSetDevice(h->device);
   Buf *bufs[] = {&h->keys, &h->keys2, &h->vals, &h->vals2, &h->sort_tmp, &h->scan_tmp,
                  &h->lcp, &h->newc, &h->off, &h->link, &h->parent, &h->nchild, &h->arrive,
-                 &h->cm64, &h->q64, &h->keep, &h->widx, &h->wnodes, &h->wscan_tmp, &h->tbod, &h->pos, &h->pos2,
+                 &h->cm64, &h->q64, &h->smask, &h->nck, &h->wbase, &h->wnodes, &h->wscan_tmp, &h->tbod, &h->pos, &h->pos2,
                  &h->vel, &h->vel2, &h->acc, &h->id, &h->id2, &h->work_sorted, &h->work_orig};
   for (Buf *b : bufs) b->release();
   cudaFree(h->flags);
@@ -575,10 +574,10 @@ static int traverse_common(bh_handle *h, const void *targets, int64_t n, double 
   fill_walk_params(h, P, n, theta, eps, leaf);
   if (f32) {
     BH_TRY(ensure_walk_tree(h, theta, leaf, s));
-    launch_walk2_f32(h->wnodes.as<WalkNode>(), h->dCp, h->tbod.as<float4>(),
-                     static_cast<const float *>(targets), 4, h->vals2.as<uint32_t>(), (int)n,
-                     (float)(eps * eps), leaf, static_cast<float *>(acc), 4, work, nullptr,
-                     h->flags, s);
+    launch_walk_f32(h->wnodes.as<WalkNode>(), h->tbod.as<float4>(),
+                    static_cast<const float *>(targets), 4, h->vals2.as<uint32_t>(), (int)n,
+                    (float)(eps * eps), leaf, static_cast<float *>(acc), 4, work, nullptr,
+                    h->flags, s);
   } else
     launch_walk_f64(P, h->cm64.as<double4>(), h->q64.as<double>(), h->link.as<int4>(),
                     h->tbod.as<double4>(), static_cast<const double *>(targets), 3,

@@ -12,7 +12,7 @@
 //   parent  i32[C], nchild i32[C], arrive i32[C]  (bottom-up moments)
 //   cm64    double4[C] {com, mass}, q64 double[C][6]           fp64 moments
 //   wnodes  WalkNode[C'] 64-byte fp32 walk records of the cells a walk with
-//                    leaf size L can reach (bh_walk.cu)
+//                    leaf size L can reach, children contiguous (bh_walk.cu)
 //
 // The pre-order layout makes the reference's depth-first walk stackless: the
 // first child of c is c+1, and "do not descend" is "jump to skip[c]".
@@ -127,24 +127,23 @@ struct WalkParams {
   float mac2f[kMaxLevel + 1];   // fp32: (side_l/theta)^2, +inf for theta == 0
   double side64[kMaxLevel + 1]; // fp64: exact side of level l
 };
-// fp32 walk tree (bh_walk.cu): compact pre-order records of the cells the
-// walk can reach for a given leaf size, MAC threshold baked per level
+// fp32 walk tree (bh_walk.cu): 64-byte records of the cells a walk with leaf
+// size L can reach, each cell's children contiguous, MAC threshold baked in
 struct __align__(16) WalkNode {
-  float4 a;  // com.x, com.y, com.z, mac2 = (side/theta)^2
+  float4 a;  // -com.x, -com.y, -com.z, mac2 = (side/theta)^2
   float4 b;  // qxx, qxy, qxy, qyy
   float4 c;  // qxz, qyz, mass, qzz
-  int4 d;    // skip (index after subtree), count, lo (first sorted body), level
+  int4 d;    // first_child (internal) | lo (bucket/leaf), count, nchild, level
 };
 struct WalkTable {
   float mac2[kMaxLevel + 1];
 };
-void launch_keep(const TreeView &t, int leaf, uint32_t *keep, cudaStream_t s);
-void launch_compact(const TreeView &t, const WalkTable &tab, int leaf, const uint32_t *keep,
-                    const uint32_t *widx, WalkNode *out, int *dCp, cudaStream_t s);
-void launch_walk2_f32(const WalkNode *T, const int *dCp, const float4 *bodies,
-                      const float *targets, int tstride, const uint32_t *tperm, int nt, float e2,
-                      int leaf, float *acc, int astride, int64_t *work64, int *work32,
-                      DeviceFlags *f, cudaStream_t s);
+void launch_walk_tree(const TreeView &t, const WalkTable &tab, int leaf, uint32_t *smask,
+                      uint32_t *nck, uint32_t *base, void *scan_tmp, size_t scan_bytes,
+                      WalkNode *out, int *dCp, cudaStream_t s);
+void launch_walk_f32(const WalkNode *T, const float4 *bodies, const float *targets, int tstride,
+                     const uint32_t *tperm, int nt, float e2, int leaf, float *acc, int astride,
+                     int64_t *work64, int *work32, DeviceFlags *f, cudaStream_t s);
 void launch_walk_f64(const WalkParams &p, const double4 *cm64, const double *q64,
                      const int4 *link, const double4 *bodies, const double *targets,
                      int tstride, const uint32_t *tperm, double *acc, int astride,

@@ -4,24 +4,36 @@
 //
 // Walk tree.  The reference tree keeps one body per leaf; with leaf size L a
 // cell of count <= L is never opened, so its subtree is dead
-// weight for the walk.  k_keep/k_compact copy the cells the walk can reach --
-// the root and every child of a cell with count > L -- in pre-order into a
-// compact array of 64-byte records, with the MAC threshold (side/theta)^2 baked
-// in and the skip links remapped.  At L = 1 every cell is kept.
+// weight for the walk.  k_slots / k_nchild / k_compact copy the cells a walk
+// can reach -- the root and every child of a cell with count > L -- into 64-byte
+// records laid out with each cell's children contiguous (in slot order), the
+// MAC threshold (side/theta)^2 baked in:
 //
-//   a = {com.x, com.y, com.z, mac2}      MAC test   (with d)
+//   a = {-com.x, -com.y, -com.z, mac2}   MAC test (d = p + a)
 //   b = {qxx, qxy, qxy, qyy}             quadrupole, paired for FFMA2
 //   c = {qxz, qyz, mass, qzz}
-//   d = {skip, count, lo, level}         skip = index after the subtree (i+1
-//                                        for pruned buckets), lo = first body
+//   d = {first_child | lo, count, nchild, level}
+//        internal (count > L): children at [first_child, first_child+nchild)
+//        bucket / leaf (count <= L): its bodies are sorted bodies [lo, lo+count)
 //
-// Walk.  One warp walks the union of its 32 targets' interaction lists in
-// pre-order; every lane keeps its own DFS position `next` and evaluates exactly
-// its reference list (per-lane MAC).  The node loads have a warp-uniform
-// address (one wavefront each).  The quadrupole evaluation pairs the x/y
-// components in FFMA2/FMUL2 instructions: the kernel is issue-bound, and a
-// packed instruction does two FMAs per issue slot (measured: FFMA2 runs at the
-// same 74 TFLOP/s pipe rate as FFMA but frees issue slots).
+// Walk.  fp32 mode must reproduce each target's reference interaction *set*
+// (which cells pass the MAC, which are opened); the summation order only moves
+// fp32 rounding.  So instead of the reference's per-target DFS, a warp walks a
+// masked stack: an entry (first_child, nchild, mask0, mask1) says "these
+// children must be examined for the targets in the masks" (the targets that
+// opened their parent).  Popping an entry runs one warp-uniform loop over the
+// siblings: per child each target applies the reference MAC itself -- accept
+// (quadrupole pc), leaf (softened pp), bucket (pp over its bodies) or open
+// (ballot -> push the child's own entry).  A cell is examined for a target
+// exactly when the target opened its parent, as in the reference recursion.
+//
+// Two targets per lane (64 per warp): lane l of warp w owns the Morton-adjacent
+// targets 64w+2l, 64w+2l+1 as float2 pairs, so the MAC / pc / pp math runs in
+// FFMA2/FMUL2/FADD2 (the kernel is issue-bound; a packed instruction does two
+// FMAs per issue slot).  The union of 64 Morton-consecutive interaction lists
+// is only ~1.11x that of 32 (cfg2: 1803 vs 1628 cells), so each 64-byte cell
+// record loaded serves ~1.8x more target interactions than with one target
+// per lane.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -31,32 +43,54 @@
 
 namespace bh {
 
-__global__ void k_keep(TreeView t, int leaf, uint32_t *__restrict__ keep) {
+__device__ __forceinline__ int child_slot(const TreeView &t, int64_t c) {
+  const int4 L = t.link[c];
+  return (int)((t.keys[L.z] >> (3 * (kMortonBits - L.w))) & 7);
+}
+
+// A cell's children are reachable when it can be opened: count > L, or it is
+// the root (the walk always starts at the root's children, flattree.py:271-279)
+__device__ __forceinline__ bool expandable(const TreeView &t, int64_t c, int leaf) {
+  const int cnt = t.link[c].y;
+  return cnt > leaf || (c == 0 && cnt > 1);
+}
+
+// slot masks of the expandable cells
+__global__ void k_slots(TreeView t, int leaf, uint32_t *__restrict__ smask) {
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c <= 0 || c >= t.C) return;
+  const int P = t.parent[c];
+  if (expandable(t, P, leaf)) atomicOr(&smask[P], 1u << child_slot(t, c));
+}
+
+// children per reachable internal cell (0 for buckets, leaves, pruned cells)
+__global__ void k_nchild(TreeView t, int leaf, const uint32_t *__restrict__ smask,
+                         uint32_t *__restrict__ nck) {
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= t.C) return;
-  uint32_t k = 1;
-  if (c > 0) k = t.link[t.parent[c]].y > leaf ? 1u : 0u;
-  keep[c] = k;
+  const bool kept = c == 0 || expandable(t, t.parent[c], leaf);
+  nck[c] = (kept && expandable(t, c, leaf)) ? (uint32_t)__popc(smask[c]) : 0u;
 }
 
-void launch_keep(const TreeView &t, int leaf, uint32_t *keep, cudaStream_t s) {
-  k_keep<<<grid_for(t.C, 256), 256, 0, s>>>(t, leaf, keep);
-}
-
-__global__ void k_compact(TreeView t, WalkTable tab, int leaf, const uint32_t *__restrict__ keep,
-                          const uint32_t *__restrict__ widx, WalkNode *__restrict__ out,
-                          int *__restrict__ dCp) {
+__global__ void k_compact(TreeView t, WalkTable tab, int leaf, const uint32_t *__restrict__ smask,
+                          const uint32_t *__restrict__ nck, const uint32_t *__restrict__ base,
+                          WalkNode *__restrict__ out, int *__restrict__ dCp) {
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t C = t.C;
   if (c >= C) return;
-  const int Cp = (int)(widx[C - 1] + keep[C - 1]);
-  if (c == C - 1) *dCp = Cp;
-  if (!keep[c]) return;
-  const int j = (int)widx[c];
+  if (c == C - 1) *dCp = (int)(1 + base[C - 1] + nck[C - 1]);
+  int j = 0;
+  if (c > 0) {
+    const int P = t.parent[c];
+    if (!expandable(t, P, leaf)) return;  // pruned (inside a bucket)
+    const int slot = child_slot(t, c);
+    j = 1 + (int)base[P] + __popc(smask[P] & ((1u << slot) - 1u));
+  }
   const int4 L = t.link[c];
   const double4 cm = t.cm64[c];
   WalkNode nd;
-  nd.a = make_float4((float)cm.x, (float)cm.y, (float)cm.z, tab.mac2[L.w]);
+  // negated com: the walk forms d = p - com as p + a (one FADD2 per axis)
+  nd.a = make_float4(-(float)cm.x, -(float)cm.y, -(float)cm.z, tab.mac2[L.w]);
   float q0 = 0.f, q1 = 0.f, q2 = 0.f, q3 = 0.f, q4 = 0.f, q5 = 0.f;
   if (L.y > 1) {
     const double *q = t.q64 + 6 * c;
@@ -65,130 +99,161 @@ __global__ void k_compact(TreeView t, WalkTable tab, int leaf, const uint32_t *_
   }
   nd.b = make_float4(q0, q1, q1, q3);
   nd.c = make_float4(q2, q4, (float)cm.w, q5);
-  int nxt;
-  if (L.y <= leaf) nxt = j + 1;  // bucket / leaf: subtree pruned
-  else nxt = L.x < C ? (int)widx[L.x] : Cp;
-  nd.d = make_int4(nxt, L.y, L.z, L.w);
+  const bool internal = expandable(t, c, leaf);
+  nd.d = make_int4(internal ? 1 + (int)base[c] : L.z, L.y, internal ? (int)nck[c] : 0, L.w);
   out[j] = nd;
 }
 
-void launch_compact(const TreeView &t, const WalkTable &tab, int leaf, const uint32_t *keep,
-                    const uint32_t *widx, WalkNode *out, int *dCp, cudaStream_t s) {
-  k_compact<<<grid_for(t.C, 256), 256, 0, s>>>(t, tab, leaf, keep, widx, out, dCp);
+void launch_walk_tree(const TreeView &t, const WalkTable &tab, int leaf, uint32_t *smask,
+                      uint32_t *nck, uint32_t *base, void *scan_tmp, size_t scan_bytes,
+                      WalkNode *out, int *dCp, cudaStream_t s) {
+  const int g = grid_for(t.C, 256);
+  cudaMemsetAsync(smask, 0, sizeof(uint32_t) * t.C, s);
+  k_slots<<<g, 256, 0, s>>>(t, leaf, smask);
+  k_nchild<<<g, 256, 0, s>>>(t, leaf, smask, nck);
+  exclusive_scan_u32(scan_tmp, scan_bytes, nck, base, t.C, s);
+  k_compact<<<g, 256, 0, s>>>(t, tab, leaf, smask, nck, base, out, dCp);
 }
 
 __device__ __forceinline__ float2 f2(float x, float y) { return make_float2(x, y); }
 __device__ __forceinline__ float2 f2(float x) { return make_float2(x, x); }
 
+constexpr int kWalkBlock = 256;
+constexpr int kStack = 8 * (kMaxLevel + 1) + 8;  // <= 8 pending siblings per level
+
 template <bool BUCKET>
-__global__ void __launch_bounds__(256) k_walk2(
-    const WalkNode *__restrict__ T, const int *__restrict__ dCp,
-    const float4 *__restrict__ bodies, const float *__restrict__ targets, int tstride,
-    const uint32_t *__restrict__ tperm, int nt, float e2, int leaf, float *__restrict__ acc,
-    int astride, int64_t *__restrict__ work64, int *__restrict__ work32, DeviceFlags *f) {
-  const int Cp = *dCp;
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool valid = t < nt;
-  const int64_t src = valid ? (tperm ? (int64_t)tperm[t] : t) : 0;
-  float px = 0.f, py = 0.f, pz = 0.f;
-  if (valid) {
-    const float *q = targets + src * tstride;
-    px = q[0]; py = q[1]; pz = q[2];
+__global__ void __launch_bounds__(kWalkBlock) k_walk(
+    const WalkNode *__restrict__ T, const float4 *__restrict__ bodies,
+    const float *__restrict__ targets, int tstride, const uint32_t *__restrict__ tperm, int nt,
+    float e2, int leaf, float *__restrict__ acc, int astride, int64_t *__restrict__ work64,
+    int *__restrict__ work32, DeviceFlags *f) {
+  __shared__ int4 stack_all[kWalkBlock / 32][kStack];
+  int4 *stk = stack_all[threadIdx.x >> 5];
+  const unsigned lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t t0 = warp * 64 + 2 * lane, t1 = t0 + 1;
+  const bool v0 = t0 < nt, v1 = t1 < nt;
+  const int64_t s0 = v0 ? (tperm ? (int64_t)tperm[t0] : t0) : 0;
+  const int64_t s1 = v1 ? (tperm ? (int64_t)tperm[t1] : t1) : 0;
+  float2 X = f2(0.f), Y = f2(0.f), Z = f2(0.f);
+  if (v0) { const float *q = targets + s0 * tstride; X.x = q[0]; Y.x = q[1]; Z.x = q[2]; }
+  if (v1) { const float *q = targets + s1 * tstride; X.y = q[0]; Y.y = q[1]; Z.y = q[2]; }
+  float2 AX = f2(0.f), AY = f2(0.f), AZ = f2(0.f);
+  int pp0 = 0, pp1 = 0, pc0 = 0, pc1 = 0;
+  const float2 E2 = f2(e2);
+  const unsigned bit = 1u << lane;
+
+  // current entry: examine children [fc, fc+nc) for the targets in (m0, m1)
+  int4 e = make_int4(0, 1, (int)__ballot_sync(0xffffffffu, v0), (int)__ballot_sync(0xffffffffu, v1));
+  if (T[0].d.y > 1) {  // root internal: the walk starts at its children (flattree.py:271-279)
+    const int4 rd = T[0].d;
+    e.x = rd.x;
+    e.y = rd.z;
   }
-  float2 axy = f2(0.f);
-  float az = 0.f;
-  int npp = 0, npc = 0;
-  int next = valid ? (Cp == 1 ? 0 : 1) : INT_MAX;
+  int sp = 0;
   for (;;) {
-    const int i = __reduce_min_sync(0xffffffffu, next);
-    if (i >= Cp) break;
-    const WalkNode *nd = T + i;
-    const float4 a = nd->a;
-    const int4 d = nd->d;
-    const bool active = next == i;
-    const float2 dxy = f2(px - a.x, py - a.y);
-    const float dz = pz - a.z;
-    const float2 sq = __fmul2_rn(dxy, dxy);
-    const float d2 = fmaf(dz, dz, sq.x + sq.y);
-    if (d.y == 1) {  // leaf: softened pp with its body (flattree.py:287-294)
-      if (active) {
-        if (d2 > 0.f) {
-          const float m = nd->c.z;
-          const float r = rsqrtf(d2 + e2);
-          const float s = -m * r * r * r;
-          axy = __ffma2_rn(f2(s), dxy, axy);
-          az = fmaf(s, dz, az);
-          ++npp;
-        }
-        next = i + 1;
+    const bool in0 = (unsigned)e.z & bit, in1 = (unsigned)e.w & bit;
+    for (int c = e.x; c < e.x + e.y; ++c) {
+      const WalkNode *nd = T + c;
+      const float4 a = nd->a;
+      const int4 d = nd->d;
+      const int cnt = __reduce_max_sync(0xffffffffu, d.y);  // warp-uniform
+      const float2 DX = __fadd2_rn(X, f2(a.x));
+      const float2 DY = __fadd2_rn(Y, f2(a.y));
+      const float2 DZ = __fadd2_rn(Z, f2(a.z));
+      const float2 D2 = __ffma2_rn(DZ, DZ, __ffma2_rn(DY, DY, __fmul2_rn(DX, DX)));
+      if (cnt == 1) {  // leaf: softened pp, the body itself skipped (flattree.py:287-294)
+        const bool m0 = in0 && D2.x > 0.f, m1 = in1 && D2.y > 0.f;
+        const float2 W = __fadd2_rn(D2, E2);
+        const float2 R = f2(m0 ? rsqrtf(W.x) : 0.f, m1 ? rsqrtf(W.y) : 0.f);
+        const float2 S = __fmul2_rn(__fmul2_rn(R, R), __fmul2_rn(R, f2(-nd->c.z)));
+        AX = __ffma2_rn(S, DX, AX);
+        AY = __ffma2_rn(S, DY, AY);
+        AZ = __ffma2_rn(S, DZ, AZ);
+        pp0 += m0; pp1 += m1;
+        continue;
       }
-    } else if (active && d2 > a.w) {  // MAC: side < theta*|d| (flattree.py:295)
-      const float4 b = nd->b;
-      const float4 c = nd->c;
-      const float r = rsqrtf(d2);
-      const float r2 = r * r;
-      const float r3 = r * r2;
-      const float r5 = r3 * r2;
-      float2 qxy = __fmul2_rn(f2(b.x, b.y), f2(dxy.x));
-      qxy = __ffma2_rn(f2(b.z, b.w), f2(dxy.y), qxy);
-      qxy = __ffma2_rn(f2(c.x, c.y), f2(dz), qxy);
-      const float qz = fmaf(c.w, dz, fmaf(c.y, dxy.y, c.x * dxy.x));
-      const float2 tq = __fmul2_rn(dxy, qxy);
-      const float rqr = fmaf(dz, qz, tq.x + tq.y);
-      // a = (-M - 2.5 (d.Q.d)/r^4) d/r^3 + (Q.d)/r^5      (physics.py:195-213)
-      const float s = fmaf(rqr * (r2 * r2), -2.5f, -c.z) * r3;
-      axy = __ffma2_rn(f2(s), dxy, axy);
-      axy = __ffma2_rn(f2(r5), qxy, axy);
-      az = fmaf(s, dz, fmaf(r5, qz, az));
-      ++npc;
-      next = d.x;
-    } else if (active) {
-      if (BUCKET && d.y <= leaf) {  // bucket rule
-        const int j1 = d.z + d.y;
-        for (int j = d.z; j < j1; ++j) {
+      const bool c0 = in0 && D2.x > a.w, c1 = in1 && D2.y > a.w;  // MAC (flattree.py:295)
+      if (__any_sync(0xffffffffu, c0 || c1)) {
+        const float4 b = nd->b;
+        const float4 q = nd->c;
+        const float2 R = f2(c0 ? rsqrtf(D2.x) : 0.f, c1 ? rsqrtf(D2.y) : 0.f);
+        const float2 R2 = __fmul2_rn(R, R);
+        const float2 R3 = __fmul2_rn(R2, R);
+        const float2 R5 = __fmul2_rn(R3, R2);
+        const float2 QX = __ffma2_rn(f2(q.x), DZ, __ffma2_rn(f2(b.y), DY, __fmul2_rn(f2(b.x), DX)));
+        const float2 QY = __ffma2_rn(f2(q.y), DZ, __ffma2_rn(f2(b.w), DY, __fmul2_rn(f2(b.y), DX)));
+        const float2 QZ = __ffma2_rn(f2(q.w), DZ, __ffma2_rn(f2(q.y), DY, __fmul2_rn(f2(q.x), DX)));
+        const float2 RQR = __ffma2_rn(DZ, QZ, __ffma2_rn(DY, QY, __fmul2_rn(DX, QX)));
+        // a = (-M - 2.5 (d.Q.d)/r^4) d/r^3 + (Q.d)/r^5      (physics.py:195-213)
+        const float2 S =
+            __fmul2_rn(__ffma2_rn(__fmul2_rn(RQR, __fmul2_rn(R2, R2)), f2(-2.5f), f2(-q.z)), R3);
+        AX = __ffma2_rn(R5, QX, __ffma2_rn(S, DX, AX));
+        AY = __ffma2_rn(R5, QY, __ffma2_rn(S, DY, AY));
+        AZ = __ffma2_rn(R5, QZ, __ffma2_rn(S, DZ, AZ));
+        pc0 += c0; pc1 += c1;
+      }
+      const bool o0 = in0 && !c0, o1 = in1 && !c1;  // opened (or bucket-resolved)
+      const unsigned b0 = __ballot_sync(0xffffffffu, o0), b1 = __ballot_sync(0xffffffffu, o1);
+      if ((b0 | b1) == 0u) continue;
+      if (cnt > leaf) {  // open: its children become an entry
+        if (lane == 0) stk[sp] = make_int4(d.x, d.z, (int)b0, (int)b1);
+        ++sp;
+      } else if (BUCKET) {  // bucket rule: pp over its bodies
+        for (int j = d.x; j < d.x + cnt; ++j) {
           const float4 bb = bodies[j];
-          const float2 exy = f2(px - bb.x, py - bb.y);
-          const float ez = pz - bb.z;
-          const float2 s2 = __fmul2_rn(exy, exy);
-          const float r2 = fmaf(ez, ez, s2.x + s2.y);
-          if (r2 > 0.f) {
-            const float r = rsqrtf(r2 + e2);
-            const float s = -bb.w * r * r * r;
-            axy = __ffma2_rn(f2(s), exy, axy);
-            az = fmaf(s, ez, az);
-            ++npp;
-          }
+          const float2 EX = __ffma2_rn(f2(bb.x), f2(-1.f), X);
+          const float2 EY = __ffma2_rn(f2(bb.y), f2(-1.f), Y);
+          const float2 EZ = __ffma2_rn(f2(bb.z), f2(-1.f), Z);
+          const float2 Q2 = __ffma2_rn(EZ, EZ, __ffma2_rn(EY, EY, __fmul2_rn(EX, EX)));
+          const bool m0 = o0 && Q2.x > 0.f, m1 = o1 && Q2.y > 0.f;
+          const float2 W = __fadd2_rn(Q2, E2);
+          const float2 R = f2(m0 ? rsqrtf(W.x) : 0.f, m1 ? rsqrtf(W.y) : 0.f);
+          const float2 S = __fmul2_rn(__fmul2_rn(R, R), __fmul2_rn(R, f2(-bb.w)));
+          AX = __ffma2_rn(S, EX, AX);
+          AY = __ffma2_rn(S, EY, AY);
+          AZ = __ffma2_rn(S, EZ, AZ);
+          pp0 += m0; pp1 += m1;
         }
       }
-      next = i + 1;
     }
+    if (sp == 0) break;
+    __syncwarp();
+    e = stk[--sp];
   }
-  if (valid) {
-    float *o = acc + src * astride;
-    o[0] = axy.x; o[1] = axy.y; o[2] = az;
-    const int w = npp + 2 * npc;  // WORK_PP, WORK_PC (octree.py:23-25)
-    if (work64) work64[src] = w;
-    if (work32) work32[src] = w;
+  if (v0) {
+    float *o = acc + s0 * astride;
+    o[0] = AX.x; o[1] = AY.x; o[2] = AZ.x;
+    const int w = pp0 + 2 * pc0;  // WORK_PP, WORK_PC (octree.py:23-25)
+    if (work64) work64[s0] = w;
+    if (work32) work32[s0] = w;
   }
-  const unsigned spp = __reduce_add_sync(0xffffffffu, (unsigned)npp);
-  const unsigned spc = __reduce_add_sync(0xffffffffu, (unsigned)npc);
-  if ((threadIdx.x & 31) == 0) {
+  if (v1) {
+    float *o = acc + s1 * astride;
+    o[0] = AX.y; o[1] = AY.y; o[2] = AZ.y;
+    const int w = pp1 + 2 * pc1;
+    if (work64) work64[s1] = w;
+    if (work32) work32[s1] = w;
+  }
+  const unsigned spp = __reduce_add_sync(0xffffffffu, (unsigned)(pp0 + pp1));
+  const unsigned spc = __reduce_add_sync(0xffffffffu, (unsigned)(pc0 + pc1));
+  if (lane == 0) {
     atomicAdd(&f->pp, (unsigned long long)spp);
     atomicAdd(&f->pc, (unsigned long long)spc);
   }
 }
 
-void launch_walk2_f32(const WalkNode *T, const int *dCp, const float4 *bodies,
-                      const float *targets, int tstride, const uint32_t *tperm, int nt, float e2,
-                      int leaf, float *acc, int astride, int64_t *work64, int *work32,
-                      DeviceFlags *f, cudaStream_t s) {
+void launch_walk_f32(const WalkNode *T, const float4 *bodies, const float *targets, int tstride,
+                     const uint32_t *tperm, int nt, float e2, int leaf, float *acc, int astride,
+                     int64_t *work64, int *work32, DeviceFlags *f, cudaStream_t s) {
   if (nt <= 0) return;
+  const int64_t threads = ((int64_t)nt + 63) / 64 * 32;
   if (leaf > 1)
-    k_walk2<true><<<grid_for(nt, 256), 256, 0, s>>>(T, dCp, bodies, targets, tstride, tperm, nt,
-                                                    e2, leaf, acc, astride, work64, work32, f);
+    k_walk<true><<<grid_for(threads, kWalkBlock), kWalkBlock, 0, s>>>(
+        T, bodies, targets, tstride, tperm, nt, e2, leaf, acc, astride, work64, work32, f);
   else
-    k_walk2<false><<<grid_for(nt, 256), 256, 0, s>>>(T, dCp, bodies, targets, tstride, tperm, nt,
-                                                     e2, leaf, acc, astride, work64, work32, f);
+    k_walk<false><<<grid_for(threads, kWalkBlock), kWalkBlock, 0, s>>>(
+        T, bodies, targets, tstride, tperm, nt, e2, leaf, acc, astride, work64, work32, f);
 }
 
 }  // namespace bh

@@ -253,6 +253,28 @@ class TestTraverse:
             assert err <= FP32_TOL
             assert np.mean(work != ref_work) < 0.01
 
+    @pytest.mark.parametrize("n", [1, 2, 5, 17, 64])
+    @pytest.mark.parametrize("precision", ["fp32", "fp64"])
+    def test_small_n_bucket(self, n, precision):
+        """n <= leaf size: every root child is a bucket (or leaf)."""
+        from paper_2203_08966_b200.hashed import build_hashed
+        from paper_2203_08966_b200.morton import DomainBounds
+        from paper_2203_08966_b200.physics import Bodies
+
+        rng = np.random.Generator(np.random.Philox(key=n))
+        pos = f32(rng.uniform(-1, 1, (n, 3)))
+        m = f32(rng.uniform(0.5, 1.5, n))
+        R = orc.bounds(pos)
+        order = orc.sort_order(orc.morton_keys(pos, R))
+        ref = orc.build_tree(m[order], pos[order], R)
+        flat = build_hashed(Bodies(m[order], pos[order], np.zeros((n, 3))), DomainBounds(R), precision=precision).flat()
+        for L in (1, 16):
+            ref_acc, ref_work = orc.traverse(ref, pos, 0.5, 0.01, L)
+            acc, work = flat.traverse(pos, 0.5, 0.01, leaf_size=L)
+            np.testing.assert_array_equal(work, ref_work)
+            if n > 1:
+                assert rel_l2(acc, ref_acc) <= (FP32_TOL if precision == "fp32" else ULP_TOL)
+
     def test_theta_zero_is_direct(self, golden):
         from paper_2203_08966_b200.physics import direct_accelerations
 
