@@ -63,7 +63,9 @@ struct bh_handle {
   // tree
   int64_t tree_n = -1, C = 0, max_level = 0;
   double R = 1.0;
-  Buf link, parent, nchild, arrive, cm64, q64, tbod;
+  Buf link, parent, child8, lvl, lvl_list, cm64, q64, tbod;
+  int *hlvl = nullptr;  // pinned: internal cells per level of the last build
+  int sms = 148;
   // fp32 walk tree (compacted per (theta, leaf size))
   Buf smask, nck, wbase, wnodes, wscan_tmp;
   int *dCp = nullptr;
@@ -124,8 +126,7 @@ struct bh_handle {
     t.newc = newc.as<uint32_t>();
     t.link = link.as<int4>();
     t.parent = parent.as<int>();
-    t.nchild = nchild.as<int>();
-    t.arrive = arrive.as<int>();
+    t.child8 = child8.as<int>();
     t.cm64 = cm64.as<double4>();
     t.q64 = q64.as<double>();
     return t;
@@ -192,13 +193,16 @@ int build_sorted(bh_handle *h, int64_t n, const float4 *bod32, const double4 *bo
   BH_CUDA(h->off.ensure(sizeof(uint32_t) * (n + 1)));
   BH_CUDA(h->scan_tmp.ensure(scan_temp_bytes(n) + 16));
   if (n > 0) {
+    BH_CUDA(h->lvl.ensure(sizeof(int) * 4 * (kMaxLevel + 2)));
     launch_lcp_new(h->keys2.as<uint64_t>(), n, h->lcp.as<int8_t>(), h->newc.as<uint32_t>(),
-                   h->flags, s);
+                   h->flags, h->lvl.as<int>(), s);
     BH_CUDA(exclusive_scan_u32(h->scan_tmp.p, h->scan_tmp.bytes, h->newc.as<uint32_t>(),
                                h->off.as<uint32_t>(), n, s));
     BH_LAUNCHED();
     BH_CUDA(cudaMemcpyAsync(h->hC, h->off.as<uint32_t>() + (n - 1), 4, cudaMemcpyDeviceToHost, s));
     BH_CUDA(cudaMemcpyAsync(h->hC + 1, h->newc.as<uint32_t>() + (n - 1), 4,
+                            cudaMemcpyDeviceToHost, s));
+    BH_CUDA(cudaMemcpyAsync(h->hlvl, h->lvl.p, sizeof(int) * (kMaxLevel + 1),
                             cudaMemcpyDeviceToHost, s));
   }
   BH_CUDA(cudaMemcpyAsync(h->hR, h->dR, sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -211,13 +215,13 @@ int build_sorted(bh_handle *h, int64_t n, const float4 *bod32, const double4 *bo
   h->R = *h->hR;
   BH_CUDA(h->link.ensure(sizeof(int4) * C));
   BH_CUDA(h->parent.ensure(sizeof(int) * C));
-  BH_CUDA(h->nchild.ensure(sizeof(int) * C));
-  BH_CUDA(h->arrive.ensure(sizeof(int) * C));
+  BH_CUDA(h->lvl_list.ensure(sizeof(int) * C));
+  BH_CUDA(h->lvl.ensure(sizeof(int) * 4 * (kMaxLevel + 2)));
+  BH_CUDA(h->child8.ensure(sizeof(int) * 8 * C));
+  BH_CUDA(cudaMemsetAsync(h->child8.p, 0xFF, sizeof(int) * 8 * C, s));
   BH_CUDA(h->cm64.ensure(sizeof(double4) * C));
   BH_CUDA(h->q64.ensure(sizeof(double) * 6 * C));
   h->walk_valid = false;
-  BH_CUDA(cudaMemsetAsync(h->nchild.p, 0, sizeof(int) * C, s));
-  BH_CUDA(cudaMemsetAsync(h->arrive.p, 0, sizeof(int) * C, s));
   if (n == 0) {  // hashed.py:459-462: an empty root
     int4 root = make_int4(1, 0, 0, 0);
     BH_CUDA(cudaMemcpyAsync(h->link.p, &root, sizeof(int4), cudaMemcpyHostToDevice, s));
@@ -231,7 +235,16 @@ int build_sorted(bh_handle *h, int64_t n, const float4 *bod32, const double4 *bo
   }
   TreeView t = h->view();
   launch_emit(t, bod32, bod64, s);
-  launch_moments(t, s);
+  LevelPlan plan;
+  int acc = 0;
+  h->max_level = 0;
+  for (int l = 0; l <= kMaxLevel; ++l) {
+    plan.count[l] = h->hlvl[l];
+    plan.offset[l] = acc;
+    acc += h->hlvl[l];
+    if (h->hlvl[l] > 0) h->max_level = l + 1;
+  }
+  launch_moments(t, plan, h->lvl.as<int>() + (kMaxLevel + 1), h->lvl_list.as<int>(), s);
   BH_LAUNCHED();
   return BH_OK;
 }
@@ -401,12 +414,14 @@ int bh_create(bh_handle **out, int device, int precision) {
   bh_handle *h = new bh_handle();
   h->device = device;
   h->precision = precision;
+  cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device);
   BH_CUDA(cudaMalloc(&h->flags, sizeof(DeviceFlags)));
   BH_CUDA(cudaMallocHost(&h->hflags, sizeof(DeviceFlags)));
   BH_CUDA(cudaMallocHost(&h->hC, 4 * sizeof(uint32_t)));
   BH_CUDA(cudaMalloc(&h->dR, sizeof(double)));
   BH_CUDA(cudaMalloc(&h->dCp, sizeof(int)));
   BH_CUDA(cudaMallocHost(&h->hR, sizeof(double)));
+  BH_CUDA(cudaMallocHost(&h->hlvl, sizeof(int) * (kMaxLevel + 2)));
   DeviceFlags init;
   memset(&init, 0, sizeof(init));
   init.first_bad = 0x7fffffffffffffffll;
@@ -420,7 +435,7 @@ int bh_destroy(bh_handle *h) {
   if (!h) return BH_OK;
   cudaSetDevice(h->device);
   Buf *bufs[] = {&h->keys, &h->keys2, &h->vals, &h->vals2, &h->sort_tmp, &h->scan_tmp,
-                 &h->lcp, &h->newc, &h->off, &h->link, &h->parent, &h->nchild, &h->arrive,
+                 &h->lcp, &h->newc, &h->off, &h->link, &h->parent, &h->child8, &h->lvl, &h->lvl_list,
                  &h->cm64, &h->q64, &h->smask, &h->nck, &h->wbase, &h->wnodes, &h->wscan_tmp, &h->tbod, &h->pos, &h->pos2,
                  &h->vel, &h->vel2, &h->acc, &h->id, &h->id2, &h->work_sorted, &h->work_orig};
   for (Buf *b : bufs) b->release();
@@ -430,6 +445,7 @@ int bh_destroy(bh_handle *h) {
   cudaFree(h->dR);
   cudaFree(h->dCp);
   cudaFreeHost(h->hR);
+  cudaFreeHost(h->hlvl);
   h->fold_marks();
   for (cudaEvent_t e : h->pool) cudaEventDestroy(e);
   delete h;

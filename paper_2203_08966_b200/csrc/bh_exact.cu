@@ -133,11 +133,17 @@ __device__ __forceinline__ int lcp_of(uint64_t a, uint64_t b) {
 
 // hashed.py:475-489: sortedness / duplicate checks, lcp, depth, cells per body.
 // newc[i] = depth[i] - start[i] with start = lcp[i-1] (0 for i = 0).
+// Also counts the internal cells each level will hold (levels start+1 ..
+// depth-1 of every body; the last created cell is the body's leaf) so that the
+// level-synchronous moments launches can be sized on the host.
 __global__ void k_lcp_new(const uint64_t *__restrict__ keys, int64_t n,
                           int8_t *__restrict__ lcp, uint32_t *__restrict__ newc,
-                          DeviceFlags *f) {
+                          DeviceFlags *f, int *__restrict__ lvl_cnt) {
+  __shared__ int h[kMaxLevel + 2];
+  if (threadIdx.x <= kMaxLevel + 1) h[threadIdx.x] = 0;
+  __syncthreads();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+  if (i < n) {
   uint64_t k = keys[i];
   int lp = -1, ln = -1;
   if (i > 0) lp = lcp_of(keys[i - 1], k);
@@ -152,12 +158,19 @@ __global__ void k_lcp_new(const uint64_t *__restrict__ keys, int64_t n,
   if (depth > kMaxLevel) atomicOr(&f->bits, FLAG_DEPTH);
   int start = i > 0 ? lp : 0;
   newc[i] = (uint32_t)(depth - start);
+  for (int l = start + 1; l < depth && l <= kMaxLevel; ++l) atomicAdd(&h[l], 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && blockIdx.x == 0) atomicAdd(&h[0], n > 1 ? 1 : 0);  // the root
+  __syncthreads();
+  if (threadIdx.x <= kMaxLevel && h[threadIdx.x]) atomicAdd(&lvl_cnt[threadIdx.x], h[threadIdx.x]);
 }
 
 void launch_lcp_new(const uint64_t *keys, int64_t n, int8_t *lcp, uint32_t *newc,
-                    DeviceFlags *f, cudaStream_t s) {
+                    DeviceFlags *f, int *lvl_cnt, cudaStream_t s) {
   if (n <= 0) return;
-  k_lcp_new<<<grid_for(n, 256), 256, 0, s>>>(keys, n, lcp, newc, f);
+  cudaMemsetAsync(lvl_cnt, 0, sizeof(int) * (kMaxLevel + 1), s);
+  k_lcp_new<<<grid_for(n, 256), 256, 0, s>>>(keys, n, lcp, newc, f, lvl_cnt);
 }
 
 // first b > i whose level-l prefix differs from body i's (n if none):
@@ -234,7 +247,7 @@ __global__ void k_emit(TreeView t, const float4 *__restrict__ bod32,
   for (int l = start + 1; l <= depth; ++l) {
     const int c = base + (l - start - 1);
     t.parent[c] = par;
-    atomicAdd(&t.nchild[par], 1);
+    t.child8[8 * (int64_t)par + (int)((k >> (3 * (kMortonBits - l))) & 7)] = c;
     if (l == depth) {
       t.link[c] = make_int4(c + 1, 1, (int)i, l);
       double4 b;
@@ -266,16 +279,22 @@ void launch_emit(const TreeView &t, const float4 *bod32, const double4 *bod64,
 // order as the reference; children written by other threads of this launch are
 // read through L2 (ld.global.cg) after the acquire fence.
 __device__ void cell_moments(const TreeView &t, int p) {
-  const int end = t.link[p].x;
+  // all child indices at once (slot order), then independent child loads
+  const int4 *row = reinterpret_cast<const int4 *>(t.child8 + 8 * (int64_t)p);
+  const int4 r0 = row[0], r1 = row[1];
+  const int ch[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+  double4 cc[8];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) cc[s] = ch[s] >= 0 ? t.cm64[ch[s]] : make_double4(0.0, 0.0, 0.0, 0.0);
   double total = 0.0, cx = 0.0, cy = 0.0, cz = 0.0;
-  for (int ch = p + 1; ch < end; ch = t.link[ch].x) {
-    double4 c = ldcg4(&t.cm64[ch]);
-    double m = c.w;
-    if (m == 0.0) continue;
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const double m = cc[s].w;
+    if (ch[s] < 0 || m == 0.0) continue;
     total += m;
-    cx += m * c.x;
-    cy += m * c.y;
-    cz += m * c.z;
+    cx += m * cc[s].x;
+    cy += m * cc[s].y;
+    cz += m * cc[s].z;
   }
   double *qo = t.q64 + 6 * (int64_t)p;
   if (total == 0.0) {
@@ -287,19 +306,20 @@ __device__ void cell_moments(const TreeView &t, int p) {
   cy /= total;
   cz /= total;
   double qxx = 0.0, qxy = 0.0, qxz = 0.0, qyy = 0.0, qyz = 0.0, qzz = 0.0;
-  for (int ch = p + 1; ch < end; ch = t.link[ch].x) {
-    double4 c = ldcg4(&t.cm64[ch]);
-    double m = c.w;
-    if (m == 0.0) continue;
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const int c = ch[s];
+    const double m = cc[s].w;
+    if (c < 0 || m == 0.0) continue;
     double q0 = 0.0, q1 = 0.0, q2 = 0.0, q3 = 0.0, q4 = 0.0, q5 = 0.0;
-    if (t.link[ch].y > 1) {  // leaves keep quad = 0 (flattree.py:207-208)
-      const double2 *qc = reinterpret_cast<const double2 *>(t.q64 + 6 * (int64_t)ch);
-      double2 a = __ldcg(qc), b = __ldcg(qc + 1), d = __ldcg(qc + 2);
+    if (t.link[c].y > 1) {  // leaves keep quad = 0 (flattree.py:207-208)
+      const double2 *qc = reinterpret_cast<const double2 *>(t.q64 + 6 * (int64_t)c);
+      double2 a = qc[0], b = qc[1], d = qc[2];
       q0 = a.x; q1 = a.y; q2 = b.x; q3 = b.y; q4 = d.x; q5 = d.y;
     }
-    double dx = c.x - cx;
-    double dy = c.y - cy;
-    double dz = c.z - cz;
+    double dx = cc[s].x - cx;
+    double dy = cc[s].y - cy;
+    double dz = cc[s].z - cz;
     double d2 = dx * dx + dy * dy + dz * dz;
     qxx += q0 + m * (3.0 * (dx * dx) - d2);
     qxy += q1 + m * (3.0 * (dx * dy) - 0.0);
@@ -315,28 +335,47 @@ __device__ void cell_moments(const TreeView &t, int p) {
   q2o[2] = make_double2(qyz, qzz);
 }
 
-// Bottom-up moments in one launch: every body climbs from its leaf; the last
-// child to arrive at a cell computes it (all its children are final by then),
-// so each internal cell is computed exactly once, in slot order.
-__global__ void k_moments(TreeView t) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= t.n) return;
-  int c = (int)t.off[i] + (int)t.newc[i];  // the leaf of body i
-  while (true) {
-    const int p = t.parent[c];
-    if (p < 0) break;
-    __threadfence();
-    const int old = atomicAdd(&t.arrive[p], 1);
-    if (old != t.nchild[p] - 1) break;
-    __threadfence();
-    cell_moments(t, p);
-    c = p;
+// Bottom-up moments, level-synchronous: internal cells are bucketed by level
+// (the per-level counts come from k_lcp_new and are read back with the cell
+// count, so every launch below is sized exactly), then one launch per level,
+// deepest first.  A cell's children are one level deeper, hence final when
+// its level runs; each internal cell is computed once by cell_moments, in the
+// reference's slot order.
+__global__ void k_level_scatter(TreeView t, const LevelPlan plan, int *__restrict__ cursor,
+                                int *__restrict__ list) {
+  __shared__ int h[kMaxLevel + 1], base[kMaxLevel + 1];
+  if (threadIdx.x <= kMaxLevel) h[threadIdx.x] = 0;
+  __syncthreads();
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int l = -1, rank = 0;
+  if (c < t.C) {
+    const int4 L = t.link[c];
+    if (L.y > 1) {
+      l = L.w;
+      rank = atomicAdd(&h[l], 1);
+    }
   }
+  __syncthreads();
+  if (threadIdx.x <= kMaxLevel && h[threadIdx.x])
+    base[threadIdx.x] = plan.offset[threadIdx.x] + atomicAdd(&cursor[threadIdx.x], h[threadIdx.x]);
+  __syncthreads();
+  if (l >= 0) list[base[l] + rank] = (int)c;
 }
 
-void launch_moments(const TreeView &t, cudaStream_t s) {
+__global__ void k_moments_level(TreeView t, const int *__restrict__ list, int begin, int count) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < count) cell_moments(t, list[begin + k]);
+}
+
+void launch_moments(const TreeView &t, const LevelPlan &plan, int *cursor, int *list,
+                    cudaStream_t s) {
   if (t.n <= 1) return;
-  k_moments<<<grid_for(t.n, 128), 128, 0, s>>>(t);
+  cudaMemsetAsync(cursor, 0, sizeof(int) * (kMaxLevel + 1), s);
+  k_level_scatter<<<grid_for(t.C, 256), 256, 0, s>>>(t, plan, cursor, list);
+  for (int l = kMaxLevel; l >= 0; --l) {
+    const int cnt = plan.count[l];
+    if (cnt > 0) k_moments_level<<<grid_for(cnt, 128), 128, 0, s>>>(t, list, plan.offset[l], cnt);
+  }
 }
 
 // FlatTree export (flattree.py:34-52; hashed.py:111-129 cell_geometry for the
@@ -372,14 +411,19 @@ __global__ void k_export(TreeView t, double R, uint64_t *key, int8_t *level, dou
     for (int k = 0; k < 6; ++k) quad[6 * c + k] = L.y > 1 ? t.q64[6 * c + k] : 0.0;
   }
   if (count) count[c] = t.n == 0 ? 0 : L.y;
-  if (children && c > 0) children[8 * (int64_t)t.parent[c] + (int)(pref & 7)] = (int32_t)c;
+  if (children) {
+    const int4 *row = reinterpret_cast<const int4 *>(t.child8 + 8 * c);
+    int4 r0 = row[0], r1 = row[1];
+    int32_t *o = children + 8 * c;
+    o[0] = r0.x; o[1] = r0.y; o[2] = r0.z; o[3] = r0.w;
+    o[4] = r1.x; o[5] = r1.y; o[6] = r1.z; o[7] = r1.w;
+  }
 }
 
 void launch_export(const TreeView &t, double R, uint64_t *key, int8_t *level, double *centre,
                    double *side, double *mass, double *com, double *quad, int64_t *count,
                    int32_t *children, cudaStream_t s) {
   if (t.C <= 0) return;
-  if (children) cudaMemsetAsync(children, 0xFF, sizeof(int32_t) * 8 * t.C, s);
   k_export<<<grid_for(t.C, 256), 256, 0, s>>>(t, R, key, level, centre, side, mass, com, quad,
                                               count, children);
 }

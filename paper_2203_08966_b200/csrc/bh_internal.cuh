@@ -9,7 +9,7 @@
 //   off     u32[n]   exclusive scan of cells created per body
 //   link    int4[C]  {skip, count, lo, level}: skip = index after the subtree
 //                    (pre-order), count = bodies below, lo = first sorted body
-//   parent  i32[C], nchild i32[C], arrive i32[C]  (bottom-up moments)
+//   parent  i32[C], child8 i32[C][8] (slot order), level-bucketed cell list
 //   cm64    double4[C] {com, mass}, q64 double[C][6]           fp64 moments
 //   wnodes  WalkNode[C'] 64-byte fp32 walk records of the cells a walk with
 //                    leaf size L can reach, children contiguous (bh_walk.cu)
@@ -95,7 +95,11 @@ void launch_keys_clamped_f64(const double *pos, int stride, int64_t n, const dou
 
 // tree build (hashed.py:376-515)
 void launch_lcp_new(const uint64_t *keys, int64_t n, int8_t *lcp, uint32_t *newc,
-                    DeviceFlags *f, cudaStream_t s);
+                    DeviceFlags *f, int *lvl_cnt, cudaStream_t s);
+struct LevelPlan {  // internal cells per level (host-known) and list offsets
+  int count[kMaxLevel + 1];
+  int offset[kMaxLevel + 1];
+};
 struct TreeView {
   int64_t n = 0;       // bodies
   int64_t C = 0;       // cells
@@ -105,13 +109,14 @@ struct TreeView {
   const uint32_t *newc = nullptr;
   int4 *link = nullptr;
   int *parent = nullptr;
-  int *nchild = nullptr;
-  int *arrive = nullptr;
+  int *child8 = nullptr;   // [C][8] child indices in slot order (-1 = absent)
   double4 *cm64 = nullptr;
   double *q64 = nullptr;   // [C][6]
 };
 void launch_emit(const TreeView &t, const float4 *bod32, const double4 *bod64, cudaStream_t s);
-void launch_moments(const TreeView &t, cudaStream_t s);
+// cursor: int[kMaxLevel+1] scratch; list: int[C]
+void launch_moments(const TreeView &t, const LevelPlan &plan, int *cursor, int *list,
+                    cudaStream_t s);
 void launch_export(const TreeView &t, double R, uint64_t *key, int8_t *level, double *centre,
                    double *side, double *mass, double *com, double *quad, int64_t *count,
                    int32_t *children, cudaStream_t s);
