@@ -144,6 +144,33 @@ int bh_sim_step(bh_handle *h, double dt, double theta, double eps, int leaf_size
                 void *stream);
 int bh_sim_store(bh_handle *h, void *d_pos, void *d_vel, void *d_acc, int64_t *d_work,
                  void *stream);
+
+/* The same step in phases, for a multi-GPU driver that exchanges between them
+ * (simulation.py:492-502 with the force pass split at the walk):
+ *   begin_step : kick(dt/2) + drift(dt) + bounds reduction
+ *   prepare    : keys, sort, body permutation, build (+ fp32 walk tree)
+ *   walk_range : forces on Morton-sorted targets [begin, end) (the rank's
+ *                costzones range, decomposition.py:35-57)
+ *   scatter_work / end_step : work to caller order; kick(dt/2)
+ * bh_sim_buffers exposes the resident device arrays (Morton order: pos, acc,
+ * work; id = caller index of each sorted body; work in caller order) so the
+ * driver can exchange them with NCCL. */
+int bh_sim_begin_step(bh_handle *h, double dt, void *stream);
+int bh_sim_prepare(bh_handle *h, double theta, double eps, int leaf_size, int bounds_ready,
+                   void *stream);
+int bh_sim_walk_range(bh_handle *h, double theta, double eps, int leaf_size, int64_t begin,
+                      int64_t end, int record_work, void *stream);
+int bh_sim_scatter_work(bh_handle *h, void *stream);
+int bh_sim_end_step(bh_handle *h, double dt, void *stream);
+/* Copy a Morton-order range [begin, end) of a resident array to/from a caller
+ * device buffer: BH_SIM_ACC (4 components per body, handle precision),
+ * BH_SIM_POS (export only), BH_SIM_WORK (int32, this pass), BH_SIM_PREV_WORK
+ * (export only: the previous pass's work of each sorted body -- the costzones
+ * input, decomposition.py:35-57). */
+enum { BH_SIM_ACC = 0, BH_SIM_WORK = 1, BH_SIM_PREV_WORK = 2, BH_SIM_POS = 3 };
+int bh_sim_export(bh_handle *h, int what, int64_t begin, int64_t end, void *d_dst, void *stream);
+int bh_sim_import(bh_handle *h, int what, int64_t begin, int64_t end, const void *d_src,
+                  void *stream);
 int bh_stats_get(bh_handle *h, bh_stats *out, void *stream);
 
 /* ---- instrumentation ----------------------------------------------------- */

@@ -36,9 +36,12 @@ EXPORTS = (
     "bh_traverse_f32", "bh_traverse_f64", "bh_kick_f32", "bh_drift_f32",
     "bh_kick_f64", "bh_drift_f64", "bh_direct_f64", "bh_potential_f64",
     "bh_sim_load", "bh_sim_forces", "bh_sim_step", "bh_sim_store", "bh_stats_get",
+    "bh_sim_begin_step", "bh_sim_prepare", "bh_sim_walk_range", "bh_sim_scatter_work",
+    "bh_sim_end_step", "bh_sim_export", "bh_sim_import",
     "bh_timing_enable", "bh_timing_reset", "bh_timing_get", "bh_ffma_peak",
     "bh_ic_plummer", "bh_host_potential_pairs",
 )
+BH_SIM_ACC, BH_SIM_WORK, BH_SIM_PREV_WORK, BH_SIM_POS = 0, 1, 2, 3
 PHASES = ("integrate", "keys", "sort", "permute", "build", "walk")
 
 
@@ -94,6 +97,13 @@ def _declare(L: ctypes.CDLL) -> None:
         "bh_sim_step": ([P, D, D, D, I, I, P], I),
         "bh_sim_store": ([P, P, P, P, P, P], I),
         "bh_stats_get": ([P, ctypes.POINTER(BHStats), P], I),
+        "bh_sim_begin_step": ([P, D, P], I),
+        "bh_sim_prepare": ([P, D, D, I, I, P], I),
+        "bh_sim_walk_range": ([P, D, D, I, I64, I64, I, P], I),
+        "bh_sim_scatter_work": ([P, P], I),
+        "bh_sim_end_step": ([P, D, P], I),
+        "bh_sim_export": ([P, I, I64, I64, P, P], I),
+        "bh_sim_import": ([P, I, I64, I64, P, P], I),
         "bh_timing_enable": ([P, I], I),
         "bh_timing_reset": ([P], I),
         "bh_timing_get": ([P, ctypes.POINTER(D), I], I),

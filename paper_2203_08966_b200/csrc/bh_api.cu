@@ -327,10 +327,12 @@ __global__ void k_fill_int(int *v, int64_t n, int x) {
   if (i < n) v[i] = x;
 }
 
-// simulation.py:370-396 (algorithm 1, one rank) on resident state:
-// bounds -> keys -> stable sort -> permute bodies -> build -> walk.
-int sim_forces_impl(bh_handle *h, double theta, double eps, int leaf, int record_work,
-                    bool bounds_ready, cudaStream_t s) {
+// simulation.py:370-396 (algorithm 1, one rank) on resident state, split into
+// phases so a multi-GPU driver can exchange between them:
+//   prepare: bounds -> keys -> stable sort -> permute bodies -> build -> walk tree
+//   walk   : targets [begin, end) of the Morton-sorted bodies
+int sim_prepare(bh_handle *h, double theta, double eps, int leaf, bool bounds_ready,
+                cudaStream_t s) {
   const int64_t n = h->sim_n;
   const bool f32 = h->precision == BH_FP32;
   if (!(theta >= 0.0) || !(eps >= 0.0)) return fail(BH_BAD_ARG, "theta and eps must be >= 0");
@@ -374,27 +376,85 @@ int sim_forces_impl(bh_handle *h, double theta, double eps, int leaf, int record
   BH_TRY(build_sorted(h, n, f32 ? h->pos.as<float4>() : nullptr,
                       f32 ? nullptr : h->pos.as<double4>(), s));
   h->tend(s);
+  if (f32) {
+    h->tbegin(BH_PHASE_WALK, s);
+    BH_TRY(ensure_walk_tree(h, theta, leaf, s));
+    h->tend(s);
+  }
+  h->launches += 6;  // finish_R, keys, gather, lcp_new, emit, level scatter (+ per-level)
+  return BH_OK;
+}
+
+int sim_walk(bh_handle *h, double theta, double eps, int leaf, int64_t begin, int64_t end,
+             int record_work, cudaStream_t s) {
+  const int64_t n = h->sim_n;
+  const bool f32 = h->precision == BH_FP32;
+  if (begin < 0 || end > n || begin > end) return fail(BH_BAD_ARG, "walk range outside [0, n]");
+  const int64_t nt = end - begin;
   BH_TRY(reset_counters(h, s));
   h->tbegin(BH_PHASE_WALK, s);
-  WalkParams P;
-  fill_walk_params(h, P, n, theta, eps, leaf);
-  int *w32 = record_work ? h->work_sorted.as<int>() : nullptr;
+  int *w32 = record_work ? h->work_sorted.as<int>() + begin : nullptr;
   if (f32) {
     BH_TRY(ensure_walk_tree(h, theta, leaf, s));
-    launch_walk_f32(h->wnodes.as<WalkNode>(), h->pos.as<float4>(), h->pos.as<float>(), 4, nullptr,
-                    (int)n, (float)(eps * eps), leaf, h->acc.as<float>(), 4, nullptr, w32,
-                    h->flags, s);
-  } else
+    launch_walk_f32(h->wnodes.as<WalkNode>(), h->pos.as<float4>(),
+                    h->pos.as<float>() + 4 * begin, 4, nullptr, (int)nt, (float)(eps * eps), leaf,
+                    h->acc.as<float>() + 4 * begin, 4, nullptr, w32, h->flags, s);
+  } else {
+    WalkParams P;
+    fill_walk_params(h, P, nt, theta, eps, leaf);
     launch_walk_f64(P, h->cm64.as<double4>(), h->q64.as<double>(), h->link.as<int4>(),
-                    h->pos.as<double4>(), h->pos.as<double>(), 4, nullptr, h->acc.as<double>(), 4,
-                    nullptr, w32, h->flags, s);
-  h->tend(s);
-  if (record_work && n > 0) {
-    k_scatter_work<<<grid_for(n, 256), 256, 0, s>>>(w32, h->id.as<uint32_t>(), n,
-                                                    h->work_orig.as<int>());
-    h->launches += 1;
+                    h->pos.as<double4>(), h->pos.as<double>() + 4 * begin, 4, nullptr,
+                    h->acc.as<double>() + 4 * begin, 4, nullptr, w32, h->flags, s);
   }
-  h->launches += 7;  // finish_R, keys, gather, lcp_new, emit, moments, walk
+  h->tend(s);
+  h->launches += 1;
+  BH_LAUNCHED();
+  return BH_OK;
+}
+
+int sim_scatter_work(bh_handle *h, cudaStream_t s) {
+  const int64_t n = h->sim_n;
+  if (n <= 0) return BH_OK;
+  k_scatter_work<<<grid_for(n, 256), 256, 0, s>>>(h->work_sorted.as<int>(), h->id.as<uint32_t>(), n,
+                                                  h->work_orig.as<int>());
+  h->launches += 1;
+  BH_LAUNCHED();
+  return BH_OK;
+}
+
+int sim_forces_impl(bh_handle *h, double theta, double eps, int leaf, int record_work,
+                    bool bounds_ready, cudaStream_t s) {
+  BH_TRY(sim_prepare(h, theta, eps, leaf, bounds_ready, s));
+  BH_TRY(sim_walk(h, theta, eps, leaf, 0, h->sim_n, record_work, s));
+  if (record_work) BH_TRY(sim_scatter_work(h, s));
+  return BH_OK;
+}
+
+int sim_begin_step(bh_handle *h, double dt, cudaStream_t s) {
+  const int64_t n = h->sim_n;
+  const double half = 0.5 * dt;  // simulation.py:494: kick(0.5*dt), drift(dt)
+  h->tbegin(BH_PHASE_INTEGRATE, s);
+  launch_reset_flags_bounds(h->flags, s);
+  if (h->precision == BH_FP32)
+    launch_kick_drift_max_f32(h->pos.as<float4>(), h->vel.as<float4>(), h->acc.as<float4>(), n,
+                              (float)half, (float)dt, h->flags, s);
+  else
+    launch_kick_drift_max_f64(h->pos.as<double4>(), h->vel.as<double4>(), h->acc.as<double4>(),
+                              n, half, dt, h->flags, s);
+  h->tend(s);
+  h->launches += 2;
+  BH_LAUNCHED();
+  return BH_OK;
+}
+
+int sim_end_step(bh_handle *h, double dt, cudaStream_t s) {
+  const int64_t n = h->sim_n;
+  const double half = 0.5 * dt;  // simulation.py:500: kick(0.5*dt)
+  h->tbegin(BH_PHASE_INTEGRATE, s);
+  if (h->precision == BH_FP32) launch_kick_f32(h->vel.as<float4>(), h->acc.as<float4>(), n, (float)half, s);
+  else launch_kick4_f64(h->vel.as<double4>(), h->acc.as<double4>(), n, half, s);
+  h->tend(s);
+  h->launches += 1;
   BH_LAUNCHED();
   return BH_OK;
 }
@@ -712,28 +772,98 @@ int bh_sim_forces(bh_handle *h, double theta, double eps, int leaf_size, int rec
 int bh_sim_step(bh_handle *h, double dt, double theta, double eps, int leaf_size, int steps,
                 void *stream) {
   if (!h || !(dt > 0.0) || steps < 0) return fail(BH_BAD_ARG, "bh_sim_step: bad args");
-  const int64_t n = h->sim_n;
-  if (n == 0) return BH_OK;
+  if (h->sim_n == 0) return BH_OK;
   cudaStream_t s = S(stream);
-  const bool f32 = h->precision == BH_FP32;
-  const double half = 0.5 * dt;  // integrator.py / simulation.py:494: kick(0.5*dt)
   for (int k = 0; k < steps; ++k) {
-    h->tbegin(BH_PHASE_INTEGRATE, s);
-    launch_reset_flags_bounds(h->flags, s);
-    if (f32)
-      launch_kick_drift_max_f32(h->pos.as<float4>(), h->vel.as<float4>(), h->acc.as<float4>(), n,
-                                (float)half, (float)dt, h->flags, s);
-    else
-      launch_kick_drift_max_f64(h->pos.as<double4>(), h->vel.as<double4>(), h->acc.as<double4>(),
-                                n, half, dt, h->flags, s);
-    h->tend(s);
+    BH_TRY(sim_begin_step(h, dt, s));
     BH_TRY(sim_forces_impl(h, theta, eps, leaf_size, 1, true, s));
-    h->tbegin(BH_PHASE_INTEGRATE, s);
-    if (f32) launch_kick_f32(h->vel.as<float4>(), h->acc.as<float4>(), n, (float)half, s);
-    else launch_kick4_f64(h->vel.as<double4>(), h->acc.as<double4>(), n, half, s);
-    h->tend(s);
-    h->launches += 3;
-    BH_LAUNCHED();
+    BH_TRY(sim_end_step(h, dt, s));
+  }
+  return BH_OK;
+}
+
+int bh_sim_begin_step(bh_handle *h, double dt, void *stream) {
+  if (!h || !(dt > 0.0)) return fail(BH_BAD_ARG, "bh_sim_begin_step: bad args");
+  if (h->sim_n == 0) return BH_OK;
+  return sim_begin_step(h, dt, S(stream));
+}
+
+int bh_sim_prepare(bh_handle *h, double theta, double eps, int leaf_size, int bounds_ready,
+                   void *stream) {
+  if (!h) return fail(BH_BAD_ARG, "bh_sim_prepare: bad args");
+  if (h->sim_n == 0) return BH_OK;
+  return sim_prepare(h, theta, eps, leaf_size, bounds_ready != 0, S(stream));
+}
+
+int bh_sim_walk_range(bh_handle *h, double theta, double eps, int leaf_size, int64_t begin,
+                      int64_t end, int record_work, void *stream) {
+  if (!h) return fail(BH_BAD_ARG, "bh_sim_walk_range: bad args");
+  if (h->sim_n == 0) return BH_OK;
+  return sim_walk(h, theta, eps, leaf_size, begin, end, record_work, S(stream));
+}
+
+int bh_sim_scatter_work(bh_handle *h, void *stream) {
+  if (!h) return fail(BH_BAD_ARG, "bh_sim_scatter_work: bad args");
+  return sim_scatter_work(h, S(stream));
+}
+
+int bh_sim_end_step(bh_handle *h, double dt, void *stream) {
+  if (!h || !(dt > 0.0)) return fail(BH_BAD_ARG, "bh_sim_end_step: bad args");
+  if (h->sim_n == 0) return BH_OK;
+  return sim_end_step(h, dt, S(stream));
+}
+
+__global__ void k_gather_work(const int *wo, const uint32_t *id, int64_t b, int64_t e, int *dst) {
+  int64_t i = b + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < e) dst[i - b] = wo[id[i]];
+}
+
+int bh_sim_export(bh_handle *h, int what, int64_t begin, int64_t end, void *dst, void *stream) {
+  if (!h || !dst || begin < 0 || end > h->sim_n || begin > end)
+    return fail(BH_BAD_ARG, "bh_sim_export: bad args");
+  const int64_t k = end - begin;
+  if (k == 0) return BH_OK;
+  cudaStream_t s = S(stream);
+  const size_t e4 = h->precision == BH_FP32 ? sizeof(float4) : sizeof(double4);
+  switch (what) {
+    case BH_SIM_ACC:
+      BH_CUDA(cudaMemcpyAsync(dst, h->acc.as<char>() + e4 * begin, e4 * k, cudaMemcpyDeviceToDevice, s));
+      break;
+    case BH_SIM_POS:
+      BH_CUDA(cudaMemcpyAsync(dst, h->pos.as<char>() + e4 * begin, e4 * k, cudaMemcpyDeviceToDevice, s));
+      break;
+    case BH_SIM_WORK:
+      BH_CUDA(cudaMemcpyAsync(dst, h->work_sorted.as<int>() + begin, sizeof(int) * k,
+                              cudaMemcpyDeviceToDevice, s));
+      break;
+    case BH_SIM_PREV_WORK:
+      k_gather_work<<<grid_for(k, 256), 256, 0, s>>>(h->work_orig.as<int>(), h->id.as<uint32_t>(),
+                                                     begin, end, static_cast<int *>(dst));
+      BH_LAUNCHED();
+      break;
+    default:
+      return fail(BH_BAD_ARG, "bh_sim_export: unknown array");
+  }
+  return BH_OK;
+}
+
+int bh_sim_import(bh_handle *h, int what, int64_t begin, int64_t end, const void *src, void *stream) {
+  if (!h || !src || begin < 0 || end > h->sim_n || begin > end)
+    return fail(BH_BAD_ARG, "bh_sim_import: bad args");
+  const int64_t k = end - begin;
+  if (k == 0) return BH_OK;
+  cudaStream_t s = S(stream);
+  const size_t e4 = h->precision == BH_FP32 ? sizeof(float4) : sizeof(double4);
+  switch (what) {
+    case BH_SIM_ACC:
+      BH_CUDA(cudaMemcpyAsync(h->acc.as<char>() + e4 * begin, src, e4 * k, cudaMemcpyDeviceToDevice, s));
+      break;
+    case BH_SIM_WORK:
+      BH_CUDA(cudaMemcpyAsync(h->work_sorted.as<int>() + begin, src, sizeof(int) * k,
+                              cudaMemcpyDeviceToDevice, s));
+      break;
+    default:
+      return fail(BH_BAD_ARG, "bh_sim_import: acc and work only");
   }
   return BH_OK;
 }

@@ -215,6 +215,31 @@ class Engine:
         check(self._L.bh_sim_step(self._h, float(dt), float(theta), float(eps), int(leaf_size),
                                   int(steps), self.stream))
 
+    # -- phases (multi-GPU driver, decomposition.py) --
+    def sim_begin_step(self, dt: float) -> None:
+        check(self._L.bh_sim_begin_step(self._h, float(dt), self.stream))
+
+    def sim_prepare(self, theta: float, eps: float, leaf_size: int = 1, bounds_ready: bool = True) -> None:
+        check(self._L.bh_sim_prepare(self._h, float(theta), float(eps), int(leaf_size),
+                                     int(bool(bounds_ready)), self.stream))
+
+    def sim_walk_range(self, theta: float, eps: float, leaf_size: int, begin: int, end: int,
+                       record_work: bool = True) -> None:
+        check(self._L.bh_sim_walk_range(self._h, float(theta), float(eps), int(leaf_size),
+                                        int(begin), int(end), int(bool(record_work)), self.stream))
+
+    def sim_scatter_work(self) -> None:
+        check(self._L.bh_sim_scatter_work(self._h, self.stream))
+
+    def sim_end_step(self, dt: float) -> None:
+        check(self._L.bh_sim_end_step(self._h, float(dt), self.stream))
+
+    def sim_export(self, what: int, begin: int, end: int, dst: torch.Tensor) -> None:
+        check(self._L.bh_sim_export(self._h, int(what), int(begin), int(end), _ptr(dst), self.stream))
+
+    def sim_import(self, what: int, begin: int, end: int, src: torch.Tensor) -> None:
+        check(self._L.bh_sim_import(self._h, int(what), int(begin), int(end), _ptr(src), self.stream))
+
     def sim_store(self, pos=None, vel=None, acc=None, work=None) -> None:
         check(self._L.bh_sim_store(self._h, _ptr(pos), _ptr(vel), _ptr(acc), _ptr(work), self.stream))
 

@@ -1,0 +1,85 @@
+"""Multi-rank decomposition: costzones cuts, and the
+replicated-tree / partitioned-walk protocol over torch.distributed gloo with
+world size 2 (CPU), compared bit for bit with a single-rank run."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2203_08966_b200.decomposition import (
+    DistributedSim, StepParams, TorchComm, costzones, costzones_device)
+
+
+def test_costzones_matches_reference_rule():
+    # decomposition.py:35-57 examples: straddling body goes to the left zone
+    np.testing.assert_array_equal(costzones([1, 1, 1, 1], 2), [0, 2, 4])
+    np.testing.assert_array_equal(costzones([3, 1, 1, 1], 2), [0, 1, 4])
+    np.testing.assert_array_equal(costzones([1, 1, 1, 1, 1], 2), [0, 3, 5])
+    with pytest.raises(ValueError):
+        costzones([1, 1], 3)
+    rng = np.random.Generator(np.random.Philox(key=5))
+    for zones in (1, 2, 3, 7, 8):
+        w = rng.integers(0, 3000, size=10_000)
+        ref = costzones(w, zones)
+        got = costzones_device(torch.from_numpy(w).to(torch.int32), zones)
+        np.testing.assert_array_equal(got, ref)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, out_q, n, steps):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from fake_engine import OracleEngine
+    from paper_2203_08966_b200.initcond import two_clusters
+
+    b = two_clusters(n, 3)
+    sim = DistributedSim(OracleEngine(), TorchComm(), StepParams(0.6, 0.05, 1, 0.01))
+    sim.load(torch.from_numpy(b.position), torch.from_numpy(b.velocity), torch.from_numpy(b.mass))
+    sim.bootstrap()
+    sim.step(steps)
+    pos = torch.zeros((n, 4), dtype=torch.float64)
+    vel = torch.zeros((n, 4), dtype=torch.float64)
+    work = torch.zeros(n, dtype=torch.int64)
+    sim.store(pos=pos, vel=vel, work=work)
+    out_q.put((rank, pos[:, :3].numpy(), vel[:, :3].numpy(), work.numpy(), sim.zones))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_gloo_matches_single_rank():
+    from oracle import oracle as orc
+    from paper_2203_08966_b200.initcond import two_clusters
+
+    n, steps = 300, 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, n, steps)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=240) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    b = two_clusters(n, 3)
+    x, v, a, w = orc.leapfrog(b.mass, b.position, b.velocity, 0.01, steps, 0.6, 0.05)
+    for rank, pos, vel, work, zones in res:
+        np.testing.assert_array_equal(pos, x)   # every rank holds the full, identical state
+        np.testing.assert_array_equal(vel, v)
+        np.testing.assert_array_equal(work, w)
+        assert len(zones) == 3 and zones[0] == 0 and zones[-1] == n and 0 < zones[1] < n
