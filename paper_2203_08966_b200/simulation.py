@@ -197,9 +197,29 @@ def simulate(cfg: SimConfig, *, transport: str = "inproc", record_trace: bool = 
     pos = eng.bodies_tensor(bodies.position, bodies.mass)
     vel = eng.vec_tensor(bodies.velocity)
     m = None if eng.fp32 else torch.as_tensor(bodies.mass).to(eng.device)
-    eng.sim_load(pos, vel, m)
     leaf = cfg.walk_leaf_size
-    eng.sim_forces(cfg.theta, cfg.eps, leaf, record_work=False)  # simulation.py:487
+    dsim = None
+    if cfg.devices > 1:  # one process per GPU (torchrun); decomposition.py
+        import torch.distributed as dist
+
+        from .decomposition import DistributedSim, StepParams, TorchComm
+
+        if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() != cfg.devices:
+            raise ValueError(
+                f"devices={cfg.devices} needs torch.distributed initialised with that world size "
+                "(one process per GPU, e.g. torchrun --nproc-per-node)")
+        dsim = DistributedSim(eng, TorchComm(), StepParams(cfg.theta, cfg.eps, leaf, cfg.dt))
+        dsim.load(pos, vel, m)
+        dsim.bootstrap()
+    else:
+        eng.sim_load(pos, vel, m)
+        eng.sim_forces(cfg.theta, cfg.eps, leaf, record_work=False)  # simulation.py:487
+
+    def advance(k: int) -> None:
+        if dsim is not None:
+            dsim.step(k)
+        else:
+            eng.sim_step(cfg.dt, cfg.theta, cfg.eps, leaf, k)
 
     def snapshot() -> Bodies:
         p = torch.empty_like(vel)
@@ -221,12 +241,12 @@ def simulate(cfg: SimConfig, *, transport: str = "inproc", record_trace: bool = 
         step = 0
         while step < cfg.steps:
             k = min(snapshot_every, cfg.steps - step)
-            eng.sim_step(cfg.dt, cfg.theta, cfg.eps, leaf, k)
+            advance(k)
             step += k
             if step % snapshot_every == 0:
                 snaps.append((step * cfg.dt, snapshot()))
     elif cfg.steps:
-        eng.sim_step(cfg.dt, cfg.theta, cfg.eps, leaf, cfg.steps)
+        advance(cfg.steps)
     st = eng.stats()
     interactions = st.interactions
     final = snapshot()
