@@ -97,6 +97,11 @@ int bh_build_f32(bh_handle *h, const float *d_pos4_sorted, int64_t n, const doub
 int bh_build_f64(bh_handle *h, const double *d_pos3_sorted, const double *d_mass_sorted,
                  int64_t n, const double *d_R, void *stream);
 int bh_tree_size(bh_handle *h, int64_t *n_cells);
+/* Bucket-mode extension: bodies with identical Morton keys share
+ * one level-21 cell that is resolved body by body, instead of the reference's
+ * "tree resolution" error (hashed.py:477-482).  Off by default for
+ * bh_build_*; the resident bh_sim_* path enables it whenever leaf_size > 1. */
+int bh_set_allow_duplicates(bh_handle *h, int allow);
 
 /* flattree.py:34-52 FlatTree arrays of the current tree (pre-order).
  * Any pointer may be NULL to skip that array.  Shapes: centre/com [C][3],

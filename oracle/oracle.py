@@ -57,6 +57,10 @@ def lib():
         L.or_tree_size.restype = I64
         L.or_build.argtypes = [P, P, P, I64, D, I64] + [P] * 10
         L.or_build.restype = ctypes.c_int
+        L.or_build2.argtypes = [P, P, P, I64, D, I64] + [P] * 10 + [ctypes.c_int]
+        L.or_build2.restype = ctypes.c_int
+        L.or_tree_size2.argtypes = [P, I64, ctypes.c_int]
+        L.or_tree_size2.restype = I64
         L.or_traverse.argtypes = [I64] + [P] * 10 + [I64, D, D, I64, P, P, ctypes.c_int, P]
         L.or_traverse.restype = None
         L.or_direct.argtypes = [P, P, I64, D, P, ctypes.c_int]
@@ -134,13 +138,14 @@ class OracleTree:
         return len(self.count)
 
 
-def build_tree(mass_sorted, pos_sorted, R: float) -> OracleTree:
-    """hashed.py:448-515 build_hashed on Morton-sorted bodies (with moments)."""
+def build_tree(mass_sorted, pos_sorted, R: float, allow_duplicates: bool = False) -> OracleTree:
+    """hashed.py:448-515 build_hashed on Morton-sorted bodies (with moments).
+    ``allow_duplicates``: bucket-mode extension, equal keys share a level-21 cell."""
     m = _f64(mass_sorted).reshape(-1)
     pos = _f64(pos_sorted).reshape(-1, 3)
     n = len(m)
     keys = morton_keys(pos, R) if n else np.zeros(0, dtype=np.uint64)
-    C = int(lib().or_tree_size(_p(keys), n))
+    C = int(lib().or_tree_size2(_p(keys), n, int(allow_duplicates)))
     if C == -1:
         raise ValueError("bodies must be sorted by spatial key for a hashed build")
     if C == -2:
@@ -159,10 +164,10 @@ def build_tree(mass_sorted, pos_sorted, R: float) -> OracleTree:
         bmass=m,
         bpos=pos,
     )
-    rc = lib().or_build(
+    rc = lib().or_build2(
         _p(keys), _p(m), _p(pos), n, float(R), C,
         _p(t.key), _p(t.level), _p(t.centre), _p(t.side), _p(t.mass), _p(t.com),
-        _p(t.quad), _p(t.count), _p(t.children), _p(t.lo),
+        _p(t.quad), _p(t.count), _p(t.children), _p(t.lo), int(allow_duplicates),
     )
     assert rc == 0, rc
     return t
@@ -228,7 +233,7 @@ def kinetic_energy(mass, vel) -> float:
 
 
 def tree_accelerations(mass, pos, theta: float, eps: float, leaf_size: int = 1,
-                       R: float | None = None, nthreads: int = 0):
+                       R: float | None = None, nthreads: int = 0, allow_duplicates: bool = False):
     """simulation.py:218-221 + 390-393: bounds -> keys -> stable sort -> take ->
     build_hashed -> traverse the bodies in caller order."""
     m = _f64(mass).reshape(-1)
@@ -236,7 +241,7 @@ def tree_accelerations(mass, pos, theta: float, eps: float, leaf_size: int = 1,
     if R is None:
         R = bounds(p)
     order = sort_order(morton_keys(p, R))
-    tree = build_tree(m[order], p[order], R)
+    tree = build_tree(m[order], p[order], R, allow_duplicates)
     return traverse(tree, p, theta, eps, leaf_size, nthreads)
 
 

@@ -66,6 +66,9 @@ struct bh_handle {
   Buf link, parent, child8, lvl, lvl_list, cm64, q64, tbod;
   int *hlvl = nullptr;  // pinned: internal cells per level of the last build
   int sms = 148;
+  int allow_dup = 0;       // bh_set_allow_duplicates; the sim path uses leaf_size > 1
+  const float4 *tbod32 = nullptr;   // bodies of the current tree (sorted)
+  const double4 *tbod64 = nullptr;
   // fp32 walk tree (compacted per (theta, leaf size))
   Buf smask, nck, wbase, wnodes, wscan_tmp;
   int *dCp = nullptr;
@@ -127,6 +130,8 @@ struct bh_handle {
     t.link = link.as<int4>();
     t.parent = parent.as<int>();
     t.child8 = child8.as<int>();
+    t.bod32 = tbod32;
+    t.bod64 = tbod64;
     t.cm64 = cm64.as<double4>();
     t.q64 = q64.as<double>();
     return t;
@@ -187,7 +192,8 @@ int sort_keys(bh_handle *h, int64_t n, cudaStream_t s) {
 // Build over Morton-sorted bodies whose keys are already in keys2
 // (hashed.py:448-515).  Exactly one of bod32 / bod64 is non-null.
 int build_sorted(bh_handle *h, int64_t n, const float4 *bod32, const double4 *bod64,
-                 cudaStream_t s) {
+                 cudaStream_t s, int allow_dup = -1) {
+  if (allow_dup < 0) allow_dup = h->allow_dup;
   BH_CUDA(h->lcp.ensure(n + 16));
   BH_CUDA(h->newc.ensure(sizeof(uint32_t) * (n + 1)));
   BH_CUDA(h->off.ensure(sizeof(uint32_t) * (n + 1)));
@@ -195,7 +201,7 @@ int build_sorted(bh_handle *h, int64_t n, const float4 *bod32, const double4 *bo
   if (n > 0) {
     BH_CUDA(h->lvl.ensure(sizeof(int) * 4 * (kMaxLevel + 2)));
     launch_lcp_new(h->keys2.as<uint64_t>(), n, h->lcp.as<int8_t>(), h->newc.as<uint32_t>(),
-                   h->flags, h->lvl.as<int>(), s);
+                   h->flags, h->lvl.as<int>(), allow_dup, s);
     BH_CUDA(exclusive_scan_u32(h->scan_tmp.p, h->scan_tmp.bytes, h->newc.as<uint32_t>(),
                                h->off.as<uint32_t>(), n, s));
     BH_LAUNCHED();
@@ -234,6 +240,10 @@ int build_sorted(bh_handle *h, int64_t n, const float4 *bod32, const double4 *bo
     return BH_OK;
   }
   TreeView t = h->view();
+  t.bod32 = bod32;
+  t.bod64 = bod64;
+  h->tbod32 = bod32;
+  h->tbod64 = bod64;
   launch_emit(t, bod32, bod64, s);
   LevelPlan plan;
   int acc = 0;
@@ -374,7 +384,7 @@ int sim_prepare(bh_handle *h, double theta, double eps, int leaf, bool bounds_re
   BH_LAUNCHED();
   h->tbegin(BH_PHASE_BUILD, s);
   BH_TRY(build_sorted(h, n, f32 ? h->pos.as<float4>() : nullptr,
-                      f32 ? nullptr : h->pos.as<double4>(), s));
+                      f32 ? nullptr : h->pos.as<double4>(), s, h->allow_dup || leaf > 1));
   h->tend(s);
   if (f32) {
     h->tbegin(BH_PHASE_WALK, s);
@@ -598,6 +608,12 @@ int bh_build_f64(bh_handle *h, const double *d_pos3_sorted, const double *d_mass
   BH_CUDA(cudaMemcpyAsync(h->dR, d_R, sizeof(double), cudaMemcpyDeviceToDevice, s));
   launch_keys_f64(d_pos3_sorted, 3, n, h->dR, h->keys2.as<uint64_t>(), nullptr, h->flags, s);
   return build_sorted(h, n, nullptr, h->tbod.as<double4>(), s);
+}
+
+int bh_set_allow_duplicates(bh_handle *h, int allow) {
+  if (!h) return fail(BH_BAD_ARG, "bh_set_allow_duplicates: bad args");
+  h->allow_dup = allow != 0;
+  return BH_OK;
 }
 
 int bh_tree_size(bh_handle *h, int64_t *n_cells) {

@@ -136,9 +136,13 @@ __device__ __forceinline__ int lcp_of(uint64_t a, uint64_t b) {
 // Also counts the internal cells each level will hold (levels start+1 ..
 // depth-1 of every body; the last created cell is the body's leaf) so that the
 // level-synchronous moments launches can be sized on the host.
+// allow_dup (bucket mode, SURVEY.md §7 "Duplicate keys"): bodies with equal
+// keys cannot be separated; they share one level-21 cell (count = run length)
+// that is never opened and is resolved body by body.  The reference raises
+// instead (hashed.py:477-482), which is what allow_dup = 0 reproduces.
 __global__ void k_lcp_new(const uint64_t *__restrict__ keys, int64_t n,
                           int8_t *__restrict__ lcp, uint32_t *__restrict__ newc,
-                          DeviceFlags *f, int *__restrict__ lvl_cnt) {
+                          DeviceFlags *f, int *__restrict__ lvl_cnt, int allow_dup) {
   __shared__ int h[kMaxLevel + 2];
   if (threadIdx.x <= kMaxLevel + 1) h[threadIdx.x] = 0;
   __syncthreads();
@@ -150,15 +154,19 @@ __global__ void k_lcp_new(const uint64_t *__restrict__ keys, int64_t n,
   if (i + 1 < n) {
     uint64_t kn = keys[i + 1];
     if (kn < k) atomicOr(&f->bits, FLAG_UNSORTED);
-    if (kn == k) atomicOr(&f->bits, FLAG_DUPLICATE);
+    if (kn == k && !allow_dup) atomicOr(&f->bits, FLAG_DUPLICATE);
     ln = lcp_of(k, kn);
     lcp[i] = (int8_t)ln;
   }
   int depth = (lp > ln ? lp : ln) + 1;
-  if (depth > kMaxLevel) atomicOr(&f->bits, FLAG_DEPTH);
+  if (depth > kMaxLevel) {
+    if (allow_dup) depth = kMaxLevel;
+    else atomicOr(&f->bits, FLAG_DEPTH);
+  }
   int start = i > 0 ? lp : 0;
   newc[i] = (uint32_t)(depth - start);
   for (int l = start + 1; l < depth && l <= kMaxLevel; ++l) atomicAdd(&h[l], 1);
+  if (ln == kMaxLevel && lp < kMaxLevel) atomicAdd(&h[kMaxLevel], 1);  // duplicate-run cell
   }
   __syncthreads();
   if (threadIdx.x == 0 && blockIdx.x == 0) atomicAdd(&h[0], n > 1 ? 1 : 0);  // the root
@@ -167,10 +175,10 @@ __global__ void k_lcp_new(const uint64_t *__restrict__ keys, int64_t n,
 }
 
 void launch_lcp_new(const uint64_t *keys, int64_t n, int8_t *lcp, uint32_t *newc,
-                    DeviceFlags *f, int *lvl_cnt, cudaStream_t s) {
+                    DeviceFlags *f, int *lvl_cnt, int allow_dup, cudaStream_t s) {
   if (n <= 0) return;
   cudaMemsetAsync(lvl_cnt, 0, sizeof(int) * (kMaxLevel + 1), s);
-  k_lcp_new<<<grid_for(n, 256), 256, 0, s>>>(keys, n, lcp, newc, f, lvl_cnt);
+  k_lcp_new<<<grid_for(n, 256), 256, 0, s>>>(keys, n, lcp, newc, f, lvl_cnt, allow_dup);
 }
 
 // first b > i whose level-l prefix differs from body i's (n if none):
@@ -234,7 +242,7 @@ __global__ void k_emit(TreeView t, const float4 *__restrict__ bod32,
   const uint64_t k = t.keys[i];
   const int lp = i > 0 ? t.lcp[i - 1] : -1;
   const int ln = i + 1 < n ? t.lcp[i] : -1;
-  const int depth = (lp > ln ? lp : ln) + 1;
+  const int depth = min((lp > ln ? lp : ln) + 1, kMaxLevel);  // clamp: duplicate keys
   const int start = i > 0 ? lp : 0;
   const int base = 1 + (int)t.off[i];
   int par = 0;
@@ -248,7 +256,11 @@ __global__ void k_emit(TreeView t, const float4 *__restrict__ bod32,
     const int c = base + (l - start - 1);
     t.parent[c] = par;
     t.child8[8 * (int64_t)par + (int)((k >> (3 * (kMortonBits - l))) & 7)] = c;
-    if (l == depth) {
+    if (l == depth && ln == kMaxLevel) {  // first body of a duplicate-key run
+      const int64_t end = run_end(t.keys, n, i, k, 0);
+      const int skip = end < n ? 1 + (int)t.off[end] : C;
+      t.link[c] = make_int4(skip, (int)(end - i), (int)i, l);
+    } else if (l == depth) {
       t.link[c] = make_int4(c + 1, 1, (int)i, l);
       double4 b;
       if (bod64) {
@@ -278,11 +290,64 @@ void launch_emit(const TreeView &t, const float4 *bod32, const double4 *bod64,
 // (pre-order: first child c+1, next sibling skip[child]).  Same expression
 // order as the reference; children written by other threads of this launch are
 // read through L2 (ld.global.cg) after the acquire fence.
+__device__ __forceinline__ double4 body64(const TreeView &t, int64_t j) {
+  if (t.bod64) return t.bod64[j];
+  const float4 v = t.bod32[j];
+  return make_double4(v.x, v.y, v.z, v.w);
+}
+
+// Moments of a level-21 cell holding bodies with identical keys (bucket mode
+// only): the same combine as _moments_kernel with the bodies, in sorted order,
+// as leaf children.  Mirrored by the extended oracle (oracle/bh_oracle.c).
+__device__ void dup_cell_moments(const TreeView &t, int p) {
+  const int4 L = t.link[p];
+  double total = 0.0, cx = 0.0, cy = 0.0, cz = 0.0;
+  for (int j = L.z; j < L.z + L.y; ++j) {
+    const double4 b = body64(t, j);
+    if (b.w == 0.0) continue;
+    total += b.w;
+    cx += b.w * b.x;
+    cy += b.w * b.y;
+    cz += b.w * b.z;
+  }
+  double2 *q2o = reinterpret_cast<double2 *>(t.q64 + 6 * (int64_t)p);
+  if (total == 0.0) {
+    t.cm64[p] = make_double4(0.0, 0.0, 0.0, 0.0);
+    q2o[0] = q2o[1] = q2o[2] = make_double2(0.0, 0.0);
+    return;
+  }
+  cx /= total;
+  cy /= total;
+  cz /= total;
+  double qxx = 0.0, qxy = 0.0, qxz = 0.0, qyy = 0.0, qyz = 0.0, qzz = 0.0;
+  for (int j = L.z; j < L.z + L.y; ++j) {
+    const double4 b = body64(t, j);
+    const double m = b.w;
+    if (m == 0.0) continue;
+    double dx = b.x - cx, dy = b.y - cy, dz = b.z - cz;
+    double d2 = dx * dx + dy * dy + dz * dz;
+    qxx += 0.0 + m * (3.0 * (dx * dx) - d2);
+    qxy += 0.0 + m * (3.0 * (dx * dy) - 0.0);
+    qxz += 0.0 + m * (3.0 * (dx * dz) - 0.0);
+    qyy += 0.0 + m * (3.0 * (dy * dy) - d2);
+    qyz += 0.0 + m * (3.0 * (dy * dz) - 0.0);
+    qzz += 0.0 + m * (3.0 * (dz * dz) - d2);
+  }
+  t.cm64[p] = make_double4(cx, cy, cz, total);
+  q2o[0] = make_double2(qxx, qxy);
+  q2o[1] = make_double2(qxz, qyy);
+  q2o[2] = make_double2(qyz, qzz);
+}
+
 __device__ void cell_moments(const TreeView &t, int p) {
   // all child indices at once (slot order), then independent child loads
   const int4 *row = reinterpret_cast<const int4 *>(t.child8 + 8 * (int64_t)p);
   const int4 r0 = row[0], r1 = row[1];
   const int ch[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+  if ((r0.x & r0.y & r0.z & r0.w & r1.x & r1.y & r1.z & r1.w) == -1) {
+    dup_cell_moments(t, p);  // a duplicate-key cell: its bodies are its children
+    return;
+  }
   double4 cc[8];
 #pragma unroll
   for (int s = 0; s < 8; ++s) cc[s] = ch[s] >= 0 ? t.cm64[ch[s]] : make_double4(0.0, 0.0, 0.0, 0.0);
@@ -507,7 +572,7 @@ __global__ void __launch_bounds__(128) k_walk_f64(
       az += mono * dz + qrz / c5 - c7 * dz;
       ++npc;
       next = L.x;
-    } else if (P.leaf > 1 && L.y <= P.leaf) {
+    } else if (P.leaf > 1 && (L.y <= P.leaf || L.w == kMaxLevel)) {  // bucket / dup cell
       for (int j = L.z; j < L.z + L.y; ++j) pp64(px, py, pz, bodies[j], P.e2, ax, ay, az, npp);
       next = L.x;
     } else {

@@ -95,7 +95,7 @@ void launch_keys_clamped_f64(const double *pos, int stride, int64_t n, const dou
 
 // tree build (hashed.py:376-515)
 void launch_lcp_new(const uint64_t *keys, int64_t n, int8_t *lcp, uint32_t *newc,
-                    DeviceFlags *f, int *lvl_cnt, cudaStream_t s);
+                    DeviceFlags *f, int *lvl_cnt, int allow_dup, cudaStream_t s);
 struct LevelPlan {  // internal cells per level (host-known) and list offsets
   int count[kMaxLevel + 1];
   int offset[kMaxLevel + 1];
@@ -110,6 +110,8 @@ struct TreeView {
   int4 *link = nullptr;
   int *parent = nullptr;
   int *child8 = nullptr;   // [C][8] child indices in slot order (-1 = absent)
+  const float4 *bod32 = nullptr;   // sorted bodies the tree was built from
+  const double4 *bod64 = nullptr;
   double4 *cm64 = nullptr;
   double *q64 = nullptr;   // [C][6]
 };

@@ -14,7 +14,8 @@
 //   c = {qxz, qyz, mass, qzz}
 //   d = {first_child | lo, count, nchild, level}
 //        internal (count > L): children at [first_child, first_child+nchild)
-//        bucket / leaf (count <= L): its bodies are sorted bodies [lo, lo+count)
+//        bucket / leaf (count <= L, or a level-21 duplicate-key cell):
+//        nchild = 0, its bodies are the sorted bodies [lo, lo+count)
 //
 // Walk.  fp32 mode must reproduce each target's reference interaction *set*
 // (which cells pass the MAC, which are opened); the summation order only moves
@@ -51,8 +52,9 @@ __device__ __forceinline__ int child_slot(const TreeView &t, int64_t c) {
 // A cell's children are reachable when it can be opened: count > L, or it is
 // the root (the walk always starts at the root's children, flattree.py:271-279)
 __device__ __forceinline__ bool expandable(const TreeView &t, int64_t c, int leaf) {
-  const int cnt = t.link[c].y;
-  return cnt > leaf || (c == 0 && cnt > 1);
+  const int4 L = t.link[c];
+  // level-21 cells of duplicate keys have no children: always buckets
+  return (L.y > leaf || (c == 0 && L.y > 1)) && L.w < kMaxLevel;
 }
 
 // slot masks of the expandable cells
@@ -196,7 +198,7 @@ __global__ void __launch_bounds__(kWalkBlock) k_walk(
       const bool o0 = in0 && !c0, o1 = in1 && !c1;  // opened (or bucket-resolved)
       const unsigned b0 = __ballot_sync(0xffffffffu, o0), b1 = __ballot_sync(0xffffffffu, o1);
       if ((b0 | b1) == 0u) continue;
-      if (cnt > leaf) {  // open: its children become an entry
+      if (d.z > 0) {  // open: its children become an entry
         if (lane == 0) stk[sp] = make_int4(d.x, d.z, (int)b0, (int)b1);
         ++sp;
       } else if (BUCKET) {  // bucket rule: pp over its bodies

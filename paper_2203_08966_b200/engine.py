@@ -157,6 +157,10 @@ class Engine:
         check(self._L.bh_tree_size(self._h, ctypes.byref(c)))
         return int(c.value)
 
+    def set_allow_duplicates(self, allow: bool) -> None:
+        """Bucket-mode extension: identical keys share a level-21 cell."""
+        check(self._L.bh_set_allow_duplicates(self._h, int(bool(allow))))
+
     def tree_size(self) -> int:
         c = ctypes.c_int64()
         check(self._L.bh_tree_size(self._h, ctypes.byref(c)))

@@ -79,10 +79,13 @@ class DeviceTree:
 
 
 def build_hashed(bodies: Bodies, bounds: DomainBounds, precision: str = "fp64",
-                 engine: Engine | None = None) -> DeviceTree:
+                 engine: Engine | None = None, allow_duplicates: bool = False) -> DeviceTree:
     """hashed.py:448: bodies must be Morton-sorted with distinct keys
-    (ValueError otherwise, with the reference's message fragments)."""
+    (ValueError otherwise, with the reference's message fragments).
+    ``allow_duplicates`` is the bucket-mode extension: bodies
+    with equal keys share one level-21 cell, resolved body by body."""
     eng = engine if engine is not None else Engine(precision)
+    eng.set_allow_duplicates(allow_duplicates)
     pos = eng.bodies_tensor(bodies.position, bodies.mass)
     R = torch.tensor([float(bounds.half_extent)], dtype=torch.float64, device=eng.device)
     if eng.fp32:

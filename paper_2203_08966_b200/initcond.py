@@ -120,3 +120,58 @@ def colliding_plummers(n_per_cluster: int, seed: int, total_mass: float = 1.0,
     b.position -= off
     b.velocity += v
     return Bodies.concat([a, b])
+
+
+def hernquist_cosmology(n: int, seed: int = 4, n_halos: int = 1000, halo_fraction: float = 0.7,
+                        a_range=(0.005, 0.05), mass_decades: float = 2.0, sigma_v: float = 0.1,
+                        truncation: float = 10.0, dtype=np.float32):
+    """BASELINE.json config 4: clustered cosmology-like cloud.
+
+    * ``halo_fraction`` of the bodies in ``n_halos`` Hernquist halos: scale
+      radius a ~ U[a_range], halo mass log-uniform over ``mass_decades``
+      decades, body count proportional to mass (largest-remainder rounding),
+      radius from the inverse CDF r = a sqrt(u) / (1 - sqrt(u)), isotropic
+      directions;
+    * the rest uniform in the unit cube [0, 1)^3;
+    * velocities N(0, sigma_v^2) per component; equal masses, total 1;
+      no periodic wrapping.
+
+    Choices the configuration leaves open, recorded here and in DESIGN.md:
+    halo centres are uniform in [0.1, 0.9)^3, and radii are truncated at
+    ``truncation`` * a by drawing u below (t / (1 + t))^2 (exact inverse-CDF
+    truncation, no rejection).  Philox key ``seed``; vectorised (numpy), so it
+    is not a bit-level restatement of any reference generator (the reference
+    has none for this configuration).  Returns (pos (n,3), vel (n,3), mass (n,))
+    in ``dtype``.
+    """
+    rng = make_rng(seed)
+    n_h = int(round(halo_fraction * n))
+    logm = rng.uniform(0.0, mass_decades, n_halos)
+    w = 10.0 ** logm
+    share = n_h * w / w.sum()
+    counts = np.floor(share).astype(np.int64)
+    rem = n_h - int(counts.sum())
+    if rem > 0:
+        counts[np.argsort(-(share - counts), kind="stable")[:rem]] += 1
+    centres = rng.uniform(0.1, 0.9, (n_halos, 3))
+    scale = rng.uniform(a_range[0], a_range[1], n_halos)
+    pos = np.empty((n, 3), dtype=dtype)
+    umax = (truncation / (1.0 + truncation)) ** 2
+    off = 0
+    for h in range(n_halos):
+        k = int(counts[h])
+        if k == 0:
+            continue
+        su = np.sqrt(rng.uniform(0.0, umax, k))
+        r = scale[h] * su / (1.0 - su)
+        z = rng.uniform(-1.0, 1.0, k)
+        phi = rng.uniform(0.0, 2.0 * np.pi, k)
+        s = np.sqrt(np.maximum(0.0, 1.0 - z * z))
+        pos[off:off + k, 0] = centres[h, 0] + r * s * np.cos(phi)
+        pos[off:off + k, 1] = centres[h, 1] + r * s * np.sin(phi)
+        pos[off:off + k, 2] = centres[h, 2] + r * z
+        off += k
+    pos[off:] = rng.uniform(0.0, 1.0, (n - off, 3))
+    vel = (rng.standard_normal((n, 3)) * sigma_v).astype(dtype)
+    mass = np.full(n, 1.0 / n, dtype=dtype)
+    return pos, vel, mass

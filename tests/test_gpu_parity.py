@@ -430,3 +430,34 @@ class TestFullSize:
         acc, work = eng32.traverse(tg, 0.6, 1e-3, 16)
         ref_acc, _ = orc.traverse(ref, pos[sample], 0.6, 1e-3, 16)
         assert rel_l2(acc[:, :3].double().cpu().numpy(), ref_acc) <= FP32_TOL
+
+
+class TestDuplicateKeysGPU:
+    @pytest.mark.parametrize("precision", ["fp32", "fp64"])
+    def test_bucket_mode_duplicates_vs_oracle(self, precision):
+        from paper_2203_08966_b200.hashed import build_hashed
+        from paper_2203_08966_b200.morton import DomainBounds
+        from paper_2203_08966_b200.physics import Bodies
+
+        rng = np.random.Generator(np.random.Philox(key=8))
+        pos = f32(rng.uniform(-1, 1, (5000, 3)))
+        pos[10:50] = pos[9]        # a 41-body run (> leaf size)
+        pos[200:202] = pos[100]
+        m = f32(rng.uniform(0.5, 1.5, 5000))
+        R = orc.bounds(pos)
+        order = orc.sort_order(orc.morton_keys(pos, R))
+        ref = orc.build_tree(m[order], pos[order], R, allow_duplicates=True)
+        with pytest.raises(ValueError, match="tree resolution"):
+            build_hashed(Bodies(m[order], pos[order], np.zeros_like(pos)), DomainBounds(R), precision=precision)
+        tree = build_hashed(Bodies(m[order], pos[order], np.zeros_like(pos)), DomainBounds(R),
+                            precision=precision, allow_duplicates=True)
+        if precision == "fp64":
+            a = tree.arrays()
+            for name in ("key", "level", "mass", "com", "quad", "count", "children"):
+                np.testing.assert_array_equal(a[name], getattr(ref, name), err_msg=name)
+        for L in (16, 32):
+            ref_acc, ref_work = orc.traverse(ref, pos, 0.5, 0.01, L)
+            acc, work = tree.flat().traverse(pos, 0.5, 0.01, leaf_size=L)
+            tol = FP32_TOL if precision == "fp32" else ULP_TOL
+            assert rel_l2(acc, ref_acc) <= tol
+            assert np.mean(work != ref_work) < (0.01 if precision == "fp32" else 1e-12)

@@ -180,3 +180,38 @@ class TestLeapfrog:
         g = golden("cfg0.npz")
         np.testing.assert_array_equal(
             orc.direct_accelerations(g["mass"], g["pos0"], float(g["eps"])), g["direct0"])
+
+
+class TestDuplicateKeys:
+    """Bucket-mode extension: equal keys share a level-21 cell."""
+
+    def _cloud(self):
+        rng = np.random.Generator(np.random.Philox(key=8))
+        pos = rng.uniform(-1, 1, (300, 3))
+        pos[10:15] = pos[9]          # a run of six identical bodies
+        pos[200:202] = pos[100]      # and a pair
+        m = rng.uniform(0.5, 1.5, 300)
+        R = orc.bounds(pos)
+        order = orc.sort_order(orc.morton_keys(pos, R))
+        return m[order], pos[order], R
+
+    def test_reference_semantics_still_reject(self):
+        m, pos, R = self._cloud()
+        with pytest.raises(ValueError, match="tree resolution"):
+            orc.build_tree(m, pos, R)
+
+    def test_dup_cells(self):
+        m, pos, R = self._cloud()
+        t = orc.build_tree(m, pos, R, allow_duplicates=True)
+        dup = np.flatnonzero((t.count > 1) & (t.children.max(axis=1) < 0))
+        assert sorted(t.count[dup].tolist()) == [3, 6]
+        assert np.all(t.level[dup] == 21)
+        assert t.mass[0] == pytest.approx(m.sum(), rel=1e-14)
+        assert t.count[0] == len(m)
+
+    def test_theta_zero_bucket_is_direct(self):
+        m, pos, R = self._cloud()
+        t = orc.build_tree(m, pos, R, allow_duplicates=True)
+        acc, _ = orc.traverse(t, pos, 0.0, 0.05, leaf_size=4)
+        ref = orc.direct_accelerations(m, pos, 0.05)
+        np.testing.assert_allclose(acc, ref, rtol=1e-12, atol=1e-14)
