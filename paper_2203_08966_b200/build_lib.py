@@ -59,6 +59,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for unit, extra in UNITS.items():
         obj = os.path.join(objdir, os.path.splitext(unit)[0] + ".o")
         cmd = [cc, *ARCH, *COMMON, *extra, "-c", os.path.join(CSRC, unit), "-o", obj]
+        cmd += os.environ.get("BH_NVCC_EXTRA", "").split()
         if verbose:
             cmd += ["-Xptxas", "-v"]
             print(" ".join(cmd), file=sys.stderr)

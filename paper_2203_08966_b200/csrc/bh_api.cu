@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -62,6 +63,13 @@ struct bh_handle {
   Buf keys, keys2, vals, vals2, sort_tmp, scan_tmp, lcp, newc, off;
   // tree
   int64_t tree_n = -1, C = 0, max_level = 0;
+  // sync-free build (fp32 resident path): capacity, device count, snapshot
+  bool async_tree = false;
+  int64_t cap = 0, C_true = 0;
+  int *dCtrue = nullptr;
+  int *hstat = nullptr;  // pinned: [0] = C, [1..22] = internal cells per level
+  int grid_lvl[kMaxLevel + 1] = {0};
+  Buf bk_pos, bk_vel, bk_acc, bk_id, bk_work;
   double R = 1.0;
   Buf link, parent, child8, lvl, lvl_list, cm64, q64, tbod;
   int *hlvl = nullptr;  // pinned: internal cells per level of the last build
@@ -123,6 +131,7 @@ struct bh_handle {
     TreeView t;
     t.n = tree_n;
     t.C = C;
+    t.dC = async_tree ? dCtrue : nullptr;
     t.keys = keys2.as<uint64_t>();
     t.lcp = lcp.as<int8_t>();
     t.off = off.as<uint32_t>();
@@ -217,6 +226,8 @@ int build_sorted(bh_handle *h, int64_t n, const float4 *bod32, const double4 *bo
   const int64_t C = n > 0 ? 1 + (int64_t)h->hC[0] + (int64_t)h->hC[1] : 1;
   if (C > 0x7fffffffll) return fail(BH_OUT_OF_MEMORY, "more than 2^31-1 cells");
   h->C = C;
+  h->C_true = C;
+  h->async_tree = false;
   h->tree_n = n;
   h->R = *h->hR;
   BH_CUDA(h->link.ensure(sizeof(int4) * C));
@@ -259,6 +270,77 @@ int build_sorted(bh_handle *h, int64_t n, const float4 *bod32, const double4 *bo
   return BH_OK;
 }
 
+// Sync-free variant of build_sorted for the fp32 resident path: the cell
+// count and the per-level counts stay on the device; buffers are sized to a
+// capacity (2n, grown from the largest tree seen) and an overflow is flagged,
+// detected at the end of the bh_sim_step call and repaired by re-running it.
+int build_sorted_async(bh_handle *h, int64_t n, const float4 *bod32, cudaStream_t s,
+                       int allow_dup) {
+  if (n <= 1) return build_sorted(h, n, bod32, nullptr, s, allow_dup);
+  int64_t cap = std::max<int64_t>(h->cap, 2 * n + 1024);
+  if (cap > 0x7fffffffll) cap = 0x7fffffffll;
+  h->cap = cap;
+  BH_CUDA(h->lcp.ensure(n + 16));
+  BH_CUDA(h->newc.ensure(sizeof(uint32_t) * (n + 1)));
+  BH_CUDA(h->off.ensure(sizeof(uint32_t) * (n + 1)));
+  BH_CUDA(h->scan_tmp.ensure(scan_temp_bytes(n) + 16));
+  BH_CUDA(h->lvl.ensure(sizeof(int) * 4 * (kMaxLevel + 2)));
+  launch_lcp_new(h->keys2.as<uint64_t>(), n, h->lcp.as<int8_t>(), h->newc.as<uint32_t>(),
+                 h->flags, h->lvl.as<int>(), allow_dup, s);
+  BH_CUDA(exclusive_scan_u32(h->scan_tmp.p, h->scan_tmp.bytes, h->newc.as<uint32_t>(),
+                             h->off.as<uint32_t>(), n, s));
+  launch_set_count(h->off.as<uint32_t>(), h->newc.as<uint32_t>(), n, cap, h->dCtrue, h->flags, s);
+  BH_CUDA(h->link.ensure(sizeof(int4) * cap));
+  BH_CUDA(h->parent.ensure(sizeof(int) * cap));
+  BH_CUDA(h->lvl_list.ensure(sizeof(int) * cap));
+  BH_CUDA(h->child8.ensure(sizeof(int) * 8 * cap));
+  BH_CUDA(h->cm64.ensure(sizeof(double4) * cap));
+  BH_CUDA(h->q64.ensure(sizeof(double) * 6 * cap));
+  BH_CUDA(cudaMemsetAsync(h->child8.p, 0xFF, sizeof(int) * 8 * cap, s));
+  h->C = cap;
+  h->tree_n = n;
+  h->async_tree = true;
+  h->walk_valid = false;
+  h->tbod32 = bod32;
+  h->tbod64 = nullptr;
+  TreeView t = h->view();
+  launch_emit(t, bod32, nullptr, s);
+  BH_CUDA((cudaError_t)launch_moments_coop(t, h->lvl.as<int>(), h->lvl_list.as<int>(), h->sms, s));
+  h->launches += 4;
+  BH_LAUNCHED();
+  return BH_OK;
+}
+
+// Read back (one sync) what the sync-free builds of this call left on the
+// device: the true cell count (stats, capacity growth), per-level counts
+// (next call's grid sizes) and the flags.  Returns 1 on a capacity overflow.
+int async_readback(bh_handle *h, cudaStream_t s, int *overflow) {
+  *overflow = 0;
+  if (!h->async_tree) return BH_OK;
+  BH_CUDA(cudaMemcpyAsync(h->hstat, h->dCtrue, sizeof(int), cudaMemcpyDeviceToHost, s));
+  BH_CUDA(cudaMemcpyAsync(h->hstat + 1, h->lvl.p, sizeof(int) * (kMaxLevel + 1),
+                          cudaMemcpyDeviceToHost, s));
+  BH_TRY(read_flags(h, s));
+  if (h->hflags->bits & FLAG_OVERFLOW) {
+    *overflow = 1;
+    int keep = h->hflags->bits & ~FLAG_OVERFLOW;
+    BH_CUDA(cudaMemcpyAsync(&h->flags->bits, &keep, sizeof(int), cudaMemcpyHostToDevice, s));
+    BH_CUDA(cudaStreamSynchronize(s));
+    h->hflags->bits = keep;
+    h->cap = std::min<int64_t>(0x7fffffffll, h->hstat[0] + h->hstat[0] / 4 + 1024);
+    return BH_OK;
+  }
+  BH_TRY(take_flag_error(h, s));
+  h->C_true = h->hstat[0];
+  h->max_level = 0;
+  for (int l = 0; l <= kMaxLevel; ++l) {
+    const int cnt = h->hstat[1 + l];
+    h->grid_lvl[l] = cnt > 0 ? grid_for(cnt + cnt / 4 + 64, 128) : 1;
+    if (cnt > 0) h->max_level = l + 1;
+  }
+  return BH_OK;
+}
+
 void fill_walk_params(bh_handle *h, WalkParams &P, int64_t nt, double theta, double eps,
                       int leaf) {
   P.C = (int)h->C;
@@ -286,12 +368,7 @@ int ensure_walk_tree(bh_handle *h, double theta, int leaf, cudaStream_t s) {
   BH_CUDA(h->wnodes.ensure(sizeof(WalkNode) * C));
   BH_CUDA(h->wscan_tmp.ensure(scan_temp_bytes(C) + 16));
   TreeView t = h->view();
-  WalkTable tab;
-  for (int l = 0; l <= kMaxLevel; ++l) {
-    double r = std::ldexp(2.0 * h->R, -l) / theta;  // theta == 0 -> inf: never accept
-    tab.mac2[l] = (float)(r * r);
-  }
-  launch_walk_tree(t, tab, leaf, h->smask.as<uint32_t>(), h->nck.as<uint32_t>(),
+  launch_walk_tree(t, h->dR, theta, leaf, h->smask.as<uint32_t>(), h->nck.as<uint32_t>(),
                    h->wbase.as<uint32_t>(), h->wscan_tmp.p, h->wscan_tmp.bytes,
                    h->wnodes.as<WalkNode>(), h->dCp, s);
   h->launches += 3;
@@ -383,8 +460,10 @@ int sim_prepare(bh_handle *h, double theta, double eps, int leaf, bool bounds_re
   h->tend(s);
   BH_LAUNCHED();
   h->tbegin(BH_PHASE_BUILD, s);
-  BH_TRY(build_sorted(h, n, f32 ? h->pos.as<float4>() : nullptr,
-                      f32 ? nullptr : h->pos.as<double4>(), s, h->allow_dup || leaf > 1));
+  if (f32)
+    BH_TRY(build_sorted_async(h, n, h->pos.as<float4>(), s, h->allow_dup || leaf > 1));
+  else
+    BH_TRY(build_sorted(h, n, nullptr, h->pos.as<double4>(), s, h->allow_dup || leaf > 1));
   h->tend(s);
   if (f32) {
     h->tbegin(BH_PHASE_WALK, s);
@@ -490,6 +569,8 @@ int bh_create(bh_handle **out, int device, int precision) {
   BH_CUDA(cudaMallocHost(&h->hC, 4 * sizeof(uint32_t)));
   BH_CUDA(cudaMalloc(&h->dR, sizeof(double)));
   BH_CUDA(cudaMalloc(&h->dCp, sizeof(int)));
+  BH_CUDA(cudaMalloc(&h->dCtrue, sizeof(int)));
+  BH_CUDA(cudaMallocHost(&h->hstat, sizeof(int) * (kMaxLevel + 4)));
   BH_CUDA(cudaMallocHost(&h->hR, sizeof(double)));
   BH_CUDA(cudaMallocHost(&h->hlvl, sizeof(int) * (kMaxLevel + 2)));
   DeviceFlags init;
@@ -507,13 +588,16 @@ int bh_destroy(bh_handle *h) {
   Buf *bufs[] = {&h->keys, &h->keys2, &h->vals, &h->vals2, &h->sort_tmp, &h->scan_tmp,
                  &h->lcp, &h->newc, &h->off, &h->link, &h->parent, &h->child8, &h->lvl, &h->lvl_list,
                  &h->cm64, &h->q64, &h->smask, &h->nck, &h->wbase, &h->wnodes, &h->wscan_tmp, &h->tbod, &h->pos, &h->pos2,
-                 &h->vel, &h->vel2, &h->acc, &h->id, &h->id2, &h->work_sorted, &h->work_orig};
+                 &h->vel, &h->vel2, &h->acc, &h->id, &h->id2, &h->work_sorted, &h->work_orig,
+                 &h->bk_pos, &h->bk_vel, &h->bk_acc, &h->bk_id, &h->bk_work};
   for (Buf *b : bufs) b->release();
   cudaFree(h->flags);
   cudaFreeHost(h->hflags);
   cudaFreeHost(h->hC);
   cudaFree(h->dR);
   cudaFree(h->dCp);
+  cudaFree(h->dCtrue);
+  cudaFreeHost(h->hstat);
   cudaFreeHost(h->hR);
   cudaFreeHost(h->hlvl);
   h->fold_marks();
@@ -525,6 +609,11 @@ int bh_destroy(bh_handle *h) {
 int bh_check(bh_handle *h, void *stream) {
   if (!h) return fail(BH_BAD_ARG, "handle is NULL");
   BH_CUDA(cudaGetLastError());
+  int overflow = 0;
+  BH_TRY(async_readback(h, S(stream), &overflow));
+  if (overflow)
+    return fail(BH_OUT_OF_MEMORY,
+                "tree cell capacity exceeded during a phased step; capacity grown, redo the step");
   BH_TRY(read_flags(h, S(stream)));
   return take_flag_error(h, S(stream));
 }
@@ -619,7 +708,12 @@ int bh_set_allow_duplicates(bh_handle *h, int allow) {
 int bh_tree_size(bh_handle *h, int64_t *n_cells) {
   if (!h || !n_cells) return fail(BH_BAD_ARG, "bh_tree_size: bad args");
   if (h->tree_n < 0) return fail(BH_NO_TREE, "no tree has been built");
-  *n_cells = h->C;
+  if (h->async_tree) {
+    int overflow = 0;
+    BH_TRY(async_readback(h, nullptr, &overflow));
+    if (overflow) return fail(BH_OUT_OF_MEMORY, "tree cell capacity exceeded");
+  }
+  *n_cells = h->async_tree ? h->C_true : h->C;
   return BH_OK;
 }
 
@@ -782,20 +876,49 @@ int bh_sim_forces(bh_handle *h, double theta, double eps, int leaf_size, int rec
                   void *stream) {
   if (!h) return fail(BH_BAD_ARG, "bh_sim_forces: bad args");
   if (h->sim_n == 0) return BH_OK;
-  return sim_forces_impl(h, theta, eps, leaf_size, record_work, false, S(stream));
+  for (int attempt = 0; attempt < 3; ++attempt) {  // forces only permute: safe to redo
+    BH_TRY(sim_forces_impl(h, theta, eps, leaf_size, record_work, false, S(stream)));
+    int overflow = 0;
+    BH_TRY(async_readback(h, S(stream), &overflow));
+    if (!overflow) return BH_OK;
+  }
+  return fail(BH_OUT_OF_MEMORY, "tree cell capacity kept overflowing");
+}
+
+static int sim_snapshot(bh_handle *h, bool restore, cudaStream_t s) {
+  const int64_t n = h->sim_n;
+  const size_t e4 = h->precision == BH_FP32 ? sizeof(float4) : sizeof(double4);
+  struct { Buf *live, *bk; size_t bytes; } items[] = {
+      {&h->pos, &h->bk_pos, e4 * n}, {&h->vel, &h->bk_vel, e4 * n}, {&h->acc, &h->bk_acc, e4 * n},
+      {&h->id, &h->bk_id, sizeof(uint32_t) * n}, {&h->work_orig, &h->bk_work, sizeof(int) * n}};
+  for (auto &it : items) {
+    if (!restore) BH_CUDA(it.bk->ensure(it.bytes));
+    void *dst = restore ? it.live->p : it.bk->p;
+    void *src = restore ? it.bk->p : it.live->p;
+    BH_CUDA(cudaMemcpyAsync(dst, src, it.bytes, cudaMemcpyDeviceToDevice, s));
+  }
+  return BH_OK;
 }
 
 int bh_sim_step(bh_handle *h, double dt, double theta, double eps, int leaf_size, int steps,
                 void *stream) {
   if (!h || !(dt > 0.0) || steps < 0) return fail(BH_BAD_ARG, "bh_sim_step: bad args");
-  if (h->sim_n == 0) return BH_OK;
+  if (h->sim_n == 0 || steps == 0) return BH_OK;
   cudaStream_t s = S(stream);
-  for (int k = 0; k < steps; ++k) {
-    BH_TRY(sim_begin_step(h, dt, s));
-    BH_TRY(sim_forces_impl(h, theta, eps, leaf_size, 1, true, s));
-    BH_TRY(sim_end_step(h, dt, s));
+  const bool f32 = h->precision == BH_FP32;
+  for (int attempt = 0; attempt < 3; ++attempt) {
+    if (f32) BH_TRY(sim_snapshot(h, false, s));
+    for (int k = 0; k < steps; ++k) {
+      BH_TRY(sim_begin_step(h, dt, s));
+      BH_TRY(sim_forces_impl(h, theta, eps, leaf_size, 1, true, s));
+      BH_TRY(sim_end_step(h, dt, s));
+    }
+    int overflow = 0;
+    BH_TRY(async_readback(h, s, &overflow));
+    if (!overflow) return BH_OK;
+    BH_TRY(sim_snapshot(h, true, s));  // grown capacity: redo the call
   }
-  return BH_OK;
+  return fail(BH_OUT_OF_MEMORY, "tree cell capacity kept overflowing");
 }
 
 int bh_sim_begin_step(bh_handle *h, double dt, void *stream) {
@@ -910,7 +1033,11 @@ int bh_stats_get(bh_handle *h, bh_stats *out, void *stream) {
   if (!h || !out) return fail(BH_BAD_ARG, "bh_stats_get: bad args");
   BH_TRY(read_flags(h, S(stream)));
   out->n_bodies = h->tree_n < 0 ? 0 : h->tree_n;
-  out->n_cells = h->C;
+  if (h->async_tree) {
+    int overflow = 0;
+    BH_TRY(async_readback(h, S(stream), &overflow));
+  }
+  out->n_cells = h->async_tree ? h->C_true : h->C;
   out->max_level = h->max_level;
   out->pp = (int64_t)h->hflags->pp;
   out->pc = (int64_t)h->hflags->pc;

@@ -7,6 +7,7 @@
 #include <stdint.h>
 
 #include <climits>
+#include <cooperative_groups.h>
 
 #include "bh_internal.cuh"
 
@@ -118,6 +119,8 @@ void launch_keys_clamped_f64(const double *pos, int stride, int64_t n, const dou
 }
 
 // ------------------------------------------------------------- tree build
+__device__ __forceinline__ int64_t tree_count(const TreeView &t) { return t.dC ? *t.dC : t.C; }
+
 __device__ __forceinline__ double4 ldcg4(const double4 *p) {
   const double2 *q = reinterpret_cast<const double2 *>(p);
   double2 a = __ldcg(q), b = __ldcg(q + 1);
@@ -223,7 +226,8 @@ __global__ void k_emit(TreeView t, const float4 *__restrict__ bod32,
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n = t.n;
   if (i >= n) return;
-  const int C = (int)t.C;
+  const int C = (int)tree_count(t);
+  if (C > t.C) return;  // sync-free build overflowed its capacity (flagged; redone)
   if (i == 0) {
     t.link[0] = make_int4(C, (int)n, 0, 0);
     t.parent[0] = -1;
@@ -432,6 +436,79 @@ __global__ void k_moments_level(TreeView t, const int *__restrict__ list, int be
   if (k < count) cell_moments(t, list[begin + k]);
 }
 
+// C = 1 + off[n-1] + newc[n-1] on device; flag an overflow of the capacity
+__global__ void k_set_count(const uint32_t *off, const uint32_t *newc, int64_t n, int64_t cap,
+                            int *dC, DeviceFlags *f) {
+  int64_t C = n > 0 ? 1 + (int64_t)off[n - 1] + newc[n - 1] : 1;
+  if (C > cap) atomicOr(&f->bits, FLAG_OVERFLOW);
+  dC[0] = (int)C;
+}
+void launch_set_count(const uint32_t *off, const uint32_t *newc, int64_t n, int64_t cap,
+                      int *dC, DeviceFlags *f, cudaStream_t s) {
+  k_set_count<<<1, 1, 0, s>>>(off, newc, n, cap, dC, f);
+}
+
+// One cooperative launch (all blocks co-resident): offsets from the device
+// level counts, bucket the internal cells by level, then sweep the levels
+// deepest-first with a grid-wide barrier between levels -- the same
+// cell_moments work as the per-level launches, without ~22 dependent launches.
+namespace cg = cooperative_groups;
+__global__ void __launch_bounds__(256) k_moments_coop(TreeView t, int *__restrict__ lvl,
+                                                     int *__restrict__ list) {
+  cg::grid_group grid = cg::this_grid();
+  const int64_t C = tree_count(t);
+  if (C > t.C) return;  // overflowed build (uniform across the grid): nothing valid
+  int *cnt = lvl, *offs = lvl + (kMaxLevel + 1), *cur = lvl + 2 * (kMaxLevel + 1);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    int acc = 0;
+    for (int l = 0; l <= kMaxLevel; ++l) {
+      offs[l] = acc;
+      cur[l] = 0;
+      acc += cnt[l];
+    }
+  }
+  grid.sync();
+  __shared__ int h[kMaxLevel + 1], base[kMaxLevel + 1];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t c0 = (int64_t)blockIdx.x * blockDim.x; c0 < C; c0 += stride) {
+    if (threadIdx.x <= kMaxLevel) h[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t c = c0 + threadIdx.x;
+    int l = -1, rank = 0;
+    if (c < C) {
+      const int4 L = t.link[c];
+      if (L.y > 1) {
+        l = L.w;
+        rank = atomicAdd(&h[l], 1);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x <= kMaxLevel && h[threadIdx.x])
+      base[threadIdx.x] = offs[threadIdx.x] + atomicAdd(&cur[threadIdx.x], h[threadIdx.x]);
+    __syncthreads();
+    if (l >= 0) list[base[l] + rank] = (int)c;
+    __syncthreads();
+  }
+  grid.sync();
+  for (int l = kMaxLevel; l >= 0; --l) {
+    const int n_l = cnt[l], b_l = offs[l];
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n_l; k += stride)
+      cell_moments(t, list[b_l + k]);
+    if (n_l > 0) grid.sync();
+  }
+}
+
+int launch_moments_coop(const TreeView &t, int *lvl, int *list, int sms, cudaStream_t s) {
+  if (t.n <= 1) return 0;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_moments_coop, 256, 0);
+  if (per_sm < 1) per_sm = 1;
+  dim3 grid(sms * per_sm), block(256);
+  TreeView tv = t;
+  void *args[] = {&tv, &lvl, &list};
+  return (int)cudaLaunchCooperativeKernel((void *)k_moments_coop, grid, block, args, 0, s);
+}
+
 void launch_moments(const TreeView &t, const LevelPlan &plan, int *cursor, int *list,
                     cudaStream_t s) {
   if (t.n <= 1) return;
@@ -449,7 +526,7 @@ __global__ void k_export(TreeView t, double R, uint64_t *key, int8_t *level, dou
                          double *side, double *mass, double *com, double *quad,
                          int64_t *count, int32_t *children) {
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= t.C) return;
+  if (c >= t.C || c >= tree_count(t)) return;
   int4 L = t.link[c];
   int l = L.w;
   uint64_t pref = 0;

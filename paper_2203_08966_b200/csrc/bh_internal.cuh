@@ -37,6 +37,7 @@ enum : int {
   FLAG_DUPLICATE = 2,
   FLAG_UNSORTED = 4,
   FLAG_DEPTH = 8,
+  FLAG_OVERFLOW = 16,  // sync-free build: more cells than the preallocated capacity
 };
 
 struct DeviceFlags {
@@ -102,7 +103,8 @@ struct LevelPlan {  // internal cells per level (host-known) and list offsets
 };
 struct TreeView {
   int64_t n = 0;       // bodies
-  int64_t C = 0;       // cells
+  int64_t C = 0;       // cells; with dC set: the allocated capacity (grid bound)
+  const int *dC = nullptr;  // sync-free build: the true cell count, on device
   const uint64_t *keys = nullptr;
   const int8_t *lcp = nullptr;
   const uint32_t *off = nullptr;   // exclusive scan of newc
@@ -119,6 +121,12 @@ void launch_emit(const TreeView &t, const float4 *bod32, const double4 *bod64, c
 // cursor: int[kMaxLevel+1] scratch; list: int[C]
 void launch_moments(const TreeView &t, const LevelPlan &plan, int *cursor, int *list,
                     cudaStream_t s);
+// Sync-free variant: C on device (launch_set_count), per-level counts on device
+// (lvl: counts[22] from k_lcp_new | offsets[22] | cursors[22]); one cooperative
+// launch sweeps the levels deepest-first with grid-wide barriers between them.
+void launch_set_count(const uint32_t *off, const uint32_t *newc, int64_t n, int64_t cap,
+                      int *dC, DeviceFlags *f, cudaStream_t s);
+int launch_moments_coop(const TreeView &t, int *lvl, int *list, int sms, cudaStream_t s);
 void launch_export(const TreeView &t, double R, uint64_t *key, int8_t *level, double *centre,
                    double *side, double *mass, double *com, double *quad, int64_t *count,
                    int32_t *children, cudaStream_t s);
@@ -142,12 +150,10 @@ struct __align__(16) WalkNode {
   float4 c;  // qxz, qyz, mass, qzz
   int4 d;    // first_child (internal) | lo (bucket/leaf), count, nchild, level
 };
-struct WalkTable {
-  float mac2[kMaxLevel + 1];
-};
-void launch_walk_tree(const TreeView &t, const WalkTable &tab, int leaf, uint32_t *smask,
-                      uint32_t *nck, uint32_t *base, void *scan_tmp, size_t scan_bytes,
-                      WalkNode *out, int *dCp, cudaStream_t s);
+// MAC threshold (side_l/theta)^2 per level is formed on device from R
+void launch_walk_tree(const TreeView &t, const double *dR, double theta, int leaf,
+                      uint32_t *smask, uint32_t *nck, uint32_t *base, void *scan_tmp,
+                      size_t scan_bytes, WalkNode *out, int *dCp, cudaStream_t s);
 void launch_walk_f32(const WalkNode *T, const float4 *bodies, const float *targets, int tstride,
                      const uint32_t *tperm, int nt, float e2, int leaf, float *acc, int astride,
                      int64_t *work64, int *work32, DeviceFlags *f, cudaStream_t s);

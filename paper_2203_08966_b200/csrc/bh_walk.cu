@@ -44,6 +44,8 @@
 
 namespace bh {
 
+__device__ __forceinline__ int64_t tree_count(const TreeView &t) { return t.dC ? *t.dC : t.C; }
+
 __device__ __forceinline__ int child_slot(const TreeView &t, int64_t c) {
   const int4 L = t.link[c];
   return (int)((t.keys[L.z] >> (3 * (kMortonBits - L.w))) & 7);
@@ -60,7 +62,7 @@ __device__ __forceinline__ bool expandable(const TreeView &t, int64_t c, int lea
 // slot masks of the expandable cells
 __global__ void k_slots(TreeView t, int leaf, uint32_t *__restrict__ smask) {
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c <= 0 || c >= t.C) return;
+  if (c <= 0 || c >= tree_count(t) || c >= t.C) return;
   const int P = t.parent[c];
   if (expandable(t, P, leaf)) atomicOr(&smask[P], 1u << child_slot(t, c));
 }
@@ -70,16 +72,21 @@ __global__ void k_nchild(TreeView t, int leaf, const uint32_t *__restrict__ smas
                          uint32_t *__restrict__ nck) {
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= t.C) return;
+  if (c >= tree_count(t)) {  // capacity tail (sync-free build): scans as zero
+    nck[c] = 0u;
+    return;
+  }
   const bool kept = c == 0 || expandable(t, t.parent[c], leaf);
   nck[c] = (kept && expandable(t, c, leaf)) ? (uint32_t)__popc(smask[c]) : 0u;
 }
 
-__global__ void k_compact(TreeView t, WalkTable tab, int leaf, const uint32_t *__restrict__ smask,
-                          const uint32_t *__restrict__ nck, const uint32_t *__restrict__ base,
-                          WalkNode *__restrict__ out, int *__restrict__ dCp) {
+__global__ void k_compact(TreeView t, const double *__restrict__ dR, double theta, int leaf,
+                          const uint32_t *__restrict__ smask, const uint32_t *__restrict__ nck,
+                          const uint32_t *__restrict__ base, WalkNode *__restrict__ out,
+                          int *__restrict__ dCp) {
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t C = t.C;
-  if (c >= C) return;
+  const int64_t C = tree_count(t);
+  if (c >= C || c >= t.C) return;
   if (c == C - 1) *dCp = (int)(1 + base[C - 1] + nck[C - 1]);
   int j = 0;
   if (c > 0) {
@@ -92,7 +99,8 @@ __global__ void k_compact(TreeView t, WalkTable tab, int leaf, const uint32_t *_
   const double4 cm = t.cm64[c];
   WalkNode nd;
   // negated com: the walk forms d = p - com as p + a (one FADD2 per axis)
-  nd.a = make_float4(-(float)cm.x, -(float)cm.y, -(float)cm.z, tab.mac2[L.w]);
+  const double r = ldexp(2.0 * dR[0], -L.w) / theta;  // theta == 0 -> inf: never accept
+  nd.a = make_float4(-(float)cm.x, -(float)cm.y, -(float)cm.z, (float)(r * r));
   float q0 = 0.f, q1 = 0.f, q2 = 0.f, q3 = 0.f, q4 = 0.f, q5 = 0.f;
   if (L.y > 1) {
     const double *q = t.q64 + 6 * c;
@@ -106,25 +114,28 @@ __global__ void k_compact(TreeView t, WalkTable tab, int leaf, const uint32_t *_
   out[j] = nd;
 }
 
-void launch_walk_tree(const TreeView &t, const WalkTable &tab, int leaf, uint32_t *smask,
-                      uint32_t *nck, uint32_t *base, void *scan_tmp, size_t scan_bytes,
-                      WalkNode *out, int *dCp, cudaStream_t s) {
+void launch_walk_tree(const TreeView &t, const double *dR, double theta, int leaf,
+                      uint32_t *smask, uint32_t *nck, uint32_t *base, void *scan_tmp,
+                      size_t scan_bytes, WalkNode *out, int *dCp, cudaStream_t s) {
   const int g = grid_for(t.C, 256);
   cudaMemsetAsync(smask, 0, sizeof(uint32_t) * t.C, s);
   k_slots<<<g, 256, 0, s>>>(t, leaf, smask);
   k_nchild<<<g, 256, 0, s>>>(t, leaf, smask, nck);
   exclusive_scan_u32(scan_tmp, scan_bytes, nck, base, t.C, s);
-  k_compact<<<g, 256, 0, s>>>(t, tab, leaf, smask, nck, base, out, dCp);
+  k_compact<<<g, 256, 0, s>>>(t, dR, theta, leaf, smask, nck, base, out, dCp);
 }
 
 __device__ __forceinline__ float2 f2(float x, float y) { return make_float2(x, y); }
 __device__ __forceinline__ float2 f2(float x) { return make_float2(x, x); }
 
 constexpr int kWalkBlock = 256;
+#ifndef BH_WALK_MINB
+#define BH_WALK_MINB 4  // blocks/SM the register budget must allow (4 -> <= 64 regs)
+#endif
 constexpr int kStack = 8 * (kMaxLevel + 1) + 8;  // <= 8 pending siblings per level
 
 template <bool BUCKET>
-__global__ void __launch_bounds__(kWalkBlock) k_walk(
+__global__ void __launch_bounds__(kWalkBlock, BH_WALK_MINB) k_walk(
     const WalkNode *__restrict__ T, const float4 *__restrict__ bodies,
     const float *__restrict__ targets, int tstride, const uint32_t *__restrict__ tperm, int nt,
     float e2, int leaf, float *__restrict__ acc, int astride, int64_t *__restrict__ work64,

@@ -224,6 +224,8 @@ class DistributedSim:
             self.eng.sim_begin_step(self.p.dt)
             self._forces(record_work=True, bounds_ready=True)
             self.eng.sim_end_step(self.p.dt)
+            if hasattr(self.eng, "check"):
+                self.eng.check()  # latched device errors (incl. tree-capacity overflow)
 
     def store(self, pos=None, vel=None, acc=None, work=None) -> None:
         self.eng.sim_store(pos, vel, acc, work)
