@@ -168,11 +168,19 @@ def run_ours(args, cfg) -> dict | None:
     vel = eng.vec_tensor(b.velocity)
     theta, eps, leaf, dt = cfg["theta"], cfg["eps"], cfg["leaf"], cfg["dt"]
     sim = None
-    if ws > 1:  # replicated tree, costzones-partitioned walk, NCCL exchange
+    if ws > 1 and args.decomp == "replicated":  # replicated tree, partitioned walk
         from paper_2203_08966_b200.decomposition import DistributedSim, StepParams, TorchComm
 
         sim = DistributedSim(eng, TorchComm(), StepParams(theta, eps, leaf, dt))
         sim.load(pos, vel)
+        sim.bootstrap()
+    elif ws > 1:  # key-range decomposition, distributed build
+        from paper_2203_08966_b200.decomposition import DistributedBuildSim, StepParams, TorchComm
+
+        sim = DistributedBuildSim(eng, TorchComm(), StepParams(theta, eps, leaf, dt))
+        lo, hi = n * rank // ws, n * (rank + 1) // ws  # initial chunk (simulation.py:190-198)
+        sim.load(pos[lo:hi].contiguous(), vel[lo:hi].contiguous(),
+                 gid=torch.arange(lo, hi, device=dev))
         sim.bootstrap()
     else:
         eng.sim_load(pos, vel)
@@ -226,10 +234,19 @@ def run_ours(args, cfg) -> dict | None:
     dpos = _t.empty((n, 4), dtype=_t.float32, device=dev)
     dvel = _t.empty_like(dpos)
     dacc = _t.empty_like(dpos)
-    eng.sim_store(dpos, dvel, dacc)
-    hpos.copy_(dpos)
-    hvel.copy_(dvel)
-    hacc.copy_(dacc)
+    distributed = ws > 1 and args.decomp == "distributed"
+    if distributed:  # this rank's bodies only
+        p_, v_, a_, w_, g_ = sim.store()
+        nl = p_.shape[0]
+        dpos, dvel, dacc = p_.clone(), v_.clone(), a_.clone()
+        dwork, dgid = w_.to(_t.int32).clone(), g_.clone()
+        hpos, hvel, hacc = (x.cpu().pin_memory() for x in (dpos, dvel, dacc))
+        hwork, hgid = dwork.cpu().pin_memory(), dgid.cpu().pin_memory()
+    else:
+        eng.sim_store(dpos, dvel, dacc)
+        hpos.copy_(dpos)
+        hvel.copy_(dvel)
+        hacc.copy_(dacc)
     torch.cuda.synchronize()
     e2e_ms = 0.0
     e2e_inter = 0
@@ -239,19 +256,26 @@ def run_ours(args, cfg) -> dict | None:
             dist.barrier()
         torch.cuda.synchronize()
         ev0.record()
-        dpos.copy_(hpos, non_blocking=True)
-        dvel.copy_(hvel, non_blocking=True)
-        dacc.copy_(hacc, non_blocking=True)
-        if sim is not None:
-            eng.sim_load(dpos, dvel, acc=dacc)
+        if distributed:
+            dpos, dvel, dacc = (x.to(dev, non_blocking=True) for x in (hpos, hvel, hacc))
+            sim.upload(dpos, dvel, dacc, hwork.to(dev, non_blocking=True), hgid.to(dev, non_blocking=True))
             sim.step(1)
+            p_, v_, a_, w_, g_ = sim.store()
+            hpos, hvel, hacc = (x.to("cpu", non_blocking=True) for x in (p_, v_, a_))
+            hwork, hgid = w_.to(_t.int32).to("cpu", non_blocking=True), g_.to("cpu", non_blocking=True)
         else:
+            dpos.copy_(hpos, non_blocking=True)
+            dvel.copy_(hvel, non_blocking=True)
+            dacc.copy_(hacc, non_blocking=True)
             eng.sim_load(dpos, dvel, acc=dacc)
-            eng.sim_step(dt, theta, eps, leaf, 1)
-        eng.sim_store(dpos, dvel, dacc)
-        hpos.copy_(dpos, non_blocking=True)
-        hvel.copy_(dvel, non_blocking=True)
-        hacc.copy_(dacc, non_blocking=True)
+            if sim is not None:
+                sim.step(1)
+            else:
+                eng.sim_step(dt, theta, eps, leaf, 1)
+            eng.sim_store(dpos, dvel, dacc)
+            hpos.copy_(dpos, non_blocking=True)
+            hvel.copy_(dvel, non_blocking=True)
+            hacc.copy_(dacc, non_blocking=True)
         ev1.record()
         torch.cuda.synchronize()
         e2e_ms += ev0.elapsed_time(ev1)
@@ -301,8 +325,11 @@ def run_ours(args, cfg) -> dict | None:
             "data": "synthetic: reference plummer_cluster sampler (bit-identical restatement), seed %d" % cfg["seed"],
             "config": {"workload": args.config, "n_bodies": n, "theta": theta, "eps": eps,
                        "leaf_size": leaf, "dt": dt, "precision": "fp32",
-                       "parallelism": (f"{ws} ranks: replicated tree, costzones-partitioned walk, "
-                                       "NCCL all-reduce of zone accelerations") if ws > 1 else "single GPU",
+                       "parallelism": ((f"{ws} ranks: costzones key ranges, body migration, "
+                                        "distributed build, branch-node + walk-record allgather")
+                                       if args.decomp == "distributed" else
+                                       (f"{ws} ranks: replicated tree, costzones-partitioned walk, "
+                                        "NCCL all-reduce of zone accelerations")) if ws > 1 else "single GPU",
                        "l2": "flushed between timed steps (256 MB write)"},
             "interactions_per_step": inter_all / args.steps,
             "pp_per_step": pp / args.steps,
@@ -445,6 +472,9 @@ def main() -> None:
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="cfg2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--decomp", choices=["distributed", "replicated"], default="distributed",
+                    help="multi-GPU scheme (N>1): key-range decomposition with a distributed "
+                         "build, or replicated tree with a partitioned walk")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: W < 3 violates the timing rules; using 3", file=sys.stderr)

@@ -172,10 +172,33 @@ int bh_sim_end_step(bh_handle *h, double dt, void *stream);
  * BH_SIM_POS (export only), BH_SIM_WORK (int32, this pass), BH_SIM_PREV_WORK
  * (export only: the previous pass's work of each sorted body -- the costzones
  * input, decomposition.py:35-57). */
-enum { BH_SIM_ACC = 0, BH_SIM_WORK = 1, BH_SIM_PREV_WORK = 2, BH_SIM_POS = 3 };
+enum { BH_SIM_ACC = 0, BH_SIM_WORK = 1, BH_SIM_PREV_WORK = 2, BH_SIM_POS = 3, BH_SIM_VEL = 4,
+       BH_SIM_ID = 5, BH_SIM_KEYS = 6 };
 int bh_sim_export(bh_handle *h, int what, int64_t begin, int64_t end, void *d_dst, void *stream);
 int bh_sim_import(bh_handle *h, int what, int64_t begin, int64_t end, const void *d_src,
                   void *stream);
+
+/* ---- distributed build: one rank of a key-range decomposition -----------
+ * (decomposition.py:35-263 costzones/migration, hashed.py:539-824 branch nodes)
+ *   local_maxabs -> allreduce max -> set_R          (simulation.py:201-208)
+ *   sort (keys with R) -> migrate bodies by splitter keys -> load_state -> sort
+ *   build_local: the rank's tree with global leaf depths (neighbour boundary
+ *     keys), shared cells marked, walk records with every branch node present
+ *   branch_export / walk_records: the payloads allgathered between ranks
+ *   walk_records_f32: walk own targets over the assembled global walk tree. */
+int bh_sim_local_maxabs(bh_handle *h, double *out, void *stream);
+int bh_sim_set_R(bh_handle *h, double R, void *stream);
+int bh_sim_sort(bh_handle *h, void *stream);
+int bh_sim_load_state(bh_handle *h, const void *d_pos, const void *d_vel, const void *d_acc,
+                      const int32_t *d_work, int64_t n, void *stream);
+int bh_sim_build_local(bh_handle *h, double theta, int leaf_size, int has_prev, uint64_t prev_key,
+                       int has_next, uint64_t next_key, int64_t *nbranch, void *stream);
+int bh_sim_branch_export(bh_handle *h, uint64_t *d_key, int32_t *d_level, int64_t *d_count,
+                         double *d_mom10, int32_t *d_rec, int32_t *d_lo, void *stream);
+int bh_sim_walk_records(bh_handle *h, void *d_out, int64_t *n_out, void *stream);
+int bh_walk_records_f32(bh_handle *h, const void *d_records, int64_t nrec, const float *d_bodies4,
+                        const float *d_targets4, int64_t nt, double eps, int leaf_size,
+                        float *d_acc4, int32_t *d_work, void *stream);
 int bh_stats_get(bh_handle *h, bh_stats *out, void *stream);
 
 /* ---- instrumentation ----------------------------------------------------- */

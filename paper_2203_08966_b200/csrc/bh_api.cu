@@ -70,6 +70,10 @@ struct bh_handle {
   int *hstat = nullptr;  // pinned: [0] = C, [1..22] = internal cells per level
   int grid_lvl[kMaxLevel + 1] = {0};
   Buf bk_pos, bk_vel, bk_acc, bk_id, bk_work;
+  // distributed build (decomposition.py): boundary lcps, shared cells, branches
+  int bnd_prev = -1, bnd_next = -1;
+  Buf shared, branch, rec_of_cell;
+  int64_t nbranch = 0;
   double R = 1.0;
   Buf link, parent, child8, lvl, lvl_list, cm64, q64, tbod;
   int *hlvl = nullptr;  // pinned: internal cells per level of the last build
@@ -132,6 +136,8 @@ struct bh_handle {
     t.n = tree_n;
     t.C = C;
     t.dC = async_tree ? dCtrue : nullptr;
+    t.bnd_prev = bnd_prev;
+    t.bnd_next = bnd_next;
     t.keys = keys2.as<uint64_t>();
     t.lcp = lcp.as<int8_t>();
     t.off = off.as<uint32_t>();
@@ -210,7 +216,7 @@ int build_sorted(bh_handle *h, int64_t n, const float4 *bod32, const double4 *bo
   if (n > 0) {
     BH_CUDA(h->lvl.ensure(sizeof(int) * 4 * (kMaxLevel + 2)));
     launch_lcp_new(h->keys2.as<uint64_t>(), n, h->lcp.as<int8_t>(), h->newc.as<uint32_t>(),
-                   h->flags, h->lvl.as<int>(), allow_dup, s);
+                   h->flags, h->lvl.as<int>(), allow_dup, s, h->bnd_prev, h->bnd_next);
     BH_CUDA(exclusive_scan_u32(h->scan_tmp.p, h->scan_tmp.bytes, h->newc.as<uint32_t>(),
                                h->off.as<uint32_t>(), n, s));
     BH_LAUNCHED();
@@ -471,6 +477,45 @@ int sim_prepare(bh_handle *h, double theta, double eps, int leaf, bool bounds_re
     h->tend(s);
   }
   h->launches += 6;  // finish_R, keys, gather, lcp_new, emit, level scatter (+ per-level)
+  return BH_OK;
+}
+
+// keys (with the R already in dR), stable sort, permutation -- no build
+int sim_sort(bh_handle *h, cudaStream_t s) {
+  const int64_t n = h->sim_n;
+  const bool f32 = h->precision == BH_FP32;
+  BH_TRY(ensure_sort(h, n));
+  if (n == 0) return BH_OK;
+  if (f32)
+    launch_keys_f32(h->pos.as<float4>(), n, h->dR, h->keys.as<uint64_t>(), h->vals.as<uint32_t>(),
+                    h->flags, s);
+  else
+    launch_keys_f64(h->pos.as<double>(), 4, n, h->dR, h->keys.as<uint64_t>(),
+                    h->vals.as<uint32_t>(), h->flags, s);
+  BH_TRY(sort_keys(h, n, s));
+  if (f32)
+    launch_gather_f32(h->vals2.as<uint32_t>(), n, h->pos.as<float4>(), h->pos2.as<float4>(),
+                      h->vel.as<float4>(), h->vel2.as<float4>(), h->id.as<uint32_t>(),
+                      h->id2.as<uint32_t>(), s);
+  else
+    launch_gather_f64(h->vals2.as<uint32_t>(), n, h->pos.as<double4>(), h->pos2.as<double4>(),
+                      h->vel.as<double4>(), h->vel2.as<double4>(), h->id.as<uint32_t>(),
+                      h->id2.as<uint32_t>(), s);
+  std::swap(h->pos, h->pos2);
+  std::swap(h->vel, h->vel2);
+  std::swap(h->id, h->id2);
+  // acc follows its body too (a migrated state's kick needs it)
+  if (f32) {
+    launch_gather_f32(h->vals2.as<uint32_t>(), n, h->acc.as<float4>(), h->pos2.as<float4>(),
+                      nullptr, nullptr, nullptr, nullptr, s);
+    BH_CUDA(cudaMemcpyAsync(h->acc.p, h->pos2.p, sizeof(float4) * n, cudaMemcpyDeviceToDevice, s));
+  } else {
+    launch_gather_f64(h->vals2.as<uint32_t>(), n, h->acc.as<double4>(), h->pos2.as<double4>(),
+                      nullptr, nullptr, nullptr, nullptr, s);
+    BH_CUDA(cudaMemcpyAsync(h->acc.p, h->pos2.p, sizeof(double4) * n, cudaMemcpyDeviceToDevice, s));
+  }
+  h->launches += 4;
+  BH_LAUNCHED();
   return BH_OK;
 }
 
@@ -957,6 +1002,130 @@ __global__ void k_gather_work(const int *wo, const uint32_t *id, int64_t b, int6
   if (i < e) dst[i - b] = wo[id[i]];
 }
 
+// ------------------------------------------------ distributed build entry points
+int bh_sim_local_maxabs(bh_handle *h, double *out, void *stream) {
+  if (!h || !out) return fail(BH_BAD_ARG, "bh_sim_local_maxabs: bad args");
+  BH_TRY(read_flags(h, S(stream)));
+  union { unsigned u; float f; } v;
+  v.u = h->hflags->maxabs_bits;
+  *out = h->precision == BH_FP32 ? (double)v.f : h->hflags->maxabs64;
+  return BH_OK;
+}
+
+int bh_sim_set_R(bh_handle *h, double R, void *stream) {
+  if (!h || !(R > 0.0)) return fail(BH_BAD_ARG, "bh_sim_set_R: bad args");
+  *h->hR = R;
+  BH_CUDA(cudaMemcpyAsync(h->dR, h->hR, sizeof(double), cudaMemcpyHostToDevice, S(stream)));
+  BH_CUDA(cudaStreamSynchronize(S(stream)));
+  return BH_OK;
+}
+
+int bh_sim_sort(bh_handle *h, void *stream) {
+  if (!h) return fail(BH_BAD_ARG, "bh_sim_sort: bad args");
+  return sim_sort(h, S(stream));
+}
+
+int bh_sim_load_state(bh_handle *h, const void *d_pos, const void *d_vel, const void *d_acc,
+                      const int32_t *d_work, int64_t n, void *stream) {
+  BH_TRY(bh_sim_load(h, d_pos, d_vel, nullptr, d_acc, n, stream));
+  if (n > 0 && d_work)
+    BH_CUDA(cudaMemcpyAsync(h->work_orig.p, d_work, sizeof(int) * n, cudaMemcpyDeviceToDevice,
+                            S(stream)));
+  return BH_OK;
+}
+
+// Build this rank's tree over its (sorted) key range, with leaf depths made
+// global by the neighbour ranks' boundary keys; mark the shared cells; build the
+// walk tree (shared cells always expanded, so every branch node has a record);
+// return the number of branch nodes.  fp32 handles.  Synchronises.
+int bh_sim_build_local(bh_handle *h, double theta, int leaf_size, int has_prev, uint64_t prev_key,
+                       int has_next, uint64_t next_key, int64_t *nbranch, void *stream) {
+  if (!h || !nbranch) return fail(BH_BAD_ARG, "bh_sim_build_local: bad args");
+  if (h->precision != BH_FP32) return fail(BH_BAD_ARG, "distributed build is fp32");
+  cudaStream_t s = S(stream);
+  const int64_t n = h->sim_n;
+  if (n == 0) { *nbranch = 0; return BH_OK; }
+  uint64_t kfirst = 0, klast = 0;
+  BH_CUDA(cudaMemcpyAsync(&kfirst, h->keys2.p, 8, cudaMemcpyDeviceToHost, s));
+  BH_CUDA(cudaMemcpyAsync(&klast, h->keys2.as<uint64_t>() + (n - 1), 8, cudaMemcpyDeviceToHost, s));
+  BH_CUDA(cudaStreamSynchronize(s));
+  auto lcp_host = [](uint64_t a, uint64_t b) {
+    uint64_t x = a ^ b;
+    int bits = x ? 64 - __builtin_clzll(x) : 0;
+    return kMortonBits - (bits + 2) / 3;
+  };
+  h->bnd_prev = has_prev ? lcp_host(prev_key, kfirst) : -1;
+  h->bnd_next = has_next ? lcp_host(klast, next_key) : -1;
+  const int allow_dup = h->allow_dup || leaf_size > 1;
+  int rc = build_sorted(h, n, h->pos.as<float4>(), nullptr, s, allow_dup);
+  if (rc != BH_OK) { h->bnd_prev = h->bnd_next = -1; return rc; }
+  const int64_t C = h->C;
+  BH_CUDA(h->shared.ensure(C + 16));
+  BH_CUDA(h->branch.ensure(sizeof(int) * (8 * (2 * kMaxLevel + 2) + 8)));
+  BH_CUDA(h->rec_of_cell.ensure(sizeof(int) * C));
+  TreeView t = h->view();
+  launch_mark_shared(t, h->shared.as<uint8_t>(), h->branch.as<int>() + 1, h->branch.as<int>(), s);
+  BH_CUDA(h->smask.ensure(sizeof(uint32_t) * C));
+  BH_CUDA(h->nck.ensure(sizeof(uint32_t) * C));
+  BH_CUDA(h->wbase.ensure(sizeof(uint32_t) * C));
+  BH_CUDA(h->wnodes.ensure(sizeof(WalkNode) * C));
+  BH_CUDA(h->wscan_tmp.ensure(scan_temp_bytes(C) + 16));
+  launch_walk_tree(t, h->dR, theta, leaf_size, h->smask.as<uint32_t>(), h->nck.as<uint32_t>(),
+                   h->wbase.as<uint32_t>(), h->wscan_tmp.p, h->wscan_tmp.bytes,
+                   h->wnodes.as<WalkNode>(), h->dCp, s, h->shared.as<uint8_t>(),
+                   h->rec_of_cell.as<int>());
+  h->walk_valid = false;  // a forced-shared walk tree is not the local-walk tree
+  int nb = 0;
+  BH_CUDA(cudaMemcpyAsync(&nb, h->branch.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  BH_CUDA(cudaStreamSynchronize(s));
+  BH_LAUNCHED();
+  h->nbranch = nb;
+  *nbranch = nb;
+  h->bnd_prev = h->bnd_next = -1;
+  return BH_OK;
+}
+
+int bh_sim_branch_export(bh_handle *h, uint64_t *d_key, int32_t *d_level, int64_t *d_count,
+                         double *d_mom10, int32_t *d_rec, int32_t *d_lo, void *stream) {
+  if (!h) return fail(BH_BAD_ARG, "bh_sim_branch_export: bad args");
+  TreeView t = h->view();
+  launch_branch_export(t, h->branch.as<int>() + 1, (int)h->nbranch, h->rec_of_cell.as<int>(), d_key,
+                       d_level, d_count, d_mom10, d_rec, d_lo, S(stream));
+  BH_LAUNCHED();
+  return BH_OK;
+}
+
+// Copy the walk records of the last bh_sim_build_local (d_out may be NULL to
+// query the count).  Synchronises.
+int bh_sim_walk_records(bh_handle *h, void *d_out, int64_t *n_out, void *stream) {
+  if (!h || !n_out) return fail(BH_BAD_ARG, "bh_sim_walk_records: bad args");
+  cudaStream_t s = S(stream);
+  int cp = 0;
+  BH_CUDA(cudaMemcpyAsync(&cp, h->dCp, sizeof(int), cudaMemcpyDeviceToHost, s));
+  BH_CUDA(cudaStreamSynchronize(s));
+  *n_out = cp;
+  if (d_out && cp > 0)
+    BH_CUDA(cudaMemcpyAsync(d_out, h->wnodes.p, sizeof(WalkNode) * cp, cudaMemcpyDeviceToDevice, s));
+  return BH_OK;
+}
+
+// The fp32 walk over a caller-assembled record array (layout of WalkNode in
+// bh_walk.cu; record 0 is the root) and a caller body array (bucket bodies).
+int bh_walk_records_f32(bh_handle *h, const void *d_records, int64_t nrec, const float *d_bodies4,
+                        const float *d_targets4, int64_t nt, double eps, int leaf_size,
+                        float *d_acc4, int32_t *d_work, void *stream) {
+  if (!h || nrec <= 0 || !d_records || nt < 0 || (nt && (!d_targets4 || !d_acc4)))
+    return fail(BH_BAD_ARG, "bh_walk_records_f32: bad args");
+  cudaStream_t s = S(stream);
+  BH_TRY(reset_counters(h, s));
+  launch_walk_f32(static_cast<const WalkNode *>(d_records), reinterpret_cast<const float4 *>(d_bodies4),
+                  d_targets4, 4, nullptr, (int)nt, (float)(eps * eps), leaf_size, d_acc4, 4, nullptr,
+                  d_work, h->flags, s);
+  h->launches += 1;
+  BH_LAUNCHED();
+  return BH_OK;
+}
+
 int bh_sim_export(bh_handle *h, int what, int64_t begin, int64_t end, void *dst, void *stream) {
   if (!h || !dst || begin < 0 || end > h->sim_n || begin > end)
     return fail(BH_BAD_ARG, "bh_sim_export: bad args");
@@ -979,6 +1148,17 @@ int bh_sim_export(bh_handle *h, int what, int64_t begin, int64_t end, void *dst,
       k_gather_work<<<grid_for(k, 256), 256, 0, s>>>(h->work_orig.as<int>(), h->id.as<uint32_t>(),
                                                      begin, end, static_cast<int *>(dst));
       BH_LAUNCHED();
+      break;
+    case BH_SIM_VEL:
+      BH_CUDA(cudaMemcpyAsync(dst, h->vel.as<char>() + e4 * begin, e4 * k, cudaMemcpyDeviceToDevice, s));
+      break;
+    case BH_SIM_ID:
+      BH_CUDA(cudaMemcpyAsync(dst, h->id.as<uint32_t>() + begin, sizeof(uint32_t) * k,
+                              cudaMemcpyDeviceToDevice, s));
+      break;
+    case BH_SIM_KEYS:
+      BH_CUDA(cudaMemcpyAsync(dst, h->keys2.as<uint64_t>() + begin, sizeof(uint64_t) * k,
+                              cudaMemcpyDeviceToDevice, s));
       break;
     default:
       return fail(BH_BAD_ARG, "bh_sim_export: unknown array");

@@ -143,9 +143,14 @@ __device__ __forceinline__ int lcp_of(uint64_t a, uint64_t b) {
 // keys cannot be separated; they share one level-21 cell (count = run length)
 // that is never opened and is resolved body by body.  The reference raises
 // instead (hashed.py:477-482), which is what allow_dup = 0 reproduces.
+// bnd_prev / bnd_next (>= 0 on a rank of a distributed build): shared octant
+// levels of the first / last local key with the neighbouring rank's last / first
+// key, so leaves sit at their global depth (the reference inserts the
+// neighbour bodies for the same purpose, hashed.py:539-602).
 __global__ void k_lcp_new(const uint64_t *__restrict__ keys, int64_t n,
                           int8_t *__restrict__ lcp, uint32_t *__restrict__ newc,
-                          DeviceFlags *f, int *__restrict__ lvl_cnt, int allow_dup) {
+                          DeviceFlags *f, int *__restrict__ lvl_cnt, int allow_dup,
+                          int bnd_prev, int bnd_next) {
   __shared__ int h[kMaxLevel + 2];
   if (threadIdx.x <= kMaxLevel + 1) h[threadIdx.x] = 0;
   __syncthreads();
@@ -166,9 +171,12 @@ __global__ void k_lcp_new(const uint64_t *__restrict__ keys, int64_t n,
     if (allow_dup) depth = kMaxLevel;
     else atomicOr(&f->bits, FLAG_DEPTH);
   }
+  const int depth_local = depth;  // cells above it hold >= 2 local bodies
+  if (i == 0 && bnd_prev >= 0) depth = max(depth, min(bnd_prev + 1, kMaxLevel));
+  if (i == n - 1 && bnd_next >= 0) depth = max(depth, min(bnd_next + 1, kMaxLevel));
   int start = i > 0 ? lp : 0;
   newc[i] = (uint32_t)(depth - start);
-  for (int l = start + 1; l < depth && l <= kMaxLevel; ++l) atomicAdd(&h[l], 1);
+  for (int l = start + 1; l < depth_local && l <= kMaxLevel; ++l) atomicAdd(&h[l], 1);
   if (ln == kMaxLevel && lp < kMaxLevel) atomicAdd(&h[kMaxLevel], 1);  // duplicate-run cell
   }
   __syncthreads();
@@ -178,10 +186,12 @@ __global__ void k_lcp_new(const uint64_t *__restrict__ keys, int64_t n,
 }
 
 void launch_lcp_new(const uint64_t *keys, int64_t n, int8_t *lcp, uint32_t *newc,
-                    DeviceFlags *f, int *lvl_cnt, int allow_dup, cudaStream_t s) {
+                    DeviceFlags *f, int *lvl_cnt, int allow_dup, cudaStream_t s, int bnd_prev,
+                    int bnd_next) {
   if (n <= 0) return;
   cudaMemsetAsync(lvl_cnt, 0, sizeof(int) * (kMaxLevel + 1), s);
-  k_lcp_new<<<grid_for(n, 256), 256, 0, s>>>(keys, n, lcp, newc, f, lvl_cnt, allow_dup);
+  k_lcp_new<<<grid_for(n, 256), 256, 0, s>>>(keys, n, lcp, newc, f, lvl_cnt, allow_dup, bnd_prev,
+                                             bnd_next);
 }
 
 // first b > i whose level-l prefix differs from body i's (n if none):
@@ -231,7 +241,7 @@ __global__ void k_emit(TreeView t, const float4 *__restrict__ bod32,
   if (i == 0) {
     t.link[0] = make_int4(C, (int)n, 0, 0);
     t.parent[0] = -1;
-    if (n == 1) {  // hashed.py:464-474: the root is the leaf
+    if (n == 1 && t.bnd_prev < 0 && t.bnd_next < 0) {  // hashed.py:464-474: root = leaf
       double4 b;
       if (bod64) {
         b = bod64[0];
@@ -246,7 +256,9 @@ __global__ void k_emit(TreeView t, const float4 *__restrict__ bod32,
   const uint64_t k = t.keys[i];
   const int lp = i > 0 ? t.lcp[i - 1] : -1;
   const int ln = i + 1 < n ? t.lcp[i] : -1;
-  const int depth = min((lp > ln ? lp : ln) + 1, kMaxLevel);  // clamp: duplicate keys
+  int depth = min((lp > ln ? lp : ln) + 1, kMaxLevel);  // clamp: duplicate keys
+  if (i == 0 && t.bnd_prev >= 0) depth = max(depth, min(t.bnd_prev + 1, kMaxLevel));
+  if (i == n - 1 && t.bnd_next >= 0) depth = max(depth, min(t.bnd_next + 1, kMaxLevel));
   const int start = i > 0 ? lp : 0;
   const int base = 1 + (int)t.off[i];
   int par = 0;
@@ -568,6 +580,92 @@ void launch_export(const TreeView &t, double R, uint64_t *key, int8_t *level, do
   if (t.C <= 0) return;
   k_export<<<grid_for(t.C, 256), 256, 0, s>>>(t, R, key, level, centre, side, mass, com, quad,
                                               count, children);
+}
+
+// ------------------------------------------- distributed build (one rank)
+// Shared cells of a rank's local tree: the root and the cells on the first /
+// last local body's path down to the levels it shares with the neighbouring
+// rank's boundary key.  Their counts and moments are partial (the neighbour
+// holds bodies in them); every other cell holds only this rank's bodies and is
+// exactly the global tree's cell.  Branch nodes (hashed.py:609-630) are the
+// unshared children of shared cells -- or the root when there is no neighbour.
+__global__ void k_mark_shared(TreeView t, uint8_t *__restrict__ shared, int *__restrict__ branch,
+                              int *__restrict__ nbranch) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  int nb = 0;
+  if (t.bnd_prev < 0 && t.bnd_next < 0) {  // no neighbour: the root is the branch
+    branch[nb++] = 0;
+    *nbranch = nb;
+    return;
+  }
+  int list[2 * kMaxLevel + 2];
+  int ns = 0;
+  shared[0] = 1;
+  list[ns++] = 0;
+  for (int side = 0; side < 2; ++side) {
+    const int bnd = side == 0 ? t.bnd_prev : t.bnd_next;
+    if (bnd < 0) continue;
+    const uint64_t k = t.keys[side == 0 ? 0 : t.n - 1];
+    int cur = 0;
+    for (int l = 1; l <= bnd && l <= kMaxLevel; ++l) {
+      const int c = t.child8[8 * (int64_t)cur + (int)((k >> (3 * (kMortonBits - l))) & 7)];
+      if (c < 0) break;
+      if (!shared[c]) {
+        shared[c] = 1;
+        list[ns++] = c;
+      }
+      cur = c;
+    }
+  }
+  // branch nodes: unshared children of shared cells (shared cells in pre-order)
+  for (int a = 1; a < ns; ++a)  // insertion sort of the <= 43 shared cells
+    for (int b = a; b > 0 && list[b - 1] > list[b]; --b) {
+      int tmp = list[b]; list[b] = list[b - 1]; list[b - 1] = tmp;
+    }
+  for (int q = 0; q < ns; ++q) {
+    const int c = list[q];
+    for (int s = 0; s < 8; ++s) {
+      const int ch = t.child8[8 * (int64_t)c + s];
+      if (ch >= 0 && !shared[ch]) branch[nb++] = ch;
+    }
+  }
+  *nbranch = nb;
+}
+
+void launch_mark_shared(const TreeView &t, uint8_t *shared, int *branch, int *nbranch,
+                        cudaStream_t s) {
+  cudaMemsetAsync(shared, 0, t.C, s);
+  k_mark_shared<<<1, 32, 0, s>>>(t, shared, branch, nbranch);
+}
+
+// One row per branch node: cell key, level, count, exact fp64 moments, and its
+// walk record index (rec_of_cell) -- the payload of the branch-node allgather
+// (hashed.py:633-639).
+__global__ void k_branch_export(TreeView t, const int *__restrict__ branch, int nb,
+                                const int *__restrict__ rec_of_cell, uint64_t *key, int *level,
+                                int64_t *count, double *mom /* [nb][10] */, int *rec, int *lo) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nb) return;
+  const int c = branch[k];
+  const int4 L = t.link[c];
+  const uint64_t pref = t.keys[L.z] >> (3 * (kMortonBits - L.w));
+  key[k] = c == 0 ? 1ull : (pref | (1ull << (3 * L.w)));
+  level[k] = L.w;
+  count[k] = L.y;
+  const double4 cm = t.cm64[c];
+  double *m = mom + 10 * (int64_t)k;
+  m[0] = cm.w; m[1] = cm.x; m[2] = cm.y; m[3] = cm.z;
+  for (int q = 0; q < 6; ++q) m[4 + q] = L.y > 1 ? t.q64[6 * (int64_t)c + q] : 0.0;
+  rec[k] = rec_of_cell ? rec_of_cell[c] : -1;
+  if (lo) lo[k] = L.z;
+}
+
+void launch_branch_export(const TreeView &t, const int *branch, int nb, const int *rec_of_cell,
+                          uint64_t *key, int *level, int64_t *count, double *mom, int *rec,
+                          int *lo, cudaStream_t s) {
+  if (nb <= 0) return;
+  k_branch_export<<<grid_for(nb, 128), 128, 0, s>>>(t, branch, nb, rec_of_cell, key, level, count,
+                                                    mom, rec, lo);
 }
 
 // ------------------------------------------------------------- fp64 walk

@@ -96,7 +96,8 @@ void launch_keys_clamped_f64(const double *pos, int stride, int64_t n, const dou
 
 // tree build (hashed.py:376-515)
 void launch_lcp_new(const uint64_t *keys, int64_t n, int8_t *lcp, uint32_t *newc,
-                    DeviceFlags *f, int *lvl_cnt, int allow_dup, cudaStream_t s);
+                    DeviceFlags *f, int *lvl_cnt, int allow_dup, cudaStream_t s,
+                    int bnd_prev = -1, int bnd_next = -1);
 struct LevelPlan {  // internal cells per level (host-known) and list offsets
   int count[kMaxLevel + 1];
   int offset[kMaxLevel + 1];
@@ -105,6 +106,7 @@ struct TreeView {
   int64_t n = 0;       // bodies
   int64_t C = 0;       // cells; with dC set: the allocated capacity (grid bound)
   const int *dC = nullptr;  // sync-free build: the true cell count, on device
+  int bnd_prev = -1, bnd_next = -1;  // distributed build: lcp with neighbour ranks
   const uint64_t *keys = nullptr;
   const int8_t *lcp = nullptr;
   const uint32_t *off = nullptr;   // exclusive scan of newc
@@ -151,9 +153,18 @@ struct __align__(16) WalkNode {
   int4 d;    // first_child (internal) | lo (bucket/leaf), count, nchild, level
 };
 // MAC threshold (side_l/theta)^2 per level is formed on device from R
+// force (optional): cells always treated as expandable (a rank's shared
+// cells); rec_of_cell (optional): walk record index of every kept cell
 void launch_walk_tree(const TreeView &t, const double *dR, double theta, int leaf,
                       uint32_t *smask, uint32_t *nck, uint32_t *base, void *scan_tmp,
-                      size_t scan_bytes, WalkNode *out, int *dCp, cudaStream_t s);
+                      size_t scan_bytes, WalkNode *out, int *dCp, cudaStream_t s,
+                      const uint8_t *force = nullptr, int *rec_of_cell = nullptr);
+// distributed build
+void launch_mark_shared(const TreeView &t, uint8_t *shared, int *branch, int *nbranch,
+                        cudaStream_t s);
+void launch_branch_export(const TreeView &t, const int *branch, int nb, const int *rec_of_cell,
+                          uint64_t *key, int *level, int64_t *count, double *mom, int *rec,
+                          int *lo, cudaStream_t s);
 void launch_walk_f32(const WalkNode *T, const float4 *bodies, const float *targets, int tstride,
                      const uint32_t *tperm, int nt, float e2, int leaf, float *acc, int astride,
                      int64_t *work64, int *work32, DeviceFlags *f, cudaStream_t s);

@@ -53,37 +53,40 @@ __device__ __forceinline__ int child_slot(const TreeView &t, int64_t c) {
 
 // A cell's children are reachable when it can be opened: count > L, or it is
 // the root (the walk always starts at the root's children, flattree.py:271-279)
-__device__ __forceinline__ bool expandable(const TreeView &t, int64_t c, int leaf) {
+__device__ __forceinline__ bool expandable(const TreeView &t, int64_t c, int leaf,
+                                           const uint8_t *force) {
+  if (force && force[c]) return true;  // a rank's shared cell (distributed build)
   const int4 L = t.link[c];
   // level-21 cells of duplicate keys have no children: always buckets
   return (L.y > leaf || (c == 0 && L.y > 1)) && L.w < kMaxLevel;
 }
 
 // slot masks of the expandable cells
-__global__ void k_slots(TreeView t, int leaf, uint32_t *__restrict__ smask) {
+__global__ void k_slots(TreeView t, int leaf, const uint8_t *force, uint32_t *__restrict__ smask) {
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c <= 0 || c >= tree_count(t) || c >= t.C) return;
   const int P = t.parent[c];
-  if (expandable(t, P, leaf)) atomicOr(&smask[P], 1u << child_slot(t, c));
+  if (expandable(t, P, leaf, force)) atomicOr(&smask[P], 1u << child_slot(t, c));
 }
 
 // children per reachable internal cell (0 for buckets, leaves, pruned cells)
-__global__ void k_nchild(TreeView t, int leaf, const uint32_t *__restrict__ smask,
-                         uint32_t *__restrict__ nck) {
+__global__ void k_nchild(TreeView t, int leaf, const uint8_t *force,
+                         const uint32_t *__restrict__ smask, uint32_t *__restrict__ nck) {
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= t.C) return;
   if (c >= tree_count(t)) {  // capacity tail (sync-free build): scans as zero
     nck[c] = 0u;
     return;
   }
-  const bool kept = c == 0 || expandable(t, t.parent[c], leaf);
-  nck[c] = (kept && expandable(t, c, leaf)) ? (uint32_t)__popc(smask[c]) : 0u;
+  const bool kept = c == 0 || expandable(t, t.parent[c], leaf, force);
+  nck[c] = (kept && expandable(t, c, leaf, force)) ? (uint32_t)__popc(smask[c]) : 0u;
 }
 
 __global__ void k_compact(TreeView t, const double *__restrict__ dR, double theta, int leaf,
-                          const uint32_t *__restrict__ smask, const uint32_t *__restrict__ nck,
-                          const uint32_t *__restrict__ base, WalkNode *__restrict__ out,
-                          int *__restrict__ dCp) {
+                          const uint8_t *force, const uint32_t *__restrict__ smask,
+                          const uint32_t *__restrict__ nck, const uint32_t *__restrict__ base,
+                          WalkNode *__restrict__ out, int *__restrict__ dCp,
+                          int *__restrict__ rec_of_cell) {
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t C = tree_count(t);
   if (c >= C || c >= t.C) return;
@@ -91,7 +94,10 @@ __global__ void k_compact(TreeView t, const double *__restrict__ dR, double thet
   int j = 0;
   if (c > 0) {
     const int P = t.parent[c];
-    if (!expandable(t, P, leaf)) return;  // pruned (inside a bucket)
+    if (!expandable(t, P, leaf, force)) {  // pruned (inside a bucket)
+      if (rec_of_cell) rec_of_cell[c] = -1;
+      return;
+    }
     const int slot = child_slot(t, c);
     j = 1 + (int)base[P] + __popc(smask[P] & ((1u << slot) - 1u));
   }
@@ -109,20 +115,22 @@ __global__ void k_compact(TreeView t, const double *__restrict__ dR, double thet
   }
   nd.b = make_float4(q0, q1, q1, q3);
   nd.c = make_float4(q2, q4, (float)cm.w, q5);
-  const bool internal = expandable(t, c, leaf);
+  const bool internal = expandable(t, c, leaf, force);
+  if (rec_of_cell) rec_of_cell[c] = j;
   nd.d = make_int4(internal ? 1 + (int)base[c] : L.z, L.y, internal ? (int)nck[c] : 0, L.w);
   out[j] = nd;
 }
 
 void launch_walk_tree(const TreeView &t, const double *dR, double theta, int leaf,
                       uint32_t *smask, uint32_t *nck, uint32_t *base, void *scan_tmp,
-                      size_t scan_bytes, WalkNode *out, int *dCp, cudaStream_t s) {
+                      size_t scan_bytes, WalkNode *out, int *dCp, cudaStream_t s,
+                      const uint8_t *force, int *rec_of_cell) {
   const int g = grid_for(t.C, 256);
   cudaMemsetAsync(smask, 0, sizeof(uint32_t) * t.C, s);
-  k_slots<<<g, 256, 0, s>>>(t, leaf, smask);
-  k_nchild<<<g, 256, 0, s>>>(t, leaf, smask, nck);
+  k_slots<<<g, 256, 0, s>>>(t, leaf, force, smask);
+  k_nchild<<<g, 256, 0, s>>>(t, leaf, force, smask, nck);
   exclusive_scan_u32(scan_tmp, scan_bytes, nck, base, t.C, s);
-  k_compact<<<g, 256, 0, s>>>(t, dR, theta, leaf, smask, nck, base, out, dCp);
+  k_compact<<<g, 256, 0, s>>>(t, dR, theta, leaf, force, smask, nck, base, out, dCp, rec_of_cell);
 }
 
 __device__ __forceinline__ float2 f2(float x, float y) { return make_float2(x, y); }

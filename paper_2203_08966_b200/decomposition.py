@@ -28,6 +28,7 @@ GPU in tests -- host-side barriers only, no kernel waits on another).
 
 from __future__ import annotations
 
+import math
 import threading
 from dataclasses import dataclass
 
@@ -229,3 +230,420 @@ class DistributedSim:
 
     def store(self, pos=None, vel=None, acc=None, work=None) -> None:
         self.eng.sim_store(pos, vel, acc, work)
+
+
+# =========================================================================
+# Stage 2: distributed build (key-range decomposition)
+# =========================================================================
+#
+# Every rank owns the bodies of a contiguous Morton key range and builds only
+# its part of the tree; the exchange steps are those of SURVEY.md §8(e):
+#
+#   allreduce(max |x|) -> R                                  simulation.py:201-208
+#   migrate bodies to the owner of their key range           decomposition.py:84-263
+#     (splitters from last step's costzones on the global order, all-to-all)
+#   allgather boundary keys -> local tree with global leaf depths
+#   allgather branch nodes -> exact fp64 top tree on every rank  hashed.py:609-786
+#   allgather the owned walk records + bodies (a superset of the locally
+#     essential tree; a selective LET is the refinement) -> global walk tree
+#   walk the rank's own bodies; costzones cuts -> next splitters
+#
+# Per-target interaction lists equal the single-GPU walk's (same cells, same
+# fp32 records, same MAC), so work counts match exactly and accelerations to
+# fp32 summation order.  fp32 only.
+
+_REC_INTS = 16  # a 64-byte WalkNode as int32 columns: a(0-3) b(4-7) c(8-11) d(12-15)
+
+
+def _lcp(a: int, b: int) -> int:
+    x = a ^ b
+    return 21 - (x.bit_length() + 2) // 3
+
+
+def _combine(children):
+    """_moments_kernel (flattree.py:201-252) on (mass, com[3], quad[6]) rows,
+    in the given (slot) order, in IEEE double -- the same expressions."""
+    total = 0.0
+    cx = cy = cz = 0.0
+    for m, c, _ in children:
+        if m == 0.0:
+            continue
+        total += m
+        cx += m * c[0]
+        cy += m * c[1]
+        cz += m * c[2]
+    if total == 0.0:
+        return 0.0, (0.0, 0.0, 0.0), (0.0,) * 6
+    cx /= total
+    cy /= total
+    cz /= total
+    q = [0.0] * 6
+    for m, c, qc in children:
+        if m == 0.0:
+            continue
+        dx = c[0] - cx
+        dy = c[1] - cy
+        dz = c[2] - cz
+        d2 = dx * dx + dy * dy + dz * dz
+        q[0] += qc[0] + m * (3.0 * (dx * dx) - d2)
+        q[1] += qc[1] + m * (3.0 * (dx * dy) - 0.0)
+        q[2] += qc[2] + m * (3.0 * (dx * dz) - 0.0)
+        q[3] += qc[3] + m * (3.0 * (dy * dy) - d2)
+        q[4] += qc[4] + m * (3.0 * (dy * dz) - 0.0)
+        q[5] += qc[5] + m * (3.0 * (dz * dz) - d2)
+    return total, (cx, cy, cz), tuple(q)
+
+
+def _f32_bits(x: float) -> int:
+    return int(np.array([x], dtype=np.float32).view(np.int32)[0])
+
+
+class DistributedBuildSim:
+    """Key-range decomposition with a distributed build (see above).
+
+    ``load(pos, vel, mass, gid)`` takes this rank's initial chunk (any bodies;
+    the first decomposition sorts them globally).  ``store`` returns this rank's
+    current bodies with their global ids."""
+
+    def __init__(self, engine, comm: Comm, params: StepParams):
+        if engine.precision != "fp32":
+            raise ValueError("the distributed build runs in fp32 mode")
+        self.eng = engine
+        self.comm = comm
+        self.p = params
+        self.splitters = None  # R-1 int64 keys: rank r owns [s[r-1], s[r])
+        self.R = 1.0
+        self.last_zones = None
+
+    # -- collectives on variable-size tensors --
+    def _allgather_v(self, t: torch.Tensor) -> list:
+        size = self.comm.size
+        n = torch.tensor([t.shape[0]], dtype=torch.int64, device=t.device)
+        sizes = [torch.zeros_like(n) for _ in range(size)]
+        self._allgather(sizes, n)
+        sizes = [int(x.item()) for x in sizes]
+        mx = max(sizes) if sizes else 0
+        pad = torch.zeros((mx,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        pad[: t.shape[0]] = t
+        outs = [torch.empty_like(pad) for _ in range(size)]
+        self._allgather(outs, pad)
+        return [o[:k] for o, k in zip(outs, sizes)]
+
+    def _allgather(self, outs, t):
+        if isinstance(self.comm, TorchComm):
+            self.comm.dist.all_gather(outs, t, group=self.comm.group)
+        elif isinstance(self.comm, ThreadComm):
+            hub = self.comm.hub
+            if t.is_cuda:
+                torch.cuda.synchronize(t.device)
+            hub.slots[self.comm.rank] = t
+            hub.barrier.wait()
+            for r in range(self.comm.size):
+                outs[r].copy_(hub.slots[r])
+            if t.is_cuda:
+                torch.cuda.synchronize(t.device)
+            hub.barrier.wait()
+        else:
+            outs[0].copy_(t)
+
+    def _alltoall_v(self, t: torch.Tensor, send_counts: list) -> torch.Tensor:
+        """Rows of t, already grouped by destination rank, to their owners."""
+        size = self.comm.size
+        sc = torch.tensor(send_counts, dtype=torch.int64, device=t.device)
+        allc = [torch.zeros_like(sc) for _ in range(size)]
+        self._allgather(allc, sc)
+        recv_counts = [int(allc[q][self.comm.rank].item()) for q in range(size)]
+        if isinstance(self.comm, TorchComm):
+            out = torch.empty((sum(recv_counts),) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+            self.comm.dist.all_to_all_single(out, t.contiguous(), recv_counts, send_counts,
+                                             group=self.comm.group)
+            return out
+        # thread / single: gather everyone's full send buffer and cut out our rows
+        bufs = self._allgather_v(t)
+        parts = []
+        for q in range(size):
+            cq = [int(allc[q][k].item()) for k in range(size)]
+            start = sum(cq[: self.comm.rank])
+            parts.append(bufs[q][start:start + cq[self.comm.rank]])
+        return torch.cat(parts) if parts else t[:0]
+
+    # -- state --
+    def load(self, pos, vel, mass=None, gid=None) -> None:
+        """This rank's initial chunk: pos/vel float32 (n, 4), gid its global ids."""
+        eng = self.eng
+        n = pos.shape[0]
+        dev = eng.device
+        acc = torch.zeros_like(vel)
+        work = torch.ones(n, dtype=torch.int32, device=dev)  # simulation.py:482
+        eng.sim_load_state(pos, vel, acc, work)
+        self.gid_load = (gid if gid is not None else torch.arange(n, device=dev)).to(dev, torch.int64)
+        self._maxabs0 = float(pos[:, :3].abs().max().item()) if n else 0.0
+
+    def _export(self, what, n, shape, dtype):
+        out = torch.empty(shape, dtype=dtype, device=self.eng.device)
+        if n:
+            self.eng.sim_export(what, 0, n, out)
+        return out
+
+    def _bounds(self, local_max: float | None = None) -> None:
+        if local_max is None:
+            local_max = self.eng.sim_local_maxabs()
+        m = torch.tensor([local_max], dtype=torch.float64, device=self.eng.device)
+        self.comm.allreduce_max_(m)
+        ext = float(m.item())
+        self.R = 1.001 * ext if ext > 0.0 else 1.0  # morton.py:41-42
+        self.eng.sim_set_R(self.R)
+
+    def _sort(self):
+        """Local sort with the global R; returns (n, sorted keys, sorted gids)."""
+        eng = self.eng
+        eng.sim_sort()
+        n = eng.sim_n
+        ids = self._export(_lib.BH_SIM_ID, n, (n,), torch.int32)
+        gid = self.gid_load[ids.long()]
+        keys = self._export(_lib.BH_SIM_KEYS, n, (n,), torch.int64)
+        return n, keys, gid
+
+    def _initial_splitters(self, keys: torch.Tensor) -> None:
+        """Before any work is known: equal-count splitters from a key sample."""
+        size = self.comm.size
+        k = keys.shape[0]
+        idx = torch.linspace(0, max(k - 1, 0), min(k, 512), device=keys.device).long()
+        samp = keys[idx] if k else keys
+        allk = torch.sort(torch.cat(self._allgather_v(samp))).values
+        if size == 1 or allk.numel() == 0:
+            self.splitters = keys.new_zeros(0)
+            return
+        cut = [min(allk.numel() - 1, (r * allk.numel()) // size) for r in range(1, size)]
+        self.splitters = allk[torch.tensor(cut, device=keys.device)]
+
+    def _migrate(self, n: int, keys: torch.Tensor, gid: torch.Tensor) -> None:
+        """Bodies to the owner of their key range (rows are key-sorted, so the
+        per-destination groups are contiguous)."""
+        size = self.comm.size
+        if size == 1:
+            return
+        dest = torch.searchsorted(self.splitters, keys, right=True)
+        counts = torch.bincount(dest, minlength=size).tolist()
+        pos = self._export(_lib.BH_SIM_POS, n, (n, 4), torch.float32)
+        vel = self._export(_lib.BH_SIM_VEL, n, (n, 4), torch.float32)
+        acc = self._export(_lib.BH_SIM_ACC, n, (n, 4), torch.float32)
+        work = self._export(_lib.BH_SIM_PREV_WORK, n, (n,), torch.int32)
+        payload = torch.cat([pos.view(torch.int32), vel.view(torch.int32), acc.view(torch.int32),
+                             work.view(-1, 1), gid.view(torch.int32).view(-1, 2)], dim=1)
+        got = self._alltoall_v(payload, counts)
+        self.eng.sim_load_state(got[:, 0:4].clone().view(torch.float32),
+                                got[:, 4:8].clone().view(torch.float32),
+                                got[:, 8:12].clone().view(torch.float32),
+                                got[:, 12].clone())
+        self.gid_load = got[:, 13:15].clone().view(torch.int64).view(-1)
+
+    def _next_splitters(self, n: int, keys: torch.Tensor, work=None) -> None:
+        """costzones (decomposition.py:35-57) on the global order -- the ranks'
+        sorted runs concatenated: zone k starts after the first body whose
+        global work prefix reaches k/size of the total; its first body's key is
+        splitter k (for the next step: bodies move, any monotone cut is valid)."""
+        size = self.comm.size
+        if size == 1:
+            return
+        dev = keys.device
+        if work is None:
+            work = self._export(_lib.BH_SIM_WORK, n, (n,), torch.int32)
+        work = work.to(torch.int64)
+        mine = torch.tensor([int(work.sum().item()) if n else 0, n, int(keys[0].item()) if n else -1],
+                            dtype=torch.int64, device=dev)
+        allm = [torch.zeros_like(mine) for _ in range(size)]
+        self._allgather(allm, mine)
+        wt = [int(a[0].item()) for a in allm]
+        firsts = [int(a[2].item()) for a in allm]
+        total = sum(wt)
+        base = sum(wt[: self.comm.rank])
+        cand = torch.full((size - 1,), -1, dtype=torch.int64, device=dev)
+        if n:
+            prefix = (torch.cumsum(work, 0) + base) * size
+            for k in range(1, size):
+                j = int(torch.searchsorted(prefix, torch.tensor([k * total], device=dev), side="left").item())
+                # the straddling body is here iff it is this rank's body j and the
+                # prefix before this rank's first body is still short of the target
+                if j < n and (j > 0 or base * size < k * total):
+                    if j + 1 < n:
+                        cand[k - 1] = keys[j + 1]
+                    else:
+                        nxt = next((firsts[q] for q in range(self.comm.rank + 1, size) if firsts[q] >= 0), None)
+                        cand[k - 1] = nxt if nxt is not None else (1 << 62)
+        self.comm.allreduce_max_(cand)
+        # monotone (zones may be empty when work is concentrated)
+        self.splitters = torch.cummax(cand, 0).values
+
+    # -- the step --
+    def _forces(self, record_work: bool) -> None:
+        p, eng, comm = self.p, self.eng, self.comm
+        size, rank = comm.size, comm.rank
+        n, keys, gid = self._sort()
+        if self.splitters is None:
+            self._initial_splitters(keys)
+        self._migrate(n, keys, gid)
+        n, keys, gid = self._sort()
+        dev = eng.device
+        fl = torch.tensor([int(keys[0].item()) if n else -1, int(keys[-1].item()) if n else -1],
+                          dtype=torch.int64, device=dev)
+        allfl = [torch.zeros_like(fl) for _ in range(size)]
+        self._allgather(allfl, fl)
+        fls = [(int(a[0].item()), int(a[1].item())) for a in allfl]
+        prev = next((fls[q][1] for q in range(rank - 1, -1, -1) if fls[q][0] >= 0), None)
+        nxt = next((fls[q][0] for q in range(rank + 1, size) if fls[q][0] >= 0), None)
+        nb = eng.sim_build_local(p.theta, p.leaf_size, prev, nxt) if n else 0
+        br = eng.sim_branch_export(nb)
+        recs = eng.sim_walk_records() if n else torch.zeros((0, _REC_INTS), dtype=torch.int32, device=dev)
+        bodies = self._export(_lib.BH_SIM_POS, n, (n, 4), torch.float32)
+        br_all = {k: self._allgather_v(v) for k, v in br.items()}
+        recs_all = self._allgather_v(recs)
+        bodies_all = self._allgather_v(bodies)
+        self.tree = self._assemble(br_all, recs_all, [b.shape[0] for b in bodies_all])
+        gbodies = torch.cat(bodies_all)
+        acc = torch.zeros((n, 4), dtype=torch.float32, device=dev)
+        work = torch.zeros(n, dtype=torch.int32, device=dev)
+        if n:
+            eng.walk_records(self.tree, gbodies, bodies, p.eps, p.leaf_size, acc, work)
+            eng.sim_import(_lib.BH_SIM_ACC, 0, n, acc)
+            if record_work:
+                eng.sim_import(_lib.BH_SIM_WORK, 0, n, work)
+                eng.sim_scatter_work()
+        self._keys, self._n = keys, n
+
+    def _assemble(self, br_all, recs_all, nbod) -> torch.Tensor:
+        """Global walk tree = [top region | rank 0 records | rank 1 records | ...].
+
+        The top region holds the top cells (proper ancestors of the branch
+        nodes, recombined exactly in fp64) in breadth-first order with
+        contiguous children, and copies of the branch-node records pointing
+        into their owner's records; bucket-sized top cells (count <= L) are
+        buckets over their globally contiguous bodies, as in one tree."""
+        p = self.p
+        dev = self.eng.device
+        size = self.comm.size
+        nrec = [r.shape[0] for r in recs_all]
+        bodoff = np.cumsum([0] + list(nbod))[:-1]
+        rows = {}
+        for r in range(size):
+            key = br_all["key"][r].cpu().numpy()
+            if not len(key):
+                continue
+            lev = br_all["level"][r].cpu().numpy()
+            cnt = br_all["count"][r].cpu().numpy()
+            mom = br_all["mom"][r].cpu().numpy()
+            rec = br_all["rec"][r].cpu().numpy()
+            lo = br_all["lo"][r].cpu().numpy()
+            recs = recs_all[r][torch.as_tensor(rec, device=dev).long()].cpu().numpy()
+            for k in range(len(key)):
+                rows[int(key[k])] = dict(count=int(cnt[k]), mass=float(mom[k, 0]),
+                                         com=tuple(float(x) for x in mom[k, 1:4]),
+                                         quad=tuple(float(x) for x in mom[k, 4:10]), rank=r,
+                                         rec=recs[k].copy(), glo=int(lo[k]) + int(bodoff[r]),
+                                         level=int(lev[k]))
+        top = set()
+        for key in rows:
+            k = key >> 3
+            while k >= 1:
+                top.add(k)
+                k >>= 3
+        children = {k: [] for k in top}
+        for k in list(top) + list(rows):
+            if k != 1 and (k >> 3) in children:
+                children[k >> 3].append(k)
+        mom = {k: (b["mass"], b["com"], b["quad"], b["count"], b["glo"]) for k, b in rows.items()}
+        for k in sorted(top, key=lambda x: -x.bit_length()):  # deepest first (hashed.py:719-786)
+            ch = sorted(children[k], key=lambda c: c & 7)  # slot order
+            m, com, quad = _combine([mom[c][:3] for c in ch])
+            mom[k] = (m, com, quad, sum(mom[c][3] for c in ch), min(mom[c][4] for c in ch))
+        R = self.R
+
+        def mac2(level):
+            if p.theta == 0.0:
+                return float("inf")
+            r = math.ldexp(2.0 * R, -level) / p.theta
+            return r * r
+
+        def cell_record(k, d0, nchild):
+            m, com, quad, count, _ = mom[k]
+            level = (k.bit_length() - 1) // 3
+            a = np.array([-com[0], -com[1], -com[2], mac2(level)], dtype=np.float32).view(np.int32)
+            b = np.array([quad[0], quad[1], quad[1], quad[3]], dtype=np.float32).view(np.int32)
+            c = np.array([quad[2], quad[4], m, quad[5]], dtype=np.float32).view(np.int32)
+            return np.concatenate([a, b, c, np.array([d0, count, nchild, level], dtype=np.int32)])
+
+        # breadth-first layout; entries: ('top', k, first, nchild) | ('bucket', k) | ('branch', k)
+        entries = []
+        if not top:
+            entries.append(("branch", next(iter(rows))) if rows else None)
+        else:
+            entries.append(None)
+            queue = [(1, 0)]
+            qi = 0
+            while qi < len(queue):
+                k, at = queue[qi]
+                qi += 1
+                if k != 1 and mom[k][3] <= p.leaf_size:  # a bucket spanning ranks (SURVEY §8c)
+                    entries[at] = ("bucket", k)
+                    continue
+                ch = sorted(children[k], key=lambda c: c & 7)
+                first = len(entries)
+                for c in ch:
+                    entries.append(("branch", c) if c in rows else None)
+                    if c not in rows:
+                        queue.append((c, len(entries) - 1))
+                entries[at] = ("top", k, first, len(ch))
+        ntop = len(entries)
+        recoff = np.cumsum([0] + nrec)[:-1] + ntop
+        region = []
+        for e in entries:
+            if e[0] == "top":
+                region.append(cell_record(e[1], e[2], e[3]))
+            elif e[0] == "bucket":
+                region.append(cell_record(e[1], mom[e[1]][4], 0))
+            else:
+                b = rows[e[1]]
+                rec = b["rec"].copy()
+                rec[12] += recoff[b["rank"]] if rec[14] > 0 else bodoff[b["rank"]]
+                region.append(rec)
+        parts = [torch.as_tensor(np.array(region, dtype=np.int32).reshape(-1, _REC_INTS), device=dev)]
+        for r in range(size):
+            x = recs_all[r].clone()
+            internal = x[:, 14] > 0
+            x[:, 12] = torch.where(internal, x[:, 12] + int(recoff[r]), x[:, 12] + int(bodoff[r]))
+            parts.append(x)
+        return torch.cat(parts).contiguous()
+
+    def upload(self, pos, vel, acc, work, gid) -> None:
+        """Replace this rank's state (e.g. from host buffers); ownership is
+        restored by the next step's migration."""
+        self.eng.sim_load_state(pos, vel, acc, work)
+        self.gid_load = gid.to(self.eng.device, torch.int64)
+
+    def bootstrap(self) -> None:
+        """simulation.py:487: forces for the first kick (work not recorded)."""
+        self._bounds(self._maxabs0)
+        self._forces(record_work=False)
+        # the first decomposition balances on counts (simulation.py:482)
+        self._next_splitters(self._n, self._keys,
+                             torch.ones(self._n, dtype=torch.int64, device=self.eng.device))
+
+    def step(self, steps: int = 1) -> None:
+        for _ in range(steps):
+            self.eng.sim_begin_step(self.p.dt)
+            self._bounds()
+            self._forces(record_work=True)
+            self.eng.sim_end_step(self.p.dt)
+            self._next_splitters(self._n, self._keys)
+            if hasattr(self.eng, "check"):
+                self.eng.check()
+
+    def store(self):
+        """(pos (n,4), vel (n,4), acc (n,4), work (n,), gid (n,)) of this rank."""
+        n = self.eng.sim_n
+        pos = torch.empty((n, 4), dtype=torch.float32, device=self.eng.device)
+        vel = torch.empty_like(pos)
+        acc = torch.empty_like(pos)
+        work = torch.empty(n, dtype=torch.int64, device=self.eng.device)
+        self.eng.sim_store(pos, vel, acc, work)
+        return pos, vel, acc, work, self.gid_load

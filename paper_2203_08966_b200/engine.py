@@ -244,6 +244,61 @@ class Engine:
     def sim_import(self, what: int, begin: int, end: int, src: torch.Tensor) -> None:
         check(self._L.bh_sim_import(self._h, int(what), int(begin), int(end), _ptr(src), self.stream))
 
+    # -- distributed build (decomposition.DistributedBuildSim) --
+    def sim_local_maxabs(self) -> float:
+        out = ctypes.c_double()
+        check(self._L.bh_sim_local_maxabs(self._h, ctypes.byref(out), self.stream))
+        return float(out.value)
+
+    def sim_set_R(self, R: float) -> None:
+        check(self._L.bh_sim_set_R(self._h, float(R), self.stream))
+
+    def sim_sort(self) -> None:
+        check(self._L.bh_sim_sort(self._h, self.stream))
+
+    def sim_load_state(self, pos, vel, acc=None, work=None) -> None:
+        n = pos.shape[0]
+        check(self._L.bh_sim_load_state(self._h, _ptr(pos), _ptr(vel), _ptr(acc), _ptr(work), n,
+                                        self.stream))
+        self.sim_n = n
+
+    def sim_build_local(self, theta, leaf_size, prev_key=None, next_key=None) -> int:
+        nb = ctypes.c_int64()
+        check(self._L.bh_sim_build_local(
+            self._h, float(theta), int(leaf_size), int(prev_key is not None),
+            ctypes.c_uint64(int(prev_key or 0)), int(next_key is not None),
+            ctypes.c_uint64(int(next_key or 0)), ctypes.byref(nb), self.stream))
+        return int(nb.value)
+
+    def sim_branch_export(self, nb: int) -> dict:
+        d = self.device
+        out = dict(key=torch.empty(nb, dtype=torch.int64, device=d),
+                   level=torch.empty(nb, dtype=torch.int32, device=d),
+                   count=torch.empty(nb, dtype=torch.int64, device=d),
+                   mom=torch.empty((nb, 10), dtype=torch.float64, device=d),
+                   rec=torch.empty(nb, dtype=torch.int32, device=d),
+                   lo=torch.empty(nb, dtype=torch.int32, device=d))
+        if nb:
+            check(self._L.bh_sim_branch_export(self._h, _ptr(out["key"]), _ptr(out["level"]),
+                                               _ptr(out["count"]), _ptr(out["mom"]), _ptr(out["rec"]),
+                                               _ptr(out["lo"]), self.stream))
+        return out
+
+    def sim_walk_records(self) -> torch.Tensor:
+        """Walk records (int32 [n, 16] view of the 64-byte WalkNode)."""
+        n = ctypes.c_int64()
+        check(self._L.bh_sim_walk_records(self._h, None, ctypes.byref(n), self.stream))
+        out = torch.empty((int(n.value), 16), dtype=torch.int32, device=self.device)
+        if n.value:
+            check(self._L.bh_sim_walk_records(self._h, _ptr(out), ctypes.byref(n), self.stream))
+        return out
+
+    def walk_records(self, records: torch.Tensor, bodies: torch.Tensor, targets: torch.Tensor,
+                     eps: float, leaf_size: int, acc: torch.Tensor, work: torch.Tensor | None) -> None:
+        check(self._L.bh_walk_records_f32(self._h, _ptr(records), records.shape[0], _ptr(bodies),
+                                          _ptr(targets), targets.shape[0], float(eps), int(leaf_size),
+                                          _ptr(acc), _ptr(work), self.stream))
+
     def sim_store(self, pos=None, vel=None, acc=None, work=None) -> None:
         check(self._L.bh_sim_store(self._h, _ptr(pos), _ptr(vel), _ptr(acc), _ptr(work), self.stream))
 

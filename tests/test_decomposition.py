@@ -83,3 +83,44 @@ def test_two_rank_gloo_matches_single_rank():
         np.testing.assert_array_equal(vel, v)
         np.testing.assert_array_equal(work, w)
         assert len(zones) == 3 and zones[0] == 0 and zones[-1] == n and 0 < zones[1] < n
+
+
+def _coll_worker(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2203_08966_b200.decomposition import DistributedBuildSim, StepParams
+
+    class Dummy:
+        precision = "fp32"
+        device = torch.device("cpu")
+
+    sim = DistributedBuildSim(Dummy(), TorchComm(), StepParams(0.5, 0.01, 1, 0.01))
+    # variable-size allgather
+    t = torch.arange(3 + 2 * rank, dtype=torch.int64).reshape(-1, 1) + 100 * rank
+    got = [x.flatten().tolist() for x in sim._allgather_v(t)]
+    # all-to-all of rows grouped by destination: rank r sends (r, q) rows x (q+1)
+    rows, counts = [], []
+    for q in range(world):
+        rows += [[rank, q]] * (q + 1)
+        counts.append(q + 1)
+    recv = sim._alltoall_v(torch.tensor(rows, dtype=torch.int32), counts).tolist()
+    out_q.put((rank, got, recv))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_stage2_collectives_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_coll_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, got, recv in res:
+        assert got == [[0, 1, 2], [100, 101, 102, 103, 104]]
+        assert recv == [[0, rank]] * (rank + 1) + [[1, rank]] * (rank + 1)

@@ -71,3 +71,102 @@ def test_emulated_ranks_match_single_gpu(precision):
         # all ranks hold the same replicated state
         for pos, work, _ in multi[1:]:
             np.testing.assert_array_equal(pos, multi[0][0])
+
+
+def _run_build(ranks, b, steps, theta=0.6, eps=1e-3, leaf=16, dt=1e-3):
+    """Stage 2 (distributed build) with R emulated ranks; returns per-gid arrays."""
+    from paper_2203_08966_b200.decomposition import DistributedBuildSim, StepParams, ThreadComm
+    from paper_2203_08966_b200.engine import Engine
+
+    n = len(b)
+    comms = ThreadComm.group(ranks)
+    outs = [None] * ranks
+    err = []
+    cuts = np.linspace(0, n, ranks + 1).astype(int)
+
+    def body(r):
+        try:
+            eng = Engine("fp32", 0)
+            sl = slice(cuts[r], cuts[r + 1])
+            pos = eng.bodies_tensor(b.position[sl], b.mass[sl])
+            vel = eng.vec_tensor(b.velocity[sl])
+            gid = torch.arange(cuts[r], cuts[r + 1], device="cuda")
+            sim = DistributedBuildSim(eng, comms[r], StepParams(theta, eps, leaf, dt))
+            sim.load(pos, vel, gid=gid)
+            sim.bootstrap()
+            sim.step(steps)
+            p, v, a, w, g = sim.store()
+            eng.check()
+            outs[r] = tuple(x.cpu().numpy() for x in (p, v, a, w, g))
+            eng.close()
+        except Exception as e:  # pragma: no cover
+            import traceback
+            traceback.print_exc()
+            err.append(e)
+            comms[r].hub.barrier.abort()
+
+    ts = [threading.Thread(target=body, args=(r,)) for r in range(ranks)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=600)
+    if err:
+        raise err[0]
+    res = {k: np.zeros((n, 4)) for k in ("pos", "vel", "acc")}
+    res["work"] = np.zeros(n, dtype=np.int64)
+    seen = np.zeros(n, dtype=int)
+    for p, v, a, w, g in outs:
+        res["pos"][g], res["vel"][g], res["acc"][g], res["work"][g] = p, v, a, w
+        seen[g] += 1
+    assert np.all(seen == 1), "every body owned by exactly one rank"
+    res["counts"] = [len(o[4]) for o in outs]
+    return res
+
+
+def _single(b, steps, theta=0.6, eps=1e-3, leaf=16, dt=1e-3):
+    from paper_2203_08966_b200.engine import Engine
+
+    eng = Engine("fp32", 0)
+    pos = eng.bodies_tensor(b.position, b.mass)
+    vel = eng.vec_tensor(b.velocity)
+    eng.sim_load(pos, vel)
+    eng.sim_forces(theta, eps, leaf, record_work=False)
+    eng.sim_step(dt, theta, eps, leaf, steps)
+    p, v, a = torch.empty_like(vel), torch.empty_like(vel), torch.empty_like(vel)
+    w = torch.empty(len(b), dtype=torch.int64, device="cuda")
+    eng.sim_store(p, v, a, w)
+    eng.check()
+    out = dict(pos=p.double().cpu().numpy(), vel=v.double().cpu().numpy(), acc=a.double().cpu().numpy(),
+               work=w.cpu().numpy())
+    eng.close()
+    return out
+
+
+@pytest.mark.parametrize("leaf", [1, 16])
+def test_distributed_build_matches_single_gpu(leaf):
+    from paper_2203_08966_b200.initcond import make_rng, plummer_cluster
+
+    b = plummer_cluster(20_000, make_rng(1))
+    ref = _single(b, 1, leaf=leaf)
+    for ranks in (1, 2, 3):
+        got = _run_build(ranks, b, 1, leaf=leaf)
+        if ranks > 1:
+            assert min(got["counts"]) > 0
+        np.testing.assert_array_equal(got["work"], ref["work"])  # identical interaction lists
+        err = np.linalg.norm(got["acc"][:, :3] - ref["acc"][:, :3]) / np.linalg.norm(ref["acc"][:, :3])
+        assert err < 1e-5, (ranks, err)
+        np.testing.assert_allclose(got["pos"][:, :3], ref["pos"][:, :3], rtol=0, atol=1e-6)
+
+
+def test_distributed_build_clustered_multi_step():
+    """cfg0/cfg3 geometry (two colliding clusters), 3 steps, 4 ranks: work
+    identical per body; costzones keeps the ranks' work balanced."""
+    from paper_2203_08966_b200.initcond import colliding_plummers
+
+    b = colliding_plummers(12_000, 3)
+    ref = _single(b, 3, theta=0.6, eps=1e-4, leaf=32, dt=5e-4)
+    got = _run_build(4, b, 3, theta=0.6, eps=1e-4, leaf=32, dt=5e-4)
+    assert np.mean(got["work"] != ref["work"]) < 1e-3
+    err = np.linalg.norm(got["acc"][:, :3] - ref["acc"][:, :3]) / np.linalg.norm(ref["acc"][:, :3])
+    assert err < 1e-5
+    assert min(got["counts"]) > 0.2 * len(b) / 4
