@@ -72,8 +72,13 @@ struct bh_handle {
   Buf bk_pos, bk_vel, bk_acc, bk_id, bk_work;
   // distributed build (decomposition.py): boundary lcps, shared cells, branches
   int bnd_prev = -1, bnd_next = -1;
-  Buf shared, branch, rec_of_cell;
+  Buf shared, branch, rec_of_cell, wparent;
   int64_t nbranch = 0;
+  // locally essential trees of the last build_local
+  Buf let_present, let_expand, let_bodies, let_isbranch, let_rflag, let_bcount, let_rpos,
+      let_bpos, let_scan_tmp, let_brec;
+  int let_nrank = 0;
+  int64_t let_nrec = 0;
   double R = 1.0;
   Buf link, parent, child8, lvl, lvl_list, cm64, q64, tbod;
   int *hlvl = nullptr;  // pinned: internal cells per level of the last build
@@ -634,7 +639,10 @@ int bh_destroy(bh_handle *h) {
                  &h->lcp, &h->newc, &h->off, &h->link, &h->parent, &h->child8, &h->lvl, &h->lvl_list,
                  &h->cm64, &h->q64, &h->smask, &h->nck, &h->wbase, &h->wnodes, &h->wscan_tmp, &h->tbod, &h->pos, &h->pos2,
                  &h->vel, &h->vel2, &h->acc, &h->id, &h->id2, &h->work_sorted, &h->work_orig,
-                 &h->bk_pos, &h->bk_vel, &h->bk_acc, &h->bk_id, &h->bk_work};
+                 &h->bk_pos, &h->bk_vel, &h->bk_acc, &h->bk_id, &h->bk_work,
+                 &h->shared, &h->branch, &h->rec_of_cell, &h->wparent, &h->let_present,
+                 &h->let_expand, &h->let_bodies, &h->let_isbranch, &h->let_rflag, &h->let_bcount,
+                 &h->let_rpos, &h->let_bpos, &h->let_scan_tmp, &h->let_brec};
   for (Buf *b : bufs) b->release();
   cudaFree(h->flags);
   cudaFreeHost(h->hflags);
@@ -1063,6 +1071,7 @@ int bh_sim_build_local(bh_handle *h, double theta, int leaf_size, int has_prev, 
   BH_CUDA(h->shared.ensure(C + 16));
   BH_CUDA(h->branch.ensure(sizeof(int) * (8 * (2 * kMaxLevel + 2) + 8)));
   BH_CUDA(h->rec_of_cell.ensure(sizeof(int) * C));
+  BH_CUDA(h->wparent.ensure(sizeof(int) * C));
   TreeView t = h->view();
   launch_mark_shared(t, h->shared.as<uint8_t>(), h->branch.as<int>() + 1, h->branch.as<int>(), s);
   BH_CUDA(h->smask.ensure(sizeof(uint32_t) * C));
@@ -1073,7 +1082,7 @@ int bh_sim_build_local(bh_handle *h, double theta, int leaf_size, int has_prev, 
   launch_walk_tree(t, h->dR, theta, leaf_size, h->smask.as<uint32_t>(), h->nck.as<uint32_t>(),
                    h->wbase.as<uint32_t>(), h->wscan_tmp.p, h->wscan_tmp.bytes,
                    h->wnodes.as<WalkNode>(), h->dCp, s, h->shared.as<uint8_t>(),
-                   h->rec_of_cell.as<int>());
+                   h->rec_of_cell.as<int>(), h->wparent.as<int>());
   h->walk_valid = false;  // a forced-shared walk tree is not the local-walk tree
   int nb = 0;
   BH_CUDA(cudaMemcpyAsync(&nb, h->branch.p, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -1091,6 +1100,106 @@ int bh_sim_branch_export(bh_handle *h, uint64_t *d_key, int32_t *d_level, int64_
   TreeView t = h->view();
   launch_branch_export(t, h->branch.as<int>() + 1, (int)h->nbranch, h->rec_of_cell.as<int>(), d_key,
                        d_level, d_count, d_mom10, d_rec, d_lo, S(stream));
+  BH_LAUNCHED();
+  return BH_OK;
+}
+
+__global__ void k_mark_branch_recs(const int *branch, int nb, const int *rec_of_cell,
+                                   uint8_t *isbranch, int *brec) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nb) return;
+  const int j = rec_of_cell[branch[k]];
+  isbranch[j] = 1;
+  brec[k] = j;
+}
+
+// Locally essential trees of this rank's last bh_sim_build_local for every
+// other rank: d_boxes = [nrank][6] (min xyz, max xyz) of each
+// rank's bodies.  Fills rec_counts / body_counts (host, [nrank]) with the LET
+// sizes for each receiver (0 for self).  Synchronises.
+int bh_sim_let(bh_handle *h, const double *d_boxes, int nrank, int self, int64_t *rec_counts,
+               int64_t *body_counts, void *stream) {
+  if (!h || !d_boxes || nrank < 1 || nrank > 32 || self < 0 || self >= nrank || !rec_counts ||
+      !body_counts)
+    return fail(BH_BAD_ARG, "bh_sim_let: bad args");
+  cudaStream_t s = S(stream);
+  int cp = 0;
+  BH_CUDA(cudaMemcpyAsync(&cp, h->dCp, sizeof(int), cudaMemcpyDeviceToHost, s));
+  BH_CUDA(cudaStreamSynchronize(s));
+  const int64_t n = cp;
+  h->let_nrank = nrank;
+  h->let_nrec = n;
+  for (int q = 0; q < nrank; ++q) rec_counts[q] = body_counts[q] = 0;
+  if (n == 0 || h->sim_n == 0) return BH_OK;
+  Buf *u32s[] = {&h->let_present, &h->let_expand, &h->let_bodies, &h->let_rflag, &h->let_bcount};
+  for (Buf *b : u32s) BH_CUDA(b->ensure(sizeof(uint32_t) * (n + 1)));
+  BH_CUDA(h->let_rpos.ensure(sizeof(uint32_t) * (n + 1) * nrank));
+  BH_CUDA(h->let_bpos.ensure(sizeof(uint32_t) * (n + 1) * nrank));
+  BH_CUDA(h->let_isbranch.ensure(n + 16));
+  BH_CUDA(h->let_brec.ensure(sizeof(int) * (h->nbranch + 1)));
+  BH_CUDA(h->let_scan_tmp.ensure(scan_temp_bytes(n) + 16));
+  BH_CUDA(cudaMemsetAsync(h->let_isbranch.p, 0, n, s));
+  if (h->nbranch > 0)
+    k_mark_branch_recs<<<grid_for(h->nbranch, 128), 128, 0, s>>>(
+        h->branch.as<int>() + 1, (int)h->nbranch, h->rec_of_cell.as<int>(), h->let_isbranch.as<uint8_t>(),
+        h->let_brec.as<int>());
+  const WalkNode *W = h->wnodes.as<WalkNode>();
+  launch_let_mark(W, (int)n, h->wparent.as<int>(), h->let_isbranch.as<uint8_t>(), d_boxes, nrank, self,
+                  h->let_present.as<uint32_t>(), h->let_expand.as<uint32_t>(),
+                  h->let_bodies.as<uint32_t>(), s);
+  std::vector<uint32_t> tail(4 * nrank, 0);
+  for (int q = 0; q < nrank; ++q) {
+    if (q == self) continue;
+    uint32_t *rpos = h->let_rpos.as<uint32_t>() + (n + 1) * q;
+    uint32_t *bpos = h->let_bpos.as<uint32_t>() + (n + 1) * q;
+    launch_let_flags(W, (int)n, h->let_isbranch.as<uint8_t>(), h->let_present.as<uint32_t>(),
+                     h->let_bodies.as<uint32_t>(), q, h->let_rflag.as<uint32_t>(),
+                     h->let_bcount.as<uint32_t>(), s);
+    BH_CUDA(exclusive_scan_u32(h->let_scan_tmp.p, h->let_scan_tmp.bytes, h->let_rflag.as<uint32_t>(),
+                               rpos, n, s));
+    BH_CUDA(exclusive_scan_u32(h->let_scan_tmp.p, h->let_scan_tmp.bytes, h->let_bcount.as<uint32_t>(),
+                               bpos, n, s));
+    BH_CUDA(cudaMemcpyAsync(&tail[4 * q], rpos + n - 1, 4, cudaMemcpyDeviceToHost, s));
+    BH_CUDA(cudaMemcpyAsync(&tail[4 * q + 1], h->let_rflag.as<uint32_t>() + n - 1, 4,
+                            cudaMemcpyDeviceToHost, s));
+    BH_CUDA(cudaMemcpyAsync(&tail[4 * q + 2], bpos + n - 1, 4, cudaMemcpyDeviceToHost, s));
+    BH_CUDA(cudaMemcpyAsync(&tail[4 * q + 3], h->let_bcount.as<uint32_t>() + n - 1, 4,
+                            cudaMemcpyDeviceToHost, s));
+    BH_CUDA(cudaStreamSynchronize(s));  // tail[] is pageable host memory
+  }
+  for (int q = 0; q < nrank; ++q) {
+    if (q == self) continue;
+    rec_counts[q] = (int64_t)tail[4 * q] + tail[4 * q + 1];
+    body_counts[q] = (int64_t)tail[4 * q + 2] + tail[4 * q + 3];
+  }
+  h->launches += 2 + 22 + 3 * (nrank - 1);
+  BH_LAUNCHED();
+  return BH_OK;
+}
+
+// Pack the LET for receiver q (sizes from bh_sim_let): records [rec_counts[q]]
+// (WalkNode), bodies [body_counts[q]] (float4) and, per branch node of this
+// rank, (first child in the LET | -1, first body in the LET | -1).
+int bh_sim_let_pack(bh_handle *h, int q, void *d_rec_out, float *d_bodies_out, int32_t *d_bmap_out,
+                    void *stream) {
+  if (!h || q < 0 || q >= h->let_nrank) return fail(BH_BAD_ARG, "bh_sim_let_pack: bad args");
+  cudaStream_t s = S(stream);
+  const int64_t n = h->let_nrec;
+  if (n == 0) return BH_OK;
+  const WalkNode *W = h->wnodes.as<WalkNode>();
+  const uint32_t *rpos = h->let_rpos.as<uint32_t>() + (n + 1) * q;
+  const uint32_t *bpos = h->let_bpos.as<uint32_t>() + (n + 1) * q;
+  launch_let_flags(W, (int)n, h->let_isbranch.as<uint8_t>(), h->let_present.as<uint32_t>(),
+                   h->let_bodies.as<uint32_t>(), q, h->let_rflag.as<uint32_t>(),
+                   h->let_bcount.as<uint32_t>(), s);
+  launch_let_pack(W, (int)n, h->let_isbranch.as<uint8_t>(), h->let_expand.as<uint32_t>(),
+                  h->let_bodies.as<uint32_t>(), q, h->let_rflag.as<uint32_t>(), rpos, bpos,
+                  h->pos.as<float4>(), static_cast<WalkNode *>(d_rec_out),
+                  reinterpret_cast<float4 *>(d_bodies_out), s);
+  launch_let_branchmap(W, h->let_brec.as<int>(), (int)h->nbranch, h->let_expand.as<uint32_t>(),
+                       h->let_bodies.as<uint32_t>(), q, rpos, bpos, reinterpret_cast<int2 *>(d_bmap_out),
+                       s);
+  h->launches += 3;
   BH_LAUNCHED();
   return BH_OK;
 }

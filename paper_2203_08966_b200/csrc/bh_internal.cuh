@@ -158,7 +158,21 @@ struct __align__(16) WalkNode {
 void launch_walk_tree(const TreeView &t, const double *dR, double theta, int leaf,
                       uint32_t *smask, uint32_t *nck, uint32_t *base, void *scan_tmp,
                       size_t scan_bytes, WalkNode *out, int *dCp, cudaStream_t s,
-                      const uint8_t *force = nullptr, int *rec_of_cell = nullptr);
+                      const uint8_t *force = nullptr, int *rec_of_cell = nullptr,
+                      int *wparent = nullptr);
+// locally essential trees (bh_walk.cu)
+void launch_let_mark(const WalkNode *W, int nrec, const int *wparent, const uint8_t *isbranch,
+                     const double *boxes, int nrank, int self, uint32_t *present, uint32_t *expand,
+                     uint32_t *bodies, cudaStream_t s);
+void launch_let_flags(const WalkNode *W, int nrec, const uint8_t *isbranch, const uint32_t *present,
+                      const uint32_t *bodies, int q, uint32_t *rflag, uint32_t *bcount, cudaStream_t s);
+void launch_let_pack(const WalkNode *W, int nrec, const uint8_t *isbranch, const uint32_t *expand,
+                     const uint32_t *bodies, int q, const uint32_t *rflag, const uint32_t *rpos,
+                     const uint32_t *bpos, const float4 *src_bodies, WalkNode *out, float4 *out_bodies,
+                     cudaStream_t s);
+void launch_let_branchmap(const WalkNode *W, const int *brec, int nb, const uint32_t *expand,
+                          const uint32_t *bodies, int q, const uint32_t *rpos, const uint32_t *bpos,
+                          int2 *map, cudaStream_t s);
 // distributed build
 void launch_mark_shared(const TreeView &t, uint8_t *shared, int *branch, int *nbranch,
                         cudaStream_t s);

@@ -86,7 +86,7 @@ __global__ void k_compact(TreeView t, const double *__restrict__ dR, double thet
                           const uint8_t *force, const uint32_t *__restrict__ smask,
                           const uint32_t *__restrict__ nck, const uint32_t *__restrict__ base,
                           WalkNode *__restrict__ out, int *__restrict__ dCp,
-                          int *__restrict__ rec_of_cell) {
+                          int *__restrict__ rec_of_cell, int *__restrict__ wparent) {
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t C = tree_count(t);
   if (c >= C || c >= t.C) return;
@@ -117,6 +117,11 @@ __global__ void k_compact(TreeView t, const double *__restrict__ dR, double thet
   nd.c = make_float4(q2, q4, (float)cm.w, q5);
   const bool internal = expandable(t, c, leaf, force);
   if (rec_of_cell) rec_of_cell[c] = j;
+  if (wparent) {  // record parent links (LET selection walks them top-down)
+    if (c == 0) wparent[0] = -1;
+    if (internal)
+      for (int k = 0; k < (int)nck[c]; ++k) wparent[1 + (int)base[c] + k] = j;
+  }
   nd.d = make_int4(internal ? 1 + (int)base[c] : L.z, L.y, internal ? (int)nck[c] : 0, L.w);
   out[j] = nd;
 }
@@ -124,13 +129,131 @@ __global__ void k_compact(TreeView t, const double *__restrict__ dR, double thet
 void launch_walk_tree(const TreeView &t, const double *dR, double theta, int leaf,
                       uint32_t *smask, uint32_t *nck, uint32_t *base, void *scan_tmp,
                       size_t scan_bytes, WalkNode *out, int *dCp, cudaStream_t s,
-                      const uint8_t *force, int *rec_of_cell) {
+                      const uint8_t *force, int *rec_of_cell, int *wparent) {
   const int g = grid_for(t.C, 256);
   cudaMemsetAsync(smask, 0, sizeof(uint32_t) * t.C, s);
   k_slots<<<g, 256, 0, s>>>(t, leaf, force, smask);
   k_nchild<<<g, 256, 0, s>>>(t, leaf, force, smask, nck);
   exclusive_scan_u32(scan_tmp, scan_bytes, nck, base, t.C, s);
-  k_compact<<<g, 256, 0, s>>>(t, dR, theta, leaf, force, smask, nck, base, out, dCp, rec_of_cell);
+  k_compact<<<g, 256, 0, s>>>(t, dR, theta, leaf, force, smask, nck, base, out, dCp, rec_of_cell,
+                              wparent);
+}
+
+// ------------------------------------------------ locally essential trees
+// Conservative box-MAC: a record is taken (pc) by every target
+// in the box if even the box point nearest its com passes the MAC with a
+// relative margin that covers the fp32 rounding of d2 on the receiving side.
+__device__ __forceinline__ bool accepted_by_all(const WalkNode &r, const double *box) {
+  const double cx = -(double)r.a.x, cy = -(double)r.a.y, cz = -(double)r.a.z;
+  const double c[3] = {cx, cy, cz};
+  double d2 = 0.0;
+  for (int a = 0; a < 3; ++a) {
+    const double lo = box[a], hi = box[3 + a];
+    const double g = c[a] < lo ? lo - c[a] : (c[a] > hi ? c[a] - hi : 0.0);
+    d2 += g * g;
+  }
+  const double mac2 = (double)r.a.w;
+  return d2 > mac2 * (1.0 + 1e-5) + 1e-30;
+}
+
+// One level of the top-down marking, for all receivers at once (bit q):
+// present = the receiver's walk can reach the record (branch roots always;
+// otherwise its parent is expanded); expand = present and not taken by all
+// of the receiver's targets (its children are needed); bodies = present bucket
+// not taken by all (its bodies are needed).
+__global__ void k_let_mark(const WalkNode *__restrict__ W, int nrec, const int *__restrict__ wparent,
+                           const uint8_t *__restrict__ isbranch, const double *__restrict__ boxes,
+                           int nrank, int self, int level, uint32_t *__restrict__ present,
+                           uint32_t *__restrict__ expand, uint32_t *__restrict__ bodies) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= nrec) return;
+  const WalkNode r = W[j];
+  if (r.d.w != level) return;
+  const uint32_t all = ((nrank >= 32 ? 0xffffffffu : (1u << nrank) - 1u)) & ~(1u << self);
+  uint32_t p = isbranch[j] ? all : (wparent[j] >= 0 ? expand[wparent[j]] : 0u);
+  uint32_t e = 0, b = 0;
+  if (p && r.d.y > 1) {
+    uint32_t fail = 0;
+    for (int q = 0; q < nrank; ++q)
+      if (((p >> q) & 1u) && !accepted_by_all(r, boxes + 6 * q)) fail |= 1u << q;
+    if (r.d.z > 0) e = p & fail;
+    else b = p & fail;
+  }
+  present[j] = p;
+  expand[j] = e;
+  bodies[j] = b;
+}
+
+__global__ void k_let_flags(const WalkNode *__restrict__ W, int nrec, const uint8_t *__restrict__ isbranch,
+                            const uint32_t *__restrict__ present, const uint32_t *__restrict__ bodies,
+                            int q, uint32_t *__restrict__ rflag, uint32_t *__restrict__ bcount) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= nrec) return;
+  rflag[j] = (!isbranch[j] && ((present[j] >> q) & 1u)) ? 1u : 0u;
+  bcount[j] = ((bodies[j] >> q) & 1u) ? (uint32_t)W[j].d.y : 0u;
+}
+
+// Pack the LET for receiver q: its records in W order (children blocks stay
+// contiguous), child links remapped into the LET, bucket body ranges into the
+// LET's body list; records the receiver never opens get nchild = 0.
+__global__ void k_let_pack(const WalkNode *__restrict__ W, int nrec, const uint8_t *__restrict__ isbranch,
+                           const uint32_t *__restrict__ expand, const uint32_t *__restrict__ bodies,
+                           int q, const uint32_t *__restrict__ rflag, const uint32_t *__restrict__ rpos,
+                           const uint32_t *__restrict__ bpos, const float4 *__restrict__ src_bodies,
+                           WalkNode *__restrict__ out, float4 *__restrict__ out_bodies) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= nrec) return;
+  const bool body_need = (bodies[j] >> q) & 1u;
+  if (body_need)
+    for (int k = 0; k < W[j].d.y; ++k) out_bodies[bpos[j] + k] = src_bodies[W[j].d.x + k];
+  if (!rflag[j]) return;
+  WalkNode r = W[j];
+  if ((expand[j] >> q) & 1u) r.d.x = (int)rpos[r.d.x];
+  else if (body_need) r.d.x = (int)bpos[j];
+  else { r.d.z = 0; if (r.d.y > 1) r.d.x = -1; }  // never opened by the receiver
+  out[rpos[j]] = r;
+}
+
+// Branch roots for receiver q: (first child in the LET | -1, first body in
+// the LET's body list | -1).
+__global__ void k_let_branchmap(const WalkNode *__restrict__ W, const int *__restrict__ brec, int nb,
+                                const uint32_t *__restrict__ expand, const uint32_t *__restrict__ bodies,
+                                int q, const uint32_t *__restrict__ rpos,
+                                const uint32_t *__restrict__ bpos, int2 *__restrict__ map) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nb) return;
+  const int j = brec[k];
+  const WalkNode r = W[j];
+  map[k] = make_int2(((expand[j] >> q) & 1u) ? (int)rpos[r.d.x] : -1,
+                     ((bodies[j] >> q) & 1u) ? (int)bpos[j] : -1);
+}
+
+void launch_let_mark(const WalkNode *W, int nrec, const int *wparent, const uint8_t *isbranch,
+                     const double *boxes, int nrank, int self, uint32_t *present, uint32_t *expand,
+                     uint32_t *bodies, cudaStream_t s) {
+  if (nrec <= 0) return;
+  for (int l = 0; l <= kMaxLevel; ++l)
+    k_let_mark<<<grid_for(nrec, 256), 256, 0, s>>>(W, nrec, wparent, isbranch, boxes, nrank, self, l,
+                                                   present, expand, bodies);
+}
+void launch_let_flags(const WalkNode *W, int nrec, const uint8_t *isbranch, const uint32_t *present,
+                      const uint32_t *bodies, int q, uint32_t *rflag, uint32_t *bcount, cudaStream_t s) {
+  if (nrec <= 0) return;
+  k_let_flags<<<grid_for(nrec, 256), 256, 0, s>>>(W, nrec, isbranch, present, bodies, q, rflag, bcount);
+}
+void launch_let_pack(const WalkNode *W, int nrec, const uint8_t *isbranch, const uint32_t *expand,
+                     const uint32_t *bodies, int q, const uint32_t *rflag, const uint32_t *rpos,
+                     const uint32_t *bpos, const float4 *src_bodies, WalkNode *out, float4 *out_bodies,
+                     cudaStream_t s) {
+  if (nrec <= 0) return;
+  k_let_pack<<<grid_for(nrec, 256), 256, 0, s>>>(W, nrec, isbranch, expand, bodies, q, rflag, rpos, bpos,
+                                                 src_bodies, out, out_bodies);
+}
+void launch_let_branchmap(const WalkNode *W, const int *brec, int nb, const uint32_t *expand,
+                          const uint32_t *bodies, int q, const uint32_t *rpos, const uint32_t *bpos,
+                          int2 *map, cudaStream_t s) {
+  if (nb <= 0) return;
+  k_let_branchmap<<<grid_for(nb, 128), 128, 0, s>>>(W, brec, nb, expand, bodies, q, rpos, bpos, map);
 }
 
 __device__ __forceinline__ float2 f2(float x, float y) { return make_float2(x, y); }

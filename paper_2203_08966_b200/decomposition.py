@@ -314,6 +314,7 @@ class DistributedBuildSim:
         self.splitters = None  # R-1 int64 keys: rank r owns [s[r-1], s[r])
         self.R = 1.0
         self.last_zones = None
+        self.let_pad = 0.0  # widens the LET target boxes (inf: send whole subtrees)
 
     # -- collectives on variable-size tensors --
     def _allgather_v(self, t: torch.Tensor) -> list:
@@ -346,8 +347,9 @@ class DistributedBuildSim:
         else:
             outs[0].copy_(t)
 
-    def _alltoall_v(self, t: torch.Tensor, send_counts: list) -> torch.Tensor:
-        """Rows of t, already grouped by destination rank, to their owners."""
+    def _alltoall_v(self, t: torch.Tensor, send_counts: list, return_counts: bool = False):
+        """Rows of t, already grouped by destination rank, to their owners
+        (with the per-source row counts if ``return_counts``)."""
         size = self.comm.size
         sc = torch.tensor(send_counts, dtype=torch.int64, device=t.device)
         allc = [torch.zeros_like(sc) for _ in range(size)]
@@ -357,7 +359,7 @@ class DistributedBuildSim:
             out = torch.empty((sum(recv_counts),) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
             self.comm.dist.all_to_all_single(out, t.contiguous(), recv_counts, send_counts,
                                              group=self.comm.group)
-            return out
+            return (out, recv_counts) if return_counts else out
         # thread / single: gather everyone's full send buffer and cut out our rows
         bufs = self._allgather_v(t)
         parts = []
@@ -365,7 +367,8 @@ class DistributedBuildSim:
             cq = [int(allc[q][k].item()) for k in range(size)]
             start = sum(cq[: self.comm.rank])
             parts.append(bufs[q][start:start + cq[self.comm.rank]])
-        return torch.cat(parts) if parts else t[:0]
+        out = torch.cat(parts) if parts else t[:0]
+        return (out, recv_counts) if return_counts else out
 
     # -- state --
     def load(self, pos, vel, mass=None, gid=None) -> None:
@@ -479,6 +482,7 @@ class DistributedBuildSim:
     def _forces(self, record_work: bool) -> None:
         p, eng, comm = self.p, self.eng, self.comm
         size, rank = comm.size, comm.rank
+        L = p.leaf_size
         n, keys, gid = self._sort()
         if self.splitters is None:
             self._initial_splitters(keys)
@@ -492,39 +496,89 @@ class DistributedBuildSim:
         fls = [(int(a[0].item()), int(a[1].item())) for a in allfl]
         prev = next((fls[q][1] for q in range(rank - 1, -1, -1) if fls[q][0] >= 0), None)
         nxt = next((fls[q][0] for q in range(rank + 1, size) if fls[q][0] >= 0), None)
-        nb = eng.sim_build_local(p.theta, p.leaf_size, prev, nxt) if n else 0
+        nb = eng.sim_build_local(p.theta, L, prev, nxt) if n else 0
         br = eng.sim_branch_export(nb)
         recs = eng.sim_walk_records() if n else torch.zeros((0, _REC_INTS), dtype=torch.int32, device=dev)
         bodies = self._export(_lib.BH_SIM_POS, n, (n, 4), torch.float32)
+        # branch nodes in body order (a top bucket's bodies must be contiguous)
+        perm = torch.argsort(br["lo"]) if nb else torch.zeros(0, dtype=torch.int64, device=dev)
+        br = {k: v[perm] for k, v in br.items()}
+        br["recs"] = recs[br["rec"].long()]
+        # bodies of the bucket-sized branch nodes (a top bucket spans several)
+        small = br["count"] <= L
+        cnt = br["count"][small].long()
+        lo = br["lo"][small].long()
+        tot = int(cnt.sum().item()) if cnt.numel() else 0
+        start = torch.cumsum(cnt, 0) - cnt
+        idx = torch.repeat_interleave(lo - start, cnt) + torch.arange(tot, device=dev)
+        bb_all = self._allgather_v(bodies[idx])
         br_all = {k: self._allgather_v(v) for k, v in br.items()}
-        recs_all = self._allgather_v(recs)
-        bodies_all = self._allgather_v(bodies)
-        self.tree = self._assemble(br_all, recs_all, [b.shape[0] for b in bodies_all])
-        gbodies = torch.cat(bodies_all)
+        # locally essential trees: what each peer's targets can open
+        box = torch.full((6,), float("inf"), dtype=torch.float64, device=dev)
+        box[3:] = -float("inf")
+        if n:
+            box[:3] = bodies[:, :3].min(0).values.double()
+            box[3:] = bodies[:, :3].max(0).values.double()
+        box[:3] -= self.let_pad
+        box[3:] += self.let_pad
+        allbox = [torch.zeros_like(box) for _ in range(size)]
+        self._allgather(allbox, box)
+        boxes = torch.stack(allbox).contiguous()
+        rc, bc = eng.sim_let(boxes, size, rank) if n else ([0] * size, [0] * size)
+        send_rec = torch.empty((sum(rc), _REC_INTS), dtype=torch.int32, device=dev)
+        send_bod = torch.empty((sum(bc), 4), dtype=torch.float32, device=dev)
+        mcounts = [0 if (q == rank or not n) else nb for q in range(size)]
+        send_map = torch.empty((sum(mcounts), 2), dtype=torch.int32, device=dev)
+        ro = bo = mo = 0
+        for q in range(size):
+            if mcounts[q] == 0 and rc[q] == 0:
+                continue
+            bmap = torch.empty((nb, 2), dtype=torch.int32, device=dev)
+            eng.sim_let_pack(q, send_rec[ro:], send_bod[bo:], bmap)
+            send_map[mo:mo + nb] = bmap[perm]
+            ro, bo, mo = ro + rc[q], bo + bc[q], mo + nb
+        let_rec, rcnt = self._alltoall_v(send_rec, rc, True)
+        let_bod, bcnt = self._alltoall_v(send_bod, bc, True)
+        let_map, mcnt = self._alltoall_v(send_map, mcounts, True)
+        nbb = sum(b.shape[0] for b in bb_all)
+        self.tree = self._assemble(br_all, recs, n, nbb, let_rec, rcnt, bcnt, let_map, mcnt)
+        self.let_stats = dict(records=int(let_rec.shape[0]), bodies=int(let_bod.shape[0]),
+                              sent_records=sum(rc), sent_bodies=sum(bc), own_records=int(recs.shape[0]))
+        gbodies = torch.cat([bodies] + list(bb_all) + [let_bod])
         acc = torch.zeros((n, 4), dtype=torch.float32, device=dev)
         work = torch.zeros(n, dtype=torch.int32, device=dev)
         if n:
-            eng.walk_records(self.tree, gbodies, bodies, p.eps, p.leaf_size, acc, work)
+            eng.walk_records(self.tree, gbodies, bodies, p.eps, L, acc, work)
             eng.sim_import(_lib.BH_SIM_ACC, 0, n, acc)
             if record_work:
                 eng.sim_import(_lib.BH_SIM_WORK, 0, n, work)
                 eng.sim_scatter_work()
-        self._keys, self._n = keys, n
+        self._keys, self._n, self._nb = keys, n, nb
+        self._acc, self._work = acc, work
 
-    def _assemble(self, br_all, recs_all, nbod) -> torch.Tensor:
-        """Global walk tree = [top region | rank 0 records | rank 1 records | ...].
+    def _assemble(self, br_all, recs, n, nbb, let_rec, rcnt, bcnt, let_map, mcnt) -> torch.Tensor:
+        """This rank's walk tree = [top region | own records | LET from each peer];
+        its body list = [own bodies | bucket-sized branch bodies | LET bodies].
 
         The top region holds the top cells (proper ancestors of the branch
         nodes, recombined exactly in fp64) in breadth-first order with
-        contiguous children, and copies of the branch-node records pointing
-        into their owner's records; bucket-sized top cells (count <= L) are
-        buckets over their globally contiguous bodies, as in one tree."""
+        contiguous children, and copies of the branch-node records: own ones
+        point into the own records, remote ones into that peer's LET (or are
+        closed when no target here can open them); bucket-sized top cells
+        (count <= L) are buckets over the branch bodies, as in one tree."""
         p = self.p
         dev = self.eng.device
-        size = self.comm.size
-        nrec = [r.shape[0] for r in recs_all]
-        bodoff = np.cumsum([0] + list(nbod))[:-1]
+        size, me = self.comm.size, self.comm.rank
+        L = p.leaf_size
+        nW = recs.shape[0]
+        BIG = 1 << 62
         rows = {}
+        bbpos = n
+        maps = {}
+        off = 0
+        for q in range(size):
+            maps[q] = let_map[off:off + mcnt[q]].cpu().numpy()
+            off += mcnt[q]
         for r in range(size):
             key = br_all["key"][r].cpu().numpy()
             if not len(key):
@@ -532,15 +586,16 @@ class DistributedBuildSim:
             lev = br_all["level"][r].cpu().numpy()
             cnt = br_all["count"][r].cpu().numpy()
             mom = br_all["mom"][r].cpu().numpy()
-            rec = br_all["rec"][r].cpu().numpy()
-            lo = br_all["lo"][r].cpu().numpy()
-            recs = recs_all[r][torch.as_tensor(rec, device=dev).long()].cpu().numpy()
+            brecs = br_all["recs"][r].cpu().numpy()
             for k in range(len(key)):
-                rows[int(key[k])] = dict(count=int(cnt[k]), mass=float(mom[k, 0]),
+                c = int(cnt[k])
+                rows[int(key[k])] = dict(count=c, mass=float(mom[k, 0]),
                                          com=tuple(float(x) for x in mom[k, 1:4]),
-                                         quad=tuple(float(x) for x in mom[k, 4:10]), rank=r,
-                                         rec=recs[k].copy(), glo=int(lo[k]) + int(bodoff[r]),
+                                         quad=tuple(float(x) for x in mom[k, 4:10]), rank=r, k=k,
+                                         rec=brecs[k].copy(), bb=bbpos if c <= L else BIG,
                                          level=int(lev[k]))
+                if c <= L:
+                    bbpos += c
         top = set()
         for key in rows:
             k = key >> 3
@@ -551,7 +606,7 @@ class DistributedBuildSim:
         for k in list(top) + list(rows):
             if k != 1 and (k >> 3) in children:
                 children[k >> 3].append(k)
-        mom = {k: (b["mass"], b["com"], b["quad"], b["count"], b["glo"]) for k, b in rows.items()}
+        mom = {k: (b["mass"], b["com"], b["quad"], b["count"], b["bb"]) for k, b in rows.items()}
         for k in sorted(top, key=lambda x: -x.bit_length()):  # deepest first (hashed.py:719-786)
             ch = sorted(children[k], key=lambda c: c & 7)  # slot order
             m, com, quad = _combine([mom[c][:3] for c in ch])
@@ -583,7 +638,7 @@ class DistributedBuildSim:
             while qi < len(queue):
                 k, at = queue[qi]
                 qi += 1
-                if k != 1 and mom[k][3] <= p.leaf_size:  # a bucket spanning ranks
+                if k != 1 and mom[k][3] <= L:  # a bucket spanning ranks
                     entries[at] = ("bucket", k)
                     continue
                 ch = sorted(children[k], key=lambda c: c & 7)
@@ -594,7 +649,8 @@ class DistributedBuildSim:
                         queue.append((c, len(entries) - 1))
                 entries[at] = ("top", k, first, len(ch))
         ntop = len(entries)
-        recoff = np.cumsum([0] + nrec)[:-1] + ntop
+        letoff = np.cumsum([0] + list(rcnt))[:-1] + ntop + nW
+        lbodoff = np.cumsum([0] + list(bcnt))[:-1] + n + nbb
         region = []
         for e in entries:
             if e[0] == "top":
@@ -604,14 +660,37 @@ class DistributedBuildSim:
             else:
                 b = rows[e[1]]
                 rec = b["rec"].copy()
-                rec[12] += recoff[b["rank"]] if rec[14] > 0 else bodoff[b["rank"]]
+                q = b["rank"]
+                if q == me:  # own subtree: first child in the own records, bodies at 0
+                    if rec[14] > 0:
+                        rec[12] += ntop
+                elif rec[14] > 0:
+                    fc = int(maps[q][b["k"], 0])
+                    if fc >= 0:
+                        rec[12] = fc + letoff[q]
+                    else:  # no target here opens it
+                        rec[12], rec[14] = -1, 0
+                elif b["count"] <= L:
+                    rec[12] = b["bb"]
+                else:
+                    fb = int(maps[q][b["k"], 1])
+                    rec[12] = fb + lbodoff[q] if fb >= 0 else -1
                 region.append(rec)
         parts = [torch.as_tensor(np.array(region, dtype=np.int32).reshape(-1, _REC_INTS), device=dev)]
-        for r in range(size):
-            x = recs_all[r].clone()
-            internal = x[:, 14] > 0
-            x[:, 12] = torch.where(internal, x[:, 12] + int(recoff[r]), x[:, 12] + int(bodoff[r]))
-            parts.append(x)
+        x = recs.clone()
+        x[:, 12] = torch.where(x[:, 14] > 0, x[:, 12] + ntop, x[:, 12])
+        parts.append(x)
+        o = 0
+        for q in range(size):
+            if rcnt[q] == 0:
+                continue
+            y = let_rec[o:o + rcnt[q]].clone()
+            o += rcnt[q]
+            internal = y[:, 14] > 0
+            withbod = (~internal) & (y[:, 13] > 1) & (y[:, 12] >= 0)
+            y[:, 12] = torch.where(internal, y[:, 12] + int(letoff[q]),
+                                   torch.where(withbod, y[:, 12] + int(lbodoff[q]), y[:, 12]))
+            parts.append(y)
         return torch.cat(parts).contiguous()
 
     def upload(self, pos, vel, acc, work, gid) -> None:

@@ -293,6 +293,16 @@ class Engine:
             check(self._L.bh_sim_walk_records(self._h, _ptr(out), ctypes.byref(n), self.stream))
         return out
 
+    def sim_let(self, boxes: torch.Tensor, nrank: int, self_rank: int):
+        """LET sizes (records, bodies) per receiver; boxes float64 [nrank, 6]."""
+        rc = (ctypes.c_int64 * nrank)()
+        bc = (ctypes.c_int64 * nrank)()
+        check(self._L.bh_sim_let(self._h, _ptr(boxes), int(nrank), int(self_rank), rc, bc, self.stream))
+        return list(rc), list(bc)
+
+    def sim_let_pack(self, q: int, recs: torch.Tensor, bodies: torch.Tensor, bmap: torch.Tensor) -> None:
+        check(self._L.bh_sim_let_pack(self._h, int(q), _ptr(recs), _ptr(bodies), _ptr(bmap), self.stream))
+
     def walk_records(self, records: torch.Tensor, bodies: torch.Tensor, targets: torch.Tensor,
                      eps: float, leaf_size: int, acc: torch.Tensor, work: torch.Tensor | None) -> None:
         check(self._L.bh_walk_records_f32(self._h, _ptr(records), records.shape[0], _ptr(bodies),

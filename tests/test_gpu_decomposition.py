@@ -81,6 +81,7 @@ def _run_build(ranks, b, steps, theta=0.6, eps=1e-3, leaf=16, dt=1e-3):
     n = len(b)
     comms = ThreadComm.group(ranks)
     outs = [None] * ranks
+    lets = [None] * ranks
     err = []
     cuts = np.linspace(0, n, ranks + 1).astype(int)
 
@@ -98,6 +99,7 @@ def _run_build(ranks, b, steps, theta=0.6, eps=1e-3, leaf=16, dt=1e-3):
             p, v, a, w, g = sim.store()
             eng.check()
             outs[r] = tuple(x.cpu().numpy() for x in (p, v, a, w, g))
+            lets[r] = sim.let_stats
             eng.close()
         except Exception as e:  # pragma: no cover
             import traceback
@@ -120,6 +122,7 @@ def _run_build(ranks, b, steps, theta=0.6, eps=1e-3, leaf=16, dt=1e-3):
         seen[g] += 1
     assert np.all(seen == 1), "every body owned by exactly one rank"
     res["counts"] = [len(o[4]) for o in outs]
+    res["let"] = lets
     return res
 
 
@@ -170,3 +173,8 @@ def test_distributed_build_clustered_multi_step():
     err = np.linalg.norm(got["acc"][:, :3] - ref["acc"][:, :3]) / np.linalg.norm(ref["acc"][:, :3])
     assert err < 1e-5
     assert min(got["counts"]) > 0.2 * len(b) / 4
+    # the locally essential trees are a strict subset of the peers' trees
+    own = sum(s["own_records"] for s in got["let"])
+    for s in got["let"]:
+        assert s["records"] < own - s["own_records"], got["let"]
+    print("LET", got["let"])
