@@ -157,9 +157,17 @@ def run_ours(args, cfg) -> dict | None:
     from paper_2203_08966_b200.engine import Engine
 
     ws, rank, local = dist_setup()
+    # BH_DIST_BACKEND=gloo + BH_SHARE_GPU=1: several ranks on one GPU with
+    # host-staged collectives (a smoke run of the multi-rank path, not a number)
+    backend = os.environ.get("BH_DIST_BACKEND", "nccl")
+    if os.environ.get("BH_SHARE_GPU") == "1":
+        local = 0
     torch.cuda.set_device(local)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
     b = make_bodies(cfg)
     n = len(b)
@@ -284,8 +292,9 @@ def run_ours(args, cfg) -> dict | None:
     eng.check()
 
     # ---- max over ranks
-    t = torch.tensor([total_ms, e2e_ms], dtype=torch.float64, device=dev)
-    work = torch.tensor([pp + pc, e2e_inter, pp, pc], dtype=torch.float64, device=dev)
+    rdev = dev if backend == "nccl" else "cpu"
+    t = torch.tensor([total_ms, e2e_ms], dtype=torch.float64, device=rdev)
+    work = torch.tensor([pp + pc, e2e_inter, pp, pc], dtype=torch.float64, device=rdev)
     if ws > 1:  # each rank walked its own zone: interactions sum, time is the max
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.all_reduce(work, op=dist.ReduceOp.SUM)
@@ -326,7 +335,8 @@ def run_ours(args, cfg) -> dict | None:
             "config": {"workload": args.config, "n_bodies": n, "theta": theta, "eps": eps,
                        "leaf_size": leaf, "dt": dt, "precision": "fp32",
                        "parallelism": ((f"{ws} ranks: costzones key ranges, body migration, "
-                                        "distributed build, branch-node + walk-record allgather")
+                                        "distributed build, branch-node allgather, "
+                                        "locally-essential-tree all-to-all")
                                        if args.decomp == "distributed" else
                                        (f"{ws} ranks: replicated tree, costzones-partitioned walk, "
                                         "NCCL all-reduce of zone accelerations")) if ws > 1 else "single GPU",

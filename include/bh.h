@@ -62,7 +62,8 @@ enum {
   BH_PHASE_PERMUTE = 3,   /* body gather into Morton order */
   BH_PHASE_BUILD = 4,     /* lcp, scan, cell count, emit, moments */
   BH_PHASE_WALK = 5,      /* traversal */
-  BH_NPHASES = 6
+  BH_PHASE_LET = 6,       /* locally-essential-tree marking and packing (distributed build) */
+  BH_NPHASES = 7
 };
 
 /* ---- lifecycle ---------------------------------------------------------- */
@@ -199,12 +200,13 @@ int bh_sim_walk_records(bh_handle *h, void *d_out, int64_t *n_out, void *stream)
 /* Locally essential trees: for every other rank q, the cells of
  * this rank's subtrees that a target inside q's bounding box could open under a
  * conservative box-MAC, plus the bucket bodies it could resolve (replaces the
- * reference's on-demand child fetches, hashed.py:831-911).  d_boxes: [nrank][6]
- * device doubles (min xyz, max xyz).  let: sizes per receiver (host arrays,
+ * reference's on-demand child fetches, hashed.py:831-911).  d_boxes:
+ * [nrank][nbox][6] device doubles (min xyz, max xyz; empty boxes have min > max)
+ * whose union covers each rank's bodies.  let: sizes per receiver (host arrays,
  * synchronises); let_pack: the receiver's records, bodies and branch map
  * ([nbranch][2] ints: first child in the LET | -1, first body | -1). */
-int bh_sim_let(bh_handle *h, const double *d_boxes, int nrank, int self, int64_t *rec_counts,
-               int64_t *body_counts, void *stream);
+int bh_sim_let(bh_handle *h, const double *d_boxes, int nbox, int nrank, int self,
+               int64_t *rec_counts, int64_t *body_counts, void *stream);
 int bh_sim_let_pack(bh_handle *h, int q, void *d_rec_out, float *d_bodies_out, int32_t *d_bmap_out,
                     void *stream);
 int bh_walk_records_f32(bh_handle *h, const void *d_records, int64_t nrec, const float *d_bodies4,

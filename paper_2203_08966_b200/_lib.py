@@ -45,7 +45,7 @@ EXPORTS = (
     "bh_ic_plummer", "bh_host_potential_pairs",
 )
 BH_SIM_ACC, BH_SIM_WORK, BH_SIM_PREV_WORK, BH_SIM_POS, BH_SIM_VEL, BH_SIM_ID, BH_SIM_KEYS = range(7)
-PHASES = ("integrate", "keys", "sort", "permute", "build", "walk")
+PHASES = ("integrate", "keys", "sort", "permute", "build", "walk", "let")
 
 
 class BHStats(ctypes.Structure):
@@ -116,7 +116,7 @@ def _declare(L: ctypes.CDLL) -> None:
         "bh_sim_branch_export": ([P, P, P, P, P, P, P, P], I),
         "bh_sim_walk_records": ([P, P, ctypes.POINTER(I64), P], I),
         "bh_walk_records_f32": ([P, P, I64, P, P, I64, D, I, P, P, P], I),
-        "bh_sim_let": ([P, P, I, I, ctypes.POINTER(I64), ctypes.POINTER(I64), P], I),
+        "bh_sim_let": ([P, P, I, I, I, ctypes.POINTER(I64), ctypes.POINTER(I64), P], I),
         "bh_sim_let_pack": ([P, I, P, P, P, P], I),
         "bh_timing_enable": ([P, I], I),
         "bh_timing_reset": ([P], I),

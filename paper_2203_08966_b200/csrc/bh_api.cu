@@ -76,7 +76,8 @@ struct bh_handle {
   int64_t nbranch = 0;
   // locally essential trees of the last build_local
   Buf let_present, let_expand, let_bodies, let_isbranch, let_rflag, let_bcount, let_rpos,
-      let_bpos, let_scan_tmp, let_brec;
+      let_bpos, let_scan_tmp, let_brec, let_tail;
+  uint32_t *hlet = nullptr;  // pinned: LET sizes per receiver
   int let_nrank = 0;
   int64_t let_nrec = 0;
   double R = 1.0;
@@ -491,13 +492,18 @@ int sim_sort(bh_handle *h, cudaStream_t s) {
   const bool f32 = h->precision == BH_FP32;
   BH_TRY(ensure_sort(h, n));
   if (n == 0) return BH_OK;
+  h->tbegin(BH_PHASE_KEYS, s);
   if (f32)
     launch_keys_f32(h->pos.as<float4>(), n, h->dR, h->keys.as<uint64_t>(), h->vals.as<uint32_t>(),
                     h->flags, s);
   else
     launch_keys_f64(h->pos.as<double>(), 4, n, h->dR, h->keys.as<uint64_t>(),
                     h->vals.as<uint32_t>(), h->flags, s);
+  h->tend(s);
+  h->tbegin(BH_PHASE_SORT, s);
   BH_TRY(sort_keys(h, n, s));
+  h->tend(s);
+  h->tbegin(BH_PHASE_PERMUTE, s);
   if (f32)
     launch_gather_f32(h->vals2.as<uint32_t>(), n, h->pos.as<float4>(), h->pos2.as<float4>(),
                       h->vel.as<float4>(), h->vel2.as<float4>(), h->id.as<uint32_t>(),
@@ -521,6 +527,7 @@ int sim_sort(bh_handle *h, cudaStream_t s) {
   }
   h->launches += 4;
   BH_LAUNCHED();
+  h->tend(s);
   return BH_OK;
 }
 
@@ -623,6 +630,7 @@ int bh_create(bh_handle **out, int device, int precision) {
   BH_CUDA(cudaMallocHost(&h->hstat, sizeof(int) * (kMaxLevel + 4)));
   BH_CUDA(cudaMallocHost(&h->hR, sizeof(double)));
   BH_CUDA(cudaMallocHost(&h->hlvl, sizeof(int) * (kMaxLevel + 2)));
+  BH_CUDA(cudaMallocHost(&h->hlet, sizeof(uint32_t) * 4 * 32));
   DeviceFlags init;
   memset(&init, 0, sizeof(init));
   init.first_bad = 0x7fffffffffffffffll;
@@ -642,7 +650,7 @@ int bh_destroy(bh_handle *h) {
                  &h->bk_pos, &h->bk_vel, &h->bk_acc, &h->bk_id, &h->bk_work,
                  &h->shared, &h->branch, &h->rec_of_cell, &h->wparent, &h->let_present,
                  &h->let_expand, &h->let_bodies, &h->let_isbranch, &h->let_rflag, &h->let_bcount,
-                 &h->let_rpos, &h->let_bpos, &h->let_scan_tmp, &h->let_brec};
+                 &h->let_rpos, &h->let_bpos, &h->let_scan_tmp, &h->let_brec, &h->let_tail};
   for (Buf *b : bufs) b->release();
   cudaFree(h->flags);
   cudaFreeHost(h->hflags);
@@ -653,6 +661,7 @@ int bh_destroy(bh_handle *h) {
   cudaFreeHost(h->hstat);
   cudaFreeHost(h->hR);
   cudaFreeHost(h->hlvl);
+  cudaFreeHost(h->hlet);
   h->fold_marks();
   for (cudaEvent_t e : h->pool) cudaEventDestroy(e);
   delete h;
@@ -1065,6 +1074,7 @@ int bh_sim_build_local(bh_handle *h, double theta, int leaf_size, int has_prev, 
   h->bnd_prev = has_prev ? lcp_host(prev_key, kfirst) : -1;
   h->bnd_next = has_next ? lcp_host(klast, next_key) : -1;
   const int allow_dup = h->allow_dup || leaf_size > 1;
+  h->tbegin(BH_PHASE_BUILD, s);
   int rc = build_sorted(h, n, h->pos.as<float4>(), nullptr, s, allow_dup);
   if (rc != BH_OK) { h->bnd_prev = h->bnd_next = -1; return rc; }
   const int64_t C = h->C;
@@ -1086,6 +1096,7 @@ int bh_sim_build_local(bh_handle *h, double theta, int leaf_size, int has_prev, 
   h->walk_valid = false;  // a forced-shared walk tree is not the local-walk tree
   int nb = 0;
   BH_CUDA(cudaMemcpyAsync(&nb, h->branch.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  h->tend(s);
   BH_CUDA(cudaStreamSynchronize(s));
   BH_LAUNCHED();
   h->nbranch = nb;
@@ -1114,13 +1125,13 @@ __global__ void k_mark_branch_recs(const int *branch, int nb, const int *rec_of_
 }
 
 // Locally essential trees of this rank's last bh_sim_build_local for every
-// other rank: d_boxes = [nrank][6] (min xyz, max xyz) of each
-// rank's bodies.  Fills rec_counts / body_counts (host, [nrank]) with the LET
+// other rank: d_boxes = [nrank][nbox][6] (min xyz, max xyz)
+// covering each rank's bodies (empty boxes: min > max).  Fills rec_counts / body_counts (host, [nrank]) with the LET
 // sizes for each receiver (0 for self).  Synchronises.
-int bh_sim_let(bh_handle *h, const double *d_boxes, int nrank, int self, int64_t *rec_counts,
-               int64_t *body_counts, void *stream) {
-  if (!h || !d_boxes || nrank < 1 || nrank > 32 || self < 0 || self >= nrank || !rec_counts ||
-      !body_counts)
+int bh_sim_let(bh_handle *h, const double *d_boxes, int nbox, int nrank, int self,
+               int64_t *rec_counts, int64_t *body_counts, void *stream) {
+  if (!h || !d_boxes || nbox < 1 || nrank < 1 || nrank > 32 || self < 0 || self >= nrank ||
+      !rec_counts || !body_counts)
     return fail(BH_BAD_ARG, "bh_sim_let: bad args");
   cudaStream_t s = S(stream);
   int cp = 0;
@@ -1138,16 +1149,18 @@ int bh_sim_let(bh_handle *h, const double *d_boxes, int nrank, int self, int64_t
   BH_CUDA(h->let_isbranch.ensure(n + 16));
   BH_CUDA(h->let_brec.ensure(sizeof(int) * (h->nbranch + 1)));
   BH_CUDA(h->let_scan_tmp.ensure(scan_temp_bytes(n) + 16));
+  h->tbegin(BH_PHASE_LET, s);
   BH_CUDA(cudaMemsetAsync(h->let_isbranch.p, 0, n, s));
   if (h->nbranch > 0)
     k_mark_branch_recs<<<grid_for(h->nbranch, 128), 128, 0, s>>>(
         h->branch.as<int>() + 1, (int)h->nbranch, h->rec_of_cell.as<int>(), h->let_isbranch.as<uint8_t>(),
         h->let_brec.as<int>());
   const WalkNode *W = h->wnodes.as<WalkNode>();
-  launch_let_mark(W, (int)n, h->wparent.as<int>(), h->let_isbranch.as<uint8_t>(), d_boxes, nrank, self,
+  launch_let_mark(W, (int)n, h->wparent.as<int>(), h->let_isbranch.as<uint8_t>(), d_boxes, nbox, nrank, self,
                   h->let_present.as<uint32_t>(), h->let_expand.as<uint32_t>(),
                   h->let_bodies.as<uint32_t>(), s);
-  std::vector<uint32_t> tail(4 * nrank, 0);
+  BH_CUDA(h->let_tail.ensure(sizeof(uint32_t) * 4 * nrank));
+  BH_CUDA(cudaMemsetAsync(h->let_tail.p, 0, sizeof(uint32_t) * 4 * nrank, s));
   for (int q = 0; q < nrank; ++q) {
     if (q == self) continue;
     uint32_t *rpos = h->let_rpos.as<uint32_t>() + (n + 1) * q;
@@ -1159,14 +1172,16 @@ int bh_sim_let(bh_handle *h, const double *d_boxes, int nrank, int self, int64_t
                                rpos, n, s));
     BH_CUDA(exclusive_scan_u32(h->let_scan_tmp.p, h->let_scan_tmp.bytes, h->let_bcount.as<uint32_t>(),
                                bpos, n, s));
-    BH_CUDA(cudaMemcpyAsync(&tail[4 * q], rpos + n - 1, 4, cudaMemcpyDeviceToHost, s));
-    BH_CUDA(cudaMemcpyAsync(&tail[4 * q + 1], h->let_rflag.as<uint32_t>() + n - 1, 4,
-                            cudaMemcpyDeviceToHost, s));
-    BH_CUDA(cudaMemcpyAsync(&tail[4 * q + 2], bpos + n - 1, 4, cudaMemcpyDeviceToHost, s));
-    BH_CUDA(cudaMemcpyAsync(&tail[4 * q + 3], h->let_bcount.as<uint32_t>() + n - 1, 4,
-                            cudaMemcpyDeviceToHost, s));
-    BH_CUDA(cudaStreamSynchronize(s));  // tail[] is pageable host memory
+    uint32_t *tl = h->let_tail.as<uint32_t>() + 4 * q;  // device copies; one D2H below
+    BH_CUDA(cudaMemcpyAsync(tl, rpos + n - 1, 4, cudaMemcpyDeviceToDevice, s));
+    BH_CUDA(cudaMemcpyAsync(tl + 1, h->let_rflag.as<uint32_t>() + n - 1, 4, cudaMemcpyDeviceToDevice, s));
+    BH_CUDA(cudaMemcpyAsync(tl + 2, bpos + n - 1, 4, cudaMemcpyDeviceToDevice, s));
+    BH_CUDA(cudaMemcpyAsync(tl + 3, h->let_bcount.as<uint32_t>() + n - 1, 4, cudaMemcpyDeviceToDevice, s));
   }
+  h->tend(s);
+  BH_CUDA(cudaMemcpyAsync(h->hlet, h->let_tail.p, sizeof(uint32_t) * 4 * nrank, cudaMemcpyDeviceToHost, s));
+  BH_CUDA(cudaStreamSynchronize(s));
+  const uint32_t *tail = h->hlet;
   for (int q = 0; q < nrank; ++q) {
     if (q == self) continue;
     rec_counts[q] = (int64_t)tail[4 * q] + tail[4 * q + 1];
@@ -1187,6 +1202,7 @@ int bh_sim_let_pack(bh_handle *h, int q, void *d_rec_out, float *d_bodies_out, i
   const int64_t n = h->let_nrec;
   if (n == 0) return BH_OK;
   const WalkNode *W = h->wnodes.as<WalkNode>();
+  h->tbegin(BH_PHASE_LET, s);
   const uint32_t *rpos = h->let_rpos.as<uint32_t>() + (n + 1) * q;
   const uint32_t *bpos = h->let_bpos.as<uint32_t>() + (n + 1) * q;
   launch_let_flags(W, (int)n, h->let_isbranch.as<uint8_t>(), h->let_present.as<uint32_t>(),
@@ -1199,6 +1215,7 @@ int bh_sim_let_pack(bh_handle *h, int q, void *d_rec_out, float *d_bodies_out, i
   launch_let_branchmap(W, h->let_brec.as<int>(), (int)h->nbranch, h->let_expand.as<uint32_t>(),
                        h->let_bodies.as<uint32_t>(), q, rpos, bpos, reinterpret_cast<int2 *>(d_bmap_out),
                        s);
+  h->tend(s);
   h->launches += 3;
   BH_LAUNCHED();
   return BH_OK;
@@ -1227,9 +1244,11 @@ int bh_walk_records_f32(bh_handle *h, const void *d_records, int64_t nrec, const
     return fail(BH_BAD_ARG, "bh_walk_records_f32: bad args");
   cudaStream_t s = S(stream);
   BH_TRY(reset_counters(h, s));
+  h->tbegin(BH_PHASE_WALK, s);
   launch_walk_f32(static_cast<const WalkNode *>(d_records), reinterpret_cast<const float4 *>(d_bodies4),
                   d_targets4, 4, nullptr, (int)nt, (float)(eps * eps), leaf_size, d_acc4, 4, nullptr,
                   d_work, h->flags, s);
+  h->tend(s);
   h->launches += 1;
   BH_LAUNCHED();
   return BH_OK;

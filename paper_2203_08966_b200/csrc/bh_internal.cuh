@@ -162,8 +162,8 @@ void launch_walk_tree(const TreeView &t, const double *dR, double theta, int lea
                       int *wparent = nullptr);
 // locally essential trees (bh_walk.cu)
 void launch_let_mark(const WalkNode *W, int nrec, const int *wparent, const uint8_t *isbranch,
-                     const double *boxes, int nrank, int self, uint32_t *present, uint32_t *expand,
-                     uint32_t *bodies, cudaStream_t s);
+                     const double *boxes, int nbox, int nrank, int self, uint32_t *present,
+                     uint32_t *expand, uint32_t *bodies, cudaStream_t s);
 void launch_let_flags(const WalkNode *W, int nrec, const uint8_t *isbranch, const uint32_t *present,
                       const uint32_t *bodies, int q, uint32_t *rflag, uint32_t *bcount, cudaStream_t s);
 void launch_let_pack(const WalkNode *W, int nrec, const uint8_t *isbranch, const uint32_t *expand,

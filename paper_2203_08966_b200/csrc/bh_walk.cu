@@ -141,29 +141,38 @@ void launch_walk_tree(const TreeView &t, const double *dR, double theta, int lea
 
 // ------------------------------------------------ locally essential trees
 // Conservative box-MAC: a record is taken (pc) by every target
-// in the box if even the box point nearest its com passes the MAC with a
-// relative margin that covers the fp32 rounding of d2 on the receiving side.
-__device__ __forceinline__ bool accepted_by_all(const WalkNode &r, const double *box) {
-  const double cx = -(double)r.a.x, cy = -(double)r.a.y, cz = -(double)r.a.z;
-  const double c[3] = {cx, cy, cz};
-  double d2 = 0.0;
-  for (int a = 0; a < 3; ++a) {
-    const double lo = box[a], hi = box[3 + a];
-    const double g = c[a] < lo ? lo - c[a] : (c[a] > hi ? c[a] - hi : 0.0);
-    d2 += g * g;
+// of a receiver if, for each of the receiver's target boxes, even the box point
+// nearest its com passes the MAC with a relative margin that covers the fp32
+// rounding of d2 on the receiving side.  Empty boxes (lo > hi) never object.
+// box[0] is the union of the receiver's boxes: passing it passes them all.
+__device__ __forceinline__ bool accepted_by_all(const WalkNode &r, const double *box, int nbox) {
+  const double c[3] = {-(double)r.a.x, -(double)r.a.y, -(double)r.a.z};
+  const double lim = (double)r.a.w * (1.0 + 1e-5) + 1e-30;
+  for (int k = 0; k < nbox; ++k, box += 6) {
+    double d2 = 0.0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double lo = box[a], hi = box[3 + a];
+      const double g = c[a] < lo ? lo - c[a] : (c[a] > hi ? c[a] - hi : 0.0);
+      d2 += g * g;
+    }
+    if (d2 > lim) {
+      if (k == 0) return true;  // clear of the union box
+    } else if (k > 0 || nbox == 1) {
+      return false;
+    }
   }
-  const double mac2 = (double)r.a.w;
-  return d2 > mac2 * (1.0 + 1e-5) + 1e-30;
+  return true;  // near the union, but clear of every member box
 }
 
 // One level of the top-down marking, for all receivers at once (bit q):
 // present = the receiver's walk can reach the record (branch roots always;
 // otherwise its parent is expanded); expand = present and not taken by all
 // of the receiver's targets (its children are needed); bodies = present bucket
-// not taken by all (its bodies are needed).
+// not taken by all (its bodies are needed).  boxes: [nrank][nbox][6].
 __global__ void k_let_mark(const WalkNode *__restrict__ W, int nrec, const int *__restrict__ wparent,
                            const uint8_t *__restrict__ isbranch, const double *__restrict__ boxes,
-                           int nrank, int self, int level, uint32_t *__restrict__ present,
+                           int nbox, int nrank, int self, int level, uint32_t *__restrict__ present,
                            uint32_t *__restrict__ expand, uint32_t *__restrict__ bodies) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= nrec) return;
@@ -175,7 +184,7 @@ __global__ void k_let_mark(const WalkNode *__restrict__ W, int nrec, const int *
   if (p && r.d.y > 1) {
     uint32_t fail = 0;
     for (int q = 0; q < nrank; ++q)
-      if (((p >> q) & 1u) && !accepted_by_all(r, boxes + 6 * q)) fail |= 1u << q;
+      if (((p >> q) & 1u) && !accepted_by_all(r, boxes + (size_t)6 * nbox * q, nbox)) fail |= 1u << q;
     if (r.d.z > 0) e = p & fail;
     else b = p & fail;
   }
@@ -229,12 +238,12 @@ __global__ void k_let_branchmap(const WalkNode *__restrict__ W, const int *__res
 }
 
 void launch_let_mark(const WalkNode *W, int nrec, const int *wparent, const uint8_t *isbranch,
-                     const double *boxes, int nrank, int self, uint32_t *present, uint32_t *expand,
-                     uint32_t *bodies, cudaStream_t s) {
+                     const double *boxes, int nbox, int nrank, int self, uint32_t *present,
+                     uint32_t *expand, uint32_t *bodies, cudaStream_t s) {
   if (nrec <= 0) return;
   for (int l = 0; l <= kMaxLevel; ++l)
-    k_let_mark<<<grid_for(nrec, 256), 256, 0, s>>>(W, nrec, wparent, isbranch, boxes, nrank, self, l,
-                                                   present, expand, bodies);
+    k_let_mark<<<grid_for(nrec, 256), 256, 0, s>>>(W, nrec, wparent, isbranch, boxes, nbox, nrank, self,
+                                                   l, present, expand, bodies);
 }
 void launch_let_flags(const WalkNode *W, int nrec, const uint8_t *isbranch, const uint32_t *present,
                       const uint32_t *bodies, int q, uint32_t *rflag, uint32_t *bcount, cudaStream_t s) {
@@ -259,9 +268,12 @@ void launch_let_branchmap(const WalkNode *W, const int *brec, int nb, const uint
 __device__ __forceinline__ float2 f2(float x, float y) { return make_float2(x, y); }
 __device__ __forceinline__ float2 f2(float x) { return make_float2(x, x); }
 
-constexpr int kWalkBlock = 256;
+#ifndef BH_WALK_BLOCK
+#define BH_WALK_BLOCK 128  // 4 warps; 8 blocks/SM at <= 64 registers
+#endif
+constexpr int kWalkBlock = BH_WALK_BLOCK;
 #ifndef BH_WALK_MINB
-#define BH_WALK_MINB 4  // blocks/SM the register budget must allow (4 -> <= 64 regs)
+#define BH_WALK_MINB (1024 / BH_WALK_BLOCK)  // blocks/SM the register budget must allow (<= 64 regs)
 #endif
 constexpr int kStack = 8 * (kMaxLevel + 1) + 8;  // <= 8 pending siblings per level
 

@@ -89,7 +89,9 @@ class Comm:
 
 
 class TorchComm(Comm):
-    """torch.distributed collectives (NCCL for CUDA tensors, gloo on CPU)."""
+    """torch.distributed collectives: NCCL on CUDA tensors.  Under a gloo
+    group CUDA tensors are staged through host memory (tests, and several
+    ranks sharing one GPU for a smoke run)."""
 
     def __init__(self, group=None):
         import torch.distributed as dist
@@ -98,12 +100,41 @@ class TorchComm(Comm):
         self.group = group
         self.rank = dist.get_rank(group)
         self.size = dist.get_world_size(group)
+        self.staged = dist.get_backend(group) == "gloo"
+
+    def _host(self, t):
+        return t.cpu() if (self.staged and t.is_cuda) else t
+
+    def _reduce(self, t, op):
+        h = self._host(t)
+        self.dist.all_reduce(h, op=op, group=self.group)
+        if h is not t:
+            t.copy_(h)
 
     def allreduce_sum_(self, t):
-        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
+        self._reduce(t, self.dist.ReduceOp.SUM)
 
     def allreduce_max_(self, t):
-        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        self._reduce(t, self.dist.ReduceOp.MAX)
+
+    def allgather(self, outs, t):
+        h = self._host(t)
+        if h is t:
+            self.dist.all_gather(outs, t, group=self.group)
+            return
+        hs = [torch.empty_like(h) for _ in outs]
+        self.dist.all_gather(hs, h.contiguous(), group=self.group)
+        for o, x in zip(outs, hs):
+            o.copy_(x)
+
+    def alltoall_single(self, out, t, recv_counts, send_counts):
+        h = self._host(t)
+        if h is t:
+            self.dist.all_to_all_single(out, t, recv_counts, send_counts, group=self.group)
+            return
+        ho = torch.empty(out.shape, dtype=out.dtype)
+        self.dist.all_to_all_single(ho, h.contiguous(), recv_counts, send_counts, group=self.group)
+        out.copy_(ho)
 
     def barrier(self):
         self.dist.barrier(group=self.group)
@@ -332,7 +363,7 @@ class DistributedBuildSim:
 
     def _allgather(self, outs, t):
         if isinstance(self.comm, TorchComm):
-            self.comm.dist.all_gather(outs, t, group=self.comm.group)
+            self.comm.allgather(outs, t)
         elif isinstance(self.comm, ThreadComm):
             hub = self.comm.hub
             if t.is_cuda:
@@ -357,8 +388,7 @@ class DistributedBuildSim:
         recv_counts = [int(allc[q][self.comm.rank].item()) for q in range(size)]
         if isinstance(self.comm, TorchComm):
             out = torch.empty((sum(recv_counts),) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
-            self.comm.dist.all_to_all_single(out, t.contiguous(), recv_counts, send_counts,
-                                             group=self.comm.group)
+            self.comm.alltoall_single(out, t.contiguous(), recv_counts, send_counts)
             return (out, recv_counts) if return_counts else out
         # thread / single: gather everyone's full send buffer and cut out our rows
         bufs = self._allgather_v(t)
@@ -513,18 +543,15 @@ class DistributedBuildSim:
         idx = torch.repeat_interleave(lo - start, cnt) + torch.arange(tot, device=dev)
         bb_all = self._allgather_v(bodies[idx])
         br_all = {k: self._allgather_v(v) for k, v in br.items()}
-        # locally essential trees: what each peer's targets can open
-        box = torch.full((6,), float("inf"), dtype=torch.float64, device=dev)
-        box[3:] = -float("inf")
-        if n:
-            box[:3] = bodies[:, :3].min(0).values.double()
-            box[3:] = bodies[:, :3].max(0).values.double()
-        box[:3] -= self.let_pad
-        box[3:] += self.let_pad
-        allbox = [torch.zeros_like(box) for _ in range(size)]
-        self._allgather(allbox, box)
+        # locally essential trees: what each peer's targets can open.
+        # Target region = tight boxes of this rank's bodies per group of branch
+        # nodes (a key range is not a box: one box per rank would cover most of
+        # the domain and send nearly whole subtrees).
+        boxes = self._target_boxes(bodies, br, n, nb)
+        allbox = [torch.zeros_like(boxes) for _ in range(size)]
+        self._allgather(allbox, boxes)
         boxes = torch.stack(allbox).contiguous()
-        rc, bc = eng.sim_let(boxes, size, rank) if n else ([0] * size, [0] * size)
+        rc, bc = eng.sim_let(boxes, rank) if n else ([0] * size, [0] * size)
         send_rec = torch.empty((sum(rc), _REC_INTS), dtype=torch.int32, device=dev)
         send_bod = torch.empty((sum(bc), 4), dtype=torch.float32, device=dev)
         mcounts = [0 if (q == rank or not n) else nb for q in range(size)]
@@ -555,6 +582,32 @@ class DistributedBuildSim:
                 eng.sim_scatter_work()
         self._keys, self._n, self._nb = keys, n, nb
         self._acc, self._work = acc, work
+
+    LET_BOXES = 64  # target boxes per rank (groups of consecutive branch nodes)
+
+    def _target_boxes(self, bodies, br, n, nb):
+        """[1 + LET_BOXES, 6] float64 (min xyz, max xyz): the union box, then the
+        boxes of groups of consecutive branch nodes; unused boxes are empty
+        (min > max)."""
+        K = self.LET_BOXES
+        dev = bodies.device
+        box = torch.empty((K + 1, 6), dtype=torch.float64, device=dev)
+        box[:, :3] = float("inf")
+        box[:, 3:] = -float("inf")
+        if n == 0 or nb == 0:
+            return box
+        lo = br["lo"].long()  # branch nodes in body order; they partition the bodies
+        gid_branch = (torch.arange(nb, device=dev) * K) // nb
+        bidx = torch.searchsorted(lo, torch.arange(n, device=dev), right=True) - 1
+        g = gid_branch[bidx].view(-1, 1).expand(-1, 3)
+        x = bodies[:, :3].double()
+        box[1:, :3] = box[1:, :3].scatter_reduce(0, g, x, reduce="amin")
+        box[1:, 3:] = box[1:, 3:].scatter_reduce(0, g, x, reduce="amax")
+        box[0, :3] = x.min(0).values  # the union first: a cheap accept for far cells
+        box[0, 3:] = x.max(0).values
+        box[:, :3] -= self.let_pad
+        box[:, 3:] += self.let_pad
+        return box
 
     def _assemble(self, br_all, recs, n, nbb, let_rec, rcnt, bcnt, let_map, mcnt) -> torch.Tensor:
         """This rank's walk tree = [top region | own records | LET from each peer];

@@ -293,11 +293,12 @@ class Engine:
             check(self._L.bh_sim_walk_records(self._h, _ptr(out), ctypes.byref(n), self.stream))
         return out
 
-    def sim_let(self, boxes: torch.Tensor, nrank: int, self_rank: int):
-        """LET sizes (records, bodies) per receiver; boxes float64 [nrank, 6]."""
+    def sim_let(self, boxes: torch.Tensor, self_rank: int):
+        """LET sizes (records, bodies) per receiver; boxes float64 [nrank, nbox, 6]."""
+        nrank, nbox = int(boxes.shape[0]), int(boxes.shape[1])
         rc = (ctypes.c_int64 * nrank)()
         bc = (ctypes.c_int64 * nrank)()
-        check(self._L.bh_sim_let(self._h, _ptr(boxes), int(nrank), int(self_rank), rc, bc, self.stream))
+        check(self._L.bh_sim_let(self._h, _ptr(boxes), nbox, nrank, int(self_rank), rc, bc, self.stream))
         return list(rc), list(bc)
 
     def sim_let_pack(self, q: int, recs: torch.Tensor, bodies: torch.Tensor, bmap: torch.Tensor) -> None:

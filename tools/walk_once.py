@@ -1,0 +1,15 @@
+"""Run the cfg2 force pass a few times (profiling target: ncu -k regex:k_walk)."""
+import sys, torch
+sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
+from paper_2203_08966_b200.engine import Engine
+from paper_2203_08966_b200.initcond import make_rng, plummer_cluster
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_000
+b = plummer_cluster(n, make_rng(2), 1.0)
+eng = Engine("fp32", 0)
+eng.sim_load(eng.bodies_tensor(b.position, b.mass), eng.vec_tensor(b.velocity))
+for _ in range(3):
+    eng.sim_forces(0.6, 1e-3, 16, True)
+torch.cuda.synchronize()
+eng.check()
+print("ok", eng.stats().interactions)
