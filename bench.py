@@ -32,6 +32,8 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+AUTO_DISTRIBUTED_N = 5_000_000  # --decomp auto: distributed build from this many bodies
+
 CONFIGS = {
     "cfg1": dict(n=100_000, seed=1, theta=0.5, eps=1e-3, leaf=16, dt=1e-3, kind="plummer"),
     "cfg2": dict(n=1_000_000, seed=2, theta=0.6, eps=1e-3, leaf=16, dt=1e-3, kind="plummer"),
@@ -482,10 +484,14 @@ def main() -> None:
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="cfg2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--decomp", choices=["distributed", "replicated"], default="distributed",
+    ap.add_argument("--decomp", choices=["auto", "distributed", "replicated"], default="auto",
                     help="multi-GPU scheme (N>1): key-range decomposition with a distributed "
-                         "build, or replicated tree with a partitioned walk")
+                         "build, or replicated tree with a partitioned walk; auto = distributed "
+                         f"from N >= {AUTO_DISTRIBUTED_N:.0e} bodies (below that the replicated "
+                         "O(N) build costs less than the distributed step's fixed exchange)")
     args = ap.parse_args()
+    if args.decomp == "auto":
+        args.decomp = "distributed" if CONFIGS[args.config]["n"] >= AUTO_DISTRIBUTED_N else "replicated"
     if args.warmup < 3 and args.impl == "ours":
         print("warning: W < 3 violates the timing rules; using 3", file=sys.stderr)
         args.warmup = 3

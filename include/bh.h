@@ -190,6 +190,10 @@ int bh_sim_import(bh_handle *h, int what, int64_t begin, int64_t end, const void
 int bh_sim_local_maxabs(bh_handle *h, double *out, void *stream);
 int bh_sim_set_R(bh_handle *h, double R, void *stream);
 int bh_sim_sort(bh_handle *h, void *stream);
+/* Morton keys of the resident bodies in their current order (no sort), with
+ * the R set by bh_sim_set_R: the routing keys of the migration step
+ * (morton.py:109-125 on the rank's bodies; decomposition.py:84-263). */
+int bh_sim_keys(bh_handle *h, uint64_t *d_keys, void *stream);
 int bh_sim_load_state(bh_handle *h, const void *d_pos, const void *d_vel, const void *d_acc,
                       const int32_t *d_work, int64_t n, void *stream);
 int bh_sim_build_local(bh_handle *h, double theta, int leaf_size, int has_prev, uint64_t prev_key,
@@ -205,6 +209,12 @@ int bh_sim_walk_records(bh_handle *h, void *d_out, int64_t *n_out, void *stream)
  * whose union covers each rank's bodies.  let: sizes per receiver (host arrays,
  * synchronises); let_pack: the receiver's records, bodies and branch map
  * ([nbranch][2] ints: first child in the LET | -1, first body | -1). */
+/* Bounding boxes of contiguous ranges of this rank's sorted bodies (the LET
+ * target region): d_start[ngroup + 1] body offsets (device int64); d_out
+ * [(1 + ngroup) * 6] device doubles: the union, then one box per range
+ * (empty range: min = +inf, max = -inf); 1 <= ngroup <= 256.  fp32 handles,
+ * after bh_sim_sort. */
+int bh_sim_target_boxes(bh_handle *h, const int64_t *d_start, int ngroup, double *d_out, void *stream);
 int bh_sim_let(bh_handle *h, const double *d_boxes, int nbox, int nrank, int self,
                int64_t *rec_counts, int64_t *body_counts, void *stream);
 int bh_sim_let_pack(bh_handle *h, int q, void *d_rec_out, float *d_bodies_out, int32_t *d_bmap_out,

@@ -38,9 +38,9 @@ EXPORTS = (
     "bh_sim_load", "bh_sim_forces", "bh_sim_step", "bh_sim_store", "bh_stats_get",
     "bh_sim_begin_step", "bh_sim_prepare", "bh_sim_walk_range", "bh_sim_scatter_work",
     "bh_sim_end_step", "bh_sim_export", "bh_sim_import",
-    "bh_sim_local_maxabs", "bh_sim_set_R", "bh_sim_sort", "bh_sim_load_state",
+    "bh_sim_local_maxabs", "bh_sim_set_R", "bh_sim_sort", "bh_sim_keys", "bh_sim_load_state",
     "bh_sim_build_local", "bh_sim_branch_export", "bh_sim_walk_records", "bh_walk_records_f32",
-    "bh_sim_let", "bh_sim_let_pack",
+    "bh_sim_let", "bh_sim_let_pack", "bh_sim_target_boxes",
     "bh_timing_enable", "bh_timing_reset", "bh_timing_get", "bh_ffma_peak",
     "bh_ic_plummer", "bh_host_potential_pairs",
 )
@@ -111,6 +111,7 @@ def _declare(L: ctypes.CDLL) -> None:
         "bh_sim_local_maxabs": ([P, ctypes.POINTER(D), P], I),
         "bh_sim_set_R": ([P, D, P], I),
         "bh_sim_sort": ([P, P], I),
+        "bh_sim_keys": ([P, P, P], I),
         "bh_sim_load_state": ([P, P, P, P, P, I64, P], I),
         "bh_sim_build_local": ([P, D, I, I, ctypes.c_uint64, I, ctypes.c_uint64, ctypes.POINTER(I64), P], I),
         "bh_sim_branch_export": ([P, P, P, P, P, P, P, P], I),
@@ -118,6 +119,7 @@ def _declare(L: ctypes.CDLL) -> None:
         "bh_walk_records_f32": ([P, P, I64, P, P, I64, D, I, P, P, P], I),
         "bh_sim_let": ([P, P, I, I, I, ctypes.POINTER(I64), ctypes.POINTER(I64), P], I),
         "bh_sim_let_pack": ([P, I, P, P, P, P], I),
+        "bh_sim_target_boxes": ([P, P, I, P, P], I),
         "bh_timing_enable": ([P, I], I),
         "bh_timing_reset": ([P], I),
         "bh_timing_get": ([P, ctypes.POINTER(D), I], I),

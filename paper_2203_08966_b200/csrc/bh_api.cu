@@ -76,7 +76,7 @@ struct bh_handle {
   int64_t nbranch = 0;
   // locally essential trees of the last build_local
   Buf let_present, let_expand, let_bodies, let_isbranch, let_rflag, let_bcount, let_rpos,
-      let_bpos, let_scan_tmp, let_brec, let_tail;
+      let_bpos, let_scan_tmp, let_brec, let_tail, let_boxkey;
   uint32_t *hlet = nullptr;  // pinned: LET sizes per receiver
   int let_nrank = 0;
   int64_t let_nrec = 0;
@@ -650,7 +650,7 @@ int bh_destroy(bh_handle *h) {
                  &h->bk_pos, &h->bk_vel, &h->bk_acc, &h->bk_id, &h->bk_work,
                  &h->shared, &h->branch, &h->rec_of_cell, &h->wparent, &h->let_present,
                  &h->let_expand, &h->let_bodies, &h->let_isbranch, &h->let_rflag, &h->let_bcount,
-                 &h->let_rpos, &h->let_bpos, &h->let_scan_tmp, &h->let_brec, &h->let_tail};
+                 &h->let_rpos, &h->let_bpos, &h->let_scan_tmp, &h->let_brec, &h->let_tail, &h->let_boxkey};
   for (Buf *b : bufs) b->release();
   cudaFree(h->flags);
   cudaFreeHost(h->hflags);
@@ -1042,6 +1042,28 @@ int bh_sim_sort(bh_handle *h, void *stream) {
   return sim_sort(h, S(stream));
 }
 
+// Morton keys of the current bodies in their current order (no sort) with the
+// R already set -- the routing keys of the distributed step's migration.
+int bh_sim_keys(bh_handle *h, uint64_t *d_keys, void *stream) {
+  if (!h || (!d_keys && h->sim_n)) return fail(BH_BAD_ARG, "bh_sim_keys: bad args");
+  const int64_t n = h->sim_n;
+  if (n == 0) return BH_OK;
+  cudaStream_t s = S(stream);
+  BH_TRY(ensure_sort(h, n));
+  h->tbegin(BH_PHASE_KEYS, s);
+  if (h->precision == BH_FP32)
+    launch_keys_f32(h->pos.as<float4>(), n, h->dR, h->keys.as<uint64_t>(), h->vals.as<uint32_t>(),
+                    h->flags, s);
+  else
+    launch_keys_f64(h->pos.as<double>(), 4, n, h->dR, h->keys.as<uint64_t>(),
+                    h->vals.as<uint32_t>(), h->flags, s);
+  h->tend(s);
+  BH_CUDA(cudaMemcpyAsync(d_keys, h->keys.p, sizeof(uint64_t) * n, cudaMemcpyDeviceToDevice, s));
+  h->launches += 1;
+  BH_LAUNCHED();
+  return BH_OK;
+}
+
 int bh_sim_load_state(bh_handle *h, const void *d_pos, const void *d_vel, const void *d_acc,
                       const int32_t *d_work, int64_t n, void *stream) {
   BH_TRY(bh_sim_load(h, d_pos, d_vel, nullptr, d_acc, n, stream));
@@ -1216,6 +1238,131 @@ int bh_sim_let_pack(bh_handle *h, int q, void *d_rec_out, float *d_bodies_out, i
                        h->let_bodies.as<uint32_t>(), q, rpos, bpos, reinterpret_cast<int2 *>(d_bmap_out),
                        s);
   h->tend(s);
+  h->launches += 3;
+  BH_LAUNCHED();
+  return BH_OK;
+}
+
+// Bounding box of each contiguous range of the sorted bodies: out[1 + g] for
+// bodies [start[g], start[g+1]) (empty range: min = +inf, max = -inf), and
+// out[0] = their union.  Float min/max through order-preserving int keys so a
+// range of any length is reduced by the whole grid: one warp reduction and 6
+// atomics per warp when the warp's bodies share a range (the common case).
+__device__ __forceinline__ int ord_key(float f) {
+  const int i = __float_as_int(f);
+  return i >= 0 ? i : i ^ 0x7fffffff;
+}
+__device__ __forceinline__ float ord_val(int k) { return __int_as_float(k >= 0 ? k : k ^ 0x7fffffff); }
+
+__global__ void k_box_init(int *__restrict__ key, int ngroup) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < 6 * ngroup) key[t] = (t % 6) < 3 ? INT_MAX : INT_MIN;
+}
+
+// Each warp reduces a contiguous chunk of bodies; per-lane running min/max are
+// flushed (warp reduction, then shared-memory atomics) whenever the warp's
+// range changes, and each block flushes its shared boxes to global at the end.
+__device__ __forceinline__ void box_flush(int g, float (&mn)[3], float (&mx)[3], int *sk) {
+  for (int a = 0; a < 3; ++a)
+    for (int o = 16; o > 0; o >>= 1) {
+      mn[a] = fminf(mn[a], __shfl_xor_sync(0xffffffffu, mn[a], o));
+      mx[a] = fmaxf(mx[a], __shfl_xor_sync(0xffffffffu, mx[a], o));
+    }
+  if ((threadIdx.x & 31) == 0 && g >= 0)
+    for (int a = 0; a < 3; ++a) {
+      atomicMin(&sk[6 * g + a], ord_key(mn[a]));
+      atomicMax(&sk[6 * g + 3 + a], ord_key(mx[a]));
+    }
+  for (int a = 0; a < 3; ++a) { mn[a] = INFINITY; mx[a] = -INFINITY; }
+}
+
+__global__ void k_range_boxes(const float4 *__restrict__ pos, int64_t n, const int64_t *__restrict__ start,
+                              int ngroup, int64_t chunk, int *__restrict__ key) {
+  __shared__ int64_t st[257];
+  __shared__ int sk[6 * 256];
+  for (int g = threadIdx.x; g <= ngroup; g += blockDim.x) st[g] = start[g];
+  for (int t = threadIdx.x; t < 6 * ngroup; t += blockDim.x) sk[t] = (t % 6) < 3 ? INT_MAX : INT_MIN;
+  __syncthreads();
+  const unsigned lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t b = warp * chunk, e = b + chunk < n ? b + chunk : n;
+  float mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+  int gcur = -1;
+  for (int64_t base = b; base < e; base += 32) {
+    const int64_t i = base + lane;
+    const bool v = i < e;
+    // range of the warp's first body; the whole warp handles one range per pass
+    int g0 = 0;
+    {
+      int lo = 0, hi = ngroup - 1;  // last g with st[g] <= base
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (st[mid] <= base) lo = mid; else hi = mid - 1;
+      }
+      g0 = lo;
+    }
+    if (g0 != gcur) {
+      box_flush(gcur, mn, mx, sk);
+      gcur = g0;
+    }
+    if (v) {
+      const float4 p = pos[i];
+      if (i < st[g0 + 1]) {
+        mn[0] = fminf(mn[0], p.x); mn[1] = fminf(mn[1], p.y); mn[2] = fminf(mn[2], p.z);
+        mx[0] = fmaxf(mx[0], p.x); mx[1] = fmaxf(mx[1], p.y); mx[2] = fmaxf(mx[2], p.z);
+      } else {  // the warp straddles a range boundary: later ranges go straight to shared
+        int lo = g0, hi = ngroup - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (st[mid] <= i) lo = mid; else hi = mid - 1;
+        }
+        atomicMin(&sk[6 * lo + 0], ord_key(p.x)); atomicMin(&sk[6 * lo + 1], ord_key(p.y));
+        atomicMin(&sk[6 * lo + 2], ord_key(p.z)); atomicMax(&sk[6 * lo + 3], ord_key(p.x));
+        atomicMax(&sk[6 * lo + 4], ord_key(p.y)); atomicMax(&sk[6 * lo + 5], ord_key(p.z));
+      }
+    }
+  }
+  box_flush(gcur, mn, mx, sk);
+  __syncthreads();
+  for (int t = threadIdx.x; t < 6 * ngroup; t += blockDim.x) {
+    const int k = sk[t];
+    if ((t % 6) < 3) { if (k != INT_MAX) atomicMin(&key[t], k); }
+    else if (k != INT_MIN) atomicMax(&key[t], k);
+  }
+}
+
+__global__ void k_box_finish(const int *__restrict__ key, int ngroup, double *__restrict__ out) {
+  const int a = threadIdx.x;
+  if (a >= 6) return;
+  double u = a < 3 ? INFINITY : -INFINITY;
+  for (int g = 0; g < ngroup; ++g) {
+    const int k = key[6 * g + a];
+    const bool empty = a < 3 ? k == INT_MAX : k == INT_MIN;
+    const double v = empty ? (a < 3 ? INFINITY : -INFINITY) : (double)ord_val(k);
+    out[6 * (1 + g) + a] = v;
+    u = a < 3 ? fmin(u, v) : fmax(u, v);
+  }
+  out[a] = u;
+}
+
+// Target boxes of this rank for the LET (fp32 handles, after bh_sim_sort):
+// d_start[ngroup + 1] body offsets; d_out[(1 + ngroup) * 6].
+int bh_sim_target_boxes(bh_handle *h, const int64_t *d_start, int ngroup, double *d_out, void *stream) {
+  if (!h || !d_start || !d_out || ngroup < 1 || ngroup > 256)
+    return fail(BH_BAD_ARG, "bh_sim_target_boxes: bad args");
+  if (h->precision != BH_FP32) return fail(BH_BAD_ARG, "bh_sim_target_boxes: fp32 handles");
+  cudaStream_t s = S(stream);
+  BH_CUDA(h->let_boxkey.ensure(sizeof(int) * 6 * ngroup));
+  k_box_init<<<grid_for(6 * ngroup, 256), 256, 0, s>>>(h->let_boxkey.as<int>(), ngroup);
+  const int64_t n = h->sim_n;
+  if (n > 0) {
+    const int64_t warps = std::min<int64_t>((n + 255) / 256, 4 * 8 * (int64_t)h->sms);
+    const int64_t chunk = ((n + warps - 1) / warps + 31) / 32 * 32;
+    const int blocks = (int)((((n + chunk - 1) / chunk) + 7) / 8);
+    k_range_boxes<<<blocks, 256, 0, s>>>(h->pos.as<float4>(), n, d_start, ngroup, chunk,
+                                          h->let_boxkey.as<int>());
+  }
+  k_box_finish<<<1, 32, 0, s>>>(h->let_boxkey.as<int>(), ngroup, d_out);
   h->launches += 3;
   BH_LAUNCHED();
   return BH_OK;

@@ -29,7 +29,9 @@ GPU in tests -- host-side barriers only, no kernel waits on another).
 from __future__ import annotations
 
 import math
+import os
 import threading
+import time
 from dataclasses import dataclass
 
 import numpy as np
@@ -275,8 +277,8 @@ class DistributedSim:
 #     (splitters from last step's costzones on the global order, all-to-all)
 #   allgather boundary keys -> local tree with global leaf depths
 #   allgather branch nodes -> exact fp64 top tree on every rank  hashed.py:609-786
-#   allgather the owned walk records + bodies (a superset of the locally
-#     essential tree; a selective LET is the refinement) -> global walk tree
+#   locally essential trees: each rank sends each peer the records its target
+#     boxes could open and the bucket bodies they could resolve (all-to-all)
 #   walk the rank's own bodies; costzones cuts -> next splitters
 #
 # Per-target interaction lists equal the single-GPU walk's (same cells, same
@@ -325,6 +327,27 @@ def _combine(children):
     return total, (cx, cy, cz), tuple(q)
 
 
+_BR_INTS = 2 + 1 + 2 + 20 + 1 + 1 + _REC_INTS  # key, level, count, mom[10] f64, rec, lo, record
+
+
+def _pack_branches(br) -> torch.Tensor:
+    """Branch-node rows as one int32 [nb, _BR_INTS] tensor (one allgather)."""
+    nb = br["key"].shape[0]
+    return torch.cat([br["key"].view(torch.int32).view(nb, 2), br["level"].view(nb, 1),
+                      br["count"].view(torch.int32).view(nb, 2), br["mom"].view(torch.int32).view(nb, 20),
+                      br["rec"].view(nb, 1), br["lo"].view(nb, 1), br["recs"]], dim=1).contiguous()
+
+
+def _unpack_branches(rows: np.ndarray):
+    """numpy inverse of _pack_branches: key, level, count, mom, rec, lo, record."""
+    rows = np.ascontiguousarray(rows)
+    key = rows[:, 0:2].copy().view(np.int64).ravel()
+    level = rows[:, 2]
+    count = rows[:, 3:5].copy().view(np.int64).ravel()
+    mom = rows[:, 5:25].copy().view(np.float64)
+    return key, level, count, mom, rows[:, 25], rows[:, 26], rows[:, 27:27 + _REC_INTS]
+
+
 def _f32_bits(x: float) -> int:
     return int(np.array([x], dtype=np.float32).view(np.int32)[0])
 
@@ -346,6 +369,8 @@ class DistributedBuildSim:
         self.R = 1.0
         self.last_zones = None
         self.let_pad = 0.0  # widens the LET target boxes (inf: send whole subtrees)
+        self.trace = {} if os.environ.get("BH_DIST_TRACE") else None  # host wall per section
+        self._tlast = None
 
     # -- collectives on variable-size tensors --
     def _allgather_v(self, t: torch.Tensor) -> list:
@@ -353,7 +378,7 @@ class DistributedBuildSim:
         n = torch.tensor([t.shape[0]], dtype=torch.int64, device=t.device)
         sizes = [torch.zeros_like(n) for _ in range(size)]
         self._allgather(sizes, n)
-        sizes = [int(x.item()) for x in sizes]
+        sizes = torch.cat(sizes).cpu().tolist()
         mx = max(sizes) if sizes else 0
         pad = torch.zeros((mx,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
         pad[: t.shape[0]] = t
@@ -378,27 +403,37 @@ class DistributedBuildSim:
         else:
             outs[0].copy_(t)
 
+    def _alltoall_many(self, items):
+        """[(t, send_counts)] -> [(out, recv_counts)]: rows of each t, grouped by
+        destination rank, to their owners, with one exchange of the counts."""
+        size, me = self.comm.size, self.comm.rank
+        dev = items[0][0].device
+        sc = torch.tensor([c for _, cs in items for c in cs], dtype=torch.int64, device=dev)
+        allc = [torch.zeros_like(sc) for _ in range(size)]
+        self._allgather(allc, sc)
+        A = torch.stack(allc).cpu().view(size, len(items), size)  # A[q, i, k]: q sends k
+        res = []
+        for i, (t, send_counts) in enumerate(items):
+            recv = A[:, i, me].tolist()
+            if isinstance(self.comm, TorchComm):
+                out = torch.empty((sum(recv),) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+                self.comm.alltoall_single(out, t.contiguous(), recv, list(send_counts))
+            else:  # thread / single: gather everyone's full send buffer and cut out our rows
+                bufs = self._allgather_v(t)
+                parts = []
+                for q in range(size):
+                    cq = A[q, i].tolist()
+                    start = sum(cq[:me])
+                    parts.append(bufs[q][start:start + cq[me]])
+                out = torch.cat(parts) if parts else t[:0]
+            res.append((out, recv))
+        return res
+
     def _alltoall_v(self, t: torch.Tensor, send_counts: list, return_counts: bool = False):
         """Rows of t, already grouped by destination rank, to their owners
         (with the per-source row counts if ``return_counts``)."""
-        size = self.comm.size
-        sc = torch.tensor(send_counts, dtype=torch.int64, device=t.device)
-        allc = [torch.zeros_like(sc) for _ in range(size)]
-        self._allgather(allc, sc)
-        recv_counts = [int(allc[q][self.comm.rank].item()) for q in range(size)]
-        if isinstance(self.comm, TorchComm):
-            out = torch.empty((sum(recv_counts),) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
-            self.comm.alltoall_single(out, t.contiguous(), recv_counts, send_counts)
-            return (out, recv_counts) if return_counts else out
-        # thread / single: gather everyone's full send buffer and cut out our rows
-        bufs = self._allgather_v(t)
-        parts = []
-        for q in range(size):
-            cq = [int(allc[q][k].item()) for k in range(size)]
-            start = sum(cq[: self.comm.rank])
-            parts.append(bufs[q][start:start + cq[self.comm.rank]])
-        out = torch.cat(parts) if parts else t[:0]
-        return (out, recv_counts) if return_counts else out
+        out, recv = self._alltoall_many([(t, send_counts)])[0]
+        return (out, recv) if return_counts else out
 
     # -- state --
     def load(self, pos, vel, mass=None, gid=None) -> None:
@@ -427,6 +462,14 @@ class DistributedBuildSim:
         self.R = 1.001 * ext if ext > 0.0 else 1.0  # morton.py:41-42
         self.eng.sim_set_R(self.R)
 
+    def _route_keys(self):
+        """Keys of the bodies in their current order (no sort) and their gids."""
+        eng = self.eng
+        n = eng.sim_n
+        keys = eng.sim_keys()
+        ids = self._export(_lib.BH_SIM_ID, n, (n,), torch.int32)
+        return n, keys, self.gid_load[ids.long()]
+
     def _sort(self):
         """Local sort with the global R; returns (n, sorted keys, sorted gids)."""
         eng = self.eng
@@ -451,19 +494,25 @@ class DistributedBuildSim:
         self.splitters = allk[torch.tensor(cut, device=keys.device)]
 
     def _migrate(self, n: int, keys: torch.Tensor, gid: torch.Tensor) -> None:
-        """Bodies to the owner of their key range (rows are key-sorted, so the
-        per-destination groups are contiguous)."""
+        """Bodies to the owner of their key range (rows grouped by destination
+        with a stable partition; skipped when no body changes owner)."""
         size = self.comm.size
         if size == 1:
             return
         dest = torch.searchsorted(self.splitters, keys, right=True)
-        counts = torch.bincount(dest, minlength=size).tolist()
+        counts = torch.bincount(dest, minlength=size)
+        moves = torch.tensor([n - int(counts[self.comm.rank].item())], dtype=torch.int64, device=keys.device)
+        self.comm.allreduce_sum_(moves)
+        if int(moves.item()) == 0:
+            return  # ownership unchanged everywhere: the local sort follows
+        order = torch.argsort(dest, stable=True)
+        counts = counts.tolist()
         pos = self._export(_lib.BH_SIM_POS, n, (n, 4), torch.float32)
         vel = self._export(_lib.BH_SIM_VEL, n, (n, 4), torch.float32)
         acc = self._export(_lib.BH_SIM_ACC, n, (n, 4), torch.float32)
         work = self._export(_lib.BH_SIM_PREV_WORK, n, (n,), torch.int32)
         payload = torch.cat([pos.view(torch.int32), vel.view(torch.int32), acc.view(torch.int32),
-                             work.view(-1, 1), gid.view(torch.int32).view(-1, 2)], dim=1)
+                             work.view(-1, 1), gid.view(torch.int32).view(-1, 2)], dim=1)[order]
         got = self._alltoall_v(payload, counts)
         self.eng.sim_load_state(got[:, 0:4].clone().view(torch.float32),
                                 got[:, 4:8].clone().view(torch.float32),
@@ -508,16 +557,30 @@ class DistributedBuildSim:
         # monotone (zones may be empty when work is concentrated)
         self.splitters = torch.cummax(cand, 0).values
 
+    def _t(self, label: str) -> None:
+        """BH_DIST_TRACE: synchronise and charge the wall time since the last
+        mark to ``label`` (diagnostics only; off by default)."""
+        if self.trace is None:
+            return
+        torch.cuda.synchronize(self.eng.device)
+        now = time.perf_counter()
+        if self._tlast is not None and label:
+            self.trace[label] = self.trace.get(label, 0.0) + (now - self._tlast) * 1e3
+        self._tlast = now
+
     # -- the step --
     def _forces(self, record_work: bool) -> None:
         p, eng, comm = self.p, self.eng, self.comm
         size, rank = comm.size, comm.rank
         L = p.leaf_size
-        n, keys, gid = self._sort()
+        n, keys, gid = self._route_keys()
         if self.splitters is None:
             self._initial_splitters(keys)
+        self._t("route_keys")
         self._migrate(n, keys, gid)
+        self._t("migrate")
         n, keys, gid = self._sort()
+        self._t("sort2")
         dev = eng.device
         fl = torch.tensor([int(keys[0].item()) if n else -1, int(keys[-1].item()) if n else -1],
                           dtype=torch.int64, device=dev)
@@ -526,14 +589,16 @@ class DistributedBuildSim:
         fls = [(int(a[0].item()), int(a[1].item())) for a in allfl]
         prev = next((fls[q][1] for q in range(rank - 1, -1, -1) if fls[q][0] >= 0), None)
         nxt = next((fls[q][0] for q in range(rank + 1, size) if fls[q][0] >= 0), None)
+        self._t("boundary")
         nb = eng.sim_build_local(p.theta, L, prev, nxt) if n else 0
+        self._t("build_local")
         br = eng.sim_branch_export(nb)
         recs = eng.sim_walk_records() if n else torch.zeros((0, _REC_INTS), dtype=torch.int32, device=dev)
         bodies = self._export(_lib.BH_SIM_POS, n, (n, 4), torch.float32)
         # branch nodes in body order (a top bucket's bodies must be contiguous)
         perm = torch.argsort(br["lo"]) if nb else torch.zeros(0, dtype=torch.int64, device=dev)
         br = {k: v[perm] for k, v in br.items()}
-        br["recs"] = recs[br["rec"].long()]
+        br["recs"] = recs[br["rec"].long()] if nb else torch.zeros((0, _REC_INTS), dtype=torch.int32, device=dev)
         # bodies of the bucket-sized branch nodes (a top bucket spans several)
         small = br["count"] <= L
         cnt = br["count"][small].long()
@@ -541,17 +606,22 @@ class DistributedBuildSim:
         tot = int(cnt.sum().item()) if cnt.numel() else 0
         start = torch.cumsum(cnt, 0) - cnt
         idx = torch.repeat_interleave(lo - start, cnt) + torch.arange(tot, device=dev)
+        self._t("branch_export")
         bb_all = self._allgather_v(bodies[idx])
-        br_all = {k: self._allgather_v(v) for k, v in br.items()}
+        br_all = self._allgather_v(_pack_branches(br))  # one row of _BR_INTS per branch node
+        self._t("branch_allgather")
         # locally essential trees: what each peer's targets can open.
         # Target region = tight boxes of this rank's bodies per group of branch
         # nodes (a key range is not a box: one box per rank would cover most of
         # the domain and send nearly whole subtrees).
         boxes = self._target_boxes(bodies, br, n, nb)
+        self._t("let_boxes")
         allbox = [torch.zeros_like(boxes) for _ in range(size)]
         self._allgather(allbox, boxes)
-        boxes = torch.stack(allbox).contiguous()
+        boxes = torch.stack(allbox).contiguous() if size > 1 else boxes.view(1, -1, 6)
+        self._t("let_box_allgather")
         rc, bc = eng.sim_let(boxes, rank) if n else ([0] * size, [0] * size)
+        self._t("let_mark")
         send_rec = torch.empty((sum(rc), _REC_INTS), dtype=torch.int32, device=dev)
         send_bod = torch.empty((sum(bc), 4), dtype=torch.float32, device=dev)
         mcounts = [0 if (q == rank or not n) else nb for q in range(size)]
@@ -564,13 +634,15 @@ class DistributedBuildSim:
             eng.sim_let_pack(q, send_rec[ro:], send_bod[bo:], bmap)
             send_map[mo:mo + nb] = bmap[perm]
             ro, bo, mo = ro + rc[q], bo + bc[q], mo + nb
-        let_rec, rcnt = self._alltoall_v(send_rec, rc, True)
-        let_bod, bcnt = self._alltoall_v(send_bod, bc, True)
-        let_map, mcnt = self._alltoall_v(send_map, mcounts, True)
+        self._t("let_pack")
+        (let_rec, rcnt), (let_bod, bcnt), (let_map, mcnt) = self._alltoall_many(
+            [(send_rec, rc), (send_bod, bc), (send_map, mcounts)])
+        self._t("let_exchange")
         nbb = sum(b.shape[0] for b in bb_all)
         self.tree = self._assemble(br_all, recs, n, nbb, let_rec, rcnt, bcnt, let_map, mcnt)
         self.let_stats = dict(records=int(let_rec.shape[0]), bodies=int(let_bod.shape[0]),
                               sent_records=sum(rc), sent_bodies=sum(bc), own_records=int(recs.shape[0]))
+        self._t("assemble")
         gbodies = torch.cat([bodies] + list(bb_all) + [let_bod])
         acc = torch.zeros((n, 4), dtype=torch.float32, device=dev)
         work = torch.zeros(n, dtype=torch.int32, device=dev)
@@ -580,6 +652,7 @@ class DistributedBuildSim:
             if record_work:
                 eng.sim_import(_lib.BH_SIM_WORK, 0, n, work)
                 eng.sim_scatter_work()
+        self._t("walk")
         self._keys, self._n, self._nb = keys, n, nb
         self._acc, self._work = acc, work
 
@@ -596,15 +669,13 @@ class DistributedBuildSim:
         box[:, 3:] = -float("inf")
         if n == 0 or nb == 0:
             return box
-        lo = br["lo"].long()  # branch nodes in body order; they partition the bodies
-        gid_branch = (torch.arange(nb, device=dev) * K) // nb
-        bidx = torch.searchsorted(lo, torch.arange(n, device=dev), right=True) - 1
-        g = gid_branch[bidx].view(-1, 1).expand(-1, 3)
-        x = bodies[:, :3].double()
-        box[1:, :3] = box[1:, :3].scatter_reduce(0, g, x, reduce="amin")
-        box[1:, 3:] = box[1:, 3:].scatter_reduce(0, g, x, reduce="amax")
-        box[0, :3] = x.min(0).values  # the union first: a cheap accept for far cells
-        box[0, 3:] = x.max(0).values
+        # branch nodes are in body order and partition the bodies: group g = a
+        # run of consecutive branch nodes = a contiguous range of bodies
+        gid = (torch.arange(nb, device=dev) * K) // nb
+        first = torch.searchsorted(gid, torch.arange(K + 1, device=dev))
+        lo = torch.cat([br["lo"].long(), torch.tensor([n], dtype=torch.int64, device=dev)])
+        start = lo[first].contiguous()  # first == nb -> n (empty group)
+        self.eng.sim_target_boxes(start, box)
         box[:, :3] -= self.let_pad
         box[:, 3:] += self.let_pad
         return box
@@ -629,17 +700,18 @@ class DistributedBuildSim:
         bbpos = n
         maps = {}
         off = 0
+        let_map_h = let_map.cpu().numpy()
         for q in range(size):
-            maps[q] = let_map[off:off + mcnt[q]].cpu().numpy()
+            maps[q] = let_map_h[off:off + mcnt[q]]
             off += mcnt[q]
+        host = torch.cat(br_all).cpu().numpy() if br_all else np.zeros((0, _BR_INTS), np.int32)
+        off = 0
         for r in range(size):
-            key = br_all["key"][r].cpu().numpy()
-            if not len(key):
+            rows_r = host[off:off + br_all[r].shape[0]]
+            off += br_all[r].shape[0]
+            if not len(rows_r):
                 continue
-            lev = br_all["level"][r].cpu().numpy()
-            cnt = br_all["count"][r].cpu().numpy()
-            mom = br_all["mom"][r].cpu().numpy()
-            brecs = br_all["recs"][r].cpu().numpy()
+            key, lev, cnt, mom, _, _, brecs = _unpack_branches(rows_r)
             for k in range(len(key)):
                 c = int(cnt[k])
                 rows[int(key[k])] = dict(count=c, mass=float(mom[k, 0]),
@@ -762,11 +834,15 @@ class DistributedBuildSim:
 
     def step(self, steps: int = 1) -> None:
         for _ in range(steps):
+            self._t("")
             self.eng.sim_begin_step(self.p.dt)
             self._bounds()
+            self._t("kick_drift_bounds")
             self._forces(record_work=True)
             self.eng.sim_end_step(self.p.dt)
+            self._t("kick")
             self._next_splitters(self._n, self._keys)
+            self._t("splitters")
             if hasattr(self.eng, "check"):
                 self.eng.check()
 

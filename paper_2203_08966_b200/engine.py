@@ -256,6 +256,13 @@ class Engine:
     def sim_sort(self) -> None:
         check(self._L.bh_sim_sort(self._h, self.stream))
 
+    def sim_keys(self) -> torch.Tensor:
+        """Morton keys (int64 view) of the resident bodies in their current order."""
+        out = torch.empty(self.sim_n, dtype=torch.int64, device=self.device)
+        if self.sim_n:
+            check(self._L.bh_sim_keys(self._h, _ptr(out), self.stream))
+        return out
+
     def sim_load_state(self, pos, vel, acc=None, work=None) -> None:
         n = pos.shape[0]
         check(self._L.bh_sim_load_state(self._h, _ptr(pos), _ptr(vel), _ptr(acc), _ptr(work), n,
@@ -300,6 +307,11 @@ class Engine:
         bc = (ctypes.c_int64 * nrank)()
         check(self._L.bh_sim_let(self._h, _ptr(boxes), nbox, nrank, int(self_rank), rc, bc, self.stream))
         return list(rc), list(bc)
+
+    def sim_target_boxes(self, start: torch.Tensor, out: torch.Tensor) -> None:
+        """Boxes of body ranges [start[g], start[g+1]) into out [(1 + G), 6] (union first)."""
+        check(self._L.bh_sim_target_boxes(self._h, _ptr(start), int(start.shape[0]) - 1, _ptr(out),
+                                          self.stream))
 
     def sim_let_pack(self, q: int, recs: torch.Tensor, bodies: torch.Tensor, bmap: torch.Tensor) -> None:
         check(self._L.bh_sim_let_pack(self._h, int(q), _ptr(recs), _ptr(bodies), _ptr(bmap), self.stream))

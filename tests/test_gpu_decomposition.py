@@ -178,3 +178,38 @@ def test_distributed_build_clustered_multi_step():
     for s in got["let"]:
         assert s["records"] < own - s["own_records"], got["let"]
     print("LET", got["let"])
+
+
+def test_target_boxes_match_numpy():
+    """bh_sim_target_boxes: per-range bounding boxes (any range length, empty
+    ranges, ranges straddling warps) and their union, exactly."""
+    from paper_2203_08966_b200.engine import Engine
+    from paper_2203_08966_b200.initcond import make_rng, plummer_cluster
+
+    b = plummer_cluster(100_003, make_rng(5))
+    eng = Engine("fp32", 0)
+    pos = eng.bodies_tensor(b.position, b.mass)
+    eng.sim_load_state(pos, eng.vec_tensor(b.velocity))
+    eng.sim_set_R(1.001 * float(pos[:, :3].abs().max()))
+    eng.sim_sort()
+    n = eng.sim_n
+    x = torch.empty((n, 4), dtype=torch.float32, device="cuda")
+    from paper_2203_08966_b200 import _lib
+    eng.sim_export(_lib.BH_SIM_POS, 0, n, x)
+    xs = x[:, :3].double().cpu().numpy()
+    for cuts in ([0, n], [0, 0, 17, 17, 5000, 5031, 99_000, n], list(range(0, n, 1563)) + [n]):
+        start = torch.tensor(cuts, dtype=torch.int64, device="cuda")
+        g = len(cuts) - 1
+        out = torch.empty((g + 1, 6), dtype=torch.float64, device="cuda")
+        eng.sim_target_boxes(start, out)
+        got = out.cpu().numpy()
+        for k in range(g):
+            seg = xs[cuts[k]:cuts[k + 1]]
+            if len(seg):
+                np.testing.assert_array_equal(got[1 + k, :3], seg.min(0))
+                np.testing.assert_array_equal(got[1 + k, 3:], seg.max(0))
+            else:
+                assert np.all(np.isposinf(got[1 + k, :3])) and np.all(np.isneginf(got[1 + k, 3:]))
+        np.testing.assert_array_equal(got[0, :3], xs.min(0))
+        np.testing.assert_array_equal(got[0, 3:], xs.max(0))
+    eng.close()

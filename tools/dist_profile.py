@@ -22,6 +22,8 @@ sim.load(eng.bodies_tensor(b.position[lo:hi], b.mass[lo:hi]), eng.vec_tensor(b.v
 sim.bootstrap()
 sim.step(3)
 torch.cuda.synchronize()
+if sim.trace is not None:
+    sim.trace.clear()
 eng.timing(True)
 eng.timing_reset()
 prof = cProfile.Profile()
@@ -34,6 +36,8 @@ wall = (time.perf_counter() - t0) / 5 * 1e3
 ph = {k: round(v / 5, 3) for k, v in eng.timing_get().items()}
 if rank == 0:
     print(f"ranks={ws} n={n} wall_ms/step={wall:.2f} device_ms/step={ph} let={sim.let_stats}")
+    if sim.trace is not None:
+        print("trace ms/step:", {k: round(v / 5, 3) for k, v in sim.trace.items()})
     pstats.Stats(prof).sort_stats("cumulative").print_stats(25)
 dist.barrier()
 dist.destroy_process_group()
