@@ -277,6 +277,14 @@ constexpr int kWalkBlock = BH_WALK_BLOCK;
 #endif
 constexpr int kStack = 8 * (kMaxLevel + 1) + 8;  // <= 8 pending siblings per level
 
+#ifdef BH_WALK_HIST
+// diagnostics: [0, 65) targets accepting each non-leaf visit; [65, 130) targets examining it
+__device__ unsigned long long g_walk_hist[130];
+extern "C" int bh_debug_walk_hist(unsigned long long *out) {
+  return (int)cudaMemcpyFromSymbol(out, g_walk_hist, sizeof(g_walk_hist));
+}
+#endif
+
 template <bool BUCKET>
 __global__ void __launch_bounds__(kWalkBlock, BH_WALK_MINB) k_walk(
     const WalkNode *__restrict__ T, const float4 *__restrict__ bodies,
@@ -330,6 +338,13 @@ __global__ void __launch_bounds__(kWalkBlock, BH_WALK_MINB) k_walk(
         continue;
       }
       const bool c0 = in0 && D2.x > a.w, c1 = in1 && D2.y > a.w;  // MAC (flattree.py:295)
+#ifdef BH_WALK_HIST
+      {
+        const int na = __popc(__ballot_sync(0xffffffffu, c0)) + __popc(__ballot_sync(0xffffffffu, c1));
+        const int ni = __popc((unsigned)e.z) + __popc((unsigned)e.w);
+        if (lane == 0) { atomicAdd(&g_walk_hist[na], 1ull); atomicAdd(&g_walk_hist[65 + ni], 1ull); }
+      }
+#endif
       if (__any_sync(0xffffffffu, c0 || c1)) {
         const float4 b = nd->b;
         const float4 q = nd->c;
