@@ -416,6 +416,91 @@ __device__ void cell_moments(const TreeView &t, int p) {
   q2o[2] = make_double2(qyz, qzz);
 }
 
+// The same moments with one lane per child slot (8 lanes per cell, 4 cells per
+// warp): the child loads of a cell go out in parallel from 8 lanes, and the
+// slot-ordered sums -- the reference's exact expression order -- are formed
+// from a per-warp shared-memory exchange.  Each lane forms its child's
+// products (m*x, and q_c + m*(3 dx dx - d2)); the sums are sequential in slot
+// order, skipping absent and massless children, as in cell_moments.
+// Every lane of the warp must call it (p < 0: no cell).  xs: the warp's [32][11].
+__device__ void cell_moments8(const TreeView &t, int p, double (*xs)[11]) {
+  const int lane = threadIdx.x & 31, s = lane & 7, g0 = lane & ~7;
+  int c = -1;
+  if (p >= 0) c = t.child8[8 * (int64_t)p + s];
+  const unsigned have = (__ballot_sync(0xffffffffu, c >= 0) >> g0) & 0xffu;
+  const bool cell = p >= 0 && have != 0u;
+  if (p >= 0 && have == 0u && s == 0) dup_cell_moments(t, p);  // duplicate-key cell
+  double4 cm = make_double4(0.0, 0.0, 0.0, 0.0);
+  bool hasq = false;
+  if (c >= 0) {
+    cm = t.cm64[c];
+    hasq = t.link[c].y > 1;  // leaves keep quad = 0 (flattree.py:207-208)
+  }
+  const double m = cm.w;
+  const bool use = c >= 0 && m != 0.0;
+  double *mine = xs[lane];
+  mine[0] = use ? 1.0 : 0.0;
+  mine[1] = m;
+  mine[2] = m * cm.x;
+  mine[3] = m * cm.y;
+  mine[4] = m * cm.z;
+  __syncwarp();
+  double total = 0.0, cx = 0.0, cy = 0.0, cz = 0.0;
+  for (int j = 0; j < 8; ++j) {
+    const double *o = xs[g0 + j];
+    if (o[0] == 0.0) continue;
+    total += o[1];
+    cx += o[2];
+    cy += o[3];
+    cz += o[4];
+  }
+  double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0, t4 = 0.0, t5 = 0.0;
+  if (cell && total != 0.0) {
+    cx /= total;
+    cy /= total;
+    cz /= total;
+    if (use) {
+      double q0 = 0.0, q1 = 0.0, q2 = 0.0, q3 = 0.0, q4 = 0.0, q5 = 0.0;
+      if (hasq) {
+        const double2 *qc = reinterpret_cast<const double2 *>(t.q64 + 6 * (int64_t)c);
+        const double2 a = qc[0], b = qc[1], d = qc[2];
+        q0 = a.x; q1 = a.y; q2 = b.x; q3 = b.y; q4 = d.x; q5 = d.y;
+      }
+      const double dx = cm.x - cx, dy = cm.y - cy, dz = cm.z - cz;
+      const double d2 = dx * dx + dy * dy + dz * dz;
+      t0 = q0 + m * (3.0 * (dx * dx) - d2);
+      t1 = q1 + m * (3.0 * (dx * dy) - 0.0);
+      t2 = q2 + m * (3.0 * (dx * dz) - 0.0);
+      t3 = q3 + m * (3.0 * (dy * dy) - d2);
+      t4 = q4 + m * (3.0 * (dy * dz) - 0.0);
+      t5 = q5 + m * (3.0 * (dz * dz) - d2);
+    }
+  }
+  __syncwarp();
+  mine[5] = t0; mine[6] = t1; mine[7] = t2; mine[8] = t3; mine[9] = t4; mine[10] = t5;
+  __syncwarp();
+  if (cell && s == 0) {
+    double *qo = t.q64 + 6 * (int64_t)p;
+    if (total == 0.0) {
+      t.cm64[p] = make_double4(0.0, 0.0, 0.0, 0.0);
+      for (int k = 0; k < 6; ++k) qo[k] = 0.0;
+    } else {
+      double qxx = 0.0, qxy = 0.0, qxz = 0.0, qyy = 0.0, qyz = 0.0, qzz = 0.0;
+      for (int j = 0; j < 8; ++j) {
+        const double *o = xs[g0 + j];
+        if (o[0] == 0.0) continue;
+        qxx += o[5]; qxy += o[6]; qxz += o[7]; qyy += o[8]; qyz += o[9]; qzz += o[10];
+      }
+      t.cm64[p] = make_double4(cx, cy, cz, total);
+      double2 *q2o = reinterpret_cast<double2 *>(qo);
+      q2o[0] = make_double2(qxx, qxy);
+      q2o[1] = make_double2(qxz, qyy);
+      q2o[2] = make_double2(qyz, qzz);
+    }
+  }
+  __syncwarp();
+}
+
 // Bottom-up moments, level-synchronous: internal cells are bucketed by level
 // (the per-level counts come from k_lcp_new and are read back with the cell
 // count, so every launch below is sized exactly), then one launch per level,
@@ -443,9 +528,11 @@ __global__ void k_level_scatter(TreeView t, const LevelPlan plan, int *__restric
   if (l >= 0) list[base[l] + rank] = (int)c;
 }
 
-__global__ void k_moments_level(TreeView t, const int *__restrict__ list, int begin, int count) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k < count) cell_moments(t, list[begin + k]);
+__global__ void __launch_bounds__(128) k_moments_level(TreeView t, const int *__restrict__ list, int begin,
+                                                     int count) {
+  __shared__ double xs[128 / 32][32][11];
+  const int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
+  cell_moments8(t, k < count ? list[begin + k] : -1, xs[threadIdx.x >> 5]);
 }
 
 // C = 1 + off[n-1] + newc[n-1] on device; flag an overflow of the capacity
@@ -465,7 +552,10 @@ void launch_set_count(const uint32_t *off, const uint32_t *newc, int64_t n, int6
 // deepest-first with a grid-wide barrier between levels -- the same
 // cell_moments work as the per-level launches, without ~22 dependent launches.
 namespace cg = cooperative_groups;
-__global__ void __launch_bounds__(256) k_moments_coop(TreeView t, int *__restrict__ lvl,
+#ifndef BH_MOM_MINB
+#define BH_MOM_MINB 4
+#endif
+__global__ void __launch_bounds__(256, BH_MOM_MINB) k_moments_coop(TreeView t, int *__restrict__ lvl,
                                                      int *__restrict__ list) {
   cg::grid_group grid = cg::this_grid();
   const int64_t C = tree_count(t);
@@ -502,11 +592,44 @@ __global__ void __launch_bounds__(256) k_moments_coop(TreeView t, int *__restric
     __syncthreads();
   }
   grid.sync();
-  for (int l = kMaxLevel; l >= 0; --l) {
-    const int n_l = cnt[l], b_l = offs[l];
-    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n_l; k += stride)
-      cell_moments(t, list[b_l + k]);
-    if (n_l > 0) grid.sync();
+  // Runs of consecutive small levels (few cells: the top of the tree and the
+  // deepest levels) are swept by block 0 alone with block barriers; the rest
+  // of the grid waits at one grid barrier after the run.
+  // 8 lanes per cell (cell_moments8): a warp takes 4 cells per pass.
+  __shared__ double xs[256 / 32][32][11];
+  double(*wx)[11] = xs[threadIdx.x >> 5];
+  const int sub = (threadIdx.x & 31) >> 3;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = stride >> 5;
+  const int small = 2 * (int)(blockDim.x >> 3);
+  int l = kMaxLevel;
+  while (l >= 0) {
+    const int n_l = cnt[l];
+    if (n_l == 0) { --l; continue; }
+    if (n_l <= small) {
+      int l2 = l;
+      while (l2 >= 0 && cnt[l2] <= small) --l2;  // run = levels (l2, l]
+      if (blockIdx.x == 0) {
+        for (int ll = l; ll > l2; --ll) {
+          const int nll = cnt[ll], bll = offs[ll];
+          for (int base = (int)(threadIdx.x >> 5) * 4; base < nll; base += (int)(blockDim.x >> 5) * 4) {
+            const int k = base + sub;
+            cell_moments8(t, k < nll ? list[bll + k] : -1, wx);
+          }
+          __syncthreads();
+        }
+      }
+      l = l2;
+      grid.sync();
+      continue;
+    }
+    const int b_l = offs[l];
+    for (int64_t base = warp * 4; base < n_l; base += nwarps * 4) {
+      const int64_t k = base + sub;
+      cell_moments8(t, k < n_l ? list[b_l + k] : -1, wx);
+    }
+    grid.sync();
+    --l;
   }
 }
 
@@ -528,7 +651,7 @@ void launch_moments(const TreeView &t, const LevelPlan &plan, int *cursor, int *
   k_level_scatter<<<grid_for(t.C, 256), 256, 0, s>>>(t, plan, cursor, list);
   for (int l = kMaxLevel; l >= 0; --l) {
     const int cnt = plan.count[l];
-    if (cnt > 0) k_moments_level<<<grid_for(cnt, 128), 128, 0, s>>>(t, list, plan.offset[l], cnt);
+    if (cnt > 0) k_moments_level<<<grid_for((int64_t)cnt * 8, 128), 128, 0, s>>>(t, list, plan.offset[l], cnt);
   }
 }
 
