@@ -257,6 +257,9 @@ def run_ours(args, cfg) -> dict | None:
         hpos.copy_(dpos)
         hvel.copy_(dvel)
         hacc.copy_(dacc)
+    hvel3 = hvel[:, :3].contiguous().pin_memory()
+    hacc3 = hacc[:, :3].contiguous().pin_memory()
+    host_api = not distributed and sim is None
     torch.cuda.synchronize()
     e2e_ms = 0.0
     e2e_inter = 0
@@ -273,19 +276,18 @@ def run_ours(args, cfg) -> dict | None:
             p_, v_, a_, w_, g_ = sim.store()
             hpos, hvel, hacc = (x.to("cpu", non_blocking=True) for x in (p_, v_, a_))
             hwork, hgid = w_.to(_t.int32).to("cpu", non_blocking=True), g_.to("cpu", non_blocking=True)
-        else:
+        elif sim is not None:  # replicated multi-GPU: every rank holds the full state
             dpos.copy_(hpos, non_blocking=True)
             dvel.copy_(hvel, non_blocking=True)
             dacc.copy_(hacc, non_blocking=True)
             eng.sim_load(dpos, dvel, acc=dacc)
-            if sim is not None:
-                sim.step(1)
-            else:
-                eng.sim_step(dt, theta, eps, leaf, 1)
+            sim.step(1)
             eng.sim_store(dpos, dvel, dacc)
             hpos.copy_(dpos, non_blocking=True)
             hvel.copy_(dvel, non_blocking=True)
             hacc.copy_(dacc, non_blocking=True)
+        else:  # one call from host arrays: pos (n,4), vel/acc (n,3) (bh_sim_step_host)
+            eng.sim_step_host(hpos, hvel3, hacc3, dt, theta, eps, leaf, 1)
         ev1.record()
         torch.cuda.synchronize()
         e2e_ms += ev0.elapsed_time(ev1)
@@ -361,9 +363,13 @@ def run_ours(args, cfg) -> dict | None:
                               "frac": sort_gbs / hbm if sort_gbs else None,
                               "bytes_per_body": SORT_BYTES_PER_BODY, "impl": "cub::DeviceRadixSort (onesweep)"},
             "e2e": {"value": e2e_all / (e2e_ms / 1e3), "unit": "interactions/s",
-                    "h2d_bytes_per_step": 3 * 16 * n, "d2h_bytes_per_step": 3 * 16 * n,
+                    "h2d_bytes_per_step": (16 + 12 + 12) * n if host_api else 3 * 16 * n,
+                    "d2h_bytes_per_step": (16 + 12 + 12) * n if host_api else 3 * 16 * n,
                     "ms_per_step": e2e_ms / args.steps,
-                    "path": "Engine.sim_load/sim_step/sim_store (C-ABI) from pinned host pos/vel/acc"},
+                    "path": ("Engine.sim_step_host -> bh_sim_step_host (C-ABI): pinned host pos (n,4), "
+                             "vel/acc (n,3) in, state back in caller order; positions copied back under "
+                             "the force computation") if host_api else
+                            "Engine.sim_load/sim_step/sim_store (C-ABI) from pinned host pos/vel/acc"},
             "gpu_launches": launches,
             "gpu_launches_note": "libbh kernels in the timed region (CUB sort/scan kernels not included)",
             "clocks": clocks.summary(),

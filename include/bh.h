@@ -150,6 +150,13 @@ int bh_sim_step(bh_handle *h, double dt, double theta, double eps, int leaf_size
                 void *stream);
 int bh_sim_store(bh_handle *h, void *d_pos, void *d_vel, void *d_acc, int64_t *d_work,
                  void *stream);
+/* One call from host arrays (fp32 handles): load pos4 (x, y, z, m; n x 4),
+ * vel3 and acc3 (n x 3), run `steps` KDK steps (simulation.py:492-502), and
+ * write the state back in the caller's order.  For one step the positions are
+ * copied back under the force computation.  Pinned host memory makes the
+ * copies asynchronous.  Synchronous on the stream at return. */
+int bh_sim_step_host(bh_handle *h, float *pos4, float *vel3, float *acc3, int64_t n, double dt,
+                     double theta, double eps, int leaf_size, int steps, void *stream);
 
 /* The same step in phases, for a multi-GPU driver that exchanges between them
  * (simulation.py:492-502 with the force pass split at the walk):

@@ -78,6 +78,10 @@ struct bh_handle {
   Buf let_present, let_expand, let_bodies, let_isbranch, let_rflag, let_bcount, let_rpos,
       let_bpos, let_scan_tmp, let_brec, let_tail, let_boxkey;
   uint32_t *hlet = nullptr;  // pinned: LET sizes per receiver
+  // bh_sim_step_host: staging and the side stream for the early position copy
+  Buf hs_a, hs_b, hs_pos;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_pos = nullptr, ev_side = nullptr;
   int let_nrank = 0;
   int64_t let_nrec = 0;
   double R = 1.0;
@@ -650,7 +654,7 @@ int bh_destroy(bh_handle *h) {
                  &h->bk_pos, &h->bk_vel, &h->bk_acc, &h->bk_id, &h->bk_work,
                  &h->shared, &h->branch, &h->rec_of_cell, &h->wparent, &h->let_present,
                  &h->let_expand, &h->let_bodies, &h->let_isbranch, &h->let_rflag, &h->let_bcount,
-                 &h->let_rpos, &h->let_bpos, &h->let_scan_tmp, &h->let_brec, &h->let_tail, &h->let_boxkey};
+                 &h->let_rpos, &h->let_bpos, &h->let_scan_tmp, &h->let_brec, &h->let_tail, &h->let_boxkey, &h->hs_a, &h->hs_b, &h->hs_pos};
   for (Buf *b : bufs) b->release();
   cudaFree(h->flags);
   cudaFreeHost(h->hflags);
@@ -662,6 +666,9 @@ int bh_destroy(bh_handle *h) {
   cudaFreeHost(h->hR);
   cudaFreeHost(h->hlvl);
   cudaFreeHost(h->hlet);
+  if (h->ev_pos) cudaEventDestroy(h->ev_pos);
+  if (h->ev_side) cudaEventDestroy(h->ev_side);
+  if (h->side) cudaStreamDestroy(h->side);
   h->fold_marks();
   for (cudaEvent_t e : h->pool) cudaEventDestroy(e);
   delete h;
@@ -981,6 +988,93 @@ int bh_sim_step(bh_handle *h, double dt, double theta, double eps, int leaf_size
     BH_TRY(sim_snapshot(h, true, s));  // grown capacity: redo the call
   }
   return fail(BH_OUT_OF_MEMORY, "tree cell capacity kept overflowing");
+}
+
+__global__ void k_expand3(const float *__restrict__ v3, int64_t n, float4 *__restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = make_float4(v3[3 * i], v3[3 * i + 1], v3[3 * i + 2], 0.f);
+}
+__global__ void k_store3f(const float4 *__restrict__ src, const uint32_t *__restrict__ id, int64_t n,
+                          float *__restrict__ dst3) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float4 v = src[i];
+  float *o = dst3 + 3 * (int64_t)id[i];
+  o[0] = v.x; o[1] = v.y; o[2] = v.z;
+}
+
+// One call from host arrays (the reference's numpy Bodies, fp32): load
+// pos4 (x, y, z, m) / vel3 / acc3, run `steps` KDK steps, write the state back
+// in the caller's order.  For one step the positions are final after the
+// drift, so their device->host copy runs on a side stream under the tree
+// build and walk; velocities and accelerations follow the final kick.  Host
+// arrays should be pinned for the copies to be asynchronous.
+int bh_sim_step_host(bh_handle *h, float *pos4, float *vel3, float *acc3, int64_t n, double dt,
+                     double theta, double eps, int leaf_size, int steps, void *stream) {
+  if (!h || n < 1 || !pos4 || !vel3 || !acc3 || !(dt > 0.0) || steps < 1)
+    return fail(BH_BAD_ARG, "bh_sim_step_host: bad args");
+  if (h->precision != BH_FP32) return fail(BH_BAD_ARG, "bh_sim_step_host: fp32 handles");
+  cudaStream_t s = S(stream);
+  if (!h->side) BH_CUDA(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+  if (!h->ev_pos) BH_CUDA(cudaEventCreateWithFlags(&h->ev_pos, cudaEventDisableTiming));
+  if (!h->ev_side) BH_CUDA(cudaEventCreateWithFlags(&h->ev_side, cudaEventDisableTiming));
+  BH_CUDA(h->hs_a.ensure(sizeof(float) * 3 * n));
+  BH_CUDA(h->hs_b.ensure(sizeof(float) * 3 * n));
+  BH_CUDA(h->hs_pos.ensure(sizeof(float4) * n));
+  // load: positions straight into the resident buffer, 3-vectors through staging
+  {
+    Buf *b4[] = {&h->pos, &h->pos2, &h->vel, &h->vel2, &h->acc};
+    for (Buf *b : b4) BH_CUDA(b->ensure(sizeof(float4) * (n + 1)));
+    BH_CUDA(h->id.ensure(sizeof(uint32_t) * (n + 1)));
+    BH_CUDA(h->id2.ensure(sizeof(uint32_t) * (n + 1)));
+    BH_CUDA(h->work_sorted.ensure(sizeof(int64_t) * (n + 1)));
+    BH_CUDA(h->work_orig.ensure(sizeof(int) * (n + 1)));
+  }
+  h->sim_n = n;
+  BH_CUDA(cudaMemcpyAsync(h->pos.p, pos4, sizeof(float4) * n, cudaMemcpyHostToDevice, s));
+  BH_CUDA(cudaMemcpyAsync(h->hs_a.p, vel3, sizeof(float) * 3 * n, cudaMemcpyHostToDevice, s));
+  BH_CUDA(cudaMemcpyAsync(h->hs_b.p, acc3, sizeof(float) * 3 * n, cudaMemcpyHostToDevice, s));
+  const int g = grid_for(n, 256);
+  k_expand3<<<g, 256, 0, s>>>(h->hs_a.as<float>(), n, h->vel.as<float4>());
+  k_expand3<<<g, 256, 0, s>>>(h->hs_b.as<float>(), n, h->acc.as<float4>());
+  k_iota32<<<g, 256, 0, s>>>(h->id.as<uint32_t>(), n);
+  k_fill_int<<<g, 256, 0, s>>>(h->work_orig.as<int>(), n, 1);  // simulation.py:482
+  h->launches += 4;
+  bool pos_sent = false;
+  for (int attempt = 0; attempt < 3; ++attempt) {
+    BH_TRY(sim_snapshot(h, false, s));
+    for (int k = 0; k < steps; ++k) {
+      BH_TRY(sim_begin_step(h, dt, s));
+      if (steps == 1 && !pos_sent) {  // final positions, still in the caller's order
+        BH_CUDA(cudaMemcpyAsync(h->hs_pos.p, h->pos.p, sizeof(float4) * n, cudaMemcpyDeviceToDevice, s));
+        BH_CUDA(cudaEventRecord(h->ev_pos, s));
+        BH_CUDA(cudaStreamWaitEvent(h->side, h->ev_pos, 0));
+        BH_CUDA(cudaMemcpyAsync(pos4, h->hs_pos.p, sizeof(float4) * n, cudaMemcpyDeviceToHost, h->side));
+        BH_CUDA(cudaEventRecord(h->ev_side, h->side));
+        pos_sent = true;
+      }
+      BH_TRY(sim_forces_impl(h, theta, eps, leaf_size, 1, true, s));
+      BH_TRY(sim_end_step(h, dt, s));
+    }
+    int overflow = 0;
+    BH_TRY(async_readback(h, s, &overflow));
+    if (!overflow) break;
+    if (attempt == 2) return fail(BH_OUT_OF_MEMORY, "tree cell capacity kept overflowing");
+    BH_TRY(sim_snapshot(h, true, s));  // grown capacity: redo (same positions after the drift)
+  }
+  const uint32_t *id = h->id.as<uint32_t>();
+  if (!pos_sent) {
+    k_store4<float4><<<g, 256, 0, s>>>(h->pos.as<float4>(), id, n, h->hs_pos.as<float4>());
+    BH_CUDA(cudaMemcpyAsync(pos4, h->hs_pos.p, sizeof(float4) * n, cudaMemcpyDeviceToHost, s));
+  }
+  k_store3f<<<g, 256, 0, s>>>(h->vel.as<float4>(), id, n, h->hs_a.as<float>());
+  k_store3f<<<g, 256, 0, s>>>(h->acc.as<float4>(), id, n, h->hs_b.as<float>());
+  BH_CUDA(cudaMemcpyAsync(vel3, h->hs_a.p, sizeof(float) * 3 * n, cudaMemcpyDeviceToHost, s));
+  BH_CUDA(cudaMemcpyAsync(acc3, h->hs_b.p, sizeof(float) * 3 * n, cudaMemcpyDeviceToHost, s));
+  if (pos_sent) BH_CUDA(cudaStreamWaitEvent(s, h->ev_side, 0));
+  h->launches += 2 + (pos_sent ? 0 : 1);
+  BH_LAUNCHED();
+  return BH_OK;
 }
 
 int bh_sim_begin_step(bh_handle *h, double dt, void *stream) {

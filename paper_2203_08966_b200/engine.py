@@ -322,6 +322,18 @@ class Engine:
                                           _ptr(targets), targets.shape[0], float(eps), int(leaf_size),
                                           _ptr(acc), _ptr(work), self.stream))
 
+    def sim_step_host(self, pos4: torch.Tensor, vel3: torch.Tensor, acc3: torch.Tensor, dt: float,
+                      theta: float, eps: float, leaf_size: int, steps: int = 1) -> None:
+        """KDK steps on host (CPU, ideally pinned) float32 arrays pos4 (n,4), vel3/acc3
+        (n,3), updated in place; synchronous (bh_sim_step_host)."""
+        for t, w in ((pos4, 4), (vel3, 3), (acc3, 3)):
+            if t.device.type != "cpu" or t.dtype != torch.float32 or not t.is_contiguous() or t.shape[-1] != w:
+                raise ValueError("sim_step_host takes contiguous float32 host arrays (n,4), (n,3), (n,3)")
+        n = pos4.shape[0]
+        check(self._L.bh_sim_step_host(self._h, _ptr(pos4), _ptr(vel3), _ptr(acc3), n, dt, theta, eps,
+                                       leaf_size, steps, self.stream))
+        torch.cuda.current_stream(self.device).synchronize()
+
     def sim_store(self, pos=None, vel=None, acc=None, work=None) -> None:
         check(self._L.bh_sim_store(self._h, _ptr(pos), _ptr(vel), _ptr(acc), _ptr(work), self.stream))
 

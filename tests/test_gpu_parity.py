@@ -461,3 +461,32 @@ class TestDuplicateKeysGPU:
             tol = FP32_TOL if precision == "fp32" else ULP_TOL
             assert rel_l2(acc, ref_acc) <= tol
             assert np.mean(work != ref_work) < (0.01 if precision == "fp32" else 1e-12)
+
+
+@pytest.mark.parametrize("steps", [1, 3])
+def test_sim_step_host_matches_device_path(steps):
+    """bh_sim_step_host (host arrays, early position copy) == sim_load/sim_step/sim_store."""
+    from paper_2203_08966_b200.engine import Engine
+    from paper_2203_08966_b200.initcond import make_rng, plummer_cluster
+
+    b = plummer_cluster(50_000, make_rng(7))
+    eng = Engine("fp32", 0)
+    pos = eng.bodies_tensor(b.position, b.mass)
+    vel = eng.vec_tensor(b.velocity)
+    eng.sim_load(pos, vel)
+    eng.sim_forces(0.6, 1e-3, 16, record_work=False)
+    acc = torch.empty_like(vel)
+    eng.sim_store(acc=acc)
+    hp, hv, ha = pos.cpu().pin_memory(), vel[:, :3].contiguous().cpu().pin_memory(), acc[:, :3].contiguous().cpu().pin_memory()
+    # device path
+    eng.sim_load(pos, vel, acc=acc)
+    eng.sim_step(1e-3, 0.6, 1e-3, 16, steps)
+    p2, v2, a2 = torch.empty_like(vel), torch.empty_like(vel), torch.empty_like(vel)
+    eng.sim_store(p2, v2, a2)
+    # host path
+    eng.sim_step_host(hp, hv, ha, 1e-3, 0.6, 1e-3, 16, steps)
+    eng.check()
+    np.testing.assert_array_equal(hp.numpy(), p2.cpu().numpy())
+    np.testing.assert_array_equal(hv.numpy(), v2[:, :3].cpu().numpy())
+    np.testing.assert_array_equal(ha.numpy(), a2[:, :3].cpu().numpy())
+    eng.close()
