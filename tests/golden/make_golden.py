@@ -177,12 +177,33 @@ def gen_work_totals() -> None:
     print("work totals", totals)
 
 
-if __name__ == "__main__":
+def gen_report() -> None:
+    """The reference CLI's report and one snapshot file (harness.py:276-354)."""
+    import shutil
+    import tempfile
+
+    from nbsim.harness import main as nbsim_main
+
+    for alg, n, steps in ((1, 600, 8), (0, 300, 4)):
+        out = tempfile.mkdtemp()
+        args = ["--algorithm", str(alg), "--n", str(n), "--steps", str(steps), "--dt", "0.01",
+                "--eps", "0.05", "--seed", "3", "--snapshot-every", "4", "--audit-every", "4", "--out", out]
+        assert nbsim_main(args) == 0
+        shutil.copy(os.path.join(out, "report.txt"), os.path.join(HERE, f"report_alg{alg}.txt"))
+        shutil.copy(os.path.join(out, "snapshot_000004.csv"), os.path.join(HERE, f"snapshot_alg{alg}_000004.csv"))
+        shutil.rmtree(out)
+    print("reports", [f for f in os.listdir(HERE) if f.startswith(("report_", "snapshot_"))])
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "report":
+    gen_report()
+elif __name__ == "__main__":
     gen_keys()
     gen_trees()
     gen_plummer()
     gen_cfg0()
     gen_work_totals()
+    gen_report()
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))
