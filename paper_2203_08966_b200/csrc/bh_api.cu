@@ -76,7 +76,7 @@ struct bh_handle {
   int64_t nbranch = 0;
   // locally essential trees of the last build_local
   Buf let_present, let_expand, let_bodies, let_isbranch, let_rflag, let_bcount, let_rpos,
-      let_bpos, let_scan_tmp, let_brec, let_tail, let_boxkey;
+      let_bpos, let_scan_tmp, let_brec, let_tail, let_boxkey, let_lvl, let_list;
   uint32_t *hlet = nullptr;  // pinned: LET sizes per receiver
   // bh_sim_step_host: staging and the side stream for the early position copy
   Buf hs_a, hs_b, hs_pos;
@@ -272,16 +272,11 @@ int build_sorted(bh_handle *h, int64_t n, const float4 *bod32, const double4 *bo
   h->tbod32 = bod32;
   h->tbod64 = bod64;
   launch_emit(t, bod32, bod64, s);
-  LevelPlan plan;
-  int acc = 0;
   h->max_level = 0;
-  for (int l = 0; l <= kMaxLevel; ++l) {
-    plan.count[l] = h->hlvl[l];
-    plan.offset[l] = acc;
-    acc += h->hlvl[l];
+  for (int l = 0; l <= kMaxLevel; ++l)
     if (h->hlvl[l] > 0) h->max_level = l + 1;
-  }
-  launch_moments(t, plan, h->lvl.as<int>() + (kMaxLevel + 1), h->lvl_list.as<int>(), s);
+  // one cooperative sweep over the device level counts (no launch per level)
+  BH_CUDA((cudaError_t)launch_moments_coop(t, h->lvl.as<int>(), h->lvl_list.as<int>(), h->sms, s));
   BH_LAUNCHED();
   return BH_OK;
 }
@@ -654,7 +649,7 @@ int bh_destroy(bh_handle *h) {
                  &h->bk_pos, &h->bk_vel, &h->bk_acc, &h->bk_id, &h->bk_work,
                  &h->shared, &h->branch, &h->rec_of_cell, &h->wparent, &h->let_present,
                  &h->let_expand, &h->let_bodies, &h->let_isbranch, &h->let_rflag, &h->let_bcount,
-                 &h->let_rpos, &h->let_bpos, &h->let_scan_tmp, &h->let_brec, &h->let_tail, &h->let_boxkey, &h->hs_a, &h->hs_b, &h->hs_pos};
+                 &h->let_rpos, &h->let_bpos, &h->let_scan_tmp, &h->let_brec, &h->let_tail, &h->let_boxkey, &h->let_lvl, &h->let_list, &h->hs_a, &h->hs_b, &h->hs_pos};
   for (Buf *b : bufs) b->release();
   cudaFree(h->flags);
   cudaFreeHost(h->hflags);
@@ -1258,13 +1253,17 @@ int bh_sim_let(bh_handle *h, const double *d_boxes, int nbox, int nrank, int sel
   h->let_nrec = n;
   for (int q = 0; q < nrank; ++q) rec_counts[q] = body_counts[q] = 0;
   if (n == 0 || h->sim_n == 0) return BH_OK;
-  Buf *u32s[] = {&h->let_present, &h->let_expand, &h->let_bodies, &h->let_rflag, &h->let_bcount};
+  Buf *u32s[] = {&h->let_present, &h->let_expand, &h->let_bodies};
   for (Buf *b : u32s) BH_CUDA(b->ensure(sizeof(uint32_t) * (n + 1)));
-  BH_CUDA(h->let_rpos.ensure(sizeof(uint32_t) * (n + 1) * nrank));
-  BH_CUDA(h->let_bpos.ensure(sizeof(uint32_t) * (n + 1) * nrank));
+  const int64_t nn = n * nrank;  // [receiver][record]
+  BH_CUDA(h->let_rflag.ensure(sizeof(uint32_t) * (nn + 1)));
+  BH_CUDA(h->let_bcount.ensure(sizeof(uint32_t) * (nn + 1)));
+  BH_CUDA(h->let_rpos.ensure(sizeof(uint32_t) * (nn + 1)));  // inclusive scans
+  BH_CUDA(h->let_bpos.ensure(sizeof(uint32_t) * (nn + 1)));
   BH_CUDA(h->let_isbranch.ensure(n + 16));
   BH_CUDA(h->let_brec.ensure(sizeof(int) * (h->nbranch + 1)));
-  BH_CUDA(h->let_scan_tmp.ensure(scan_temp_bytes(n) + 16));
+  BH_CUDA(h->let_scan_tmp.ensure(inclusive_scan_temp_bytes(nn) + 16));
+  BH_CUDA(h->let_tail.ensure(sizeof(uint32_t) * 2 * nrank));
   h->tbegin(BH_PHASE_LET, s);
   BH_CUDA(cudaMemsetAsync(h->let_isbranch.p, 0, n, s));
   if (h->nbranch > 0)
@@ -1272,38 +1271,30 @@ int bh_sim_let(bh_handle *h, const double *d_boxes, int nbox, int nrank, int sel
         h->branch.as<int>() + 1, (int)h->nbranch, h->rec_of_cell.as<int>(), h->let_isbranch.as<uint8_t>(),
         h->let_brec.as<int>());
   const WalkNode *W = h->wnodes.as<WalkNode>();
+  BH_CUDA(h->let_lvl.ensure(sizeof(int) * 3 * (kMaxLevel + 1)));
+  BH_CUDA(h->let_list.ensure(sizeof(int) * (n + 1)));
   launch_let_mark(W, (int)n, h->wparent.as<int>(), h->let_isbranch.as<uint8_t>(), d_boxes, nbox, nrank, self,
-                  h->let_present.as<uint32_t>(), h->let_expand.as<uint32_t>(),
-                  h->let_bodies.as<uint32_t>(), s);
-  BH_CUDA(h->let_tail.ensure(sizeof(uint32_t) * 4 * nrank));
-  BH_CUDA(cudaMemsetAsync(h->let_tail.p, 0, sizeof(uint32_t) * 4 * nrank, s));
-  for (int q = 0; q < nrank; ++q) {
-    if (q == self) continue;
-    uint32_t *rpos = h->let_rpos.as<uint32_t>() + (n + 1) * q;
-    uint32_t *bpos = h->let_bpos.as<uint32_t>() + (n + 1) * q;
-    launch_let_flags(W, (int)n, h->let_isbranch.as<uint8_t>(), h->let_present.as<uint32_t>(),
-                     h->let_bodies.as<uint32_t>(), q, h->let_rflag.as<uint32_t>(),
-                     h->let_bcount.as<uint32_t>(), s);
-    BH_CUDA(exclusive_scan_u32(h->let_scan_tmp.p, h->let_scan_tmp.bytes, h->let_rflag.as<uint32_t>(),
-                               rpos, n, s));
-    BH_CUDA(exclusive_scan_u32(h->let_scan_tmp.p, h->let_scan_tmp.bytes, h->let_bcount.as<uint32_t>(),
-                               bpos, n, s));
-    uint32_t *tl = h->let_tail.as<uint32_t>() + 4 * q;  // device copies; one D2H below
-    BH_CUDA(cudaMemcpyAsync(tl, rpos + n - 1, 4, cudaMemcpyDeviceToDevice, s));
-    BH_CUDA(cudaMemcpyAsync(tl + 1, h->let_rflag.as<uint32_t>() + n - 1, 4, cudaMemcpyDeviceToDevice, s));
-    BH_CUDA(cudaMemcpyAsync(tl + 2, bpos + n - 1, 4, cudaMemcpyDeviceToDevice, s));
-    BH_CUDA(cudaMemcpyAsync(tl + 3, h->let_bcount.as<uint32_t>() + n - 1, 4, cudaMemcpyDeviceToDevice, s));
-  }
+                  h->let_lvl.as<int>(), h->let_list.as<int>(), h->sms, h->let_present.as<uint32_t>(),
+                  h->let_expand.as<uint32_t>(), h->let_bodies.as<uint32_t>(), s);
+  BH_CUDA(cudaGetLastError());
+  launch_let_flags_all(W, (int)n, h->let_isbranch.as<uint8_t>(), h->let_present.as<uint32_t>(),
+                       h->let_bodies.as<uint32_t>(), nrank, self, h->let_rflag.as<uint32_t>(),
+                       h->let_bcount.as<uint32_t>(), s);
+  BH_CUDA(inclusive_scan_u32(h->let_scan_tmp.p, h->let_scan_tmp.bytes, h->let_rflag.as<uint32_t>(),
+                             h->let_rpos.as<uint32_t>(), nn, s));
+  BH_CUDA(inclusive_scan_u32(h->let_scan_tmp.p, h->let_scan_tmp.bytes, h->let_bcount.as<uint32_t>(),
+                             h->let_bpos.as<uint32_t>(), nn, s));
+  launch_let_tails(h->let_rpos.as<uint32_t>(), h->let_bpos.as<uint32_t>(), (int)n, nrank,
+                   h->let_tail.as<uint32_t>(), s);
   h->tend(s);
-  BH_CUDA(cudaMemcpyAsync(h->hlet, h->let_tail.p, sizeof(uint32_t) * 4 * nrank, cudaMemcpyDeviceToHost, s));
+  BH_CUDA(cudaMemcpyAsync(h->hlet, h->let_tail.p, sizeof(uint32_t) * 2 * nrank, cudaMemcpyDeviceToHost, s));
   BH_CUDA(cudaStreamSynchronize(s));
-  const uint32_t *tail = h->hlet;
   for (int q = 0; q < nrank; ++q) {
     if (q == self) continue;
-    rec_counts[q] = (int64_t)tail[4 * q] + tail[4 * q + 1];
-    body_counts[q] = (int64_t)tail[4 * q + 2] + tail[4 * q + 3];
+    rec_counts[q] = h->hlet[2 * q];
+    body_counts[q] = h->hlet[2 * q + 1];
   }
-  h->launches += 2 + 22 + 3 * (nrank - 1);
+  h->launches += 8;
   BH_LAUNCHED();
   return BH_OK;
 }
@@ -1319,20 +1310,16 @@ int bh_sim_let_pack(bh_handle *h, int q, void *d_rec_out, float *d_bodies_out, i
   if (n == 0) return BH_OK;
   const WalkNode *W = h->wnodes.as<WalkNode>();
   h->tbegin(BH_PHASE_LET, s);
-  const uint32_t *rpos = h->let_rpos.as<uint32_t>() + (n + 1) * q;
-  const uint32_t *bpos = h->let_bpos.as<uint32_t>() + (n + 1) * q;
-  launch_let_flags(W, (int)n, h->let_isbranch.as<uint8_t>(), h->let_present.as<uint32_t>(),
-                   h->let_bodies.as<uint32_t>(), q, h->let_rflag.as<uint32_t>(),
-                   h->let_bcount.as<uint32_t>(), s);
-  launch_let_pack(W, (int)n, h->let_isbranch.as<uint8_t>(), h->let_expand.as<uint32_t>(),
-                  h->let_bodies.as<uint32_t>(), q, h->let_rflag.as<uint32_t>(), rpos, bpos,
-                  h->pos.as<float4>(), static_cast<WalkNode *>(d_rec_out),
+  launch_let_pack(W, (int)n, h->let_expand.as<uint32_t>(), h->let_bodies.as<uint32_t>(), q,
+                  h->let_rflag.as<uint32_t>(), h->let_rpos.as<uint32_t>(), h->let_bcount.as<uint32_t>(),
+                  h->let_bpos.as<uint32_t>(), h->pos.as<float4>(), static_cast<WalkNode *>(d_rec_out),
                   reinterpret_cast<float4 *>(d_bodies_out), s);
-  launch_let_branchmap(W, h->let_brec.as<int>(), (int)h->nbranch, h->let_expand.as<uint32_t>(),
-                       h->let_bodies.as<uint32_t>(), q, rpos, bpos, reinterpret_cast<int2 *>(d_bmap_out),
-                       s);
+  launch_let_branchmap(W, h->let_brec.as<int>(), (int)h->nbranch, (int)n, h->let_expand.as<uint32_t>(),
+                       h->let_bodies.as<uint32_t>(), q, h->let_rflag.as<uint32_t>(), h->let_rpos.as<uint32_t>(),
+                       h->let_bcount.as<uint32_t>(), h->let_bpos.as<uint32_t>(),
+                       reinterpret_cast<int2 *>(d_bmap_out), s);
   h->tend(s);
-  h->launches += 3;
+  h->launches += 2;
   BH_LAUNCHED();
   return BH_OK;
 }

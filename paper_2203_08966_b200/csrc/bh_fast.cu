@@ -189,5 +189,14 @@ cudaError_t exclusive_scan_u32(void *temp, size_t temp_bytes, const uint32_t *in
                                int64_t n, cudaStream_t s) {
   return cub::DeviceScan::ExclusiveSum(temp, temp_bytes, in, out, (int)n, s);
 }
+size_t inclusive_scan_temp_bytes(int64_t n) {
+  size_t bytes = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, bytes, (const uint32_t *)nullptr, (uint32_t *)nullptr, (int)n);
+  return bytes;
+}
+cudaError_t inclusive_scan_u32(void *temp, size_t temp_bytes, const uint32_t *in, uint32_t *out,
+                               int64_t n, cudaStream_t s) {
+  return cub::DeviceScan::InclusiveSum(temp, temp_bytes, in, out, (int)n, s);
+}
 
 }  // namespace bh

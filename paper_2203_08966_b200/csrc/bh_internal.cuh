@@ -162,17 +162,22 @@ void launch_walk_tree(const TreeView &t, const double *dR, double theta, int lea
                       int *wparent = nullptr);
 // locally essential trees (bh_walk.cu)
 void launch_let_mark(const WalkNode *W, int nrec, const int *wparent, const uint8_t *isbranch,
-                     const double *boxes, int nbox, int nrank, int self, uint32_t *present,
-                     uint32_t *expand, uint32_t *bodies, cudaStream_t s);
-void launch_let_flags(const WalkNode *W, int nrec, const uint8_t *isbranch, const uint32_t *present,
-                      const uint32_t *bodies, int q, uint32_t *rflag, uint32_t *bcount, cudaStream_t s);
-void launch_let_pack(const WalkNode *W, int nrec, const uint8_t *isbranch, const uint32_t *expand,
-                     const uint32_t *bodies, int q, const uint32_t *rflag, const uint32_t *rpos,
-                     const uint32_t *bpos, const float4 *src_bodies, WalkNode *out, float4 *out_bodies,
+                     const double *boxes, int nbox, int nrank, int self, int *lvl /* 3 x 22 ints */,
+                     int *list /* nrec */, int sms, uint32_t *present, uint32_t *expand, uint32_t *bodies,
                      cudaStream_t s);
-void launch_let_branchmap(const WalkNode *W, const int *brec, int nb, const uint32_t *expand,
-                          const uint32_t *bodies, int q, const uint32_t *rpos, const uint32_t *bpos,
-                          int2 *map, cudaStream_t s);
+// all receivers at once: rflag/bcount [nrank][nrec]; after inclusive scans of
+// both (rinc/binc), tails[2q..] = receiver q's record and body counts
+void launch_let_flags_all(const WalkNode *W, int nrec, const uint8_t *isbranch, const uint32_t *present,
+                          const uint32_t *bodies, int nrank, int self, uint32_t *rflag, uint32_t *bcount,
+                          cudaStream_t s);
+void launch_let_tails(const uint32_t *rinc, const uint32_t *binc, int nrec, int nrank, uint32_t *tails,
+                      cudaStream_t s);
+void launch_let_pack(const WalkNode *W, int nrec, const uint32_t *expand, const uint32_t *bodies, int q,
+                     const uint32_t *rflag, const uint32_t *rinc, const uint32_t *bcount, const uint32_t *binc,
+                     const float4 *src_bodies, WalkNode *out, float4 *out_bodies, cudaStream_t s);
+void launch_let_branchmap(const WalkNode *W, const int *brec, int nb, int nrec, const uint32_t *expand,
+                          const uint32_t *bodies, int q, const uint32_t *rflag, const uint32_t *rinc,
+                          const uint32_t *bcount, const uint32_t *binc, int2 *map, cudaStream_t s);
 // distributed build
 void launch_mark_shared(const TreeView &t, uint8_t *shared, int *branch, int *nbranch,
                         cudaStream_t s);
@@ -222,6 +227,9 @@ size_t sort_temp_bytes(int64_t n);
 cudaError_t sort_pairs(void *temp, size_t temp_bytes, const uint64_t *kin, uint64_t *kout,
                        const uint32_t *vin, uint32_t *vout, int64_t n, cudaStream_t s);
 size_t scan_temp_bytes(int64_t n);
+size_t inclusive_scan_temp_bytes(int64_t n);
+cudaError_t inclusive_scan_u32(void *temp, size_t temp_bytes, const uint32_t *in, uint32_t *out,
+                               int64_t n, cudaStream_t s);
 cudaError_t exclusive_scan_u32(void *temp, size_t temp_bytes, const uint32_t *in, uint32_t *out,
                                int64_t n, cudaStream_t s);
 

@@ -38,7 +38,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <climits>
+#include <cooperative_groups.h>
 
 #include "bh_internal.cuh"
 
@@ -144,125 +146,211 @@ void launch_walk_tree(const TreeView &t, const double *dR, double theta, int lea
 // of a receiver if, for each of the receiver's target boxes, even the box point
 // nearest its com passes the MAC with a relative margin that covers the fp32
 // rounding of d2 on the receiving side.  Empty boxes (lo > hi) never object.
-// box[0] is the union of the receiver's boxes: passing it passes them all.
-__device__ __forceinline__ bool accepted_by_all(const WalkNode &r, const double *box, int nbox) {
-  const double c[3] = {-(double)r.a.x, -(double)r.a.y, -(double)r.a.z};
-  const double lim = (double)r.a.w * (1.0 + 1e-5) + 1e-30;
-  for (int k = 0; k < nbox; ++k, box += 6) {
-    double d2 = 0.0;
+__device__ __forceinline__ double box_d2(const double c[3], const double *box) {
+  double d2 = 0.0;
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      const double lo = box[a], hi = box[3 + a];
-      const double g = c[a] < lo ? lo - c[a] : (c[a] > hi ? c[a] - hi : 0.0);
-      d2 += g * g;
-    }
-    if (d2 > lim) {
-      if (k == 0) return true;  // clear of the union box
-    } else if (k > 0 || nbox == 1) {
-      return false;
-    }
+  for (int a = 0; a < 3; ++a) {
+    const double lo = box[a], hi = box[3 + a];
+    const double g = c[a] < lo ? lo - c[a] : (c[a] > hi ? c[a] - hi : 0.0);
+    d2 += g * g;
   }
-  return true;  // near the union, but clear of every member box
+  return d2;
 }
 
-// One level of the top-down marking, for all receivers at once (bit q):
-// present = the receiver's walk can reach the record (branch roots always;
-// otherwise its parent is expanded); expand = present and not taken by all
-// of the receiver's targets (its children are needed); bodies = present bucket
-// not taken by all (its bodies are needed).  boxes: [nrank][nbox][6].
-__global__ void k_let_mark(const WalkNode *__restrict__ W, int nrec, const int *__restrict__ wparent,
-                           const uint8_t *__restrict__ isbranch, const double *__restrict__ boxes,
-                           int nbox, int nrank, int self, int level, uint32_t *__restrict__ present,
-                           uint32_t *__restrict__ expand, uint32_t *__restrict__ bodies) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= nrec) return;
+// One record, one warp: the receivers' member boxes are tested lane-parallel
+// A record is taken by every target of receiver q if it is clear of q's union
+// box (box 0: passing it passes them all) or of every member box.
+__device__ __forceinline__ void let_mark_warp(const WalkNode *__restrict__ W, int j, const int *__restrict__ wparent,
+                                              const uint8_t *__restrict__ isbranch, const double *__restrict__ boxes,
+                                              int nbox, int nrank, int self, uint32_t *__restrict__ present,
+                                              uint32_t *__restrict__ expand, uint32_t *__restrict__ bodies) {
+  const unsigned lane = threadIdx.x & 31;
   const WalkNode r = W[j];
-  if (r.d.w != level) return;
   const uint32_t all = ((nrank >= 32 ? 0xffffffffu : (1u << nrank) - 1u)) & ~(1u << self);
-  uint32_t p = isbranch[j] ? all : (wparent[j] >= 0 ? expand[wparent[j]] : 0u);
-  uint32_t e = 0, b = 0;
+  const uint32_t p = isbranch[j] ? all : (wparent[j] >= 0 ? expand[wparent[j]] : 0u);
+  uint32_t fail = 0;
   if (p && r.d.y > 1) {
-    uint32_t fail = 0;
-    for (int q = 0; q < nrank; ++q)
-      if (((p >> q) & 1u) && !accepted_by_all(r, boxes + (size_t)6 * nbox * q, nbox)) fail |= 1u << q;
-    if (r.d.z > 0) e = p & fail;
-    else b = p & fail;
+    const double c[3] = {-(double)r.a.x, -(double)r.a.y, -(double)r.a.z};
+    const double lim = (double)r.a.w * (1.0 + 1e-5) + 1e-30;
+    for (int q = 0; q < nrank; ++q) {
+      if (!((p >> q) & 1u)) continue;
+      const double *bq = boxes + (size_t)6 * nbox * q;
+      if (box_d2(c, bq) > lim) continue;  // clear of the union: taken by every target of q
+      bool f = nbox == 1;
+      for (int k = 1 + (int)lane; k < nbox; k += 32) f = f || !(box_d2(c, bq + 6 * k) > lim);
+      if (__any_sync(0xffffffffu, f)) fail |= 1u << q;
+    }
   }
-  present[j] = p;
-  expand[j] = e;
-  bodies[j] = b;
+  if (lane == 0) {
+    present[j] = p;
+    expand[j] = r.d.z > 0 ? (p & fail) : 0u;
+    bodies[j] = (r.d.z > 0 || r.d.y <= 1) ? 0u : (p & fail);
+  }
 }
 
-__global__ void k_let_flags(const WalkNode *__restrict__ W, int nrec, const uint8_t *__restrict__ isbranch,
-                            const uint32_t *__restrict__ present, const uint32_t *__restrict__ bodies,
-                            int q, uint32_t *__restrict__ rflag, uint32_t *__restrict__ bcount) {
+// One cooperative launch: bucket the records by level, then sweep the levels
+// top-down with a grid barrier between them (a record's parent is one level up).
+namespace cg = cooperative_groups;
+__global__ void __launch_bounds__(256) k_let_mark_coop(const WalkNode *__restrict__ W, int nrec,
+                                                       const int *__restrict__ wparent,
+                                                       const uint8_t *__restrict__ isbranch,
+                                                       const double *__restrict__ boxes, int nbox, int nrank,
+                                                       int self, int *__restrict__ lvl, int *__restrict__ list,
+                                                       uint32_t *__restrict__ present, uint32_t *__restrict__ expand,
+                                                       uint32_t *__restrict__ bodies) {
+  cg::grid_group grid = cg::this_grid();
+  int *cnt = lvl, *offs = lvl + (kMaxLevel + 1), *cur = lvl + 2 * (kMaxLevel + 1);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid <= kMaxLevel) { cnt[tid] = 0; cur[tid] = 0; }
+  grid.sync();
+  __shared__ int h[kMaxLevel + 1], base[kMaxLevel + 1];
+  for (int64_t c0 = (int64_t)blockIdx.x * blockDim.x; c0 < nrec; c0 += stride) {  // level histogram
+    if (threadIdx.x <= kMaxLevel) h[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t j = c0 + threadIdx.x;
+    if (j < nrec) atomicAdd(&h[W[j].d.w], 1);
+    __syncthreads();
+    if (threadIdx.x <= kMaxLevel && h[threadIdx.x]) atomicAdd(&cnt[threadIdx.x], h[threadIdx.x]);
+    __syncthreads();
+  }
+  grid.sync();
+  if (tid == 0) {
+    int acc = 0;
+    for (int l = 0; l <= kMaxLevel; ++l) { offs[l] = acc; acc += cnt[l]; }
+  }
+  grid.sync();
+  for (int64_t c0 = (int64_t)blockIdx.x * blockDim.x; c0 < nrec; c0 += stride) {  // bucket by level
+    if (threadIdx.x <= kMaxLevel) h[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t j = c0 + threadIdx.x;
+    int l = -1, rank = 0;
+    if (j < nrec) { l = W[j].d.w; rank = atomicAdd(&h[l], 1); }
+    __syncthreads();
+    if (threadIdx.x <= kMaxLevel && h[threadIdx.x])
+      base[threadIdx.x] = offs[threadIdx.x] + atomicAdd(&cur[threadIdx.x], h[threadIdx.x]);
+    __syncthreads();
+    if (l >= 0) list[base[l] + rank] = (int)j;
+    __syncthreads();
+  }
+  grid.sync();
+  const int64_t warp = tid >> 5, nwarps = stride >> 5;
+  for (int l = 0; l <= kMaxLevel; ++l) {
+    const int n_l = cnt[l];
+    if (n_l == 0) continue;
+    for (int64_t k = warp; k < n_l; k += nwarps)
+      let_mark_warp(W, list[offs[l] + k], wparent, isbranch, boxes, nbox, nrank, self, present, expand, bodies);
+    grid.sync();
+  }
+}
+
+// all receivers at once (grid.y = receiver): rflag = the record goes to q
+// (present and not a branch node -- those travel with the branch allgather);
+// bcount = bodies shipped with it
+__global__ void k_let_flags_all(const WalkNode *__restrict__ W, int nrec, const uint8_t *__restrict__ isbranch,
+                                const uint32_t *__restrict__ present, const uint32_t *__restrict__ bodies,
+                                int self, uint32_t *__restrict__ rflag, uint32_t *__restrict__ bcount) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int q = blockIdx.y;
   if (j >= nrec) return;
-  rflag[j] = (!isbranch[j] && ((present[j] >> q) & 1u)) ? 1u : 0u;
-  bcount[j] = ((bodies[j] >> q) & 1u) ? (uint32_t)W[j].d.y : 0u;
+  const size_t o = (size_t)q * nrec + j;
+  const bool me = q == self;
+  rflag[o] = (!me && !isbranch[j] && ((present[j] >> q) & 1u)) ? 1u : 0u;
+  bcount[o] = (!me && ((bodies[j] >> q) & 1u)) ? (uint32_t)W[j].d.y : 0u;
+}
+
+// receiver q's LET sizes from the inclusive scans over [nrank][nrec]
+__global__ void k_let_tails(const uint32_t *__restrict__ rinc, const uint32_t *__restrict__ binc, int nrec,
+                            int nrank, uint32_t *__restrict__ tails) {
+  const int q = threadIdx.x;
+  if (q >= nrank) return;
+  const size_t e = (size_t)(q + 1) * nrec - 1, b = (size_t)q * nrec;
+  tails[2 * q] = rinc[e] - (q ? rinc[b - 1] : 0u);
+  tails[2 * q + 1] = binc[e] - (q ? binc[b - 1] : 0u);
+}
+
+// exclusive position of record j in receiver q's LET / body list
+__device__ __forceinline__ uint32_t let_pos(const uint32_t *flag, const uint32_t *inc, int nrec, int q, int j) {
+  const size_t o = (size_t)q * nrec + j;
+  return inc[o] - flag[o] - (q ? inc[(size_t)q * nrec - 1] : 0u);
 }
 
 // Pack the LET for receiver q: its records in W order (children blocks stay
 // contiguous), child links remapped into the LET, bucket body ranges into the
 // LET's body list; records the receiver never opens get nchild = 0.
-__global__ void k_let_pack(const WalkNode *__restrict__ W, int nrec, const uint8_t *__restrict__ isbranch,
-                           const uint32_t *__restrict__ expand, const uint32_t *__restrict__ bodies,
-                           int q, const uint32_t *__restrict__ rflag, const uint32_t *__restrict__ rpos,
-                           const uint32_t *__restrict__ bpos, const float4 *__restrict__ src_bodies,
+__global__ void k_let_pack(const WalkNode *__restrict__ W, int nrec, const uint32_t *__restrict__ expand,
+                           const uint32_t *__restrict__ bodies, int q, const uint32_t *__restrict__ rflag,
+                           const uint32_t *__restrict__ rinc, const uint32_t *__restrict__ bcount,
+                           const uint32_t *__restrict__ binc, const float4 *__restrict__ src_bodies,
                            WalkNode *__restrict__ out, float4 *__restrict__ out_bodies) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= nrec) return;
   const bool body_need = (bodies[j] >> q) & 1u;
-  if (body_need)
-    for (int k = 0; k < W[j].d.y; ++k) out_bodies[bpos[j] + k] = src_bodies[W[j].d.x + k];
-  if (!rflag[j]) return;
+  if (body_need) {
+    const uint32_t bp = let_pos(bcount, binc, nrec, q, j);
+    for (int k = 0; k < W[j].d.y; ++k) out_bodies[bp + k] = src_bodies[W[j].d.x + k];
+  }
+  if (!rflag[(size_t)q * nrec + j]) return;
   WalkNode r = W[j];
-  if ((expand[j] >> q) & 1u) r.d.x = (int)rpos[r.d.x];
-  else if (body_need) r.d.x = (int)bpos[j];
+  if ((expand[j] >> q) & 1u) r.d.x = (int)let_pos(rflag, rinc, nrec, q, r.d.x);
+  else if (body_need) r.d.x = (int)let_pos(bcount, binc, nrec, q, j);
   else { r.d.z = 0; if (r.d.y > 1) r.d.x = -1; }  // never opened by the receiver
-  out[rpos[j]] = r;
+  out[let_pos(rflag, rinc, nrec, q, j)] = r;
 }
 
 // Branch roots for receiver q: (first child in the LET | -1, first body in
 // the LET's body list | -1).
-__global__ void k_let_branchmap(const WalkNode *__restrict__ W, const int *__restrict__ brec, int nb,
-                                const uint32_t *__restrict__ expand, const uint32_t *__restrict__ bodies,
-                                int q, const uint32_t *__restrict__ rpos,
-                                const uint32_t *__restrict__ bpos, int2 *__restrict__ map) {
+__global__ void k_let_branchmap(const WalkNode *__restrict__ W, const int *__restrict__ brec, int nb, int nrec,
+                                const uint32_t *__restrict__ expand, const uint32_t *__restrict__ bodies, int q,
+                                const uint32_t *__restrict__ rflag, const uint32_t *__restrict__ rinc,
+                                const uint32_t *__restrict__ bcount, const uint32_t *__restrict__ binc,
+                                int2 *__restrict__ map) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= nb) return;
   const int j = brec[k];
   const WalkNode r = W[j];
-  map[k] = make_int2(((expand[j] >> q) & 1u) ? (int)rpos[r.d.x] : -1,
-                     ((bodies[j] >> q) & 1u) ? (int)bpos[j] : -1);
+  map[k] = make_int2(((expand[j] >> q) & 1u) ? (int)let_pos(rflag, rinc, nrec, q, r.d.x) : -1,
+                     ((bodies[j] >> q) & 1u) ? (int)let_pos(bcount, binc, nrec, q, j) : -1);
 }
 
 void launch_let_mark(const WalkNode *W, int nrec, const int *wparent, const uint8_t *isbranch,
-                     const double *boxes, int nbox, int nrank, int self, uint32_t *present,
-                     uint32_t *expand, uint32_t *bodies, cudaStream_t s) {
+                     const double *boxes, int nbox, int nrank, int self, int *lvl, int *list, int sms,
+                     uint32_t *present, uint32_t *expand, uint32_t *bodies, cudaStream_t s) {
   if (nrec <= 0) return;
-  for (int l = 0; l <= kMaxLevel; ++l)
-    k_let_mark<<<grid_for(nrec, 256), 256, 0, s>>>(W, nrec, wparent, isbranch, boxes, nbox, nrank, self,
-                                                   l, present, expand, bodies);
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_let_mark_coop, 256, 0);
+    if (per_sm < 1) per_sm = 1;
+  }
+  const int blocks = (int)std::min<int64_t>((int64_t)sms * per_sm, ((int64_t)nrec + 255) / 256);
+  void *args[] = {(void *)&W, &nrec, (void *)&wparent, (void *)&isbranch, (void *)&boxes, &nbox, &nrank, &self,
+                  &lvl, &list, &present, &expand, &bodies};
+  cudaLaunchCooperativeKernel((void *)k_let_mark_coop, dim3(blocks < 1 ? 1 : blocks), dim3(256), args, 0, s);
 }
-void launch_let_flags(const WalkNode *W, int nrec, const uint8_t *isbranch, const uint32_t *present,
-                      const uint32_t *bodies, int q, uint32_t *rflag, uint32_t *bcount, cudaStream_t s) {
+void launch_let_flags_all(const WalkNode *W, int nrec, const uint8_t *isbranch, const uint32_t *present,
+                          const uint32_t *bodies, int nrank, int self, uint32_t *rflag, uint32_t *bcount,
+                          cudaStream_t s) {
   if (nrec <= 0) return;
-  k_let_flags<<<grid_for(nrec, 256), 256, 0, s>>>(W, nrec, isbranch, present, bodies, q, rflag, bcount);
+  dim3 g(grid_for(nrec, 256), nrank);
+  k_let_flags_all<<<g, 256, 0, s>>>(W, nrec, isbranch, present, bodies, self, rflag, bcount);
 }
-void launch_let_pack(const WalkNode *W, int nrec, const uint8_t *isbranch, const uint32_t *expand,
-                     const uint32_t *bodies, int q, const uint32_t *rflag, const uint32_t *rpos,
-                     const uint32_t *bpos, const float4 *src_bodies, WalkNode *out, float4 *out_bodies,
-                     cudaStream_t s) {
+void launch_let_tails(const uint32_t *rinc, const uint32_t *binc, int nrec, int nrank, uint32_t *tails,
+                      cudaStream_t s) {
+  k_let_tails<<<1, 32, 0, s>>>(rinc, binc, nrec, nrank, tails);
+}
+void launch_let_pack(const WalkNode *W, int nrec, const uint32_t *expand, const uint32_t *bodies, int q,
+                     const uint32_t *rflag, const uint32_t *rinc, const uint32_t *bcount, const uint32_t *binc,
+                     const float4 *src_bodies, WalkNode *out, float4 *out_bodies, cudaStream_t s) {
   if (nrec <= 0) return;
-  k_let_pack<<<grid_for(nrec, 256), 256, 0, s>>>(W, nrec, isbranch, expand, bodies, q, rflag, rpos, bpos,
+  k_let_pack<<<grid_for(nrec, 256), 256, 0, s>>>(W, nrec, expand, bodies, q, rflag, rinc, bcount, binc,
                                                  src_bodies, out, out_bodies);
 }
-void launch_let_branchmap(const WalkNode *W, const int *brec, int nb, const uint32_t *expand,
-                          const uint32_t *bodies, int q, const uint32_t *rpos, const uint32_t *bpos,
-                          int2 *map, cudaStream_t s) {
+void launch_let_branchmap(const WalkNode *W, const int *brec, int nb, int nrec, const uint32_t *expand,
+                          const uint32_t *bodies, int q, const uint32_t *rflag, const uint32_t *rinc,
+                          const uint32_t *bcount, const uint32_t *binc, int2 *map, cudaStream_t s) {
   if (nb <= 0) return;
-  k_let_branchmap<<<grid_for(nb, 128), 128, 0, s>>>(W, brec, nb, expand, bodies, q, rpos, bpos, map);
+  k_let_branchmap<<<grid_for(nb, 128), 128, 0, s>>>(W, brec, nb, nrec, expand, bodies, q, rflag, rinc, bcount,
+                                                    binc, map);
 }
 
 __device__ __forceinline__ float2 f2(float x, float y) { return make_float2(x, y); }

@@ -654,7 +654,8 @@ class DistributedBuildSim:
                 eng.sim_scatter_work()
         self._t("walk")
         self._keys, self._n, self._nb = keys, n, nb
-        self._acc, self._work = acc, work
+        # the last step's walk inputs (replayed by tools/dist_emulate.py)
+        self.last = dict(bodies=gbodies, targets=bodies, boxes=boxes, bounds=(prev, nxt))
 
     LET_BOXES = 64  # target boxes per rank (groups of consecutive branch nodes)
 
