@@ -484,7 +484,8 @@ class DistributedBuildSim:
         """Before any work is known: equal-count splitters from a key sample."""
         size = self.comm.size
         k = keys.shape[0]
-        idx = torch.linspace(0, max(k - 1, 0), min(k, 512), device=keys.device).long()
+        m = min(k, 512)  # integer sample positions (a float32 linspace rounds past k-1 above 2^24)
+        idx = (torch.arange(m, device=keys.device, dtype=torch.int64) * max(k - 1, 0)) // max(m - 1, 1)
         samp = keys[idx] if k else keys
         allk = torch.sort(torch.cat(self._allgather_v(samp))).values
         if size == 1 or allk.numel() == 0:
