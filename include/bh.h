@@ -216,6 +216,19 @@ int bh_sim_walk_records(bh_handle *h, void *d_out, int64_t *n_out, void *stream)
  * whose union covers each rank's bodies.  let: sizes per receiver (host arrays,
  * synchronises); let_pack: the receiver's records, bodies and branch map
  * ([nbranch][2] ints: first child in the LET | -1, first body | -1). */
+/* The LET exchange overlapped with the walk.  Pass A walks the
+ * local part of an assembled tree while the LETs are in flight: records whose
+ * d.w carries bit 30 (remote branch nodes) are not opened; each warp appends
+ * (target chunk, record, m0, m1) to d_defer (int4 x cap; *d_count = entries,
+ * possibly > cap = overflow).  Pass B walks those entries over the completed
+ * tree, d_fcnc[record] = (first child, nchild), adding into acc and work. */
+int bh_walk_records_defer_f32(bh_handle *h, const void *d_records, int64_t nrec, const float *d_bodies4,
+                              const float *d_targets4, int64_t nt, double eps, int leaf_size, float *d_acc4,
+                              int32_t *d_work, int32_t *d_defer, uint32_t *d_count, int64_t cap, void *stream);
+int bh_walk_records_resume_f32(bh_handle *h, const void *d_records, int64_t nrec, const float *d_bodies4,
+                               const float *d_targets4, int64_t nt, double eps, int leaf_size, float *d_acc4,
+                               int32_t *d_work, const int32_t *d_entries, int64_t n_entries,
+                               const int32_t *d_fcnc, void *stream);
 /* Bounding boxes of contiguous ranges of this rank's sorted bodies (the LET
  * target region): d_start[ngroup + 1] body offsets (device int64); d_out
  * [(1 + ngroup) * 6] device doubles: the union, then one box per range

@@ -41,6 +41,7 @@ EXPORTS = (
     "bh_sim_local_maxabs", "bh_sim_set_R", "bh_sim_sort", "bh_sim_keys", "bh_sim_load_state",
     "bh_sim_build_local", "bh_sim_branch_export", "bh_sim_walk_records", "bh_walk_records_f32",
     "bh_sim_let", "bh_sim_let_pack", "bh_sim_target_boxes", "bh_sim_step_host",
+    "bh_walk_records_defer_f32", "bh_walk_records_resume_f32",
     "bh_timing_enable", "bh_timing_reset", "bh_timing_get", "bh_ffma_peak",
     "bh_ic_plummer", "bh_host_potential_pairs",
 )
@@ -121,6 +122,8 @@ def _declare(L: ctypes.CDLL) -> None:
         "bh_sim_let_pack": ([P, I, P, P, P, P], I),
         "bh_sim_target_boxes": ([P, P, I, P, P], I),
         "bh_sim_step_host": ([P, P, P, P, I64, D, D, D, I, I, P], I),
+        "bh_walk_records_defer_f32": ([P, P, I64, P, P, I64, D, I, P, P, P, P, I64, P], I),
+        "bh_walk_records_resume_f32": ([P, P, I64, P, P, I64, D, I, P, P, P, I64, P, P], I),
         "bh_timing_enable": ([P, I], I),
         "bh_timing_reset": ([P], I),
         "bh_timing_get": ([P, ctypes.POINTER(D), I], I),

@@ -1482,6 +1482,55 @@ int bh_walk_records_f32(bh_handle *h, const void *d_records, int64_t nrec, const
   return BH_OK;
 }
 
+// The LET overlap, pass A: walk over the local part of the
+// assembled tree; remote branch records flagged (d.w | 1<<30) are not opened
+// and each warp's (target chunk, record, masks) goes to d_defer[cap] (count in
+// *d_count; entries past cap are dropped and the count says so).
+int bh_walk_records_defer_f32(bh_handle *h, const void *d_records, int64_t nrec, const float *d_bodies4,
+                              const float *d_targets4, int64_t nt, double eps, int leaf_size, float *d_acc4,
+                              int32_t *d_work, int32_t *d_defer, uint32_t *d_count, int64_t cap, void *stream) {
+  if (!h || nrec <= 0 || !d_records || nt < 0 || (nt && (!d_targets4 || !d_acc4)) || !d_defer || !d_count)
+    return fail(BH_BAD_ARG, "bh_walk_records_defer_f32: bad args");
+  cudaStream_t s = S(stream);
+  BH_TRY(reset_counters(h, s));
+  BH_CUDA(cudaMemsetAsync(d_count, 0, sizeof(uint32_t), s));
+  DeferArgs dfr;
+  dfr.out = reinterpret_cast<int4 *>(d_defer);
+  dfr.count = d_count;
+  dfr.cap = (int)std::min<int64_t>(cap, 0x7fffffff);
+  h->tbegin(BH_PHASE_WALK, s);
+  launch_walk_defer_f32(static_cast<const WalkNode *>(d_records), reinterpret_cast<const float4 *>(d_bodies4),
+                        d_targets4, (int)nt, (float)(eps * eps), leaf_size, d_acc4, d_work, h->flags, dfr, false, s);
+  h->tend(s);
+  h->launches += 1;
+  BH_LAUNCHED();
+  return BH_OK;
+}
+
+// Pass B: resume the deferred entries d_entries[n_entries] (target chunk,
+// record, m0, m1) over the full tree, d_fcnc[record] = (first child, nchild);
+// results are added into d_acc4 / d_work.
+int bh_walk_records_resume_f32(bh_handle *h, const void *d_records, int64_t nrec, const float *d_bodies4,
+                               const float *d_targets4, int64_t nt, double eps, int leaf_size, float *d_acc4,
+                               int32_t *d_work, const int32_t *d_entries, int64_t n_entries,
+                               const int32_t *d_fcnc, void *stream) {
+  if (!h || nrec <= 0 || !d_records || nt < 0 || n_entries < 0 || (n_entries && (!d_entries || !d_fcnc)))
+    return fail(BH_BAD_ARG, "bh_walk_records_resume_f32: bad args");
+  if (n_entries == 0 || nt == 0) return BH_OK;
+  cudaStream_t s = S(stream);
+  DeferArgs dfr;
+  dfr.in = reinterpret_cast<const int4 *>(d_entries);
+  dfr.nin = (int)n_entries;
+  dfr.fcnc = reinterpret_cast<const int2 *>(d_fcnc);
+  h->tbegin(BH_PHASE_WALK, s);
+  launch_walk_defer_f32(static_cast<const WalkNode *>(d_records), reinterpret_cast<const float4 *>(d_bodies4),
+                        d_targets4, (int)nt, (float)(eps * eps), leaf_size, d_acc4, d_work, h->flags, dfr, true, s);
+  h->tend(s);
+  h->launches += 1;
+  BH_LAUNCHED();
+  return BH_OK;
+}
+
 int bh_sim_export(bh_handle *h, int what, int64_t begin, int64_t end, void *dst, void *stream) {
   if (!h || !dst || begin < 0 || end > h->sim_n || begin > end)
     return fail(BH_BAD_ARG, "bh_sim_export: bad args");

@@ -187,6 +187,20 @@ void launch_branch_export(const TreeView &t, const int *branch, int nb, const in
 void launch_walk_f32(const WalkNode *T, const float4 *bodies, const float *targets, int tstride,
                      const uint32_t *tperm, int nt, float e2, int leaf, float *acc, int astride,
                      int64_t *work64, int *work32, DeviceFlags *f, cudaStream_t s);
+// deferred walk (LET overlap): pass A appends (target chunk, record, m0, m1) to
+// out[cap] for records flagged in d.w; pass B (resume) walks in[nin] with
+// fcnc[record] = (first child, nchild) and adds into acc/work atomically
+struct DeferArgs {
+  int4 *out = nullptr;
+  unsigned *count = nullptr;
+  int cap = 0;
+  const int4 *in = nullptr;
+  int nin = 0;
+  const int2 *fcnc = nullptr;
+};
+void launch_walk_defer_f32(const WalkNode *T, const float4 *bodies, const float *targets, int nt, float e2,
+                           int leaf, float *acc, int *work32, DeviceFlags *f, const DeferArgs &dfr,
+                           bool resume, cudaStream_t s);
 void launch_walk_f64(const WalkParams &p, const double4 *cm64, const double *q64,
                      const int4 *link, const double4 *bodies, const double *targets,
                      int tstride, const uint32_t *tperm, double *acc, int astride,

@@ -373,16 +373,33 @@ extern "C" int bh_debug_walk_hist(unsigned long long *out) {
 }
 #endif
 
-template <bool BUCKET>
+// Walk modes (the LET overlap of the distributed step):
+//   kWalkFull   -- the whole tree;
+//   kWalkDefer  -- pass A: records flagged kDeferBit in d.w (remote branch nodes
+//                  whose subtrees are still in flight) are not opened; the
+//                  warp's (record, masks) is appended to a list instead;
+//   kWalkResume -- pass B: one warp per deferred (target chunk, record, masks),
+//                  walking the record's subtree (first child, nchild from
+//                  fcnc[record]) and adding into acc/work atomically.
+enum { kWalkFull = 0, kWalkDefer = 1, kWalkResume = 2 };
+constexpr int kDeferBit = 1 << 30;
+
+template <bool BUCKET, int MODE>
 __global__ void __launch_bounds__(kWalkBlock, BH_WALK_MINB) k_walk(
     const WalkNode *__restrict__ T, const float4 *__restrict__ bodies,
     const float *__restrict__ targets, int tstride, const uint32_t *__restrict__ tperm, int nt,
     float e2, int leaf, float *__restrict__ acc, int astride, int64_t *__restrict__ work64,
-    int *__restrict__ work32, DeviceFlags *f) {
+    int *__restrict__ work32, DeviceFlags *f, DeferArgs dfr) {
   __shared__ int4 stack_all[kWalkBlock / 32][kStack];
   int4 *stk = stack_all[threadIdx.x >> 5];
   const unsigned lane = threadIdx.x & 31;
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int4 entry = make_int4(0, 0, 0, 0);
+  if (MODE == kWalkResume) {
+    if (gwarp >= dfr.nin) return;  // warp-uniform
+    entry = dfr.in[gwarp];
+  }
+  const int64_t warp = MODE == kWalkResume ? (int64_t)entry.x : gwarp;
   const int64_t t0 = warp * 64 + 2 * lane, t1 = t0 + 1;
   const bool v0 = t0 < nt, v1 = t1 < nt;
   const int64_t s0 = v0 ? (tperm ? (int64_t)tperm[t0] : t0) : 0;
@@ -397,7 +414,10 @@ __global__ void __launch_bounds__(kWalkBlock, BH_WALK_MINB) k_walk(
 
   // current entry: examine children [fc, fc+nc) for the targets in (m0, m1)
   int4 e = make_int4(0, 1, (int)__ballot_sync(0xffffffffu, v0), (int)__ballot_sync(0xffffffffu, v1));
-  if (T[0].d.y > 1) {  // root internal: the walk starts at its children (flattree.py:271-279)
+  if (MODE == kWalkResume) {
+    const int2 fc = dfr.fcnc[entry.y];
+    e = make_int4(fc.x, fc.y, entry.z, entry.w);
+  } else if (T[0].d.y > 1) {  // root internal: the walk starts at its children (flattree.py:271-279)
     const int4 rd = T[0].d;
     e.x = rd.x;
     e.y = rd.z;
@@ -458,6 +478,11 @@ __global__ void __launch_bounds__(kWalkBlock, BH_WALK_MINB) k_walk(
       if (d.z > 0) {  // open: its children become an entry
         if (lane == 0) stk[sp] = make_int4(d.x, d.z, (int)b0, (int)b1);
         ++sp;
+      } else if (MODE == kWalkDefer && (d.w & kDeferBit)) {  // subtree not here yet: defer
+        if (lane == 0) {
+          const unsigned slot = atomicAdd(dfr.count, 1u);
+          if (slot < (unsigned)dfr.cap) dfr.out[slot] = make_int4((int)warp, c, (int)b0, (int)b1);
+        }
       } else if (BUCKET) {  // bucket rule: pp over its bodies
         for (int j = d.x; j < d.x + cnt; ++j) {
           const float4 bb = bodies[j];
@@ -480,19 +505,35 @@ __global__ void __launch_bounds__(kWalkBlock, BH_WALK_MINB) k_walk(
     __syncwarp();
     e = stk[--sp];
   }
-  if (v0) {
-    float *o = acc + s0 * astride;
-    o[0] = AX.x; o[1] = AY.x; o[2] = AZ.x;
-    const int w = pp0 + 2 * pc0;  // WORK_PP, WORK_PC (octree.py:23-25)
-    if (work64) work64[s0] = w;
-    if (work32) work32[s0] = w;
-  }
-  if (v1) {
-    float *o = acc + s1 * astride;
-    o[0] = AX.y; o[1] = AY.y; o[2] = AZ.y;
-    const int w = pp1 + 2 * pc1;
-    if (work64) work64[s1] = w;
-    if (work32) work32[s1] = w;
+  if (MODE == kWalkResume) {  // add to pass A's results (several entries may share a target)
+    const bool u0 = v0 && ((unsigned)entry.z >> lane & 1u), u1 = v1 && ((unsigned)entry.w >> lane & 1u);
+    if (u0) {
+      float *o = acc + s0 * astride;
+      atomicAdd(o, AX.x); atomicAdd(o + 1, AY.x); atomicAdd(o + 2, AZ.x);
+      if (work32) atomicAdd(work32 + s0, pp0 + 2 * pc0);
+      if (work64) atomicAdd((unsigned long long *)(work64 + s0), (unsigned long long)(pp0 + 2 * pc0));
+    }
+    if (u1) {
+      float *o = acc + s1 * astride;
+      atomicAdd(o, AX.y); atomicAdd(o + 1, AY.y); atomicAdd(o + 2, AZ.y);
+      if (work32) atomicAdd(work32 + s1, pp1 + 2 * pc1);
+      if (work64) atomicAdd((unsigned long long *)(work64 + s1), (unsigned long long)(pp1 + 2 * pc1));
+    }
+  } else {
+    if (v0) {
+      float *o = acc + s0 * astride;
+      o[0] = AX.x; o[1] = AY.x; o[2] = AZ.x;
+      const int w = pp0 + 2 * pc0;  // WORK_PP, WORK_PC (octree.py:23-25)
+      if (work64) work64[s0] = w;
+      if (work32) work32[s0] = w;
+    }
+    if (v1) {
+      float *o = acc + s1 * astride;
+      o[0] = AX.y; o[1] = AY.y; o[2] = AZ.y;
+      const int w = pp1 + 2 * pc1;
+      if (work64) work64[s1] = w;
+      if (work32) work32[s1] = w;
+    }
   }
   const unsigned spp = __reduce_add_sync(0xffffffffu, (unsigned)(pp0 + pp1));
   const unsigned spc = __reduce_add_sync(0xffffffffu, (unsigned)(pc0 + pc1));
@@ -502,17 +543,37 @@ __global__ void __launch_bounds__(kWalkBlock, BH_WALK_MINB) k_walk(
   }
 }
 
+template <int MODE>
+static void launch_walk_mode(const WalkNode *T, const float4 *bodies, const float *targets, int tstride,
+                             const uint32_t *tperm, int nt, float e2, int leaf, float *acc, int astride,
+                             int64_t *work64, int *work32, DeviceFlags *f, const DeferArgs &dfr, cudaStream_t s) {
+  const int64_t warps = MODE == kWalkResume ? (int64_t)dfr.nin : ((int64_t)nt + 63) / 64;
+  if (warps <= 0) return;
+  const int g = grid_for(warps * 32, kWalkBlock);
+  if (leaf > 1)
+    k_walk<true, MODE><<<g, kWalkBlock, 0, s>>>(T, bodies, targets, tstride, tperm, nt, e2, leaf, acc, astride,
+                                                work64, work32, f, dfr);
+  else
+    k_walk<false, MODE><<<g, kWalkBlock, 0, s>>>(T, bodies, targets, tstride, tperm, nt, e2, leaf, acc, astride,
+                                                 work64, work32, f, dfr);
+}
+
 void launch_walk_f32(const WalkNode *T, const float4 *bodies, const float *targets, int tstride,
                      const uint32_t *tperm, int nt, float e2, int leaf, float *acc, int astride,
                      int64_t *work64, int *work32, DeviceFlags *f, cudaStream_t s) {
   if (nt <= 0) return;
-  const int64_t threads = ((int64_t)nt + 63) / 64 * 32;
-  if (leaf > 1)
-    k_walk<true><<<grid_for(threads, kWalkBlock), kWalkBlock, 0, s>>>(
-        T, bodies, targets, tstride, tperm, nt, e2, leaf, acc, astride, work64, work32, f);
+  launch_walk_mode<kWalkFull>(T, bodies, targets, tstride, tperm, nt, e2, leaf, acc, astride, work64, work32, f,
+                              DeferArgs{}, s);
+}
+
+void launch_walk_defer_f32(const WalkNode *T, const float4 *bodies, const float *targets, int nt, float e2,
+                           int leaf, float *acc, int *work32, DeviceFlags *f, const DeferArgs &dfr,
+                           bool resume, cudaStream_t s) {
+  if (nt <= 0) return;
+  if (resume)
+    launch_walk_mode<kWalkResume>(T, bodies, targets, 4, nullptr, nt, e2, leaf, acc, 4, nullptr, work32, f, dfr, s);
   else
-    k_walk<false><<<grid_for(threads, kWalkBlock), kWalkBlock, 0, s>>>(
-        T, bodies, targets, tstride, tperm, nt, e2, leaf, acc, astride, work64, work32, f);
+    launch_walk_mode<kWalkDefer>(T, bodies, targets, 4, nullptr, nt, e2, leaf, acc, 4, nullptr, work32, f, dfr, s);
 }
 
 }  // namespace bh

@@ -286,6 +286,7 @@ class DistributedSim:
 # fp32 summation order.  fp32 only.
 
 _REC_INTS = 16  # a 64-byte WalkNode as int32 columns: a(0-3) b(4-7) c(8-11) d(12-15)
+_DEFER_BIT = 1 << 30  # in d.w (level): pass A of the overlapped walk defers the record
 
 
 def _lcp(a: int, b: int) -> int:
@@ -369,6 +370,9 @@ class DistributedBuildSim:
         self.R = 1.0
         self.last_zones = None
         self.let_pad = 0.0  # widens the LET target boxes (inf: send whole subtrees)
+        self.overlap = True  # walk the local part while the LETs travel
+        self._side = None
+        self._pack_done = None
         self.trace = {} if os.environ.get("BH_DIST_TRACE") else None  # host wall per section
         self._tlast = None
 
@@ -427,6 +431,28 @@ class DistributedBuildSim:
                     parts.append(bufs[q][start:start + cq[me]])
                 out = torch.cat(parts) if parts else t[:0]
             res.append((out, recv))
+        return res
+
+    def _exchange_async(self, items):
+        """_alltoall_many on a side stream that waits only for the work queued
+        so far (the LET packing), so the collective overlaps the pass-A walk
+        already queued on the compute stream; the compute stream then waits for
+        it.  Host-mediated comms (ThreadComm) simply run it."""
+        if not isinstance(self.comm, TorchComm) or not torch.cuda.is_available():
+            return self._alltoall_many(items)
+        main = torch.cuda.current_stream(self.eng.device)
+        if self._side is None:
+            self._side = torch.cuda.Stream(self.eng.device)
+        ready = self._pack_done
+        if ready is None:
+            ready = torch.cuda.Event()
+            ready.record(main)
+        with torch.cuda.stream(self._side):
+            self._side.wait_event(ready)
+            res = self._alltoall_many(items)
+        main.wait_stream(self._side)
+        for out, _ in res:
+            out.record_stream(main)
         return res
 
     def _alltoall_v(self, t: torch.Tensor, send_counts: list, return_counts: bool = False):
@@ -635,20 +661,64 @@ class DistributedBuildSim:
             eng.sim_let_pack(q, send_rec[ro:], send_bod[bo:], bmap)
             send_map[mo:mo + nb] = bmap[perm]
             ro, bo, mo = ro + rc[q], bo + bc[q], mo + nb
+        self._pack_done = None
+        if isinstance(comm, TorchComm) and torch.cuda.is_available():
+            self._pack_done = torch.cuda.Event()  # the LET exchange waits for this, not for pass A
+            self._pack_done.record()
         self._t("let_pack")
-        (let_rec, rcnt), (let_bod, bcnt), (let_map, mcnt) = self._alltoall_many(
-            [(send_rec, rc), (send_bod, bc), (send_map, mcounts)])
-        self._t("let_exchange")
         nbb = sum(b.shape[0] for b in bb_all)
-        self.tree = self._assemble(br_all, recs, n, nbb, let_rec, rcnt, bcnt, let_map, mcnt)
-        self.let_stats = dict(records=int(let_rec.shape[0]), bodies=int(let_bod.shape[0]),
-                              sent_records=sum(rc), sent_bodies=sum(bc), own_records=int(recs.shape[0]))
-        self._t("assemble")
-        gbodies = torch.cat([bodies] + list(bb_all) + [let_bod])
         acc = torch.zeros((n, 4), dtype=torch.float32, device=dev)
         work = torch.zeros(n, dtype=torch.int32, device=dev)
+        items = [(send_rec, rc), (send_bod, bc), (send_map, mcounts)]
+        gA = torch.cat([bodies] + list(bb_all))
+        treeA, deferred = (self._assemble(br_all, recs, n, nbb, defer=True) if (self.overlap and size > 1)
+                           else (None, None))
+        if treeA is not None and n:
+            # pass A walks the local part while the LETs travel
+            nwarp = (n + 63) // 64
+            cap = nwarp * min(len(deferred), 8) + 1024
+            dbuf = torch.empty((cap, 4), dtype=torch.int32, device=dev)
+            dcnt = torch.zeros(1, dtype=torch.int32, device=dev)
+            eng.walk_records_defer(treeA, gA, bodies, p.eps, L, acc, work, dbuf, dcnt)
+            self._t("walk_local")
+            (let_rec, rcnt), (let_bod, bcnt), (let_map, mcnt) = self._exchange_async(items)
+            self._t("let_exchange")
+            letoff = np.cumsum([0] + list(rcnt))[:-1] + treeA.shape[0]
+            lbodoff = np.cumsum([0] + list(bcnt))[:-1] + n + nbb
+            self.tree = torch.cat([treeA] + self._let_parts(let_rec, rcnt, letoff, lbodoff)).contiguous()
+            gbodies = torch.cat([gA, let_bod])
+            maps_h, off = let_map.cpu().numpy(), 0
+            maps = {}
+            for q in range(size):
+                maps[q] = maps_h[off:off + mcnt[q]]
+                off += mcnt[q]
+            fcnc = np.zeros((treeA.shape[0], 2), dtype=np.int32)
+            for row, q, k, nch in deferred:
+                fc = int(maps[q][k, 0])
+                if fc >= 0:
+                    fcnc[row] = (fc + letoff[q], nch)
+            k = int(dcnt.item())
+            self.let_stats = dict(records=int(let_rec.shape[0]), bodies=int(let_bod.shape[0]),
+                                  sent_records=sum(rc), sent_bodies=sum(bc), own_records=int(recs.shape[0]),
+                                  deferred=k, overlap=k <= cap)
+            if k <= cap:
+                eng.walk_records_resume(self.tree, gbodies, bodies, p.eps, L, acc, work, dbuf[:k],
+                                        torch.as_tensor(fcnc, device=dev))
+            else:  # deferral list overflowed: the one-pass walk over the full tree
+                self.tree = self._assemble(br_all, recs, n, nbb, let_rec, rcnt, bcnt, let_map, mcnt)
+                eng.walk_records(self.tree, gbodies, bodies, p.eps, L, acc, work)
+        else:
+            (let_rec, rcnt), (let_bod, bcnt), (let_map, mcnt) = self._alltoall_many(items)
+            self._t("let_exchange")
+            self.tree = self._assemble(br_all, recs, n, nbb, let_rec, rcnt, bcnt, let_map, mcnt)
+            self.let_stats = dict(records=int(let_rec.shape[0]), bodies=int(let_bod.shape[0]),
+                                  sent_records=sum(rc), sent_bodies=sum(bc), own_records=int(recs.shape[0]),
+                                  deferred=0, overlap=False)
+            self._t("assemble")
+            gbodies = torch.cat([gA, let_bod])
+            if n:
+                eng.walk_records(self.tree, gbodies, bodies, p.eps, L, acc, work)
         if n:
-            eng.walk_records(self.tree, gbodies, bodies, p.eps, L, acc, work)
             eng.sim_import(_lib.BH_SIM_ACC, 0, n, acc)
             if record_work:
                 eng.sim_import(_lib.BH_SIM_WORK, 0, n, work)
@@ -682,7 +752,8 @@ class DistributedBuildSim:
         box[:, 3:] += self.let_pad
         return box
 
-    def _assemble(self, br_all, recs, n, nbb, let_rec, rcnt, bcnt, let_map, mcnt) -> torch.Tensor:
+    def _assemble(self, br_all, recs, n, nbb, let_rec=None, rcnt=None, bcnt=None, let_map=None, mcnt=None,
+                  defer=False):
         """This rank's walk tree = [top region | own records | LET from each peer];
         its body list = [own bodies | bucket-sized branch bodies | LET bodies].
 
@@ -701,11 +772,13 @@ class DistributedBuildSim:
         rows = {}
         bbpos = n
         maps = {}
-        off = 0
-        let_map_h = let_map.cpu().numpy()
-        for q in range(size):
-            maps[q] = let_map_h[off:off + mcnt[q]]
-            off += mcnt[q]
+        if not defer:
+            off = 0
+            let_map_h = let_map.cpu().numpy()
+            for q in range(size):
+                maps[q] = let_map_h[off:off + mcnt[q]]
+                off += mcnt[q]
+        deferred = []  # defer mode: (region row, owner rank, branch index, nchild)
         host = torch.cat(br_all).cpu().numpy() if br_all else np.zeros((0, _BR_INTS), np.int32)
         off = 0
         for r in range(size):
@@ -776,8 +849,9 @@ class DistributedBuildSim:
                         queue.append((c, len(entries) - 1))
                 entries[at] = ("top", k, first, len(ch))
         ntop = len(entries)
-        letoff = np.cumsum([0] + list(rcnt))[:-1] + ntop + nW
-        lbodoff = np.cumsum([0] + list(bcnt))[:-1] + n + nbb
+        if not defer:
+            letoff = np.cumsum([0] + list(rcnt))[:-1] + ntop + nW
+            lbodoff = np.cumsum([0] + list(bcnt))[:-1] + n + nbb
         region = []
         for e in entries:
             if e[0] == "top":
@@ -791,6 +865,10 @@ class DistributedBuildSim:
                 if q == me:  # own subtree: first child in the own records, bodies at 0
                     if rec[14] > 0:
                         rec[12] += ntop
+                elif rec[14] > 0 and defer:  # subtree in flight: pass A defers it (f4)
+                    deferred.append((len(region), q, b["k"], int(rec[14])))
+                    rec[12], rec[14] = -1, 0
+                    rec[15] |= _DEFER_BIT
                 elif rec[14] > 0:
                     fc = int(maps[q][b["k"], 0])
                     if fc >= 0:
@@ -799,6 +877,8 @@ class DistributedBuildSim:
                         rec[12], rec[14] = -1, 0
                 elif b["count"] <= L:
                     rec[12] = b["bb"]
+                elif defer:  # a duplicate-key cell resolved over LET bodies: no overlap this step
+                    return None, None
                 else:
                     fb = int(maps[q][b["k"], 1])
                     rec[12] = fb + lbodoff[q] if fb >= 0 else -1
@@ -807,18 +887,28 @@ class DistributedBuildSim:
         x = recs.clone()
         x[:, 12] = torch.where(x[:, 14] > 0, x[:, 12] + ntop, x[:, 12])
         parts.append(x)
+        if defer:
+            return torch.cat(parts).contiguous(), deferred
+        parts += self._let_parts(let_rec, rcnt, letoff, lbodoff)
+        return torch.cat(parts).contiguous()
+
+    @staticmethod
+    def _let_parts(let_rec, rcnt, letoff, lbodoff) -> list:
+        """The received LETs with child links and bucket body ranges moved to
+        their place in the assembled tree / body list."""
+        parts = []
         o = 0
-        for q in range(size):
-            if rcnt[q] == 0:
+        for q, c in enumerate(rcnt):
+            if c == 0:
                 continue
-            y = let_rec[o:o + rcnt[q]].clone()
-            o += rcnt[q]
+            y = let_rec[o:o + c].clone()
+            o += c
             internal = y[:, 14] > 0
             withbod = (~internal) & (y[:, 13] > 1) & (y[:, 12] >= 0)
             y[:, 12] = torch.where(internal, y[:, 12] + int(letoff[q]),
                                    torch.where(withbod, y[:, 12] + int(lbodoff[q]), y[:, 12]))
             parts.append(y)
-        return torch.cat(parts).contiguous()
+        return parts
 
     def upload(self, pos, vel, acc, work, gid) -> None:
         """Replace this rank's state (e.g. from host buffers); ownership is

@@ -322,6 +322,21 @@ class Engine:
                                           _ptr(targets), targets.shape[0], float(eps), int(leaf_size),
                                           _ptr(acc), _ptr(work), self.stream))
 
+    def walk_records_defer(self, records, bodies, targets, eps, leaf_size, acc, work, defer, count) -> None:
+        """Pass A of the LET overlap: flagged remote branch records are deferred
+        into ``defer`` (int32 [cap, 4]); ``count`` (int32 [1], device) gets the entries."""
+        check(self._L.bh_walk_records_defer_f32(self._h, _ptr(records), records.shape[0], _ptr(bodies),
+                                                _ptr(targets), targets.shape[0], float(eps), int(leaf_size),
+                                                _ptr(acc), _ptr(work), _ptr(defer), _ptr(count),
+                                                defer.shape[0], self.stream))
+
+    def walk_records_resume(self, records, bodies, targets, eps, leaf_size, acc, work, entries, fcnc) -> None:
+        """Pass B: resume ``entries`` (int32 [k, 4]) over the completed tree; fcnc int32 [nrec, 2]."""
+        check(self._L.bh_walk_records_resume_f32(self._h, _ptr(records), records.shape[0], _ptr(bodies),
+                                                 _ptr(targets), targets.shape[0], float(eps), int(leaf_size),
+                                                 _ptr(acc), _ptr(work), _ptr(entries), entries.shape[0],
+                                                 _ptr(fcnc), self.stream))
+
     def sim_step_host(self, pos4: torch.Tensor, vel3: torch.Tensor, acc3: torch.Tensor, dt: float,
                       theta: float, eps: float, leaf_size: int, steps: int = 1) -> None:
         """KDK steps on host (CPU, ideally pinned) float32 arrays pos4 (n,4), vel3/acc3

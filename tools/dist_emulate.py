@@ -67,6 +67,7 @@ for R in ranks_list:
             e = Engine("fp32", 0)
             sl = slice(cuts[r], cuts[r + 1])
             s = DistributedBuildSim(e, comms[r], StepParams(theta, eps, L, dt))
+            s.overlap = False  # replay the one-pass walk over the full assembled tree
             s.load(e.bodies_tensor(b.position[sl], b.mass[sl]), e.vec_tensor(b.velocity[sl]),
                    gid=torch.arange(int(cuts[r]), int(cuts[r + 1]), device="cuda"))
             s.bootstrap()
