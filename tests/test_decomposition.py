@@ -124,3 +124,74 @@ def test_stage2_collectives_gloo():
     for rank, got, recv in res:
         assert got == [[0, 1, 2], [100, 101, 102, 103, 104]]
         assert recv == [[0, rank]] * (rank + 1) + [[1, rank]] * (rank + 1)
+
+
+def test_top_tree_combine_matches_reference_moments():
+    """The distributed step's exact fp64 top-tree recombination (_combine,
+    hashed.py:719-786 / flattree.py:201-252) reproduces every internal cell of
+    the oracle tree bit for bit from its children, in slot order."""
+    from oracle import oracle as orc
+    from paper_2203_08966_b200.decomposition import _combine
+    from paper_2203_08966_b200.initcond import make_rng, plummer_cluster
+
+    b = plummer_cluster(3000, make_rng(11))
+    pos = np.asarray(b.position, dtype=np.float64)
+    m = np.asarray(b.mass, dtype=np.float64)
+    R = orc.bounds(pos)
+    o = orc.sort_order(orc.morton_keys(pos, R))
+    t = orc.build_tree(m[o], pos[o], R)
+    ch = np.asarray(t.children).reshape(len(t), -1)
+    checked = 0
+    for c in range(len(t)):
+        kids = [int(k) for k in ch[c] if k >= 0]
+        if not kids:
+            continue
+        rows = [(float(t.mass[k]), tuple(float(x) for x in t.com[k]), tuple(float(x) for x in t.quad[k]))
+                for k in kids]
+        mass, com, quad = _combine(rows)
+        assert mass == t.mass[c]
+        assert com == tuple(float(x) for x in t.com[c])
+        assert quad == tuple(float(x) for x in t.quad[c])
+        checked += 1
+    assert checked > 500
+
+
+def test_branch_rows_pack_roundtrip():
+    from paper_2203_08966_b200.decomposition import _BR_INTS, _REC_INTS, _pack_branches, _unpack_branches
+
+    rng = np.random.default_rng(3)
+    nb = 37
+    br = dict(key=torch.from_numpy(rng.integers(1, 1 << 62, nb, dtype=np.int64)),
+              level=torch.from_numpy(rng.integers(0, 22, nb).astype(np.int32)),
+              count=torch.from_numpy(rng.integers(1, 1 << 40, nb, dtype=np.int64)),
+              mom=torch.from_numpy(rng.normal(size=(nb, 10))),
+              rec=torch.from_numpy(rng.integers(0, 1 << 30, nb).astype(np.int32)),
+              lo=torch.from_numpy(rng.integers(0, 1 << 30, nb).astype(np.int32)),
+              recs=torch.from_numpy(rng.integers(-(1 << 31), 1 << 31, (nb, _REC_INTS)).astype(np.int32)))
+    rows = _pack_branches(br)
+    assert rows.shape == (nb, _BR_INTS) and rows.dtype == torch.int32
+    key, level, count, mom, rec, lo, recs = _unpack_branches(rows.numpy())
+    np.testing.assert_array_equal(key, br["key"].numpy())
+    np.testing.assert_array_equal(level, br["level"].numpy())
+    np.testing.assert_array_equal(count, br["count"].numpy())
+    np.testing.assert_array_equal(mom, br["mom"].numpy())
+    np.testing.assert_array_equal(rec, br["rec"].numpy())
+    np.testing.assert_array_equal(lo, br["lo"].numpy())
+    np.testing.assert_array_equal(recs, br["recs"].numpy())
+
+
+def test_lcp_matches_key_prefix_levels():
+    """_lcp: the deepest level at which two Morton keys share a cell
+    (hashed.py:376-388): 21 - ceil(bitlen(a ^ b) / 3)."""
+    from paper_2203_08966_b200.decomposition import _lcp
+
+    rng = np.random.default_rng(4)
+    for _ in range(2000):
+        a, b = (int(x) for x in rng.integers(0, 1 << 63, 2, dtype=np.uint64))
+        shared = 0
+        for lvl in range(1, 22):
+            if (a >> (3 * (21 - lvl))) == (b >> (3 * (21 - lvl))):
+                shared = lvl
+            else:
+                break
+        assert _lcp(a, b) == shared, (a, b)
