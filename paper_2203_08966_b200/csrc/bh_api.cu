@@ -78,6 +78,11 @@ struct bh_handle {
   Buf let_present, let_expand, let_bodies, let_isbranch, let_rflag, let_bcount, let_rpos,
       let_bpos, let_scan_tmp, let_brec, let_tail, let_boxkey, let_lvl, let_list;
   uint32_t *hlet = nullptr;  // pinned: LET sizes per receiver
+  // work of the last walk is in work_sorted; its scatter to the caller's order
+  // (work_orig) is deferred until someone reads it (a random 4-byte scatter:
+  // ~3.8 ms per step at 1e8 bodies), and dropped inside a multi-step call
+  bool work_dirty = false;
+  bool drop_work = false;
   // bh_sim_step_host: staging and the side stream for the early position copy
   Buf hs_a, hs_b, hs_pos;
   cudaStream_t side = nullptr;
@@ -429,8 +434,10 @@ __global__ void k_fill_int(int *v, int64_t n, int x) {
 // phases so a multi-GPU driver can exchange between them:
 //   prepare: bounds -> keys -> stable sort -> permute bodies -> build -> walk tree
 //   walk   : targets [begin, end) of the Morton-sorted bodies
+int flush_work(bh_handle *h, cudaStream_t s);
 int sim_prepare(bh_handle *h, double theta, double eps, int leaf, bool bounds_ready,
                 cudaStream_t s) {
+  BH_TRY(flush_work(h, s));
   const int64_t n = h->sim_n;
   const bool f32 = h->precision == BH_FP32;
   if (!(theta >= 0.0) || !(eps >= 0.0)) return fail(BH_BAD_ARG, "theta and eps must be >= 0");
@@ -487,6 +494,7 @@ int sim_prepare(bh_handle *h, double theta, double eps, int leaf, bool bounds_re
 
 // keys (with the R already in dR), stable sort, permutation -- no build
 int sim_sort(bh_handle *h, cudaStream_t s) {
+  BH_TRY(flush_work(h, s));
   const int64_t n = h->sim_n;
   const bool f32 = h->precision == BH_FP32;
   BH_TRY(ensure_sort(h, n));
@@ -559,6 +567,7 @@ int sim_walk(bh_handle *h, double theta, double eps, int leaf, int64_t begin, in
 
 int sim_scatter_work(bh_handle *h, cudaStream_t s) {
   const int64_t n = h->sim_n;
+  h->work_dirty = false;
   if (n <= 0) return BH_OK;
   k_scatter_work<<<grid_for(n, 256), 256, 0, s>>>(h->work_sorted.as<int>(), h->id.as<uint32_t>(), n,
                                                   h->work_orig.as<int>());
@@ -571,8 +580,18 @@ int sim_forces_impl(bh_handle *h, double theta, double eps, int leaf, int record
                     bool bounds_ready, cudaStream_t s) {
   BH_TRY(sim_prepare(h, theta, eps, leaf, bounds_ready, s));
   BH_TRY(sim_walk(h, theta, eps, leaf, 0, h->sim_n, record_work, s));
-  if (record_work) BH_TRY(sim_scatter_work(h, s));
+  if (record_work) h->work_dirty = true;  // scattered when read (flush_work)
   return BH_OK;
+}
+
+// the pending work scatter must run before the permutation changes or a read
+int flush_work(bh_handle *h, cudaStream_t s) {
+  if (!h->work_dirty) return BH_OK;
+  if (h->drop_work) {  // a multi-step call: the next walk records work again
+    h->work_dirty = false;
+    return BH_OK;
+  }
+  return sim_scatter_work(h, s);
 }
 
 int sim_begin_step(bh_handle *h, double dt, cudaStream_t s) {
@@ -913,6 +932,7 @@ int bh_sim_load(bh_handle *h, const void *d_pos, const void *d_vel, const double
   BH_CUDA(h->work_sorted.ensure(sizeof(int64_t) * (n + 1)));
   BH_CUDA(h->work_orig.ensure(sizeof(int) * (n + 1)));
   h->sim_n = n;
+  h->work_dirty = false;
   if (n == 0) return BH_OK;
   if (f32) {
     BH_CUDA(cudaMemcpyAsync(h->pos.p, d_pos, e4 * n, cudaMemcpyDeviceToDevice, s));
@@ -950,6 +970,8 @@ int bh_sim_forces(bh_handle *h, double theta, double eps, int leaf_size, int rec
 }
 
 static int sim_snapshot(bh_handle *h, bool restore, cudaStream_t s) {
+  if (!restore) BH_TRY(flush_work(h, s));
+  else h->work_dirty = false;  // work_orig comes back from the snapshot
   const int64_t n = h->sim_n;
   const size_t e4 = h->precision == BH_FP32 ? sizeof(float4) : sizeof(double4);
   struct { Buf *live, *bk; size_t bytes; } items[] = {
@@ -970,6 +992,11 @@ int bh_sim_step(bh_handle *h, double dt, double theta, double eps, int leaf_size
   if (h->sim_n == 0 || steps == 0) return BH_OK;
   cudaStream_t s = S(stream);
   const bool f32 = h->precision == BH_FP32;
+  struct DropWork {  // inside the call every walk records work: only the last one is kept
+    bh_handle *h;
+    explicit DropWork(bh_handle *hh) : h(hh) { h->drop_work = true; }
+    ~DropWork() { h->drop_work = false; }
+  } drop(h);
   for (int attempt = 0; attempt < 3; ++attempt) {
     if (f32) BH_TRY(sim_snapshot(h, false, s));
     for (int k = 0; k < steps; ++k) {
@@ -1036,6 +1063,7 @@ int bh_sim_step_host(bh_handle *h, float *pos4, float *vel3, float *acc3, int64_
   k_fill_int<<<g, 256, 0, s>>>(h->work_orig.as<int>(), n, 1);  // simulation.py:482
   h->launches += 4;
   bool pos_sent = false;
+  h->work_dirty = false;  // freshly loaded: work_orig = 1
   for (int attempt = 0; attempt < 3; ++attempt) {
     BH_TRY(sim_snapshot(h, false, s));
     for (int k = 0; k < steps; ++k) {
@@ -1550,6 +1578,7 @@ int bh_sim_export(bh_handle *h, int what, int64_t begin, int64_t end, void *dst,
                               cudaMemcpyDeviceToDevice, s));
       break;
     case BH_SIM_PREV_WORK:
+      BH_TRY(flush_work(h, s));
       k_gather_work<<<grid_for(k, 256), 256, 0, s>>>(h->work_orig.as<int>(), h->id.as<uint32_t>(),
                                                      begin, end, static_cast<int *>(dst));
       BH_LAUNCHED();
@@ -1609,7 +1638,10 @@ int bh_sim_store(bh_handle *h, void *d_pos, void *d_vel, void *d_acc, int64_t *d
     if (d_vel) k_store3<<<g, 256, 0, s>>>(h->vel.as<double4>(), id, n, (double *)d_vel);
     if (d_acc) k_store3<<<g, 256, 0, s>>>(h->acc.as<double4>(), id, n, (double *)d_acc);
   }
-  if (d_work) k_work64<<<g, 256, 0, s>>>(h->work_orig.as<int>(), n, d_work);
+  if (d_work) {
+    BH_TRY(flush_work(h, s));
+    k_work64<<<g, 256, 0, s>>>(h->work_orig.as<int>(), n, d_work);
+  }
   BH_LAUNCHED();
   return BH_OK;
 }
