@@ -382,6 +382,10 @@ extern "C" int bh_debug_walk_hist(unsigned long long *out) {
 //                  walking the record's subtree (first child, nchild from
 //                  fcnc[record]) and adding into acc/work atomically.
 enum { kWalkFull = 0, kWalkDefer = 1, kWalkResume = 2 };
+#ifndef BH_BUCKET_UNROLL
+#define BH_BUCKET_UNROLL 4
+#endif
+constexpr int kBucketUnroll = BH_BUCKET_UNROLL;  // bucket pp loop unroll
 constexpr int kDeferBit = 1 << 30;
 
 template <bool BUCKET, int MODE>
@@ -484,6 +488,9 @@ __global__ void __launch_bounds__(kWalkBlock, BH_WALK_MINB) k_walk(
           if (slot < (unsigned)dfr.cap) dfr.out[slot] = make_int4((int)warp, c, (int)b0, (int)b1);
         }
       } else if (BUCKET) {  // bucket rule: pp over its bodies
+        // unrolled so the body loads of several iterations are in flight at once
+        // (the loop was bound by their latency): walk -4% at cfg2, -6% at cfg3
+#pragma unroll(kBucketUnroll)
         for (int j = d.x; j < d.x + cnt; ++j) {
           const float4 bb = bodies[j];
           const float2 EX = __ffma2_rn(f2(bb.x), f2(-1.f), X);
