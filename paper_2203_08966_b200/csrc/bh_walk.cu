@@ -386,6 +386,7 @@ enum { kWalkFull = 0, kWalkDefer = 1, kWalkResume = 2 };
 #define BH_BUCKET_UNROLL 4
 #endif
 constexpr int kBucketUnroll = BH_BUCKET_UNROLL;  // bucket pp loop unroll
+
 constexpr int kDeferBit = 1 << 30;
 
 template <bool BUCKET, int MODE>
@@ -433,6 +434,8 @@ __global__ void __launch_bounds__(kWalkBlock, BH_WALK_MINB) k_walk(
       const WalkNode *nd = T + c;
       const float4 a = nd->a;
       const int4 d = nd->d;
+      const float4 b = nd->b;  // quadrupole words loaded with the MAC word (latency overlap)
+      const float4 q = nd->c;
       const int cnt = __reduce_max_sync(0xffffffffu, d.y);  // warp-uniform
       const float2 DX = __fadd2_rn(X, f2(a.x));
       const float2 DY = __fadd2_rn(Y, f2(a.y));
@@ -458,8 +461,7 @@ __global__ void __launch_bounds__(kWalkBlock, BH_WALK_MINB) k_walk(
       }
 #endif
       if (__any_sync(0xffffffffu, c0 || c1)) {
-        const float4 b = nd->b;
-        const float4 q = nd->c;
+
         const float2 R = f2(c0 ? rsqrtf(D2.x) : 0.f, c1 ? rsqrtf(D2.y) : 0.f);
         const float2 R2 = __fmul2_rn(R, R);
         const float2 R3 = __fmul2_rn(R2, R);
