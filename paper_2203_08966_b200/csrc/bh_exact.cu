@@ -302,10 +302,7 @@ void launch_emit(const TreeView &t, const float4 *bod32, const double4 *bod64,
   k_emit<<<grid_for(t.n, 128), 128, 0, s>>>(t, bod32, bod64);
 }
 
-// flattree.py:201-252 _moments_kernel for one cell, children in slot order
-// (pre-order: first child c+1, next sibling skip[child]).  Same expression
-// order as the reference; children written by other threads of this launch are
-// read through L2 (ld.global.cg) after the acquire fence.
+// a sorted body as (x, y, z, m) in double
 __device__ __forceinline__ double4 body64(const TreeView &t, int64_t j) {
   if (t.bod64) return t.bod64[j];
   const float4 v = t.bod32[j];
@@ -355,73 +352,12 @@ __device__ void dup_cell_moments(const TreeView &t, int p) {
   q2o[2] = make_double2(qyz, qzz);
 }
 
-__device__ void cell_moments(const TreeView &t, int p) {
-  // all child indices at once (slot order), then independent child loads
-  const int4 *row = reinterpret_cast<const int4 *>(t.child8 + 8 * (int64_t)p);
-  const int4 r0 = row[0], r1 = row[1];
-  const int ch[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
-  if ((r0.x & r0.y & r0.z & r0.w & r1.x & r1.y & r1.z & r1.w) == -1) {
-    dup_cell_moments(t, p);  // a duplicate-key cell: its bodies are its children
-    return;
-  }
-  double4 cc[8];
-#pragma unroll
-  for (int s = 0; s < 8; ++s) cc[s] = ch[s] >= 0 ? t.cm64[ch[s]] : make_double4(0.0, 0.0, 0.0, 0.0);
-  double total = 0.0, cx = 0.0, cy = 0.0, cz = 0.0;
-#pragma unroll
-  for (int s = 0; s < 8; ++s) {
-    const double m = cc[s].w;
-    if (ch[s] < 0 || m == 0.0) continue;
-    total += m;
-    cx += m * cc[s].x;
-    cy += m * cc[s].y;
-    cz += m * cc[s].z;
-  }
-  double *qo = t.q64 + 6 * (int64_t)p;
-  if (total == 0.0) {
-    t.cm64[p] = make_double4(0.0, 0.0, 0.0, 0.0);
-    for (int k = 0; k < 6; ++k) qo[k] = 0.0;
-    return;
-  }
-  cx /= total;
-  cy /= total;
-  cz /= total;
-  double qxx = 0.0, qxy = 0.0, qxz = 0.0, qyy = 0.0, qyz = 0.0, qzz = 0.0;
-#pragma unroll
-  for (int s = 0; s < 8; ++s) {
-    const int c = ch[s];
-    const double m = cc[s].w;
-    if (c < 0 || m == 0.0) continue;
-    double q0 = 0.0, q1 = 0.0, q2 = 0.0, q3 = 0.0, q4 = 0.0, q5 = 0.0;
-    if (t.link[c].y > 1) {  // leaves keep quad = 0 (flattree.py:207-208)
-      const double2 *qc = reinterpret_cast<const double2 *>(t.q64 + 6 * (int64_t)c);
-      double2 a = qc[0], b = qc[1], d = qc[2];
-      q0 = a.x; q1 = a.y; q2 = b.x; q3 = b.y; q4 = d.x; q5 = d.y;
-    }
-    double dx = cc[s].x - cx;
-    double dy = cc[s].y - cy;
-    double dz = cc[s].z - cz;
-    double d2 = dx * dx + dy * dy + dz * dz;
-    qxx += q0 + m * (3.0 * (dx * dx) - d2);
-    qxy += q1 + m * (3.0 * (dx * dy) - 0.0);
-    qxz += q2 + m * (3.0 * (dx * dz) - 0.0);
-    qyy += q3 + m * (3.0 * (dy * dy) - d2);
-    qyz += q4 + m * (3.0 * (dy * dz) - 0.0);
-    qzz += q5 + m * (3.0 * (dz * dz) - d2);
-  }
-  t.cm64[p] = make_double4(cx, cy, cz, total);
-  double2 *q2o = reinterpret_cast<double2 *>(qo);
-  q2o[0] = make_double2(qxx, qxy);
-  q2o[1] = make_double2(qxz, qyy);
-  q2o[2] = make_double2(qyz, qzz);
-}
-
-// The same moments with one lane per child slot (8 lanes per cell, 4 cells per
-// warp): the child loads of a cell go out in parallel from 8 lanes, and the
-// slot-ordered sums -- the reference's exact expression order -- are formed
-// from a per-warp shared-memory exchange.  Each lane forms its child's
-// products (m*x, and q_c + m*(3 dx dx - d2)); the sums are sequential in slot
-// order, skipping absent and massless children, as in cell_moments.
+// flattree.py:201-252 _moments_kernel for one cell, with one lane per child
+// slot (8 lanes per cell, 4 cells per warp): the child loads of a cell go out
+// in parallel from 8 lanes, and the slot-ordered sums -- the reference's exact
+// expression order -- are formed from a per-warp shared-memory exchange.  Each
+// lane forms its child's products (m*x, and q_c + m*(3 dx dx - d2)); the sums
+// are sequential in slot order, skipping absent and massless children.
 // Every lane of the warp must call it (p < 0: no cell).  xs: the warp's [32][11].
 __device__ void cell_moments8(const TreeView &t, int p, double (*xs)[11]) {
   const int lane = threadIdx.x & 31, s = lane & 7, g0 = lane & ~7;
@@ -501,40 +437,6 @@ __device__ void cell_moments8(const TreeView &t, int p, double (*xs)[11]) {
   __syncwarp();
 }
 
-// Bottom-up moments, level-synchronous: internal cells are bucketed by level
-// (the per-level counts come from k_lcp_new and are read back with the cell
-// count, so every launch below is sized exactly), then one launch per level,
-// deepest first.  A cell's children are one level deeper, hence final when
-// its level runs; each internal cell is computed once by cell_moments, in the
-// reference's slot order.
-__global__ void k_level_scatter(TreeView t, const LevelPlan plan, int *__restrict__ cursor,
-                                int *__restrict__ list) {
-  __shared__ int h[kMaxLevel + 1], base[kMaxLevel + 1];
-  if (threadIdx.x <= kMaxLevel) h[threadIdx.x] = 0;
-  __syncthreads();
-  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  int l = -1, rank = 0;
-  if (c < t.C) {
-    const int4 L = t.link[c];
-    if (L.y > 1) {
-      l = L.w;
-      rank = atomicAdd(&h[l], 1);
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x <= kMaxLevel && h[threadIdx.x])
-    base[threadIdx.x] = plan.offset[threadIdx.x] + atomicAdd(&cursor[threadIdx.x], h[threadIdx.x]);
-  __syncthreads();
-  if (l >= 0) list[base[l] + rank] = (int)c;
-}
-
-__global__ void __launch_bounds__(128) k_moments_level(TreeView t, const int *__restrict__ list, int begin,
-                                                     int count) {
-  __shared__ double xs[128 / 32][32][11];
-  const int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
-  cell_moments8(t, k < count ? list[begin + k] : -1, xs[threadIdx.x >> 5]);
-}
-
 // C = 1 + off[n-1] + newc[n-1] on device; flag an overflow of the capacity
 __global__ void k_set_count(const uint32_t *off, const uint32_t *newc, int64_t n, int64_t cap,
                             int *dC, DeviceFlags *f) {
@@ -549,8 +451,8 @@ void launch_set_count(const uint32_t *off, const uint32_t *newc, int64_t n, int6
 
 // One cooperative launch (all blocks co-resident): offsets from the device
 // level counts, bucket the internal cells by level, then sweep the levels
-// deepest-first with a grid-wide barrier between levels -- the same
-// cell_moments work as the per-level launches, without ~22 dependent launches.
+// deepest-first with a grid-wide barrier between levels (a cell's children are
+// one level deeper, hence final when its level runs).
 namespace cg = cooperative_groups;
 #ifndef BH_MOM_MINB
 #define BH_MOM_MINB 4
@@ -644,16 +546,6 @@ int launch_moments_coop(const TreeView &t, int *lvl, int *list, int sms, cudaStr
   return (int)cudaLaunchCooperativeKernel((void *)k_moments_coop, grid, block, args, 0, s);
 }
 
-void launch_moments(const TreeView &t, const LevelPlan &plan, int *cursor, int *list,
-                    cudaStream_t s) {
-  if (t.n <= 1) return;
-  cudaMemsetAsync(cursor, 0, sizeof(int) * (kMaxLevel + 1), s);
-  k_level_scatter<<<grid_for(t.C, 256), 256, 0, s>>>(t, plan, cursor, list);
-  for (int l = kMaxLevel; l >= 0; --l) {
-    const int cnt = plan.count[l];
-    if (cnt > 0) k_moments_level<<<grid_for((int64_t)cnt * 8, 128), 128, 0, s>>>(t, list, plan.offset[l], cnt);
-  }
-}
 
 // FlatTree export (flattree.py:34-52; hashed.py:111-129 cell_geometry for the
 // centre, same child-offset arithmetic as _build_kernel).

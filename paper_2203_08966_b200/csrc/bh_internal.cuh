@@ -98,10 +98,6 @@ void launch_keys_clamped_f64(const double *pos, int stride, int64_t n, const dou
 void launch_lcp_new(const uint64_t *keys, int64_t n, int8_t *lcp, uint32_t *newc,
                     DeviceFlags *f, int *lvl_cnt, int allow_dup, cudaStream_t s,
                     int bnd_prev = -1, int bnd_next = -1);
-struct LevelPlan {  // internal cells per level (host-known) and list offsets
-  int count[kMaxLevel + 1];
-  int offset[kMaxLevel + 1];
-};
 struct TreeView {
   int64_t n = 0;       // bodies
   int64_t C = 0;       // cells; with dC set: the allocated capacity (grid bound)
@@ -121,9 +117,7 @@ struct TreeView {
 };
 void launch_emit(const TreeView &t, const float4 *bod32, const double4 *bod64, cudaStream_t s);
 // cursor: int[kMaxLevel+1] scratch; list: int[C]
-void launch_moments(const TreeView &t, const LevelPlan &plan, int *cursor, int *list,
-                    cudaStream_t s);
-// Sync-free variant: C on device (launch_set_count), per-level counts on device
+// Moments: C on device (launch_set_count) or host, per-level counts on device
 // (lvl: counts[22] from k_lcp_new | offsets[22] | cursors[22]); one cooperative
 // launch sweeps the levels deepest-first with grid-wide barriers between them.
 void launch_set_count(const uint32_t *off, const uint32_t *newc, int64_t n, int64_t cap,
