@@ -93,6 +93,24 @@ class TestKeysSort:
         with pytest.raises(ValueError, match="outside domain"):
             morton_keys(np.array([[0.0, 0.0, 0.0], [1.5, 0.0, 0.0]]), DomainBounds(1.0))
 
+    def test_nonfinite_positions_raise_in_a_step(self):
+        """A NaN or inf position fails the domain check (a NaN-safe comparison)
+        instead of producing a silent garbage key; the reference's own
+        ``min < -R or max >= R`` test lets NaN through (documented divergence)."""
+        from paper_2203_08966_b200.engine import Engine
+
+        for bad in (np.nan, np.inf):
+            eng = Engine("fp32", 0)
+            pos = np.random.default_rng(0).normal(size=(5000, 3))
+            pos[17, 1] = bad
+            p = eng.bodies_tensor(pos, np.full(5000, 2e-4))
+            v = eng.vec_tensor(np.zeros((5000, 3)))
+            eng.sim_load(p, v)
+            with pytest.raises(ValueError, match="outside domain"):
+                eng.sim_forces(0.6, 1e-3, 16, False)
+                eng.check()
+            eng.close()
+
     @pytest.mark.parametrize("n", [1, 1000, 1 << 20])
     def test_fp32_keys_and_order_match_oracle(self, eng32, n):
         rng = np.random.Generator(np.random.Philox(key=n))
