@@ -361,7 +361,7 @@ __device__ __forceinline__ float2 f2(float x) { return make_float2(x, x); }
 #endif
 constexpr int kWalkBlock = BH_WALK_BLOCK;
 #ifndef BH_WALK_MINB
-#define BH_WALK_MINB (1024 / BH_WALK_BLOCK)  // blocks/SM the register budget must allow (<= 64 regs)
+#define BH_WALK_MINB (1152 / BH_WALK_BLOCK)  // 9 blocks of 128 (<= 56 registers): +12% warps, -1%
 #endif
 constexpr int kStack = 8 * (kMaxLevel + 1) + 8;  // <= 8 pending siblings per level
 
