@@ -42,6 +42,8 @@ ALGORITHM_NAMES = {  # simulation.py:64-73
 }
 
 LEAF_MODES = ("reference", "bucket")
+DECOMPOSITIONS = ("auto", "replicated", "distributed")
+AUTO_DISTRIBUTED_N = 5_000_000
 
 
 @dataclass(frozen=True)
@@ -60,6 +62,7 @@ class SimConfig:
     precision: str = "fp64"
     devices: int = 1
     leaf_mode: str = "reference"
+    decomposition: str = "auto"  # devices > 1: "replicated" | "distributed" | "auto"
 
     def __post_init__(self) -> None:
         if self.algorithm not in ALGORITHM_NAMES:
@@ -87,6 +90,19 @@ class SimConfig:
             raise ValueError(f"leaf_mode must be one of {LEAF_MODES}, got {self.leaf_mode!r}")
         if self.devices < 1:
             raise ValueError(f"devices must be positive, got {self.devices}")
+        if self.decomposition not in DECOMPOSITIONS:
+            raise ValueError(f"decomposition must be one of {DECOMPOSITIONS}, got {self.decomposition!r}")
+        if self.decomposition == "distributed" and self.precision != "fp32":
+            raise ValueError("the distributed build runs in fp32 (precision='fp32')")
+
+    @property
+    def scheme(self) -> str:
+        """Multi-GPU scheme for devices > 1 (decomposition.py): the key-range
+        decomposition with a distributed build from AUTO_DISTRIBUTED_N bodies in
+        fp32, else the replicated tree with a partitioned walk."""
+        if self.decomposition != "auto":
+            return self.decomposition
+        return "distributed" if (self.precision == "fp32" and self.n >= AUTO_DISTRIBUTED_N) else "replicated"
 
     @property
     def walk_leaf_size(self) -> int:
@@ -198,19 +214,28 @@ def simulate(cfg: SimConfig, *, transport: str = "inproc", record_trace: bool = 
     vel = eng.vec_tensor(bodies.velocity)
     m = None if eng.fp32 else torch.as_tensor(bodies.mass).to(eng.device)
     leaf = cfg.walk_leaf_size
-    dsim = None
+    dsim = bsim = None
     if cfg.devices > 1:  # one process per GPU (torchrun); decomposition.py
         import torch.distributed as dist
 
-        from .decomposition import DistributedSim, StepParams, TorchComm
+        from .decomposition import DistributedBuildSim, DistributedSim, StepParams, TorchComm
 
         if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() != cfg.devices:
             raise ValueError(
                 f"devices={cfg.devices} needs torch.distributed initialised with that world size "
                 "(one process per GPU, e.g. torchrun --nproc-per-node)")
-        dsim = DistributedSim(eng, TorchComm(), StepParams(cfg.theta, cfg.eps, leaf, cfg.dt))
-        dsim.load(pos, vel, m)
-        dsim.bootstrap()
+        params = StepParams(cfg.theta, cfg.eps, leaf, cfg.dt)
+        if cfg.scheme == "distributed":  # each rank starts from a contiguous chunk
+            bsim = DistributedBuildSim(eng, TorchComm(), params)
+            r, R = dist.get_rank(), dist.get_world_size()
+            lo, hi = n * r // R, n * (r + 1) // R
+            bsim.load(pos[lo:hi].contiguous(), vel[lo:hi].contiguous(),
+                      gid=torch.arange(lo, hi, device=eng.device))
+            bsim.bootstrap()
+        else:
+            dsim = DistributedSim(eng, TorchComm(), params)
+            dsim.load(pos, vel, m)
+            dsim.bootstrap()
     else:
         eng.sim_load(pos, vel, m)
         eng.sim_forces(cfg.theta, cfg.eps, leaf, record_work=False)  # simulation.py:487
@@ -218,10 +243,24 @@ def simulate(cfg: SimConfig, *, transport: str = "inproc", record_trace: bool = 
     def advance(k: int) -> None:
         if dsim is not None:
             dsim.step(k)
+        elif bsim is not None:
+            bsim.step(k)
         else:
             eng.sim_step(cfg.dt, cfg.theta, cfg.eps, leaf, k)
 
     def snapshot() -> Bodies:
+        if bsim is not None:  # gather every rank's bodies back into the caller's order
+            p_, v_, a_, w_, g_ = bsim.store()
+            rows = torch.cat([p_.view(torch.int32), v_.view(torch.int32), a_.view(torch.int32),
+                              w_.view(torch.int32).view(-1, 2), g_.view(torch.int32).view(-1, 2)], dim=1)
+            allr = torch.cat(bsim._allgather_v(rows))
+            gid = allr[:, 14:16].contiguous().view(torch.int64).view(-1)
+            order = torch.argsort(gid)
+            allr = allr[order]
+            f = allr[:, 0:12].contiguous().view(torch.float32).view(-1, 3, 4)
+            return Bodies(bodies.mass.copy(), f[:, 0, :3].double().cpu().numpy(),
+                          f[:, 1, :3].double().cpu().numpy(), f[:, 2, :3].double().cpu().numpy(),
+                          allr[:, 12:14].contiguous().view(torch.int64).view(-1).cpu().numpy())
         p = torch.empty_like(vel)
         v = torch.empty_like(vel)
         a = torch.empty_like(vel)

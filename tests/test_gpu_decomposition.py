@@ -4,6 +4,7 @@ libbh handle, exchanging through ThreadComm.  Must equal the single-GPU run:
 bitwise in fp64 (the fp64 walk keeps the reference's order), to fp32 rounding
 in fp32 with identical work counts."""
 
+import os
 import threading
 
 import numpy as np
@@ -213,3 +214,43 @@ def test_target_boxes_match_numpy():
         np.testing.assert_array_equal(got[0, :3], xs.min(0))
         np.testing.assert_array_equal(got[0, 3:], xs.max(0))
     eng.close()
+
+
+def _simulate_worker(rank, port, scheme, out_path):
+    import torch.distributed as dist
+
+    from paper_2203_08966_b200.simulation import SimConfig, simulate
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)  # both ranks share the one GPU; gloo collectives are host-staged
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    cfg = SimConfig(n=24_000, algorithm=1, theta=0.6, dt=1e-3, steps=3, eps=1e-3, seed=4, leaf_size=16,
+                    precision="fp32", leaf_mode="bucket", devices=2, decomposition=scheme)
+    res = simulate(cfg)
+    if rank == 0:
+        np.savez(out_path, pos=res.bodies.position, vel=res.bodies.velocity, work=res.bodies.work)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("scheme", ["distributed", "replicated"])
+def test_simulate_devices2_matches_one_device(tmp_path, scheme):
+    """simulate(devices=2) through torch.distributed (two processes sharing this
+    GPU, gloo): the same per-body work as devices=1, positions to fp32 rounding."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    from paper_2203_08966_b200.simulation import SimConfig, simulate
+
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    out = str(tmp_path / "r.npz")
+    mp.spawn(_simulate_worker, args=(port, scheme, out), nprocs=2, join=True)
+    got = np.load(out)
+    ref = simulate(SimConfig(n=24_000, algorithm=1, theta=0.6, dt=1e-3, steps=3, eps=1e-3, seed=4, leaf_size=16,
+                             precision="fp32", leaf_mode="bucket"))
+    np.testing.assert_array_equal(got["work"], ref.bodies.work)
+    np.testing.assert_allclose(got["pos"], ref.bodies.position, rtol=0, atol=1e-5)
+    np.testing.assert_allclose(got["vel"], ref.bodies.velocity, rtol=0, atol=1e-4)
