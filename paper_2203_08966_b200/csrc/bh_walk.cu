@@ -552,6 +552,387 @@ __global__ void __launch_bounds__(kWalkBlock, BH_WALK_MINB) k_walk(
   }
 }
 
+// ------------------------------------------------ group-classified walk (v9)
+// Same per-target interaction sets as k_walk, different schedule.  The warp's
+// 64 targets have a bounding box [lo, hi].  Because fp32 rounding is monotone,
+// evaluating the per-target MAC expression d2 = fma(dz,dz, fma(dy,dy, dx*dx)),
+// d = p + a, on the box's nearest / farthest corner bounds every target's d2
+// from below / above exactly.  So a cell whose nearest-corner d2 passes the MAC
+// is accepted by every target (certain-accept), one whose farthest-corner d2
+// fails it is opened by every target (certain-open); only the rest (mixed)
+// need the per-target test.  Cells are classified 32 at a time, one per lane,
+// taken from a frontier of (first_child, nchild, mask0, mask1) entries:
+//   certain-accept -> pc list (cell, masks)           evaluated densely
+//   leaf / certain-open bucket -> pp list (lo, count | cell, 0 for a leaf, masks)
+//   certain-open internal -> frontier entry (its children, same masks)
+//   mixed -> per-target MAC, warp-uniform (as k_walk): pc for the accepting
+//            targets now, open / bucket for the others
+// The lists are drained (flushed) in tight loops with no tree control, which is
+// where the FP32 pipe does its work.  A cell is examined for a target exactly
+// when the target opened its parent, as in the reference recursion.
+#ifndef BH_W9_FULLMAX
+#define BH_W9_FULLMAX 64
+#endif
+constexpr int kW9Full = BH_W9_FULLMAX;  // full 32-cell batches while sp <= this
+// after a full batch sp <= kW9Full + 32; single-entry (DFS) batches above it add
+// at most 8 entries per level
+constexpr int kW9Frontier = kW9Full + 32 + 8 * (kMaxLevel + 1) + 8;
+#ifndef BH_W9_MXSTAGE
+#define BH_W9_MXSTAGE 1
+#endif
+#ifndef BH_W9_STAGE
+#define BH_W9_STAGE 1
+#endif
+#ifndef BH_W9_FLUSH
+#define BH_W9_FLUSH 16
+#endif
+constexpr int kW9Flush = BH_W9_FLUSH;      // pc / pp lists are drained at >= kW9Flush entries
+constexpr int kW9List = kW9Flush + 32;  // a batch adds <= 32
+#ifndef BH_W9_BLOCK
+#define BH_W9_BLOCK 128
+#endif
+#ifndef BH_W9_MINB
+#define BH_W9_MINB 6
+#endif
+constexpr int kW9Block = BH_W9_BLOCK;
+#ifndef BH_W9_PCUNROLL
+#define BH_W9_PCUNROLL 4
+#endif
+constexpr int kW9PcUnroll = BH_W9_PCUNROLL;
+
+struct W9Warp {
+  int4 fr[kW9Frontier];  // frontier: (first_child, nchild, mask0, mask1)
+  int4 pc[kW9List];      // accepted cells: (cell, -, mask0, mask1)
+  int4 pp[kW9List];      // pp: (lo, count, mask0, mask1) or a leaf record (cell, 0, ...)
+  int4 mx[32];           // mixed cells of the current batch
+#if BH_W9_STAGE
+  float4 pcr[kW9List][3];  // the accepted cells' a, b, c words (read back by broadcast)
+#endif
+#if BH_W9_MXSTAGE
+  float4 mxr[32][3];       // the mixed cells' a, b, c words
+  int4 mxd[32];            // and their d words
+#endif
+};
+
+__device__ __forceinline__ float w9_shfl_min(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float w9_shfl_max(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+// |d| over the box's range of d = p + a (d in [gl, gh]): nearest and farthest
+__device__ __forceinline__ void w9_range(float lo, float hi, float a, float &mn, float &mx) {
+  const float gl = __fadd_rn(lo, a), gh = __fadd_rn(hi, a);
+  mn = gl > 0.f ? gl : (gh < 0.f ? -gh : 0.f);
+  mx = fmaxf(fabsf(gl), fabsf(gh));
+}
+
+template <bool BUCKET>
+__global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
+    const WalkNode *__restrict__ T, const float4 *__restrict__ bodies,
+    const float *__restrict__ targets, int tstride, const uint32_t *__restrict__ tperm, int nt,
+    float e2, float *__restrict__ acc, int astride, int64_t *__restrict__ work64,
+    int *__restrict__ work32, DeviceFlags *f) {
+  extern __shared__ int4 w9_smem[];
+  W9Warp &S = reinterpret_cast<W9Warp *>(w9_smem)[threadIdx.x >> 5];
+  const unsigned lane = threadIdx.x & 31;
+  const unsigned FULL = 0xffffffffu;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t t0 = warp * 64 + 2 * lane, t1 = t0 + 1;
+  const bool v0 = t0 < nt, v1 = t1 < nt;
+  const int64_t s0 = v0 ? (tperm ? (int64_t)tperm[t0] : t0) : 0;
+  const int64_t s1 = v1 ? (tperm ? (int64_t)tperm[t1] : t1) : 0;
+  float2 X = f2(0.f), Y = f2(0.f), Z = f2(0.f);
+  if (v0) { const float *q = targets + s0 * tstride; X.x = q[0]; Y.x = q[1]; Z.x = q[2]; }
+  if (v1) { const float *q = targets + s1 * tstride; X.y = q[0]; Y.y = q[1]; Z.y = q[2]; }
+  // the box of the warp's valid targets (lane 0 always has a valid target)
+  const float INF = __int_as_float(0x7f800000);
+  const float lox = w9_shfl_min(fminf(v0 ? X.x : INF, v1 ? X.y : INF));
+  const float loy = w9_shfl_min(fminf(v0 ? Y.x : INF, v1 ? Y.y : INF));
+  const float loz = w9_shfl_min(fminf(v0 ? Z.x : INF, v1 ? Z.y : INF));
+  const float hix = w9_shfl_max(fmaxf(v0 ? X.x : -INF, v1 ? X.y : -INF));
+  const float hiy = w9_shfl_max(fmaxf(v0 ? Y.x : -INF, v1 ? Y.y : -INF));
+  const float hiz = w9_shfl_max(fmaxf(v0 ? Z.x : -INF, v1 ? Z.y : -INF));
+  float2 AX = f2(0.f), AY = f2(0.f), AZ = f2(0.f);
+  int pp0 = 0, pp1 = 0, pc0 = 0, pc1 = 0;
+  const float2 E2 = f2(e2);
+  const unsigned bit = 1u << lane;
+  const unsigned lt = bit - 1u;
+
+  int sp = 1, npc = 0, npp = 0;
+  {
+    const unsigned m0 = __ballot_sync(FULL, v0), m1 = __ballot_sync(FULL, v1);
+    if (lane == 0) {  // root internal: start at its children (flattree.py:271-279)
+      const int4 rd = T[0].d;
+      S.fr[0] = rd.y > 1 ? make_int4(rd.x, rd.z, (int)m0, (int)m1) : make_int4(0, 1, (int)m0, (int)m1);
+    }
+  }
+  __syncwarp();
+
+  // dense pc over the list (the FP32-pipe work)
+  auto flush_pc = [&](int n) {
+#pragma unroll(kW9PcUnroll)
+    for (int k = 0; k < n; ++k) {
+      const int4 en = S.pc[k];
+      const bool u0 = (unsigned)en.z & bit, u1 = (unsigned)en.w & bit;
+#if BH_W9_STAGE
+      const float4 a = S.pcr[k][0];
+      const float4 b = S.pcr[k][1];
+      const float4 q = S.pcr[k][2];
+#else
+      const WalkNode *nd = T + en.x;
+      const float4 a = nd->a;
+      const float4 b = nd->b;
+      const float4 q = nd->c;
+#endif
+      const float2 DX = __fadd2_rn(X, f2(a.x));
+      const float2 DY = __fadd2_rn(Y, f2(a.y));
+      const float2 DZ = __fadd2_rn(Z, f2(a.z));
+      const float2 D2 = __ffma2_rn(DZ, DZ, __ffma2_rn(DY, DY, __fmul2_rn(DX, DX)));
+      const float2 R = f2(u0 ? rsqrtf(D2.x) : 0.f, u1 ? rsqrtf(D2.y) : 0.f);
+      const float2 R2 = __fmul2_rn(R, R);
+      const float2 R3 = __fmul2_rn(R2, R);
+      const float2 R5 = __fmul2_rn(R3, R2);
+      const float2 QX = __ffma2_rn(f2(q.x), DZ, __ffma2_rn(f2(b.y), DY, __fmul2_rn(f2(b.x), DX)));
+      const float2 QY = __ffma2_rn(f2(q.y), DZ, __ffma2_rn(f2(b.w), DY, __fmul2_rn(f2(b.y), DX)));
+      const float2 QZ = __ffma2_rn(f2(q.w), DZ, __ffma2_rn(f2(q.y), DY, __fmul2_rn(f2(q.x), DX)));
+      const float2 RQR = __ffma2_rn(DZ, QZ, __ffma2_rn(DY, QY, __fmul2_rn(DX, QX)));
+      const float2 Sc = __fmul2_rn(__ffma2_rn(__fmul2_rn(RQR, __fmul2_rn(R2, R2)), f2(-2.5f), f2(-q.z)), R3);
+      AX = __ffma2_rn(R5, QX, __ffma2_rn(Sc, DX, AX));
+      AY = __ffma2_rn(R5, QY, __ffma2_rn(Sc, DY, AY));
+      AZ = __ffma2_rn(R5, QZ, __ffma2_rn(Sc, DZ, AZ));
+      pc0 += u0; pc1 += u1;
+    }
+  };
+  // dense pp over the bodies of the listed leaves / buckets (self skipped by r2 > 0)
+  auto flush_pp = [&](int n) {
+    for (int k = 0; k < n; ++k) {
+      const int4 en = S.pp[k];
+      const bool u0 = (unsigned)en.z & bit, u1 = (unsigned)en.w & bit;
+      if (en.y == 0) {  // leaf record: its com and mass are the body (a LET leaf has no body index here)
+        const WalkNode *nd = T + en.x;
+        const float4 a = nd->a;
+        const float m = nd->c.z;
+        const float2 DX = __fadd2_rn(X, f2(a.x));
+        const float2 DY = __fadd2_rn(Y, f2(a.y));
+        const float2 DZ = __fadd2_rn(Z, f2(a.z));
+        const float2 D2 = __ffma2_rn(DZ, DZ, __ffma2_rn(DY, DY, __fmul2_rn(DX, DX)));
+        const bool l0 = u0 && D2.x > 0.f, l1 = u1 && D2.y > 0.f;
+        const float2 W = __fadd2_rn(D2, E2);
+        const float2 R = f2(l0 ? rsqrtf(W.x) : 0.f, l1 ? rsqrtf(W.y) : 0.f);
+        const float2 Sc = __fmul2_rn(__fmul2_rn(R, R), __fmul2_rn(R, f2(-m)));
+        AX = __ffma2_rn(Sc, DX, AX);
+        AY = __ffma2_rn(Sc, DY, AY);
+        AZ = __ffma2_rn(Sc, DZ, AZ);
+        pp0 += l0; pp1 += l1;
+        continue;
+      }
+#pragma unroll(kBucketUnroll)
+      for (int j = en.x; j < en.x + en.y; ++j) {
+        const float4 bb = bodies[j];
+        const float2 EX = __ffma2_rn(f2(bb.x), f2(-1.f), X);
+        const float2 EY = __ffma2_rn(f2(bb.y), f2(-1.f), Y);
+        const float2 EZ = __ffma2_rn(f2(bb.z), f2(-1.f), Z);
+        const float2 Q2 = __ffma2_rn(EZ, EZ, __ffma2_rn(EY, EY, __fmul2_rn(EX, EX)));
+        const bool m0 = u0 && Q2.x > 0.f, m1 = u1 && Q2.y > 0.f;
+        const float2 W = __fadd2_rn(Q2, E2);
+        const float2 R = f2(m0 ? rsqrtf(W.x) : 0.f, m1 ? rsqrtf(W.y) : 0.f);
+        const float2 Sc = __fmul2_rn(__fmul2_rn(R, R), __fmul2_rn(R, f2(-bb.w)));
+        AX = __ffma2_rn(Sc, EX, AX);
+        AY = __ffma2_rn(Sc, EY, AY);
+        AZ = __ffma2_rn(Sc, EZ, AZ);
+        pp0 += m0; pp1 += m1;
+      }
+    }
+  };
+
+  while (sp > 0) {
+    // ---- gather up to 32 cells from the top entries (one entry above kW9Full)
+    const int ne = sp <= kW9Full ? min(sp, 32) : 1;
+    int4 E = make_int4(0, 0, 0, 0);
+    if ((int)lane < ne) E = S.fr[sp - 1 - lane];
+    const int nc = (int)lane < ne ? E.y : 0;
+    int incl = nc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(FULL, incl, o);
+      if ((int)lane >= o) incl += v;
+    }
+    const int excl = incl - nc;
+    const int take = nc > 0 ? max(0, min(nc, 32 - excl)) : 0;
+    const int kfull = __popc(__ballot_sync(FULL, nc > 0 && incl <= 32));  // entries used up
+    const int ncell = min(32, __shfl_sync(FULL, incl, ne - 1));
+    const unsigned starts = __reduce_or_sync(FULL, take > 0 ? 1u << excl : 0u);
+    __syncwarp();
+    if ((int)lane == kfull && lane < (unsigned)ne && take > 0)  // partly used: keep the rest
+      S.fr[sp - 1 - lane] = make_int4(E.x + take, E.y - take, E.z, E.w);
+    sp -= kfull;
+    const int src = __popc(starts & (FULL >> (31 - lane))) - 1;
+    const int cfc = __shfl_sync(FULL, E.x, src), cex = __shfl_sync(FULL, excl, src);
+    const unsigned m0 = (unsigned)__shfl_sync(FULL, E.z, src), m1 = (unsigned)__shfl_sync(FULL, E.w, src);
+    const bool valid = (int)lane < ncell;
+    const int cell = cfc + ((int)lane - cex);
+
+    // ---- classify one cell per lane
+    bool to_pp = false, to_pc = false, to_fr = false, to_mx = false;
+    int4 d = make_int4(0, 0, 0, 0);
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (valid) {
+      const WalkNode *nd = T + cell;
+      a = nd->a;
+      d = nd->d;
+      if (d.y == 0) {
+        // empty tree (no bodies): nothing to interact with
+      } else if (d.y == 1) {
+        to_pp = true;  // leaf: pp, no MAC (flattree.py:287-294)
+      } else {
+        float nx, ny, nz, xx, xy, xz;
+        w9_range(lox, hix, a.x, nx, xx);
+        w9_range(loy, hiy, a.y, ny, xy);
+        w9_range(loz, hiz, a.z, nz, xz);
+        const float dmin2 = __fmaf_rn(nz, nz, __fmaf_rn(ny, ny, __fmul_rn(nx, nx)));
+        const float dmax2 = __fmaf_rn(xz, xz, __fmaf_rn(xy, xy, __fmul_rn(xx, xx)));
+        if (dmin2 > a.w) to_pc = true;                      // every target accepts
+        else if (!(dmax2 > a.w)) {                          // every target opens
+          if (d.z > 0) to_fr = true;
+          else to_pp = BUCKET;
+        } else to_mx = true;
+      }
+    }
+    const unsigned bpp = __ballot_sync(FULL, to_pp), bpc = __ballot_sync(FULL, to_pc);
+    const unsigned bfr = __ballot_sync(FULL, to_fr), bmx = __ballot_sync(FULL, to_mx);
+    if (to_pp) S.pp[npp + __popc(bpp & lt)] = d.y == 1 ? make_int4(cell, 0, (int)m0, (int)m1)
+                                                   : make_int4(d.x, d.y, (int)m0, (int)m1);
+    if (to_pc) {
+      const int slot = npc + __popc(bpc & lt);
+      S.pc[slot] = make_int4(cell, 0, (int)m0, (int)m1);
+#if BH_W9_STAGE
+      S.pcr[slot][0] = a;
+      S.pcr[slot][1] = T[cell].b;
+      S.pcr[slot][2] = T[cell].c;
+#endif
+    }
+    if (to_fr) S.fr[sp + __popc(bfr & lt)] = make_int4(d.x, d.z, (int)m0, (int)m1);
+    if (to_mx) {
+      const int slot = __popc(bmx & lt);
+      S.mx[slot] = make_int4(cell, 0, (int)m0, (int)m1);
+#if BH_W9_MXSTAGE
+      S.mxr[slot][0] = a;
+      S.mxr[slot][1] = T[cell].b;
+      S.mxr[slot][2] = T[cell].c;
+      S.mxd[slot] = d;
+#endif
+    }
+    npp += __popc(bpp);
+    npc += __popc(bpc);
+    sp += __popc(bfr);
+    const int nmx = __popc(bmx);
+    __syncwarp();
+
+    // ---- mixed cells: the per-target MAC (warp-uniform, as k_walk)
+    for (int k = 0; k < nmx; ++k) {
+      const int4 me = S.mx[k];
+      const bool in0 = (unsigned)me.z & bit, in1 = (unsigned)me.w & bit;
+#if BH_W9_MXSTAGE
+      const float4 a = S.mxr[k][0];
+      const float4 b = S.mxr[k][1];
+      const float4 q = S.mxr[k][2];
+      const int4 dd = S.mxd[k];
+#else
+      const WalkNode *nd = T + me.x;
+      const float4 a = nd->a;
+      const int4 dd = nd->d;
+      const float4 b = nd->b;
+      const float4 q = nd->c;
+#endif
+      const float2 DX = __fadd2_rn(X, f2(a.x));
+      const float2 DY = __fadd2_rn(Y, f2(a.y));
+      const float2 DZ = __fadd2_rn(Z, f2(a.z));
+      const float2 D2 = __ffma2_rn(DZ, DZ, __ffma2_rn(DY, DY, __fmul2_rn(DX, DX)));
+      const bool c0 = in0 && D2.x > a.w, c1 = in1 && D2.y > a.w;  // MAC (flattree.py:295)
+      if (__any_sync(FULL, c0 || c1)) {
+        const float2 R = f2(c0 ? rsqrtf(D2.x) : 0.f, c1 ? rsqrtf(D2.y) : 0.f);
+        const float2 R2 = __fmul2_rn(R, R);
+        const float2 R3 = __fmul2_rn(R2, R);
+        const float2 R5 = __fmul2_rn(R3, R2);
+        const float2 QX = __ffma2_rn(f2(q.x), DZ, __ffma2_rn(f2(b.y), DY, __fmul2_rn(f2(b.x), DX)));
+        const float2 QY = __ffma2_rn(f2(q.y), DZ, __ffma2_rn(f2(b.w), DY, __fmul2_rn(f2(b.y), DX)));
+        const float2 QZ = __ffma2_rn(f2(q.w), DZ, __ffma2_rn(f2(q.y), DY, __fmul2_rn(f2(q.x), DX)));
+        const float2 RQR = __ffma2_rn(DZ, QZ, __ffma2_rn(DY, QY, __fmul2_rn(DX, QX)));
+        const float2 Sc = __fmul2_rn(__ffma2_rn(__fmul2_rn(RQR, __fmul2_rn(R2, R2)), f2(-2.5f), f2(-q.z)), R3);
+        AX = __ffma2_rn(R5, QX, __ffma2_rn(Sc, DX, AX));
+        AY = __ffma2_rn(R5, QY, __ffma2_rn(Sc, DY, AY));
+        AZ = __ffma2_rn(R5, QZ, __ffma2_rn(Sc, DZ, AZ));
+        pc0 += c0; pc1 += c1;
+      }
+      const unsigned o0 = __ballot_sync(FULL, in0 && !c0), o1 = __ballot_sync(FULL, in1 && !c1);
+      if ((o0 | o1) == 0u) continue;
+      if (dd.z > 0) {
+        if (lane == 0) S.fr[sp] = make_int4(dd.x, dd.z, (int)o0, (int)o1);
+        ++sp;
+      } else if (BUCKET) {
+        if (lane == 0) S.pp[npp] = make_int4(dd.x, dd.y, (int)o0, (int)o1);
+        ++npp;
+      }
+    }
+    __syncwarp();
+    if (npc >= kW9Flush) { flush_pc(npc); npc = 0; }
+    if (npp >= kW9Flush) { flush_pp(npp); npp = 0; }
+    __syncwarp();
+  }
+  flush_pc(npc);
+  flush_pp(npp);
+
+  if (v0) {
+    float *o = acc + s0 * astride;
+    o[0] = AX.x; o[1] = AY.x; o[2] = AZ.x;
+    const int w = pp0 + 2 * pc0;  // WORK_PP, WORK_PC (octree.py:23-25)
+    if (work64) work64[s0] = w;
+    if (work32) work32[s0] = w;
+  }
+  if (v1) {
+    float *o = acc + s1 * astride;
+    o[0] = AX.y; o[1] = AY.y; o[2] = AZ.y;
+    const int w = pp1 + 2 * pc1;
+    if (work64) work64[s1] = w;
+    if (work32) work32[s1] = w;
+  }
+  const unsigned spp = __reduce_add_sync(FULL, (unsigned)(pp0 + pp1));
+  const unsigned spc = __reduce_add_sync(FULL, (unsigned)(pc0 + pc1));
+  if (lane == 0) {
+    atomicAdd(&f->pp, (unsigned long long)spp);
+    atomicAdd(&f->pc, (unsigned long long)spc);
+  }
+}
+
+static bool walk9_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char *e = getenv("BH_WALK_V4");
+    on = (e && *e && *e != '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
+template <bool BUCKET>
+static void launch_walk9(const WalkNode *T, const float4 *bodies, const float *targets, int tstride,
+                         const uint32_t *tperm, int nt, float e2, float *acc, int astride, int64_t *work64,
+                         int *work32, DeviceFlags *f, cudaStream_t s) {
+  const size_t smem = sizeof(W9Warp) * (kW9Block / 32);
+  static bool init = false;
+  if (!init) {
+    cudaFuncSetAttribute(k_walk9<BUCKET>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    init = true;
+  }
+  const int64_t warps = ((int64_t)nt + 63) / 64;
+  k_walk9<BUCKET><<<grid_for(warps * 32, kW9Block), kW9Block, smem, s>>>(T, bodies, targets, tstride, tperm, nt,
+                                                                         e2, acc, astride, work64, work32, f);
+}
+
 template <int MODE>
 static void launch_walk_mode(const WalkNode *T, const float4 *bodies, const float *targets, int tstride,
                              const uint32_t *tperm, int nt, float e2, int leaf, float *acc, int astride,
@@ -571,6 +952,11 @@ void launch_walk_f32(const WalkNode *T, const float4 *bodies, const float *targe
                      const uint32_t *tperm, int nt, float e2, int leaf, float *acc, int astride,
                      int64_t *work64, int *work32, DeviceFlags *f, cudaStream_t s) {
   if (nt <= 0) return;
+  if (walk9_enabled()) {
+    if (leaf > 1) launch_walk9<true>(T, bodies, targets, tstride, tperm, nt, e2, acc, astride, work64, work32, f, s);
+    else launch_walk9<false>(T, bodies, targets, tstride, tperm, nt, e2, acc, astride, work64, work32, f, s);
+    return;
+  }
   launch_walk_mode<kWalkFull>(T, bodies, targets, tstride, tperm, nt, e2, leaf, acc, astride, work64, work32, f,
                               DeferArgs{}, s);
 }
