@@ -40,6 +40,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cooperative_groups.h>
 
 #include "bh_internal.cuh"
@@ -577,6 +578,9 @@ constexpr int kW9Full = BH_W9_FULLMAX;  // full 32-cell batches while sp <= this
 // after a full batch sp <= kW9Full + 32; single-entry (DFS) batches above it add
 // at most 8 entries per level
 constexpr int kW9Frontier = kW9Full + 32 + 8 * (kMaxLevel + 1) + 8;
+#ifndef BH_W9_PFPP
+#define BH_W9_PFPP 0
+#endif
 #ifndef BH_W9_MXSTAGE
 #define BH_W9_MXSTAGE 1
 #endif
@@ -636,7 +640,7 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
     const WalkNode *__restrict__ T, const float4 *__restrict__ bodies,
     const float *__restrict__ targets, int tstride, const uint32_t *__restrict__ tperm, int nt,
     float e2, float *__restrict__ acc, int astride, int64_t *__restrict__ work64,
-    int *__restrict__ work32, DeviceFlags *f) {
+    int *__restrict__ work32, DeviceFlags *f, int fullmax) {
   extern __shared__ int4 w9_smem[];
   W9Warp &S = reinterpret_cast<W9Warp *>(w9_smem)[threadIdx.x >> 5];
   const unsigned lane = threadIdx.x & 31;
@@ -752,7 +756,7 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
 
   while (sp > 0) {
     // ---- gather up to 32 cells from the top entries (one entry above kW9Full)
-    const int ne = sp <= kW9Full ? min(sp, 32) : 1;
+    const int ne = sp <= fullmax ? min(sp, 32) : 1;
     int4 E = make_int4(0, 0, 0, 0);
     if ((int)lane < ne) E = S.fr[sp - 1 - lane];
     const int nc = (int)lane < ne ? E.y : 0;
@@ -807,6 +811,10 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
     const unsigned bfr = __ballot_sync(FULL, to_fr), bmx = __ballot_sync(FULL, to_mx);
     if (to_pp) S.pp[npp + __popc(bpp & lt)] = d.y == 1 ? make_int4(cell, 0, (int)m0, (int)m1)
                                                    : make_int4(d.x, d.y, (int)m0, (int)m1);
+#if BH_W9_PFPP
+    if (to_pp && d.y > 1)  // the bucket's bodies, read by the pp drain a few steps later
+      for (int j = d.x; j < d.x + d.y; j += 8) asm volatile("prefetch.global.L1 [%0];" ::"l"(bodies + j));
+#endif
     if (to_pc) {
       const int slot = npc + __popc(bpc & lt);
       S.pc[slot] = make_int4(cell, 0, (int)m0, (int)m1);
@@ -909,13 +917,23 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
   }
 }
 
-static bool walk9_enabled() {
+static bool walk9_enabled() {  // BH_WALK_V4=1: the masked-stack walk (k_walk) instead
   static int on = -1;
   if (on < 0) {
     const char *e = getenv("BH_WALK_V4");
     on = (e && *e && *e != '0') ? 0 : 1;
   }
   return on == 1;
+}
+// full-batch threshold (<= kW9Full, which sizes the frontier); BH_W9_FULL=0 runs
+// every batch as one sibling set (the DFS mode the frontier bound rests on)
+static int walk9_fullmax() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("BH_W9_FULL");
+    v = e && *e ? std::max(0, std::min(kW9Full, atoi(e))) : kW9Full;
+  }
+  return v;
 }
 
 template <bool BUCKET>
@@ -930,7 +948,8 @@ static void launch_walk9(const WalkNode *T, const float4 *bodies, const float *t
   }
   const int64_t warps = ((int64_t)nt + 63) / 64;
   k_walk9<BUCKET><<<grid_for(warps * 32, kW9Block), kW9Block, smem, s>>>(T, bodies, targets, tstride, tperm, nt,
-                                                                         e2, acc, astride, work64, work32, f);
+                                                                         e2, acc, astride, work64, work32, f,
+                                                                         walk9_fullmax());
 }
 
 template <int MODE>
