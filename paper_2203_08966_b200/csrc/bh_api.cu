@@ -549,7 +549,7 @@ int sim_walk(bh_handle *h, double theta, double eps, int leaf, int64_t begin, in
   int *w32 = record_work ? h->work_sorted.as<int>() + begin : nullptr;
   if (f32) {
     BH_TRY(ensure_walk_tree(h, theta, leaf, s));
-    launch_walk_f32(h->wnodes.as<WalkNode>(), h->pos.as<float4>(),
+    launch_walk_f32(h->wnodes.as<WalkNode>(), (int64_t)(h->wnodes.bytes / sizeof(WalkNode)), h->pos.as<float4>(),
                     h->pos.as<float>() + 4 * begin, 4, nullptr, (int)nt, (float)(eps * eps), leaf,
                     h->acc.as<float>() + 4 * begin, 4, nullptr, w32, h->flags, s);
   } else {
@@ -843,7 +843,7 @@ static int traverse_common(bh_handle *h, const void *targets, int64_t n, double 
   fill_walk_params(h, P, n, theta, eps, leaf);
   if (f32) {
     BH_TRY(ensure_walk_tree(h, theta, leaf, s));
-    launch_walk_f32(h->wnodes.as<WalkNode>(), h->tbod.as<float4>(),
+    launch_walk_f32(h->wnodes.as<WalkNode>(), (int64_t)(h->wnodes.bytes / sizeof(WalkNode)), h->tbod.as<float4>(),
                     static_cast<const float *>(targets), 4, h->vals2.as<uint32_t>(), (int)n,
                     (float)(eps * eps), leaf, static_cast<float *>(acc), 4, work, nullptr,
                     h->flags, s);
@@ -1501,7 +1501,7 @@ int bh_walk_records_f32(bh_handle *h, const void *d_records, int64_t nrec, const
   cudaStream_t s = S(stream);
   BH_TRY(reset_counters(h, s));
   h->tbegin(BH_PHASE_WALK, s);
-  launch_walk_f32(static_cast<const WalkNode *>(d_records), reinterpret_cast<const float4 *>(d_bodies4),
+  launch_walk_f32(static_cast<const WalkNode *>(d_records), nrec, reinterpret_cast<const float4 *>(d_bodies4),
                   d_targets4, 4, nullptr, (int)nt, (float)(eps * eps), leaf_size, d_acc4, 4, nullptr,
                   d_work, h->flags, s);
   h->tend(s);

@@ -178,8 +178,10 @@ void launch_mark_shared(const TreeView &t, uint8_t *shared, int *branch, int *nb
 void launch_branch_export(const TreeView &t, const int *branch, int nb, const int *rec_of_cell,
                           uint64_t *key, int *level, int64_t *count, double *mom, int *rec,
                           int *lo, cudaStream_t s);
-void launch_walk_f32(const WalkNode *T, const float4 *bodies, const float *targets, int tstride,
-                     const uint32_t *tperm, int nt, float e2, int leaf, float *acc, int astride,
+// nrec_max: an upper bound on the records in T (the group-classified walk packs
+// record indices in 28 bits; larger trees take the masked-stack walk)
+void launch_walk_f32(const WalkNode *T, int64_t nrec_max, const float4 *bodies, const float *targets,
+                     int tstride, const uint32_t *tperm, int nt, float e2, int leaf, float *acc, int astride,
                      int64_t *work64, int *work32, DeviceFlags *f, cudaStream_t s);
 // deferred walk (LET overlap): pass A appends (target chunk, record, m0, m1) to
 // out[cap] for records flagged in d.w; pass B (resume) walks in[nin] with

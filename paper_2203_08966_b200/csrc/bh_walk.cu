@@ -563,7 +563,7 @@ __global__ void __launch_bounds__(kWalkBlock, BH_WALK_MINB) k_walk(
 // fails it is opened by every target (certain-open); only the rest (mixed)
 // need the per-target test.  Cells are classified 32 at a time, one per lane,
 // taken from a frontier of (first_child, nchild, mask0, mask1) entries:
-//   certain-accept -> pc list (cell, masks)           evaluated densely
+//   certain-accept -> pc list (the record, masks)      evaluated densely
 //   leaf / certain-open bucket -> pp list (lo, count | cell, 0 for a leaf, masks)
 //   certain-open internal -> frontier entry (its children, same masks)
 //   mixed -> per-target MAC, warp-uniform (as k_walk): pc for the accepting
@@ -578,15 +578,6 @@ constexpr int kW9Full = BH_W9_FULLMAX;  // full 32-cell batches while sp <= this
 // after a full batch sp <= kW9Full + 32; single-entry (DFS) batches above it add
 // at most 8 entries per level
 constexpr int kW9Frontier = kW9Full + 32 + 8 * (kMaxLevel + 1) + 8;
-#ifndef BH_W9_PFPP
-#define BH_W9_PFPP 0
-#endif
-#ifndef BH_W9_MXSTAGE
-#define BH_W9_MXSTAGE 1
-#endif
-#ifndef BH_W9_STAGE
-#define BH_W9_STAGE 1
-#endif
 #ifndef BH_W9_FLUSH
 #define BH_W9_FLUSH 16
 #endif
@@ -603,19 +594,18 @@ constexpr int kW9Block = BH_W9_BLOCK;
 #define BH_W9_PCUNROLL 4
 #endif
 constexpr int kW9PcUnroll = BH_W9_PCUNROLL;
+constexpr int kW9NcShift = 28;  // frontier entry: first_child | nchild << 28, unsigned (records < 2^28)
 
+// Per-warp shared memory (~7.4 KB).  Masks ride in record words the drains do
+// not read: a.w (mac2) and b.z (the duplicate qxy) of a staged pc record, b.z
+// and d.w (level) of a staged mixed record.
 struct W9Warp {
-  int4 fr[kW9Frontier];  // frontier: (first_child, nchild, mask0, mask1)
-  int4 pc[kW9List];      // accepted cells: (cell, -, mask0, mask1)
-  int4 pp[kW9List];      // pp: (lo, count, mask0, mask1) or a leaf record (cell, 0, ...)
-  int4 mx[32];           // mixed cells of the current batch
-#if BH_W9_STAGE
-  float4 pcr[kW9List][3];  // the accepted cells' a, b, c words (read back by broadcast)
-#endif
-#if BH_W9_MXSTAGE
-  float4 mxr[32][3];       // the mixed cells' a, b, c words
-  int4 mxd[32];            // and their d words
-#endif
+  int fc[kW9Frontier];     // frontier: first_child | nchild << kW9NcShift
+  uint2 fm[kW9Frontier];   //           (mask0, mask1)
+  float4 pcr[kW9List][3];  // accepted cells: a (mask0 in .w), b (mask1 in .z), c
+  int4 pp[kW9List];        // pp: (lo, count, mask0, mask1) or a leaf record (cell, 0, ...)
+  float4 mxr[32][3];       // mixed cells of the batch: a, b (mask0 in .z), c
+  int4 mxd[32];            //                           d (mask1 in .w)
 };
 
 __device__ __forceinline__ float w9_shfl_min(float v) {
@@ -672,7 +662,8 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
     const unsigned m0 = __ballot_sync(FULL, v0), m1 = __ballot_sync(FULL, v1);
     if (lane == 0) {  // root internal: start at its children (flattree.py:271-279)
       const int4 rd = T[0].d;
-      S.fr[0] = rd.y > 1 ? make_int4(rd.x, rd.z, (int)m0, (int)m1) : make_int4(0, 1, (int)m0, (int)m1);
+      S.fc[0] = rd.y > 1 ? (rd.x | rd.z << kW9NcShift) : (0 | 1 << kW9NcShift);
+      S.fm[0] = make_uint2(m0, m1);
     }
   }
   __syncwarp();
@@ -681,18 +672,10 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
   auto flush_pc = [&](int n) {
 #pragma unroll(kW9PcUnroll)
     for (int k = 0; k < n; ++k) {
-      const int4 en = S.pc[k];
-      const bool u0 = (unsigned)en.z & bit, u1 = (unsigned)en.w & bit;
-#if BH_W9_STAGE
       const float4 a = S.pcr[k][0];
       const float4 b = S.pcr[k][1];
       const float4 q = S.pcr[k][2];
-#else
-      const WalkNode *nd = T + en.x;
-      const float4 a = nd->a;
-      const float4 b = nd->b;
-      const float4 q = nd->c;
-#endif
+      const bool u0 = (unsigned)__float_as_int(a.w) & bit, u1 = (unsigned)__float_as_int(b.z) & bit;
       const float2 DX = __fadd2_rn(X, f2(a.x));
       const float2 DY = __fadd2_rn(Y, f2(a.y));
       const float2 DZ = __fadd2_rn(Z, f2(a.z));
@@ -758,7 +741,11 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
     // ---- gather up to 32 cells from the top entries (one entry above kW9Full)
     const int ne = sp <= fullmax ? min(sp, 32) : 1;
     int4 E = make_int4(0, 0, 0, 0);
-    if ((int)lane < ne) E = S.fr[sp - 1 - lane];
+    if ((int)lane < ne) {
+      const int fcnc = S.fc[sp - 1 - lane];
+      const uint2 fm = S.fm[sp - 1 - lane];
+      E = make_int4(fcnc & ((1 << kW9NcShift) - 1), (int)((unsigned)fcnc >> kW9NcShift), (int)fm.x, (int)fm.y);
+    }
     const int nc = (int)lane < ne ? E.y : 0;
     int incl = nc;
 #pragma unroll
@@ -773,7 +760,7 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
     const unsigned starts = __reduce_or_sync(FULL, take > 0 ? 1u << excl : 0u);
     __syncwarp();
     if ((int)lane == kfull && lane < (unsigned)ne && take > 0)  // partly used: keep the rest
-      S.fr[sp - 1 - lane] = make_int4(E.x + take, E.y - take, E.z, E.w);
+      S.fc[sp - 1 - lane] = (E.x + take) | (E.y - take) << kW9NcShift;
     sp -= kfull;
     const int src = __popc(starts & (FULL >> (31 - lane))) - 1;
     const int cfc = __shfl_sync(FULL, E.x, src), cex = __shfl_sync(FULL, excl, src);
@@ -811,29 +798,27 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
     const unsigned bfr = __ballot_sync(FULL, to_fr), bmx = __ballot_sync(FULL, to_mx);
     if (to_pp) S.pp[npp + __popc(bpp & lt)] = d.y == 1 ? make_int4(cell, 0, (int)m0, (int)m1)
                                                    : make_int4(d.x, d.y, (int)m0, (int)m1);
-#if BH_W9_PFPP
-    if (to_pp && d.y > 1)  // the bucket's bodies, read by the pp drain a few steps later
-      for (int j = d.x; j < d.x + d.y; j += 8) asm volatile("prefetch.global.L1 [%0];" ::"l"(bodies + j));
-#endif
     if (to_pc) {
       const int slot = npc + __popc(bpc & lt);
-      S.pc[slot] = make_int4(cell, 0, (int)m0, (int)m1);
-#if BH_W9_STAGE
-      S.pcr[slot][0] = a;
-      S.pcr[slot][1] = T[cell].b;
+      float4 b = T[cell].b;
+      b.z = __int_as_float((int)m1);
+      S.pcr[slot][0] = make_float4(a.x, a.y, a.z, __int_as_float((int)m0));
+      S.pcr[slot][1] = b;
       S.pcr[slot][2] = T[cell].c;
-#endif
     }
-    if (to_fr) S.fr[sp + __popc(bfr & lt)] = make_int4(d.x, d.z, (int)m0, (int)m1);
+    if (to_fr) {
+      const int slot = sp + __popc(bfr & lt);
+      S.fc[slot] = d.x | d.z << kW9NcShift;
+      S.fm[slot] = make_uint2(m0, m1);
+    }
     if (to_mx) {
       const int slot = __popc(bmx & lt);
-      S.mx[slot] = make_int4(cell, 0, (int)m0, (int)m1);
-#if BH_W9_MXSTAGE
+      float4 b = T[cell].b;
+      b.z = __int_as_float((int)m0);
       S.mxr[slot][0] = a;
-      S.mxr[slot][1] = T[cell].b;
+      S.mxr[slot][1] = b;
       S.mxr[slot][2] = T[cell].c;
-      S.mxd[slot] = d;
-#endif
+      S.mxd[slot] = make_int4(d.x, d.y, d.z, (int)m1);
     }
     npp += __popc(bpp);
     npc += __popc(bpc);
@@ -843,20 +828,11 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
 
     // ---- mixed cells: the per-target MAC (warp-uniform, as k_walk)
     for (int k = 0; k < nmx; ++k) {
-      const int4 me = S.mx[k];
-      const bool in0 = (unsigned)me.z & bit, in1 = (unsigned)me.w & bit;
-#if BH_W9_MXSTAGE
       const float4 a = S.mxr[k][0];
       const float4 b = S.mxr[k][1];
       const float4 q = S.mxr[k][2];
       const int4 dd = S.mxd[k];
-#else
-      const WalkNode *nd = T + me.x;
-      const float4 a = nd->a;
-      const int4 dd = nd->d;
-      const float4 b = nd->b;
-      const float4 q = nd->c;
-#endif
+      const bool in0 = (unsigned)__float_as_int(b.z) & bit, in1 = (unsigned)dd.w & bit;
       const float2 DX = __fadd2_rn(X, f2(a.x));
       const float2 DY = __fadd2_rn(Y, f2(a.y));
       const float2 DZ = __fadd2_rn(Z, f2(a.z));
@@ -880,7 +856,10 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
       const unsigned o0 = __ballot_sync(FULL, in0 && !c0), o1 = __ballot_sync(FULL, in1 && !c1);
       if ((o0 | o1) == 0u) continue;
       if (dd.z > 0) {
-        if (lane == 0) S.fr[sp] = make_int4(dd.x, dd.z, (int)o0, (int)o1);
+        if (lane == 0) {
+          S.fc[sp] = dd.x | dd.z << kW9NcShift;
+          S.fm[sp] = make_uint2(o0, o1);
+        }
         ++sp;
       } else if (BUCKET) {
         if (lane == 0) S.pp[npp] = make_int4(dd.x, dd.y, (int)o0, (int)o1);
@@ -967,11 +946,11 @@ static void launch_walk_mode(const WalkNode *T, const float4 *bodies, const floa
                                                  work64, work32, f, dfr);
 }
 
-void launch_walk_f32(const WalkNode *T, const float4 *bodies, const float *targets, int tstride,
-                     const uint32_t *tperm, int nt, float e2, int leaf, float *acc, int astride,
+void launch_walk_f32(const WalkNode *T, int64_t nrec_max, const float4 *bodies, const float *targets,
+                     int tstride, const uint32_t *tperm, int nt, float e2, int leaf, float *acc, int astride,
                      int64_t *work64, int *work32, DeviceFlags *f, cudaStream_t s) {
   if (nt <= 0) return;
-  if (walk9_enabled()) {
+  if (walk9_enabled() && nrec_max < (int64_t(1) << kW9NcShift)) {
     if (leaf > 1) launch_walk9<true>(T, bodies, targets, tstride, tperm, nt, e2, acc, astride, work64, work32, f, s);
     else launch_walk9<false>(T, bodies, targets, tstride, tperm, nt, e2, acc, astride, work64, work32, f, s);
     return;

@@ -35,10 +35,14 @@ iW, iI = h.index("Warp Stall Sampling (All Samples)"), h.index("Instructions Exe
 data = rows[2:]
 base = int(data[0][0], 16)
 W, I = defaultdict(float), defaultdict(float)
+stall_cols = [(i, c.replace("stall_", "")) for i, c in enumerate(h) if c.startswith("stall_") and "Not Issued" not in c]
+ST = defaultdict(lambda: defaultdict(float))
 for r in data:
     ln = m.get(int(r[0], 16) - base, -1)
     W[ln] += float(r[iW] or 0)
     I[ln] += float(r[iI] or 0)
+    for i, c in stall_cols:
+        ST[ln][c] += float(r[i] or 0)
 tw, ti = sum(W.values()), sum(I.values())
 src = open(srcf).read().split("\n")
 print(f"samples {tw:.0f}  warp-instructions {ti:.4g}")
@@ -50,4 +54,10 @@ for reg in filter(None, regions.split(",")):
     lo, hi = map(int, rng.split("-"))
     w = sum(v for k, v in W.items() if lo <= k <= hi)
     i = sum(v for k, v in I.items() if lo <= k <= hi)
-    print(f"region {name:12s} {w / tw * 100:5.1f}% samp {i / ti * 100:5.1f}% inst ({i:.3g})")
+    st = defaultdict(float)
+    for k, d in ST.items():
+        if lo <= k <= hi:
+            for c, v in d.items():
+                st[c] += v
+    tops = ", ".join(f"{c} {v / max(w, 1) * 100:.0f}%" for c, v in sorted(st.items(), key=lambda kv: -kv[1])[:6])
+    print(f"region {name:12s} {w / tw * 100:5.1f}% samp {i / ti * 100:5.1f}% inst ({i:.3g})  [{tops}]")
