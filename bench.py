@@ -96,15 +96,22 @@ class ClockSampler:
         self.index = index
         self.rows: list[list[str]] = []
         self.proc = None
+        self.first = 0
 
     def __enter__(self):
+        # nvidia-smi takes a while to start: wait for its first sample before the
+        # timed region begins, so a short region (cfg2: ~40 ms) is bracketed
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.QUERY}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 10.0 and self.proc.poll() is None:
+                time.sleep(0.01)
+            self.first = max(0, len(self.rows) - 1)  # the last sample before the region
         except FileNotFoundError:
             self.proc = None
         return self
@@ -115,7 +122,10 @@ class ClockSampler:
 
     def __exit__(self, *exc):
         if self.proc:
-            time.sleep(0.25)
+            n0 = len(self.rows)  # and at least one sample taken after it ended
+            t0 = time.time()
+            while len(self.rows) <= n0 and time.time() - t0 < 2.0 and self.proc.poll() is None:
+                time.sleep(0.01)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -123,7 +133,7 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self) -> dict:
-        rows = [r for r in self.rows if len(r) >= 7]
+        rows = [r for r in self.rows[self.first:] if len(r) >= 7]
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
 
