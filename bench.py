@@ -327,11 +327,13 @@ def run_ours(args, cfg) -> dict | None:
         build_gbs = bpb * n / build_s / 1e9 if build_s > 0 else None
         sort_gbs = SORT_BYTES_PER_BODY * n / sort_s / 1e9 if sort_s > 0 else None
         hbm = float(peaks["hbm_gbs"])
-        traffic = None
+        traffic = pipe = None
         tp = os.path.join(ROOT, "profiles", "walk_traffic.json")
         if os.path.exists(tp):
             with open(tp) as f:
-                traffic = json.load(f).get(args.config)
+                wt = json.load(f)
+            traffic = wt.get(args.config)
+            pipe = wt.get("fp32_pipe_active", {}).get(args.config)
         result = {
             "metric": METRIC,
             "value": inter_all / sec,
@@ -360,12 +362,13 @@ def run_ours(args, cfg) -> dict | None:
             "pc_per_step": pc / args.steps,
             "cells": cells,
             "phase_ms_per_step": {k: v / args.steps for k, v in phases.items()},
-            "roofline": {"bound": "fp32", "kernel": "k_walk_f32",
+            "roofline": {"bound": "fp32", "kernel": "k_walk9 (k_walk_f32)",
                          "achieved": walk_tf, "peak": peak_fp32, "unit": "TFLOP/s",
                          "frac": (walk_tf / peak_fp32) if walk_tf else None,
                          "peak_source": "FFMA microbenchmark on this GPU (bh_ffma_peak); MEASURED_PEAKS.json has no FP32 entry",
                          "flops_per_unit": {"pp": FLOPS_PP, "pc": FLOPS_PC},
-                         "traffic": traffic},
+                         "traffic": traffic,
+                         "fp32_pipe_active_ncu": pipe},
             "roofline_build": {"bound": "hbm", "achieved": build_gbs, "peak": hbm, "unit": "GB/s",
                                "frac": build_gbs / hbm if build_gbs else None,
                                "bytes_per_body": bpb, "peak_source": peaks.get("source")},
