@@ -1527,7 +1527,7 @@ int bh_walk_records_defer_f32(bh_handle *h, const void *d_records, int64_t nrec,
   dfr.count = d_count;
   dfr.cap = (int)std::min<int64_t>(cap, 0x7fffffff);
   h->tbegin(BH_PHASE_WALK, s);
-  launch_walk_defer_f32(static_cast<const WalkNode *>(d_records), reinterpret_cast<const float4 *>(d_bodies4),
+  launch_walk_defer_f32(static_cast<const WalkNode *>(d_records), nrec, reinterpret_cast<const float4 *>(d_bodies4),
                         d_targets4, (int)nt, (float)(eps * eps), leaf_size, d_acc4, d_work, h->flags, dfr, false, s);
   h->tend(s);
   h->launches += 1;
@@ -1551,7 +1551,7 @@ int bh_walk_records_resume_f32(bh_handle *h, const void *d_records, int64_t nrec
   dfr.nin = (int)n_entries;
   dfr.fcnc = reinterpret_cast<const int2 *>(d_fcnc);
   h->tbegin(BH_PHASE_WALK, s);
-  launch_walk_defer_f32(static_cast<const WalkNode *>(d_records), reinterpret_cast<const float4 *>(d_bodies4),
+  launch_walk_defer_f32(static_cast<const WalkNode *>(d_records), nrec, reinterpret_cast<const float4 *>(d_bodies4),
                         d_targets4, (int)nt, (float)(eps * eps), leaf_size, d_acc4, d_work, h->flags, dfr, true, s);
   h->tend(s);
   h->launches += 1;

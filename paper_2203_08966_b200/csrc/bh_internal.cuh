@@ -194,8 +194,8 @@ struct DeferArgs {
   int nin = 0;
   const int2 *fcnc = nullptr;
 };
-void launch_walk_defer_f32(const WalkNode *T, const float4 *bodies, const float *targets, int nt, float e2,
-                           int leaf, float *acc, int *work32, DeviceFlags *f, const DeferArgs &dfr,
+void launch_walk_defer_f32(const WalkNode *T, int64_t nrec_max, const float4 *bodies, const float *targets, int nt,
+                           float e2, int leaf, float *acc, int *work32, DeviceFlags *f, const DeferArgs &dfr,
                            bool resume, cudaStream_t s);
 void launch_walk_f64(const WalkParams &p, const double4 *cm64, const double *q64,
                      const int4 *link, const double4 *bodies, const double *targets,

@@ -625,17 +625,23 @@ __device__ __forceinline__ void w9_range(float lo, float hi, float a, float &mn,
   mx = fmaxf(fabsf(gl), fabsf(gh));
 }
 
-template <bool BUCKET>
+template <bool BUCKET, int MODE>
 __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
     const WalkNode *__restrict__ T, const float4 *__restrict__ bodies,
     const float *__restrict__ targets, int tstride, const uint32_t *__restrict__ tperm, int nt,
     float e2, float *__restrict__ acc, int astride, int64_t *__restrict__ work64,
-    int *__restrict__ work32, DeviceFlags *f, int fullmax) {
+    int *__restrict__ work32, DeviceFlags *f, int fullmax, DeferArgs dfr) {
   extern __shared__ int4 w9_smem[];
   W9Warp &S = reinterpret_cast<W9Warp *>(w9_smem)[threadIdx.x >> 5];
   const unsigned lane = threadIdx.x & 31;
   const unsigned FULL = 0xffffffffu;
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int4 entry = make_int4(0, 0, 0, 0);  // kWalkResume: (target chunk, record, mask0, mask1)
+  if (MODE == kWalkResume) {
+    if (gwarp >= dfr.nin) return;  // warp-uniform
+    entry = dfr.in[gwarp];
+  }
+  const int64_t warp = MODE == kWalkResume ? (int64_t)entry.x : gwarp;
   const int64_t t0 = warp * 64 + 2 * lane, t1 = t0 + 1;
   const bool v0 = t0 < nt, v1 = t1 < nt;
   const int64_t s0 = v0 ? (tperm ? (int64_t)tperm[t0] : t0) : 0;
@@ -658,7 +664,14 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
   const unsigned lt = bit - 1u;
 
   int sp = 1, npc = 0, npp = 0;
-  {
+  if (MODE == kWalkResume) {  // the deferred record's subtree, for the targets that opened it
+    const int2 fc = dfr.fcnc[entry.y];
+    if (fc.y <= 0) sp = 0;
+    else if (lane == 0) {
+      S.fc[0] = fc.x | fc.y << kW9NcShift;
+      S.fm[0] = make_uint2((unsigned)entry.z, (unsigned)entry.w);
+    }
+  } else {
     const unsigned m0 = __ballot_sync(FULL, v0), m1 = __ballot_sync(FULL, v1);
     if (lane == 0) {  // root internal: start at its children (flattree.py:271-279)
       const int4 rd = T[0].d;
@@ -790,7 +803,10 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
         if (dmin2 > a.w) to_pc = true;                      // every target accepts
         else if (!(dmax2 > a.w)) {                          // every target opens
           if (d.z > 0) to_fr = true;
-          else to_pp = BUCKET;
+          else if (MODE == kWalkDefer && (d.w & kDeferBit)) {  // subtree not here yet: defer
+            const unsigned slot = atomicAdd(dfr.count, 1u);
+            if (slot < (unsigned)dfr.cap) dfr.out[slot] = make_int4((int)warp, cell, (int)m0, (int)m1);
+          } else to_pp = BUCKET;
         } else to_mx = true;
       }
     }
@@ -818,7 +834,9 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
       S.mxr[slot][0] = a;
       S.mxr[slot][1] = b;
       S.mxr[slot][2] = T[cell].c;
-      S.mxd[slot] = make_int4(d.x, d.y, d.z, (int)m1);
+      // a deferrable record (pass A) keeps its index, flagged by nchild = -1
+      const bool dfr_rec = MODE == kWalkDefer && d.z == 0 && (d.w & kDeferBit);
+      S.mxd[slot] = make_int4(dfr_rec ? cell : d.x, d.y, dfr_rec ? -1 : d.z, (int)m1);
     }
     npp += __popc(bpp);
     npc += __popc(bpc);
@@ -861,6 +879,11 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
           S.fm[sp] = make_uint2(o0, o1);
         }
         ++sp;
+      } else if (MODE == kWalkDefer && dd.z < 0) {
+        if (lane == 0) {
+          const unsigned slot = atomicAdd(dfr.count, 1u);
+          if (slot < (unsigned)dfr.cap) dfr.out[slot] = make_int4((int)warp, dd.x, (int)o0, (int)o1);
+        }
       } else if (BUCKET) {
         if (lane == 0) S.pp[npp] = make_int4(dd.x, dd.y, (int)o0, (int)o1);
         ++npp;
@@ -874,19 +897,35 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
   flush_pc(npc);
   flush_pp(npp);
 
-  if (v0) {
-    float *o = acc + s0 * astride;
-    o[0] = AX.x; o[1] = AY.x; o[2] = AZ.x;
-    const int w = pp0 + 2 * pc0;  // WORK_PP, WORK_PC (octree.py:23-25)
-    if (work64) work64[s0] = w;
-    if (work32) work32[s0] = w;
-  }
-  if (v1) {
-    float *o = acc + s1 * astride;
-    o[0] = AX.y; o[1] = AY.y; o[2] = AZ.y;
-    const int w = pp1 + 2 * pc1;
-    if (work64) work64[s1] = w;
-    if (work32) work32[s1] = w;
+  if (MODE == kWalkResume) {  // add to pass A's results (several entries may share a target)
+    const bool u0 = v0 && ((unsigned)entry.z >> lane & 1u), u1 = v1 && ((unsigned)entry.w >> lane & 1u);
+    if (u0) {
+      float *o = acc + s0 * astride;
+      atomicAdd(o, AX.x); atomicAdd(o + 1, AY.x); atomicAdd(o + 2, AZ.x);
+      if (work32) atomicAdd(work32 + s0, pp0 + 2 * pc0);
+      if (work64) atomicAdd((unsigned long long *)(work64 + s0), (unsigned long long)(pp0 + 2 * pc0));
+    }
+    if (u1) {
+      float *o = acc + s1 * astride;
+      atomicAdd(o, AX.y); atomicAdd(o + 1, AY.y); atomicAdd(o + 2, AZ.y);
+      if (work32) atomicAdd(work32 + s1, pp1 + 2 * pc1);
+      if (work64) atomicAdd((unsigned long long *)(work64 + s1), (unsigned long long)(pp1 + 2 * pc1));
+    }
+  } else {
+    if (v0) {
+      float *o = acc + s0 * astride;
+      o[0] = AX.x; o[1] = AY.x; o[2] = AZ.x;
+      const int w = pp0 + 2 * pc0;  // WORK_PP, WORK_PC (octree.py:23-25)
+      if (work64) work64[s0] = w;
+      if (work32) work32[s0] = w;
+    }
+    if (v1) {
+      float *o = acc + s1 * astride;
+      o[0] = AX.y; o[1] = AY.y; o[2] = AZ.y;
+      const int w = pp1 + 2 * pc1;
+      if (work64) work64[s1] = w;
+      if (work32) work32[s1] = w;
+    }
   }
   const unsigned spp = __reduce_add_sync(FULL, (unsigned)(pp0 + pp1));
   const unsigned spc = __reduce_add_sync(FULL, (unsigned)(pc0 + pc1));
@@ -915,20 +954,29 @@ static int walk9_fullmax() {
   return v;
 }
 
-template <bool BUCKET>
+template <bool BUCKET, int MODE>
 static void launch_walk9(const WalkNode *T, const float4 *bodies, const float *targets, int tstride,
                          const uint32_t *tperm, int nt, float e2, float *acc, int astride, int64_t *work64,
-                         int *work32, DeviceFlags *f, cudaStream_t s) {
+                         int *work32, DeviceFlags *f, const DeferArgs &dfr, cudaStream_t s) {
   const size_t smem = sizeof(W9Warp) * (kW9Block / 32);
   static bool init = false;
   if (!init) {
-    cudaFuncSetAttribute(k_walk9<BUCKET>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_walk9<BUCKET, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     init = true;
   }
-  const int64_t warps = ((int64_t)nt + 63) / 64;
-  k_walk9<BUCKET><<<grid_for(warps * 32, kW9Block), kW9Block, smem, s>>>(T, bodies, targets, tstride, tperm, nt,
-                                                                         e2, acc, astride, work64, work32, f,
-                                                                         walk9_fullmax());
+  const int64_t warps = MODE == kWalkResume ? (int64_t)dfr.nin : ((int64_t)nt + 63) / 64;
+  if (warps <= 0) return;
+  k_walk9<BUCKET, MODE><<<grid_for(warps * 32, kW9Block), kW9Block, smem, s>>>(
+      T, bodies, targets, tstride, tperm, nt, e2, acc, astride, work64, work32, f, walk9_fullmax(), dfr);
+}
+template <int MODE>
+static void launch_walk9_mode(const WalkNode *T, const float4 *bodies, const float *targets, int tstride,
+                              const uint32_t *tperm, int nt, float e2, int leaf, float *acc, int astride,
+                              int64_t *work64, int *work32, DeviceFlags *f, const DeferArgs &dfr, cudaStream_t s) {
+  if (leaf > 1)
+    launch_walk9<true, MODE>(T, bodies, targets, tstride, tperm, nt, e2, acc, astride, work64, work32, f, dfr, s);
+  else
+    launch_walk9<false, MODE>(T, bodies, targets, tstride, tperm, nt, e2, acc, astride, work64, work32, f, dfr, s);
 }
 
 template <int MODE>
@@ -951,18 +999,26 @@ void launch_walk_f32(const WalkNode *T, int64_t nrec_max, const float4 *bodies, 
                      int64_t *work64, int *work32, DeviceFlags *f, cudaStream_t s) {
   if (nt <= 0) return;
   if (walk9_enabled() && nrec_max < (int64_t(1) << kW9NcShift)) {
-    if (leaf > 1) launch_walk9<true>(T, bodies, targets, tstride, tperm, nt, e2, acc, astride, work64, work32, f, s);
-    else launch_walk9<false>(T, bodies, targets, tstride, tperm, nt, e2, acc, astride, work64, work32, f, s);
+    launch_walk9_mode<kWalkFull>(T, bodies, targets, tstride, tperm, nt, e2, leaf, acc, astride, work64, work32,
+                                 f, DeferArgs{}, s);
     return;
   }
   launch_walk_mode<kWalkFull>(T, bodies, targets, tstride, tperm, nt, e2, leaf, acc, astride, work64, work32, f,
                               DeferArgs{}, s);
 }
 
-void launch_walk_defer_f32(const WalkNode *T, const float4 *bodies, const float *targets, int nt, float e2,
-                           int leaf, float *acc, int *work32, DeviceFlags *f, const DeferArgs &dfr,
+void launch_walk_defer_f32(const WalkNode *T, int64_t nrec_max, const float4 *bodies, const float *targets, int nt,
+                           float e2, int leaf, float *acc, int *work32, DeviceFlags *f, const DeferArgs &dfr,
                            bool resume, cudaStream_t s) {
   if (nt <= 0) return;
+  if (walk9_enabled() && nrec_max < (int64_t(1) << kW9NcShift)) {
+    if (resume)
+      launch_walk9_mode<kWalkResume>(T, bodies, targets, 4, nullptr, nt, e2, leaf, acc, 4, nullptr, work32, f, dfr,
+                                     s);
+    else
+      launch_walk9_mode<kWalkDefer>(T, bodies, targets, 4, nullptr, nt, e2, leaf, acc, 4, nullptr, work32, f, dfr, s);
+    return;
+  }
   if (resume)
     launch_walk_mode<kWalkResume>(T, bodies, targets, 4, nullptr, nt, e2, leaf, acc, 4, nullptr, work32, f, dfr, s);
   else
