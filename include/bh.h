@@ -175,6 +175,20 @@ int bh_sim_walk_range(bh_handle *h, double theta, double eps, int leaf_size, int
                       int64_t end, int record_work, void *stream);
 int bh_sim_scatter_work(bh_handle *h, void *stream);
 int bh_sim_end_step(bh_handle *h, double dt, void *stream);
+/* Replicated ranks over NVLink peer memory (replaces the all-reduce of the zone
+ * accelerations and work that follows _BroadcastTreeForces' per-rank walk,
+ * simulation.py:370-416, decomposition.py:35-57): with peers set, walk_range
+ * also stores its rows of acc / work into every peer's resident buffers, so
+ * after a stream-ordered barrier every rank holds the full results.
+ *   ipc_handles : 2 x 64 bytes (cudaIpcMemHandle_t of this handle's resident
+ *                 acc and work buffers; valid until the next sim_load)
+ *   set_peers   : open npeers (<= 7) such handle pairs; npeers = 0 closes them
+ *   set_peer_ptrs: the same from raw device pointers (ranks in one process) */
+int bh_sim_ipc_handles(bh_handle *h, void *out128);
+int bh_sim_set_peers(bh_handle *h, int npeers, const void *handles);
+int bh_sim_set_peer_ptrs(bh_handle *h, int npeers, void *const *acc, void *const *work);
+/* the resident acc / work device buffers (for set_peer_ptrs) */
+int bh_sim_result_ptrs(bh_handle *h, void **acc, void **work);
 /* Copy a Morton-order range [begin, end) of a resident array to/from a caller
  * device buffer: BH_SIM_ACC (4 components per body, handle precision),
  * BH_SIM_POS (export only), BH_SIM_WORK (int32, this pass), BH_SIM_PREV_WORK

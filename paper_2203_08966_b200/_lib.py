@@ -38,6 +38,7 @@ EXPORTS = (
     "bh_sim_load", "bh_sim_forces", "bh_sim_step", "bh_sim_store", "bh_stats_get",
     "bh_sim_begin_step", "bh_sim_prepare", "bh_sim_walk_range", "bh_sim_scatter_work",
     "bh_sim_end_step", "bh_sim_export", "bh_sim_import",
+    "bh_sim_ipc_handles", "bh_sim_set_peers", "bh_sim_set_peer_ptrs", "bh_sim_result_ptrs",
     "bh_sim_local_maxabs", "bh_sim_set_R", "bh_sim_sort", "bh_sim_keys", "bh_sim_load_state",
     "bh_sim_build_local", "bh_sim_branch_export", "bh_sim_walk_records", "bh_walk_records_f32",
     "bh_sim_let", "bh_sim_let_pack", "bh_sim_target_boxes", "bh_sim_step_host",
@@ -106,6 +107,10 @@ def _declare(L: ctypes.CDLL) -> None:
         "bh_sim_prepare": ([P, D, D, I, I, P], I),
         "bh_sim_walk_range": ([P, D, D, I, I64, I64, I, P], I),
         "bh_sim_scatter_work": ([P, P], I),
+        "bh_sim_ipc_handles": ([P, P], I),
+        "bh_sim_set_peers": ([P, I, P], I),
+        "bh_sim_set_peer_ptrs": ([P, I, P, P], I),
+        "bh_sim_result_ptrs": ([P, ctypes.POINTER(P), ctypes.POINTER(P)], I),
         "bh_sim_end_step": ([P, D, P], I),
         "bh_sim_export": ([P, I, I64, I64, P, P], I),
         "bh_sim_import": ([P, I, I64, I64, P, P], I),

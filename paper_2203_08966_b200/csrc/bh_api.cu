@@ -54,6 +54,10 @@ inline cudaStream_t S(void *s) { return static_cast<cudaStream_t>(s); }
 struct bh_handle {
   int device = 0;
   int precision = BH_FP32;
+  // replicated ranks: peers' resident acc / work (bh_sim_set_peers)
+  int npeers = 0;
+  void *peer_acc[kMaxPeers] = {}, *peer_work[kMaxPeers] = {};
+  bool peer_ipc = false;
   DeviceFlags *flags = nullptr;   // device
   DeviceFlags *hflags = nullptr;  // pinned host mirror
   uint32_t *hC = nullptr;         // pinned: off[n-1], newc[n-1]
@@ -167,6 +171,17 @@ struct bh_handle {
     return t;
   }
 };
+
+static void close_peers(bh_handle *h) {
+  if (h->peer_ipc)
+    for (int r = 0; r < h->npeers; ++r) {
+      if (h->peer_acc[r]) cudaIpcCloseMemHandle(h->peer_acc[r]);
+      if (h->peer_work[r]) cudaIpcCloseMemHandle(h->peer_work[r]);
+    }
+  for (int r = 0; r < kMaxPeers; ++r) h->peer_acc[r] = h->peer_work[r] = nullptr;
+  h->npeers = 0;
+  h->peer_ipc = false;
+}
 
 namespace {
 
@@ -547,17 +562,25 @@ int sim_walk(bh_handle *h, double theta, double eps, int leaf, int64_t begin, in
   BH_TRY(reset_counters(h, s));
   h->tbegin(BH_PHASE_WALK, s);
   int *w32 = record_work ? h->work_sorted.as<int>() + begin : nullptr;
+  W9Peers peers;  // the same rows of every peer's buffers (replicated ranks)
+  peers.n = h->npeers;
+  const size_t row = f32 ? sizeof(float4) : sizeof(double4);
+  for (int r = 0; r < h->npeers; ++r) {
+    peers.acc[r] = reinterpret_cast<float *>(static_cast<char *>(h->peer_acc[r]) + row * begin);
+    peers.work[r] = static_cast<int *>(h->peer_work[r]) + begin;
+  }
   if (f32) {
     BH_TRY(ensure_walk_tree(h, theta, leaf, s));
     launch_walk_f32(h->wnodes.as<WalkNode>(), (int64_t)(h->wnodes.bytes / sizeof(WalkNode)), h->pos.as<float4>(),
                     h->pos.as<float>() + 4 * begin, 4, nullptr, (int)nt, (float)(eps * eps), leaf,
-                    h->acc.as<float>() + 4 * begin, 4, nullptr, w32, h->flags, s);
+                    h->acc.as<float>() + 4 * begin, 4, nullptr, w32, h->flags, s, h->npeers ? &peers : nullptr);
   } else {
     WalkParams P;
     fill_walk_params(h, P, nt, theta, eps, leaf);
     launch_walk_f64(P, h->cm64.as<double4>(), h->q64.as<double>(), h->link.as<int4>(),
                     h->pos.as<double4>(), h->pos.as<double>() + 4 * begin, 4, nullptr,
                     h->acc.as<double>() + 4 * begin, 4, nullptr, w32, h->flags, s);
+    if (h->npeers) launch_peer_scatter(h->acc.as<double>() + 4 * begin, row, w32, nt, peers, s);
   }
   h->tend(s);
   h->launches += 1;
@@ -661,6 +684,7 @@ int bh_create(bh_handle **out, int device, int precision) {
 int bh_destroy(bh_handle *h) {
   if (!h) return BH_OK;
   cudaSetDevice(h->device);
+  close_peers(h);
   Buf *bufs[] = {&h->keys, &h->keys2, &h->vals, &h->vals2, &h->sort_tmp, &h->scan_tmp,
                  &h->lcp, &h->newc, &h->off, &h->link, &h->parent, &h->child8, &h->lvl, &h->lvl_list,
                  &h->cm64, &h->q64, &h->smask, &h->nck, &h->wbase, &h->wnodes, &h->wscan_tmp, &h->tbod, &h->pos, &h->pos2,
@@ -1118,6 +1142,60 @@ int bh_sim_walk_range(bh_handle *h, double theta, double eps, int leaf_size, int
   if (!h) return fail(BH_BAD_ARG, "bh_sim_walk_range: bad args");
   if (h->sim_n == 0) return BH_OK;
   return sim_walk(h, theta, eps, leaf_size, begin, end, record_work, S(stream));
+}
+
+int bh_sim_ipc_handles(bh_handle *h, void *out128) {
+  if (!h || !out128 || !h->acc.p || !h->work_sorted.p) return fail(BH_BAD_ARG, "bh_sim_ipc_handles: no state");
+  cudaIpcMemHandle_t a, w;
+  BH_CUDA(cudaIpcGetMemHandle(&a, h->acc.p));
+  BH_CUDA(cudaIpcGetMemHandle(&w, h->work_sorted.p));
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle size");
+  memcpy(out128, &a, 64);
+  memcpy(static_cast<char *>(out128) + 64, &w, 64);
+  return BH_OK;
+}
+
+int bh_sim_set_peers(bh_handle *h, int npeers, const void *handles) {
+  if (!h || npeers < 0 || npeers > kMaxPeers || (npeers && !handles))
+    return fail(BH_BAD_ARG, "bh_sim_set_peers: bad args (at most 7 peers)");
+  BH_CUDA(cudaSetDevice(h->device));
+  close_peers(h);
+  for (int r = 0; r < npeers; ++r) {
+    cudaIpcMemHandle_t a, w;
+    memcpy(&a, static_cast<const char *>(handles) + 128 * r, 64);
+    memcpy(&w, static_cast<const char *>(handles) + 128 * r + 64, 64);
+    void *pa = nullptr, *pw = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&pa, a, cudaIpcMemLazyEnablePeerAccess);
+    if (e == cudaSuccess) e = cudaIpcOpenMemHandle(&pw, w, cudaIpcMemLazyEnablePeerAccess);
+    h->peer_acc[r] = pa;
+    h->peer_work[r] = pw;
+    h->npeers = r + 1;
+    h->peer_ipc = true;
+    if (e != cudaSuccess) {
+      close_peers(h);
+      return fail(BH_CUDA_ERROR, std::string("bh_sim_set_peers: ") + cudaGetErrorString(e));
+    }
+  }
+  return BH_OK;
+}
+
+int bh_sim_set_peer_ptrs(bh_handle *h, int npeers, void *const *acc, void *const *work) {
+  if (!h || npeers < 0 || npeers > kMaxPeers || (npeers && (!acc || !work)))
+    return fail(BH_BAD_ARG, "bh_sim_set_peer_ptrs: bad args (at most 7 peers)");
+  close_peers(h);
+  for (int r = 0; r < npeers; ++r) {
+    h->peer_acc[r] = acc[r];
+    h->peer_work[r] = work[r];
+  }
+  h->npeers = npeers;
+  return BH_OK;
+}
+
+int bh_sim_result_ptrs(bh_handle *h, void **acc, void **work) {
+  if (!h || !acc || !work) return fail(BH_BAD_ARG, "bh_sim_result_ptrs: bad args");
+  *acc = h->acc.p;
+  *work = h->work_sorted.p;
+  return BH_OK;
 }
 
 int bh_sim_scatter_work(bh_handle *h, void *stream) {

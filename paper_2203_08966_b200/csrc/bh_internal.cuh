@@ -178,11 +178,25 @@ void launch_mark_shared(const TreeView &t, uint8_t *shared, int *branch, int *nb
 void launch_branch_export(const TreeView &t, const int *branch, int nb, const int *rec_of_cell,
                           uint64_t *key, int *level, int64_t *count, double *mom, int *rec,
                           int *lo, cudaStream_t s);
+// Replicated-tree ranks (SURVEY §8e stage 1): peer ranks' result buffers,
+// opened over NVLink (cudaIpcOpenMemHandle), already offset to the walked
+// range.  The walk's epilogue stores each target's acceleration and work into
+// every peer as well as locally, so no all-reduce follows the walk.
+constexpr int kMaxPeers = 7;
+struct W9Peers {
+  int n = 0;
+  float *acc[kMaxPeers] = {};
+  int *work[kMaxPeers] = {};
+};
+// copy rows [0, nt) of acc (row_bytes each) and work (int) into every peer
+void launch_peer_scatter(const void *acc, size_t row_bytes, const int *work, int64_t nt, const W9Peers &p,
+                         cudaStream_t s);
 // nrec_max: an upper bound on the records in T (the group-classified walk packs
 // record indices in 28 bits; larger trees take the masked-stack walk)
 void launch_walk_f32(const WalkNode *T, int64_t nrec_max, const float4 *bodies, const float *targets,
                      int tstride, const uint32_t *tperm, int nt, float e2, int leaf, float *acc, int astride,
-                     int64_t *work64, int *work32, DeviceFlags *f, cudaStream_t s);
+                     int64_t *work64, int *work32, DeviceFlags *f, cudaStream_t s,
+                     const W9Peers *peers = nullptr);
 // deferred walk (LET overlap): pass A appends (target chunk, record, m0, m1) to
 // out[cap] for records flagged in d.w; pass B (resume) walks in[nin] with
 // fcnc[record] = (first child, nchild) and adds into acc/work atomically

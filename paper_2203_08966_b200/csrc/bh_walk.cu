@@ -630,7 +630,7 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
     const WalkNode *__restrict__ T, const float4 *__restrict__ bodies,
     const float *__restrict__ targets, int tstride, const uint32_t *__restrict__ tperm, int nt,
     float e2, float *__restrict__ acc, int astride, int64_t *__restrict__ work64,
-    int *__restrict__ work32, DeviceFlags *f, int fullmax, DeferArgs dfr) {
+    int *__restrict__ work32, DeviceFlags *f, int fullmax, DeferArgs dfr, W9Peers peers) {
   extern __shared__ int4 w9_smem[];
   W9Warp &S = reinterpret_cast<W9Warp *>(w9_smem)[threadIdx.x >> 5];
   const unsigned lane = threadIdx.x & 31;
@@ -926,6 +926,19 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
       if (work64) work64[s1] = w;
       if (work32) work32[s1] = w;
     }
+    // replicated ranks: the same rows of every peer's buffers, over NVLink
+    for (int r = 0; r < peers.n; ++r) {
+      if (v0) {
+        float *o = peers.acc[r] + s0 * astride;
+        o[0] = AX.x; o[1] = AY.x; o[2] = AZ.x;
+        if (work32 && peers.work[r]) peers.work[r][s0] = pp0 + 2 * pc0;
+      }
+      if (v1) {
+        float *o = peers.acc[r] + s1 * astride;
+        o[0] = AX.y; o[1] = AY.y; o[2] = AZ.y;
+        if (work32 && peers.work[r]) peers.work[r][s1] = pp1 + 2 * pc1;
+      }
+    }
   }
   const unsigned spp = __reduce_add_sync(FULL, (unsigned)(pp0 + pp1));
   const unsigned spc = __reduce_add_sync(FULL, (unsigned)(pc0 + pc1));
@@ -957,7 +970,8 @@ static int walk9_fullmax() {
 template <bool BUCKET, int MODE>
 static void launch_walk9(const WalkNode *T, const float4 *bodies, const float *targets, int tstride,
                          const uint32_t *tperm, int nt, float e2, float *acc, int astride, int64_t *work64,
-                         int *work32, DeviceFlags *f, const DeferArgs &dfr, cudaStream_t s) {
+                         int *work32, DeviceFlags *f, const DeferArgs &dfr, cudaStream_t s,
+                         const W9Peers &peers) {
   const size_t smem = sizeof(W9Warp) * (kW9Block / 32);
   static bool init = false;
   if (!init) {
@@ -967,16 +981,19 @@ static void launch_walk9(const WalkNode *T, const float4 *bodies, const float *t
   const int64_t warps = MODE == kWalkResume ? (int64_t)dfr.nin : ((int64_t)nt + 63) / 64;
   if (warps <= 0) return;
   k_walk9<BUCKET, MODE><<<grid_for(warps * 32, kW9Block), kW9Block, smem, s>>>(
-      T, bodies, targets, tstride, tperm, nt, e2, acc, astride, work64, work32, f, walk9_fullmax(), dfr);
+      T, bodies, targets, tstride, tperm, nt, e2, acc, astride, work64, work32, f, walk9_fullmax(), dfr, peers);
 }
 template <int MODE>
 static void launch_walk9_mode(const WalkNode *T, const float4 *bodies, const float *targets, int tstride,
                               const uint32_t *tperm, int nt, float e2, int leaf, float *acc, int astride,
-                              int64_t *work64, int *work32, DeviceFlags *f, const DeferArgs &dfr, cudaStream_t s) {
+                              int64_t *work64, int *work32, DeviceFlags *f, const DeferArgs &dfr, cudaStream_t s,
+                              const W9Peers &peers = W9Peers{}) {
   if (leaf > 1)
-    launch_walk9<true, MODE>(T, bodies, targets, tstride, tperm, nt, e2, acc, astride, work64, work32, f, dfr, s);
+    launch_walk9<true, MODE>(T, bodies, targets, tstride, tperm, nt, e2, acc, astride, work64, work32, f, dfr, s,
+                             peers);
   else
-    launch_walk9<false, MODE>(T, bodies, targets, tstride, tperm, nt, e2, acc, astride, work64, work32, f, dfr, s);
+    launch_walk9<false, MODE>(T, bodies, targets, tstride, tperm, nt, e2, acc, astride, work64, work32, f, dfr, s,
+                              peers);
 }
 
 template <int MODE>
@@ -996,15 +1013,38 @@ static void launch_walk_mode(const WalkNode *T, const float4 *bodies, const floa
 
 void launch_walk_f32(const WalkNode *T, int64_t nrec_max, const float4 *bodies, const float *targets,
                      int tstride, const uint32_t *tperm, int nt, float e2, int leaf, float *acc, int astride,
-                     int64_t *work64, int *work32, DeviceFlags *f, cudaStream_t s) {
+                     int64_t *work64, int *work32, DeviceFlags *f, cudaStream_t s, const W9Peers *peers) {
   if (nt <= 0) return;
-  if (walk9_enabled() && nrec_max < (int64_t(1) << kW9NcShift)) {
+  if (walk9_enabled() && nrec_max < (int64_t(1) << kW9NcShift)) {  // peers stored by the epilogue
     launch_walk9_mode<kWalkFull>(T, bodies, targets, tstride, tperm, nt, e2, leaf, acc, astride, work64, work32,
-                                 f, DeferArgs{}, s);
+                                 f, DeferArgs{}, s, peers ? *peers : W9Peers{});
     return;
   }
   launch_walk_mode<kWalkFull>(T, bodies, targets, tstride, tperm, nt, e2, leaf, acc, astride, work64, work32, f,
                               DeferArgs{}, s);
+  if (peers && peers->n > 0) launch_peer_scatter(acc, sizeof(float) * astride, work32, nt, *peers, s);
+}
+
+// rows of the walked range to every peer (the fp64 walk and the v4 fallback):
+// 16-byte vector copies, one grid per peer
+__global__ void k_peer_scatter(const int4 *__restrict__ src, int64_t n16, int4 *__restrict__ dst) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+__global__ void k_peer_scatter_i32(const int *__restrict__ src, int64_t n, int *__restrict__ dst) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+void launch_peer_scatter(const void *acc, size_t row_bytes, const int *work, int64_t nt, const W9Peers &p,
+                         cudaStream_t s) {
+  if (nt <= 0) return;
+  const int64_t n16 = nt * (int64_t)row_bytes / 16;
+  for (int r = 0; r < p.n; ++r) {
+    k_peer_scatter<<<std::min<int64_t>(1184, (n16 + 255) / 256), 256, 0, s>>>(static_cast<const int4 *>(acc), n16,
+                                                                            reinterpret_cast<int4 *>(p.acc[r]));
+    if (work && p.work[r])
+      k_peer_scatter_i32<<<std::min<int64_t>(1184, (nt + 255) / 256), 256, 0, s>>>(work, nt, p.work[r]);
+  }
 }
 
 void launch_walk_defer_f32(const WalkNode *T, int64_t nrec_max, const float4 *bodies, const float *targets, int nt,

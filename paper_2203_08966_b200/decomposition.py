@@ -89,6 +89,13 @@ class Comm:
     def barrier(self) -> None:
         pass
 
+    def stream_barrier(self) -> None:
+        """Every rank's device work queued so far is done before any rank's
+        work queued after this (orders peer-memory stores between ranks)."""
+
+    def allgather_bytes(self, b: bytes) -> list[bytes]:
+        return [b]
+
 
 class TorchComm(Comm):
     """torch.distributed collectives: NCCL on CUDA tensors.  Under a gloo
@@ -141,6 +148,22 @@ class TorchComm(Comm):
     def barrier(self):
         self.dist.barrier(group=self.group)
 
+    def stream_barrier(self):
+        if self.staged:  # host-staged (gloo): the device must be idle first
+            torch.cuda.synchronize()
+            self.dist.barrier(group=self.group)
+            return
+        if getattr(self, "_tick", None) is None:
+            self._tick = torch.zeros(1, dtype=torch.int32, device=torch.cuda.current_device())
+        self.dist.all_reduce(self._tick, group=self.group)  # NCCL: ordered on the current stream
+
+    def allgather_bytes(self, b: bytes) -> list[bytes]:
+        dev = "cpu" if self.staged else torch.device("cuda", torch.cuda.current_device())
+        t = torch.frombuffer(bytearray(b), dtype=torch.uint8).to(dev)
+        outs = [torch.empty_like(t) for _ in range(self.size)]
+        self.dist.all_gather(outs, t, group=self.group)
+        return [bytes(o.cpu().numpy().tobytes()) for o in outs]
+
 
 class _ThreadHub:
     def __init__(self, size: int):
@@ -184,6 +207,17 @@ class ThreadComm(Comm):
     def barrier(self):
         self.hub.barrier.wait()
 
+    def stream_barrier(self):
+        torch.cuda.synchronize()
+        self.hub.barrier.wait()
+
+    def allgather_bytes(self, b):
+        self.hub.slots[self.rank] = b
+        self.hub.barrier.wait()
+        out = list(self.hub.slots)
+        self.hub.barrier.wait()
+        return out
+
 
 # ------------------------------------------------------------------ the driver
 
@@ -210,6 +244,7 @@ class DistributedSim:
         self.p = params
         self.n = 0
         self.zones: list[int] = []
+        self.p2p = False  # results through peer memory (set up by load)
 
     def _bufs(self):
         dev = self.eng.device
@@ -224,6 +259,35 @@ class DistributedSim:
     def load(self, pos, vel, mass=None) -> None:
         self.n = pos.shape[0]
         self.eng.sim_load(pos, vel, mass)
+        self.p2p = self._setup_peers()
+
+    # -- results over peer memory: the walk's epilogue stores its zone's rows
+    # into every rank's resident buffers (NVLink), replacing the all-reduce
+    def _setup_peers(self) -> bool:
+        mode = os.environ.get("BH_P2P", "auto")
+        size = self.comm.size
+        if mode == "0" or size == 1 or size > 8 or not hasattr(self.eng, "sim_set_peers"):
+            return False
+        me = self.comm.rank
+        try:
+            if isinstance(self.comm, ThreadComm):  # ranks in one process: raw device pointers
+                ptrs = self.comm.allgather_bytes(self.eng.sim_result_ptrs())
+                self.eng.sim_set_peer_ptrs([ptrs[q] for q in range(size) if q != me])
+            else:
+                hs = self.comm.allgather_bytes(self.eng.sim_ipc_handles())
+                self.eng.sim_set_peers([hs[q] for q in range(size) if q != me])
+            ok = 1
+        except (ValueError, RuntimeError):
+            ok = 0
+        flag = torch.tensor([ok], dtype=torch.int64, device=self.eng.device)
+        self.comm.allreduce_sum_(flag)
+        if int(flag.item()) != size:  # some rank could not map its peers: all-reduce path
+            if ok:
+                self.eng.sim_set_peers([])
+            if mode == "1":
+                raise RuntimeError("BH_P2P=1: peer buffers could not be mapped on every rank")
+            return False
+        return True
 
     def _zone(self) -> tuple[int, int]:
         _, _, prev = self._bufs()
@@ -236,6 +300,13 @@ class DistributedSim:
         p = self.p
         self.eng.sim_prepare(p.theta, p.eps, p.leaf_size, bounds_ready)
         b, e = self._zone()
+        if getattr(self, "p2p", False):
+            self.comm.stream_barrier()  # every rank is done reading its acc (the kick)
+            self.eng.sim_walk_range(p.theta, p.eps, p.leaf_size, b, e, record_work)  # + peers' rows
+            self.comm.stream_barrier()  # every rank's rows have landed
+            if record_work:
+                self.eng.sim_scatter_work()
+            return
         self.eng.sim_walk_range(p.theta, p.eps, p.leaf_size, b, e, record_work)
         acc, work, _ = self._bufs()
         acc.zero_()
@@ -252,6 +323,25 @@ class DistributedSim:
     def bootstrap(self) -> None:
         """simulation.py:487: forces for the first kick, work not recorded."""
         self._forces(record_work=False, bounds_ready=False)
+        if getattr(self, "p2p", False) and not self._replicas_agree():
+            # peer stores did not land everywhere: fall back to the all-reduce
+            if os.environ.get("BH_P2P") == "1":
+                raise RuntimeError("BH_P2P=1: ranks disagree after the peer-memory walk")
+            self.eng.sim_set_peers([])
+            self.p2p = False
+            self._forces(record_work=False, bounds_ready=False)
+
+    def _replicas_agree(self) -> bool:
+        """Every rank holds bit-identical accelerations (a digest of the bit
+        patterns, compared by max and -min over ranks)."""
+        acc, _, _ = self._bufs()
+        self.eng.sim_export(_lib.BH_SIM_ACC, 0, self.n, acc)
+        bits = acc.view(torch.int32).reshape(-1).to(torch.int64)
+        w = torch.arange(bits.shape[0], device=bits.device, dtype=torch.int64) % 1021 + 1
+        d = (bits * w).sum()
+        mm = torch.stack([d, -d])
+        self.comm.allreduce_max_(mm)
+        return bool((mm[0] == -mm[1]).item())
 
     def step(self, steps: int = 1) -> None:
         for _ in range(steps):

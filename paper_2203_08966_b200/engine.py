@@ -232,6 +232,31 @@ class Engine:
         check(self._L.bh_sim_walk_range(self._h, float(theta), float(eps), int(leaf_size),
                                         int(begin), int(end), int(bool(record_work)), self.stream))
 
+    # ---- replicated ranks over NVLink peer memory (bh_sim_set_peers)
+    def sim_ipc_handles(self) -> bytes:
+        """128 bytes: IPC handles of this engine's resident acc and work buffers."""
+        buf = ctypes.create_string_buffer(128)
+        check(self._L.bh_sim_ipc_handles(self._h, buf))
+        return buf.raw
+
+    def sim_set_peers(self, handles: list[bytes]) -> None:
+        """Open the peers' acc/work buffers; walk_range then stores into them too."""
+        blob = b"".join(handles)
+        buf = ctypes.create_string_buffer(blob, len(blob)) if blob else None
+        check(self._L.bh_sim_set_peers(self._h, len(handles), buf))
+
+    def sim_result_ptrs(self) -> tuple[int, int]:
+        a, w = ctypes.c_void_p(), ctypes.c_void_p()
+        check(self._L.bh_sim_result_ptrs(self._h, ctypes.byref(a), ctypes.byref(w)))
+        return a.value, w.value
+
+    def sim_set_peer_ptrs(self, ptrs: list[tuple[int, int]]) -> None:
+        """Same-process ranks: the peers' (acc, work) device pointers."""
+        k = len(ptrs)
+        acc = (ctypes.c_void_p * max(k, 1))(*[a for a, _ in ptrs])
+        work = (ctypes.c_void_p * max(k, 1))(*[w for _, w in ptrs])
+        check(self._L.bh_sim_set_peer_ptrs(self._h, k, acc, work))
+
     def sim_scatter_work(self) -> None:
         check(self._L.bh_sim_scatter_work(self._h, self.stream))
 

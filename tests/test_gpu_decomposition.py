@@ -36,7 +36,7 @@ def _run(precision, ranks, b, steps, theta=0.6, eps=1e-3, leaf=16, dt=1e-3):
             w = torch.empty(len(b), dtype=torch.int64, device="cuda")
             sim.store(pos=p, work=w)
             eng.check()
-            out[r] = (p[:, :3].double().cpu().numpy(), w.cpu().numpy(), list(sim.zones))
+            out[r] = (p[:, :3].double().cpu().numpy(), w.cpu().numpy(), list(sim.zones), sim.p2p)
             eng.close()
         except Exception as e:  # pragma: no cover - surfaced below
             err.append(e)
@@ -52,15 +52,20 @@ def _run(precision, ranks, b, steps, theta=0.6, eps=1e-3, leaf=16, dt=1e-3):
     return out
 
 
+@pytest.mark.parametrize("p2p", ["0", "1"])
 @pytest.mark.parametrize("precision", ["fp64", "fp32"])
-def test_emulated_ranks_match_single_gpu(precision):
+def test_emulated_ranks_match_single_gpu(precision, p2p, monkeypatch):
+    """p2p=1: results reach the other ranks through the walk's peer stores
+    (raw device pointers here) instead of an all-reduce."""
     from paper_2203_08966_b200.initcond import make_rng, plummer_cluster
 
+    monkeypatch.setenv("BH_P2P", p2p)
     b = plummer_cluster(20_000, make_rng(1))
     single = _run(precision, 1, b, 3)[0]
     for ranks in (2, 3):
         multi = _run(precision, ranks, b, 3)
-        for pos, work, zones in multi:
+        for pos, work, zones, used in multi:
+            assert used == (p2p == "1")
             assert len(zones) == ranks + 1
             if precision == "fp64":
                 np.testing.assert_array_equal(pos, single[0])
@@ -70,7 +75,7 @@ def test_emulated_ranks_match_single_gpu(precision):
                 assert rel < 1e-5, rel
                 assert np.mean(work != single[1]) < 1e-3
         # all ranks hold the same replicated state
-        for pos, work, _ in multi[1:]:
+        for pos, work, _, _ in multi[1:]:
             np.testing.assert_array_equal(pos, multi[0][0])
 
 
@@ -216,12 +221,12 @@ def test_target_boxes_match_numpy():
     eng.close()
 
 
-def _simulate_worker(rank, port, scheme, out_path):
+def _simulate_worker(rank, port, scheme, out_path, p2p="0"):
     import torch.distributed as dist
 
     from paper_2203_08966_b200.simulation import SimConfig, simulate
 
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), BH_P2P=p2p)
     torch.cuda.set_device(0)  # both ranks share the one GPU; gloo collectives are host-staged
     dist.init_process_group("gloo", rank=rank, world_size=2)
     cfg = SimConfig(n=24_000, algorithm=1, theta=0.6, dt=1e-3, steps=3, eps=1e-3, seed=4, leaf_size=16,
@@ -233,10 +238,12 @@ def _simulate_worker(rank, port, scheme, out_path):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("scheme", ["distributed", "replicated"])
-def test_simulate_devices2_matches_one_device(tmp_path, scheme):
+@pytest.mark.parametrize("scheme,p2p", [("distributed", "0"), ("replicated", "0"), ("replicated", "1")])
+def test_simulate_devices2_matches_one_device(tmp_path, scheme, p2p):
     """simulate(devices=2) through torch.distributed (two processes sharing this
-    GPU, gloo): the same per-body work as devices=1, positions to fp32 rounding."""
+    GPU, gloo): the same per-body work as devices=1, positions to fp32 rounding.
+    replicated + p2p=1: each process opens the other's result buffers by CUDA
+    IPC handle and the walk stores its rows into them (must succeed)."""
     import socket
 
     import torch.multiprocessing as mp
@@ -247,7 +254,7 @@ def test_simulate_devices2_matches_one_device(tmp_path, scheme):
         s_.bind(("127.0.0.1", 0))
         port = s_.getsockname()[1]
     out = str(tmp_path / "r.npz")
-    mp.spawn(_simulate_worker, args=(port, scheme, out), nprocs=2, join=True)
+    mp.spawn(_simulate_worker, args=(port, scheme, out, p2p), nprocs=2, join=True)
     got = np.load(out)
     ref = simulate(SimConfig(n=24_000, algorithm=1, theta=0.6, dt=1e-3, steps=3, eps=1e-3, seed=4, leaf_size=16,
                              precision="fp32", leaf_mode="bucket"))
