@@ -927,7 +927,10 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
       if (work32) work32[s1] = w;
     }
     // replicated ranks: the same rows of every peer's buffers, over NVLink
-    for (int r = 0; r < peers.n; ++r) {
+    // (static indices: the parameter struct is not copied to local memory)
+#pragma unroll
+    for (int r = 0; r < kMaxPeers; ++r) {
+      if (r >= peers.n) break;
       if (v0) {
         float *o = peers.acc[r] + s0 * astride;
         o[0] = AX.x; o[1] = AY.x; o[2] = AZ.x;
