@@ -183,7 +183,9 @@ int bh_sim_end_step(bh_handle *h, double dt, void *stream);
  *   ipc_handles : 2 x 64 bytes (cudaIpcMemHandle_t of this handle's resident
  *                 acc and work buffers; valid until the next sim_load)
  *   set_peers   : open npeers (<= 7) such handle pairs; npeers = 0 closes them
- *   set_peer_ptrs: the same from raw device pointers (ranks in one process) */
+ *   set_peer_ptrs: the same from raw device pointers (ranks in one process)
+ * A load that reallocates the result buffers invalidates the mapping: walk_range
+ * then fails (BH_BAD_ARG) until every rank sets its peers again. */
 int bh_sim_ipc_handles(bh_handle *h, void *out128);
 int bh_sim_set_peers(bh_handle *h, int npeers, const void *handles);
 int bh_sim_set_peer_ptrs(bh_handle *h, int npeers, void *const *acc, void *const *work);

@@ -58,6 +58,7 @@ struct bh_handle {
   int npeers = 0;
   void *peer_acc[kMaxPeers] = {}, *peer_work[kMaxPeers] = {};
   bool peer_ipc = false;
+  void *peer_own_acc = nullptr, *peer_own_work = nullptr;  // our buffers when the peers mapped them
   DeviceFlags *flags = nullptr;   // device
   DeviceFlags *hflags = nullptr;  // pinned host mirror
   uint32_t *hC = nullptr;         // pinned: off[n-1], newc[n-1]
@@ -562,6 +563,8 @@ int sim_walk(bh_handle *h, double theta, double eps, int leaf, int64_t begin, in
   BH_TRY(reset_counters(h, s));
   h->tbegin(BH_PHASE_WALK, s);
   int *w32 = record_work ? h->work_sorted.as<int>() + begin : nullptr;
+  if (h->npeers && (h->acc.p != h->peer_own_acc || h->work_sorted.p != h->peer_own_work))
+    return fail(BH_BAD_ARG, "result buffers reallocated since the peers mapped them: set peers again");
   W9Peers peers;  // the same rows of every peer's buffers (replicated ranks)
   peers.n = h->npeers;
   const size_t row = f32 ? sizeof(float4) : sizeof(double4);
@@ -1171,6 +1174,8 @@ int bh_sim_set_peers(bh_handle *h, int npeers, const void *handles) {
     h->peer_work[r] = pw;
     h->npeers = r + 1;
     h->peer_ipc = true;
+    h->peer_own_acc = h->acc.p;
+    h->peer_own_work = h->work_sorted.p;
     if (e != cudaSuccess) {
       close_peers(h);
       return fail(BH_CUDA_ERROR, std::string("bh_sim_set_peers: ") + cudaGetErrorString(e));
@@ -1188,6 +1193,8 @@ int bh_sim_set_peer_ptrs(bh_handle *h, int npeers, void *const *acc, void *const
     h->peer_work[r] = work[r];
   }
   h->npeers = npeers;
+  h->peer_own_acc = h->acc.p;
+  h->peer_own_work = h->work_sorted.p;
   return BH_OK;
 }
 
