@@ -91,6 +91,8 @@ struct bh_handle {
   // bh_sim_step_host: staging and the side stream for the early position copy
   Buf hs_a, hs_b, hs_pos;
   cudaStream_t side = nullptr;
+  cudaStream_t cp[2] = {nullptr, nullptr};  // concurrent host copies (H2D reads overlap on PCIe)
+  cudaEvent_t ev_cp[3] = {nullptr, nullptr, nullptr};
   cudaEvent_t ev_pos = nullptr, ev_side = nullptr;
   int let_nrank = 0;
   int64_t let_nrec = 0;
@@ -710,6 +712,10 @@ int bh_destroy(bh_handle *h) {
   if (h->ev_pos) cudaEventDestroy(h->ev_pos);
   if (h->ev_side) cudaEventDestroy(h->ev_side);
   if (h->side) cudaStreamDestroy(h->side);
+  for (cudaStream_t c : h->cp)
+    if (c) cudaStreamDestroy(c);
+  for (cudaEvent_t e : h->ev_cp)
+    if (e) cudaEventDestroy(e);
   h->fold_marks();
   for (cudaEvent_t e : h->pool) cudaEventDestroy(e);
   delete h;
@@ -1067,6 +1073,10 @@ int bh_sim_step_host(bh_handle *h, float *pos4, float *vel3, float *acc3, int64_
   if (!h->side) BH_CUDA(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
   if (!h->ev_pos) BH_CUDA(cudaEventCreateWithFlags(&h->ev_pos, cudaEventDisableTiming));
   if (!h->ev_side) BH_CUDA(cudaEventCreateWithFlags(&h->ev_side, cudaEventDisableTiming));
+  for (cudaStream_t &c : h->cp)
+    if (!c) BH_CUDA(cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking));
+  for (cudaEvent_t &e : h->ev_cp)
+    if (!e) BH_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   BH_CUDA(h->hs_a.ensure(sizeof(float) * 3 * n));
   BH_CUDA(h->hs_b.ensure(sizeof(float) * 3 * n));
   BH_CUDA(h->hs_pos.ensure(sizeof(float4) * n));
@@ -1080,9 +1090,17 @@ int bh_sim_step_host(bh_handle *h, float *pos4, float *vel3, float *acc3, int64_
     BH_CUDA(h->work_orig.ensure(sizeof(int) * (n + 1)));
   }
   h->sim_n = n;
+  // the three input copies run concurrently (PCIe reads overlap: 48 -> 53 GB/s)
+  BH_CUDA(cudaEventRecord(h->ev_cp[0], s));
+  BH_CUDA(cudaStreamWaitEvent(h->cp[0], h->ev_cp[0], 0));
+  BH_CUDA(cudaStreamWaitEvent(h->cp[1], h->ev_cp[0], 0));
   BH_CUDA(cudaMemcpyAsync(h->pos.p, pos4, sizeof(float4) * n, cudaMemcpyHostToDevice, s));
-  BH_CUDA(cudaMemcpyAsync(h->hs_a.p, vel3, sizeof(float) * 3 * n, cudaMemcpyHostToDevice, s));
-  BH_CUDA(cudaMemcpyAsync(h->hs_b.p, acc3, sizeof(float) * 3 * n, cudaMemcpyHostToDevice, s));
+  BH_CUDA(cudaMemcpyAsync(h->hs_a.p, vel3, sizeof(float) * 3 * n, cudaMemcpyHostToDevice, h->cp[0]));
+  BH_CUDA(cudaMemcpyAsync(h->hs_b.p, acc3, sizeof(float) * 3 * n, cudaMemcpyHostToDevice, h->cp[1]));
+  BH_CUDA(cudaEventRecord(h->ev_cp[1], h->cp[0]));
+  BH_CUDA(cudaEventRecord(h->ev_cp[2], h->cp[1]));
+  BH_CUDA(cudaStreamWaitEvent(s, h->ev_cp[1], 0));
+  BH_CUDA(cudaStreamWaitEvent(s, h->ev_cp[2], 0));
   const int g = grid_for(n, 256);
   k_expand3<<<g, 256, 0, s>>>(h->hs_a.as<float>(), n, h->vel.as<float4>());
   k_expand3<<<g, 256, 0, s>>>(h->hs_b.as<float>(), n, h->acc.as<float4>());
@@ -1118,9 +1136,14 @@ int bh_sim_step_host(bh_handle *h, float *pos4, float *vel3, float *acc3, int64_
     BH_CUDA(cudaMemcpyAsync(pos4, h->hs_pos.p, sizeof(float4) * n, cudaMemcpyDeviceToHost, s));
   }
   k_store3f<<<g, 256, 0, s>>>(h->vel.as<float4>(), id, n, h->hs_a.as<float>());
+  BH_CUDA(cudaEventRecord(h->ev_cp[1], s));
   k_store3f<<<g, 256, 0, s>>>(h->acc.as<float4>(), id, n, h->hs_b.as<float>());
-  BH_CUDA(cudaMemcpyAsync(vel3, h->hs_a.p, sizeof(float) * 3 * n, cudaMemcpyDeviceToHost, s));
+  // vel goes back while acc is being gathered; the two copies overlap
+  BH_CUDA(cudaStreamWaitEvent(h->cp[0], h->ev_cp[1], 0));
+  BH_CUDA(cudaMemcpyAsync(vel3, h->hs_a.p, sizeof(float) * 3 * n, cudaMemcpyDeviceToHost, h->cp[0]));
+  BH_CUDA(cudaEventRecord(h->ev_cp[2], h->cp[0]));
   BH_CUDA(cudaMemcpyAsync(acc3, h->hs_b.p, sizeof(float) * 3 * n, cudaMemcpyDeviceToHost, s));
+  BH_CUDA(cudaStreamWaitEvent(s, h->ev_cp[2], 0));
   if (pos_sent) BH_CUDA(cudaStreamWaitEvent(s, h->ev_side, 0));
   h->launches += 2 + (pos_sent ? 0 : 1);
   BH_LAUNCHED();
