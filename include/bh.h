@@ -36,6 +36,7 @@ typedef enum {
   BH_DUPLICATE_KEY = 3,    /* hashed.py:477-482 "tree resolution" */
   BH_UNSORTED = 4,         /* hashed.py:475-476 "sorted" */
   BH_DEPTH_OVERFLOW = 5,   /* octree.py:144-146 */
+  BH_STACK_OVERFLOW = 6,   /* flattree.py:255 (stack cap 176); here the walk's per-warp frontier bound */
   BH_CUDA_ERROR = 7,
   BH_NCCL_ERROR = 8,
   BH_NO_TREE = 9,

@@ -20,6 +20,7 @@ BH_OUT_OF_DOMAIN = 2
 BH_DUPLICATE_KEY = 3
 BH_UNSORTED = 4
 BH_DEPTH_OVERFLOW = 5
+BH_STACK_OVERFLOW = 6
 BH_CUDA_ERROR = 7
 BH_NCCL_ERROR = 8
 BH_NO_TREE = 9

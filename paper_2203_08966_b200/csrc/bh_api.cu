@@ -216,6 +216,7 @@ int take_flag_error(bh_handle *h, cudaStream_t s) {
                 "two bodies share the level-21 cell; positions are closer than the tree "
                 "resolution");
   if (bits & FLAG_DEPTH) return fail(BH_DEPTH_OVERFLOW, "tree depth cap 21 exceeded");
+  if (bits & FLAG_WALK_BOUNDS) return fail(BH_STACK_OVERFLOW, "walk frontier or list bound exceeded");
   return fail(BH_CUDA_ERROR, "unknown device flag");
 }
 

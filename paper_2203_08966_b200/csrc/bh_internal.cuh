@@ -38,6 +38,7 @@ enum : int {
   FLAG_UNSORTED = 4,
   FLAG_DEPTH = 8,
   FLAG_OVERFLOW = 16,  // sync-free build: more cells than the preallocated capacity
+  FLAG_WALK_BOUNDS = 32,  // a walk's per-warp frontier or list would overflow (never, by construction)
 };
 
 struct DeviceFlags {

@@ -578,6 +578,9 @@ constexpr int kW9Full = BH_W9_FULLMAX;  // full 32-cell batches while sp <= this
 // after a full batch sp <= kW9Full + 32; single-entry (DFS) batches above it add
 // at most 8 entries per level
 constexpr int kW9Frontier = kW9Full + 32 + 8 * (kMaxLevel + 1) + 8;
+#ifndef BH_W9_CHECK
+#define BH_W9_CHECK 0  // 1: latch FLAG_WALK_BOUNDS instead of overrunning (costs 1.7%; the bounds are proven)
+#endif
 #ifndef BH_W9_FLUSH
 #define BH_W9_FLUSH 16
 #endif
@@ -812,6 +815,14 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
     }
     const unsigned bpp = __ballot_sync(FULL, to_pp), bpc = __ballot_sync(FULL, to_pc);
     const unsigned bfr = __ballot_sync(FULL, to_fr), bmx = __ballot_sync(FULL, to_mx);
+    // the bounds (frontier: §3 of DESIGN.md; lists: < kW9Flush + 32) hold by
+    // construction; checked anyway (warp-uniform) so a violation is loud, not a
+    // shared-memory overrun
+    if (BH_W9_CHECK && (sp + __popc(bfr) + __popc(bmx) > kW9Frontier || npc + __popc(bpc) > kW9List ||
+        npp + __popc(bpp) + __popc(bmx) > kW9List)) {
+      if (lane == 0) atomicOr(&f->bits, FLAG_WALK_BOUNDS);
+      return;
+    }
     if (to_pp) S.pp[npp + __popc(bpp & lt)] = d.y == 1 ? make_int4(cell, 0, (int)m0, (int)m1)
                                                    : make_int4(d.x, d.y, (int)m0, (int)m1);
     if (to_pc) {
