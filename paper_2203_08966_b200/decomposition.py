@@ -208,7 +208,8 @@ class ThreadComm(Comm):
         self.hub.barrier.wait()
 
     def stream_barrier(self):
-        torch.cuda.synchronize()
+        if torch.cuda.is_available():
+            torch.cuda.synchronize()
         self.hub.barrier.wait()
 
     def allgather_bytes(self, b):

@@ -76,3 +76,33 @@ class OracleEngine:
                 dst.copy_(torch.from_numpy(out))
         if work is not None:
             work.copy_(torch.from_numpy(self.work_orig.astype(np.int64)))
+
+
+class PeerOracleEngine(OracleEngine):
+    """OracleEngine whose walk also stores its rows into peer engines' result
+    arrays (the CPU stand-in for bh_sim_set_peer_ptrs' NVLink peer stores).
+    ``drop`` > 0 loses that many rows per peer store (a broken mapping)."""
+
+    def __init__(self, drop=0):
+        self.peers = []
+        self.drop = drop
+
+    def sim_result_ptrs(self):
+        return self
+
+    def sim_set_peer_ptrs(self, peers):
+        self.peers = list(peers)
+
+    def sim_set_peers(self, handles):  # IPC form: not used by in-process ranks
+        if handles:
+            raise RuntimeError("no IPC in the CPU fake")
+        self.peers = []
+
+    def sim_walk_range(self, theta, eps, leaf, b, e, record_work=True):
+        super().sim_walk_range(theta, eps, leaf, b, e, record_work)
+        for q in self.peers:
+            hi = max(b, e - self.drop)
+            q.acc[b:hi] = self.acc[b:hi]
+            if record_work:
+                q.work_sorted[b:hi] = self.work_sorted[b:hi]
+

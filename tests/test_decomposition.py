@@ -195,3 +195,73 @@ def test_lcp_matches_key_prefix_levels():
             else:
                 break
         assert _lcp(a, b) == shared, (a, b)
+
+
+def _thread_ranks(engines, steps, n=600):
+    """DistributedSim on in-process ranks (ThreadComm) with the given engines."""
+    import threading
+
+    from paper_2203_08966_b200.decomposition import DistributedSim, StepParams, ThreadComm
+    from paper_2203_08966_b200.initcond import make_rng, plummer_cluster
+
+    b = plummer_cluster(n, make_rng(3))
+    comms = ThreadComm.group(len(engines))
+    out, err = [None] * len(engines), []
+
+    def body(r):
+        try:
+            sim = DistributedSim(engines[r], comms[r], StepParams(0.6, 0.05, 1, 0.01))
+            pos = torch.from_numpy(np.c_[b.position, b.mass])
+            sim.load(pos, torch.from_numpy(np.c_[b.velocity, np.zeros(n)]), torch.from_numpy(b.mass))
+            sim.bootstrap()
+            sim.step(steps)
+            p = torch.empty((n, 4), dtype=torch.float64)
+            w = torch.empty(n, dtype=torch.int64)
+            sim.store(pos=p, work=w)
+            out[r] = (p[:, :3].numpy(), w.numpy(), sim.p2p)
+        except Exception as e:  # pragma: no cover - surfaced below
+            err.append(e)
+            comms[r].hub.barrier.abort()
+
+    ts = [threading.Thread(target=body, args=(r,)) for r in range(len(engines))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=300)
+    if err:
+        raise err[0]
+    return out
+
+
+def test_peer_store_protocol_matches_allreduce(monkeypatch):
+    """Replicated ranks whose walk stores into the peers (BH_P2P auto) give the
+    same trajectory, bit for bit, as the all-reduce exchange (BH_P2P=0)."""
+    from fake_engine import OracleEngine, PeerOracleEngine
+
+    monkeypatch.setenv("BH_P2P", "auto")
+    p2p = _thread_ranks([PeerOracleEngine(), PeerOracleEngine()], 2)
+    monkeypatch.setenv("BH_P2P", "0")
+    ar = _thread_ranks([OracleEngine(), OracleEngine()], 2)
+    for (pa, wa, used), (pb, wb, _) in zip(p2p, ar):
+        assert used
+        np.testing.assert_array_equal(pa, pb)
+        np.testing.assert_array_equal(wa, wb)
+
+
+def test_peer_store_failure_falls_back(monkeypatch):
+    """Peer stores that do not land (rows dropped) are caught by the bootstrap
+    digest check; the ranks fall back to the all-reduce and stay exact.  With
+    BH_P2P=1 the same failure raises."""
+    from fake_engine import OracleEngine, PeerOracleEngine
+
+    monkeypatch.setenv("BH_P2P", "auto")
+    got = _thread_ranks([PeerOracleEngine(drop=5), PeerOracleEngine(drop=5)], 1)
+    monkeypatch.setenv("BH_P2P", "0")
+    ref = _thread_ranks([OracleEngine(), OracleEngine()], 1)
+    for (pa, wa, used), (pb, wb, _) in zip(got, ref):
+        assert not used
+        np.testing.assert_array_equal(pa, pb)
+        np.testing.assert_array_equal(wa, wb)
+    monkeypatch.setenv("BH_P2P", "1")
+    with pytest.raises(RuntimeError, match="disagree"):
+        _thread_ranks([PeerOracleEngine(drop=5), PeerOracleEngine(drop=5)], 1)
