@@ -271,7 +271,9 @@ __global__ void k_emit(TreeView t, const float4 *__restrict__ bod32,
   for (int l = start + 1; l <= depth; ++l) {
     const int c = base + (l - start - 1);
     t.parent[c] = par;
-    t.child8[8 * (int64_t)par + (int)((k >> (3 * (kMortonBits - l))) & 7)] = c;
+    // a leaf child is stored as -(c + 2): the moments read no link word for it
+    const bool leafc = l == depth && ln != kMaxLevel;
+    t.child8[8 * (int64_t)par + (int)((k >> (3 * (kMortonBits - l))) & 7)] = leafc ? -(c + 2) : c;
     if (l == depth && ln == kMaxLevel) {  // first body of a duplicate-key run
       const int64_t end = run_end(t.keys, n, i, k, 0);
       const int skip = end < n ? 1 + (int)t.off[end] : C;
@@ -362,7 +364,12 @@ __device__ void dup_cell_moments(const TreeView &t, int p) {
 __device__ void cell_moments8(const TreeView &t, int p, double (*xs)[11]) {
   const int lane = threadIdx.x & 31, s = lane & 7, g0 = lane & ~7;
   int c = -1;
-  if (p >= 0) c = t.child8[8 * (int64_t)p + s];
+  bool leafc = false;
+  if (p >= 0) {
+    c = t.child8[8 * (int64_t)p + s];
+    leafc = c < -1;  // leaf child, stored as -(c + 2)
+    if (leafc) c = -c - 2;
+  }
   const unsigned have = (__ballot_sync(0xffffffffu, c >= 0) >> g0) & 0xffu;
   const bool cell = p >= 0 && have != 0u;
   if (p >= 0 && have == 0u && s == 0) dup_cell_moments(t, p);  // duplicate-key cell
@@ -370,7 +377,7 @@ __device__ void cell_moments8(const TreeView &t, int p, double (*xs)[11]) {
   bool hasq = false;
   if (c >= 0) {
     cm = t.cm64[c];
-    hasq = t.link[c].y > 1;  // leaves keep quad = 0 (flattree.py:207-208)
+    hasq = !leafc;  // leaves keep quad = 0 (flattree.py:207-208); other cells hold > 1 body
   }
   const double m = cm.w;
   const bool use = c >= 0 && m != 0.0;
@@ -583,6 +590,9 @@ __global__ void k_export(TreeView t, double R, uint64_t *key, int8_t *level, dou
   if (children) {
     const int4 *row = reinterpret_cast<const int4 *>(t.child8 + 8 * c);
     int4 r0 = row[0], r1 = row[1];
+    auto dec = [](int v) { return v < -1 ? -v - 2 : v; };  // leaf children are stored as -(c + 2)
+    r0 = make_int4(dec(r0.x), dec(r0.y), dec(r0.z), dec(r0.w));
+    r1 = make_int4(dec(r1.x), dec(r1.y), dec(r1.z), dec(r1.w));
     int32_t *o = children + 8 * c;
     o[0] = r0.x; o[1] = r0.y; o[2] = r0.z; o[3] = r0.w;
     o[4] = r1.x; o[5] = r1.y; o[6] = r1.z; o[7] = r1.w;
@@ -623,8 +633,9 @@ __global__ void k_mark_shared(TreeView t, uint8_t *__restrict__ shared, int *__r
     const uint64_t k = t.keys[side == 0 ? 0 : t.n - 1];
     int cur = 0;
     for (int l = 1; l <= bnd && l <= kMaxLevel; ++l) {
-      const int c = t.child8[8 * (int64_t)cur + (int)((k >> (3 * (kMortonBits - l))) & 7)];
-      if (c < 0) break;
+      int c = t.child8[8 * (int64_t)cur + (int)((k >> (3 * (kMortonBits - l))) & 7)];
+      if (c == -1) break;
+      if (c < -1) c = -c - 2;  // a leaf child
       if (!shared[c]) {
         shared[c] = 1;
         list[ns++] = c;
@@ -640,7 +651,8 @@ __global__ void k_mark_shared(TreeView t, uint8_t *__restrict__ shared, int *__r
   for (int q = 0; q < ns; ++q) {
     const int c = list[q];
     for (int s = 0; s < 8; ++s) {
-      const int ch = t.child8[8 * (int64_t)c + s];
+      int ch = t.child8[8 * (int64_t)c + s];
+      if (ch < -1) ch = -ch - 2;  // a leaf child
       if (ch >= 0 && !shared[ch]) branch[nb++] = ch;
     }
   }
