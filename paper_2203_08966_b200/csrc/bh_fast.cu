@@ -1,9 +1,9 @@
 // bh_fast.cu -- fp32 kernels (FMA contraction allowed): bounds reduction,
-// the fp32 warp-cooperative traversal, the fused integrator, body gathers, and
-// the radix-sort / scan wrappers.
+// the fused integrator, body gathers, and the radix-sort / scan wrappers.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <climits>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
@@ -15,22 +15,42 @@ namespace bh {
 // ---------------------------------------------------------------- bounds
 __device__ __forceinline__ unsigned fabs_bits(float a) { return __float_as_uint(fabsf(a)); }
 
-__device__ __forceinline__ void warp_max_to(unsigned m, unsigned *dst) {
+// one atomic per block (a per-warp atomic on one address serialises in L2:
+// 3e6 of them at 1e8 bodies)
+__device__ __forceinline__ void block_max_to(unsigned m, unsigned *dst) {
+  __shared__ unsigned wm[32];
   m = __reduce_max_sync(0xffffffffu, m);
-  if ((threadIdx.x & 31) == 0 && m) atomicMax(dst, m);
+  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    unsigned v = threadIdx.x < (blockDim.x >> 5) ? wm[threadIdx.x] : 0u;
+    v = __reduce_max_sync(0xffffffffu, v);
+    if (threadIdx.x == 0 && v) atomicMax(dst, v);
+  }
+}
+// grid for the streaming kernels: a few resident waves, grid-stride inside
+static inline int stream_grid(int64_t n) {
+  static int g = 0;
+  if (g == 0) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    g = sms * 8;
+  }
+  const int64_t need = (n + 255) / 256;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(need, g));
 }
 
 // morton.py:39-42: max |x| over all bodies and axes (float bits are
 // order-preserving for non-negative floats; NaN sorts above +inf and makes R
 // NaN, which the key kernel then reports as out of domain)
 __global__ void k_maxabs_f32(const float4 *__restrict__ p, int64_t n, DeviceFlags *f) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   unsigned m = 0;
-  if (i < n) {
-    float4 v = p[i];
-    m = max(fabs_bits(v.x), max(fabs_bits(v.y), fabs_bits(v.z)));
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = p[i];
+    m = max(m, max(fabs_bits(v.x), max(fabs_bits(v.y), fabs_bits(v.z))));
   }
-  warp_max_to(m, &f->maxabs_bits);
+  block_max_to(m, &f->maxabs_bits);
 }
 
 __global__ void k_reset_bounds(DeviceFlags *f) {
@@ -41,7 +61,7 @@ void launch_reset_flags_bounds(DeviceFlags *f, cudaStream_t s) { k_reset_bounds<
 
 void launch_maxabs_f32(const float4 *pos, int64_t n, DeviceFlags *f, cudaStream_t s) {
   if (n <= 0) return;
-  k_maxabs_f32<<<grid_for(n, 256), 256, 0, s>>>(pos, n, f);
+  k_maxabs_f32<<<stream_grid(n), 256, 0, s>>>(pos, n, f);
 }
 
 // ------------------------------------------------------------ integrator
@@ -74,9 +94,8 @@ void launch_drift_f32(float4 *pos, const float4 *vel, int64_t n, float dt, cudaS
 __global__ void k_kick_drift_max_f32(float4 *__restrict__ pos, float4 *__restrict__ vel,
                                      const float4 *__restrict__ acc, int64_t n, float h,
                                      float dt, DeviceFlags *f) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   unsigned m = 0;
-  if (i < n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     float4 x = pos[i];
     if (dt != 0.f) {
       float4 v = vel[i];
@@ -88,14 +107,14 @@ __global__ void k_kick_drift_max_f32(float4 *__restrict__ pos, float4 *__restric
       x.x += v.x * dt; x.y += v.y * dt; x.z += v.z * dt;
       pos[i] = x;
     }
-    m = max(fabs_bits(x.x), max(fabs_bits(x.y), fabs_bits(x.z)));
+    m = max(m, max(fabs_bits(x.x), max(fabs_bits(x.y), fabs_bits(x.z))));
   }
-  warp_max_to(m, &f->maxabs_bits);
+  block_max_to(m, &f->maxabs_bits);
 }
 void launch_kick_drift_max_f32(float4 *pos, float4 *vel, const float4 *acc, int64_t n,
                                float h, float dt, DeviceFlags *f, cudaStream_t s) {
   if (n <= 0) return;
-  k_kick_drift_max_f32<<<grid_for(n, 256), 256, 0, s>>>(pos, vel, acc, n, h, dt, f);
+  k_kick_drift_max_f32<<<stream_grid(n), 256, 0, s>>>(pos, vel, acc, n, h, dt, f);
 }
 
 // ---------------------------------------------------------------- gathers
