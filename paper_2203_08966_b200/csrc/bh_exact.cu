@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <climits>
 #include <cooperative_groups.h>
 
@@ -154,8 +155,9 @@ __global__ void k_lcp_new(const uint64_t *__restrict__ keys, int64_t n,
   __shared__ int h[kMaxLevel + 2];
   if (threadIdx.x <= kMaxLevel + 1) h[threadIdx.x] = 0;
   __syncthreads();
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) {
+  // grid-stride: the per-level counts leave each block once (global atomics on
+  // 22 addresses from every block of a one-body-per-thread grid serialise in L2)
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
   uint64_t k = keys[i];
   int lp = -1, ln = -1;
   if (i > 0) lp = lcp_of(keys[i - 1], k);
@@ -190,8 +192,15 @@ void launch_lcp_new(const uint64_t *keys, int64_t n, int8_t *lcp, uint32_t *newc
                     int bnd_next) {
   if (n <= 0) return;
   cudaMemsetAsync(lvl_cnt, 0, sizeof(int) * (kMaxLevel + 1), s);
-  k_lcp_new<<<grid_for(n, 256), 256, 0, s>>>(keys, n, lcp, newc, f, lvl_cnt, allow_dup, bnd_prev,
-                                             bnd_next);
+  static int g = 0;
+  if (g == 0) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    g = sms * 8;
+  }
+  const int blocks = (int)std::min<int64_t>(g, (n + 255) / 256);
+  k_lcp_new<<<blocks, 256, 0, s>>>(keys, n, lcp, newc, f, lvl_cnt, allow_dup, bnd_prev, bnd_next);
 }
 
 // first b > i whose level-l prefix differs from body i's (n if none):
