@@ -85,6 +85,23 @@ __global__ void k_nchild(TreeView t, int leaf, const uint8_t *force,
   nck[c] = (kept && expandable(t, c, leaf, force)) ? (uint32_t)__popc(smask[c]) : 0u;
 }
 
+// children per reachable internal cell from the child8 rows (leaf children are
+// stored as -(c + 2), absent as -1).  Without shared-cell flags a cell that can
+// be opened has a parent that can be opened (counts grow up the tree), so no
+// reachability test is needed.
+__global__ void k_nchild_rows(TreeView t, int leaf, uint32_t *__restrict__ nck) {
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= t.C) return;
+  uint32_t k = 0u;
+  if (c < tree_count(t) && expandable(t, c, leaf, nullptr)) {
+    const int4 *row = reinterpret_cast<const int4 *>(t.child8 + 8 * c);
+    const int4 r0 = row[0], r1 = row[1];
+    k = (r0.x != -1) + (r0.y != -1) + (r0.z != -1) + (r0.w != -1) + (r1.x != -1) + (r1.y != -1) +
+        (r1.z != -1) + (r1.w != -1);
+  }
+  nck[c] = k;
+}
+
 __global__ void k_compact(TreeView t, const double *__restrict__ dR, double theta, int leaf,
                           const uint8_t *force, const uint32_t *__restrict__ smask,
                           const uint32_t *__restrict__ nck, const uint32_t *__restrict__ base,
@@ -101,8 +118,22 @@ __global__ void k_compact(TreeView t, const double *__restrict__ dR, double thet
       if (rec_of_cell) rec_of_cell[c] = -1;
       return;
     }
-    const int slot = child_slot(t, c);
-    j = 1 + (int)base[P] + __popc(smask[P] & ((1u << slot) - 1u));
+    if (smask) {
+      const int slot = child_slot(t, c);
+      j = 1 + (int)base[P] + __popc(smask[P] & ((1u << slot) - 1u));
+    } else {  // rank among the parent's present children, from its child8 row
+      const int4 *row = reinterpret_cast<const int4 *>(t.child8 + 8 * (int64_t)P);
+      const int4 r0 = row[0], r1 = row[1];
+      const int v[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+      const int cl = -(int)c - 2;  // a leaf child is stored as -(c + 2)
+      int rank = 0;
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        if (v[s] == (int)c || v[s] == cl) break;
+        rank += v[s] != -1;
+      }
+      j = 1 + (int)base[P] + rank;
+    }
   }
   const int4 L = t.link[c];
   const double4 cm = t.cm64[c];
@@ -134,6 +165,12 @@ void launch_walk_tree(const TreeView &t, const double *dR, double theta, int lea
                       size_t scan_bytes, WalkNode *out, int *dCp, cudaStream_t s,
                       const uint8_t *force, int *rec_of_cell, int *wparent) {
   const int g = grid_for(t.C, 256);
+  if (!force) {  // children counted and ranked from the child8 rows: no slot-mask pass
+    k_nchild_rows<<<g, 256, 0, s>>>(t, leaf, nck);
+    exclusive_scan_u32(scan_tmp, scan_bytes, nck, base, t.C, s);
+    k_compact<<<g, 256, 0, s>>>(t, dR, theta, leaf, force, nullptr, nck, base, out, dCp, rec_of_cell, wparent);
+    return;
+  }
   cudaMemsetAsync(smask, 0, sizeof(uint32_t) * t.C, s);
   k_slots<<<g, 256, 0, s>>>(t, leaf, force, smask);
   k_nchild<<<g, 256, 0, s>>>(t, leaf, force, smask, nck);
