@@ -277,7 +277,7 @@ int build_sorted(bh_handle *h, int64_t n, const float4 *bod32, const double4 *bo
   BH_CUDA(h->child8.ensure(sizeof(int) * 8 * C));
   BH_CUDA(cudaMemsetAsync(h->child8.p, 0xFF, sizeof(int) * 8 * C, s));
   BH_CUDA(h->cm64.ensure(sizeof(double4) * C));
-  BH_CUDA(h->q64.ensure(sizeof(double) * 6 * C));
+  BH_CUDA(h->q64.ensure(sizeof(double) * kQStride * C));
   h->walk_valid = false;
   if (n == 0) {  // hashed.py:459-462: an empty root
     int4 root = make_int4(1, 0, 0, 0);
@@ -330,7 +330,7 @@ int build_sorted_async(bh_handle *h, int64_t n, const float4 *bod32, cudaStream_
   BH_CUDA(h->lvl_list.ensure(sizeof(int) * cap));
   BH_CUDA(h->child8.ensure(sizeof(int) * 8 * cap));
   BH_CUDA(h->cm64.ensure(sizeof(double4) * cap));
-  BH_CUDA(h->q64.ensure(sizeof(double) * 6 * cap));
+  BH_CUDA(h->q64.ensure(sizeof(double) * kQStride * cap));
   BH_CUDA(cudaMemsetAsync(h->child8.p, 0xFF, sizeof(int) * 8 * cap, s));
   h->C = cap;
   h->tree_n = n;

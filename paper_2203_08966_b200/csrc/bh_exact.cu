@@ -334,7 +334,7 @@ __device__ void dup_cell_moments(const TreeView &t, int p) {
     cy += b.w * b.y;
     cz += b.w * b.z;
   }
-  double2 *q2o = reinterpret_cast<double2 *>(t.q64 + 6 * (int64_t)p);
+  double2 *q2o = reinterpret_cast<double2 *>(t.q64 + kQStride * (int64_t)p);
   if (total == 0.0) {
     t.cm64[p] = make_double4(0.0, 0.0, 0.0, 0.0);
     q2o[0] = q2o[1] = q2o[2] = make_double2(0.0, 0.0);
@@ -414,7 +414,7 @@ __device__ void cell_moments8(const TreeView &t, int p, double (*xs)[11]) {
     if (use) {
       double q0 = 0.0, q1 = 0.0, q2 = 0.0, q3 = 0.0, q4 = 0.0, q5 = 0.0;
       if (hasq) {
-        const double2 *qc = reinterpret_cast<const double2 *>(t.q64 + 6 * (int64_t)c);
+        const double2 *qc = reinterpret_cast<const double2 *>(t.q64 + kQStride * (int64_t)c);
         const double2 a = qc[0], b = qc[1], d = qc[2];
         q0 = a.x; q1 = a.y; q2 = b.x; q3 = b.y; q4 = d.x; q5 = d.y;
       }
@@ -432,7 +432,7 @@ __device__ void cell_moments8(const TreeView &t, int p, double (*xs)[11]) {
   mine[5] = t0; mine[6] = t1; mine[7] = t2; mine[8] = t3; mine[9] = t4; mine[10] = t5;
   __syncwarp();
   if (cell && s == 0) {
-    double *qo = t.q64 + 6 * (int64_t)p;
+    double *qo = t.q64 + kQStride * (int64_t)p;
     if (total == 0.0) {
       t.cm64[p] = make_double4(0.0, 0.0, 0.0, 0.0);
       for (int k = 0; k < 6; ++k) qo[k] = 0.0;
@@ -448,6 +448,7 @@ __device__ void cell_moments8(const TreeView &t, int p, double (*xs)[11]) {
       q2o[0] = make_double2(qxx, qxy);
       q2o[1] = make_double2(qxz, qyy);
       q2o[2] = make_double2(qyz, qzz);
+      q2o[3] = make_double2(0.0, 0.0);  // pad: whole-sector write
     }
   }
   __syncwarp();
@@ -593,7 +594,7 @@ __global__ void k_export(TreeView t, double R, uint64_t *key, int8_t *level, dou
   if (mass) mass[c] = cm.w;
   if (com) { com[3 * c] = cm.x; com[3 * c + 1] = cm.y; com[3 * c + 2] = cm.z; }
   if (quad) {
-    for (int k = 0; k < 6; ++k) quad[6 * c + k] = L.y > 1 ? t.q64[6 * c + k] : 0.0;
+    for (int k = 0; k < 6; ++k) quad[6 * c + k] = L.y > 1 ? t.q64[kQStride * c + k] : 0.0;
   }
   if (count) count[c] = t.n == 0 ? 0 : L.y;
   if (children) {
@@ -691,7 +692,7 @@ __global__ void k_branch_export(TreeView t, const int *__restrict__ branch, int 
   const double4 cm = t.cm64[c];
   double *m = mom + 10 * (int64_t)k;
   m[0] = cm.w; m[1] = cm.x; m[2] = cm.y; m[3] = cm.z;
-  for (int q = 0; q < 6; ++q) m[4 + q] = L.y > 1 ? t.q64[6 * (int64_t)c + q] : 0.0;
+  for (int q = 0; q < 6; ++q) m[4 + q] = L.y > 1 ? t.q64[kQStride * (int64_t)c + q] : 0.0;
   rec[k] = rec_of_cell ? rec_of_cell[c] : -1;
   if (lo) lo[k] = L.z;
 }
@@ -769,7 +770,7 @@ __global__ void __launch_bounds__(128) k_walk_f64(
       }
       next = i + 1;
     } else if (d2 > 0.0 && P.side64[L.w] < P.theta * sqrt(d2)) {
-      const double *q = q64 + 6 * (int64_t)i;
+      const double *q = q64 + kQStride * (int64_t)i;
       const double r1 = sqrt(d2);
       const double qrx = q[0] * dx + q[1] * dy + q[2] * dz;
       const double qry = q[1] * dx + q[3] * dy + q[4] * dz;

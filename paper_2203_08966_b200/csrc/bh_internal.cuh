@@ -10,7 +10,7 @@
 //   link    int4[C]  {skip, count, lo, level}: skip = index after the subtree
 //                    (pre-order), count = bodies below, lo = first sorted body
 //   parent  i32[C], child8 i32[C][8] (slot order), level-bucketed cell list
-//   cm64    double4[C] {com, mass}, q64 double[C][6]           fp64 moments
+//   cm64    double4[C] {com, mass}, q64 double[C][kQStride] (6 used) fp64 moments
 //   wnodes  WalkNode[C'] 64-byte fp32 walk records of the cells a walk with
 //                    leaf size L can reach, children contiguous (bh_walk.cu)
 //
@@ -30,6 +30,9 @@ namespace bh {
 constexpr int kMortonBits = 21;
 constexpr int kMaxLevel = 21;
 constexpr int kWarp = 32;
+// quadrupole row stride in doubles: 8 (64-byte aligned rows: whole-sector reads
+// and writes; 6 are used)
+constexpr int kQStride = 8;
 
 // device error flag bits (latched, reported by bh_check / build)
 enum : int {

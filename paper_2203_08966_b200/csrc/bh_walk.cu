@@ -143,7 +143,7 @@ __global__ void k_compact(TreeView t, const double *__restrict__ dR, double thet
   nd.a = make_float4(-(float)cm.x, -(float)cm.y, -(float)cm.z, (float)(r * r));
   float q0 = 0.f, q1 = 0.f, q2 = 0.f, q3 = 0.f, q4 = 0.f, q5 = 0.f;
   if (L.y > 1) {
-    const double *q = t.q64 + 6 * c;
+    const double *q = t.q64 + kQStride * c;
     q0 = (float)q[0]; q1 = (float)q[1]; q2 = (float)q[2];
     q3 = (float)q[3]; q4 = (float)q[4]; q5 = (float)q[5];
   }
