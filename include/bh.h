@@ -92,6 +92,12 @@ int bh_morton_f64(bh_handle *h, const double *d_pos3, int64_t n, const double *d
 int bh_sort(bh_handle *h, const uint64_t *d_keys, int64_t n, uint64_t *d_keys_sorted,
             int64_t *d_perm, void *stream);
 
+/* The single-pass u32 prefix sum the build uses (cells per body -> pre-order
+ * offsets, hashed.py:489 `1 + depth[0] + sum(depth - lcp)`): exclusive
+ * (inclusive != 0: inclusive) scan of d_in into d_out, mod 2^32. */
+int bh_scan_u32(bh_handle *h, const uint32_t *d_in, int64_t n, uint32_t *d_out, int inclusive,
+                void *stream);
+
 /* hashed.py:448-515 build_hashed over Morton-sorted bodies (moments included).
  * The tree stays in the handle.  Synchronises once (cell count). */
 int bh_build_f32(bh_handle *h, const float *d_pos4_sorted, int64_t n, const double *d_R,
@@ -271,6 +277,8 @@ int bh_timing_get(bh_handle *h, double *ms_out, int nphases);
 /* FP32 FFMA throughput microbenchmark (the roofline denominator for the walk):
  * runs a dependent-chain-free FFMA loop on every SM, returns TFLOP/s. */
 int bh_ffma_peak(bh_handle *h, double *tflops_out, void *stream);
+/* The same loop in fp64 (DFMA): the roofline denominator of the fp64 walk. */
+int bh_dfma_peak(bh_handle *h, double *tflops_out, void *stream);
 
 #ifdef __cplusplus
 }

@@ -69,6 +69,8 @@ def lib():
         L.or_from_sources.restype = None
         L.or_potential.argtypes = [P, P, I64, D]
         L.or_potential.restype = D
+        L.or_ic_plummer.argtypes = [P, I64, I64, D, P, P, ctypes.POINTER(I64)]
+        L.or_ic_plummer.restype = I64
         L.or_num_threads.argtypes = []
         L.or_num_threads.restype = ctypes.c_int
         _lib = L
@@ -260,3 +262,51 @@ def leapfrog(mass, pos, vel, dt: float, steps: int, theta: float, eps: float,
         a, work = tree_accelerations(m, x, theta, eps, leaf_size)
         v += a * (0.5 * dt)
     return x, v, a, work
+
+
+# ------------------------------------------------------------ initcond.py
+# Inputs for bench.py's reference arm, generated without the product library.
+
+
+def make_rng(seed: int) -> np.random.Generator:
+    """initcond.py:27-29."""
+    return np.random.Generator(np.random.Philox(key=seed))
+
+
+def plummer_cluster(n: int, rng: np.random.Generator, total_mass: float = 1.0):
+    """initcond.py:62-77 -> (mass (n,), pos (n,3), vel (n,3)) fp64, consuming the
+    same draws from ``rng`` as the reference (or_ic_plummer)."""
+    if n < 1:
+        raise ValueError(f"cluster needs at least one body, got n={n}")
+    mass = np.full(n, total_mass / n)
+    pos = np.empty((n, 3))
+    vel = np.empty((n, 3))
+    done = 0
+    chunk = 1 << 20
+    while done < n:
+        want = min(n - done, chunk)
+        state = rng.bit_generator.state
+        buf = rng.random(40 * want + 4096)
+        used = ctypes.c_int64()
+        got = lib().or_ic_plummer(_p(buf), len(buf), want, float(total_mass), _p(pos[done:]),
+                                  _p(vel[done:]), ctypes.byref(used))
+        rng.bit_generator.state = state  # consume exactly the completed bodies' draws
+        if used.value:
+            rng.random(used.value)
+        if got == 0:
+            raise RuntimeError("draw buffer too small for one body")
+        done += got
+    return mass, pos, vel
+
+
+def colliding_plummers(n_per_cluster: int, seed: int, total_mass: float = 1.0,
+                       offset=(10.0, 2.0, 0.0), bulk=(0.3, 0.0, 0.0)):
+    """BASELINE.json configs 0 and 3: two Plummer clusters from one stream, the
+    first at +offset moving -bulk."""
+    rng = make_rng(seed)
+    ma, pa, va = plummer_cluster(n_per_cluster, rng, total_mass)
+    mb, pb, vb = plummer_cluster(n_per_cluster, rng, total_mass)
+    off = np.asarray(offset, dtype=np.float64)
+    v = np.asarray(bulk, dtype=np.float64)
+    return (np.concatenate([ma, mb]), np.concatenate([pa + off, pb - off]),
+            np.concatenate([va - v, vb + v]))

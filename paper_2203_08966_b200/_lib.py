@@ -32,7 +32,7 @@ BH_FP64 = 1
 #: every symbol include/bh.h declares (checked by tests/test_abi.py)
 EXPORTS = (
     "bh_create", "bh_destroy", "bh_last_error", "bh_version", "bh_check",
-    "bh_bounds_f32", "bh_bounds_f64", "bh_morton_f32", "bh_morton_f64", "bh_sort",
+    "bh_bounds_f32", "bh_bounds_f64", "bh_morton_f32", "bh_morton_f64", "bh_sort", "bh_scan_u32",
     "bh_build_f32", "bh_build_f64", "bh_tree_size", "bh_set_allow_duplicates", "bh_export_tree",
     "bh_traverse_f32", "bh_traverse_f64", "bh_kick_f32", "bh_drift_f32",
     "bh_kick_f64", "bh_drift_f64", "bh_direct_f64", "bh_potential_f64",
@@ -44,7 +44,7 @@ EXPORTS = (
     "bh_sim_build_local", "bh_sim_branch_export", "bh_sim_walk_records", "bh_walk_records_f32",
     "bh_sim_let", "bh_sim_let_pack", "bh_sim_target_boxes", "bh_sim_step_host",
     "bh_walk_records_defer_f32", "bh_walk_records_resume_f32",
-    "bh_timing_enable", "bh_timing_reset", "bh_timing_get", "bh_ffma_peak",
+    "bh_timing_enable", "bh_timing_reset", "bh_timing_get", "bh_ffma_peak", "bh_dfma_peak",
     "bh_ic_plummer", "bh_host_potential_pairs",
 )
 BH_SIM_ACC, BH_SIM_WORK, BH_SIM_PREV_WORK, BH_SIM_POS, BH_SIM_VEL, BH_SIM_ID, BH_SIM_KEYS = range(7)
@@ -86,6 +86,7 @@ def _declare(L: ctypes.CDLL) -> None:
         "bh_morton_f32": ([P, P, I64, P, P, P], I),
         "bh_morton_f64": ([P, P, I64, P, P, P], I),
         "bh_sort": ([P, P, I64, P, P, P], I),
+        "bh_scan_u32": ([P, P, I64, P, I, P], I),
         "bh_build_f32": ([P, P, I64, P, P], I),
         "bh_build_f64": ([P, P, P, I64, P, P], I),
         "bh_tree_size": ([P, ctypes.POINTER(I64)], I),
@@ -134,6 +135,7 @@ def _declare(L: ctypes.CDLL) -> None:
         "bh_timing_reset": ([P], I),
         "bh_timing_get": ([P, ctypes.POINTER(D), I], I),
         "bh_ffma_peak": ([P, ctypes.POINTER(D), P], I),
+        "bh_dfma_peak": ([P, ctypes.POINTER(D), P], I),
         "bh_ic_plummer": ([P, I64, I64, D, P, P, ctypes.POINTER(I64)], I64),
         "bh_host_potential_pairs": ([P, P, I64, D], D),
     }

@@ -24,6 +24,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", INCLUDE
 UNITS = {
     "bh_exact.cu": ["-fmad=false"],
     "bh_fast.cu": [],
+    "bh_sort.cu": [],
     "bh_walk.cu": ["-ftz=true"],
     "bh_api.cu": [],
     "bh_host.cpp": ["-Xcompiler", "-ffp-contract=off", "-x", "cu"],

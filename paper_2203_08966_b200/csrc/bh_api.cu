@@ -235,6 +235,7 @@ int sort_keys(bh_handle *h, int64_t n, cudaStream_t s) {
   BH_CUDA(sort_pairs(h->sort_tmp.p, h->sort_tmp.bytes, h->keys.as<uint64_t>(),
                      h->keys2.as<uint64_t>(), h->vals.as<uint32_t>(), h->vals2.as<uint32_t>(),
                      n, s));
+  h->launches += sort_launches();
   return BH_OK;
 }
 
@@ -784,6 +785,16 @@ int bh_sort(bh_handle *h, const uint64_t *d_keys, int64_t n, uint64_t *d_keys_so
                             cudaMemcpyDeviceToDevice, s));
   launch_iota64(d_perm, h->vals2.as<uint32_t>(), n, s);
   BH_LAUNCHED();
+  return BH_OK;
+}
+
+int bh_scan_u32(bh_handle *h, const uint32_t *d_in, int64_t n, uint32_t *d_out, int inclusive, void *stream) {
+  if (!h || n < 0 || (n && (!d_in || !d_out))) return fail(BH_BAD_ARG, "bh_scan_u32: bad args");
+  if (n == 0) return BH_OK;
+  BH_CUDA(h->scan_tmp.ensure(scan_temp_bytes(n) + 16));
+  if (inclusive) BH_CUDA(inclusive_scan_u32(h->scan_tmp.p, h->scan_tmp.bytes, d_in, d_out, n, S(stream)));
+  else BH_CUDA(exclusive_scan_u32(h->scan_tmp.p, h->scan_tmp.bytes, d_in, d_out, n, S(stream)));
+  h->launches += 1;
   return BH_OK;
 }
 
@@ -1793,8 +1804,7 @@ int bh_timing_get(bh_handle *h, double *ms_out, int nphases) {
   return BH_OK;
 }
 
-int bh_ffma_peak(bh_handle *h, double *tflops_out, void *stream) {
-  if (!h || !tflops_out) return fail(BH_BAD_ARG, "bh_ffma_peak: bad args");
+static int fma_peak(bh_handle *h, bool fp64, double *tflops_out, void *stream) {
   cudaStream_t s = S(stream);
   int sms = 0;
   BH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
@@ -1804,10 +1814,12 @@ int bh_ffma_peak(bh_handle *h, double *tflops_out, void *stream) {
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   double flops = 0.0;
-  const int iters = 1 << 14;
-  run_ffma(out.as<float>(), sms, iters, &flops, s);  // warm-up
-  cudaEventRecord(a, s);
-  run_ffma(out.as<float>(), sms, iters, &flops, s);
+  const int iters = fp64 ? 1 << 12 : 1 << 14;
+  for (int k = 0; k < 2; ++k) {  // warm-up, then timed
+    if (k) cudaEventRecord(a, s);
+    if (fp64) run_dfma(out.as<double>(), sms, iters, &flops, s);
+    else run_ffma(out.as<float>(), sms, iters, &flops, s);
+  }
   cudaEventRecord(b, s);
   BH_LAUNCHED();
   BH_CUDA(cudaEventSynchronize(b));
@@ -1818,6 +1830,14 @@ int bh_ffma_peak(bh_handle *h, double *tflops_out, void *stream) {
   out.release();
   *tflops_out = flops / (ms * 1e-3) / 1e12;
   return BH_OK;
+}
+int bh_ffma_peak(bh_handle *h, double *tflops_out, void *stream) {
+  if (!h || !tflops_out) return fail(BH_BAD_ARG, "bh_ffma_peak: bad args");
+  return fma_peak(h, false, tflops_out, stream);
+}
+int bh_dfma_peak(bh_handle *h, double *tflops_out, void *stream) {
+  if (!h || !tflops_out) return fail(BH_BAD_ARG, "bh_dfma_peak: bad args");
+  return fma_peak(h, true, tflops_out, stream);
 }
 
 }  // extern "C"

@@ -1,12 +1,10 @@
 // bh_fast.cu -- fp32 kernels (FMA contraction allowed): bounds reduction,
-// the fused integrator, body gathers, and the radix-sort / scan wrappers.
+// the fused integrator and body gathers (radix sort and scans: bh_sort.cu).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include <algorithm>
 #include <climits>
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_scan.cuh>
 
 #include "bh_internal.cuh"
 
@@ -165,8 +163,9 @@ void launch_iota64(int64_t *out, const uint32_t *vals, int64_t n, cudaStream_t s
 // --------------------------------------------------- FFMA peak microbench
 // 8 independent FFMA chains per thread, 8 warps x 4 blocks per SM: the FP32
 // pipe's sustained issue rate at the current clock (walk roofline denominator)
-__global__ void __launch_bounds__(256) k_ffma(float *out, int iters, float a, float b) {
-  float x[8];
+template <class T>
+__global__ void __launch_bounds__(256) k_ffma(T *out, int iters, T a, T b) {
+  T x[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) x[k] = threadIdx.x * 1e-3f + k;
   for (int i = 0; i < iters; ++i) {
@@ -176,46 +175,21 @@ __global__ void __launch_bounds__(256) k_ffma(float *out, int iters, float a, fl
       for (int k = 0; k < 8; ++k) x[k] = fmaf(x[k], a, b);
     }
   }
-  float sum = 0.f;
+  T sum = 0;
 #pragma unroll
   for (int k = 0; k < 8; ++k) sum += x[k];
-  if (sum == 1234.5f) out[0] = sum;
+  if (sum == (T)1234.5) out[0] = sum;
 }
 void run_ffma(float *out, int sms, int iters, double *flops, cudaStream_t s) {
   const int blocks = sms * 4, threads = 256;
-  k_ffma<<<blocks, threads, 0, s>>>(out, iters, 0.999999f, 1e-7f);
+  k_ffma<float><<<blocks, threads, 0, s>>>(out, iters, 0.999999f, 1e-7f);
   *flops = 2.0 * 64.0 * (double)iters * blocks * threads;
 }
-
-// ------------------------------------------------------- sort / scan (CUB)
-size_t sort_temp_bytes(int64_t n) {
-  size_t bytes = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint64_t *)nullptr, (uint64_t *)nullptr,
-                                  (const uint32_t *)nullptr, (uint32_t *)nullptr, (int)n, 0, 63);
-  return bytes;
-}
-cudaError_t sort_pairs(void *temp, size_t temp_bytes, const uint64_t *kin, uint64_t *kout,
-                       const uint32_t *vin, uint32_t *vout, int64_t n, cudaStream_t s) {
-  return cub::DeviceRadixSort::SortPairs(temp, temp_bytes, kin, kout, vin, vout, (int)n, 0, 63, s);
-}
-size_t scan_temp_bytes(int64_t n) {
-  size_t bytes = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, bytes, (const uint32_t *)nullptr, (uint32_t *)nullptr,
-                                (int)n);
-  return bytes;
-}
-cudaError_t exclusive_scan_u32(void *temp, size_t temp_bytes, const uint32_t *in, uint32_t *out,
-                               int64_t n, cudaStream_t s) {
-  return cub::DeviceScan::ExclusiveSum(temp, temp_bytes, in, out, (int)n, s);
-}
-size_t inclusive_scan_temp_bytes(int64_t n) {
-  size_t bytes = 0;
-  cub::DeviceScan::InclusiveSum(nullptr, bytes, (const uint32_t *)nullptr, (uint32_t *)nullptr, (int)n);
-  return bytes;
-}
-cudaError_t inclusive_scan_u32(void *temp, size_t temp_bytes, const uint32_t *in, uint32_t *out,
-                               int64_t n, cudaStream_t s) {
-  return cub::DeviceScan::InclusiveSum(temp, temp_bytes, in, out, (int)n, s);
+// the same loop in fp64 (DFMA): the roofline denominator of the fp64 walk
+void run_dfma(double *out, int sms, int iters, double *flops, cudaStream_t s) {
+  const int blocks = sms * 4, threads = 256;
+  k_ffma<double><<<blocks, threads, 0, s>>>(out, iters, 0.999999, 1e-7);
+  *flops = 2.0 * 64.0 * (double)iters * blocks * threads;
 }
 
 }  // namespace bh

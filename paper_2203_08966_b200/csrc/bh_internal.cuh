@@ -66,8 +66,11 @@ struct Buf {
     bytes = 0;
     size_t grow = want + want / 8 + 256;
     cudaError_t e = cudaMalloc(&p, grow);
-    if (e == cudaSuccess) bytes = grow;
-    return e;
+    if (e != cudaSuccess) return e;
+    bytes = grow;
+    // zero once at allocation: the sort / scan look-back words must never hold a
+    // stale epoch by accident (bh_sort.cu); everything else overwrites
+    return cudaMemset(p, 0, grow);
   }
   void release() {
     if (p) cudaFree(p);
@@ -249,8 +252,9 @@ void launch_potential_f64(const double *pos3, const double *mass, int64_t n, dou
 
 // FFMA throughput microbenchmark (fills *flops with the FP32 flops issued)
 void run_ffma(float *out, int sms, int iters, double *flops, cudaStream_t s);
+void run_dfma(double *out, int sms, int iters, double *flops, cudaStream_t s);
 
-// radix sort of (key, u32 value) pairs over bits [0, 63) -- stable
+// radix sort of (key, u32 value) pairs over bits [0, 63) -- stable (bh_sort.cu)
 size_t sort_temp_bytes(int64_t n);
 cudaError_t sort_pairs(void *temp, size_t temp_bytes, const uint64_t *kin, uint64_t *kout,
                        const uint32_t *vin, uint32_t *vout, int64_t n, cudaStream_t s);
@@ -260,6 +264,7 @@ cudaError_t inclusive_scan_u32(void *temp, size_t temp_bytes, const uint32_t *in
                                int64_t n, cudaStream_t s);
 cudaError_t exclusive_scan_u32(void *temp, size_t temp_bytes, const uint32_t *in, uint32_t *out,
                                int64_t n, cudaStream_t s);
+int sort_launches();
 
 inline int grid_for(int64_t n, int block) {
   int64_t g = (n + block - 1) / block;

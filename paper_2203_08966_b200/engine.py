@@ -144,6 +144,12 @@ class Engine:
         check(self._L.bh_sort(self._h, _ptr(keys), n, _ptr(ks), _ptr(perm), self.stream))
         return ks, perm
 
+    def scan_u32(self, values: torch.Tensor, inclusive: bool = False) -> torch.Tensor:
+        """The build's device prefix sum (int32 tensor in, int32 out, mod 2^32)."""
+        out = torch.empty_like(values)
+        check(self._L.bh_scan_u32(self._h, _ptr(values), values.shape[0], _ptr(out), int(inclusive), self.stream))
+        return out
+
     def build(self, pos_sorted: torch.Tensor, R: torch.Tensor, mass_sorted: torch.Tensor | None = None) -> int:
         """hashed.py:448-515 over Morton-sorted bodies; returns the cell count."""
         n = pos_sorted.shape[0]
@@ -394,9 +400,11 @@ class Engine:
         check(self._L.bh_stats_get(self._h, ctypes.byref(s), self.stream))
         return int(s.launches)
 
-    def ffma_peak_tflops(self) -> float:
+    def ffma_peak_tflops(self, fp64: bool = False) -> float:
+        """Measured FFMA (fp64: DFMA) throughput of this GPU, TFLOP/s."""
         out = ctypes.c_double()
-        check(self._L.bh_ffma_peak(self._h, ctypes.byref(out), self.stream))
+        fn = self._L.bh_dfma_peak if fp64 else self._L.bh_ffma_peak
+        check(fn(self._h, ctypes.byref(out), self.stream))
         return float(out.value)
 
     # ------------------------------------------------------- validation
