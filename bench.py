@@ -3,17 +3,22 @@
 steps/s; + % of FP32 peak for the traversal, % of HBM for build and sort).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config cfg2]
+                    [--config cfg3] [--precision fp32|fp64]
 
 A step is one full KDK leapfrog step of the hot path (simulation.py:492-502):
 kick+drift+bounds, Morton keys, radix sort, body permutation, tree build with
-moments, traversal, kick.  Default workload = BASELINE config 2 (Plummer
-N=1e6, seed 2, fp32, theta=0.6, eps=1e-3, leaf size 16, dt=1e-3).  Synthetic
+moments, traversal, kick.  Default workload = BASELINE config 3, the largest
+configuration BASELINE lists on one GPU (two colliding Plummer clusters,
+N=1e7, seed 3, fp32, theta=0.6, eps=1e-4, leaf size 32, dt=5e-4).  Synthetic
 inputs from the reference's own Plummer sampler (bit-identical restatement).
+
+`--gpus N` without a launcher re-executes itself under torch.distributed.run
+with N processes (one per GPU); under torchrun WORLD_SIZE must equal N.
 
 `--impl reference` times the reference algorithm on the host CPU (the oracle
 port: the reference is Python/numba and cannot travel to the GPU box), with
-all host threads, on a bounded target sample per step.
+all host threads, on a bounded target sample per step.  Its inputs come from
+the oracle's own restatement of the reference sampler (no product library).
 """
 
 from __future__ import annotations
@@ -83,6 +88,43 @@ def make_bodies(cfg: dict):
     else:
         b = colliding_plummers(cfg["n"] // 2, cfg["seed"])
     return b
+
+
+def make_reference_inputs(cfg: dict):
+    """(mass, pos, vel) fp64 numpy for the reference arm, from the oracle's
+    restatement of the reference sampler (initcond.py:62-77): the arm loads no
+    product library.  cfg4's generator is new (the reference has none) and is
+    pure numpy."""
+    from oracle import oracle as orc
+
+    if cfg["kind"] == "plummer":
+        return orc.plummer_cluster(cfg["n"], orc.make_rng(cfg["seed"]), 1.0)
+    if cfg["kind"] == "two":
+        return orc.colliding_plummers(cfg["n"] // 2, cfg["seed"])
+    from paper_2203_08966_b200.initcond import hernquist_cosmology  # numpy only
+
+    pos, vel, mass = hernquist_cosmology(cfg["n"], cfg["seed"])
+    return (mass.astype(np.float64), pos.astype(np.float64), vel.astype(np.float64))
+
+
+def workload_config(args, cfg: dict, ws: int) -> dict:
+    """The `config` object both arms print (identical keys and values)."""
+    return {"workload": args.config, "n_bodies": cfg["n"], "theta": cfg["theta"], "eps": cfg["eps"],
+            "leaf_size": cfg["leaf"], "dt": cfg["dt"], "precision": args.precision,
+            "parallelism": parallelism_string(args, ws),
+            "l2": "flushed between timed steps (256 MB write)"}
+
+
+def parallelism_string(args, ws: int, p2p: bool | None = None) -> str:
+    if ws <= 1:
+        return "single GPU"
+    if args.decomp == "distributed":
+        return (f"{ws} ranks: costzones key ranges, body migration, distributed build, "
+                "branch-node allgather, locally-essential-tree all-to-all")
+    xch = ("walk epilogue stores zone results into peer buffers (NVLink, CUDA IPC)" if p2p
+           else "NCCL all-reduce of zone results" if p2p is False
+           else "zone results exchanged by peer stores or all-reduce")
+    return f"{ws} ranks: replicated tree, costzones-partitioned walk, {xch}"
 
 
 class ClockSampler:
@@ -181,29 +223,33 @@ def run_ours(args, cfg) -> dict | None:
         else:
             dist.init_process_group(backend)
     dev = torch.device("cuda", local)
+    fp64 = args.precision == "fp64"
     b = make_bodies(cfg)
     n = len(b)
-    eng = Engine("fp32", local)
+    eng = Engine(args.precision, local)
     pos = eng.bodies_tensor(b.position, b.mass)
     vel = eng.vec_tensor(b.velocity)
+    mass = torch.as_tensor(np.asarray(b.mass, dtype=np.float64)).to(dev) if fp64 else None
     theta, eps, leaf, dt = cfg["theta"], cfg["eps"], cfg["leaf"], cfg["dt"]
     sim = None
     if ws > 1 and args.decomp == "replicated":  # replicated tree, partitioned walk
         from paper_2203_08966_b200.decomposition import DistributedSim, StepParams, TorchComm
 
         sim = DistributedSim(eng, TorchComm(), StepParams(theta, eps, leaf, dt))
-        sim.load(pos, vel)
+        sim.load(pos, vel, mass) if fp64 else sim.load(pos, vel)
         sim.bootstrap()
     elif ws > 1:  # key-range decomposition, distributed build
         from paper_2203_08966_b200.decomposition import DistributedBuildSim, StepParams, TorchComm
 
+        if fp64:
+            raise SystemExit("the distributed build runs the fp32 walk; use --decomp replicated for fp64")
         sim = DistributedBuildSim(eng, TorchComm(), StepParams(theta, eps, leaf, dt))
         lo, hi = n * rank // ws, n * (rank + 1) // ws  # initial chunk (simulation.py:190-198)
         sim.load(pos[lo:hi].contiguous(), vel[lo:hi].contiguous(),
                  gid=torch.arange(lo, hi, device=dev))
         sim.bootstrap()
     else:
-        eng.sim_load(pos, vel)
+        eng.sim_load(pos, vel, mass)
         eng.sim_forces(theta, eps, leaf, record_work=False)
 
     def one_step():
@@ -211,7 +257,7 @@ def run_ours(args, cfg) -> dict | None:
             sim.step(1)
         else:
             eng.sim_step(dt, theta, eps, leaf, 1)
-    peak_fp32 = eng.ffma_peak_tflops()
+    peak_fp = eng.ffma_peak_tflops(fp64)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     for _ in range(args.warmup):
         one_step()
@@ -246,66 +292,7 @@ def run_ours(args, cfg) -> dict | None:
     eng.check()
 
     # ---- end to end through the public API with host buffers
-    import torch as _t
-
-    hpos = _t.empty((n, 4), dtype=_t.float32).pin_memory()
-    hvel = _t.empty((n, 4), dtype=_t.float32).pin_memory()
-    hacc = _t.empty((n, 4), dtype=_t.float32).pin_memory()
-    dpos = _t.empty((n, 4), dtype=_t.float32, device=dev)
-    dvel = _t.empty_like(dpos)
-    dacc = _t.empty_like(dpos)
-    distributed = ws > 1 and args.decomp == "distributed"
-    if distributed:  # this rank's bodies only
-        p_, v_, a_, w_, g_ = sim.store()
-        nl = p_.shape[0]
-        dpos, dvel, dacc = p_.clone(), v_.clone(), a_.clone()
-        dwork, dgid = w_.to(_t.int32).clone(), g_.clone()
-        hpos, hvel, hacc = (x.cpu().pin_memory() for x in (dpos, dvel, dacc))
-        hwork, hgid = dwork.cpu().pin_memory(), dgid.cpu().pin_memory()
-    else:
-        eng.sim_store(dpos, dvel, dacc)
-        hpos.copy_(dpos)
-        hvel.copy_(dvel)
-        hacc.copy_(dacc)
-    hvel3 = hvel[:, :3].contiguous().pin_memory()
-    hacc3 = hacc[:, :3].contiguous().pin_memory()
-    host_api = not distributed and sim is None
-    torch.cuda.synchronize()
-    e2e_ms = 0.0
-    e2e_inter = 0
-    for it in range(args.warmup + args.steps):  # the first W calls warm the path (staging buffers, streams)
-        flush.zero_()
-        if ws > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        ev0.record()
-        if distributed:
-            dpos, dvel, dacc = (x.to(dev, non_blocking=True) for x in (hpos, hvel, hacc))
-            sim.upload(dpos, dvel, dacc, hwork.to(dev, non_blocking=True), hgid.to(dev, non_blocking=True))
-            sim.step(1)
-            p_, v_, a_, w_, g_ = sim.store()
-            hpos, hvel, hacc = (x.to("cpu", non_blocking=True) for x in (p_, v_, a_))
-            hwork, hgid = w_.to(_t.int32).to("cpu", non_blocking=True), g_.to("cpu", non_blocking=True)
-        elif sim is not None:  # replicated multi-GPU: every rank holds the full state
-            dpos.copy_(hpos, non_blocking=True)
-            dvel.copy_(hvel, non_blocking=True)
-            dacc.copy_(hacc, non_blocking=True)
-            eng.sim_load(dpos, dvel, acc=dacc)
-            sim.step(1)
-            eng.sim_store(dpos, dvel, dacc)
-            hpos.copy_(dpos, non_blocking=True)
-            hvel.copy_(dvel, non_blocking=True)
-            hacc.copy_(dacc, non_blocking=True)
-        else:  # one call from host arrays: pos (n,4), vel/acc (n,3) (bh_sim_step_host)
-            eng.sim_step_host(hpos, hvel3, hacc3, dt, theta, eps, leaf, 1)
-        ev1.record()
-        torch.cuda.synchronize()
-        if it < args.warmup:
-            continue
-        e2e_ms += ev0.elapsed_time(ev1)
-        st = eng.stats()
-        e2e_inter += st.pp + st.pc
-    eng.check()
+    e2e_ms, e2e_inter, e2e_path, h2d, d2h = run_e2e(args, cfg, eng, sim, ws, dev, flush, ev0, ev1)
 
     # ---- max over ranks
     rdev = dev if backend == "nccl" else "cpu"
@@ -331,11 +318,13 @@ def run_ours(args, cfg) -> dict | None:
         hbm = float(peaks["hbm_gbs"])
         traffic = pipe = None
         tp = os.path.join(ROOT, "profiles", "walk_traffic.json")
-        if os.path.exists(tp):
+        if os.path.exists(tp) and not fp64:
             with open(tp) as f:
                 wt = json.load(f)
             traffic = wt.get(args.config)
             pipe = wt.get("fp32_pipe_active", {}).get(args.config)
+        config = workload_config(args, cfg, ws)
+        config["parallelism"] = parallelism_string(args, ws, getattr(sim, "p2p", None))
         result = {
             "metric": METRIC,
             "value": inter_all / sec,
@@ -348,26 +337,21 @@ def run_ours(args, cfg) -> dict | None:
             "higher_is_better": True,
             "scaling": "strong" if ws > 1 else "weak",
             "vs_baseline": None,
-            "dtype": "f32",
+            "dtype": "f64" if fp64 else "f32",
             "data": "synthetic: reference plummer_cluster sampler (bit-identical restatement), seed %d" % cfg["seed"],
-            "config": {"workload": args.config, "n_bodies": n, "theta": theta, "eps": eps,
-                       "leaf_size": leaf, "dt": dt, "precision": "fp32",
-                       "parallelism": ((f"{ws} ranks: costzones key ranges, body migration, "
-                                        "distributed build, branch-node allgather, "
-                                        "locally-essential-tree all-to-all")
-                                       if args.decomp == "distributed" else
-                                       (f"{ws} ranks: replicated tree, costzones-partitioned walk, "
-                                        "NCCL all-reduce of zone accelerations")) if ws > 1 else "single GPU",
-                       "l2": "flushed between timed steps (256 MB write)"},
+            "config": config,
             "interactions_per_step": inter_all / args.steps,
             "pp_per_step": pp / args.steps,
             "pc_per_step": pc / args.steps,
             "cells": cells,
             "phase_ms_per_step": {k: v / args.steps for k, v in phases.items()},
-            "roofline": {"bound": "fp32", "kernel": "k_walk9 (k_walk_f32)",
-                         "achieved": walk_tf, "peak": peak_fp32, "unit": "TFLOP/s",
-                         "frac": (walk_tf / peak_fp32) if walk_tf else None,
-                         "peak_source": "FFMA microbenchmark on this GPU (bh_ffma_peak); MEASURED_PEAKS.json has no FP32 entry",
+            "roofline": {"bound": "fp64" if fp64 else "fp32",
+                         "kernel": "k_walk_f64 (fp64 walk)" if fp64 else "k_walk9 (k_walk_f32)",
+                         "achieved": walk_tf, "peak": peak_fp, "unit": "TFLOP/s",
+                         "frac": (walk_tf / peak_fp) if walk_tf else None,
+                         "peak_source": ("DFMA microbenchmark on this GPU (bh_dfma_peak)" if fp64 else
+                                         "FFMA microbenchmark on this GPU (bh_ffma_peak); "
+                                         "MEASURED_PEAKS.json has no FP32 entry"),
                          "flops_per_unit": {"pp": FLOPS_PP, "pc": FLOPS_PC},
                          "traffic": traffic,
                          "fp32_pipe_active_ncu": pipe},
@@ -376,17 +360,13 @@ def run_ours(args, cfg) -> dict | None:
                                "bytes_per_body": bpb, "peak_source": peaks.get("source")},
             "roofline_sort": {"bound": "hbm", "achieved": sort_gbs, "peak": hbm, "unit": "GB/s",
                               "frac": sort_gbs / hbm if sort_gbs else None,
-                              "bytes_per_body": SORT_BYTES_PER_BODY, "impl": "cub::DeviceRadixSort (onesweep)"},
+                              "bytes_per_body": SORT_BYTES_PER_BODY,
+                              "impl": "hand-written onesweep LSD radix sort (bh_sort.cu), 8 digit passes"},
             "e2e": {"value": e2e_all / (e2e_ms / 1e3), "unit": "interactions/s",
-                    "h2d_bytes_per_step": (16 + 12 + 12) * n if host_api else 3 * 16 * n,
-                    "d2h_bytes_per_step": (16 + 12 + 12) * n if host_api else 3 * 16 * n,
-                    "ms_per_step": e2e_ms / args.steps,
-                    "path": ("Engine.sim_step_host -> bh_sim_step_host (C-ABI): pinned host pos (n,4), "
-                             "vel/acc (n,3) in, state back in caller order; positions copied back under "
-                             "the force computation") if host_api else
-                            "Engine.sim_load/sim_step/sim_store (C-ABI) from pinned host pos/vel/acc"},
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "ms_per_step": e2e_ms / args.steps, "path": e2e_path},
             "gpu_launches": launches,
-            "gpu_launches_note": "libbh kernels in the timed region (CUB sort/scan kernels not included)",
+            "gpu_launches_note": "libbh kernels launched in the timed region (sort, scans and walk included)",
             "clocks": clocks.summary(),
         }
     if ws > 1:
@@ -394,6 +374,98 @@ def run_ours(args, cfg) -> dict | None:
         dist.destroy_process_group()
     eng.close()
     return result
+
+
+def run_e2e(args, cfg, eng, sim, ws, dev, flush, ev0, ev1):
+    """The same steps through the public API from pinned host buffers: every
+    step copies its inputs host->device and its results device->host inside
+    the timed region.  Returns (ms, interactions, path, h2d bytes, d2h bytes)."""
+    import torch
+    import torch.distributed as dist
+
+    theta, eps, leaf, dt = cfg["theta"], cfg["eps"], cfg["leaf"], cfg["dt"]
+    fp64 = args.precision == "fp64"
+    distributed = ws > 1 and args.decomp == "distributed"
+    host_api = not distributed and sim is None and not fp64
+    if distributed:  # this rank's bodies only
+        p_, v_, a_, w_, g_ = sim.store()
+        dpos, dvel, dacc = p_.clone(), v_.clone(), a_.clone()
+        dwork, dgid = w_.to(torch.int32).clone(), g_.clone()
+        hpos, hvel, hacc = (x.cpu().pin_memory() for x in (dpos, dvel, dacc))
+        hwork, hgid = dwork.cpu().pin_memory(), dgid.cpu().pin_memory()
+        h2d = d2h = sum(x.numel() * x.element_size() for x in (hpos, hvel, hacc, hwork, hgid))
+        path = "DistributedBuildSim.upload/step/store from pinned host pos/vel/acc/work/ids (this rank's bodies)"
+    elif host_api:
+        n = eng.sim_n if hasattr(eng, "sim_n") and eng.sim_n else cfg["n"]
+        dpos = torch.empty((n, 4), dtype=torch.float32, device=dev)
+        dvel, dacc = torch.empty_like(dpos), torch.empty_like(dpos)
+        eng.sim_store(dpos, dvel, dacc)
+        hpos = dpos.cpu().pin_memory()
+        hvel3 = dvel[:, :3].contiguous().cpu().pin_memory()
+        hacc3 = dacc[:, :3].contiguous().cpu().pin_memory()
+        hwork = torch.empty(n, dtype=torch.int32).pin_memory()
+        h2d = (16 + 12 + 12) * n
+        d2h = (16 + 12 + 12 + 4) * n
+        path = ("Engine.sim_step_host -> bh_sim_step_host (C-ABI): pinned host pos (n,4), vel/acc (n,3) in; "
+                "state and per-body work back in caller order; positions copied back under the force computation")
+    else:  # fp64 or replicated ranks: the resident API from host arrays
+        n = cfg["n"]
+        w = 3 if fp64 else 4
+        dpos = torch.empty((n, w), dtype=eng.dtype, device=dev)
+        dvel, dacc = torch.empty_like(dpos), torch.empty_like(dpos)
+        dwork = torch.empty(n, dtype=torch.int64, device=dev)
+        eng.sim_store(dpos, dvel, dacc)
+        hpos, hvel, hacc = (x.cpu().pin_memory() for x in (dpos, dvel, dacc))
+        hwork = dwork.cpu().pin_memory()
+        hmass = torch.as_tensor(np.asarray(make_bodies(cfg).mass, dtype=np.float64)).pin_memory() if fp64 else None
+        dmass = torch.empty(n, dtype=torch.float64, device=dev) if fp64 else None
+        h2d = sum(x.numel() * x.element_size() for x in (hpos, hvel, hacc)) + (8 * n if fp64 else 0)
+        d2h = sum(x.numel() * x.element_size() for x in (hpos, hvel, hacc, hwork))
+        path = ("Engine.sim_load/sim_step/sim_store (C-ABI) from pinned host "
+                + ("fp64 pos/vel/acc (n,3) + masses" if fp64 else "pos/vel/acc") + ", work back")
+    torch.cuda.synchronize()
+    e2e_ms = 0.0
+    e2e_inter = 0
+    for it in range(args.warmup + args.steps):  # the first W calls warm the path (staging buffers, streams)
+        flush.zero_()
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev0.record()
+        if distributed:
+            dpos, dvel, dacc = (x.to(dev, non_blocking=True) for x in (hpos, hvel, hacc))
+            sim.upload(dpos, dvel, dacc, hwork.to(dev, non_blocking=True), hgid.to(dev, non_blocking=True))
+            sim.step(1)
+            p_, v_, a_, w_, g_ = sim.store()
+            hpos, hvel, hacc = (x.to("cpu", non_blocking=True) for x in (p_, v_, a_))
+            hwork, hgid = w_.to(torch.int32).to("cpu", non_blocking=True), g_.to("cpu", non_blocking=True)
+        elif host_api:  # one call: pos (n,4), vel/acc (n,3) in, state + work out (bh_sim_step_host)
+            eng.sim_step_host(hpos, hvel3, hacc3, dt, theta, eps, leaf, 1, work=hwork)
+        else:
+            dpos.copy_(hpos, non_blocking=True)
+            dvel.copy_(hvel, non_blocking=True)
+            dacc.copy_(hacc, non_blocking=True)
+            if fp64:
+                dmass.copy_(hmass, non_blocking=True)
+            eng.sim_load(dpos, dvel, dmass, acc=dacc)
+            if sim is not None:
+                sim.step(1)
+            else:
+                eng.sim_step(dt, theta, eps, leaf, 1)
+            eng.sim_store(dpos, dvel, dacc, dwork)
+            hpos.copy_(dpos, non_blocking=True)
+            hvel.copy_(dvel, non_blocking=True)
+            hacc.copy_(dacc, non_blocking=True)
+            hwork.copy_(dwork, non_blocking=True)
+        ev1.record()
+        torch.cuda.synchronize()
+        if it < args.warmup:
+            continue
+        e2e_ms += ev0.elapsed_time(ev1)
+        st = eng.stats()
+        e2e_inter += st.pp + st.pc
+    eng.check()
+    return e2e_ms, e2e_inter, path, h2d, d2h
 
 
 # --------------------------------------------------- CPU (reference) timing
@@ -455,20 +527,30 @@ def _cpu_model() -> str:
     return "unknown"
 
 
+class _RefBodies:
+    """(mass, position, velocity) of the reference arm's inputs."""
+
+    def __init__(self, mass, pos, vel):
+        self.mass, self.position, self.velocity = mass, pos, vel
+
+    def __len__(self):
+        return len(self.mass)
+
+
 def run_reference(args, cfg) -> dict | None:
     ws, rank, _ = dist_setup()
     if rank != 0:
         return None
     from oracle import oracle as orc
 
-    b = make_bodies(cfg)
+    b = _RefBodies(*make_reference_inputs(cfg))
     n = len(b)
     nthreads = orc.num_threads()
     rng = np.random.Generator(np.random.Philox(key=7))
     probe = rng.choice(n, min(n, 2000), replace=False)
     _, _, ts = cpu_reference_step(b, cfg, probe, nthreads)
     # bounded sample so that warmup + steps stays within a few minutes
-    per_step_budget = 150.0 / max(1, args.steps + args.warmup)
+    per_step_budget = 100.0 / max(1, args.steps + args.warmup)
     s = int(min(n, max(1000, len(probe) * per_step_budget / max(ts, 1e-3))))
     sample = np.sort(rng.choice(n, s, replace=False))
     for _ in range(args.warmup):
@@ -485,10 +567,12 @@ def run_reference(args, cfg) -> dict | None:
         "metric": METRIC,
         "value": value, "unit": "interactions/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": tot_s / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic: reference plummer_cluster sampler, seed %d" % cfg["seed"],
-        "config": {"workload": args.config, "n_bodies": n, "theta": cfg["theta"], "eps": cfg["eps"],
-                   "leaf_size": cfg["leaf"], "dt": cfg["dt"]},
+        "higher_is_better": True, "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None,
+        "dtype": "f64",
+        "dtype_note": "the reference computes in fp64; with precision fp32 its inputs are the same "
+                      "fp32-rounded positions and masses, upcast exactly (SURVEY.md §8c protocol)",
+        "data": "synthetic: reference plummer_cluster sampler (oracle restatement), seed %d" % cfg["seed"],
+        "config": workload_config(args, cfg, ws),
         "cpu_baseline": {"value": value, "unit": "interactions/s", "cores": nthreads, "kind": "port",
                          "sample": f"per step: serial keys+sort+build over all {n} bodies + traversal of "
                                    f"{s} targets on {nthreads} threads, extrapolated to {n}",
@@ -497,13 +581,29 @@ def run_reference(args, cfg) -> dict | None:
     }
 
 
+def spawn_ranks(args) -> int:
+    """`--gpus N` without a launcher: re-run this command under
+    torch.distributed.run with N local processes (127.0.0.1 rendezvous)."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=sorted(CONFIGS), default="cfg2")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="cfg3")
+    ap.add_argument("--precision", choices=["fp32", "fp64"], default="fp32",
+                    help="fp32: the bench configurations' storage and arithmetic; fp64: the "
+                         "validation mode (and the drop-in default of SimConfig)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--decomp", choices=["auto", "distributed", "replicated"], default="auto",
                     help="multi-GPU scheme (N>1): key-range decomposition with a distributed "
@@ -511,8 +611,16 @@ def main() -> None:
                          f"from N >= {AUTO_DISTRIBUTED_N:.0e} bodies (below that the replicated "
                          "O(N) build costs less than the distributed step's fixed exchange)")
     args = ap.parse_args()
+    if args.gpus < 1:
+        raise SystemExit("--gpus must be >= 1")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        raise SystemExit(spawn_ranks(args))
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={ws}: launch one process per GPU")
     if args.decomp == "auto":
-        args.decomp = "distributed" if CONFIGS[args.config]["n"] >= AUTO_DISTRIBUTED_N else "replicated"
+        args.decomp = ("distributed" if CONFIGS[args.config]["n"] >= AUTO_DISTRIBUTED_N and args.precision == "fp32"
+                       else "replicated")
     if args.warmup < 3 and args.impl == "ours":
         print("warning: W < 3 violates the timing rules; using 3", file=sys.stderr)
         args.warmup = 3
@@ -526,7 +634,7 @@ def main() -> None:
     if res is not None:
         ws, rank, _ = dist_setup()
         if ws == 1 and not args.no_cpu_baseline and cfg["n"] <= 20_000_000:
-            res["cpu_baseline"] = cpu_baseline(cfg, make_bodies(cfg))
+            res["cpu_baseline"] = cpu_baseline(cfg, _RefBodies(*make_reference_inputs(cfg)))
         elif ws == 1 and not args.no_cpu_baseline:
             res["cpu_baseline"] = {"value": None, "unit": "interactions/s", "cores": None,
                                    "kind": "port", "sample": "skipped: N > 2e7 (serial CPU build "

@@ -159,11 +159,13 @@ int bh_sim_store(bh_handle *h, void *d_pos, void *d_vel, void *d_acc, int64_t *d
                  void *stream);
 /* One call from host arrays (fp32 handles): load pos4 (x, y, z, m; n x 4),
  * vel3 and acc3 (n x 3), run `steps` KDK steps (simulation.py:492-502), and
- * write the state back in the caller's order.  For one step the positions are
- * copied back under the force computation.  Pinned host memory makes the
- * copies asynchronous.  Synchronous on the stream at return. */
-int bh_sim_step_host(bh_handle *h, float *pos4, float *vel3, float *acc3, int64_t n, double dt,
-                     double theta, double eps, int leaf_size, int steps, void *stream);
+ * write the state back in the caller's order; work (optional, n int32) gets
+ * the last force pass's per-body work pp + 2 pc (simulation.py:394-395,
+ * octree.py:23-25).  For one step the positions are copied back under the
+ * force computation.  Pinned host memory makes the copies asynchronous.  The
+ * results are complete once the stream has synchronised. */
+int bh_sim_step_host(bh_handle *h, float *pos4, float *vel3, float *acc3, int32_t *work, int64_t n,
+                     double dt, double theta, double eps, int leaf_size, int steps, void *stream);
 
 /* The same step in phases, for a multi-GPU driver that exchanges between them
  * (simulation.py:492-502 with the force pass split at the walk):

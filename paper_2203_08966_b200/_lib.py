@@ -128,7 +128,7 @@ def _declare(L: ctypes.CDLL) -> None:
         "bh_sim_let": ([P, P, I, I, I, ctypes.POINTER(I64), ctypes.POINTER(I64), P], I),
         "bh_sim_let_pack": ([P, I, P, P, P, P], I),
         "bh_sim_target_boxes": ([P, P, I, P, P], I),
-        "bh_sim_step_host": ([P, P, P, P, I64, D, D, D, I, I, P], I),
+        "bh_sim_step_host": ([P, P, P, P, P, I64, D, D, D, I, I, P], I),
         "bh_walk_records_defer_f32": ([P, P, I64, P, P, I64, D, I, P, P, P, P, I64, P], I),
         "bh_walk_records_resume_f32": ([P, P, I64, P, P, I64, D, I, P, P, P, I64, P, P], I),
         "bh_timing_enable": ([P, I], I),

@@ -71,6 +71,7 @@ struct bh_handle {
   // sync-free build (fp32 resident path): capacity, device count, snapshot
   bool async_tree = false;
   int64_t cap = 0, C_true = 0;
+  int cur_step = 0;       // step index inside a bh_sim_step call (recorded on overflow)
   int *dCtrue = nullptr;
   int *hstat = nullptr;  // pinned: [0] = C, [1..22] = internal cells per level
   int grid_lvl[kMaxLevel + 1] = {0};
@@ -90,6 +91,7 @@ struct bh_handle {
   bool drop_work = false;
   // bh_sim_step_host: staging and the side stream for the early position copy
   Buf hs_a, hs_b, hs_pos;
+  float *host_pos4 = nullptr;  // the caller's pos4 of the running bh_sim_step_host call
   cudaStream_t side = nullptr;
   cudaStream_t cp[2] = {nullptr, nullptr};  // concurrent host copies (H2D reads overlap on PCIe)
   cudaEvent_t ev_cp[3] = {nullptr, nullptr, nullptr};
@@ -325,7 +327,7 @@ int build_sorted_async(bh_handle *h, int64_t n, const float4 *bod32, cudaStream_
                  h->flags, h->lvl.as<int>(), allow_dup, s);
   BH_CUDA(exclusive_scan_u32(h->scan_tmp.p, h->scan_tmp.bytes, h->newc.as<uint32_t>(),
                              h->off.as<uint32_t>(), n, s));
-  launch_set_count(h->off.as<uint32_t>(), h->newc.as<uint32_t>(), n, cap, h->dCtrue, h->flags, s);
+  launch_set_count(h->off.as<uint32_t>(), h->newc.as<uint32_t>(), n, cap, h->dCtrue, h->flags, s, h->cur_step);
   BH_CUDA(h->link.ensure(sizeof(int4) * cap));
   BH_CUDA(h->parent.ensure(sizeof(int) * cap));
   BH_CUDA(h->lvl_list.ensure(sizeof(int) * cap));
@@ -645,7 +647,8 @@ int sim_end_step(bh_handle *h, double dt, cudaStream_t s) {
   const int64_t n = h->sim_n;
   const double half = 0.5 * dt;  // simulation.py:500: kick(0.5*dt)
   h->tbegin(BH_PHASE_INTEGRATE, s);
-  if (h->precision == BH_FP32) launch_kick_f32(h->vel.as<float4>(), h->acc.as<float4>(), n, (float)half, s);
+  if (h->precision == BH_FP32)  // skipped on the device if this call's build overflowed
+    launch_kick_f32(h->vel.as<float4>(), h->acc.as<float4>(), n, (float)half, s, h->flags);
   else launch_kick4_f64(h->vel.as<double4>(), h->acc.as<double4>(), n, half, s);
   h->tend(s);
   h->launches += 1;
@@ -1014,21 +1017,37 @@ int bh_sim_forces(bh_handle *h, double theta, double eps, int leaf_size, int rec
   return fail(BH_OUT_OF_MEMORY, "tree cell capacity kept overflowing");
 }
 
-static int sim_snapshot(bh_handle *h, bool restore, cudaStream_t s) {
-  if (!restore) BH_TRY(flush_work(h, s));
-  else h->work_dirty = false;  // work_orig comes back from the snapshot
-  const int64_t n = h->sim_n;
-  const size_t e4 = h->precision == BH_FP32 ? sizeof(float4) : sizeof(double4);
-  struct { Buf *live, *bk; size_t bytes; } items[] = {
-      {&h->pos, &h->bk_pos, e4 * n}, {&h->vel, &h->bk_vel, e4 * n}, {&h->acc, &h->bk_acc, e4 * n},
-      {&h->id, &h->bk_id, sizeof(uint32_t) * n}, {&h->work_orig, &h->bk_work, sizeof(int) * n}};
-  for (auto &it : items) {
-    if (!restore) BH_CUDA(it.bk->ensure(it.bytes));
-    void *dst = restore ? it.live->p : it.bk->p;
-    void *src = restore ? it.bk->p : it.live->p;
-    BH_CUDA(cudaMemcpyAsync(dst, src, it.bytes, cudaMemcpyDeviceToDevice, s));
+// `steps` KDK steps (simulation.py:492-502) with no state snapshot.  A
+// sync-free build that overflows its capacity flags the device; every later
+// kernel of the call that reads the tree or moves the state skips (the walk
+// sees an empty tree, the kicks return), so the state is exactly what the
+// failed step's kick+drift left.  The call then grows the capacity and resumes
+// at that step's force evaluation.
+static int sim_steps(bh_handle *h, double dt, double theta, double eps, int leaf_size, int steps,
+                     cudaStream_t s, bool *pos_hook_done, void (*pos_hook)(bh_handle *, cudaStream_t)) {
+  int k = 0;
+  bool resume = false;
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    for (; k < steps; ++k) {
+      h->cur_step = k;
+      if (!resume) {
+        BH_TRY(sim_begin_step(h, dt, s));
+        if (pos_hook && !*pos_hook_done) {
+          pos_hook(h, s);
+          *pos_hook_done = true;
+        }
+      }
+      BH_TRY(sim_forces_impl(h, theta, eps, leaf_size, 1, !resume, s));
+      resume = false;
+      BH_TRY(sim_end_step(h, dt, s));
+    }
+    int overflow = 0;
+    BH_TRY(async_readback(h, s, &overflow));
+    if (!overflow) return BH_OK;
+    k = std::max(0, std::min(steps - 1, h->hflags->ovf_step));  // capacity grown: redo that step's forces
+    resume = true;
   }
-  return BH_OK;
+  return fail(BH_OUT_OF_MEMORY, "tree cell capacity kept overflowing");
 }
 
 int bh_sim_step(bh_handle *h, double dt, double theta, double eps, int leaf_size, int steps,
@@ -1036,25 +1055,13 @@ int bh_sim_step(bh_handle *h, double dt, double theta, double eps, int leaf_size
   if (!h || !(dt > 0.0) || steps < 0) return fail(BH_BAD_ARG, "bh_sim_step: bad args");
   if (h->sim_n == 0 || steps == 0) return BH_OK;
   cudaStream_t s = S(stream);
-  const bool f32 = h->precision == BH_FP32;
   struct DropWork {  // inside the call every walk records work: only the last one is kept
     bh_handle *h;
     explicit DropWork(bh_handle *hh) : h(hh) { h->drop_work = true; }
     ~DropWork() { h->drop_work = false; }
   } drop(h);
-  for (int attempt = 0; attempt < 3; ++attempt) {
-    if (f32) BH_TRY(sim_snapshot(h, false, s));
-    for (int k = 0; k < steps; ++k) {
-      BH_TRY(sim_begin_step(h, dt, s));
-      BH_TRY(sim_forces_impl(h, theta, eps, leaf_size, 1, true, s));
-      BH_TRY(sim_end_step(h, dt, s));
-    }
-    int overflow = 0;
-    BH_TRY(async_readback(h, s, &overflow));
-    if (!overflow) return BH_OK;
-    BH_TRY(sim_snapshot(h, true, s));  // grown capacity: redo the call
-  }
-  return fail(BH_OUT_OF_MEMORY, "tree cell capacity kept overflowing");
+  bool unused = false;
+  return sim_steps(h, dt, theta, eps, leaf_size, steps, s, &unused, nullptr);
 }
 
 __global__ void k_expand3(const float *__restrict__ v3, int64_t n, float4 *__restrict__ out) {
@@ -1072,11 +1079,21 @@ __global__ void k_store3f(const float4 *__restrict__ src, const uint32_t *__rest
 
 // One call from host arrays (the reference's numpy Bodies, fp32): load
 // pos4 (x, y, z, m) / vel3 / acc3, run `steps` KDK steps, write the state back
-// in the caller's order.  For one step the positions are final after the
-// drift, so their device->host copy runs on a side stream under the tree
-// build and walk; velocities and accelerations follow the final kick.  Host
-// arrays should be pinned for the copies to be asynchronous.
-int bh_sim_step_host(bh_handle *h, float *pos4, float *vel3, float *acc3, int64_t n, double dt,
+// in the caller's order, and (work != NULL) the last walk's per-body work
+// pp + 2 pc (simulation.py:394-395).  For one step the positions are final
+// after the drift, so their device->host copy runs on a side stream under the
+// tree build and walk; velocities, accelerations and work follow the final
+// kick.  Host arrays should be pinned for the copies to be asynchronous.
+static void early_pos_copy(bh_handle *h, cudaStream_t s) {
+  const int64_t n = h->sim_n;
+  cudaMemcpyAsync(h->hs_pos.p, h->pos.p, sizeof(float4) * n, cudaMemcpyDeviceToDevice, s);
+  cudaEventRecord(h->ev_pos, s);
+  cudaStreamWaitEvent(h->side, h->ev_pos, 0);
+  cudaMemcpyAsync(h->host_pos4, h->hs_pos.p, sizeof(float4) * n, cudaMemcpyDeviceToHost, h->side);
+  cudaEventRecord(h->ev_side, h->side);
+}
+
+int bh_sim_step_host(bh_handle *h, float *pos4, float *vel3, float *acc3, int32_t *work, int64_t n, double dt,
                      double theta, double eps, int leaf_size, int steps, void *stream) {
   if (!h || n < 1 || !pos4 || !vel3 || !acc3 || !(dt > 0.0) || steps < 1)
     return fail(BH_BAD_ARG, "bh_sim_step_host: bad args");
@@ -1119,28 +1136,16 @@ int bh_sim_step_host(bh_handle *h, float *pos4, float *vel3, float *acc3, int64_
   k_iota32<<<g, 256, 0, s>>>(h->id.as<uint32_t>(), n);
   k_fill_int<<<g, 256, 0, s>>>(h->work_orig.as<int>(), n, 1);  // simulation.py:482
   h->launches += 4;
-  bool pos_sent = false;
   h->work_dirty = false;  // freshly loaded: work_orig = 1
-  for (int attempt = 0; attempt < 3; ++attempt) {
-    BH_TRY(sim_snapshot(h, false, s));
-    for (int k = 0; k < steps; ++k) {
-      BH_TRY(sim_begin_step(h, dt, s));
-      if (steps == 1 && !pos_sent) {  // final positions, still in the caller's order
-        BH_CUDA(cudaMemcpyAsync(h->hs_pos.p, h->pos.p, sizeof(float4) * n, cudaMemcpyDeviceToDevice, s));
-        BH_CUDA(cudaEventRecord(h->ev_pos, s));
-        BH_CUDA(cudaStreamWaitEvent(h->side, h->ev_pos, 0));
-        BH_CUDA(cudaMemcpyAsync(pos4, h->hs_pos.p, sizeof(float4) * n, cudaMemcpyDeviceToHost, h->side));
-        BH_CUDA(cudaEventRecord(h->ev_side, h->side));
-        pos_sent = true;
-      }
-      BH_TRY(sim_forces_impl(h, theta, eps, leaf_size, 1, true, s));
-      BH_TRY(sim_end_step(h, dt, s));
-    }
-    int overflow = 0;
-    BH_TRY(async_readback(h, s, &overflow));
-    if (!overflow) break;
-    if (attempt == 2) return fail(BH_OUT_OF_MEMORY, "tree cell capacity kept overflowing");
-    BH_TRY(sim_snapshot(h, true, s));  // grown capacity: redo (same positions after the drift)
+  bool pos_sent = false;
+  h->host_pos4 = pos4;
+  {
+    struct DropWork {
+      bh_handle *h;
+      explicit DropWork(bh_handle *hh) : h(hh) { h->drop_work = true; }
+      ~DropWork() { h->drop_work = false; }
+    } drop(h);
+    BH_TRY(sim_steps(h, dt, theta, eps, leaf_size, steps, s, &pos_sent, steps == 1 ? early_pos_copy : nullptr));
   }
   const uint32_t *id = h->id.as<uint32_t>();
   if (!pos_sent) {
@@ -1155,6 +1160,10 @@ int bh_sim_step_host(bh_handle *h, float *pos4, float *vel3, float *acc3, int64_
   BH_CUDA(cudaMemcpyAsync(vel3, h->hs_a.p, sizeof(float) * 3 * n, cudaMemcpyDeviceToHost, h->cp[0]));
   BH_CUDA(cudaEventRecord(h->ev_cp[2], h->cp[0]));
   BH_CUDA(cudaMemcpyAsync(acc3, h->hs_b.p, sizeof(float) * 3 * n, cudaMemcpyDeviceToHost, s));
+  if (work) {  // the last walk's work, scattered to the caller's order (int32)
+    BH_TRY(sim_scatter_work(h, s));
+    BH_CUDA(cudaMemcpyAsync(work, h->work_orig.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
+  }
   BH_CUDA(cudaStreamWaitEvent(s, h->ev_cp[2], 0));
   if (pos_sent) BH_CUDA(cudaStreamWaitEvent(s, h->ev_side, 0));
   h->launches += 2 + (pos_sent ? 0 : 1);

@@ -456,14 +456,18 @@ __device__ void cell_moments8(const TreeView &t, int p, double (*xs)[11]) {
 
 // C = 1 + off[n-1] + newc[n-1] on device; flag an overflow of the capacity
 __global__ void k_set_count(const uint32_t *off, const uint32_t *newc, int64_t n, int64_t cap,
-                            int *dC, DeviceFlags *f) {
+                            int *dC, DeviceFlags *f, int step) {
   int64_t C = n > 0 ? 1 + (int64_t)off[n - 1] + newc[n - 1] : 1;
-  if (C > cap) atomicOr(&f->bits, FLAG_OVERFLOW);
+  if (C > cap && !(f->bits & FLAG_OVERFLOW)) {  // the first overflow of the call: remember its step
+    f->ovf_step = step;
+    __threadfence();
+    atomicOr(&f->bits, FLAG_OVERFLOW);
+  }
   dC[0] = (int)C;
 }
 void launch_set_count(const uint32_t *off, const uint32_t *newc, int64_t n, int64_t cap,
-                      int *dC, DeviceFlags *f, cudaStream_t s) {
-  k_set_count<<<1, 1, 0, s>>>(off, newc, n, cap, dC, f);
+                      int *dC, DeviceFlags *f, cudaStream_t s, int step) {
+  k_set_count<<<1, 1, 0, s>>>(off, newc, n, cap, dC, f, step);
 }
 
 // One cooperative launch (all blocks co-resident): offsets from the device

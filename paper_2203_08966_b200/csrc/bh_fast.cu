@@ -63,16 +63,17 @@ void launch_maxabs_f32(const float4 *pos, int64_t n, DeviceFlags *f, cudaStream_
 }
 
 // ------------------------------------------------------------ integrator
-__global__ void k_kick_f32(float4 *v, const float4 *a, int64_t n, float h) {
+__global__ void k_kick_f32(float4 *v, const float4 *a, int64_t n, float h, const DeviceFlags *f) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+  if (i >= n || overflowed(f)) return;
   float4 x = v[i], y = a[i];
   x.x += y.x * h; x.y += y.y * h; x.z += y.z * h;
   v[i] = x;
 }
-void launch_kick_f32(float4 *vel, const float4 *acc, int64_t n, float h, cudaStream_t s) {
+void launch_kick_f32(float4 *vel, const float4 *acc, int64_t n, float h, cudaStream_t s,
+                     const DeviceFlags *skip_on_overflow) {
   if (n <= 0) return;
-  k_kick_f32<<<grid_for(n, 256), 256, 0, s>>>(vel, acc, n, h);
+  k_kick_f32<<<grid_for(n, 256), 256, 0, s>>>(vel, acc, n, h, skip_on_overflow);
 }
 // drift keeps the mass in .w untouched
 __global__ void k_drift_f32(float4 *x, const float4 *v, int64_t n, float dt) {
@@ -92,6 +93,7 @@ void launch_drift_f32(float4 *pos, const float4 *vel, int64_t n, float dt, cudaS
 __global__ void k_kick_drift_max_f32(float4 *__restrict__ pos, float4 *__restrict__ vel,
                                      const float4 *__restrict__ acc, int64_t n, float h,
                                      float dt, DeviceFlags *f) {
+  if (overflowed(f)) return;  // a failed build earlier in this call: the state waits for the redo
   unsigned m = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     float4 x = pos[i];

@@ -53,7 +53,15 @@ struct DeviceFlags {
   unsigned int maxabs_bits;  // float bits of max |x| (fp32 bounds)
   int pad2;
   double maxabs64;           // fp64 bounds scratch (as ull bits for atomicMax)
+  int ovf_step;              // sync-free build: the step of a bh_sim_step call that overflowed first
+  int pad3;
 };
+// true once a sync-free build of this call has overflowed its capacity: every
+// later kernel of the call that reads the tree or moves the state skips, so the
+// state is left as the failed step's kick+drift made it (bh_api.cu redoes it)
+__device__ __forceinline__ bool overflowed(const DeviceFlags *f) {
+  return f && (*reinterpret_cast<const volatile int *>(&f->bits) & FLAG_OVERFLOW);
+}
 
 // ---------------------------------------------------------------- buffers
 struct Buf {
@@ -128,7 +136,7 @@ void launch_emit(const TreeView &t, const float4 *bod32, const double4 *bod64, c
 // (lvl: counts[22] from k_lcp_new | offsets[22] | cursors[22]); one cooperative
 // launch sweeps the levels deepest-first with grid-wide barriers between them.
 void launch_set_count(const uint32_t *off, const uint32_t *newc, int64_t n, int64_t cap,
-                      int *dC, DeviceFlags *f, cudaStream_t s);
+                      int *dC, DeviceFlags *f, cudaStream_t s, int step = 0);
 int launch_moments_coop(const TreeView &t, int *lvl, int *list, int sms, cudaStream_t s);
 void launch_export(const TreeView &t, double R, uint64_t *key, int8_t *level, double *centre,
                    double *side, double *mass, double *com, double *quad, int64_t *count,
@@ -224,7 +232,8 @@ void launch_walk_f64(const WalkParams &p, const double4 *cm64, const double *q64
                      int64_t *work64, int *work32, DeviceFlags *f, cudaStream_t s);
 
 // integrator (integrator.py:37-44) and body permutation
-void launch_kick_f32(float4 *vel, const float4 *acc, int64_t n, float h, cudaStream_t s);
+void launch_kick_f32(float4 *vel, const float4 *acc, int64_t n, float h, cudaStream_t s,
+                     const DeviceFlags *skip_on_overflow = nullptr);
 void launch_drift_f32(float4 *pos, const float4 *vel, int64_t n, float dt, cudaStream_t s);
 void launch_kick_f64(double *vel3, const double *acc3, int64_t n, double h, cudaStream_t s);
 void launch_drift_f64(double *pos3, const double *vel3, int64_t n, double dt, cudaStream_t s);

@@ -1,5 +1,5 @@
 // bh_sort.cu -- hand-written stable LSD radix sort of (u64 key, u32 value)
-// pairs over bits [0, 63) and single-pass u32 scans, for sm_100a.
+// pairs over bits [0, 63) and u32 prefix sums, for sm_100a.
 //
 // Replaces np.argsort(keys, kind="stable") (morton.py:128-130): the sorted
 // order is the stable one (ties keep their input order), bit for bit.
@@ -9,8 +9,9 @@
 //                 aggregated shared-memory atomics, one global add per bin and
 //                 block)
 //   k_sort_pass   per 4096-key tile: load (coalesced, warp-striped), rank every
-//                 key inside its warp with __match_any_sync (stable: lanes and
-//                 items in input order), warp offsets per digit, publish the
+//                 key inside its warp (peer lanes from 8 ballots, one per digit
+//                 bit: stable, lanes and items in input order; MATCH.ANY was
+//                 38% of the stall samples), warp offsets per digit, publish the
 //                 tile's digit counts, decoupled look-back over the previous
 //                 tiles for each digit's global offset, local reorder through
 //                 shared memory, and a run-coalesced scatter of keys and values
@@ -26,6 +27,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 
 #include "bh_internal.cuh"
 
@@ -42,7 +44,6 @@ constexpr int kTile = kSortThreads * kSortItems;  // 4096 keys
 constexpr int kSortWarps = kSortThreads / 32;
 static_assert(kSortThreads == kBins, "one thread per digit");
 constexpr int kHistThreads = 256;
-constexpr int kHistItems = 16;
 
 // look-back / status word: flag (2 bits) | epoch (30 bits) | value (32 bits)
 constexpr unsigned long long kFlagAgg = 1ull << 62;
@@ -73,7 +74,8 @@ struct SortTemp {
   uint64_t *k;             // [n] ping-pong keys
   uint32_t *v;             // [n] ping-pong values
   unsigned *hist;          // [kPasses][kBins] global digit histograms
-  unsigned *counters;      // [kPasses] tile counters (self-resetting)
+  unsigned *bin_start;     // [kPasses][kBins] their exclusive scans
+  unsigned *counters;      // [kPasses] tile counters (self-resetting); [kPasses]: histogram blocks done
   unsigned long long *st;  // [tiles][kBins] look-back status
 };
 inline size_t al(size_t x) { return (x + 255) & ~size_t(255); }
@@ -84,68 +86,109 @@ inline SortTemp carve_sort(void *temp, int64_t n) {
   t.k = reinterpret_cast<uint64_t *>(p); p += al(sizeof(uint64_t) * n);
   t.v = reinterpret_cast<uint32_t *>(p); p += al(sizeof(uint32_t) * n);
   t.hist = reinterpret_cast<unsigned *>(p); p += al(sizeof(unsigned) * kPasses * kBins);
-  t.counters = reinterpret_cast<unsigned *>(p); p += al(sizeof(unsigned) * kPasses);
+  t.bin_start = reinterpret_cast<unsigned *>(p); p += al(sizeof(unsigned) * kPasses * kBins);
+  t.counters = reinterpret_cast<unsigned *>(p); p += al(sizeof(unsigned) * (kPasses + 1));
   t.st = reinterpret_cast<unsigned long long *>(p);
   return t;
 }
 
 // ------------------------------------------------------------ histograms
-// Each thread reads kHistItems consecutive keys (16-byte loads) and adds run
-// lengths: along the Morton-sorted resident order the high digits rarely
-// change, so most of the 8 x 16 digit updates fold into one add.
+// One read of the keys for all 8 digit histograms: a shared-memory add per key
+// and digit, except that a warp whose 32 consecutive keys share a digit adds
+// 32 once (along the Morton-sorted resident order the high digits are
+// warp-uniform; same-address atomics from 32 lanes would serialise).  The last
+// block to finish turns the histograms into exclusive bin offsets.
+constexpr int kHistUnroll = 4;
+constexpr int kHistParts = 8;  // interleaved copies: lanes with equal digits hit 8 banks
 __global__ void __launch_bounds__(kHistThreads) k_sort_hist(const uint64_t *__restrict__ keys, int64_t n,
-                                                            unsigned *__restrict__ hist) {
-  __shared__ unsigned sh[kPasses][kBins];
-  for (int i = threadIdx.x; i < kPasses * kBins; i += kHistThreads) (&sh[0][0])[i] = 0u;
+                                                            unsigned *__restrict__ hist,
+                                                            unsigned *__restrict__ bin_start,
+                                                            unsigned *__restrict__ done) {
+  extern __shared__ unsigned hist_smem[];  // [kPasses][kBins][kHistParts]
+  __shared__ bool last;
+  for (int i = threadIdx.x; i < kPasses * kBins * kHistParts; i += kHistThreads) hist_smem[i] = 0u;
   __syncthreads();
-  const int64_t chunk = (int64_t)kHistThreads * kHistItems;
-  for (int64_t base = (int64_t)blockIdx.x * chunk; base < n; base += (int64_t)gridDim.x * chunk) {
-    const int64_t i0 = base + (int64_t)threadIdx.x * kHistItems;
-    uint64_t k[kHistItems];
-    if (i0 + kHistItems <= n) {
-      const ulonglong2 *src = reinterpret_cast<const ulonglong2 *>(keys + i0);
+  const unsigned lane = threadIdx.x & 31, FULL = 0xffffffffu, part = lane % kHistParts;
+  const int64_t wglobal = ((int64_t)blockIdx.x * kHistThreads + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * kHistThreads) >> 5;
+  for (int64_t base = wglobal * 32 * kHistUnroll; base < n; base += nwarps * 32 * kHistUnroll) {
+    uint64_t k[kHistUnroll];
 #pragma unroll
-      for (int j = 0; j < kHistItems / 2; ++j) {
-        const ulonglong2 v = __ldcs(src + j);
-        k[2 * j] = v.x;
-        k[2 * j + 1] = v.y;
+    for (int u = 0; u < kHistUnroll; ++u) {
+      const int64_t i = base + 32 * u + lane;
+      k[u] = i < n ? __ldcs(keys + i) : 0ull;
+    }
+    if (base + 32 * kHistUnroll <= n) {  // full groups
+#pragma unroll
+      for (int u = 0; u < kHistUnroll; ++u) {
+#pragma unroll
+        for (int p = 0; p < kPasses; ++p) {
+          const unsigned d = (unsigned)(k[u] >> (kDigitBits * p)) & (kBins - 1);
+          const unsigned d0 = __shfl_sync(FULL, d, 0);
+          if (__all_sync(FULL, d == d0)) {
+            if (lane == 0) atomicAdd(&hist_smem[(p * kBins + d0) * kHistParts], 32u);
+          } else {
+            atomicAdd(&hist_smem[(p * kBins + d) * kHistParts + part], 1u);
+          }
+        }
       }
     } else {
 #pragma unroll
-      for (int j = 0; j < kHistItems; ++j) k[j] = i0 + j < n ? keys[i0 + j] : ~0ull;
-    }
-    const int64_t left = n - i0;
-    const int cnt = left >= kHistItems ? kHistItems : (left > 0 ? (int)left : 0);
-    if (cnt == 0) continue;
+      for (int u = 0; u < kHistUnroll; ++u) {
+        if (base + 32 * u + lane < n) {
 #pragma unroll
-    for (int p = 0; p < kPasses; ++p) {
-      unsigned d = (unsigned)(k[0] >> (kDigitBits * p)) & (kBins - 1);
-      unsigned run = 1;
-#pragma unroll
-      for (int j = 1; j < kHistItems; ++j) {
-        if (j >= cnt) break;
-        const unsigned e = (unsigned)(k[j] >> (kDigitBits * p)) & (kBins - 1);
-        if (e == d) {
-          ++run;
-        } else {
-          atomicAdd(&sh[p][d], run);
-          d = e;
-          run = 1;
+          for (int p = 0; p < kPasses; ++p)
+            atomicAdd(&hist_smem[(p * kBins + ((unsigned)(k[u] >> (kDigitBits * p)) & (kBins - 1))) * kHistParts + part],
+                      1u);
         }
       }
-      atomicAdd(&sh[p][d], run);
     }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < kPasses * kBins; i += kHistThreads) {
-    const unsigned v = (&sh[0][0])[i];
+    unsigned v = 0;
+#pragma unroll
+    for (int q = 0; q < kHistParts; ++q) v += hist_smem[i * kHistParts + q];
     if (v) atomicAdd(hist + i, v);
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned t = atomicAdd(done, 1u);
+    last = t == gridDim.x - 1;
+    if (last) *done = 0u;  // every block has counted: reset for the next call
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // exclusive scans of the 8 histograms (warp p handles pass p; 8 bins per lane)
+  const int w = threadIdx.x >> 5;
+  if (w < kPasses) {
+    const volatile unsigned *hp = hist + w * kBins;
+    unsigned v[kBins / 32], run = 0;
+#pragma unroll
+    for (int q = 0; q < kBins / 32; ++q) {
+      v[q] = hp[lane * (kBins / 32) + q];
+      run += v[q];
+    }
+    unsigned incl = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned t = __shfl_up_sync(FULL, incl, o);
+      if (lane >= (unsigned)o) incl += t;
+    }
+    unsigned ex = incl - run;
+#pragma unroll
+    for (int q = 0; q < kBins / 32; ++q) {
+      bin_start[w * kBins + lane * (kBins / 32) + q] = ex;
+      ex += v[q];
+    }
   }
 }
 
 __global__ void k_sort_zero(unsigned *hist, unsigned *counters) {
   for (int i = threadIdx.x; i < kPasses * kBins; i += blockDim.x) hist[i] = 0u;
-  if (threadIdx.x < kPasses) counters[threadIdx.x] = 0u;
+  if (threadIdx.x <= kPasses) counters[threadIdx.x] = 0u;
 }
 
 // ------------------------------------------------------------ one digit pass
@@ -183,9 +226,10 @@ __device__ __forceinline__ unsigned block_excl_scan(unsigned v, unsigned *wsum, 
   return woff + incl - v;
 }
 
-__global__ void __launch_bounds__(kSortThreads) k_sort_pass(
+template <int MINB, bool MATCH>
+__global__ void __launch_bounds__(kSortThreads, MINB) k_sort_pass(
     const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin, uint64_t *__restrict__ kout,
-    uint32_t *__restrict__ vout, int64_t n, int shift, const unsigned *__restrict__ hist,
+    uint32_t *__restrict__ vout, int64_t n, int shift, const unsigned *__restrict__ bin_start,
     unsigned *__restrict__ counter, unsigned long long *__restrict__ st, unsigned epoch, unsigned ntiles) {
   extern __shared__ __align__(16) unsigned char sort_smem[];
   PassSmem &S = *reinterpret_cast<PassSmem *>(sort_smem);
@@ -197,13 +241,10 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(
     S.tile = t;
   }
   // global digit offsets (the 256 bins of this pass), zeroed warp counts
-  const unsigned hv = hist[threadIdx.x];
+  S.bin_start[threadIdx.x] = bin_start[threadIdx.x];
   for (int i = threadIdx.x; i < kSortWarps * kBins; i += kSortThreads) (&S.whist[0][0])[i] = 0u;
-  {
-    unsigned tot;
-    S.bin_start[threadIdx.x] = block_excl_scan(hv, S.wsum, &tot);
-  }
-  const unsigned tile = S.tile;  // ordered by the barriers inside the scan
+  __syncthreads();
+  const unsigned tile = S.tile;
   const int64_t tbase = (int64_t)tile * kTile;
   const int64_t wbase = tbase + (int64_t)w * 32 * kSortItems;
 
@@ -222,14 +263,30 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(
     }
   }
 
-  // ---- stable rank inside the warp (items in order, lanes in order)
+  // ---- stable rank inside the warp (items in order, lanes in order): the
+  // peer masks first (independent ballots), then the sequential counter walk
   unsigned rank[kSortItems];
   unsigned *wh = S.whist[w];
   const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
     const unsigned d = (unsigned)(k[j] >> shift) & (kBins - 1);
-    const unsigned peers = __match_any_sync(FULL, d);
+    unsigned peers = FULL;  // lanes whose digit equals this lane's
+    if (MATCH) {
+      peers = __match_any_sync(FULL, d);
+    } else {
+#pragma unroll
+      for (int b = 0; b < kDigitBits; ++b) {
+        const unsigned bb = __ballot_sync(FULL, (d >> b) & 1u);
+        peers &= ((d >> b) & 1u) ? bb : ~bb;
+      }
+    }
+    rank[j] = peers;
+  }
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    const unsigned d = (unsigned)(k[j] >> shift) & (kBins - 1);
+    const unsigned peers = rank[j];
     const unsigned base = wh[d];
     __syncwarp();
     const unsigned leader = 31u - __clz(peers);
@@ -263,16 +320,27 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(
     S.vals[lp] = v[j];
   }
 
-  // ---- decoupled look-back for digit d
+  // ---- decoupled look-back for digit d: four predecessors per round trip
   unsigned excl = 0;
   if (tile > 0) {
     int64_t j = (int64_t)tile - 1;
     for (;;) {
-      const unsigned long long s = ld_status(st + (size_t)j * kBins + d);
-      if ((unsigned)((s >> 32) & kEpochMask) != epoch || (s >> 62) == 0) continue;  // not yet published
-      excl += (unsigned)(s & kValMask);
-      if ((s >> 62) == 2ull) break;
-      --j;
+      unsigned long long sv[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        sv[q] = j - q >= 0 ? ld_status(st + (size_t)(j - q) * kBins + d) : pack(kFlagInc, epoch, 0u);
+      int used = 0;
+      bool done = false;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const unsigned long long x = sv[q];
+        if (used != q || (unsigned)((x >> 32) & kEpochMask) != epoch || (x >> 62) == 0) break;  // not yet published
+        excl += (unsigned)(x & kValMask);
+        ++used;
+        if ((x >> 62) == 2ull) { done = true; break; }
+      }
+      if (done) break;
+      j -= used;
     }
     st_status(my, pack(kFlagInc, epoch, excl + cnt));
   }
@@ -293,39 +361,20 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(
 }
 
 // ------------------------------------------------------------------ scan
+// Reduce-then-scan in three bandwidth-bound launches (12 B per element): the
+// single-pass look-back version spent most of its time in the serial chain of
+// 4096-element tiles (67 us for 1e7 elements at 8 blocks per SM).
+//   k_scan_reduce  tile sums          (read 4 B)
+//   k_scan_tiles   one block scans the tile sums
+//   k_scan_down    tile scan + prefix (read 4 B, write 4 B)
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 16;
 constexpr int kScanTile = kScanThreads * kScanItems;
+constexpr int kScanTopThreads = 1024;
 
-struct ScanTemp {
-  unsigned *counter;
-  unsigned long long *st;  // [tiles]
-};
-inline ScanTemp carve_scan(void *temp) {
-  char *p = static_cast<char *>(temp);
-  ScanTemp t;
-  t.counter = reinterpret_cast<unsigned *>(p);
-  t.st = reinterpret_cast<unsigned long long *>(p + 256);
-  return t;
-}
-
-template <bool INCLUSIVE>
-__global__ void __launch_bounds__(kScanThreads) k_scan_u32(const uint32_t *__restrict__ in, uint32_t *__restrict__ out,
-                                                           int64_t n, unsigned *counter, unsigned long long *st,
-                                                           unsigned epoch, unsigned ntiles) {
-  __shared__ unsigned s_wsum[kScanThreads / 32];
-  __shared__ unsigned s_tile, s_prefix;
-  const unsigned lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (threadIdx.x == 0) {
-    const unsigned t = atomicAdd(counter, 1u);
-    if (t == ntiles - 1) *counter = 0u;
-    s_tile = t;
-  }
-  __syncthreads();
-  const unsigned tile = s_tile;
-  const int64_t i0 = (int64_t)tile * kScanTile + (int64_t)threadIdx.x * kScanItems;
-  unsigned x[kScanItems];
-  if (i0 + kScanItems <= n && ((reinterpret_cast<uintptr_t>(in) & 15) == 0)) {
+__device__ __forceinline__ void scan_load(const uint32_t *__restrict__ in, int64_t i0, int64_t n,
+                                          unsigned (&x)[kScanItems]) {
+  if (i0 + kScanItems <= n && ((reinterpret_cast<uintptr_t>(in + i0) & 15) == 0)) {
     const uint4 *src = reinterpret_cast<const uint4 *>(in + i0);
 #pragma unroll
     for (int j = 0; j < kScanItems / 4; ++j) {
@@ -336,69 +385,98 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_u32(const uint32_t *__res
 #pragma unroll
     for (int j = 0; j < kScanItems; ++j) x[j] = i0 + j < n ? in[i0 + j] : 0u;
   }
-  unsigned sum = 0;
-#pragma unroll
-  for (int j = 0; j < kScanItems; ++j) sum += x[j];
-  // block scan of the thread sums
-  unsigned incl = sum;
+}
+
+// exclusive scan over a block of T threads, one value each; *total = block sum
+template <int T>
+__device__ __forceinline__ unsigned block_scan_t(unsigned v, unsigned *wsum, unsigned *total) {
+  const unsigned lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned incl = v;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= (unsigned)o) incl += t;
   }
-  if (lane == 31) s_wsum[w] = incl;
+  if (lane == 31) wsum[w] = incl;
   __syncthreads();
   unsigned woff = 0, tot = 0;
 #pragma unroll
-  for (int i = 0; i < kScanThreads / 32; ++i) {
-    const unsigned s = s_wsum[i];
+  for (int i = 0; i < T / 32; ++i) {
+    const unsigned s = wsum[i];
     woff += i < (int)w ? s : 0u;
     tot += s;
   }
-  // look-back by warp 0: 32 predecessors per step
-  if (w == 0) {
-    unsigned prefix = 0;
-    if (tile == 0) {
-      if (lane == 0) st_status(st, pack(kFlagInc, epoch, tot));
-    } else {
-      if (lane == 0) st_status(st + tile, pack(kFlagAgg, epoch, tot));
-      int64_t j = (int64_t)tile - 1 - lane;  // this lane's predecessor
-      for (;;) {
-        unsigned long long s = 0;
-        bool ready = true;
-        if (j >= 0) {
-          s = ld_status(st + j);
-          ready = (unsigned)((s >> 32) & kEpochMask) == epoch && (s >> 62) != 0;
-        }
-        if (!__all_sync(0xffffffffu, ready)) continue;
-        // lanes past tile 0 contribute nothing; the nearest inclusive entry ends the walk
-        const bool inc = j >= 0 && (s >> 62) == 2ull;
-        const unsigned incmask = __ballot_sync(0xffffffffu, inc || j < 0);
-        const unsigned first = incmask ? __ffs(incmask) - 1 : 32u;  // nearest inclusive
-        unsigned val = (j >= 0 && lane <= first) ? (unsigned)(s & kValMask) : 0u;
-#pragma unroll
-        for (int o = 16; o; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
-        prefix += val;
-        if (incmask) break;
-        j -= 32;
-      }
-      if (lane == 0) st_status(st + tile, pack(kFlagInc, epoch, prefix + tot));
-    }
-    if (lane == 0) s_prefix = prefix;
-  }
+  *total = tot;
   __syncthreads();
-  unsigned run = s_prefix + woff + incl - sum;
+  return woff + incl - v;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const uint32_t *__restrict__ in, int64_t n,
+                                                              unsigned *__restrict__ tsum) {
+  __shared__ unsigned wsum[kScanThreads / 32];
+  unsigned x[kScanItems];
+  scan_load(in, (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems, n, x);
+  unsigned s = 0;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) s += x[j];
+  s = __reduce_add_sync(0xffffffffu, s);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned t = 0;
+#pragma unroll
+    for (int i = 0; i < kScanThreads / 32; ++i) t += wsum[i];
+    tsum[blockIdx.x] = t;
+  }
+}
+
+// exclusive scan of the tile sums in place (one block, carried across chunks)
+__global__ void __launch_bounds__(kScanTopThreads) k_scan_tiles(unsigned *__restrict__ tsum, int64_t ntiles) {
+  __shared__ unsigned wsum[kScanTopThreads / 32];
+  unsigned carry = 0;
+  for (int64_t base = 0; base < ntiles; base += kScanTopThreads) {
+    const int64_t i = base + threadIdx.x;
+    const unsigned v = i < ntiles ? tsum[i] : 0u;
+    unsigned tot;
+    const unsigned ex = block_scan_t<kScanTopThreads>(v, wsum, &tot);
+    if (i < ntiles) tsum[i] = carry + ex;
+    carry += tot;
+  }
+}
+
+template <bool INCLUSIVE>
+__global__ void __launch_bounds__(kScanThreads) k_scan_down(const uint32_t *__restrict__ in, uint32_t *__restrict__ out,
+                                                            int64_t n, const unsigned *__restrict__ tprefix) {
+  __shared__ unsigned wsum[kScanThreads / 32];
+  const int64_t i0 = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  unsigned x[kScanItems];
+  scan_load(in, i0, n, x);
+  unsigned sum = 0;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) sum += x[j];
+  unsigned tot;
+  unsigned run = tprefix[blockIdx.x] + block_scan_t<kScanThreads>(sum, wsum, &tot);
+  unsigned y[kScanItems];
 #pragma unroll
   for (int j = 0; j < kScanItems; ++j) {
     if (INCLUSIVE) run += x[j];
-    if (i0 + j < n) out[i0 + j] = run;
+    y[j] = run;
     if (!INCLUSIVE) run += x[j];
+  }
+  if (i0 + kScanItems <= n && ((reinterpret_cast<uintptr_t>(out + i0) & 15) == 0)) {
+    uint4 *dst = reinterpret_cast<uint4 *>(out + i0);
+#pragma unroll
+    for (int j = 0; j < kScanItems / 4; ++j) dst[j] = make_uint4(y[4 * j], y[4 * j + 1], y[4 * j + 2], y[4 * j + 3]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j)
+      if (i0 + j < n) out[i0 + j] = y[j];
   }
 }
 
 inline size_t scan_bytes(int64_t n) {
   const int64_t tiles = std::max<int64_t>(1, (n + kScanTile - 1) / kScanTile);
-  return 256 + sizeof(unsigned long long) * (size_t)tiles;
+  return sizeof(unsigned) * (size_t)tiles + 256;
 }
 
 template <bool INCLUSIVE>
@@ -407,9 +485,10 @@ cudaError_t scan_u32(void *temp, size_t temp_bytes, const uint32_t *in, uint32_t
   if (temp_bytes < scan_bytes(n)) return cudaErrorInvalidValue;
   const int64_t tiles = (n + kScanTile - 1) / kScanTile;
   if (tiles > 0x7fffffff) return cudaErrorInvalidValue;
-  ScanTemp t = carve_scan(temp);
-  k_scan_u32<INCLUSIVE><<<(unsigned)tiles, kScanThreads, 0, s>>>(in, out, n, t.counter, t.st, next_epoch(),
-                                                                  (unsigned)tiles);
+  unsigned *tsum = static_cast<unsigned *>(temp);
+  k_scan_reduce<<<(unsigned)tiles, kScanThreads, 0, s>>>(in, n, tsum);
+  k_scan_tiles<<<1, kScanTopThreads, 0, s>>>(tsum, tiles);
+  k_scan_down<INCLUSIVE><<<(unsigned)tiles, kScanThreads, 0, s>>>(in, out, n, tsum);
   return cudaGetLastError();
 }
 
@@ -417,8 +496,8 @@ cudaError_t scan_u32(void *temp, size_t temp_bytes, const uint32_t *in, uint32_t
 
 size_t sort_temp_bytes(int64_t n) {
   const int64_t tiles = std::max<int64_t>(1, sort_tiles(n));
-  return al(sizeof(uint64_t) * n) + al(sizeof(uint32_t) * n) + al(sizeof(unsigned) * kPasses * kBins) +
-         al(sizeof(unsigned) * kPasses) + sizeof(unsigned long long) * kBins * (size_t)tiles;
+  return al(sizeof(uint64_t) * n) + al(sizeof(uint32_t) * n) + 2 * al(sizeof(unsigned) * kPasses * kBins) +
+         al(sizeof(unsigned) * (kPasses + 1)) + sizeof(unsigned long long) * kBins * (size_t)tiles;
 }
 
 cudaError_t sort_pairs(void *temp, size_t temp_bytes, const uint64_t *kin, uint64_t *kout, const uint32_t *vin,
@@ -427,11 +506,21 @@ cudaError_t sort_pairs(void *temp, size_t temp_bytes, const uint64_t *kin, uint6
   if (temp_bytes < sort_temp_bytes(n) || n > 0x7fffffffll) return cudaErrorInvalidValue;
   SortTemp t = carve_sort(temp, n);
   const unsigned tiles = (unsigned)sort_tiles(n);
-  static bool init = false;
-  if (!init) {
-    cudaFuncSetAttribute(k_sort_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PassSmem));
-    init = true;
+  // variants for measurement: BH_SORT_MINB=2 (no register cap), BH_SORT_MATCH=1
+  // (peer masks from MATCH.ANY instead of 8 ballots)
+  static int variant = -1;
+  if (variant < 0) {
+    const char *e = getenv("BH_SORT_MINB");
+    const char *m = getenv("BH_SORT_MATCH");
+    variant = ((e && atoi(e) == 2) ? 1 : 0) | ((m && atoi(m) == 1) ? 2 : 0);
+    const int sm = (int)sizeof(PassSmem);
+    cudaFuncSetAttribute(k_sort_pass<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_sort_pass<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_sort_pass<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_sort_pass<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
   }
+  auto pass = variant == 0 ? k_sort_pass<3, false> : variant == 1 ? k_sort_pass<2, false>
+            : variant == 2 ? k_sort_pass<3, true> : k_sort_pass<2, true>;
   k_sort_zero<<<1, 256, 0, s>>>(t.hist, t.counters);
   {
     static int sms = 0;
@@ -440,9 +529,15 @@ cudaError_t sort_pairs(void *temp, size_t temp_bytes, const uint64_t *kin, uint6
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
-    const int64_t need = (n + kHistThreads * kHistItems - 1) / (kHistThreads * kHistItems);
-    const int g = (int)std::max<int64_t>(1, std::min<int64_t>(need, 2 * sms));
-    k_sort_hist<<<g, kHistThreads, 0, s>>>(kin, n, t.hist);
+    const int64_t need = (n + kHistThreads * kHistUnroll - 1) / (kHistThreads * kHistUnroll);
+    const int g = (int)std::max<int64_t>(1, std::min<int64_t>(need, 3 * sms));
+    const int hsm = (int)(sizeof(unsigned) * kPasses * kBins * kHistParts);
+    static bool hinit = false;
+    if (!hinit) {
+      cudaFuncSetAttribute(k_sort_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, hsm);
+      hinit = true;
+    }
+    k_sort_hist<<<g, kHistThreads, hsm, s>>>(kin, n, t.hist, t.bin_start, t.counters + kPasses);
   }
   // 8 passes ping-pong between the temp pair and the output (even count: ends in kout)
   const uint64_t *ka = kin;
@@ -450,7 +545,7 @@ cudaError_t sort_pairs(void *temp, size_t temp_bytes, const uint64_t *kin, uint6
   for (int p = 0; p < kPasses; ++p) {
     uint64_t *kb = (p & 1) ? kout : t.k;
     uint32_t *vb = (p & 1) ? vout : t.v;
-    k_sort_pass<<<tiles, kSortThreads, sizeof(PassSmem), s>>>(ka, va, kb, vb, n, kDigitBits * p, t.hist + p * kBins,
+    pass<<<tiles, kSortThreads, sizeof(PassSmem), s>>>(ka, va, kb, vb, n, kDigitBits * p, t.bin_start + p * kBins,
                                                                t.counters + p, t.st, next_epoch(), tiles);
     ka = kb;
     va = vb;

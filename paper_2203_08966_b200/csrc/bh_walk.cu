@@ -48,6 +48,10 @@
 namespace bh {
 
 __device__ __forceinline__ int64_t tree_count(const TreeView &t) { return t.dC ? *t.dC : t.C; }
+// a sync-free build that overflowed its capacity built nothing (k_emit and
+// k_moments_coop returned early): the walk tree is then one empty root record,
+// so nothing below reads the unbuilt cells (the call is redone, bh_api.cu)
+__device__ __forceinline__ bool tree_overflowed(const TreeView &t) { return t.dC && *t.dC > t.C; }
 
 __device__ __forceinline__ int child_slot(const TreeView &t, int64_t c) {
   const int4 L = t.link[c];
@@ -67,7 +71,7 @@ __device__ __forceinline__ bool expandable(const TreeView &t, int64_t c, int lea
 // slot masks of the expandable cells
 __global__ void k_slots(TreeView t, int leaf, const uint8_t *force, uint32_t *__restrict__ smask) {
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c <= 0 || c >= tree_count(t) || c >= t.C) return;
+  if (c <= 0 || c >= tree_count(t) || c >= t.C || tree_overflowed(t)) return;
   const int P = t.parent[c];
   if (expandable(t, P, leaf, force)) atomicOr(&smask[P], 1u << child_slot(t, c));
 }
@@ -77,7 +81,7 @@ __global__ void k_nchild(TreeView t, int leaf, const uint8_t *force,
                          const uint32_t *__restrict__ smask, uint32_t *__restrict__ nck) {
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= t.C) return;
-  if (c >= tree_count(t)) {  // capacity tail (sync-free build): scans as zero
+  if (c >= tree_count(t) || tree_overflowed(t)) {  // capacity tail (sync-free build): scans as zero
     nck[c] = 0u;
     return;
   }
@@ -93,7 +97,7 @@ __global__ void k_nchild_rows(TreeView t, int leaf, uint32_t *__restrict__ nck) 
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= t.C) return;
   uint32_t k = 0u;
-  if (c < tree_count(t) && expandable(t, c, leaf, nullptr)) {
+  if (c < tree_count(t) && !tree_overflowed(t) && expandable(t, c, leaf, nullptr)) {
     const int4 *row = reinterpret_cast<const int4 *>(t.child8 + 8 * c);
     const int4 r0 = row[0], r1 = row[1];
     k = (r0.x != -1) + (r0.y != -1) + (r0.z != -1) + (r0.w != -1) + (r1.x != -1) + (r1.y != -1) +
@@ -109,6 +113,20 @@ __global__ void k_compact(TreeView t, const double *__restrict__ dR, double thet
                           int *__restrict__ rec_of_cell, int *__restrict__ wparent) {
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t C = tree_count(t);
+  if (tree_overflowed(t)) {  // one empty root record (count 0: the walk interacts with nothing)
+    if (c == 0) {
+      WalkNode nd;
+      nd.a = make_float4(0.f, 0.f, 0.f, 0.f);
+      nd.b = nd.a;
+      nd.c = nd.a;
+      nd.d = make_int4(0, 0, 0, 0);
+      out[0] = nd;
+      *dCp = 1;
+      if (rec_of_cell) rec_of_cell[0] = 0;
+      if (wparent) wparent[0] = -1;
+    }
+    return;
+  }
   if (c >= C || c >= t.C) return;
   if (c == C - 1) *dCp = (int)(1 + base[C - 1] + nck[C - 1]);
   int j = 0;

@@ -299,7 +299,16 @@ class DistributedSim:
 
     def _forces(self, record_work: bool, bounds_ready: bool) -> None:
         p = self.p
-        self.eng.sim_prepare(p.theta, p.eps, p.leaf_size, bounds_ready)
+        for _ in range(3):
+            self.eng.sim_prepare(p.theta, p.eps, p.leaf_size, bounds_ready)
+            # a build that overflowed its cell capacity is redone before any walk
+            # (the walk would store its rows into the peers); replicas build the
+            # same tree, so every rank takes the same branch
+            if not hasattr(self.eng, "sim_tree_fits") or self.eng.sim_tree_fits():
+                break
+            bounds_ready = False
+        else:
+            raise RuntimeError("tree cell capacity kept overflowing")
         b, e = self._zone()
         if getattr(self, "p2p", False):
             self.comm.stream_barrier()  # every rank is done reading its acc (the kick)

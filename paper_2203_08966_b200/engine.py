@@ -233,6 +233,16 @@ class Engine:
         check(self._L.bh_sim_prepare(self._h, float(theta), float(eps), int(leaf_size),
                                      int(bool(bounds_ready)), self.stream))
 
+    def sim_tree_fits(self) -> bool:
+        """After sim_prepare: False if the sync-free build overflowed its cell
+        capacity (the capacity is grown; prepare again).  One host sync."""
+        c = ctypes.c_int64()
+        rc = self._L.bh_tree_size(self._h, ctypes.byref(c))
+        if rc == _lib.BH_OUT_OF_MEMORY:
+            return False
+        check(rc)
+        return True
+
     def sim_walk_range(self, theta: float, eps: float, leaf_size: int, begin: int, end: int,
                        record_work: bool = True) -> None:
         check(self._L.bh_sim_walk_range(self._h, float(theta), float(eps), int(leaf_size),
@@ -369,15 +379,19 @@ class Engine:
                                                  _ptr(fcnc), self.stream))
 
     def sim_step_host(self, pos4: torch.Tensor, vel3: torch.Tensor, acc3: torch.Tensor, dt: float,
-                      theta: float, eps: float, leaf_size: int, steps: int = 1) -> None:
+                      theta: float, eps: float, leaf_size: int, steps: int = 1,
+                      work: torch.Tensor | None = None) -> None:
         """KDK steps on host (CPU, ideally pinned) float32 arrays pos4 (n,4), vel3/acc3
-        (n,3), updated in place; synchronous (bh_sim_step_host)."""
+        (n,3), updated in place; ``work`` (int32 (n,), optional) receives the last
+        force pass's per-body work; synchronous (bh_sim_step_host)."""
         for t, w in ((pos4, 4), (vel3, 3), (acc3, 3)):
             if t.device.type != "cpu" or t.dtype != torch.float32 or not t.is_contiguous() or t.shape[-1] != w:
                 raise ValueError("sim_step_host takes contiguous float32 host arrays (n,4), (n,3), (n,3)")
         n = pos4.shape[0]
-        check(self._L.bh_sim_step_host(self._h, _ptr(pos4), _ptr(vel3), _ptr(acc3), n, dt, theta, eps,
-                                       leaf_size, steps, self.stream))
+        if work is not None and (work.device.type != "cpu" or work.dtype != torch.int32 or work.shape != (n,)):
+            raise ValueError("sim_step_host: work must be a host int32 array of n entries")
+        check(self._L.bh_sim_step_host(self._h, _ptr(pos4), _ptr(vel3), _ptr(acc3), _ptr(work), n, dt, theta,
+                                       eps, leaf_size, steps, self.stream))
         torch.cuda.current_stream(self.device).synchronize()
 
     def sim_store(self, pos=None, vel=None, acc=None, work=None) -> None:

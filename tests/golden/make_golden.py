@@ -195,8 +195,53 @@ def gen_report() -> None:
     print("reports", [f for f in os.listdir(HERE) if f.startswith(("report_", "snapshot_"))])
 
 
+def gen_drift() -> None:
+    """Energy drift at N=1e5 (BASELINE cfg1 geometry: Plummer, make_rng(1)),
+    fp64, theta 0.5, eps 1e-3, dt 1e-3, 10 KDK steps, leaf size 1 (the
+    reference's only mode), from the reference package itself: E0, E1 via
+    physics.total_energy (O(N^2)), work totals, and 2000 sampled final states."""
+    theta, eps, dt, steps = 0.5, 1e-3, 1e-3, 10
+    bodies = plummer_cluster(100_000, make_rng(1), 1.0)
+    e0 = total_energy(bodies, eps)
+    acc, work = tree_accel(bodies, theta, eps)
+    bodies.acceleration[:] = acc
+    for _ in range(steps):
+        kick(bodies, 0.5 * dt)
+        drift(bodies, dt)
+        acc, work = tree_accel(bodies, theta, eps)
+        bodies.acceleration[:] = acc
+        kick(bodies, 0.5 * dt)
+    e1 = total_energy(bodies, eps)
+    idx = np.sort(np.random.default_rng(11).choice(len(bodies), 2000, replace=False))
+    np.savez_compressed(
+        os.path.join(HERE, "drift_1e5.npz"),
+        e0=e0, e1=e1, work_total=int(work.sum()), idx=idx, pos=bodies.position[idx],
+        vel=bodies.velocity[idx], acc=bodies.acceleration[idx], work=work[idx],
+        theta=theta, eps=eps, dt=dt, steps=steps,
+    )
+    print("drift", e0, e1, (e1 - e0) / abs(e0), int(work.sum()))
+
+
+def gen_serial() -> None:
+    """The reference wire format (hashed.py:324-346, octree.py:30-34) of the
+    goldens' trees, byte for byte."""
+    out = {}
+    for n, seed in [(1, 0), (2, 1), (64, 3), (400, 4)]:
+        b, bounds = sorted_bodies(n, seed)
+        out[f"n{n}_blob"] = np.frombuffer(build_hashed(b, bounds).to_serial_bytes(), dtype=np.uint8)
+        out[f"n{n}_mass"] = b.mass
+        out[f"n{n}_pos"] = b.position
+        out[f"n{n}_R"] = bounds.half_extent
+    np.savez_compressed(os.path.join(HERE, "serial.npz"), **out)
+    print("serial blobs", {k: v.size for k, v in out.items() if k.endswith("_blob")})
+
+
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "report":
     gen_report()
+elif __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "serial":
+    gen_serial()
+elif __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "drift":
+    gen_drift()
 elif __name__ == "__main__":
     gen_keys()
     gen_trees()
@@ -204,6 +249,8 @@ elif __name__ == "__main__":
     gen_cfg0()
     gen_work_totals()
     gen_report()
+    gen_serial()
+    gen_drift()
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))

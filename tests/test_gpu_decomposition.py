@@ -79,6 +79,31 @@ def test_emulated_ranks_match_single_gpu(precision, p2p, monkeypatch):
             np.testing.assert_array_equal(pos, multi[0][0])
 
 
+class _Cloud:
+    def __init__(self, pos, vel, mass):
+        self.position, self.velocity, self.mass = pos, vel, mass
+
+    def __len__(self):
+        return len(self.mass)
+
+
+def test_replicated_ranks_recover_from_capacity_overflow(monkeypatch):
+    """Bodies in close pairs give ~10 cells per body, past the sync-free
+    build's first capacity: every rank must redo its build before the walk
+    stores rows into the peers (not after a corrupted step)."""
+    monkeypatch.setenv("BH_P2P", "1")
+    rng = np.random.default_rng(5)
+    c = rng.uniform(-0.9, 0.9, (4000, 3))
+    pos = np.concatenate([c, c + [2.0 ** -19, 0.0, 0.0]]).astype(np.float32).astype(np.float64)
+    b = _Cloud(pos, rng.normal(0, 0.05, pos.shape), np.full(len(pos), 1.0 / len(pos)))
+    single = _run("fp32", 1, b, 2, theta=0.5, leaf=1)[0]
+    for pos_r, work, _, used in _run("fp32", 2, b, 2, theta=0.5, leaf=1):
+        assert used
+        rel = np.abs(pos_r - single[0]).max() / np.abs(single[0]).max()
+        assert rel < 1e-5, rel
+        assert np.mean(work != single[1]) < 1e-3
+
+
 def _run_build(ranks, b, steps, theta=0.6, eps=1e-3, leaf=16, dt=1e-3):
     """Stage 2 (distributed build) with R emulated ranks; returns per-gid arrays."""
     from paper_2203_08966_b200.decomposition import DistributedBuildSim, StepParams, ThreadComm

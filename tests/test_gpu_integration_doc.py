@@ -40,7 +40,9 @@ def test_integration_stub_runs_and_matches_engine(monkeypatch):
     hp = torch.as_tensor(np.c_[x, m], dtype=torch.float32).pin_memory()
     hv = torch.zeros((len(m), 3), dtype=torch.float32).pin_memory()
     ha = torch.zeros((len(m), 3), dtype=torch.float32).pin_memory()
-    eng.sim_step_host(hp, hv, ha, 1e-3, 0.6, 1e-3, 16, 1)
+    hw = torch.zeros(len(m), dtype=torch.int32).pin_memory()
+    eng.sim_step_host(hp, hv, ha, 1e-3, 0.6, 1e-3, 16, 1, work=hw)
+    np.testing.assert_array_equal(ns["hw"].numpy(), hw.numpy())
     np.testing.assert_array_equal(ns["hp"].numpy(), hp.numpy())
     np.testing.assert_array_equal(ns["hv"].numpy(), hv.numpy())
     np.testing.assert_array_equal(ns["ha"].numpy(), ha.numpy())

@@ -167,6 +167,18 @@ class TestBuild:
         blob = build_hashed(b, DomainBounds(float(g["n64_R"]))).to_serial_bytes()
         assert blob[:4] == b"OCT1" and len(blob) == 12 + 121 * len(g["n64_t_count"])
 
+    @pytest.mark.parametrize("n", [1, 2, 64, 400])
+    def test_serial_bytes_equal_reference_blob(self, golden, n):
+        """hashed.py:324-346 to_serial_bytes of the reference's own build, byte for byte."""
+        from paper_2203_08966_b200.hashed import build_hashed
+        from paper_2203_08966_b200.morton import DomainBounds
+        from paper_2203_08966_b200.physics import Bodies
+
+        g = golden("serial.npz")
+        b = Bodies(g[f"n{n}_mass"], g[f"n{n}_pos"], np.zeros((n, 3)))
+        blob = build_hashed(b, DomainBounds(float(g[f"n{n}_R"]))).to_serial_bytes()
+        assert blob == g[f"n{n}_blob"].tobytes()
+
     def test_errors(self):
         from paper_2203_08966_b200.hashed import build_hashed
         from paper_2203_08966_b200.morton import DomainBounds
@@ -500,11 +512,101 @@ def test_sim_step_host_matches_device_path(steps):
     eng.sim_load(pos, vel, acc=acc)
     eng.sim_step(1e-3, 0.6, 1e-3, 16, steps)
     p2, v2, a2 = torch.empty_like(vel), torch.empty_like(vel), torch.empty_like(vel)
-    eng.sim_store(p2, v2, a2)
-    # host path
-    eng.sim_step_host(hp, hv, ha, 1e-3, 0.6, 1e-3, 16, steps)
+    w2 = torch.empty(len(b), dtype=torch.int64, device="cuda")
+    eng.sim_store(p2, v2, a2, w2)
+    # host path (per-body work of the last force pass comes back too)
+    hw = torch.zeros(len(b), dtype=torch.int32).pin_memory()
+    eng.sim_step_host(hp, hv, ha, 1e-3, 0.6, 1e-3, 16, steps, work=hw)
     eng.check()
     np.testing.assert_array_equal(hp.numpy(), p2.cpu().numpy())
     np.testing.assert_array_equal(hv.numpy(), v2[:, :3].cpu().numpy())
     np.testing.assert_array_equal(ha.numpy(), a2[:, :3].cpu().numpy())
+    np.testing.assert_array_equal(hw.numpy().astype(np.int64), w2.cpu().numpy())
+    assert hw.numpy().min() >= 1
     eng.close()
+
+
+def _close_pairs(npairs: int, seed: int):
+    """Bodies in pairs 2^-19 apart: each pair adds a chain of ~18 single-child
+    cells, so the tree has ~10 cells per body -- far above the sync-free build's
+    first capacity (2n + 1024)."""
+    rng = np.random.default_rng(seed)
+    c = rng.uniform(-0.9, 0.9, (npairs, 3))
+    d = np.zeros((npairs, 3))
+    d[:, 0] = 2.0 ** -19
+    pos = np.concatenate([c, c + d]).astype(np.float32).astype(np.float64)
+    vel = rng.normal(0, 0.05, pos.shape)
+    return pos, vel, np.full(len(pos), 1.0 / len(pos))
+
+
+@pytest.mark.parametrize("steps,host", [(1, False), (3, False), (1, True)])
+def test_capacity_overflow_inside_a_step_call_is_redone_exactly(steps, host):
+    """A sync-free build that overflows inside bh_sim_step / bh_sim_step_host is
+    redone from the failed step's kick+drift state (no snapshot): the result is
+    bit-identical to the same call on a handle whose capacity already fits."""
+    from paper_2203_08966_b200.engine import Engine
+
+    pos, vel, m = _close_pairs(6000, 3)
+    outs = []
+    for pregrow in (False, True):
+        eng = Engine("fp32", 0)
+        p = eng.bodies_tensor(pos, m)
+        v = eng.vec_tensor(vel)
+        if pregrow:  # a force pass grows the capacity to fit (it retries internally)
+            eng.sim_load(p, v)
+            eng.sim_forces(0.5, 1e-3, 1, False)
+            assert eng.tree_size() > 2 * len(m) + 1024  # the case the test is about
+        eng.sim_load(p, v)  # acc = 0, work = 1 on both handles
+        if host:
+            hp = p.cpu().pin_memory()
+            hv = v[:, :3].contiguous().cpu().pin_memory()
+            ha = torch.zeros((len(m), 3), dtype=torch.float32).pin_memory()
+            hw = torch.zeros(len(m), dtype=torch.int32).pin_memory()
+            eng.sim_step_host(hp, hv, ha, 1e-3, 0.5, 1e-3, 1, steps, work=hw)
+            outs.append([hp.numpy().copy(), hv.numpy().copy(), ha.numpy().copy(), hw.numpy().copy()])
+        else:
+            eng.sim_step(1e-3, 0.5, 1e-3, 1, steps)
+            p2, v2, a2 = torch.empty_like(v), torch.empty_like(v), torch.empty_like(v)
+            w2 = torch.empty(len(m), dtype=torch.int64, device="cuda")
+            eng.sim_store(p2, v2, a2, w2)
+            outs.append([x.cpu().numpy() for x in (p2, v2, a2, w2)])
+        eng.check()
+        eng.close()
+    for a, b in zip(*outs):
+        np.testing.assert_array_equal(a, b)
+    assert np.abs(outs[0][2]).max() > 0  # forces really ran
+
+
+def test_energy_drift_1e5_matches_reference(golden):
+    """Row f2 at N >= 1e5: BASELINE cfg1 geometry (Plummer 1e5, make_rng(1)),
+    fp64, theta 0.5, eps 1e-3, dt 1e-3, 10 KDK steps, leaf size 1.  The GPU
+    trajectory and its GPU O(N^2) energy audit give the reference's own energy
+    drift (tests/golden/drift_1e5.npz, produced by running nbsim) within 1%."""
+    from paper_2203_08966_b200.engine import Engine
+    from paper_2203_08966_b200.physics import Bodies, total_energy
+
+    g = golden("drift_1e5.npz")
+    theta, eps, dt, steps = float(g["theta"]), float(g["eps"]), float(g["dt"]), int(g["steps"])
+    b = plummer(100_000, 1)
+    e0 = total_energy(b, eps)
+    eng = Engine("fp64", 0)
+    pos = eng.bodies_tensor(b.position)
+    vel = eng.vec_tensor(b.velocity)
+    eng.sim_load(pos, vel, torch.as_tensor(b.mass).cuda())
+    eng.sim_forces(theta, eps, 1, record_work=False)
+    eng.sim_step(dt, theta, eps, 1, steps)
+    p, v, a = torch.empty_like(pos), torch.empty_like(vel), torch.empty_like(vel)
+    w = torch.empty(len(b), dtype=torch.int64, device="cuda")
+    eng.sim_store(p, v, a, w)
+    eng.check()
+    eng.close()
+    x, u, acc, work = (t.cpu().numpy() for t in (p, v, a, w))
+    e1 = total_energy(Bodies(b.mass, x, u), eps)
+    drift, ref_drift = (e1 - e0) / abs(e0), (float(g["e1"]) - float(g["e0"])) / abs(float(g["e0"]))
+    assert abs(e0 - float(g["e0"])) <= 1e-12 * abs(float(g["e0"]))
+    assert abs(drift - ref_drift) <= 0.01 * abs(ref_drift), (drift, ref_drift)
+    idx = g["idx"]  # the trajectory after 10 steps (fp64 bar of the north star)
+    assert rel_l2(x[idx], g["pos"]) <= FP64_TOL
+    assert rel_l2(acc[idx], g["acc"]) <= FP64_TOL
+    np.testing.assert_array_equal(work[idx], g["work"])
+    assert int(work.sum()) == int(g["work_total"])

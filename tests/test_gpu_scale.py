@@ -20,7 +20,7 @@ from oracle import oracle as orc  # noqa: E402
 FP32_TOL = 1e-4  # relative L2, fp32 mode (north star)
 
 
-def _gpu_forces(pos32, m32, theta, eps, leaf, allow_dup):
+def _gpu_forces(pos32, m32, theta, eps, leaf, allow_dup, sample=None):
     from paper_2203_08966_b200.engine import Engine
 
     eng = Engine("fp32", 0)
@@ -36,6 +36,9 @@ def _gpu_forces(pos32, m32, theta, eps, leaf, allow_dup):
     eng.check()
     st = eng.stats()
     eng.close()
+    if sample is not None:  # (sampled acc, sampled work, total work, stats)
+        t = torch.as_tensor(sample, device="cuda")
+        return acc[t, :3].double().cpu().numpy(), work[t].cpu().numpy(), int(work.sum().item()), st
     return acc[:, :3].double().cpu().numpy(), work.cpu().numpy(), st
 
 
@@ -77,3 +80,31 @@ def test_cfg4_shape_sampled_parity():
     pos32, _, m32 = hernquist_cosmology(2_000_000, 4)
     err, mism = _check(pos32, m32, 0.7, 1e-5, 32, allow_dup=True)
     print(f"cfg4 shape 2e6: sampled rel L2 {err:.2e}, work mismatches {mism:.1e}")
+
+
+def test_cfg4_full_size_sampled_parity():
+    """BASELINE cfg4 at the size the bench runs (N=1e8, one GPU): the resident
+    sim_forces path against the oracle's full 1e8-body tree on 4000 sampled
+    targets.  The oracle's answers are a committed fixture
+    (tests/golden/make_cfg4_fixture.py: the serial build needs ~30 GB of host
+    memory); the generator is deterministic, so the inputs are regenerated."""
+    import os
+
+    from paper_2203_08966_b200.initcond import hernquist_cosmology
+
+    path = os.path.join(os.path.dirname(__file__), "golden", "cfg4_sample_100000000.npz")
+    g = np.load(path)
+    n = int(g["n"])
+    pos32, _, m32 = hernquist_cosmology(n, 4)
+    idx = g["idx"]
+    acc, work, wsum, st = _gpu_forces(pos32, m32, float(g["theta"]), float(g["eps"]), int(g["leaf"]), True,
+                                      sample=idx)
+    del pos32, m32
+    assert np.all(np.isfinite(acc))
+    err = float(np.linalg.norm(acc - g["acc"]) / np.linalg.norm(g["acc"]))
+    assert err <= FP32_TOL, err
+    mism = int(np.sum(work != g["work"]))
+    assert mism <= 2, mism  # fp32 vs fp64 d2 at a MAC tie
+    assert st.n_cells == int(g["cells"])  # the same tree (bucket-mode duplicates included)
+    assert st.pp + 2 * st.pc == wsum
+    print(f"cfg4 1e8: sampled rel L2 {err:.2e}, work mismatches {mism}/{len(idx)}, cells {st.n_cells}")

@@ -215,3 +215,35 @@ class TestDuplicateKeys:
         acc, _ = orc.traverse(t, pos, 0.0, 0.05, leaf_size=4)
         ref = orc.direct_accelerations(m, pos, 0.05)
         np.testing.assert_allclose(acc, ref, rtol=1e-12, atol=1e-14)
+
+
+class TestSerialBytes:
+    """The wire format (hashed.py:324-346): the product's serializer applied to
+    the oracle's tree arrays equals the reference's own blob byte for byte (the
+    GPU test checks the device-built tree the same way)."""
+
+    @pytest.mark.parametrize("n", [1, 2, 64, 400])
+    def test_oracle_tree_serializes_to_reference_blob(self, golden, n):
+        from paper_2203_08966_b200.hashed import DeviceTree
+
+        g = golden("serial.npz")
+        t = orc.build_tree(g[f"n{n}_mass"], g[f"n{n}_pos"], float(g[f"n{n}_R"]))
+        dt = DeviceTree(None, n, len(t), None)
+        dt._arrays = {k: getattr(t, k) for k in ("key", "level", "centre", "side", "mass", "com", "quad",
+                                                 "count", "children")}
+        assert dt.to_serial_bytes() == g[f"n{n}_blob"].tobytes()
+
+
+class TestInitialConditions:
+    def test_oracle_plummer_sampler_matches_golden(self, golden):
+        """initcond.py:62-77 restated in the oracle (bench.py's reference arm
+        inputs) reproduces the reference's cfg0 clusters bit for bit."""
+        g = golden("plummer.npz")
+        rng = orc.make_rng(0)
+        ma, pa, va = orc.plummer_cluster(1000, rng, 1.0)
+        mb, pb, vb = orc.plummer_cluster(1000, rng, 1.0)
+        np.testing.assert_array_equal(pa, g["a_pos"])
+        np.testing.assert_array_equal(va, g["a_vel"])
+        np.testing.assert_array_equal(ma, g["a_mass"])
+        np.testing.assert_array_equal(pb, g["b_pos"])
+        np.testing.assert_array_equal(vb, g["b_vel"])

@@ -32,7 +32,11 @@ out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-so
 rows = list(csv.reader(io.StringIO(out)))
 h = rows[1]
 iW, iI = h.index("Warp Stall Sampling (All Samples)"), h.index("Instructions Executed")
-data = rows[2:]
+data = []
+for r in rows[2:]:  # the first profiled launch only
+    if not r or not re.fullmatch(r"[0-9a-fA-Fx]+", r[0]):
+        break
+    data.append(r)
 base = int(data[0][0], 16)
 W, I = defaultdict(float), defaultdict(float)
 stall_cols = [(i, c.replace("stall_", "")) for i, c in enumerate(h) if c.startswith("stall_") and "Not Issued" not in c]
