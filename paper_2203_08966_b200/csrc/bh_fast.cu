@@ -165,6 +165,8 @@ void launch_iota64(int64_t *out, const uint32_t *vals, int64_t n, cudaStream_t s
 // --------------------------------------------------- FFMA peak microbench
 // 8 independent FFMA chains per thread, 8 warps x 4 blocks per SM: the FP32
 // pipe's sustained issue rate at the current clock (walk roofline denominator)
+__device__ __forceinline__ float fma_t(float x, float a, float b) { return fmaf(x, a, b); }
+__device__ __forceinline__ double fma_t(double x, double a, double b) { return fma(x, a, b); }
 template <class T>
 __global__ void __launch_bounds__(256) k_ffma(T *out, int iters, T a, T b) {
   T x[8];
@@ -174,7 +176,7 @@ __global__ void __launch_bounds__(256) k_ffma(T *out, int iters, T a, T b) {
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
 #pragma unroll
-      for (int k = 0; k < 8; ++k) x[k] = fmaf(x[k], a, b);
+      for (int k = 0; k < 8; ++k) x[k] = fma_t(x[k], a, b);
     }
   }
   T sum = 0;

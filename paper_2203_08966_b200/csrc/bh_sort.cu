@@ -99,7 +99,8 @@ inline SortTemp carve_sort(void *temp, int64_t n) {
 // warp-uniform; same-address atomics from 32 lanes would serialise).  The last
 // block to finish turns the histograms into exclusive bin offsets.
 constexpr int kHistUnroll = 4;
-constexpr int kHistParts = 8;  // interleaved copies: lanes with equal digits hit 8 banks
+constexpr int kHistParts = 4;  // interleaved copies: fewer bank conflicts between lanes
+static_assert(kDigitBits == 8 && kPasses == 8, "byte digits: 4 from each 32-bit half of the key");
 __global__ void __launch_bounds__(kHistThreads) k_sort_hist(const uint64_t *__restrict__ keys, int64_t n,
                                                             unsigned *__restrict__ hist,
                                                             unsigned *__restrict__ bin_start,
@@ -118,29 +119,25 @@ __global__ void __launch_bounds__(kHistThreads) k_sort_hist(const uint64_t *__re
       const int64_t i = base + 32 * u + lane;
       k[u] = i < n ? __ldcs(keys + i) : 0ull;
     }
-    if (base + 32 * kHistUnroll <= n) {  // full groups
 #pragma unroll
-      for (int u = 0; u < kHistUnroll; ++u) {
+    for (int u = 0; u < kHistUnroll; ++u) {
+      const bool valid = base + 32 * u + lane < n;
+      const unsigned lo = (unsigned)k[u], hi = (unsigned)(k[u] >> 32);
+      if (valid) {  // the low bytes vary from key to key
 #pragma unroll
-        for (int p = 0; p < kPasses; ++p) {
-          const unsigned d = (unsigned)(k[u] >> (kDigitBits * p)) & (kBins - 1);
-          const unsigned d0 = __shfl_sync(FULL, d, 0);
-          if (__all_sync(FULL, d == d0)) {
-            if (lane == 0) atomicAdd(&hist_smem[(p * kBins + d0) * kHistParts], 32u);
-          } else {
-            atomicAdd(&hist_smem[(p * kBins + d) * kHistParts + part], 1u);
-          }
-        }
+        for (int p = 0; p < 4; ++p)
+          atomicAdd(&hist_smem[(p * kBins + ((lo >> (8 * p)) & 0xffu)) * kHistParts + part], 1u);
       }
-    } else {
+      // the high bytes are mostly shared by a warp's 32 consecutive keys
+      const unsigned hi0 = __shfl_sync(FULL, hi, 0);
+      const unsigned vm = __ballot_sync(FULL, valid);
+      if (__all_sync(FULL, !valid || hi == hi0)) {
+        if (lane < 4) atomicAdd(&hist_smem[((4 + lane) * kBins + ((hi0 >> (8 * lane)) & 0xffu)) * kHistParts],
+                                (unsigned)__popc(vm));
+      } else if (valid) {
 #pragma unroll
-      for (int u = 0; u < kHistUnroll; ++u) {
-        if (base + 32 * u + lane < n) {
-#pragma unroll
-          for (int p = 0; p < kPasses; ++p)
-            atomicAdd(&hist_smem[(p * kBins + ((unsigned)(k[u] >> (kDigitBits * p)) & (kBins - 1))) * kHistParts + part],
-                      1u);
-        }
+        for (int p = 0; p < 4; ++p)
+          atomicAdd(&hist_smem[((4 + p) * kBins + ((hi >> (8 * p)) & 0xffu)) * kHistParts + part], 1u);
       }
     }
   }

@@ -654,12 +654,56 @@ constexpr int kW9Block = BH_W9_BLOCK;
 constexpr int kW9PcUnroll = BH_W9_PCUNROLL;
 constexpr int kW9NcShift = 28;  // frontier entry: first_child | nchild << 28, unsigned (records < 2^28)
 
+#ifndef BH_W9_PC30
+#define BH_W9_PC30 1  // pc: a += R5 (Qd + d (-M d2 - 2.5 dQd R2)): 30 packed FP ops instead of 31
+#endif
+#ifndef BH_W9_BULK
+#define BH_W9_BULK 0  // 1: accepted records reach shared memory by cp.async.bulk (mbarrier-completed)
+#endif
+
+// cp.async.bulk (the bulk-copy / TMA engine) of one 48-byte record prefix into
+// shared memory, completing on a per-warp mbarrier.  The barrier expects one
+// arrival per phase (the flush) plus the bytes each copy announces.
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_copy_48(void *dst, const void *src, uint64_t *bar) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], 48;" ::"r"(smem_u32(bar)) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 48, [%2];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(smem_u32(bar))
+      : "memory");
+}
+// the flush: one arrival completes the phase once every announced byte landed
+__device__ __forceinline__ void mbar_arrive_wait(uint64_t *bar, unsigned &phase, bool arrive) {
+  if (arrive) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  }
+  phase ^= 1u;
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 // Per-warp shared memory (~7.4 KB).  Masks ride in record words the drains do
 // not read: a.w (mac2) and b.z (the duplicate qxy) of a staged pc record, b.z
-// and d.w (level) of a staged mixed record.
+// and d.w (level) of a staged mixed record.  (BH_W9_BULK: the pc records are
+// bulk copies of the global records, so their masks sit in pcm.)
 struct W9Warp {
   int fc[kW9Frontier];     // frontier: first_child | nchild << kW9NcShift
   uint2 fm[kW9Frontier];   //           (mask0, mask1)
+#if BH_W9_BULK
+  uint64_t bar;            // completes the bulk copies of one flush
+  uint2 pcm[kW9List];      // masks of the staged pc records
+#endif
   float4 pcr[kW9List][3];  // accepted cells: a (mask0 in .w), b (mask1 in .z), c
   int4 pp[kW9List];        // pp: (lo, count, mask0, mask1) or a leaf record (cell, 0, ...)
   float4 mxr[32][3];       // mixed cells of the batch: a, b (mask0 in .z), c
@@ -737,34 +781,59 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
       S.fm[0] = make_uint2(m0, m1);
     }
   }
+#if BH_W9_BULK
+  unsigned bphase = 0;
+  if (lane == 0) mbar_init(&S.bar, 1);
+#endif
   __syncwarp();
 
   // dense pc over the list (the FP32-pipe work)
   auto flush_pc = [&](int n) {
+#if BH_W9_BULK
+    mbar_arrive_wait(&S.bar, bphase, lane == 0);  // the staged records have landed
+#endif
 #pragma unroll(kW9PcUnroll)
     for (int k = 0; k < n; ++k) {
       const float4 a = S.pcr[k][0];
       const float4 b = S.pcr[k][1];
       const float4 q = S.pcr[k][2];
+#if BH_W9_BULK
+      const uint2 mk = S.pcm[k];
+      const bool u0 = mk.x & bit, u1 = mk.y & bit;
+#else
       const bool u0 = (unsigned)__float_as_int(a.w) & bit, u1 = (unsigned)__float_as_int(b.z) & bit;
+#endif
       const float2 DX = __fadd2_rn(X, f2(a.x));
       const float2 DY = __fadd2_rn(Y, f2(a.y));
       const float2 DZ = __fadd2_rn(Z, f2(a.z));
       const float2 D2 = __ffma2_rn(DZ, DZ, __ffma2_rn(DY, DY, __fmul2_rn(DX, DX)));
       const float2 R = f2(u0 ? rsqrtf(D2.x) : 0.f, u1 ? rsqrtf(D2.y) : 0.f);
       const float2 R2 = __fmul2_rn(R, R);
-      const float2 R3 = __fmul2_rn(R2, R);
-      const float2 R5 = __fmul2_rn(R3, R2);
       const float2 QX = __ffma2_rn(f2(q.x), DZ, __ffma2_rn(f2(b.y), DY, __fmul2_rn(f2(b.x), DX)));
       const float2 QY = __ffma2_rn(f2(q.y), DZ, __ffma2_rn(f2(b.w), DY, __fmul2_rn(f2(b.y), DX)));
       const float2 QZ = __ffma2_rn(f2(q.w), DZ, __ffma2_rn(f2(q.y), DY, __fmul2_rn(f2(q.x), DX)));
       const float2 RQR = __ffma2_rn(DZ, QZ, __ffma2_rn(DY, QY, __fmul2_rn(DX, QX)));
+#if BH_W9_PC30
+      // -M d/r^3 + Qd/r^5 - 2.5 (dQd) d/r^7 = r^-5 (Qd + d (-M d2 - 2.5 dQd r^-2))
+      const float2 R5 = __fmul2_rn(__fmul2_rn(R2, R2), R);
+      const float2 V = __ffma2_rn(__fmul2_rn(RQR, R2), f2(-2.5f), __fmul2_rn(f2(-q.z), D2));
+      AX = __ffma2_rn(R5, __ffma2_rn(DX, V, QX), AX);
+      AY = __ffma2_rn(R5, __ffma2_rn(DY, V, QY), AY);
+      AZ = __ffma2_rn(R5, __ffma2_rn(DZ, V, QZ), AZ);
+#else
+      const float2 R3 = __fmul2_rn(R2, R);
+      const float2 R5 = __fmul2_rn(R3, R2);
       const float2 Sc = __fmul2_rn(__ffma2_rn(__fmul2_rn(RQR, __fmul2_rn(R2, R2)), f2(-2.5f), f2(-q.z)), R3);
       AX = __ffma2_rn(R5, QX, __ffma2_rn(Sc, DX, AX));
       AY = __ffma2_rn(R5, QY, __ffma2_rn(Sc, DY, AY));
       AZ = __ffma2_rn(R5, QZ, __ffma2_rn(Sc, DZ, AZ));
+#endif
       pc0 += u0; pc1 += u1;
     }
+#if BH_W9_BULK
+    __syncwarp();
+    fence_proxy_async();  // these reads precede the next bulk writes into the list
+#endif
   };
   // dense pp over the bodies of the listed leaves / buckets (self skipped by r2 > 0)
   auto flush_pp = [&](int n) {
@@ -882,11 +951,16 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
                                                    : make_int4(d.x, d.y, (int)m0, (int)m1);
     if (to_pc) {
       const int slot = npc + __popc(bpc & lt);
+#if BH_W9_BULK
+      S.pcm[slot] = make_uint2(m0, m1);
+      bulk_copy_48(&S.pcr[slot][0], T + cell, &S.bar);
+#else
       float4 b = T[cell].b;
       b.z = __int_as_float((int)m1);
       S.pcr[slot][0] = make_float4(a.x, a.y, a.z, __int_as_float((int)m0));
       S.pcr[slot][1] = b;
       S.pcr[slot][2] = T[cell].c;
+#endif
     }
     if (to_fr) {
       const int slot = sp + __popc(bfr & lt);
