@@ -275,6 +275,12 @@ class DistributedSim:
                 ptrs = self.comm.allgather_bytes(self.eng.sim_result_ptrs())
                 self.eng.sim_set_peer_ptrs([ptrs[q] for q in range(size) if q != me])
             else:
+                # NVLink stores need peer access between every pair of devices
+                # (ranks sharing one device always have it)
+                devs = [int(d) for d in self.comm.allgather_bytes(str(self.eng.device.index).encode())]
+                mine = self.eng.device.index
+                if not all(d == mine or torch.cuda.can_device_access_peer(mine, d) for d in devs):
+                    raise RuntimeError("no peer access between the ranks' devices")
                 hs = self.comm.allgather_bytes(self.eng.sim_ipc_handles())
                 self.eng.sim_set_peers([hs[q] for q in range(size) if q != me])
             ok = 1

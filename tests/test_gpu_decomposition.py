@@ -286,3 +286,30 @@ def test_simulate_devices2_matches_one_device(tmp_path, scheme, p2p):
     np.testing.assert_array_equal(got["work"], ref.bodies.work)
     np.testing.assert_allclose(got["pos"], ref.bodies.position, rtol=0, atol=1e-5)
     np.testing.assert_allclose(got["vel"], ref.bodies.velocity, rtol=0, atol=1e-4)
+
+
+@pytest.mark.parametrize("scheme", ["distributed", "replicated"])
+def test_eight_ranks_cfg3_geometry(scheme, monkeypatch):
+    """The 8-GPU split of BASELINE cfg3 (two colliding Plummer clusters,
+    theta 0.6, eps 1e-4, leaf 32, dt 5e-4), emulated as 8 ranks on one GPU,
+    2 steps at 2e5 bodies: per-body work equal to one GPU, accelerations to
+    fp32 summation order, every rank holding a share of the bodies."""
+    from paper_2203_08966_b200.initcond import colliding_plummers
+
+    b = colliding_plummers(100_000, 3)
+    kw = dict(theta=0.6, eps=1e-4, leaf=32, dt=5e-4)
+    ref = _single(b, 2, **kw)
+    if scheme == "distributed":
+        got = _run_build(8, b, 2, **kw)
+        assert min(got["counts"]) > 0.2 * len(b) / 8
+        assert np.mean(got["work"] != ref["work"]) < 1e-3
+        err = np.linalg.norm(got["acc"][:, :3] - ref["acc"][:, :3]) / np.linalg.norm(ref["acc"][:, :3])
+        assert err < 1e-5, err
+    else:
+        monkeypatch.setenv("BH_P2P", "1")
+        outs = _run("fp32", 8, b, 2, **kw)
+        for pos, work, zones, used in outs:
+            assert used and len(zones) == 9
+            assert np.mean(work != ref["work"]) < 1e-3
+            rel = np.abs(pos - ref["pos"][:, :3]).max() / np.abs(ref["pos"][:, :3]).max()
+            assert rel < 1e-5, rel
