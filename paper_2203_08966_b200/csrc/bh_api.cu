@@ -72,6 +72,7 @@ struct bh_handle {
   bool async_tree = false;
   int64_t cap = 0, C_true = 0;
   int cur_step = 0;       // step index inside a bh_sim_step call (recorded on overflow)
+  int mom_leaf = 0;       // > 0: the moments cover only what a walk with leaf size >= mom_leaf reads
   int *dCtrue = nullptr;
   int *hstat = nullptr;  // pinned: [0] = C, [1..22] = internal cells per level
   int grid_lvl[kMaxLevel + 1] = {0};
@@ -271,6 +272,7 @@ int build_sorted(bh_handle *h, int64_t n, const float4 *bod32, const double4 *bo
   h->C = C;
   h->C_true = C;
   h->async_tree = false;
+  h->mom_leaf = 0;
   h->tree_n = n;
   h->R = *h->hR;
   BH_CUDA(h->link.ensure(sizeof(int4) * C));
@@ -313,7 +315,7 @@ int build_sorted(bh_handle *h, int64_t n, const float4 *bod32, const double4 *bo
 // capacity (2n, grown from the largest tree seen) and an overflow is flagged,
 // detected at the end of the bh_sim_step call and repaired by re-running it.
 int build_sorted_async(bh_handle *h, int64_t n, const float4 *bod32, cudaStream_t s,
-                       int allow_dup) {
+                       int allow_dup, int leaf) {
   if (n <= 1) return build_sorted(h, n, bod32, nullptr, s, allow_dup);
   int64_t cap = std::max<int64_t>(h->cap, 2 * n + 1024);
   if (cap > 0x7fffffffll) cap = 0x7fffffffll;
@@ -343,7 +345,9 @@ int build_sorted_async(bh_handle *h, int64_t n, const float4 *bod32, cudaStream_
   h->tbod64 = nullptr;
   TreeView t = h->view();
   launch_emit(t, bod32, nullptr, s);
-  BH_CUDA((cudaError_t)launch_moments_coop(t, h->lvl.as<int>(), h->lvl_list.as<int>(), h->sms, s));
+  // a walk-only tree: moments of the cells a leaf-size-`leaf` walk reads
+  BH_CUDA((cudaError_t)launch_moments_coop(t, h->lvl.as<int>(), h->lvl_list.as<int>(), h->sms, s, leaf));
+  h->mom_leaf = leaf > 1 ? leaf : 0;
   h->launches += 4;
   BH_LAUNCHED();
   return BH_OK;
@@ -398,6 +402,10 @@ void fill_walk_params(bh_handle *h, WalkParams &P, int64_t nt, double theta, dou
 // (Re)build the compact fp32 walk tree for (theta, leaf) -- bh_walk.cu
 int ensure_walk_tree(bh_handle *h, double theta, int leaf, cudaStream_t s) {
   if (leaf < 1) leaf = 1;
+  if (h->mom_leaf > leaf)
+    return fail(BH_BAD_ARG, "the resident tree's moments were formed for leaf size " +
+                                std::to_string(h->mom_leaf) + "; prepare again for leaf size " +
+                                std::to_string(leaf));
   if (h->walk_valid && h->walk_theta == theta && h->walk_leaf == leaf) return BH_OK;
   const int64_t C = h->C;
   BH_CUDA(h->smask.ensure(sizeof(uint32_t) * C));
@@ -501,7 +509,7 @@ int sim_prepare(bh_handle *h, double theta, double eps, int leaf, bool bounds_re
   BH_LAUNCHED();
   h->tbegin(BH_PHASE_BUILD, s);
   if (f32)
-    BH_TRY(build_sorted_async(h, n, h->pos.as<float4>(), s, h->allow_dup || leaf > 1));
+    BH_TRY(build_sorted_async(h, n, h->pos.as<float4>(), s, h->allow_dup || leaf > 1, leaf));
   else
     BH_TRY(build_sorted(h, n, nullptr, h->pos.as<double4>(), s, h->allow_dup || leaf > 1));
   h->tend(s);
@@ -853,6 +861,9 @@ int bh_export_tree(bh_handle *h, uint64_t *d_key, int8_t *d_level, double *d_cen
                    int64_t *d_count, int32_t *d_children, void *stream) {
   if (!h) return fail(BH_BAD_ARG, "bh_export_tree: bad args");
   if (h->tree_n < 0) return fail(BH_NO_TREE, "no tree has been built");
+  if (h->mom_leaf > 0)
+    return fail(BH_BAD_ARG, "the resident tree is a walk-only tree (cells inside buckets have no moments); "
+                            "build it with bh_build_* to export");
   launch_export(h->view(), h->R, d_key, d_level, d_centre, d_side, d_mass, d_com, d_quad, d_count,
                 d_children, S(stream));
   BH_LAUNCHED();

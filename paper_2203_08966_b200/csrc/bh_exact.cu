@@ -454,6 +454,78 @@ __device__ void cell_moments8(const TreeView &t, int p, double (*xs)[11]) {
   __syncwarp();
 }
 
+// fp32 walk trees only (leaf size L > 1): the moments of a bucket -- a cell the
+// walk never opens (count <= L, or a level-21 duplicate-key cell) whose parent
+// it does open -- straight from its <= L contiguous sorted bodies, 8 lanes per
+// cell (strided bodies, fixed-order butterfly sums).  The cells inside buckets
+// are never read by the walk, so their moments are not formed at all.  Equal
+// to the recursive combine up to fp64 rounding (the records are rounded to
+// fp32).  Every lane of the warp must call it (p < 0: no cell).
+__device__ void bucket_moments8(const TreeView &t, int p) {
+  const int s = threadIdx.x & 7;
+  int lo = 0, cnt = 0;
+  if (p >= 0) {
+    const int4 L = t.link[p];
+    lo = L.z;
+    cnt = L.y;
+  }
+  double tm = 0.0, sx = 0.0, sy = 0.0, sz = 0.0;
+  for (int j = s; j < cnt; j += 8) {
+    const double4 b = body64(t, lo + j);
+    tm += b.w;
+    sx += b.w * b.x;
+    sy += b.w * b.y;
+    sz += b.w * b.z;
+  }
+#pragma unroll
+  for (int o = 1; o < 8; o <<= 1) {
+    tm += __shfl_xor_sync(0xffffffffu, tm, o);
+    sx += __shfl_xor_sync(0xffffffffu, sx, o);
+    sy += __shfl_xor_sync(0xffffffffu, sy, o);
+    sz += __shfl_xor_sync(0xffffffffu, sz, o);
+  }
+  double cx = 0.0, cy = 0.0, cz = 0.0;
+  if (tm != 0.0) {
+    cx = sx / tm;
+    cy = sy / tm;
+    cz = sz / tm;
+  }
+  double q0 = 0.0, q1 = 0.0, q2 = 0.0, q3 = 0.0, q4 = 0.0, q5 = 0.0;
+  for (int j = s; j < cnt && tm != 0.0; j += 8) {
+    const double4 b = body64(t, lo + j);
+    const double dx = b.x - cx, dy = b.y - cy, dz = b.z - cz;
+    const double d2 = dx * dx + dy * dy + dz * dz;
+    q0 += b.w * (3.0 * (dx * dx) - d2);
+    q1 += b.w * (3.0 * (dx * dy));
+    q2 += b.w * (3.0 * (dx * dz));
+    q3 += b.w * (3.0 * (dy * dy) - d2);
+    q4 += b.w * (3.0 * (dy * dz));
+    q5 += b.w * (3.0 * (dz * dz) - d2);
+  }
+#pragma unroll
+  for (int o = 1; o < 8; o <<= 1) {
+    q0 += __shfl_xor_sync(0xffffffffu, q0, o);
+    q1 += __shfl_xor_sync(0xffffffffu, q1, o);
+    q2 += __shfl_xor_sync(0xffffffffu, q2, o);
+    q3 += __shfl_xor_sync(0xffffffffu, q3, o);
+    q4 += __shfl_xor_sync(0xffffffffu, q4, o);
+    q5 += __shfl_xor_sync(0xffffffffu, q5, o);
+  }
+  if (p >= 0 && s == 0) {
+    t.cm64[p] = make_double4(cx, cy, cz, tm);
+    double2 *q2o = reinterpret_cast<double2 *>(t.q64 + kQStride * (int64_t)p);
+    q2o[0] = make_double2(q0, q1);
+    q2o[1] = make_double2(q2, q3);
+    q2o[2] = make_double2(q4, q5);
+    q2o[3] = make_double2(0.0, 0.0);
+  }
+}
+
+// the fp32 walk opens a cell iff count > L (the root: count > 1) below level 21
+__device__ __forceinline__ bool walk_opens(int64_t c, int4 L, int leaf) {
+  return (L.y > leaf || (c == 0 && L.y > 1)) && L.w < kMaxLevel;
+}
+
 // C = 1 + off[n-1] + newc[n-1] on device; flag an overflow of the capacity
 __global__ void k_set_count(const uint32_t *off, const uint32_t *newc, int64_t n, int64_t cap,
                             int *dC, DeviceFlags *f, int step) {
@@ -479,11 +551,12 @@ namespace cg = cooperative_groups;
 #define BH_MOM_MINB 4
 #endif
 __global__ void __launch_bounds__(256, BH_MOM_MINB) k_moments_coop(TreeView t, int *__restrict__ lvl,
-                                                     int *__restrict__ list) {
+                                                     int *__restrict__ list, int leaf) {
   cg::grid_group grid = cg::this_grid();
   const int64_t C = tree_count(t);
   if (C > t.C) return;  // overflowed build (uniform across the grid): nothing valid
   int *cnt = lvl, *offs = lvl + (kMaxLevel + 1), *cur = lvl + 2 * (kMaxLevel + 1);
+  int *nbuck = lvl + 3 * (kMaxLevel + 1);  // pruned mode: buckets listed from the end of `list`
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     int acc = 0;
     for (int l = 0; l <= kMaxLevel; ++l) {
@@ -491,50 +564,68 @@ __global__ void __launch_bounds__(256, BH_MOM_MINB) k_moments_coop(TreeView t, i
       cur[l] = 0;
       acc += cnt[l];
     }
+    *nbuck = 0;
   }
   grid.sync();
   __shared__ int h[kMaxLevel + 1], base[kMaxLevel + 1];
+  __shared__ int hb, bbase;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t c0 = (int64_t)blockIdx.x * blockDim.x; c0 < C; c0 += stride) {
     if (threadIdx.x <= kMaxLevel) h[threadIdx.x] = 0;
+    if (threadIdx.x == 0) hb = 0;
     __syncthreads();
     const int64_t c = c0 + threadIdx.x;
-    int l = -1, rank = 0;
+    int l = -1, rank = 0, brank = -1;
     if (c < C) {
       const int4 L = t.link[c];
       if (L.y > 1) {
-        l = L.w;
-        rank = atomicAdd(&h[l], 1);
+        if (leaf <= 1 || walk_opens(c, L, leaf)) {
+          l = L.w;
+          rank = atomicAdd(&h[l], 1);
+        } else if (walk_opens(t.parent[c], t.link[t.parent[c]], leaf)) {
+          brank = atomicAdd(&hb, 1);  // a bucket: moments from its bodies
+        }  // else inside a bucket: never read by the walk
       }
     }
     __syncthreads();
     if (threadIdx.x <= kMaxLevel && h[threadIdx.x])
       base[threadIdx.x] = offs[threadIdx.x] + atomicAdd(&cur[threadIdx.x], h[threadIdx.x]);
+    if (threadIdx.x == 0 && hb) bbase = atomicAdd(nbuck, hb);
     __syncthreads();
     if (l >= 0) list[base[l] + rank] = (int)c;
+    if (brank >= 0) list[C - 1 - (bbase + brank)] = (int)c;
     __syncthreads();
   }
   grid.sync();
+  const int sub = (threadIdx.x & 31) >> 3;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = stride >> 5;
+  if (leaf > 1) {  // the buckets first (no level order among them), then only the opened cells
+    const int nb = *nbuck;
+    for (int64_t b0 = warp * 4; b0 < nb; b0 += nwarps * 4) {
+      const int64_t k = b0 + sub;
+      bucket_moments8(t, k < nb ? list[C - 1 - k] : -1);
+    }
+    grid.sync();
+  }
   // Runs of consecutive small levels (few cells: the top of the tree and the
   // deepest levels) are swept by block 0 alone with block barriers; the rest
   // of the grid waits at one grid barrier after the run.
   // 8 lanes per cell (cell_moments8): a warp takes 4 cells per pass.
+  int *lc = leaf > 1 ? cur : cnt;  // cells listed per level (pruned mode: the opened ones)
   __shared__ double xs[256 / 32][32][11];
   double(*wx)[11] = xs[threadIdx.x >> 5];
-  const int sub = (threadIdx.x & 31) >> 3;
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = stride >> 5;
   const int small = 2 * (int)(blockDim.x >> 3);
   int l = kMaxLevel;
   while (l >= 0) {
-    const int n_l = cnt[l];
+    const int n_l = lc[l];
     if (n_l == 0) { --l; continue; }
     if (n_l <= small) {
       int l2 = l;
-      while (l2 >= 0 && cnt[l2] <= small) --l2;  // run = levels (l2, l]
+      while (l2 >= 0 && lc[l2] <= small) --l2;  // run = levels (l2, l]
       if (blockIdx.x == 0) {
         for (int ll = l; ll > l2; --ll) {
-          const int nll = cnt[ll], bll = offs[ll];
+          const int nll = lc[ll], bll = offs[ll];
           for (int base = (int)(threadIdx.x >> 5) * 4; base < nll; base += (int)(blockDim.x >> 5) * 4) {
             const int k = base + sub;
             cell_moments8(t, k < nll ? list[bll + k] : -1, wx);
@@ -556,14 +647,14 @@ __global__ void __launch_bounds__(256, BH_MOM_MINB) k_moments_coop(TreeView t, i
   }
 }
 
-int launch_moments_coop(const TreeView &t, int *lvl, int *list, int sms, cudaStream_t s) {
+int launch_moments_coop(const TreeView &t, int *lvl, int *list, int sms, cudaStream_t s, int leaf) {
   if (t.n <= 1) return 0;
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_moments_coop, 256, 0);
   if (per_sm < 1) per_sm = 1;
   dim3 grid(sms * per_sm), block(256);
   TreeView tv = t;
-  void *args[] = {&tv, &lvl, &list};
+  void *args[] = {&tv, &lvl, &list, &leaf};
   return (int)cudaLaunchCooperativeKernel((void *)k_moments_coop, grid, block, args, 0, s);
 }
 

@@ -137,7 +137,9 @@ void launch_emit(const TreeView &t, const float4 *bod32, const double4 *bod64, c
 // launch sweeps the levels deepest-first with grid-wide barriers between them.
 void launch_set_count(const uint32_t *off, const uint32_t *newc, int64_t n, int64_t cap,
                       int *dC, DeviceFlags *f, cudaStream_t s, int step = 0);
-int launch_moments_coop(const TreeView &t, int *lvl, int *list, int sms, cudaStream_t s);
+// leaf > 1: the fp32 walk tree only (moments of opened cells and buckets; the
+// cells inside buckets are skipped), leaf <= 1: every cell (the reference tree)
+int launch_moments_coop(const TreeView &t, int *lvl, int *list, int sms, cudaStream_t s, int leaf = 0);
 void launch_export(const TreeView &t, double R, uint64_t *key, int8_t *level, double *centre,
                    double *side, double *mass, double *com, double *quad, int64_t *count,
                    int32_t *children, cudaStream_t s);

@@ -7,16 +7,19 @@ import torch
 import torch.distributed as dist
 from paper_2203_08966_b200.decomposition import DistributedBuildSim, StepParams, TorchComm
 from paper_2203_08966_b200.engine import Engine
-from paper_2203_08966_b200.initcond import make_rng, plummer_cluster
+import bench
 
-n = int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_000
+# argv[1]: a bench config name (cfg2, cfg3, ...) or a Plummer body count
+arg = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
+cfg = bench.CONFIGS[arg] if arg in bench.CONFIGS else dict(bench.CONFIGS["cfg2"], n=int(arg))
 dist.init_process_group(os.environ.get("BH_DIST_BACKEND", "gloo"))
 rank, ws = dist.get_rank(), dist.get_world_size()
 torch.cuda.set_device(0)
-b = plummer_cluster(n, make_rng(2), 1.0)
+b = bench.make_bodies(cfg)
+n = len(b)
 eng = Engine("fp32", 0)
 lo, hi = n * rank // ws, n * (rank + 1) // ws
-sim = DistributedBuildSim(eng, TorchComm(), StepParams(0.6, 1e-3, 16, 1e-3))
+sim = DistributedBuildSim(eng, TorchComm(), StepParams(cfg["theta"], cfg["eps"], cfg["leaf"], cfg["dt"]))
 sim.load(eng.bodies_tensor(b.position[lo:hi], b.mass[lo:hi]), eng.vec_tensor(b.velocity[lo:hi]),
          gid=torch.arange(lo, hi, device="cuda"))
 sim.bootstrap()
