@@ -100,7 +100,7 @@ struct bh_handle {
   int let_nrank = 0;
   int64_t let_nrec = 0;
   double R = 1.0;
-  Buf link, parent, child8, lvl, lvl_list, cm64, q64, tbod;
+  Buf link, parent, child8, lvl, lvl_list, cm64, q64, tbod, mclass;
   int *hlvl = nullptr;  // pinned: internal cells per level of the last build
   int sms = 148;
   int allow_dup = 0;       // bh_set_allow_duplicates; the sim path uses leaf_size > 1
@@ -232,12 +232,12 @@ int ensure_sort(bh_handle *h, int64_t n) {
   return BH_OK;
 }
 
-int sort_keys(bh_handle *h, int64_t n, cudaStream_t s) {
-  // keys/vals -> keys2/vals2
+int sort_keys(bh_handle *h, int64_t n, cudaStream_t s, bool iota_vals = false) {
+  // keys/vals -> keys2/vals2 (iota_vals: the values are the input positions, not read)
   if (n <= 0) return BH_OK;
   BH_CUDA(sort_pairs(h->sort_tmp.p, h->sort_tmp.bytes, h->keys.as<uint64_t>(),
-                     h->keys2.as<uint64_t>(), h->vals.as<uint32_t>(), h->vals2.as<uint32_t>(),
-                     n, s));
+                     h->keys2.as<uint64_t>(), iota_vals ? nullptr : h->vals.as<uint32_t>(),
+                     h->vals2.as<uint32_t>(), n, s));
   h->launches += sort_launches();
   return BH_OK;
 }
@@ -344,6 +344,11 @@ int build_sorted_async(bh_handle *h, int64_t n, const float4 *bod32, cudaStream_
   h->tbod32 = bod32;
   h->tbod64 = nullptr;
   TreeView t = h->view();
+  if (leaf > 1) {  // a walk-only tree: the emit kernel classifies the cells for the moments
+    BH_CUDA(h->mclass.ensure(cap + 16));
+    t.mclass = h->mclass.as<uint8_t>();
+    t.mleaf = leaf;
+  }
   launch_emit(t, bod32, nullptr, s);
   // a walk-only tree: moments of the cells a leaf-size-`leaf` walk reads
   BH_CUDA((cudaError_t)launch_moments_coop(t, h->lvl.as<int>(), h->lvl_list.as<int>(), h->sms, s, leaf));
@@ -484,14 +489,12 @@ int sim_prepare(bh_handle *h, double theta, double eps, int leaf, bool bounds_re
   h->tbegin(BH_PHASE_KEYS, s);
   launch_finish_R(h->flags, f32 ? 0 : 1, h->dR, s);
   if (f32)
-    launch_keys_f32(h->pos.as<float4>(), n, h->dR, h->keys.as<uint64_t>(), h->vals.as<uint32_t>(),
-                    h->flags, s);
+    launch_keys_f32(h->pos.as<float4>(), n, h->dR, h->keys.as<uint64_t>(), nullptr, h->flags, s);
   else
-    launch_keys_f64(h->pos.as<double>(), 4, n, h->dR, h->keys.as<uint64_t>(),
-                    h->vals.as<uint32_t>(), h->flags, s);
+    launch_keys_f64(h->pos.as<double>(), 4, n, h->dR, h->keys.as<uint64_t>(), nullptr, h->flags, s);
   h->tend(s);
   h->tbegin(BH_PHASE_SORT, s);
-  BH_TRY(sort_keys(h, n, s));
+  BH_TRY(sort_keys(h, n, s, true));
   h->tend(s);
   h->tbegin(BH_PHASE_PERMUTE, s);
   if (f32)
@@ -531,14 +534,12 @@ int sim_sort(bh_handle *h, cudaStream_t s) {
   if (n == 0) return BH_OK;
   h->tbegin(BH_PHASE_KEYS, s);
   if (f32)
-    launch_keys_f32(h->pos.as<float4>(), n, h->dR, h->keys.as<uint64_t>(), h->vals.as<uint32_t>(),
-                    h->flags, s);
+    launch_keys_f32(h->pos.as<float4>(), n, h->dR, h->keys.as<uint64_t>(), nullptr, h->flags, s);
   else
-    launch_keys_f64(h->pos.as<double>(), 4, n, h->dR, h->keys.as<uint64_t>(),
-                    h->vals.as<uint32_t>(), h->flags, s);
+    launch_keys_f64(h->pos.as<double>(), 4, n, h->dR, h->keys.as<uint64_t>(), nullptr, h->flags, s);
   h->tend(s);
   h->tbegin(BH_PHASE_SORT, s);
-  BH_TRY(sort_keys(h, n, s));
+  BH_TRY(sort_keys(h, n, s, true));
   h->tend(s);
   h->tbegin(BH_PHASE_PERMUTE, s);
   if (f32)
@@ -705,7 +706,7 @@ int bh_destroy(bh_handle *h) {
   close_peers(h);
   Buf *bufs[] = {&h->keys, &h->keys2, &h->vals, &h->vals2, &h->sort_tmp, &h->scan_tmp,
                  &h->lcp, &h->newc, &h->off, &h->link, &h->parent, &h->child8, &h->lvl, &h->lvl_list,
-                 &h->cm64, &h->q64, &h->smask, &h->nck, &h->wbase, &h->wnodes, &h->wscan_tmp, &h->tbod, &h->pos, &h->pos2,
+                 &h->cm64, &h->q64, &h->mclass, &h->smask, &h->nck, &h->wbase, &h->wnodes, &h->wscan_tmp, &h->tbod, &h->pos, &h->pos2,
                  &h->vel, &h->vel2, &h->acc, &h->id, &h->id2, &h->work_sorted, &h->work_orig,
                  &h->bk_pos, &h->bk_vel, &h->bk_acc, &h->bk_id, &h->bk_work,
                  &h->shared, &h->branch, &h->rec_of_cell, &h->wparent, &h->let_present,

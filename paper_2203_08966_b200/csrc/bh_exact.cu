@@ -247,9 +247,11 @@ __global__ void k_emit(TreeView t, const float4 *__restrict__ bod32,
   if (i >= n) return;
   const int C = (int)tree_count(t);
   if (C > t.C) return;  // sync-free build overflowed its capacity (flagged; redone)
+  const int L = t.mleaf;
   if (i == 0) {
     t.link[0] = make_int4(C, (int)n, 0, 0);
     t.parent[0] = -1;
+    if (t.mclass) t.mclass[0] = n > 1 ? 2 : 0;  // the walk opens a root holding > 1 body
     if (n == 1 && t.bnd_prev < 0 && t.bnd_next < 0) {  // hashed.py:464-474: root = leaf
       double4 b;
       if (bod64) {
@@ -271,11 +273,15 @@ __global__ void k_emit(TreeView t, const float4 *__restrict__ bod32,
   const int start = i > 0 ? lp : 0;
   const int base = 1 + (int)t.off[i];
   int par = 0;
+  bool par_open = n > 1;  // walk-only builds: does the walk open the parent of the next cell?
   if (start > 0) {
     const int shift = 3 * (kMortonBits - start);
     const int64_t j = run_begin(t.keys, i, k >> shift, shift);
     const int startj = j > 0 ? t.lcp[j - 1] : 0;
     par = 1 + (int)t.off[j] + (start - startj - 1);
+    // the level-`start` parent holds the run from body j: more than L bodies iff
+    // body j + L still shares its prefix
+    if (t.mclass) par_open = j + L < n && (t.keys[j + L] >> shift) == (k >> shift);
   }
   for (int l = start + 1; l <= depth; ++l) {
     const int c = base + (l - start - 1);
@@ -287,8 +293,10 @@ __global__ void k_emit(TreeView t, const float4 *__restrict__ bod32,
       const int64_t end = run_end(t.keys, n, i, k, 0);
       const int skip = end < n ? 1 + (int)t.off[end] : C;
       t.link[c] = make_int4(skip, (int)(end - i), (int)i, l);
+      if (t.mclass) t.mclass[c] = par_open ? 1 : 0;  // never opened (level 21): a bucket
     } else if (l == depth) {
       t.link[c] = make_int4(c + 1, 1, (int)i, l);
+      if (t.mclass) t.mclass[c] = 0;
       double4 b;
       if (bod64) {
         b = bod64[i];
@@ -302,6 +310,11 @@ __global__ void k_emit(TreeView t, const float4 *__restrict__ bod32,
       const int64_t end = run_end(t.keys, n, i, k >> shift, shift);
       const int skip = end < n ? 1 + (int)t.off[end] : C;
       t.link[c] = make_int4(skip, (int)(end - i), (int)i, l);
+      if (t.mclass) {
+        const bool opens = end - i > L;  // l < 21 here
+        t.mclass[c] = opens ? (uint8_t)(2 + l) : (par_open ? 1 : 0);
+        par_open = opens;
+      }
     }
     par = c;
   }
@@ -570,6 +583,41 @@ __global__ void __launch_bounds__(256, BH_MOM_MINB) k_moments_coop(TreeView t, i
   __shared__ int h[kMaxLevel + 1], base[kMaxLevel + 1];
   __shared__ int hb, bbase;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  if (leaf > 1 && t.mclass) {
+    // walk-only tree: the emit kernel classified every cell (one byte each);
+    // 4 cells per thread and pass
+    for (int64_t c0 = (int64_t)blockIdx.x * blockDim.x * 4; c0 < C; c0 += stride * 4) {
+      if (threadIdx.x <= kMaxLevel) h[threadIdx.x] = 0;
+      if (threadIdx.x == 0) hb = 0;
+      __syncthreads();
+      const int64_t cb = c0 + 4 * (int64_t)threadIdx.x;
+      uint8_t cl[4] = {0, 0, 0, 0};
+      if (cb + 4 <= C) {
+        const uchar4 v = *reinterpret_cast<const uchar4 *>(t.mclass + cb);
+        cl[0] = v.x; cl[1] = v.y; cl[2] = v.z; cl[3] = v.w;
+      } else {
+        for (int q = 0; q < 4; ++q) cl[q] = cb + q < C ? t.mclass[cb + q] : 0;
+      }
+      int rank[4], brank[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        rank[q] = brank[q] = -1;
+        if (cl[q] >= 2) rank[q] = atomicAdd(&h[cl[q] - 2], 1);
+        else if (cl[q] == 1) brank[q] = atomicAdd(&hb, 1);
+      }
+      __syncthreads();
+      if (threadIdx.x <= kMaxLevel && h[threadIdx.x])
+        base[threadIdx.x] = offs[threadIdx.x] + atomicAdd(&cur[threadIdx.x], h[threadIdx.x]);
+      if (threadIdx.x == 0 && hb) bbase = atomicAdd(nbuck, hb);
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (rank[q] >= 0) list[base[cl[q] - 2] + rank[q]] = (int)(cb + q);
+        if (brank[q] >= 0) list[C - 1 - (bbase + brank[q])] = (int)(cb + q);
+      }
+      __syncthreads();
+    }
+  } else {
   for (int64_t c0 = (int64_t)blockIdx.x * blockDim.x; c0 < C; c0 += stride) {
     if (threadIdx.x <= kMaxLevel) h[threadIdx.x] = 0;
     if (threadIdx.x == 0) hb = 0;
@@ -595,6 +643,7 @@ __global__ void __launch_bounds__(256, BH_MOM_MINB) k_moments_coop(TreeView t, i
     if (l >= 0) list[base[l] + rank] = (int)c;
     if (brank >= 0) list[C - 1 - (bbase + brank)] = (int)c;
     __syncthreads();
+  }
   }
   grid.sync();
   const int sub = (threadIdx.x & 31) >> 3;

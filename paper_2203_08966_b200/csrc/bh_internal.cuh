@@ -129,6 +129,11 @@ struct TreeView {
   const double4 *bod64 = nullptr;
   double4 *cm64 = nullptr;
   double *q64 = nullptr;   // [C][6]
+  // fp32 walk-only builds (leaf size mleaf > 1): per-cell moments class written
+  // by the emit kernel -- 0: nothing to form (a leaf, or inside a bucket),
+  // 1: a bucket (moments from its bodies), 2 + level: a cell the walk opens
+  uint8_t *mclass = nullptr;
+  int mleaf = 0;
 };
 void launch_emit(const TreeView &t, const float4 *bod32, const double4 *bod64, cudaStream_t s);
 // cursor: int[kMaxLevel+1] scratch; list: int[C]
@@ -265,7 +270,8 @@ void launch_potential_f64(const double *pos3, const double *mass, int64_t n, dou
 void run_ffma(float *out, int sms, int iters, double *flops, cudaStream_t s);
 void run_dfma(double *out, int sms, int iters, double *flops, cudaStream_t s);
 
-// radix sort of (key, u32 value) pairs over bits [0, 63) -- stable (bh_sort.cu)
+// radix sort of (key, u32 value) pairs over bits [0, 63) -- stable (bh_sort.cu);
+// vin == nullptr sorts (key, input index) pairs without reading values
 size_t sort_temp_bytes(int64_t n);
 cudaError_t sort_pairs(void *temp, size_t temp_bytes, const uint64_t *kin, uint64_t *kout,
                        const uint32_t *vin, uint32_t *vout, int64_t n, cudaStream_t s);

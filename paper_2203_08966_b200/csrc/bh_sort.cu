@@ -225,7 +225,7 @@ __device__ __forceinline__ unsigned block_excl_scan(unsigned v, unsigned *wsum, 
 
 template <int MINB, bool MATCH>
 __global__ void __launch_bounds__(kSortThreads, MINB) k_sort_pass(
-    const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin, uint64_t *__restrict__ kout,
+    const uint64_t *__restrict__ kin, const uint32_t *vin, uint64_t *__restrict__ kout,
     uint32_t *__restrict__ vout, int64_t n, int shift, const unsigned *__restrict__ bin_start,
     unsigned *__restrict__ counter, unsigned long long *__restrict__ st, unsigned epoch, unsigned ntiles) {
   extern __shared__ __align__(16) unsigned char sort_smem[];
@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(kSortThreads, MINB) k_sort_pass(
     const int64_t i = wbase + 32 * j + lane;
     if (i < n) {
       k[j] = __ldcs(kin + i);
-      v[j] = __ldcs(vin + i);
+      v[j] = vin ? __ldcs(vin + i) : (uint32_t)i;  // no input values: the identity permutation
     } else {
       k[j] = ~0ull;  // pads sort after every real key of the last tile and are never stored
       v[j] = 0u;
@@ -427,17 +427,21 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const uint32_t *__
   }
 }
 
-// exclusive scan of the tile sums in place (one block, carried across chunks)
+// exclusive scan of the tile sums in place, one block: each thread sums a
+// contiguous run of tiles, one block scan of the run totals, then each thread
+// writes its run (one barrier round instead of one per 1024 tiles)
 __global__ void __launch_bounds__(kScanTopThreads) k_scan_tiles(unsigned *__restrict__ tsum, int64_t ntiles) {
   __shared__ unsigned wsum[kScanTopThreads / 32];
-  unsigned carry = 0;
-  for (int64_t base = 0; base < ntiles; base += kScanTopThreads) {
-    const int64_t i = base + threadIdx.x;
-    const unsigned v = i < ntiles ? tsum[i] : 0u;
-    unsigned tot;
-    const unsigned ex = block_scan_t<kScanTopThreads>(v, wsum, &tot);
-    if (i < ntiles) tsum[i] = carry + ex;
-    carry += tot;
+  const int64_t per = (ntiles + kScanTopThreads - 1) / kScanTopThreads;
+  const int64_t b = per * threadIdx.x, e = b + per < ntiles ? b + per : ntiles;
+  unsigned run = 0;
+  for (int64_t i = b; i < e; ++i) run += tsum[i];
+  unsigned tot;
+  unsigned ex = block_scan_t<kScanTopThreads>(run, wsum, &tot);
+  for (int64_t i = b; i < e; ++i) {
+    const unsigned v = tsum[i];
+    tsum[i] = ex;
+    ex += v;
   }
 }
 

@@ -634,12 +634,13 @@ class DistributedBuildSim:
             return
         dest = torch.searchsorted(self.splitters, keys, right=True)
         counts = torch.bincount(dest, minlength=size)
-        moves = torch.tensor([n - int(counts[self.comm.rank].item())], dtype=torch.int64, device=keys.device)
+        moves = (n - counts[self.comm.rank]).reshape(1).to(torch.int64)
         self.comm.allreduce_sum_(moves)
-        if int(moves.item()) == 0:
+        both = torch.cat([moves, counts.to(torch.int64)]).cpu().tolist()  # one host read
+        if both[0] == 0:
             return  # ownership unchanged everywhere: the local sort follows
         order = torch.argsort(dest, stable=True)
-        counts = counts.tolist()
+        counts = both[1:]
         pos = self._export(_lib.BH_SIM_POS, n, (n, 4), torch.float32)
         vel = self._export(_lib.BH_SIM_VEL, n, (n, 4), torch.float32)
         acc = self._export(_lib.BH_SIM_ACC, n, (n, 4), torch.float32)
@@ -665,27 +666,28 @@ class DistributedBuildSim:
         if work is None:
             work = self._export(_lib.BH_SIM_WORK, n, (n,), torch.int32)
         work = work.to(torch.int64)
-        mine = torch.tensor([int(work.sum().item()) if n else 0, n, int(keys[0].item()) if n else -1],
-                            dtype=torch.int64, device=dev)
+        zero = torch.zeros((), dtype=torch.int64, device=dev)
+        mine = torch.stack([work.sum() if n else zero, zero + n, keys[0] if n else zero - 1])
         allm = [torch.zeros_like(mine) for _ in range(size)]
         self._allgather(allm, mine)
-        wt = [int(a[0].item()) for a in allm]
-        firsts = [int(a[2].item()) for a in allm]
+        allm = torch.stack(allm).cpu()  # one host read: (work, n, first key) per rank
+        wt = allm[:, 0].tolist()
+        firsts = allm[:, 2].tolist()
         total = sum(wt)
         base = sum(wt[: self.comm.rank])
         cand = torch.full((size - 1,), -1, dtype=torch.int64, device=dev)
         if n:
+            # all splitter targets at once: zone k starts after the first body whose
+            # global prefix reaches k/size of the total
             prefix = (torch.cumsum(work, 0) + base) * size
-            for k in range(1, size):
-                j = int(torch.searchsorted(prefix, torch.tensor([k * total], device=dev), side="left").item())
-                # the straddling body is here iff it is this rank's body j and the
-                # prefix before this rank's first body is still short of the target
-                if j < n and (j > 0 or base * size < k * total):
-                    if j + 1 < n:
-                        cand[k - 1] = keys[j + 1]
-                    else:
-                        nxt = next((firsts[q] for q in range(self.comm.rank + 1, size) if firsts[q] >= 0), None)
-                        cand[k - 1] = nxt if nxt is not None else (1 << 62)
+            targets = torch.arange(1, size, device=dev, dtype=torch.int64) * total
+            js = torch.searchsorted(prefix, targets, side="left")
+            nxt = next((firsts[q] for q in range(self.comm.rank + 1, size) if firsts[q] >= 0), None)
+            after = torch.cat([keys[1:], torch.tensor([nxt if nxt is not None else (1 << 62)], device=dev)])
+            # the straddling body is here iff it is this rank's body j and the prefix
+            # before this rank's first body is still short of the target
+            here = (js < n) & ((js > 0) | (base * size < targets))
+            cand = torch.where(here, after[js.clamp(max=n - 1)], cand)
         self.comm.allreduce_max_(cand)
         # monotone (zones may be empty when work is concentrated)
         self.splitters = torch.cummax(cand, 0).values
@@ -715,11 +717,11 @@ class DistributedBuildSim:
         n, keys, gid = self._sort()
         self._t("sort2")
         dev = eng.device
-        fl = torch.tensor([int(keys[0].item()) if n else -1, int(keys[-1].item()) if n else -1],
-                          dtype=torch.int64, device=dev)
+        fl = (torch.stack([keys[0], keys[-1]]) if n else
+              torch.full((2,), -1, dtype=torch.int64, device=dev))
         allfl = [torch.zeros_like(fl) for _ in range(size)]
         self._allgather(allfl, fl)
-        fls = [(int(a[0].item()), int(a[1].item())) for a in allfl]
+        fls = [tuple(r) for r in torch.stack(allfl).cpu().tolist()]  # one host read
         prev = next((fls[q][1] for q in range(rank - 1, -1, -1) if fls[q][0] >= 0), None)
         nxt = next((fls[q][0] for q in range(rank + 1, size) if fls[q][0] >= 0), None)
         self._t("boundary")
@@ -782,7 +784,9 @@ class DistributedBuildSim:
         if treeA is not None and n:
             # pass A walks the local part while the LETs travel
             nwarp = (n + 63) // 64
-            cap = nwarp * min(len(deferred), 8) + 1024
+            # each warp defers at most one entry per remote branch it opens (cfg3 at
+            # 8 ranks: ~30 per warp); 16 B per entry
+            cap = nwarp * min(len(deferred), 64) + 1024
             dbuf = torch.empty((cap, 4), dtype=torch.int32, device=dev)
             dcnt = torch.zeros(1, dtype=torch.int32, device=dev)
             eng.walk_records_defer(treeA, gA, bodies, p.eps, L, acc, work, dbuf, dcnt)
