@@ -657,6 +657,9 @@ constexpr int kW9NcShift = 28;  // frontier entry: first_child | nchild << 28, u
 #ifndef BH_W9_PC30
 #define BH_W9_PC30 1  // pc: a += R5 (Qd + d (-M d2 - 2.5 dQd R2)): 30 packed FP ops instead of 31
 #endif
+#ifndef BH_W9_PPPACK
+#define BH_W9_PPPACK 1  // pp drain: buckets with disjoint lane sets share a pass (see flush_pp)
+#endif
 #ifndef BH_W9_BULK
 #define BH_W9_BULK 0  // 1: accepted records reach shared memory by cp.async.bulk (mbarrier-completed)
 #endif
@@ -706,8 +709,13 @@ struct W9Warp {
 #endif
   float4 pcr[kW9List][3];  // accepted cells: a (mask0 in .w), b (mask1 in .z), c
   int4 pp[kW9List];        // pp: (lo, count, mask0, mask1) or a leaf record (cell, 0, ...)
-  float4 mxr[32][3];       // mixed cells of the batch: a, b (mask0 in .z), c
-  int4 mxd[32];            //                           d (mask1 in .w)
+  union {
+    struct {
+      float4 mxr[32][3];   // mixed cells of the batch: a, b (mask0 in .z), c
+      int4 mxd[32];        //                           d (mask1 in .w)
+    };
+    uint8_t psel[32][32];  // pp drain (after the batch): entry + 1 of each lane in each pass
+  };
 };
 
 __device__ __forceinline__ float w9_shfl_min(float v) {
@@ -836,45 +844,95 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
 #endif
   };
   // dense pp over the bodies of the listed leaves / buckets (self skipped by r2 > 0)
+  auto pp_body = [&](const float4 bb, bool u0, bool u1) {
+    const float2 EX = __ffma2_rn(f2(bb.x), f2(-1.f), X);
+    const float2 EY = __ffma2_rn(f2(bb.y), f2(-1.f), Y);
+    const float2 EZ = __ffma2_rn(f2(bb.z), f2(-1.f), Z);
+    const float2 Q2 = __ffma2_rn(EZ, EZ, __ffma2_rn(EY, EY, __fmul2_rn(EX, EX)));
+    const bool m0 = u0 && Q2.x > 0.f, m1 = u1 && Q2.y > 0.f;
+    const float2 W = __fadd2_rn(Q2, E2);
+    const float2 R = f2(m0 ? rsqrtf(W.x) : 0.f, m1 ? rsqrtf(W.y) : 0.f);
+    const float2 Sc = __fmul2_rn(__fmul2_rn(R, R), __fmul2_rn(R, f2(-bb.w)));
+    AX = __ffma2_rn(Sc, EX, AX);
+    AY = __ffma2_rn(Sc, EY, AY);
+    AZ = __ffma2_rn(Sc, EZ, AZ);
+    pp0 += m0; pp1 += m1;
+  };
   auto flush_pp = [&](int n) {
+#if BH_W9_PPPACK
+    // Leaf records one at a time (their body is the record); buckets packed:
+    // greedy first-fit of the listed buckets into passes whose lane sets
+    // (targets 2l, 2l+1 <-> lane l) do not overlap, so one pass over the
+    // longest of its buckets serves them all -- each lane follows the one
+    // bucket holding its targets (a pass's body loads have one address per
+    // bucket).  The interaction sets are unchanged; only the fp32 summation
+    // order per target moves.  Lane p keeps pass p's used lanes and length.
+    int k0 = 0;
+    while (k0 < n) {
+      unsigned used = 0u;
+      int plen = 0, npass = 0, k = k0;
+      for (; k < n; ++k) {
+        const int4 en = S.pp[k];
+        const bool u0 = (unsigned)en.z & bit, u1 = (unsigned)en.w & bit;
+        if (en.y == 0) {  // leaf record: its com and mass are the body (a LET leaf has no body index here)
+          const WalkNode *nd = T + en.x;
+          const float4 a = nd->a;
+          pp_body(make_float4(-a.x, -a.y, -a.z, nd->c.z), u0, u1);
+          continue;
+        }
+        const unsigned lm = (unsigned)en.z | (unsigned)en.w;
+        const unsigned fit = __ballot_sync(FULL, (int)lane < npass && (used & lm) == 0u);
+        int p;
+        if (fit) {
+          p = __ffs(fit) - 1;
+        } else {
+          if (npass == 32) break;  // run these passes, then pack the rest
+          p = npass++;
+          S.psel[p][lane] = 0;
+        }
+        if ((int)lane == p) {
+          used |= lm;
+          plen = max(plen, en.y);
+        }
+        if ((lm >> lane) & 1u) S.psel[p][lane] = (uint8_t)(k + 1);
+      }
+      __syncwarp();
+      for (int p = 0; p < npass; ++p) {
+        const int len = __shfl_sync(FULL, plen, p);
+        const int e = (int)S.psel[p][lane] - 1;
+        int lo = 0, cnt = 0;
+        bool u0 = false, u1 = false;
+        if (e >= 0) {
+          const int4 en = S.pp[e];
+          lo = en.x;
+          cnt = en.y;
+          u0 = (unsigned)en.z & bit;
+          u1 = (unsigned)en.w & bit;
+        }
+#pragma unroll(kBucketUnroll)
+        for (int j = 0; j < len; ++j) {
+          const bool v = j < cnt;
+          const float4 bb = bodies[v ? lo + j : lo];
+          pp_body(bb, u0 && v, u1 && v);
+        }
+      }
+      __syncwarp();
+      k0 = k;
+    }
+#else
     for (int k = 0; k < n; ++k) {
       const int4 en = S.pp[k];
       const bool u0 = (unsigned)en.z & bit, u1 = (unsigned)en.w & bit;
       if (en.y == 0) {  // leaf record: its com and mass are the body (a LET leaf has no body index here)
         const WalkNode *nd = T + en.x;
         const float4 a = nd->a;
-        const float m = nd->c.z;
-        const float2 DX = __fadd2_rn(X, f2(a.x));
-        const float2 DY = __fadd2_rn(Y, f2(a.y));
-        const float2 DZ = __fadd2_rn(Z, f2(a.z));
-        const float2 D2 = __ffma2_rn(DZ, DZ, __ffma2_rn(DY, DY, __fmul2_rn(DX, DX)));
-        const bool l0 = u0 && D2.x > 0.f, l1 = u1 && D2.y > 0.f;
-        const float2 W = __fadd2_rn(D2, E2);
-        const float2 R = f2(l0 ? rsqrtf(W.x) : 0.f, l1 ? rsqrtf(W.y) : 0.f);
-        const float2 Sc = __fmul2_rn(__fmul2_rn(R, R), __fmul2_rn(R, f2(-m)));
-        AX = __ffma2_rn(Sc, DX, AX);
-        AY = __ffma2_rn(Sc, DY, AY);
-        AZ = __ffma2_rn(Sc, DZ, AZ);
-        pp0 += l0; pp1 += l1;
+        pp_body(make_float4(-a.x, -a.y, -a.z, nd->c.z), u0, u1);
         continue;
       }
 #pragma unroll(kBucketUnroll)
-      for (int j = en.x; j < en.x + en.y; ++j) {
-        const float4 bb = bodies[j];
-        const float2 EX = __ffma2_rn(f2(bb.x), f2(-1.f), X);
-        const float2 EY = __ffma2_rn(f2(bb.y), f2(-1.f), Y);
-        const float2 EZ = __ffma2_rn(f2(bb.z), f2(-1.f), Z);
-        const float2 Q2 = __ffma2_rn(EZ, EZ, __ffma2_rn(EY, EY, __fmul2_rn(EX, EX)));
-        const bool m0 = u0 && Q2.x > 0.f, m1 = u1 && Q2.y > 0.f;
-        const float2 W = __fadd2_rn(Q2, E2);
-        const float2 R = f2(m0 ? rsqrtf(W.x) : 0.f, m1 ? rsqrtf(W.y) : 0.f);
-        const float2 Sc = __fmul2_rn(__fmul2_rn(R, R), __fmul2_rn(R, f2(-bb.w)));
-        AX = __ffma2_rn(Sc, EX, AX);
-        AY = __ffma2_rn(Sc, EY, AY);
-        AZ = __ffma2_rn(Sc, EZ, AZ);
-        pp0 += m0; pp1 += m1;
-      }
+      for (int j = en.x; j < en.x + en.y; ++j) pp_body(bodies[j], u0, u1);
     }
+#endif
   };
 
   while (sp > 0) {

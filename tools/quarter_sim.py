@@ -26,7 +26,9 @@ from paper_2203_08966_b200.initcond import make_rng, plummer_cluster  # noqa: E4
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_000
 G = int(sys.argv[2]) if len(sys.argv) > 2 else 150
-theta, L, S = 0.6, 16, 64
+theta = float(sys.argv[3]) if len(sys.argv) > 3 else 0.6
+L = int(sys.argv[4]) if len(sys.argv) > 4 else 16
+S = 64
 b = plummer_cluster(n, make_rng(2), 1.0)
 pos = b.position.astype(np.float32).astype(np.float64)
 m = b.mass.astype(np.float32).astype(np.float64)
@@ -108,3 +110,30 @@ report("pc mixed-accepted", pc_mix)
 report("pc all (certain + mixed in one list)", [a + b_ for a, b_ in zip(pc_cert, pc_mix)])
 report("pp (weighted by bucket bodies)", [[e for e, _ in grp] for grp in pp],
        [[c for _, c in grp] for grp in pp])
+
+
+# ---- disjoint packing: entries whose lane sets do not overlap share a pass;
+# each lane follows the one entry that holds its targets (body loads then have
+# one address per packed entry).  Greedy first-fit in list order per flush.
+def packed_cost(grp, K):
+    tot = 0
+    for q in range(0, len(grp), K):
+        batch = grp[q:q + K]
+        passes = []  # [lane mask, max count]
+        for mask, c in batch:
+            lm = mask.reshape(32, 2).any(1)
+            for pz in passes:
+                if not (pz[0] & lm).any():
+                    pz[0] |= lm
+                    pz[1] = max(pz[1], c)
+                    break
+            else:
+                passes.append([lm.copy(), c])
+        tot += sum(c for _, c in passes)
+    return tot
+
+
+base_it = sum(sum(c for _, c in grp) for grp in pp)
+for K in (16, 32, 64):
+    t = sum(packed_cost(grp, K) for grp in pp)
+    print(f"pp disjoint packing K={K}: body iterations {t / base_it:.3f} of broadcast")
