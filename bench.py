@@ -293,6 +293,7 @@ def run_ours(args, cfg) -> dict | None:
 
     # ---- end to end through the public API with host buffers
     e2e_ms, e2e_inter, e2e_path, h2d, d2h = run_e2e(args, cfg, eng, sim, ws, dev, flush, ev0, ev1)
+    plugin = run_plugin(args, cfg, eng) if ws == 1 else None
 
     # ---- max over ranks
     rdev = dev if backend == "nccl" else "cpu"
@@ -365,6 +366,7 @@ def run_ours(args, cfg) -> dict | None:
             "e2e": {"value": e2e_all / (e2e_ms / 1e3), "unit": "interactions/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e_ms / args.steps, "path": e2e_path},
+            "e2e_plugin": plugin,
             "gpu_launches": launches,
             "gpu_launches_note": "libbh kernels launched in the timed region (sort, scans and walk included)",
             "clocks": clocks.summary(),
@@ -374,6 +376,40 @@ def run_ours(args, cfg) -> dict | None:
         dist.destroy_process_group()
     eng.close()
     return result
+
+
+def run_plugin(args, cfg, eng) -> dict:
+    """The reference-facing plugin path: kdk_step (integrator.py:47-58) on fp64
+    host ``Bodies`` with ``TreeForces`` as the accel provider -- host numpy
+    kick/drift, the positions/velocities/masses uploaded and the accelerations
+    and work read back every step (synchronous API, host clock)."""
+    from paper_2203_08966_b200.integrator import kdk_step
+    from paper_2203_08966_b200.physics import Bodies
+    from paper_2203_08966_b200.simulation import TreeForces
+
+    b = make_bodies(cfg)
+    bodies = Bodies(np.asarray(b.mass, dtype=np.float64), np.asarray(b.position, dtype=np.float64),
+                    np.asarray(b.velocity, dtype=np.float64))
+    n = len(bodies)
+    prov = TreeForces(cfg["theta"], cfg["eps"], cfg["leaf"], precision=args.precision, engine=eng)
+    prov(bodies)  # bootstrap forces (simulation.py:487)
+    kdk_step(bodies, cfg["dt"], prov)  # warm
+    k = max(1, min(args.steps, 3))
+    t = 0.0
+    inter = 0
+    for _ in range(k):
+        t0 = time.perf_counter()
+        kdk_step(bodies, cfg["dt"], prov)
+        t += time.perf_counter() - t0
+        st = eng.stats()
+        inter += st.pp + st.pc
+    # fp64 numpy positions, velocities and masses go up (converted on the device);
+    # fp64 accelerations and int64 work come back
+    return {"value": inter / t, "unit": "interactions/s", "ms_per_step": t / k * 1e3, "steps": k,
+            "h2d_bytes_per_step": n * (24 + 24 + 8),
+            "d2h_bytes_per_step": n * (24 + 8),
+            "path": "integrator.kdk_step(Bodies fp64 numpy, dt, TreeForces) -> TreeForces.forces -> "
+                    "Engine.sim_load/sim_forces/sim_store (C-ABI) per step; host numpy kick/drift"}
 
 
 def run_e2e(args, cfg, eng, sim, ws, dev, flush, ev0, ev1):

@@ -129,6 +129,10 @@ class SimResult:
         return int(self.bodies.work.sum())
 
     def phase_totals(self) -> dict:
+        """simulation.py:134-142: messages and bytes sent per phase.  The GPU
+        path has no message transport (one device: nothing is sent; several:
+        NCCL collectives and peer stores, not counted as messages), so every
+        phase reports (0, 0); the time per phase is in ``phase_seconds``."""
         return {phase: (0, 0) for phase in PHASES}
 
 
@@ -209,6 +213,8 @@ def simulate(cfg: SimConfig, *, transport: str = "inproc", record_trace: bool = 
                          [] if record_trace else None, time.monotonic() - started)
 
     eng = engine if engine is not None else Engine(cfg.precision)
+    eng.timing(True)  # per-phase device time (CUDA events on the stream) for phase_seconds
+    eng.timing_reset()
     n = len(bodies)
     pos = eng.bodies_tensor(bodies.position, bodies.mass)
     vel = eng.vec_tensor(bodies.velocity)
@@ -290,7 +296,21 @@ def simulate(cfg: SimConfig, *, transport: str = "inproc", record_trace: bool = 
     interactions = st.interactions
     final = snapshot()
     wall = time.monotonic() - started
-    phase = {p: 0.0 for p in PHASES}
-    phase["force"] = wall
-    return SimResult(cfg, final, [phase], {}, 0, snaps, [] if record_trace else None, wall,
-                     interactions)
+    return SimResult(cfg, final, [phase_seconds(eng.timing_get(), wall)], {}, 0, snaps,
+                     [] if record_trace else None, wall, interactions)
+
+
+def phase_seconds(device_ms: dict, wall: float) -> dict:
+    """The reference's phase clock (simulation.py:145-169) from the library's
+    per-phase device times: keys + sort + permutation = "decompose", tree build
+    = "build", locally-essential-tree exchange = "share", walk = "force",
+    kicks and drift = "integrate"; the rest of the wall time (host, transfers,
+    initial conditions) = "other"."""
+    sec = {p: 0.0 for p in PHASES}
+    sec["decompose"] = (device_ms.get("keys", 0.0) + device_ms.get("sort", 0.0) + device_ms.get("permute", 0.0)) / 1e3
+    sec["build"] = device_ms.get("build", 0.0) / 1e3
+    sec["share"] = device_ms.get("let", 0.0) / 1e3
+    sec["force"] = device_ms.get("walk", 0.0) / 1e3
+    sec["integrate"] = device_ms.get("integrate", 0.0) / 1e3
+    sec["other"] = max(0.0, wall - sum(sec.values()))
+    return sec

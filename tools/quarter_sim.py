@@ -137,3 +137,9 @@ base_it = sum(sum(c for _, c in grp) for grp in pp)
 for K in (16, 32, 64):
     t = sum(packed_cost(grp, K) for grp in pp)
     print(f"pp disjoint packing K={K}: body iterations {t / base_it:.3f} of broadcast")
+
+# the same packing for the pc list (certain-accept entries, count 1 each)
+base_pc = sum(len(grp) for grp in pc_cert)
+for K in (16, 32, 64):
+    t = sum(packed_cost([(m_, 1) for m_ in grp], K) for grp in pc_cert)
+    print(f"pc disjoint packing K={K}: passes {t / base_pc:.3f} of broadcast")
