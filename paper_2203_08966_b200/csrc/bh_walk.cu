@@ -637,10 +637,15 @@ constexpr int kW9Frontier = kW9Full + 32 + 8 * (kMaxLevel + 1) + 8;
 #define BH_W9_CHECK 0  // 1: latch FLAG_WALK_BOUNDS instead of overrunning (costs 1.7%; the bounds are proven)
 #endif
 #ifndef BH_W9_FLUSH
-#define BH_W9_FLUSH 16
+#define BH_W9_FLUSH 24
 #endif
-constexpr int kW9Flush = BH_W9_FLUSH;      // pc / pp lists are drained at >= kW9Flush entries
-constexpr int kW9List = kW9Flush + 32;  // a batch adds <= 32
+#ifndef BH_W9_PPFLUSH
+#define BH_W9_PPFLUSH BH_W9_FLUSH
+#endif
+constexpr int kW9Flush = BH_W9_FLUSH;      // the pc list is drained at >= kW9Flush entries
+constexpr int kW9List = kW9Flush + 32;     // a batch adds <= 32
+constexpr int kW9PpFlush = BH_W9_PPFLUSH;  // the pp list at >= kW9PpFlush (more buckets to pack)
+constexpr int kW9PpList = kW9PpFlush + 32;
 #ifndef BH_W9_BLOCK
 #define BH_W9_BLOCK 128
 #endif
@@ -708,7 +713,7 @@ struct W9Warp {
   uint2 pcm[kW9List];      // masks of the staged pc records
 #endif
   float4 pcr[kW9List][3];  // accepted cells: a (mask0 in .w), b (mask1 in .z), c
-  int4 pp[kW9List];        // pp: (lo, count, mask0, mask1) or a leaf record (cell, 0, ...)
+  int4 pp[kW9PpList];      // pp: (lo, count, mask0, mask1) or a leaf record (cell, 0, ...)
   union {
     struct {
       float4 mxr[32][3];   // mixed cells of the batch: a, b (mask0 in .z), c
@@ -1001,7 +1006,7 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
     // construction; checked anyway (warp-uniform) so a violation is loud, not a
     // shared-memory overrun
     if (BH_W9_CHECK && (sp + __popc(bfr) + __popc(bmx) > kW9Frontier || npc + __popc(bpc) > kW9List ||
-        npp + __popc(bpp) + __popc(bmx) > kW9List)) {
+        npp + __popc(bpp) + __popc(bmx) > kW9PpList)) {
       if (lane == 0) atomicOr(&f->bits, FLAG_WALK_BOUNDS);
       return;
     }
@@ -1089,7 +1094,7 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
     }
     __syncwarp();
     if (npc >= kW9Flush) { flush_pc(npc); npc = 0; }
-    if (npp >= kW9Flush) { flush_pp(npp); npp = 0; }
+    if (npp >= kW9PpFlush) { flush_pp(npp); npp = 0; }
     __syncwarp();
   }
   flush_pc(npc);

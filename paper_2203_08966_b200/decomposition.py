@@ -28,6 +28,7 @@ GPU in tests -- host-side barriers only, no kernel waits on another).
 
 from __future__ import annotations
 
+import ctypes
 import math
 import os
 import threading
@@ -878,122 +879,67 @@ class DistributedBuildSim:
         size, me = self.comm.size, self.comm.rank
         L = p.leaf_size
         nW = recs.shape[0]
-        BIG = 1 << 62
-        rows = {}
-        bbpos = n
-        maps = {}
-        if not defer:
-            off = 0
-            let_map_h = let_map.cpu().numpy()
-            for q in range(size):
-                maps[q] = let_map_h[off:off + mcnt[q]]
-                off += mcnt[q]
-        deferred = []  # defer mode: (region row, owner rank, branch index, nchild)
         host = torch.cat(br_all).cpu().numpy() if br_all else np.zeros((0, _BR_INTS), np.int32)
-        off = 0
-        for r in range(size):
-            rows_r = host[off:off + br_all[r].shape[0]]
-            off += br_all[r].shape[0]
-            if not len(rows_r):
-                continue
-            key, lev, cnt, mom, _, _, brecs = _unpack_branches(rows_r)
-            for k in range(len(key)):
-                c = int(cnt[k])
-                rows[int(key[k])] = dict(count=c, mass=float(mom[k, 0]),
-                                         com=tuple(float(x) for x in mom[k, 1:4]),
-                                         quad=tuple(float(x) for x in mom[k, 4:10]), rank=r, k=k,
-                                         rec=brecs[k].copy(), bb=bbpos if c <= L else BIG,
-                                         level=int(lev[k]))
-                if c <= L:
-                    bbpos += c
-        top = set()
-        for key in rows:
-            k = key >> 3
-            while k >= 1:
-                top.add(k)
-                k >>= 3
-        children = {k: [] for k in top}
-        for k in list(top) + list(rows):
-            if k != 1 and (k >> 3) in children:
-                children[k >> 3].append(k)
-        mom = {k: (b["mass"], b["com"], b["quad"], b["count"], b["bb"]) for k, b in rows.items()}
-        for k in sorted(top, key=lambda x: -x.bit_length()):  # deepest first (hashed.py:719-786)
-            ch = sorted(children[k], key=lambda c: c & 7)  # slot order
-            m, com, quad = _combine([mom[c][:3] for c in ch])
-            mom[k] = (m, com, quad, sum(mom[c][3] for c in ch), min(mom[c][4] for c in ch))
-        R = self.R
-
-        def mac2(level):
-            if p.theta == 0.0:
-                return float("inf")
-            r = math.ldexp(2.0 * R, -level) / p.theta
-            return r * r
-
-        def cell_record(k, d0, nchild):
-            m, com, quad, count, _ = mom[k]
-            level = (k.bit_length() - 1) // 3
-            a = np.array([-com[0], -com[1], -com[2], mac2(level)], dtype=np.float32).view(np.int32)
-            b = np.array([quad[0], quad[1], quad[1], quad[3]], dtype=np.float32).view(np.int32)
-            c = np.array([quad[2], quad[4], m, quad[5]], dtype=np.float32).view(np.int32)
-            return np.concatenate([a, b, c, np.array([d0, count, nchild, level], dtype=np.int32)])
-
-        # breadth-first layout; entries: ('top', k, first, nchild) | ('bucket', k) | ('branch', k)
-        entries = []
-        if not top:
-            entries.append(("branch", next(iter(rows))) if rows else None)
-        else:
-            entries.append(None)
-            queue = [(1, 0)]
-            qi = 0
-            while qi < len(queue):
-                k, at = queue[qi]
-                qi += 1
-                if k != 1 and mom[k][3] <= L:  # a bucket spanning ranks
-                    entries[at] = ("bucket", k)
-                    continue
-                ch = sorted(children[k], key=lambda c: c & 7)
-                first = len(entries)
-                for c in ch:
-                    entries.append(("branch", c) if c in rows else None)
-                    if c not in rows:
-                        queue.append((c, len(entries) - 1))
-                entries[at] = ("top", k, first, len(ch))
-        ntop = len(entries)
+        host = np.ascontiguousarray(host, dtype=np.int32)
+        nrows = host.shape[0]
+        row_rank = np.repeat(np.arange(size, dtype=np.int64), [b.shape[0] for b in br_all]) if br_all else \
+            np.zeros(0, np.int64)
+        row_k = np.concatenate([np.arange(b.shape[0]) for b in br_all]) if br_all else np.zeros(0, np.int64)
+        # the top of the global tree, laid out breadth first (bh_top_tree, host C++:
+        # exact fp64 recombination of the branch nodes, hashed.py:719-786)
+        cap = 22 * max(nrows, 1) + 64
+        region = np.zeros((cap, _REC_INTS), dtype=np.int32)
+        kind = np.zeros(cap, dtype=np.int32)
+        row_of = np.full(cap, -1, dtype=np.int32)
+        bb = np.zeros(max(nrows, 1), dtype=np.int64)
+        L_ = _lib.lib()
+        ntop = int(L_.bh_top_tree(host.ctypes.data_as(ctypes.c_void_p), nrows, n, L, float(self.R), float(p.theta),
+                                  region.ctypes.data_as(ctypes.c_void_p), kind.ctypes.data_as(ctypes.c_void_p),
+                                  row_of.ctypes.data_as(ctypes.c_void_p), bb.ctypes.data_as(ctypes.c_void_p), cap))
+        if ntop < 0:
+            raise RuntimeError("top-tree assembly: region capacity exceeded")
+        region, kind, row_of = region[:ntop], kind[:ntop], row_of[:ntop]
+        # branch-node entries: redirect each subtree / bucket to where it lives
+        e = np.nonzero(kind == 2)[0]
+        rows = row_of[e].astype(np.int64)
+        q = row_rank[rows]
+        k = row_k[rows]
+        cnt = host[rows, 3:5].copy().view(np.int64).ravel() if len(rows) else np.zeros(0, np.int64)
+        rec = region[e]
+        internal = rec[:, 14] > 0
+        own = q == me
+        deferred = []
+        m = own & internal  # own subtree: first child in the own records, bodies at 0
+        rec[m, 12] += ntop
         if not defer:
             letoff = np.cumsum([0] + list(rcnt))[:-1] + ntop + nW
             lbodoff = np.cumsum([0] + list(bcnt))[:-1] + n + nbb
-        region = []
-        for e in entries:
-            if e[0] == "top":
-                region.append(cell_record(e[1], e[2], e[3]))
-            elif e[0] == "bucket":
-                region.append(cell_record(e[1], mom[e[1]][4], 0))
-            else:
-                b = rows[e[1]]
-                rec = b["rec"].copy()
-                q = b["rank"]
-                if q == me:  # own subtree: first child in the own records, bodies at 0
-                    if rec[14] > 0:
-                        rec[12] += ntop
-                elif rec[14] > 0 and defer:  # subtree in flight: pass A defers it (f4)
-                    deferred.append((len(region), q, b["k"], int(rec[14])))
-                    rec[12], rec[14] = -1, 0
-                    rec[15] |= _DEFER_BIT
-                elif rec[14] > 0:
-                    fc = int(maps[q][b["k"], 0])
-                    if fc >= 0:
-                        rec[12] = fc + letoff[q]
-                    else:  # no target here opens it
-                        rec[12], rec[14] = -1, 0
-                elif b["count"] <= L:
-                    rec[12] = b["bb"]
-                elif defer:  # a duplicate-key cell resolved over LET bodies: no overlap this step
-                    return None, None
-                else:
-                    fb = int(maps[q][b["k"], 1])
-                    rec[12] = fb + lbodoff[q] if fb >= 0 else -1
-                region.append(rec)
-        parts = [torch.as_tensor(np.array(region, dtype=np.int32).reshape(-1, _REC_INTS), device=dev)]
+            mbase = np.cumsum([0] + list(mcnt))[:-1]
+            let_map_h = let_map.cpu().numpy() if let_map.numel() else np.zeros((0, 2), np.int32)
+        m = (~own) & internal
+        if defer:  # subtree in flight: pass A defers it (f4)
+            idx = np.nonzero(m)[0]
+            deferred = list(zip(e[idx].tolist(), q[idx].tolist(), k[idx].tolist(), rec[idx, 14].tolist()))
+            rec[idx, 12] = -1
+            rec[idx, 14] = 0
+            rec[idx, 15] |= _DEFER_BIT
+        elif m.any():
+            idx = np.nonzero(m)[0]
+            fc = let_map_h[mbase[q[idx]] + k[idx], 0]
+            rec[idx, 12] = np.where(fc >= 0, fc + letoff[q[idx]], -1)
+            rec[idx, 14] = np.where(fc >= 0, rec[idx, 14], 0)  # no target here opens it
+        # remote leaves / buckets (own ones keep their own body index)
+        small = (~own) & (~internal) & (cnt <= L)
+        rec[small, 12] = bb[rows[small]]
+        dup = (~own) & (~internal) & (cnt > L)  # a duplicate-key cell resolved over the owner's bodies
+        if dup.any():
+            if defer:
+                return None, None  # resolved over LET bodies: no overlap this step
+            idx = np.nonzero(dup)[0]
+            fb = let_map_h[mbase[q[idx]] + k[idx], 1]
+            rec[idx, 12] = np.where(fb >= 0, fb + lbodoff[q[idx]], -1)
+        region[e] = rec
+        parts = [torch.as_tensor(region.reshape(-1, _REC_INTS), device=dev)]
         x = recs.clone()
         x[:, 12] = torch.where(x[:, 14] > 0, x[:, 12] + ntop, x[:, 12])
         parts.append(x)

@@ -265,3 +265,73 @@ def test_peer_store_failure_falls_back(monkeypatch):
     monkeypatch.setenv("BH_P2P", "1")
     with pytest.raises(RuntimeError, match="disagree"):
         _thread_ranks([PeerOracleEngine(drop=5), PeerOracleEngine(drop=5)], 1)
+
+
+def test_host_top_tree_recombines_the_oracle_tree():
+    """bh_top_tree (libbh host C++, the distributed step's top-tree assembly):
+    given the level-3 cells of the oracle tree as branch nodes (any rank
+    layout), the top cells it recombines carry the oracle's own fp64 moments,
+    counts and children, laid out breadth first with children contiguous in
+    slot order, and each branch entry points back at its row."""
+    import ctypes
+
+    from oracle import oracle as orc
+    from paper_2203_08966_b200 import _lib
+    from paper_2203_08966_b200.decomposition import _BR_INTS, _REC_INTS, _pack_branches
+    from paper_2203_08966_b200.initcond import make_rng, plummer_cluster
+
+    b = plummer_cluster(5000, make_rng(4))
+    pos = np.asarray(b.position, dtype=np.float64)
+    m = np.asarray(b.mass, dtype=np.float64)
+    R = orc.bounds(pos)
+    o = orc.sort_order(orc.morton_keys(pos, R))
+    t = orc.build_tree(m[o], pos[o], R)
+    L, theta = 16, 0.6
+    # branch nodes: the cells at level 3 plus shallower leaves (a partition of the bodies)
+    keys = t.key.astype(np.int64)
+    lev = t.level.astype(np.int64)
+    is_br = (lev == 3) | ((lev < 3) & (t.count == 1))
+    br_idx = np.nonzero(is_br)[0]
+    assert t.count[br_idx].sum() == len(m)
+    nb = len(br_idx)
+    mom = np.concatenate([t.mass[br_idx, None], t.com[br_idx], t.quad[br_idx]], axis=1)
+    rows = _pack_branches(dict(
+        key=torch.from_numpy(keys[br_idx]), level=torch.from_numpy(lev[br_idx].astype(np.int32)),
+        count=torch.from_numpy(t.count[br_idx].astype(np.int64)), mom=torch.from_numpy(mom),
+        rec=torch.zeros(nb, dtype=torch.int32), lo=torch.zeros(nb, dtype=torch.int32),
+        recs=torch.from_numpy(np.arange(nb * _REC_INTS, dtype=np.int32).reshape(nb, _REC_INTS)))).numpy()
+    rows = np.ascontiguousarray(rows)
+    cap = 22 * nb + 64
+    region = np.zeros((cap, _REC_INTS), np.int32)
+    kind = np.zeros(cap, np.int32)
+    row_of = np.zeros(cap, np.int32)
+    bb = np.zeros(nb, np.int64)
+    P = ctypes.c_void_p
+    ne = _lib.lib().bh_top_tree(rows.ctypes.data_as(P), nb, 0, L, float(R), theta, region.ctypes.data_as(P),
+                                kind.ctypes.data_as(P), row_of.ctypes.data_as(P), bb.ctypes.data_as(P), cap)
+    assert ne > 0
+    cell_of_key = {int(k): c for c, k in enumerate(keys)}
+    # walk the region from the root, matching oracle cells
+    stack = [(0, 1)]
+    seen = 0
+    while stack:
+        e, key = stack.pop()
+        c = cell_of_key[key]
+        if kind[e] == 2:
+            assert keys[br_idx[row_of[e]]] == key
+            np.testing.assert_array_equal(region[e], rows[row_of[e], 27:27 + _REC_INTS])
+            continue
+        rec = region[e]
+        f = rec.view(np.float32)
+        assert f[10] == np.float32(t.mass[c]) and rec[13] == t.count[c]
+        np.testing.assert_array_equal(f[[0, 1, 2]], (-t.com[c]).astype(np.float32))
+        np.testing.assert_array_equal(f[[4, 5, 7, 8, 9, 11]], t.quad[c][[0, 1, 3, 2, 4, 5]].astype(np.float32))
+        seen += 1
+        if kind[e] == 1:  # a bucket-sized top cell
+            assert t.count[c] <= L and rec[14] == 0
+            continue
+        kids = [int(k) for k in t.children[c] if k >= 0]
+        assert rec[14] == len(kids)
+        for j, k in enumerate(kids):
+            stack.append((rec[12] + j, int(keys[k])))
+    assert seen > 10
