@@ -174,6 +174,10 @@ struct bh_handle {
     t.bod64 = tbod64;
     t.cm64 = cm64.as<double4>();
     t.q64 = q64.as<double>();
+    if (mom_leaf > 1) {  // a walk-only tree: its class bytes (emit) speed up the compaction
+      t.mclass = mclass.as<uint8_t>();
+      t.mleaf = mom_leaf;
+    }
     return t;
   }
 };
@@ -343,6 +347,7 @@ int build_sorted_async(bh_handle *h, int64_t n, const float4 *bod32, cudaStream_
   h->walk_valid = false;
   h->tbod32 = bod32;
   h->tbod64 = nullptr;
+  h->mom_leaf = 0;  // (the class bytes of an earlier tree are stale)
   TreeView t = h->view();
   if (leaf > 1) {  // a walk-only tree: the emit kernel classifies the cells for the moments
     BH_CUDA(h->mclass.ensure(cap + 16));

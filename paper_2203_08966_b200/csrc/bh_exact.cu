@@ -296,7 +296,7 @@ __global__ void k_emit(TreeView t, const float4 *__restrict__ bod32,
       if (t.mclass) t.mclass[c] = par_open ? 1 : 0;  // never opened (level 21): a bucket
     } else if (l == depth) {
       t.link[c] = make_int4(c + 1, 1, (int)i, l);
-      if (t.mclass) t.mclass[c] = 0;
+      if (t.mclass) t.mclass[c] = par_open ? kClassLeafRecord : 0;  // a walk record iff its parent opens
       double4 b;
       if (bod64) {
         b = bod64[i];
@@ -602,7 +602,7 @@ __global__ void __launch_bounds__(256, BH_MOM_MINB) k_moments_coop(TreeView t, i
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         rank[q] = brank[q] = -1;
-        if (cl[q] >= 2) rank[q] = atomicAdd(&h[cl[q] - 2], 1);
+        if (cl[q] >= 2 && cl[q] != kClassLeafRecord) rank[q] = atomicAdd(&h[cl[q] - 2], 1);
         else if (cl[q] == 1) brank[q] = atomicAdd(&hb, 1);
       }
       __syncthreads();

@@ -129,12 +129,14 @@ struct TreeView {
   const double4 *bod64 = nullptr;
   double4 *cm64 = nullptr;
   double *q64 = nullptr;   // [C][6]
-  // fp32 walk-only builds (leaf size mleaf > 1): per-cell moments class written
-  // by the emit kernel -- 0: nothing to form (a leaf, or inside a bucket),
-  // 1: a bucket (moments from its bodies), 2 + level: a cell the walk opens
+  // fp32 walk-only builds (leaf size mleaf > 1): per-cell class written by the
+  // emit kernel -- 0: not a walk record (inside a bucket), 1: a bucket (moments
+  // from its bodies), 2 + level: a cell the walk opens, kClassLeafRecord: a
+  // one-body walk record (its body is its moments)
   uint8_t *mclass = nullptr;
   int mleaf = 0;
 };
+constexpr uint8_t kClassLeafRecord = 255;
 void launch_emit(const TreeView &t, const float4 *bod32, const double4 *bod64, cudaStream_t s);
 // cursor: int[kMaxLevel+1] scratch; list: int[C]
 // Moments: C on device (launch_set_count) or host, per-level counts on device

@@ -97,7 +97,12 @@ __global__ void k_nchild_rows(TreeView t, int leaf, uint32_t *__restrict__ nck) 
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= t.C) return;
   uint32_t k = 0u;
-  if (c < tree_count(t) && !tree_overflowed(t) && expandable(t, c, leaf, nullptr)) {
+  // walk-only builds for this leaf size: the emit kernel's class byte says which
+  // cells the walk opens (no link read for the cells inside buckets)
+  const bool opens = t.mclass && t.mleaf == leaf
+                         ? (t.mclass[c] >= 2 && t.mclass[c] != kClassLeafRecord)
+                         : (c < tree_count(t) && expandable(t, c, leaf, nullptr));
+  if (c < tree_count(t) && !tree_overflowed(t) && opens) {
     const int4 *row = reinterpret_cast<const int4 *>(t.child8 + 8 * c);
     const int4 r0 = row[0], r1 = row[1];
     k = (r0.x != -1) + (r0.y != -1) + (r0.z != -1) + (r0.w != -1) + (r1.x != -1) + (r1.y != -1) +
@@ -131,6 +136,10 @@ __global__ void k_compact(TreeView t, const double *__restrict__ dR, double thet
   if (c == C - 1) *dCp = (int)(1 + base[C - 1] + nck[C - 1]);
   int j = 0;
   if (c > 0) {
+    if (t.mclass && t.mleaf == leaf && !force && t.mclass[c] == 0) {  // inside a bucket (class byte)
+      if (rec_of_cell) rec_of_cell[c] = -1;
+      return;
+    }
     const int P = t.parent[c];
     if (!expandable(t, P, leaf, force)) {  // pruned (inside a bucket)
       if (rec_of_cell) rec_of_cell[c] = -1;
@@ -439,7 +448,7 @@ extern "C" int bh_debug_walk_hist(unsigned long long *out) {
 //                  fcnc[record]) and adding into acc/work atomically.
 enum { kWalkFull = 0, kWalkDefer = 1, kWalkResume = 2 };
 #ifndef BH_BUCKET_UNROLL
-#define BH_BUCKET_UNROLL 4
+#define BH_BUCKET_UNROLL 2
 #endif
 constexpr int kBucketUnroll = BH_BUCKET_UNROLL;  // bucket pp loop unroll
 
@@ -640,7 +649,7 @@ constexpr int kW9Frontier = kW9Full + 32 + 8 * (kMaxLevel + 1) + 8;
 #define BH_W9_FLUSH 24
 #endif
 #ifndef BH_W9_PPFLUSH
-#define BH_W9_PPFLUSH BH_W9_FLUSH
+#define BH_W9_PPFLUSH 40
 #endif
 constexpr int kW9Flush = BH_W9_FLUSH;      // the pc list is drained at >= kW9Flush entries
 constexpr int kW9List = kW9Flush + 32;     // a batch adds <= 32
