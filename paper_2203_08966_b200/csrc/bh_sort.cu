@@ -38,8 +38,14 @@ namespace {
 constexpr int kDigitBits = 8;
 constexpr int kBins = 1 << kDigitBits;
 constexpr int kPasses = 8;  // 64 bits; the top pass sees bits 56..62 (bit 63 is 0)
+#ifndef BH_SORT_ITEMS
+#define BH_SORT_ITEMS 16
+#endif
+#ifndef BH_SORT_BLOCKS
+#define BH_SORT_BLOCKS 3  // pass-kernel blocks per SM the register budget is set for
+#endif
 constexpr int kSortThreads = 256;
-constexpr int kSortItems = 16;
+constexpr int kSortItems = BH_SORT_ITEMS;
 constexpr int kTile = kSortThreads * kSortItems;  // 4096 keys
 constexpr int kSortWarps = kSortThreads / 32;
 static_assert(kSortThreads == kBins, "one thread per digit");
@@ -515,13 +521,13 @@ cudaError_t sort_pairs(void *temp, size_t temp_bytes, const uint64_t *kin, uint6
     const char *m = getenv("BH_SORT_MATCH");
     variant = ((e && atoi(e) == 2) ? 1 : 0) | ((m && atoi(m) == 1) ? 2 : 0);
     const int sm = (int)sizeof(PassSmem);
-    cudaFuncSetAttribute(k_sort_pass<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_sort_pass<BH_SORT_BLOCKS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     cudaFuncSetAttribute(k_sort_pass<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    cudaFuncSetAttribute(k_sort_pass<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_sort_pass<BH_SORT_BLOCKS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     cudaFuncSetAttribute(k_sort_pass<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
   }
-  auto pass = variant == 0 ? k_sort_pass<3, false> : variant == 1 ? k_sort_pass<2, false>
-            : variant == 2 ? k_sort_pass<3, true> : k_sort_pass<2, true>;
+  auto pass = variant == 0 ? k_sort_pass<BH_SORT_BLOCKS, false> : variant == 1 ? k_sort_pass<2, false>
+            : variant == 2 ? k_sort_pass<BH_SORT_BLOCKS, true> : k_sort_pass<2, true>;
   k_sort_zero<<<1, 256, 0, s>>>(t.hist, t.counters);
   {
     static int sms = 0;

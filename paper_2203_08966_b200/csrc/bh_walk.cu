@@ -646,10 +646,10 @@ constexpr int kW9Frontier = kW9Full + 32 + 8 * (kMaxLevel + 1) + 8;
 #define BH_W9_CHECK 0  // 1: latch FLAG_WALK_BOUNDS instead of overrunning (costs 1.7%; the bounds are proven)
 #endif
 #ifndef BH_W9_FLUSH
-#define BH_W9_FLUSH 24
+#define BH_W9_FLUSH 20
 #endif
 #ifndef BH_W9_PPFLUSH
-#define BH_W9_PPFLUSH 40
+#define BH_W9_PPFLUSH 64
 #endif
 constexpr int kW9Flush = BH_W9_FLUSH;      // the pc list is drained at >= kW9Flush entries
 constexpr int kW9List = kW9Flush + 32;     // a batch adds <= 32
