@@ -143,6 +143,10 @@ struct bh_handle {
   }
   void tbegin(int phase, cudaStream_t s) {
     if (!timing) return;
+    if (open.a) {  // a phase left open by an error return: recycle its events, drop the mark
+      pool.push_back(open.a);
+      pool.push_back(open.b);
+    }
     open.phase = phase;
     open.a = get_event();
     open.b = get_event();
@@ -435,6 +439,16 @@ int ensure_walk_tree(bh_handle *h, double theta, int leaf, cudaStream_t s) {
   return BH_OK;
 }
 
+// An upper bound on the walk records of the current tree (the walk's record
+// indices must fit the v9 frontier word's 28 bits): the records are a subset
+// of the cells; a sync-free build knows its cell count only from the last
+// readback, so the bound then takes the last count with growth slack.
+int64_t walk_records_bound(bh_handle *h) {
+  const int64_t alloc = (int64_t)(h->wnodes.bytes / sizeof(WalkNode));
+  if (!h->async_tree) return std::min<int64_t>(alloc, h->C);
+  return h->C_true > 0 ? std::min<int64_t>(alloc, h->C_true + h->C_true / 4 + 1024) : alloc;
+}
+
 int reset_counters(bh_handle *h, cudaStream_t s) {
   BH_CUDA(cudaMemsetAsync(&h->flags->pp, 0, 2 * sizeof(unsigned long long), s));
   return BH_OK;
@@ -580,11 +594,11 @@ int sim_walk(bh_handle *h, double theta, double eps, int leaf, int64_t begin, in
   const bool f32 = h->precision == BH_FP32;
   if (begin < 0 || end > n || begin > end) return fail(BH_BAD_ARG, "walk range outside [0, n]");
   const int64_t nt = end - begin;
+  if (h->npeers && (h->acc.p != h->peer_own_acc || h->work_sorted.p != h->peer_own_work))
+    return fail(BH_BAD_ARG, "result buffers reallocated since the peers mapped them: set peers again");
   BH_TRY(reset_counters(h, s));
   h->tbegin(BH_PHASE_WALK, s);
   int *w32 = record_work ? h->work_sorted.as<int>() + begin : nullptr;
-  if (h->npeers && (h->acc.p != h->peer_own_acc || h->work_sorted.p != h->peer_own_work))
-    return fail(BH_BAD_ARG, "result buffers reallocated since the peers mapped them: set peers again");
   W9Peers peers;  // the same rows of every peer's buffers (replicated ranks)
   peers.n = h->npeers;
   const size_t row = f32 ? sizeof(float4) : sizeof(double4);
@@ -594,7 +608,7 @@ int sim_walk(bh_handle *h, double theta, double eps, int leaf, int64_t begin, in
   }
   if (f32) {
     BH_TRY(ensure_walk_tree(h, theta, leaf, s));
-    launch_walk_f32(h->wnodes.as<WalkNode>(), (int64_t)(h->wnodes.bytes / sizeof(WalkNode)), h->pos.as<float4>(),
+    launch_walk_f32(h->wnodes.as<WalkNode>(), walk_records_bound(h), h->pos.as<float4>(),
                     h->pos.as<float>() + 4 * begin, 4, nullptr, (int)nt, (float)(eps * eps), leaf,
                     h->acc.as<float>() + 4 * begin, 4, nullptr, w32, h->flags, s, h->npeers ? &peers : nullptr);
   } else {
@@ -908,7 +922,7 @@ static int traverse_common(bh_handle *h, const void *targets, int64_t n, double 
   fill_walk_params(h, P, n, theta, eps, leaf);
   if (f32) {
     BH_TRY(ensure_walk_tree(h, theta, leaf, s));
-    launch_walk_f32(h->wnodes.as<WalkNode>(), (int64_t)(h->wnodes.bytes / sizeof(WalkNode)), h->tbod.as<float4>(),
+    launch_walk_f32(h->wnodes.as<WalkNode>(), walk_records_bound(h), h->tbod.as<float4>(),
                     static_cast<const float *>(targets), 4, h->vals2.as<uint32_t>(), (int)n,
                     (float)(eps * eps), leaf, static_cast<float *>(acc), 4, work, nullptr,
                     h->flags, s);

@@ -419,6 +419,11 @@ void launch_let_branchmap(const WalkNode *W, const int *brec, int nb, int nrec, 
 }
 
 __device__ __forceinline__ float2 f2(float x, float y) { return make_float2(x, y); }
+// a v9 frontier word: first child | nchild << 28, built unsigned (nchild = 8
+// would shift into the sign bit of an int)
+__device__ __forceinline__ int fc_word(int first, int nchild) {
+  return (int)((unsigned)first | ((unsigned)nchild << 28));
+}
 __device__ __forceinline__ float2 f2(float x) { return make_float2(x, x); }
 
 #ifndef BH_WALK_BLOCK
@@ -792,14 +797,14 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
     const int2 fc = dfr.fcnc[entry.y];
     if (fc.y <= 0) sp = 0;
     else if (lane == 0) {
-      S.fc[0] = fc.x | fc.y << kW9NcShift;
+      S.fc[0] = fc_word(fc.x, fc.y);
       S.fm[0] = make_uint2((unsigned)entry.z, (unsigned)entry.w);
     }
   } else {
     const unsigned m0 = __ballot_sync(FULL, v0), m1 = __ballot_sync(FULL, v1);
     if (lane == 0) {  // root internal: start at its children (flattree.py:271-279)
       const int4 rd = T[0].d;
-      S.fc[0] = rd.y > 1 ? (rd.x | rd.z << kW9NcShift) : (0 | 1 << kW9NcShift);
+      S.fc[0] = rd.y > 1 ? fc_word(rd.x, rd.z) : fc_word(0, 1);
       S.fm[0] = make_uint2(m0, m1);
     }
   }
@@ -972,7 +977,7 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
     const unsigned starts = __reduce_or_sync(FULL, take > 0 ? 1u << excl : 0u);
     __syncwarp();
     if ((int)lane == kfull && lane < (unsigned)ne && take > 0)  // partly used: keep the rest
-      S.fc[sp - 1 - lane] = (E.x + take) | (E.y - take) << kW9NcShift;
+      S.fc[sp - 1 - lane] = fc_word(E.x + take, E.y - take);
     sp -= kfull;
     const int src = __popc(starts & (FULL >> (31 - lane))) - 1;
     const int cfc = __shfl_sync(FULL, E.x, src), cex = __shfl_sync(FULL, excl, src);
@@ -1036,7 +1041,7 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
     }
     if (to_fr) {
       const int slot = sp + __popc(bfr & lt);
-      S.fc[slot] = d.x | d.z << kW9NcShift;
+      S.fc[slot] = fc_word(d.x, d.z);
       S.fm[slot] = make_uint2(m0, m1);
     }
     if (to_mx) {
@@ -1087,7 +1092,7 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
       if ((o0 | o1) == 0u) continue;
       if (dd.z > 0) {
         if (lane == 0) {
-          S.fc[sp] = dd.x | dd.z << kW9NcShift;
+          S.fc[sp] = fc_word(dd.x, dd.z);
           S.fm[sp] = make_uint2(o0, o1);
         }
         ++sp;

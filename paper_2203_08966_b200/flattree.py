@@ -1,13 +1,20 @@
 """Batched force traversal -- drop-in for ``nbsim.flattree.FlatTree.traverse``
 (/root/reference/pkg/src/nbsim/flattree.py:142-166, kernel 258-317).
 
-The walk runs as a warp-cooperative CUDA kernel (bh_traverse_*): targets are
-Morton-ordered internally, each warp walks the union of its 32 targets'
-interaction lists in pre-order (stackless, via subtree skip links), and every
-lane evaluates exactly the reference's list -- in the reference's order -- so
-the fp64 mode reproduces the reference bit for bit and the fp32 mode differs
-only by fp32 rounding.  ``leaf_size > 1`` adds the bucket rule of SURVEY.md
-§8(c) (cells of <= leaf_size bodies that fail the MAC are summed body by body).
+The walk runs as a warp-cooperative CUDA kernel (bh_traverse_*), with the
+targets Morton-ordered internally:
+
+* fp64 (validation): each warp walks the union of its 32 targets' interaction
+  lists in pre-order (stackless, via subtree skip links) and every lane
+  evaluates exactly the reference's list in the reference's order, so the
+  result is the reference's to <= 1 ulp per pp term;
+* fp32: the group-classified walk (k_walk9): 64 targets per warp,
+  cells classified 32 at a time against the group's box (certain accept, certain
+  open, or per-target MAC), with dense pc / pp drains.  Every target gets exactly
+  the reference's interaction set; only the fp32 summation order differs.
+
+``leaf_size > 1`` adds the bucket rule of SURVEY.md §8(c) (cells of <= leaf_size
+bodies that fail the MAC are summed body by body).
 """
 
 from __future__ import annotations

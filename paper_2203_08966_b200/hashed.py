@@ -4,8 +4,9 @@
 ``build_hashed`` builds the reference's tree (one body per leaf, single-child
 chains kept, pre-order cells, monopole + quadrupole moments) on the GPU from
 Morton-sorted bodies: lcp levels -> cells per body -> exclusive scan ->
-parallel cell emission -> last-arriver bottom-up moments (bh_build_*).  In fp64
-mode every cell array is bit-identical to the reference's (tests/test_gpu_*).
+parallel cell emission -> level-synchronous bottom-up moments in one
+cooperative launch (bh_build_*).  In fp64 mode every cell array is
+bit-identical to the reference's (tests/test_gpu_*).
 
 The tree stays on the device inside its own engine handle; ``arrays()``
 exports the FlatTree/HashedTree arrays and ``to_serial_bytes()`` the

@@ -21,6 +21,12 @@ FP64_TOL = 1e-10  # relative L2, fp64 mode (north star)
 # the only differences are <= 1 ulp in pp terms, where glibc's pow (used by the
 # reference for (d2+e2)**1.5) is not correctly rounded and the GPU's is.
 ULP_TOL = 1e-14
+# fp32 mode: a target whose fp32 d2 and the oracle's fp64 d2 fall on opposite
+# sides of a MAC threshold takes a different interaction (a rounding tie).
+# Measured: 0 of 2000 (golden n=2000, 3 theta), 0 of 4000 (Plummer 1e5, L=1/16/32),
+# 0 of 2000 at cfg3 1e7 and the cfg4 shape 2e6, 0 of 4000 at cfg4 1e8; the bound
+# allows one flip per 2000 targets.
+FP32_WORK_FLIPS = 5e-4
 
 
 def assert_fp64_close(got, want):
@@ -241,7 +247,9 @@ class TestTraverse:
         flat = build_hashed(Bodies(m[order], pos[order], np.zeros((n, 3))), DomainBounds(R), precision="fp32").flat()
         acc, work = flat.traverse(pos, theta, 0.05)
         assert rel_l2(acc, ref_acc) <= FP32_TOL
-        assert np.mean(work != ref_work) < 0.01
+        mism = int(np.sum(work != ref_work))
+        print(f"WORKMISMATCH golden2000 theta={theta}: {mism}/{n}")
+        assert mism <= FP32_WORK_FLIPS * n
 
     def test_work_totals_known_answers_fp64(self):
         """test_output.txt:350: 310,605 / 6,805,731 / 112,497,303 (theta .5, eps .05)."""
@@ -281,7 +289,9 @@ class TestTraverse:
             np.testing.assert_array_equal(work, ref_work)
         else:
             assert err <= FP32_TOL
-            assert np.mean(work != ref_work) < 0.01
+            mism = int(np.sum(work != ref_work))
+            print(f"WORKMISMATCH plummer1e5 L={leaf}: {mism}/{len(sample)}")
+            assert mism <= FP32_WORK_FLIPS * len(sample)
 
     @pytest.mark.parametrize("n", [1, 2, 5, 17, 64])
     @pytest.mark.parametrize("precision", ["fp32", "fp64"])
@@ -490,7 +500,12 @@ class TestDuplicateKeysGPU:
             acc, work = tree.flat().traverse(pos, 0.5, 0.01, leaf_size=L)
             tol = FP32_TOL if precision == "fp32" else ULP_TOL
             assert rel_l2(acc, ref_acc) <= tol
-            assert np.mean(work != ref_work) < (0.01 if precision == "fp32" else 1e-12)
+            mism = int(np.sum(work != ref_work))
+            print(f"WORKMISMATCH duplicates {precision} L={L}: {mism}/{len(pos)}")
+            if precision == "fp32":
+                assert mism <= FP32_WORK_FLIPS * len(pos)
+            else:
+                assert mism == 0
 
 
 @pytest.mark.parametrize("steps", [1, 3])

@@ -59,7 +59,8 @@ def _check(pos32, m32, theta, eps, leaf, allow_dup, nsample=2000, seed=11):
     err = float(np.linalg.norm(acc[sample] - ref_acc) / np.linalg.norm(ref_acc))
     assert err <= FP32_TOL, err
     mism = float(np.mean(work[sample] != ref_work))
-    assert mism <= 2e-3, mism  # fp32 d2 vs fp64 d2 at a MAC tie: rare
+    print(f"WORKMISMATCH scale n={len(pos32)}: {mism * nsample:.0f}/{nsample}")
+    assert mism <= 5e-4, mism  # fp32 d2 vs fp64 d2 at a MAC tie (measured: 0)
     assert st.pp + 2 * st.pc == int(work.sum())
     return err, mism
 
