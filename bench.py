@@ -589,7 +589,9 @@ def run_reference(args, cfg) -> dict | None:
     per_step_budget = 100.0 / max(1, args.steps + args.warmup)
     s = int(min(n, max(1000, len(probe) * per_step_budget / max(ts, 1e-3))))
     sample = np.sort(rng.choice(n, s, replace=False))
-    for _ in range(args.warmup):
+    # warm-up: one untimed step is enough for host code (the serial build of a
+    # 1e7-body tree is ~7 s; W of them would only stretch the run)
+    for _ in range(min(args.warmup, 1)):
         cpu_reference_step(b, cfg, sample, nthreads)
     tot_s = 0.0
     tot_i = 0.0
