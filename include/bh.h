@@ -269,6 +269,19 @@ int bh_walk_records_f32(bh_handle *h, const void *d_records, int64_t nrec, const
                         float *d_acc4, int32_t *d_work, void *stream);
 int bh_stats_get(bh_handle *h, bh_stats *out, void *stream);
 
+/* ---- distributed build, host side ------------------------------------------ */
+/* hashed.py:719-786: the top of the global tree from every rank's branch nodes
+ * (host memory).  rows: nrows int32 rows as decomposition._pack_branches packs
+ * them (key, level, count, fp64 mass/com/quad, record index, first body, walk
+ * record); n_own: this rank's bodies (the bucket-sized branch nodes' bodies
+ * follow them).  Writes the breadth-first top region (16-int walk records) into
+ * region[cap][16] with kind[e] (0 top cell, 1 bucket-sized top cell, 2 branch
+ * node: the row's record, unpatched) and row_of[e]; bb[r] = row r's first body
+ * in the [own | branch bodies] list (bucket-sized rows, else -1).  Returns the
+ * number of region entries, or -1 if cap is too small. */
+int64_t bh_top_tree(const int32_t *rows, int64_t nrows, int64_t n_own, int leaf, double R, double theta,
+                    int32_t *region, int32_t *kind, int32_t *row_of, int64_t *bb, int64_t cap);
+
 /* ---- instrumentation ----------------------------------------------------- */
 /* Enable per-phase CUDA-event timing of bh_sim_* calls (adds event records). */
 int bh_timing_enable(bh_handle *h, int on);

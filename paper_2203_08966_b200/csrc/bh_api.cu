@@ -178,9 +178,11 @@ struct bh_handle {
     t.bod64 = tbod64;
     t.cm64 = cm64.as<double4>();
     t.q64 = q64.as<double>();
-    if (mom_leaf > 1) {  // a walk-only tree: its class bytes (emit) speed up the compaction
-      t.mclass = mclass.as<uint8_t>();
+    if (mom_leaf > 1) {  // a walk-only tree: its class bytes (emit) and the moments'
+      t.mclass = mclass.as<uint8_t>();  // lists of opened cells drive the compaction
       t.mleaf = mom_leaf;
+      t.mlvl = lvl.as<int>();
+      t.mlist = lvl_list.as<int>();
     }
     return t;
   }

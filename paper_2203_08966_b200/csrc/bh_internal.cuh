@@ -135,6 +135,10 @@ struct TreeView {
   // one-body walk record (its body is its moments)
   uint8_t *mclass = nullptr;
   int mleaf = 0;
+  // and the moments kernel's lists of the opened cells: level counts / offsets /
+  // listed counts (3 x 22 ints) and the cell list
+  const int *mlvl = nullptr;
+  const int *mlist = nullptr;
 };
 constexpr uint8_t kClassLeafRecord = 255;
 void launch_emit(const TreeView &t, const float4 *bod32, const double4 *bod64, cudaStream_t s);

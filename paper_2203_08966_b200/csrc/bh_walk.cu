@@ -111,6 +111,29 @@ __global__ void k_nchild_rows(TreeView t, int leaf, uint32_t *__restrict__ nck) 
   nck[c] = k;
 }
 
+// The 64-byte walk record of cell c (MAC threshold from R, negated com,
+// paired quadrupole words, first child or first body)
+__device__ __forceinline__ WalkNode walk_record(const TreeView &t, int64_t c, const double *__restrict__ dR,
+                                                double theta, bool internal, const uint32_t *__restrict__ nck,
+                                                const uint32_t *__restrict__ base) {
+  const int4 L = t.link[c];
+  const double4 cm = t.cm64[c];
+  WalkNode nd;
+  // negated com: the walk forms d = p - com as p + a (one FADD2 per axis)
+  const double r = ldexp(2.0 * dR[0], -L.w) / theta;  // theta == 0 -> inf: never accept
+  nd.a = make_float4(-(float)cm.x, -(float)cm.y, -(float)cm.z, (float)(r * r));
+  float q0 = 0.f, q1 = 0.f, q2 = 0.f, q3 = 0.f, q4 = 0.f, q5 = 0.f;
+  if (L.y > 1) {
+    const double *q = t.q64 + kQStride * c;
+    q0 = (float)q[0]; q1 = (float)q[1]; q2 = (float)q[2];
+    q3 = (float)q[3]; q4 = (float)q[4]; q5 = (float)q[5];
+  }
+  nd.b = make_float4(q0, q1, q1, q3);
+  nd.c = make_float4(q2, q4, (float)cm.w, q5);
+  nd.d = make_int4(internal ? 1 + (int)base[c] : L.z, L.y, internal ? (int)nck[c] : 0, L.w);
+  return nd;
+}
+
 __global__ void k_compact(TreeView t, const double *__restrict__ dR, double theta, int leaf,
                           const uint8_t *force, const uint32_t *__restrict__ smask,
                           const uint32_t *__restrict__ nck, const uint32_t *__restrict__ base,
@@ -162,20 +185,6 @@ __global__ void k_compact(TreeView t, const double *__restrict__ dR, double thet
       j = 1 + (int)base[P] + rank;
     }
   }
-  const int4 L = t.link[c];
-  const double4 cm = t.cm64[c];
-  WalkNode nd;
-  // negated com: the walk forms d = p - com as p + a (one FADD2 per axis)
-  const double r = ldexp(2.0 * dR[0], -L.w) / theta;  // theta == 0 -> inf: never accept
-  nd.a = make_float4(-(float)cm.x, -(float)cm.y, -(float)cm.z, (float)(r * r));
-  float q0 = 0.f, q1 = 0.f, q2 = 0.f, q3 = 0.f, q4 = 0.f, q5 = 0.f;
-  if (L.y > 1) {
-    const double *q = t.q64 + kQStride * c;
-    q0 = (float)q[0]; q1 = (float)q[1]; q2 = (float)q[2];
-    q3 = (float)q[3]; q4 = (float)q[4]; q5 = (float)q[5];
-  }
-  nd.b = make_float4(q0, q1, q1, q3);
-  nd.c = make_float4(q2, q4, (float)cm.w, q5);
   const bool internal = expandable(t, c, leaf, force);
   if (rec_of_cell) rec_of_cell[c] = j;
   if (wparent) {  // record parent links (LET selection walks them top-down)
@@ -183,8 +192,69 @@ __global__ void k_compact(TreeView t, const double *__restrict__ dR, double thet
     if (internal)
       for (int k = 0; k < (int)nck[c]; ++k) wparent[1 + (int)base[c] + k] = j;
   }
-  nd.d = make_int4(internal ? 1 + (int)base[c] : L.z, L.y, internal ? (int)nck[c] : 0, L.w);
-  out[j] = nd;
+  out[j] = walk_record(t, c, dR, theta, internal, nck, base);
+}
+
+// Walk-only trees: the same records written from the parents' side.  The
+// moments kernel listed every cell the walk opens (by level, in `mlist`);
+// 8 lanes take one such cell, one child slot each, rank the present children
+// by ballot and write their records -- no per-cell parent lookups, and the
+// cells inside buckets are never touched.
+__global__ void k_compact_parents(TreeView t, const double *__restrict__ dR, double theta, int leaf,
+                                  const uint32_t *__restrict__ nck, const uint32_t *__restrict__ base,
+                                  WalkNode *__restrict__ out, int *__restrict__ dCp) {
+  const int64_t C = tree_count(t);
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tree_overflowed(t)) {
+    if (gt == 0) {
+      WalkNode nd;
+      nd.a = make_float4(0.f, 0.f, 0.f, 0.f);
+      nd.b = nd.a;
+      nd.c = nd.a;
+      nd.d = make_int4(0, 0, 0, 0);
+      out[0] = nd;
+      *dCp = 1;
+    }
+    return;
+  }
+  if (gt == 0) {  // the root's record and the record count
+    *dCp = (int)(1 + base[C - 1] + nck[C - 1]);
+    out[0] = walk_record(t, 0, dR, theta, expandable(t, 0, leaf, nullptr), nck, base);
+  }
+  const int *cnt = t.mlvl + 2 * (kMaxLevel + 1);  // cursors = cells listed per level
+  const int *offs = t.mlvl + (kMaxLevel + 1);
+  int total = 0;
+#pragma unroll 1
+  for (int l = 0; l <= kMaxLevel; ++l) total += cnt[l];
+  const int s = threadIdx.x & 7, sub = (threadIdx.x & 31) >> 3;
+  const int64_t warp = gt >> 5, nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t wb = warp * 4; wb < total; wb += nwarps * 4) {  // warp-uniform: 4 cells per pass
+    const int64_t g = wb + sub;
+    int P = -1;
+    if (g < total) {
+      int r = (int)g;
+      for (int l = 0; l <= kMaxLevel; ++l) {
+        if (r < cnt[l]) {
+          P = t.mlist[offs[l] + r];
+          break;
+        }
+        r -= cnt[l];
+      }
+    }
+    int c = -1;
+    if (P >= 0) {
+      c = t.child8[8 * (int64_t)P + s];
+      if (c < -1) c = -c - 2;  // a leaf child, stored as -(c + 2)
+    }
+    const unsigned grp = 0xffu << (threadIdx.x & 24);
+    const unsigned have = __ballot_sync(0xffffffffu, c >= 0) & grp;
+    if (c >= 0) {
+      const int rank = __popc(have & ((1u << (threadIdx.x & 31)) - 1u));
+      const int j = 1 + (int)base[P] + rank;
+      const uint8_t cl = t.mclass[c];
+      out[j] = walk_record(t, c, dR, theta, cl >= 2 && cl != kClassLeafRecord, nck, base);
+    }
+  }
 }
 
 void launch_walk_tree(const TreeView &t, const double *dR, double theta, int leaf,
@@ -195,6 +265,16 @@ void launch_walk_tree(const TreeView &t, const double *dR, double theta, int lea
   if (!force) {  // children counted and ranked from the child8 rows: no slot-mask pass
     k_nchild_rows<<<g, 256, 0, s>>>(t, leaf, nck);
     exclusive_scan_u32(scan_tmp, scan_bytes, nck, base, t.C, s);
+    if (t.mclass && t.mleaf == leaf && t.mlvl && !rec_of_cell && !wparent) {  // walk-only tree
+      static int sms = 0;
+      if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      }
+      k_compact_parents<<<sms * 8, 256, 0, s>>>(t, dR, theta, leaf, nck, base, out, dCp);
+      return;
+    }
     k_compact<<<g, 256, 0, s>>>(t, dR, theta, leaf, force, nullptr, nck, base, out, dCp, rec_of_cell, wparent);
     return;
   }

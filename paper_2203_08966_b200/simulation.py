@@ -157,17 +157,21 @@ class TreeForces:
         eng = self.engine
         n = len(local)
         pos = eng.bodies_tensor(local.position, local.mass)
-        vel = eng.vec_tensor(local.velocity)
+        # the force pass reads positions and masses only: the velocity slot gets a
+        # zero buffer kept across calls instead of an upload of local.velocity
+        if getattr(self, "_vel", None) is None or self._vel.shape[0] != n or self._vel.dtype != eng.dtype:
+            self._vel = torch.zeros((n, 4 if eng.fp32 else 3), dtype=eng.dtype, device=eng.device)
         m = None if eng.fp32 else torch.as_tensor(local.mass).to(eng.device)
-        eng.sim_load(pos, vel, m)
+        eng.sim_load(pos, self._vel, m)
         eng.sim_forces(self.theta, self.eps, self.leaf_size, record_work)
-        acc = torch.empty_like(vel)
+        acc = torch.empty((n, 4 if eng.fp32 else 3), dtype=eng.dtype, device=eng.device)
         work = torch.empty(n, dtype=torch.int64, device=eng.device) if record_work else None
         eng.sim_store(acc=acc, work=work)
         eng.check()
-        local.acceleration[:] = acc[:, :3].to(torch.float64).cpu().numpy()
+        # straight into the caller's arrays (no intermediate host copies)
+        torch.from_numpy(local.acceleration).copy_(acc[:, :3].to(torch.float64))
         if record_work:
-            local.work[:] = work.cpu().numpy()
+            torch.from_numpy(local.work).copy_(work)
         return 0
 
     def __call__(self, bodies: Bodies) -> None:
