@@ -41,6 +41,9 @@ constexpr int kPasses = 8;  // 64 bits; the top pass sees bits 56..62 (bit 63 is
 #ifndef BH_SORT_ITEMS
 #define BH_SORT_ITEMS 16
 #endif
+#ifndef BH_SORT_VIDX
+#define BH_SORT_VIDX 0  // 1: the tile keeps each key's position (u16), values are read at the scatter
+#endif
 #ifndef BH_SORT_BLOCKS
 #define BH_SORT_BLOCKS 3  // pass-kernel blocks per SM the register budget is set for
 #endif
@@ -197,7 +200,11 @@ __global__ void k_sort_zero(unsigned *hist, unsigned *counters) {
 // ------------------------------------------------------------ one digit pass
 struct PassSmem {
   uint64_t keys[kTile];
+#if BH_SORT_VIDX
+  uint16_t vidx[kTile];  // tile position of the key in each sorted slot (values read at the scatter)
+#else
   uint32_t vals[kTile];
+#endif
   unsigned whist[kSortWarps][kBins];  // per warp: running counts, then exclusive offsets
   unsigned start[kBins];              // exclusive digit offsets inside the tile
   long long gdelta[kBins];            // global position - tile position, per digit
@@ -253,16 +260,22 @@ __global__ void __launch_bounds__(kSortThreads, MINB) k_sort_pass(
 
   // ---- load (warp-striped: item j of lane l is key wbase + 32 j + l)
   uint64_t k[kSortItems];
+#if !BH_SORT_VIDX
   uint32_t v[kSortItems];
+#endif
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
     const int64_t i = wbase + 32 * j + lane;
     if (i < n) {
       k[j] = __ldcs(kin + i);
+#if !BH_SORT_VIDX
       v[j] = vin ? __ldcs(vin + i) : (uint32_t)i;  // no input values: the identity permutation
+#endif
     } else {
       k[j] = ~0ull;  // pads sort after every real key of the last tile and are never stored
+#if !BH_SORT_VIDX
       v[j] = 0u;
+#endif
     }
   }
 
@@ -320,7 +333,11 @@ __global__ void __launch_bounds__(kSortThreads, MINB) k_sort_pass(
     const unsigned dj = (unsigned)(k[j] >> shift) & (kBins - 1);
     const unsigned lp = S.start[dj] + S.whist[w][dj] + rank[j];
     S.keys[lp] = k[j];
+#if BH_SORT_VIDX
+    S.vidx[lp] = (uint16_t)(w * 32 * kSortItems + 32 * j + lane);
+#else
     S.vals[lp] = v[j];
+#endif
   }
 
   // ---- decoupled look-back for digit d: four predecessors per round trip
@@ -358,7 +375,12 @@ __global__ void __launch_bounds__(kSortThreads, MINB) k_sort_pass(
     const long long g = S.gdelta[di] + i;
     if (g < n) {
       kout[g] = key;
+#if BH_SORT_VIDX
+      const int64_t src = tbase + S.vidx[i];
+      vout[g] = vin ? vin[src] : (uint32_t)src;
+#else
       vout[g] = S.vals[i];
+#endif
     }
   }
 }
