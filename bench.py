@@ -52,9 +52,11 @@ SORT_BYTES_PER_BODY = 192  # 8 passes x (8 B key + 4 B index) x (read + write)
 L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
 
 
-def build_bytes_per_body(cells_per_body: float) -> float:
-    """243 + 32*(C/N - 1.48) algorithmic bytes per body."""
-    return 243.0 + 32.0 * (cells_per_body - 1.48)
+def build_bytes_per_body(cells_per_body: float, records_per_body: float = 0.0) -> float:
+    """243 + 32*(C/N - 1.48) algorithmic bytes per body (bounds,
+    keys, permutation, lcp / scan / emit, moments) + the 64-byte fp32 walk
+    records written."""
+    return 243.0 + 32.0 * (cells_per_body - 1.48) + 64.0 * records_per_body
 
 
 def measured_peaks() -> dict:
@@ -270,7 +272,7 @@ def run_ours(args, cfg) -> dict | None:
     ev1 = torch.cuda.Event(enable_timing=True)
     total_ms = 0.0
     pp = pc = 0
-    cells = 0
+    cells = records = 0
     with ClockSampler(local) as clocks:
         for _ in range(args.steps):
             flush.zero_()  # L2 flush between timed iterations (outside the events)
@@ -286,6 +288,7 @@ def run_ours(args, cfg) -> dict | None:
             pp += st.pp
             pc += st.pc
             cells = st.n_cells
+            records = st.n_records
     phases = eng.timing_get()
     launches = eng.launches()
     eng.timing(False)
@@ -311,9 +314,10 @@ def run_ours(args, cfg) -> dict | None:
         walk_s = phases["walk"] / 1e3
         walk_flops = (FLOPS_PP * pp + FLOPS_PC * pc) / args.steps
         walk_tf = walk_flops / (walk_s / args.steps) / 1e12 if walk_s > 0 else None
-        build_s = phases["build"] / 1e3 / args.steps
+        # keys + permutation + build (lcp, scans, emit, moments, walk records)
+        build_s = (phases["keys"] + phases["permute"] + phases["build"]) / 1e3 / args.steps
         sort_s = phases["sort"] / 1e3 / args.steps
-        bpb = build_bytes_per_body(cells / n)
+        bpb = build_bytes_per_body(cells / n, records / n)
         build_gbs = bpb * n / build_s / 1e9 if build_s > 0 else None
         sort_gbs = SORT_BYTES_PER_BODY * n / sort_s / 1e9 if sort_s > 0 else None
         hbm = float(peaks["hbm_gbs"])
@@ -358,7 +362,8 @@ def run_ours(args, cfg) -> dict | None:
                          "fp32_pipe_active_ncu": pipe},
             "roofline_build": {"bound": "hbm", "achieved": build_gbs, "peak": hbm, "unit": "GB/s",
                                "frac": build_gbs / hbm if build_gbs else None,
-                               "bytes_per_body": bpb, "peak_source": peaks.get("source")},
+                               "bytes_per_body": bpb, "peak_source": peaks.get("source"),
+                               "phases": "keys + permute + build (lcp, scans, emit, moments, walk records)"},
             "roofline_sort": {"bound": "hbm", "achieved": sort_gbs, "peak": hbm, "unit": "GB/s",
                               "frac": sort_gbs / hbm if sort_gbs else None,
                               "bytes_per_body": SORT_BYTES_PER_BODY,

@@ -53,6 +53,7 @@ typedef struct {
   int64_t pc;            /* body-cell interactions of the last traversal */
   int64_t work;          /* pp*WORK_PP + pc*WORK_PC (octree.py:23-25) */
   int64_t launches;      /* libbh kernels enqueued since the last bh_timing_reset */
+  int64_t n_records;     /* fp32 walk records of the current tree (0 if none built) */
 } bh_stats;
 
 /* Phases timed with CUDA events on the caller's stream when timing is on. */
@@ -61,7 +62,7 @@ enum {
   BH_PHASE_KEYS = 1,      /* R + Morton keys */
   BH_PHASE_SORT = 2,      /* radix sort of (key, index) */
   BH_PHASE_PERMUTE = 3,   /* body gather into Morton order */
-  BH_PHASE_BUILD = 4,     /* lcp, scan, cell count, emit, moments */
+  BH_PHASE_BUILD = 4,     /* lcp, scan, cell count, emit, moments, fp32 walk records */
   BH_PHASE_WALK = 5,      /* traversal */
   BH_PHASE_LET = 6,       /* locally-essential-tree marking and packing (distributed build) */
   BH_NPHASES = 7

@@ -60,6 +60,7 @@ class BHStats(ctypes.Structure):
         ("pc", ctypes.c_int64),
         ("work", ctypes.c_int64),
         ("launches", ctypes.c_int64),
+        ("n_records", ctypes.c_int64),
     ]
 
 

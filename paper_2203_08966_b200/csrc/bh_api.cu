@@ -357,6 +357,7 @@ int build_sorted_async(bh_handle *h, int64_t n, const float4 *bod32, cudaStream_
   TreeView t = h->view();
   if (leaf > 1) {  // a walk-only tree: the emit kernel classifies the cells for the moments
     BH_CUDA(h->mclass.ensure(cap + 16));
+    BH_CUDA(cudaMemsetAsync(h->mclass.p, 0, cap + 16, s));  // cells the emit skips: class 0
     t.mclass = h->mclass.as<uint8_t>();
     t.mleaf = leaf;
   }
@@ -418,8 +419,8 @@ void fill_walk_params(bh_handle *h, WalkParams &P, int64_t nt, double theta, dou
 // (Re)build the compact fp32 walk tree for (theta, leaf) -- bh_walk.cu
 int ensure_walk_tree(bh_handle *h, double theta, int leaf, cudaStream_t s) {
   if (leaf < 1) leaf = 1;
-  if (h->mom_leaf > leaf)
-    return fail(BH_BAD_ARG, "the resident tree's moments were formed for leaf size " +
+  if (h->mom_leaf > 0 && h->mom_leaf != leaf)  // a walk-only tree holds what one leaf size reads
+    return fail(BH_BAD_ARG, "the resident tree was built for walks with leaf size " +
                                 std::to_string(h->mom_leaf) + "; prepare again for leaf size " +
                                 std::to_string(leaf));
   if (h->walk_valid && h->walk_theta == theta && h->walk_leaf == leaf) return BH_OK;
@@ -537,8 +538,8 @@ int sim_prepare(bh_handle *h, double theta, double eps, int leaf, bool bounds_re
   else
     BH_TRY(build_sorted(h, n, nullptr, h->pos.as<double4>(), s, h->allow_dup || leaf > 1));
   h->tend(s);
-  if (f32) {
-    h->tbegin(BH_PHASE_WALK, s);
+  if (f32) {  // the walk records are part of the build (the walk phase is the traversal alone)
+    h->tbegin(BH_PHASE_BUILD, s);
     BH_TRY(ensure_walk_tree(h, theta, leaf, s));
     h->tend(s);
   }
@@ -599,6 +600,11 @@ int sim_walk(bh_handle *h, double theta, double eps, int leaf, int64_t begin, in
   if (h->npeers && (h->acc.p != h->peer_own_acc || h->work_sorted.p != h->peer_own_work))
     return fail(BH_BAD_ARG, "result buffers reallocated since the peers mapped them: set peers again");
   BH_TRY(reset_counters(h, s));
+  if (f32) {  // (normally already built by sim_prepare)
+    h->tbegin(BH_PHASE_BUILD, s);
+    BH_TRY(ensure_walk_tree(h, theta, leaf, s));
+    h->tend(s);
+  }
   h->tbegin(BH_PHASE_WALK, s);
   int *w32 = record_work ? h->work_sorted.as<int>() + begin : nullptr;
   W9Peers peers;  // the same rows of every peer's buffers (replicated ranks)
@@ -609,7 +615,6 @@ int sim_walk(bh_handle *h, double theta, double eps, int leaf, int64_t begin, in
     peers.work[r] = static_cast<int *>(h->peer_work[r]) + begin;
   }
   if (f32) {
-    BH_TRY(ensure_walk_tree(h, theta, leaf, s));
     launch_walk_f32(h->wnodes.as<WalkNode>(), walk_records_bound(h), h->pos.as<float4>(),
                     h->pos.as<float>() + 4 * begin, 4, nullptr, (int)nt, (float)(eps * eps), leaf,
                     h->acc.as<float>() + 4 * begin, 4, nullptr, w32, h->flags, s, h->npeers ? &peers : nullptr);
@@ -923,7 +928,6 @@ static int traverse_common(bh_handle *h, const void *targets, int64_t n, double 
   WalkParams P;
   fill_walk_params(h, P, n, theta, eps, leaf);
   if (f32) {
-    BH_TRY(ensure_walk_tree(h, theta, leaf, s));
     launch_walk_f32(h->wnodes.as<WalkNode>(), walk_records_bound(h), h->tbod.as<float4>(),
                     static_cast<const float *>(targets), 4, h->vals2.as<uint32_t>(), (int)n,
                     (float)(eps * eps), leaf, static_cast<float *>(acc), 4, work, nullptr,
@@ -1822,6 +1826,14 @@ int bh_stats_get(bh_handle *h, bh_stats *out, void *stream) {
   out->pc = (int64_t)h->hflags->pc;
   out->work = out->pp + 2 * out->pc;
   out->launches = h->launches;
+  out->n_records = 0;
+  if (h->walk_valid) {  // the walk tree's record count (device), one more 4-byte read
+    int nr = 0;
+    BH_CUDA(cudaMemcpyAsync(h->hstat + kMaxLevel + 2, h->dCp, sizeof(int), cudaMemcpyDeviceToHost, S(stream)));
+    BH_CUDA(cudaStreamSynchronize(S(stream)));
+    nr = h->hstat[kMaxLevel + 2];
+    out->n_records = nr;
+  }
   return BH_OK;
 }
 

@@ -283,6 +283,42 @@ __global__ void k_emit(TreeView t, const float4 *__restrict__ bod32,
     // body j + L still shares its prefix
     if (t.mclass) par_open = j + L < n && (t.keys[j + L] >> shift) == (k >> shift);
   }
+  if (t.mclass) {
+    // Walk-only tree (fp32 sim path, leaf size L > 1): only what the walk reads
+    // is written -- the cells the walk opens, its buckets and one-body records.
+    // A cell below a bucket is never read: the body stops at its first such
+    // cell (its class byte stays 0 from the memset), so the deep part of the
+    // tree costs no stores and no run-end searches.  parent[] is not needed.
+    for (int l = start + 1; l <= depth; ++l) {
+      if (!par_open) break;  // inside a bucket
+      const int c = base + (l - start - 1);
+      const bool leafc = l == depth && ln != kMaxLevel;
+      t.child8[8 * (int64_t)par + (int)((k >> (3 * (kMortonBits - l))) & 7)] = leafc ? -(c + 2) : c;
+      if (l == depth && ln == kMaxLevel) {  // first body of a duplicate-key run: a bucket
+        const int64_t end = run_end(t.keys, n, i, k, 0);
+        const int skip = end < n ? 1 + (int)t.off[end] : C;
+        t.link[c] = make_int4(skip, (int)(end - i), (int)i, l);
+        t.mclass[c] = 1;
+        break;
+      }
+      if (leafc) {  // a one-body record: its body is its moments
+        t.link[c] = make_int4(c + 1, 1, (int)i, l);
+        t.mclass[c] = kClassLeafRecord;
+        const float4 v = bod32[i];
+        t.cm64[c] = make_double4(v.x, v.y, v.z, v.w);
+        break;
+      }
+      const int shift = 3 * (kMortonBits - l);
+      const int64_t end = run_end(t.keys, n, i, k >> shift, shift);
+      const int skip = end < n ? 1 + (int)t.off[end] : C;
+      t.link[c] = make_int4(skip, (int)(end - i), (int)i, l);
+      const bool opens = end - i > L;  // l < 21 here
+      t.mclass[c] = opens ? (uint8_t)(2 + l) : 1;
+      par_open = opens;
+      par = c;
+    }
+    return;
+  }
   for (int l = start + 1; l <= depth; ++l) {
     const int c = base + (l - start - 1);
     t.parent[c] = par;
@@ -293,10 +329,8 @@ __global__ void k_emit(TreeView t, const float4 *__restrict__ bod32,
       const int64_t end = run_end(t.keys, n, i, k, 0);
       const int skip = end < n ? 1 + (int)t.off[end] : C;
       t.link[c] = make_int4(skip, (int)(end - i), (int)i, l);
-      if (t.mclass) t.mclass[c] = par_open ? 1 : 0;  // never opened (level 21): a bucket
     } else if (l == depth) {
       t.link[c] = make_int4(c + 1, 1, (int)i, l);
-      if (t.mclass) t.mclass[c] = par_open ? kClassLeafRecord : 0;  // a walk record iff its parent opens
       double4 b;
       if (bod64) {
         b = bod64[i];
@@ -310,11 +344,6 @@ __global__ void k_emit(TreeView t, const float4 *__restrict__ bod32,
       const int64_t end = run_end(t.keys, n, i, k >> shift, shift);
       const int skip = end < n ? 1 + (int)t.off[end] : C;
       t.link[c] = make_int4(skip, (int)(end - i), (int)i, l);
-      if (t.mclass) {
-        const bool opens = end - i > L;  // l < 21 here
-        t.mclass[c] = opens ? (uint8_t)(2 + l) : (par_open ? 1 : 0);
-        par_open = opens;
-      }
     }
     par = c;
   }

@@ -34,6 +34,7 @@ class TraversalStats:
     n_cells: int
     pp: int
     pc: int
+    n_records: int = 0  # fp32 walk records of the current tree
 
     @property
     def interactions(self) -> int:
@@ -95,7 +96,7 @@ class Engine:
     def stats(self) -> TraversalStats:
         s = _lib.BHStats()
         check(self._L.bh_stats_get(self._h, ctypes.byref(s), self.stream))
-        return TraversalStats(int(s.n_bodies), int(s.n_cells), int(s.pp), int(s.pc))
+        return TraversalStats(int(s.n_bodies), int(s.n_cells), int(s.pp), int(s.pc), int(s.n_records))
 
     # ------------------------------------------------------ layout helpers
     def bodies_tensor(self, positions, masses=None) -> torch.Tensor:
