@@ -928,6 +928,7 @@ static int traverse_common(bh_handle *h, const void *targets, int64_t n, double 
   WalkParams P;
   fill_walk_params(h, P, n, theta, eps, leaf);
   if (f32) {
+    BH_TRY(ensure_walk_tree(h, theta, leaf, s));
     launch_walk_f32(h->wnodes.as<WalkNode>(), walk_records_bound(h), h->tbod.as<float4>(),
                     static_cast<const float *>(targets), 4, h->vals2.as<uint32_t>(), (int)n,
                     (float)(eps * eps), leaf, static_cast<float *>(acc), 4, work, nullptr,

@@ -762,6 +762,26 @@ constexpr int kW9NcShift = 28;  // frontier entry: first_child | nchild << 28, u
 #ifndef BH_W9_BULK
 #define BH_W9_BULK 0  // 1: accepted records reach shared memory by cp.async.bulk (mbarrier-completed)
 #endif
+#ifdef BH_W9_STATS
+// diagnostics (-DBH_W9_STATS): per-warp schedule counters summed over the launch
+//  0 batches  1 cells classified  2 mixed  3 mixed with an accepting target
+//  4 pc entries flushed  5 their mask bits  6 pp leaf entries  7 their mask bits
+//  8 pp bucket entries  9 pp passes  10 pass body iterations  11 bucket (target, body) slots used
+//  12 frontier pushes (certain-open)  13 pc flushes  14 pp flushes  15 mixed opened (pushed / bucket)
+//  16 mixed accepting target bits  17 bucket entries' mask bits
+__device__ unsigned long long g_w9_stats[24];
+extern "C" int bh_debug_w9_stats(unsigned long long *out, int reset) {
+  int e = (int)cudaMemcpyFromSymbol(out, g_w9_stats, sizeof(g_w9_stats));
+  if (reset) {
+    static const unsigned long long z[24] = {};
+    cudaMemcpyToSymbol(g_w9_stats, z, sizeof(z));
+  }
+  return e;
+}
+#define W9S(i, v) (st[i] += (v))
+#else
+#define W9S(i, v) ((void)0)
+#endif
 
 // cp.async.bulk (the bulk-copy / TMA engine) of one 48-byte record prefix into
 // shared memory, completing on a per-warp mbarrier.  The barrier expects one
@@ -873,6 +893,9 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
   const unsigned lt = bit - 1u;
 
   int sp = 1, npc = 0, npp = 0;
+#ifdef BH_W9_STATS
+  unsigned long long st[18] = {};
+#endif
   if (MODE == kWalkResume) {  // the deferred record's subtree, for the targets that opened it
     const int2 fc = dfr.fcnc[entry.y];
     if (fc.y <= 0) sp = 0;
@@ -896,6 +919,11 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
 
   // dense pc over the list (the FP32-pipe work)
   auto flush_pc = [&](int n) {
+    W9S(13, n > 0); W9S(4, n);
+#ifdef BH_W9_STATS
+    for (int k = 0; k < n; ++k)
+      W9S(5, __popc((unsigned)__float_as_int(S.pcr[k][0].w)) + __popc((unsigned)__float_as_int(S.pcr[k][1].z)));
+#endif
 #if BH_W9_BULK
     mbar_arrive_wait(&S.bar, bphase, lane == 0);  // the staged records have landed
 #endif
@@ -966,6 +994,7 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
     // bucket holding its targets (a pass's body loads have one address per
     // bucket).  The interaction sets are unchanged; only the fp32 summation
     // order per target moves.  Lane p keeps pass p's used lanes and length.
+    W9S(14, n > 0);
     int k0 = 0;
     while (k0 < n) {
       unsigned used = 0u;
@@ -974,11 +1003,14 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
         const int4 en = S.pp[k];
         const bool u0 = (unsigned)en.z & bit, u1 = (unsigned)en.w & bit;
         if (en.y == 0) {  // leaf record: its com and mass are the body (a LET leaf has no body index here)
+          W9S(6, 1); W9S(7, __popc((unsigned)en.z) + __popc((unsigned)en.w));
           const WalkNode *nd = T + en.x;
           const float4 a = nd->a;
           pp_body(make_float4(-a.x, -a.y, -a.z, nd->c.z), u0, u1);
           continue;
         }
+        W9S(8, 1); W9S(17, __popc((unsigned)en.z) + __popc((unsigned)en.w));
+        W9S(11, (unsigned long long)en.y * (__popc((unsigned)en.z) + __popc((unsigned)en.w)));
         const unsigned lm = (unsigned)en.z | (unsigned)en.w;
         const unsigned fit = __ballot_sync(FULL, (int)lane < npass && (used & lm) == 0u);
         int p;
@@ -996,8 +1028,10 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
         if ((lm >> lane) & 1u) S.psel[p][lane] = (uint8_t)(k + 1);
       }
       __syncwarp();
+      W9S(9, npass);
       for (int p = 0; p < npass; ++p) {
         const int len = __shfl_sync(FULL, plen, p);
+        W9S(10, len);
         const int e = (int)S.psel[p][lane] - 1;
         int lo = 0, cnt = 0;
         bool u0 = false, u1 = false;
@@ -1139,6 +1173,7 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
     npc += __popc(bpc);
     sp += __popc(bfr);
     const int nmx = __popc(bmx);
+    W9S(0, 1); W9S(1, ncell); W9S(2, nmx); W9S(12, __popc(bfr));
     __syncwarp();
 
     // ---- mixed cells: the per-target MAC (warp-uniform, as k_walk)
@@ -1154,6 +1189,7 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
       const float2 D2 = __ffma2_rn(DZ, DZ, __ffma2_rn(DY, DY, __fmul2_rn(DX, DX)));
       const bool c0 = in0 && D2.x > a.w, c1 = in1 && D2.y > a.w;  // MAC (flattree.py:295)
       if (__any_sync(FULL, c0 || c1)) {
+        W9S(3, 1); W9S(16, __popc(__ballot_sync(FULL, c0)) + __popc(__ballot_sync(FULL, c1)));
         const float2 R = f2(c0 ? rsqrtf(D2.x) : 0.f, c1 ? rsqrtf(D2.y) : 0.f);
         const float2 R2 = __fmul2_rn(R, R);
         const float2 R3 = __fmul2_rn(R2, R);
@@ -1170,6 +1206,7 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
       }
       const unsigned o0 = __ballot_sync(FULL, in0 && !c0), o1 = __ballot_sync(FULL, in1 && !c1);
       if ((o0 | o1) == 0u) continue;
+      W9S(15, 1);
       if (dd.z > 0) {
         if (lane == 0) {
           S.fc[sp] = fc_word(dd.x, dd.z);
@@ -1245,6 +1282,9 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
   if (lane == 0) {
     atomicAdd(&f->pp, (unsigned long long)spp);
     atomicAdd(&f->pc, (unsigned long long)spc);
+#ifdef BH_W9_STATS
+    for (int i = 0; i < 18; ++i) atomicAdd(&g_w9_stats[i], st[i]);
+#endif
   }
 }
 
