@@ -727,6 +727,25 @@ constexpr int kW9Full = BH_W9_FULLMAX;  // full 32-cell batches while sp <= this
 // after a full batch sp <= kW9Full + 32; single-entry (DFS) batches above it add
 // at most 8 entries per level
 constexpr int kW9Frontier = kW9Full + 32 + 8 * (kMaxLevel + 1) + 8;
+// Only the top kW9Fcap entries live in shared memory.  Measured peaks are < 100
+// entries (cfg2-cfg4: 0 warps above 99), so the proven bound kW9Frontier is
+// served by a per-warp spill area in global memory: when a batch could push the
+// shared part past kW9Fcap, its bottom kW9Spill entries move out (LIFO order is
+// kept), and they move back when the shared part empties.  A warp takes a spill
+// slot from a device-wide bitmap on its first spill (<= 64 resident warps per SM,
+// so a slot is always free) and returns it at exit.
+#ifndef BH_W9_FCAP
+#define BH_W9_FCAP 128
+#endif
+constexpr int kW9Fcap = BH_W9_FCAP;
+constexpr int kW9Spill = 64;
+static_assert(kW9Fcap >= kW9Spill + 32 && kW9Fcap - kW9Spill <= kW9Spill, "spill layout");
+struct W9Spill {
+  unsigned *bits = nullptr;  // one bit per slot
+  int *fc = nullptr;         // [slot][kW9Frontier]
+  uint2 *fm = nullptr;
+  int nwords = 0;
+};
 #ifndef BH_W9_CHECK
 #define BH_W9_CHECK 0  // 1: latch FLAG_WALK_BOUNDS instead of overrunning (costs 1.7%; the bounds are proven)
 #endif
@@ -769,11 +788,11 @@ constexpr int kW9NcShift = 28;  // frontier entry: first_child | nchild << 28, u
 //  8 pp bucket entries  9 pp passes  10 pass body iterations  11 bucket (target, body) slots used
 //  12 frontier pushes (certain-open)  13 pc flushes  14 pp flushes  15 mixed opened (pushed / bucket)
 //  16 mixed accepting target bits  17 bucket entries' mask bits
-__device__ unsigned long long g_w9_stats[24];
+__device__ unsigned long long g_w9_stats[64];  // [32, 64): histogram of the warp's peak frontier depth / 10
 extern "C" int bh_debug_w9_stats(unsigned long long *out, int reset) {
   int e = (int)cudaMemcpyFromSymbol(out, g_w9_stats, sizeof(g_w9_stats));
   if (reset) {
-    static const unsigned long long z[24] = {};
+    static const unsigned long long z[64] = {};
     cudaMemcpyToSymbol(g_w9_stats, z, sizeof(z));
   }
   return e;
@@ -820,8 +839,8 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 // and d.w (level) of a staged mixed record.  (BH_W9_BULK: the pc records are
 // bulk copies of the global records, so their masks sit in pcm.)
 struct W9Warp {
-  int fc[kW9Frontier];     // frontier: first_child | nchild << kW9NcShift
-  uint2 fm[kW9Frontier];   //           (mask0, mask1)
+  int fc[kW9Fcap];         // frontier (top): first_child | nchild << kW9NcShift
+  uint2 fm[kW9Fcap];       //                 (mask0, mask1)
 #if BH_W9_BULK
   uint64_t bar;            // completes the bulk copies of one flush
   uint2 pcm[kW9List];      // masks of the staged pc records
@@ -859,7 +878,7 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
     const WalkNode *__restrict__ T, const float4 *__restrict__ bodies,
     const float *__restrict__ targets, int tstride, const uint32_t *__restrict__ tperm, int nt,
     float e2, float *__restrict__ acc, int astride, int64_t *__restrict__ work64,
-    int *__restrict__ work32, DeviceFlags *f, int fullmax, DeferArgs dfr, W9Peers peers) {
+    int *__restrict__ work32, DeviceFlags *f, int fullmax, DeferArgs dfr, W9Peers peers, W9Spill spl) {
   extern __shared__ int4 w9_smem[];
   W9Warp &S = reinterpret_cast<W9Warp *>(w9_smem)[threadIdx.x >> 5];
   const unsigned lane = threadIdx.x & 31;
@@ -893,8 +912,10 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
   const unsigned lt = bit - 1u;
 
   int sp = 1, npc = 0, npp = 0;
+  int gsp = 0, slot = -1;  // spilled entries, spill slot (warp-uniform)
 #ifdef BH_W9_STATS
   unsigned long long st[18] = {};
+  int spmax = 0;
 #endif
   if (MODE == kWalkResume) {  // the deferred record's subtree, for the targets that opened it
     const int2 fc = dfr.fcnc[entry.y];
@@ -1068,9 +1089,48 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
 #endif
   };
 
-  while (sp > 0) {
+  while (sp > 0 || gsp > 0) {
+    if (sp > kW9Fcap - 32) {  // a batch pushes <= 32 entries: move the bottom kW9Spill out
+      if (slot < 0) {
+        if (lane == 0) {
+          int w = (int)(gwarp % spl.nwords);
+          for (;;) {
+            const unsigned v = *((volatile unsigned *)spl.bits + w);
+            if (v != FULL) {
+              const unsigned b = 1u << (__ffs(~v) - 1);
+              if (!(atomicOr(spl.bits + w, b) & b)) {
+                slot = w * 32 + __ffs(b) - 1;
+                break;
+              }
+            } else if (++w == spl.nwords) w = 0;
+          }
+        }
+        slot = __shfl_sync(FULL, slot, 0);
+      }
+      int *gfc = spl.fc + (int64_t)slot * kW9Frontier + gsp;
+      uint2 *gfm = spl.fm + (int64_t)slot * kW9Frontier + gsp;
+      for (int i = lane; i < kW9Spill; i += 32) { gfc[i] = S.fc[i]; gfm[i] = S.fm[i]; }
+      int rfc = 0, rfc2 = 0;
+      uint2 rfm = make_uint2(0, 0), rfm2 = make_uint2(0, 0);
+      const int rest = sp - kW9Spill;  // <= kW9Spill
+      if ((int)lane < rest) { rfc = S.fc[kW9Spill + lane]; rfm = S.fm[kW9Spill + lane]; }
+      if ((int)lane + 32 < rest) { rfc2 = S.fc[kW9Spill + 32 + lane]; rfm2 = S.fm[kW9Spill + 32 + lane]; }
+      __syncwarp();
+      if ((int)lane < rest) { S.fc[lane] = rfc; S.fm[lane] = rfm; }
+      if ((int)lane + 32 < rest) { S.fc[32 + lane] = rfc2; S.fm[32 + lane] = rfm2; }
+      __syncwarp();
+      gsp += kW9Spill;
+      sp = rest;
+    } else if (sp == 0) {  // shared part empty: the top kW9Spill spilled entries come back
+      gsp -= kW9Spill;
+      const int *gfc = spl.fc + (int64_t)slot * kW9Frontier + gsp;
+      const uint2 *gfm = spl.fm + (int64_t)slot * kW9Frontier + gsp;
+      for (int i = lane; i < kW9Spill; i += 32) { S.fc[i] = gfc[i]; S.fm[i] = gfm[i]; }
+      __syncwarp();
+      sp = kW9Spill;
+    }
     // ---- gather up to 32 cells from the top entries (one entry above kW9Full)
-    const int ne = sp <= fullmax ? min(sp, 32) : 1;
+    const int ne = sp + gsp <= fullmax ? min(sp, 32) : 1;
     int4 E = make_int4(0, 0, 0, 0);
     if ((int)lane < ne) {
       const int fcnc = S.fc[sp - 1 - lane];
@@ -1133,7 +1193,8 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
     // the bounds (frontier: §3 of DESIGN.md; lists: < kW9Flush + 32) hold by
     // construction; checked anyway (warp-uniform) so a violation is loud, not a
     // shared-memory overrun
-    if (BH_W9_CHECK && (sp + __popc(bfr) + __popc(bmx) > kW9Frontier || npc + __popc(bpc) > kW9List ||
+    if (BH_W9_CHECK && (sp + __popc(bfr) + __popc(bmx) > kW9Fcap ||
+        gsp + sp + __popc(bfr) + __popc(bmx) > kW9Frontier || npc + __popc(bpc) > kW9List ||
         npp + __popc(bpp) + __popc(bmx) > kW9PpList)) {
       if (lane == 0) atomicOr(&f->bits, FLAG_WALK_BOUNDS);
       return;
@@ -1174,6 +1235,9 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
     sp += __popc(bfr);
     const int nmx = __popc(bmx);
     W9S(0, 1); W9S(1, ncell); W9S(2, nmx); W9S(12, __popc(bfr));
+#ifdef BH_W9_STATS
+    spmax = max(spmax, gsp + sp + nmx);
+#endif
     __syncwarp();
 
     // ---- mixed cells: the per-target MAC (warp-uniform, as k_walk)
@@ -1277,6 +1341,7 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
       }
     }
   }
+  if (slot >= 0 && lane == 0) atomicAnd(spl.bits + (slot >> 5), ~(1u << (slot & 31)));
   const unsigned spp = __reduce_add_sync(FULL, (unsigned)(pp0 + pp1));
   const unsigned spc = __reduce_add_sync(FULL, (unsigned)(pc0 + pc1));
   if (lane == 0) {
@@ -1284,6 +1349,7 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
     atomicAdd(&f->pc, (unsigned long long)spc);
 #ifdef BH_W9_STATS
     for (int i = 0; i < 18; ++i) atomicAdd(&g_w9_stats[i], st[i]);
+    atomicAdd(&g_w9_stats[32 + min(31, spmax / 10)], 1ull);
 #endif
   }
 }
@@ -1307,6 +1373,30 @@ static int walk9_fullmax() {
   return v;
 }
 
+__global__ void k_latch_flag(DeviceFlags *f, unsigned bit) { atomicOr(&f->bits, bit); }
+
+// the frontier spill area of the current device (allocated once per device, never freed)
+static W9Spill walk9_spill() {
+  static W9Spill per_dev[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  W9Spill &w = per_dev[dev & 63];
+  if (!w.bits) {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int nslot = sms * 64;  // >= resident warps (2048 threads per SM)
+    W9Spill t;
+    t.nwords = (nslot + 31) / 32;
+    if (cudaMalloc(&t.bits, sizeof(unsigned) * t.nwords) != cudaSuccess ||
+        cudaMemset(t.bits, 0, sizeof(unsigned) * t.nwords) != cudaSuccess ||
+        cudaMalloc(&t.fc, sizeof(int) * (size_t)t.nwords * 32 * kW9Frontier) != cudaSuccess ||
+        cudaMalloc(&t.fm, sizeof(uint2) * (size_t)t.nwords * 32 * kW9Frontier) != cudaSuccess)
+      return W9Spill{};
+    w = t;
+  }
+  return w;
+}
+
 template <bool BUCKET, int MODE>
 static void launch_walk9(const WalkNode *T, const float4 *bodies, const float *targets, int tstride,
                          const uint32_t *tperm, int nt, float e2, float *acc, int astride, int64_t *work64,
@@ -1320,8 +1410,14 @@ static void launch_walk9(const WalkNode *T, const float4 *bodies, const float *t
   }
   const int64_t warps = MODE == kWalkResume ? (int64_t)dfr.nin : ((int64_t)nt + 63) / 64;
   if (warps <= 0) return;
+  const W9Spill spl = walk9_spill();
+  if (!spl.bits) {  // no memory for the spill area: fail loudly at the next check
+    k_latch_flag<<<1, 1, 0, s>>>(f, FLAG_WALK_BOUNDS);
+    return;
+  }
   k_walk9<BUCKET, MODE><<<grid_for(warps * 32, kW9Block), kW9Block, smem, s>>>(
-      T, bodies, targets, tstride, tperm, nt, e2, acc, astride, work64, work32, f, walk9_fullmax(), dfr, peers);
+      T, bodies, targets, tstride, tperm, nt, e2, acc, astride, work64, work32, f, walk9_fullmax(), dfr, peers,
+      spl);
 }
 template <int MODE>
 static void launch_walk9_mode(const WalkNode *T, const float4 *bodies, const float *targets, int tstride,

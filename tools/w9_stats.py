@@ -15,7 +15,7 @@ b = bench.make_bodies(cfg)
 eng = Engine("fp32", 0)
 eng.sim_load(eng.bodies_tensor(b.position, b.mass), eng.vec_tensor(b.velocity))
 L = _lib.lib()
-h = (ctypes.c_ulonglong * 24)()
+h = (ctypes.c_ulonglong * 64)()
 eng.sim_forces(cfg["theta"], cfg["eps"], cfg["leaf"], True)
 torch.cuda.synchronize()
 L.bh_debug_w9_stats(h, 1)
@@ -36,4 +36,6 @@ out["mixed_acc_density"] = d["mixed_acc_bits"] / 64 / max(d["mixed_acc"], 1)
 out["leaf_density"] = d["leaf_bits"] / 64 / max(d["leaf_entries"], 1)
 out["bucket_density_packed"] = d["bucket_slots_used"] / 64 / max(d["pass_iters"], 1)
 out["pc_from_mixed_frac"] = d["mixed_acc_bits"] / max(d["mixed_acc_bits"] + d["pc_bits"], 1)
+hist = [int(h[32 + i]) for i in range(32)]
+out["peak_frontier_hist_by10"] = {f"{10*i}-{10*i+9}": v for i, v in enumerate(hist) if v}
 print(json.dumps(out, indent=1))
