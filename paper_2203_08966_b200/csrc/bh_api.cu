@@ -365,7 +365,7 @@ int build_sorted_async(bh_handle *h, int64_t n, const float4 *bod32, cudaStream_
   // a walk-only tree: moments of the cells a leaf-size-`leaf` walk reads
   BH_CUDA((cudaError_t)launch_moments_coop(t, h->lvl.as<int>(), h->lvl_list.as<int>(), h->sms, s, leaf));
   h->mom_leaf = leaf > 1 ? leaf : 0;
-  h->launches += 4;
+  h->launches += leaf > 1 ? 6 : 4;  // walk-only trees: + the list and bucket-moment kernels
   BH_LAUNCHED();
   return BH_OK;
 }

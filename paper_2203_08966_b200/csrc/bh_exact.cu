@@ -503,6 +503,31 @@ __device__ void cell_moments8(const TreeView &t, int p, double (*xs)[11]) {
 // are never read by the walk, so their moments are not formed at all.  Equal
 // to the recursive combine up to fp64 rounding (the records are rounded to
 // fp32).  Every lane of the warp must call it (p < 0: no cell).
+#ifdef BH_MOM_TIMERS
+// diagnostics (-DBH_MOM_TIMERS): %globaltimer at each phase boundary of the last
+// k_moments_coop launch ([0] start, [1] lists, [2] buckets, [3 + i] after level run i)
+__device__ unsigned long long g_mom_t[64];
+__device__ int g_mom_nt;
+extern "C" int bh_debug_mom_timers(unsigned long long *out, int *n) {
+  cudaMemcpyFromSymbol(n, g_mom_nt, sizeof(int));
+  return (int)cudaMemcpyFromSymbol(out, g_mom_t, sizeof(g_mom_t));
+}
+__device__ __forceinline__ void mom_mark(int i) {
+  if (blockIdx.x == 0 && threadIdx.x == 0 && i < 64) {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    g_mom_t[i] = v;
+    g_mom_nt = i + 1;
+  }
+}
+#define MOM_MARK(i) mom_mark(i)
+#else
+#define MOM_MARK(i) ((void)0)
+#endif
+
+#ifndef BH_BUCKET_ONEPASS
+#define BH_BUCKET_ONEPASS 1
+#endif
 __device__ void bucket_moments8(const TreeView &t, int p) {
   const int s = threadIdx.x & 7;
   int lo = 0, cnt = 0;
@@ -511,6 +536,90 @@ __device__ void bucket_moments8(const TreeView &t, int p) {
     lo = L.z;
     cnt = L.y;
   }
+#if BH_BUCKET_ONEPASS
+  // One read of the bodies: mass, first and second moments about the bucket's
+  // first body x0 (offsets are bucket-sized, so the shift to the centre of mass
+  // below cancels nothing large), then the central quadrupole
+  // Q_ab = 3 S_ab - delta_ab tr S with S = sum m r r^T - M c c^T, c = com - x0.
+  // every body load of the cell is issued before any arithmetic (one memory
+  // round trip, not one per strided step); cells of more than 32 bodies
+  // (duplicate-key cells) finish in a loop
+  double4 x0 = make_double4(0.0, 0.0, 0.0, 0.0);
+  double tm = 0.0, sx = 0.0, sy = 0.0, sz = 0.0;
+  double sxx = 0.0, syy = 0.0, szz = 0.0, sxy = 0.0, sxz = 0.0, syz = 0.0;
+  auto add = [&](const double4 b) {
+    const double dx = b.x - x0.x, dy = b.y - x0.y, dz = b.z - x0.z;
+    const double mx = b.w * dx, my = b.w * dy, mz = b.w * dz;
+    tm += b.w;
+    sx += mx; sy += my; sz += mz;
+    sxx += mx * dx; syy += my * dy; szz += mz * dz;
+    sxy += mx * dy; sxz += mx * dz; syz += my * dz;
+  };
+#ifdef BH_MOM_TIMERS
+  if (p >= 0 && s == 0) {
+    atomicAdd(&g_mom_t[60], (unsigned long long)cnt);
+    atomicMax(&g_mom_t[61], (unsigned long long)cnt);
+  }
+#endif
+#if defined(BH_BUCKET_DIAG) && BH_BUCKET_DIAG == 1  // timing only: skip the bucket entirely
+  return;
+#endif
+  if (t.bod64) {
+    if (cnt > 0) x0 = t.bod64[lo];
+    for (int j = s; j < cnt; j += 8) add(t.bod64[lo + j]);
+  } else {
+    float4 v[4];
+    const float4 v0 = cnt > 0 ? t.bod32[lo] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) v[q] = s + 8 * q < cnt ? t.bod32[lo + s + 8 * q] : make_float4(0.f, 0.f, 0.f, 0.f);
+    x0 = make_double4(v0.x, v0.y, v0.z, v0.w);
+    // absent slots have zero mass: they add exactly 0
+#pragma unroll
+    for (int q = 0; q < 4; ++q) add(make_double4(v[q].x, v[q].y, v[q].z, v[q].w));
+    for (int j = s + 32; j < cnt; j += 8) {
+      const float4 f = t.bod32[lo + j];
+      add(make_double4(f.x, f.y, f.z, f.w));
+    }
+  }
+#if defined(BH_BUCKET_DIAG) && BH_BUCKET_DIAG == 2  // timing only: no reduction
+  if (0)
+#endif
+#pragma unroll
+  for (int o = 1; o < 8; o <<= 1) {
+    tm += __shfl_xor_sync(0xffffffffu, tm, o);
+    sx += __shfl_xor_sync(0xffffffffu, sx, o);
+    sy += __shfl_xor_sync(0xffffffffu, sy, o);
+    sz += __shfl_xor_sync(0xffffffffu, sz, o);
+    sxx += __shfl_xor_sync(0xffffffffu, sxx, o);
+    syy += __shfl_xor_sync(0xffffffffu, syy, o);
+    szz += __shfl_xor_sync(0xffffffffu, szz, o);
+    sxy += __shfl_xor_sync(0xffffffffu, sxy, o);
+    sxz += __shfl_xor_sync(0xffffffffu, sxz, o);
+    syz += __shfl_xor_sync(0xffffffffu, syz, o);
+  }
+  if (p >= 0 && s == 0) {
+    double cx = 0.0, cy = 0.0, cz = 0.0;
+    double q0 = 0.0, q1 = 0.0, q2 = 0.0, q3 = 0.0, q4 = 0.0, q5 = 0.0;
+    if (tm != 0.0) {
+      cx = sx / tm; cy = sy / tm; cz = sz / tm;
+      const double Sxx = sxx - tm * cx * cx, Syy = syy - tm * cy * cy, Szz = szz - tm * cz * cz;
+      const double tr = Sxx + Syy + Szz;
+      q0 = 3.0 * Sxx - tr;
+      q1 = 3.0 * (sxy - tm * cx * cy);
+      q2 = 3.0 * (sxz - tm * cx * cz);
+      q3 = 3.0 * Syy - tr;
+      q4 = 3.0 * (syz - tm * cy * cz);
+      q5 = 3.0 * Szz - tr;
+      cx += x0.x; cy += x0.y; cz += x0.z;
+    }
+    t.cm64[p] = make_double4(cx, cy, cz, tm);
+    double2 *q2o = reinterpret_cast<double2 *>(t.q64 + kQStride * (int64_t)p);
+    q2o[0] = make_double2(q0, q1);
+    q2o[1] = make_double2(q2, q3);
+    q2o[2] = make_double2(q4, q5);
+    q2o[3] = make_double2(0.0, 0.0);
+  }
+#else
   double tm = 0.0, sx = 0.0, sy = 0.0, sz = 0.0;
   for (int j = s; j < cnt; j += 8) {
     const double4 b = body64(t, lo + j);
@@ -561,6 +670,7 @@ __device__ void bucket_moments8(const TreeView &t, int p) {
     q2o[2] = make_double2(q4, q5);
     q2o[3] = make_double2(0.0, 0.0);
   }
+#endif
 }
 
 // the fp32 walk opens a cell iff count > L (the root: count > 1) below level 21
@@ -584,35 +694,27 @@ void launch_set_count(const uint32_t *off, const uint32_t *newc, int64_t n, int6
   k_set_count<<<1, 1, 0, s>>>(off, newc, n, cap, dC, f, step);
 }
 
-// One cooperative launch (all blocks co-resident): offsets from the device
-// level counts, bucket the internal cells by level, then sweep the levels
-// deepest-first with a grid-wide barrier between levels (a cell's children are
-// one level deeper, hence final when its level runs).
-namespace cg = cooperative_groups;
-#ifndef BH_MOM_MINB
-#define BH_MOM_MINB 4
-#endif
-__global__ void __launch_bounds__(256, BH_MOM_MINB) k_moments_coop(TreeView t, int *__restrict__ lvl,
-                                                     int *__restrict__ list, int leaf) {
-  cg::grid_group grid = cg::this_grid();
+// Walk-only trees (fp32 sim path, L > 1): list the opened cells by level and
+// the buckets (from the end of `list`) from the emit kernel's class bytes, then
+// form the bucket moments -- two plain launches ahead of the level sweep.
+__global__ void __launch_bounds__(256) k_mom_lists(TreeView t, int *__restrict__ lvl, int *__restrict__ list) {
   const int64_t C = tree_count(t);
-  if (C > t.C) return;  // overflowed build (uniform across the grid): nothing valid
-  int *cnt = lvl, *offs = lvl + (kMaxLevel + 1), *cur = lvl + 2 * (kMaxLevel + 1);
-  int *nbuck = lvl + 3 * (kMaxLevel + 1);  // pruned mode: buckets listed from the end of `list`
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  if (C > t.C) return;
+  int *cnt = lvl, *offsg = lvl + (kMaxLevel + 1), *cur = lvl + 2 * (kMaxLevel + 1);
+  int *nbuck = lvl + 3 * (kMaxLevel + 1);
+  __shared__ int offs[kMaxLevel + 1];
+  __shared__ int h[kMaxLevel + 1], base[kMaxLevel + 1];
+  __shared__ int hb, bbase;
+  if (threadIdx.x == 0) {
     int acc = 0;
     for (int l = 0; l <= kMaxLevel; ++l) {
       offs[l] = acc;
-      cur[l] = 0;
+      if (blockIdx.x == 0) offsg[l] = acc;
       acc += cnt[l];
     }
-    *nbuck = 0;
   }
-  grid.sync();
-  __shared__ int h[kMaxLevel + 1], base[kMaxLevel + 1];
-  __shared__ int hb, bbase;
+  __syncthreads();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  if (leaf > 1 && t.mclass) {
     // walk-only tree: the emit kernel classified every cell (one byte each);
     // 4 cells per thread and pass
     for (int64_t c0 = (int64_t)blockIdx.x * blockDim.x * 4; c0 < C; c0 += stride * 4) {
@@ -646,6 +748,54 @@ __global__ void __launch_bounds__(256, BH_MOM_MINB) k_moments_coop(TreeView t, i
       }
       __syncthreads();
     }
+}
+
+__global__ void __launch_bounds__(256) k_bucket_moments(TreeView t, const int *__restrict__ lvl,
+                                                        const int *__restrict__ list) {
+  const int64_t C = tree_count(t);
+  if (C > t.C) return;
+  const int nb = lvl[3 * (kMaxLevel + 1)];
+  const int sub = (threadIdx.x & 31) >> 3;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t b0 = warp * 4; b0 < nb; b0 += nwarps * 4) {
+    const int64_t k = b0 + sub;
+    bucket_moments8(t, k < nb ? list[C - 1 - k] : -1);
+  }
+}
+
+// One cooperative launch (all blocks co-resident): offsets from the device
+// level counts, bucket the internal cells by level, then sweep the levels
+// deepest-first with a grid-wide barrier between levels (a cell's children are
+// one level deeper, hence final when its level runs).
+namespace cg = cooperative_groups;
+#ifndef BH_MOM_MINB
+#define BH_MOM_MINB 4
+#endif
+__global__ void __launch_bounds__(256, BH_MOM_MINB) k_moments_coop(TreeView t, int *__restrict__ lvl,
+                                                     int *__restrict__ list, int leaf) {
+  cg::grid_group grid = cg::this_grid();
+  const int64_t C = tree_count(t);
+  if (C > t.C) return;  // overflowed build (uniform across the grid): nothing valid
+  int *cnt = lvl, *offs = lvl + (kMaxLevel + 1), *cur = lvl + 2 * (kMaxLevel + 1);
+  int *nbuck = lvl + 3 * (kMaxLevel + 1);  // pruned mode: buckets listed from the end of `list`
+  MOM_MARK(0);
+  const bool prelisted = leaf > 1 && t.mclass;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && !prelisted) {
+    int acc = 0;
+    for (int l = 0; l <= kMaxLevel; ++l) {
+      offs[l] = acc;
+      cur[l] = 0;
+      acc += cnt[l];
+    }
+    *nbuck = 0;
+  }
+  grid.sync();
+  __shared__ int h[kMaxLevel + 1], base[kMaxLevel + 1];
+  __shared__ int hb, bbase;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  if (leaf > 1 && t.mclass) {
+    // walk-only tree: listed by k_mom_lists, bucket moments formed by k_bucket_moments
   } else {
   for (int64_t c0 = (int64_t)blockIdx.x * blockDim.x; c0 < C; c0 += stride) {
     if (threadIdx.x <= kMaxLevel) h[threadIdx.x] = 0;
@@ -675,17 +825,30 @@ __global__ void __launch_bounds__(256, BH_MOM_MINB) k_moments_coop(TreeView t, i
   }
   }
   grid.sync();
+  MOM_MARK(1);
   const int sub = (threadIdx.x & 31) >> 3;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = stride >> 5;
-  if (leaf > 1) {  // the buckets first (no level order among them), then only the opened cells
+  if (leaf > 1 && !prelisted) {  // the buckets first (no level order among them), then only the opened cells
     const int nb = *nbuck;
+#ifdef BH_MOM_TIMERS
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      g_mom_t[62] = (unsigned long long)nb;
+      int no = 0;
+      for (int l = 0; l <= kMaxLevel; ++l) no += cur[l];
+      g_mom_t[63] = (unsigned long long)no;
+    }
+#endif
     for (int64_t b0 = warp * 4; b0 < nb; b0 += nwarps * 4) {
       const int64_t k = b0 + sub;
       bucket_moments8(t, k < nb ? list[C - 1 - k] : -1);
     }
     grid.sync();
   }
+  MOM_MARK(2);
+#ifdef BH_MOM_TIMERS
+  int nmark = 3;
+#endif
   // Runs of consecutive small levels (few cells: the top of the tree and the
   // deepest levels) are swept by block 0 alone with block barriers; the rest
   // of the grid waits at one grid barrier after the run.
@@ -713,6 +876,7 @@ __global__ void __launch_bounds__(256, BH_MOM_MINB) k_moments_coop(TreeView t, i
       }
       l = l2;
       grid.sync();
+      MOM_MARK(nmark++);
       continue;
     }
     const int b_l = offs[l];
@@ -721,12 +885,20 @@ __global__ void __launch_bounds__(256, BH_MOM_MINB) k_moments_coop(TreeView t, i
       cell_moments8(t, k < n_l ? list[b_l + k] : -1, wx);
     }
     grid.sync();
+    MOM_MARK(nmark++);
     --l;
   }
 }
 
 int launch_moments_coop(const TreeView &t, int *lvl, int *list, int sms, cudaStream_t s, int leaf) {
   if (t.n <= 1) return 0;
+  if (leaf > 1 && t.mclass) {
+    cudaMemsetAsync(lvl + 2 * (kMaxLevel + 1), 0, sizeof(int) * (kMaxLevel + 2), s);  // cur, nbuck
+    const int64_t cells = t.C + 16;
+    const int gl = (int)std::min<int64_t>((cells + 1023) / 1024, (int64_t)sms * 8);
+    k_mom_lists<<<gl, 256, 0, s>>>(t, lvl, list);
+    k_bucket_moments<<<sms * 8, 256, 0, s>>>(t, lvl, list);
+  }
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_moments_coop, 256, 0);
   if (per_sm < 1) per_sm = 1;

@@ -44,6 +44,12 @@ constexpr int kPasses = 8;  // 64 bits; the top pass sees bits 56..62 (bit 63 is
 #ifndef BH_SORT_VIDX
 #define BH_SORT_VIDX 0  // 1: the tile keeps each key's position (u16), values are read at the scatter
 #endif
+#ifndef BH_SORT_MATCH_TOP
+#define BH_SORT_MATCH_TOP 1  // the top passes whose peer masks come from MATCH.ANY (few digit values per warp)
+#endif
+#ifndef BH_SORT_UNIFORM
+#define BH_SORT_UNIFORM 0  // 1: a warp whose 32 keys share the digit skips the ballots
+#endif
 #ifndef BH_SORT_BLOCKS
 #define BH_SORT_BLOCKS 3  // pass-kernel blocks per SM the register budget is set for
 #endif
@@ -290,6 +296,8 @@ __global__ void __launch_bounds__(kSortThreads, MINB) k_sort_pass(
     unsigned peers = FULL;  // lanes whose digit equals this lane's
     if (MATCH) {
       peers = __match_any_sync(FULL, d);
+    } else if (BH_SORT_UNIFORM && __all_sync(FULL, d == __shfl_sync(FULL, d, 0))) {
+      peers = FULL;
     } else {
 #pragma unroll
       for (int b = 0; b < kDigitBits; ++b) {
@@ -576,7 +584,7 @@ cudaError_t sort_pairs(void *temp, size_t temp_bytes, const uint64_t *kin, uint6
     uint32_t *vb = (p & 1) ? vout : t.v;
     // the top digit (octree levels 1-3) takes few values per tile: there MATCH.ANY
     // ranks faster than the 8 ballots (measured at cfg3: 65 vs 84 us)
-    auto kern = (p == kPasses - 1 && variant == 0) ? k_sort_pass<BH_SORT_BLOCKS, true> : pass;
+    auto kern = (p >= kPasses - BH_SORT_MATCH_TOP && variant == 0) ? k_sort_pass<BH_SORT_BLOCKS, true> : pass;
     kern<<<tiles, kSortThreads, sizeof(PassSmem), s>>>(ka, va, kb, vb, n, kDigitBits * p, t.bin_start + p * kBins,
                                                                t.counters + p, t.st, next_epoch(), tiles);
     ka = kb;

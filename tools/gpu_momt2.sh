@@ -1,0 +1,4 @@
+cd $GRAFT_REPO_ROOT
+timeout 900 python -m pytest tests/test_gpu_scale.py tests/test_gpu_parity.py -q -x -k "fp32 or scale or leaf or bucket or cfg" 2>&1 | tail -3
+BH_NVCC_EXTRA="-DBH_MOM_TIMERS" python -m paper_2203_08966_b200.build_lib > /dev/null 2>&1 || echo BUILD FAILED
+for c in cfg3 cfg4; do echo $c; timeout 600 python tools/mom_timers.py $c 2>&1 | head -4; done
