@@ -100,7 +100,7 @@ struct bh_handle {
   int let_nrank = 0;
   int64_t let_nrec = 0;
   double R = 1.0;
-  Buf link, parent, child8, lvl, lvl_list, cm64, q64, tbod, mclass;
+  Buf link, parent, child8, lvl, lvl_list, cm64, q64, tbod, mclass, hperm;
   int *hlvl = nullptr;  // pinned: internal cells per level of the last build
   int sms = 148;
   int allow_dup = 0;       // bh_set_allow_duplicates; the sim path uses leaf_size > 1
@@ -615,8 +615,15 @@ int sim_walk(bh_handle *h, double theta, double eps, int leaf, int64_t begin, in
     peers.work[r] = static_cast<int *>(h->peer_work[r]) + begin;
   }
   if (f32) {
+    const uint32_t *perm = nullptr;  // warps of Hilbert-ordered targets (bh_walk.cu)
+    if (walk_hilbert_enabled() && nt > 64) {
+      BH_CUDA(h->hperm.ensure(sizeof(uint32_t) * (nt + 1)));
+      launch_hilbert_chunks(h->pos.as<float4>() + begin, nt, h->dR, h->hperm.as<uint32_t>(), s);
+      perm = h->hperm.as<uint32_t>();
+      h->launches += 1;
+    }
     launch_walk_f32(h->wnodes.as<WalkNode>(), walk_records_bound(h), h->pos.as<float4>(),
-                    h->pos.as<float>() + 4 * begin, 4, nullptr, (int)nt, (float)(eps * eps), leaf,
+                    h->pos.as<float>() + 4 * begin, 4, perm, (int)nt, (float)(eps * eps), leaf,
                     h->acc.as<float>() + 4 * begin, 4, nullptr, w32, h->flags, s, h->npeers ? &peers : nullptr);
   } else {
     WalkParams P;
@@ -731,7 +738,7 @@ int bh_destroy(bh_handle *h) {
   cudaSetDevice(h->device);
   close_peers(h);
   Buf *bufs[] = {&h->keys, &h->keys2, &h->vals, &h->vals2, &h->sort_tmp, &h->scan_tmp,
-                 &h->lcp, &h->newc, &h->off, &h->link, &h->parent, &h->child8, &h->lvl, &h->lvl_list,
+                 &h->lcp, &h->newc, &h->off, &h->link, &h->parent, &h->child8, &h->lvl, &h->lvl_list, &h->hperm,
                  &h->cm64, &h->q64, &h->mclass, &h->smask, &h->nck, &h->wbase, &h->wnodes, &h->wscan_tmp, &h->tbod, &h->pos, &h->pos2,
                  &h->vel, &h->vel2, &h->acc, &h->id, &h->id2, &h->work_sorted, &h->work_orig,
                  &h->bk_pos, &h->bk_vel, &h->bk_acc, &h->bk_id, &h->bk_work,
