@@ -143,3 +143,30 @@ base_pc = sum(len(grp) for grp in pc_cert)
 for K in (16, 32, 64):
     t = sum(packed_cost([(m_, 1) for m_ in grp], K) for grp in pc_cert)
     print(f"pc disjoint packing K={K}: passes {t / base_pc:.3f} of broadcast")
+
+
+# ---- packing order variants for the pp flush: first-fit decreasing by bucket
+# length (passes then group buckets of similar length), and by lane count
+def packed_cost_sorted(grp, K, key):
+    tot = 0
+    for q in range(0, len(grp), K):
+        batch = sorted(grp[q:q + K], key=key)
+        passes = []
+        for mask, c in batch:
+            lm = mask.reshape(32, 2).any(1)
+            for pz in passes:
+                if not (pz[0] & lm).any():
+                    pz[0] |= lm
+                    pz[1] = max(pz[1], c)
+                    break
+            else:
+                passes.append([lm.copy(), c])
+        tot += sum(c for _, c in passes)
+    return tot
+
+
+for K in (32, 64):
+    for name, key in (("count desc", lambda e: -e[1]), ("lanes desc", lambda e: -e[0].reshape(32, 2).any(1).sum()),
+                      ("count desc, lanes desc", lambda e: (-e[1], -e[0].reshape(32, 2).any(1).sum()))):
+        t = sum(packed_cost_sorted(grp, K, key) for grp in pp)
+        print(f"pp packing K={K} sorted by {name}: body iterations {t / base_it:.3f} of broadcast")
