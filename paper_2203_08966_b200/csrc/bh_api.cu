@@ -346,7 +346,12 @@ int build_sorted_async(bh_handle *h, int64_t n, const float4 *bod32, cudaStream_
   BH_CUDA(h->child8.ensure(sizeof(int) * 8 * cap));
   BH_CUDA(h->cm64.ensure(sizeof(double4) * cap));
   BH_CUDA(h->q64.ensure(sizeof(double) * kQStride * cap));
-  BH_CUDA(cudaMemsetAsync(h->child8.p, 0xFF, sizeof(int) * 8 * cap, s));
+  // walk-only trees (leaf > 1): the two-pass emit sets the rows of the opened
+  // cells itself; the other rows are never read
+  // (not for a rank's local tree of the distributed build: k_mark_shared follows
+  // child rows down the boundary paths, through buckets)
+  const bool two_pass = leaf > 1 && leaf <= 64 && h->bnd_prev < 0 && h->bnd_next < 0;
+  if (!two_pass) BH_CUDA(cudaMemsetAsync(h->child8.p, 0xFF, sizeof(int) * 8 * cap, s));
   h->C = cap;
   h->tree_n = n;
   h->async_tree = true;
@@ -361,11 +366,16 @@ int build_sorted_async(bh_handle *h, int64_t n, const float4 *bod32, cudaStream_
     t.mclass = h->mclass.as<uint8_t>();
     t.mleaf = leaf;
   }
-  launch_emit(t, bod32, nullptr, s);
+  // (the creator list lives in lvl_list, which the moments kernels fill afterwards)
+  if (!(two_pass && launch_emit_walk(t, bod32, h->lvl_list.as<int>(), h->lvl.as<int>() + 4 * (kMaxLevel + 1),
+                                     h->sms, s))) {
+    if (two_pass) BH_CUDA(cudaMemsetAsync(h->child8.p, 0xFF, sizeof(int) * 8 * cap, s));
+    launch_emit(t, bod32, nullptr, s);
+  }
   // a walk-only tree: moments of the cells a leaf-size-`leaf` walk reads
   BH_CUDA((cudaError_t)launch_moments_coop(t, h->lvl.as<int>(), h->lvl_list.as<int>(), h->sms, s, leaf));
   h->mom_leaf = leaf > 1 ? leaf : 0;
-  h->launches += leaf > 1 ? 6 : 4;  // walk-only trees: + the list and bucket-moment kernels
+  h->launches += leaf > 1 ? 7 : 4;  // walk-only trees: two emit passes + the list and bucket-moment kernels
   BH_LAUNCHED();
   return BH_OK;
 }

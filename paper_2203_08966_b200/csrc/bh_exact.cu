@@ -355,6 +355,159 @@ void launch_emit(const TreeView &t, const float4 *bod32, const double4 *bod64,
   k_emit<<<grid_for(t.n, 128), 128, 0, s>>>(t, bod32, bod64);
 }
 
+// ---- walk-only emit in two passes (fp32 sim path, leaf size 1 < L <= 64)
+// Only ~15% of the bodies create a cell the walk reads (the first body of each
+// walk record), and each of them searches the sorted keys for run ends -- long
+// chains of dependent loads.  Pass 1 finds them without a search and lists
+// them densely; pass 2 runs the searches for the listed bodies only.
+//   The level-l cell holding body i has more than L bodies iff some window of
+// L + 1 consecutive sorted bodies containing i shares its level-l prefix, i.e.
+// iff l <= maxW(i) = max over a in [i - L, i] of lcp(keys[a], keys[a + L]).
+// So body i creates walk records iff its first new cell's parent (level
+// start = lcp[i-1]) is opened -- start <= maxW(i), or the root (n > 1) -- and
+// its new cell at level l is opened iff l <= maxW(i).  Pass 1 also sets the
+// child rows of the opened cells it will create to -1 (absent), so the tree
+// needs no memset of the full child8 array (32 B per cell).
+constexpr int kEmitThreads = 256;
+constexpr int kEmitHalo = 64;  // >= L
+__global__ void __launch_bounds__(kEmitThreads) k_emit_mark(TreeView t, const float4 *__restrict__ bod32,
+                                                            int *__restrict__ creators, int *__restrict__ ncreators) {
+  __shared__ uint64_t ks[kEmitThreads + 2 * kEmitHalo];
+  __shared__ int8_t ws[kEmitThreads + kEmitHalo];
+  const int64_t n = t.n;
+  const int C = (int)tree_count(t);
+  if (C > t.C) return;  // sync-free build overflowed its capacity (flagged; redone)
+  const int L = t.mleaf;
+  const int64_t b0 = (int64_t)blockIdx.x * kEmitThreads;
+  for (int k = threadIdx.x; k < kEmitThreads + 2 * kEmitHalo; k += kEmitThreads) {
+    const int64_t g = b0 - kEmitHalo + k;  // ks[k] = keys[b0 - H + k]
+    ks[k] = g >= 0 && g < n ? t.keys[g] : 0ull;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < kEmitThreads + kEmitHalo; k += kEmitThreads) {
+    const int64_t a = b0 - kEmitHalo + k;  // ws[k] = W(a), -1 without a full window
+    ws[k] = (int8_t)(a >= 0 && a + L < n ? lcp_of(ks[k], ks[k + L]) : -1);
+  }
+  __syncthreads();
+  const int64_t i = b0 + threadIdx.x;
+  bool creator = false;
+  if (i < n) {
+    const int li = threadIdx.x + kEmitHalo;
+    if (i == 0) {
+      t.link[0] = make_int4(C, (int)n, 0, 0);
+      if (t.parent) t.parent[0] = -1;
+      t.mclass[0] = n > 1 ? 2 : 0;  // the walk opens a root holding > 1 body
+      if (n > 1) {
+        int4 *row = reinterpret_cast<int4 *>(t.child8);
+        row[0] = row[1] = make_int4(-1, -1, -1, -1);
+      }
+      if (n == 1 && t.bnd_prev < 0 && t.bnd_next < 0) {  // hashed.py:464-474: root = leaf
+        const float4 v = bod32[0];
+        t.cm64[0] = make_double4(v.x, v.y, v.z, v.w);
+      }
+    }
+    const int lp = i > 0 ? t.lcp[i - 1] : -1;
+    const int ln = i + 1 < n ? t.lcp[i] : -1;
+    int depth = min((lp > ln ? lp : ln) + 1, kMaxLevel);
+    if (i == 0 && t.bnd_prev >= 0) depth = max(depth, min(t.bnd_prev + 1, kMaxLevel));
+    if (i == n - 1 && t.bnd_next >= 0) depth = max(depth, min(t.bnd_next + 1, kMaxLevel));
+    const int start = i > 0 ? lp : 0;
+    int maxw = -1;
+    for (int a = li - L; a <= li; ++a) maxw = max(maxw, (int)ws[a]);
+    creator = n > 1 && (start == 0 || start <= maxw);
+    if (creator) {  // the rows of the opened cells this body creates: all slots absent
+      const int base = 1 + (int)t.off[i];
+      int4 *row = reinterpret_cast<int4 *>(t.child8);
+      for (int l = start + 1; l <= depth && l <= maxw && l < kMaxLevel; ++l) {
+        if (l == depth) break;  // the body's last cell is a leaf or a duplicate-key bucket
+        const int64_t c = base + (l - start - 1);
+        row[2 * c] = row[2 * c + 1] = make_int4(-1, -1, -1, -1);
+      }
+    }
+  }
+  // densely list the creators (one atomic per warp)
+  const unsigned m = __ballot_sync(0xffffffffu, creator);
+  const unsigned lane = threadIdx.x & 31;
+  int wbase = 0;
+  if (lane == 0 && m) wbase = atomicAdd(ncreators, __popc(m));
+  wbase = __shfl_sync(0xffffffffu, wbase, 0);
+  if (creator) creators[wbase + __popc(m & ((1u << lane) - 1u))] = (int)i;
+}
+
+__global__ void __launch_bounds__(128) k_emit_create(TreeView t, const float4 *__restrict__ bod32,
+                                                     const int *__restrict__ creators,
+                                                     const int *__restrict__ ncreators) {
+  const int64_t n = t.n;
+  const int C = (int)tree_count(t);
+  if (C > t.C) return;
+  const int L = t.mleaf;
+  const int nc = *ncreators;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nc; q += gridDim.x * blockDim.x) {
+    const int64_t i = creators[q];
+    const uint64_t k = t.keys[i];
+    const int lp = i > 0 ? t.lcp[i - 1] : -1;
+    const int ln = i + 1 < n ? t.lcp[i] : -1;
+    int depth = min((lp > ln ? lp : ln) + 1, kMaxLevel);
+    if (i == 0 && t.bnd_prev >= 0) depth = max(depth, min(t.bnd_prev + 1, kMaxLevel));
+    if (i == n - 1 && t.bnd_next >= 0) depth = max(depth, min(t.bnd_next + 1, kMaxLevel));
+    const int start = i > 0 ? lp : 0;
+    const int base = 1 + (int)t.off[i];
+    int par = 0;
+    if (start > 0) {
+      const int shift = 3 * (kMortonBits - start);
+      const int64_t j = run_begin(t.keys, i, k >> shift, shift);
+      const int startj = j > 0 ? t.lcp[j - 1] : 0;
+      par = 1 + (int)t.off[j] + (start - startj - 1);
+    }
+    for (int l = start + 1; l <= depth; ++l) {
+      const int c = base + (l - start - 1);
+      const bool leafc = l == depth && ln != kMaxLevel;
+      t.child8[8 * (int64_t)par + (int)((k >> (3 * (kMortonBits - l))) & 7)] = leafc ? -(c + 2) : c;
+      if (l == depth && ln == kMaxLevel) {  // first body of a duplicate-key run: a bucket
+        const int64_t end = run_end(t.keys, n, i, k, 0);
+        const int skip = end < n ? 1 + (int)t.off[end] : C;
+        t.link[c] = make_int4(skip, (int)(end - i), (int)i, l);
+        t.mclass[c] = 1;
+        break;
+      }
+      if (leafc) {  // a one-body record: its body is its moments
+        t.link[c] = make_int4(c + 1, 1, (int)i, l);
+        t.mclass[c] = kClassLeafRecord;
+        const float4 v = bod32[i];
+        t.cm64[c] = make_double4(v.x, v.y, v.z, v.w);
+        break;
+      }
+      const int shift = 3 * (kMortonBits - l);
+      // more than L bodies iff body i + L still shares the prefix (l < 21 here)
+      const bool opens = i + L < n && (t.keys[i + L] >> shift) == (k >> shift);
+      int64_t end;
+      if (opens) {
+        end = run_end(t.keys, n, i + L, k >> shift, shift);
+      } else {  // <= L bodies: a short forward probe
+        int64_t e = i + 1;
+        while (e < n && e <= i + L && (t.keys[e] >> shift) == (k >> shift)) ++e;
+        end = e;
+      }
+      const int skip = end < n ? 1 + (int)t.off[end] : C;
+      t.link[c] = make_int4(skip, (int)(end - i), (int)i, l);
+      t.mclass[c] = opens ? (uint8_t)(2 + l) : 1;
+      if (!opens) break;
+      par = c;
+    }
+  }
+}
+
+bool launch_emit_walk(const TreeView &t, const float4 *bod32, int *scratch, int *counter, int sms, cudaStream_t s) {
+  if (t.n <= 0 || !t.mclass || !bod32 || t.mleaf <= 1 || t.mleaf > kEmitHalo) return false;
+  cudaMemsetAsync(counter, 0, sizeof(int), s);
+  k_emit_mark<<<(unsigned)((t.n + kEmitThreads - 1) / kEmitThreads), kEmitThreads, 0, s>>>(t, bod32, scratch, counter);
+  // one thread per creator for up to n / 4 of them (measured ~15%: the searches
+  // are latency chains, so they want many threads, not a few long loops)
+  const int64_t g = std::max<int64_t>(sms * 16, (t.n / 4 + 127) / 128);
+  k_emit_create<<<(unsigned)g, 128, 0, s>>>(t, bod32, scratch, counter);
+  return true;
+}
+
 // a sorted body as (x, y, z, m) in double
 __device__ __forceinline__ double4 body64(const TreeView &t, int64_t j) {
   if (t.bod64) return t.bod64[j];

@@ -142,6 +142,10 @@ struct TreeView {
 };
 constexpr uint8_t kClassLeafRecord = 255;
 void launch_emit(const TreeView &t, const float4 *bod32, const double4 *bod64, cudaStream_t s);
+// walk-only trees (t.mclass, 1 < t.mleaf <= 64, fp32 bodies): the two-pass emit
+// (scratch: int[n] creator list, counter: one int); no memset of child8 needed.
+// Returns false (nothing launched) when the tree is not of that kind.
+bool launch_emit_walk(const TreeView &t, const float4 *bod32, int *scratch, int *counter, int sms, cudaStream_t s);
 // cursor: int[kMaxLevel+1] scratch; list: int[C]
 // Moments: C on device (launch_set_count) or host, per-level counts on device
 // (lvl: counts[22] from k_lcp_new | offsets[22] | cursors[22]); one cooperative
