@@ -444,7 +444,7 @@ int ensure_walk_tree(bh_handle *h, double theta, int leaf, cudaStream_t s) {
   launch_walk_tree(t, h->dR, theta, leaf, h->smask.as<uint32_t>(), h->nck.as<uint32_t>(),
                    h->wbase.as<uint32_t>(), h->wscan_tmp.p, h->wscan_tmp.bytes,
                    h->wnodes.as<WalkNode>(), h->dCp, s);
-  h->launches += 3;
+  h->launches += h->mom_leaf > 1 && h->mom_leaf == leaf ? 6 : 5;  // walk-only: list count, 3 scan, bases, records
   BH_LAUNCHED();
   h->walk_valid = true;
   h->walk_theta = theta;

@@ -217,8 +217,8 @@ __global__ void k_compact_parents(TreeView t, const double *__restrict__ dR, dou
     }
     return;
   }
-  if (gt == 0) {  // the root's record and the record count
-    *dCp = (int)(1 + base[C - 1] + nck[C - 1]);
+  if (gt == 0) {  // the root's record (and the record count, unless the list scan set it)
+    if (dCp) *dCp = (int)(1 + base[C - 1] + nck[C - 1]);
     out[0] = walk_record(t, 0, dR, theta, expandable(t, 0, leaf, nullptr), nck, base);
   }
   const int *cnt = t.mlvl + 2 * (kMaxLevel + 1);  // cursors = cells listed per level
@@ -257,24 +257,179 @@ __global__ void k_compact_parents(TreeView t, const double *__restrict__ dR, dou
   }
 }
 
+// Walk-only trees: children are counted and the record bases scanned over the
+// list of opened cells only (~1% of the cells), not over every cell.
+//   k_nchild_list   nck[P] and ncl[g] for the g-th listed cell P (level order)
+//   k_scan_list_*   exclusive scan of ncl[0, total) in place (total on device)
+//   k_base_list     base[P] = scanned ncl[g]; the record count
+__device__ __forceinline__ int listed_cell(const int *cnt, const int *offs, const int *list, int64_t g) {
+  int r = (int)g;
+  for (int l = 0; l <= kMaxLevel; ++l) {
+    if (r < cnt[l]) return list[offs[l] + r];
+    r -= cnt[l];
+  }
+  return -1;
+}
+__global__ void k_nchild_list(TreeView t, uint32_t *__restrict__ nck, uint32_t *__restrict__ ncl) {
+  if (tree_overflowed(t)) return;
+  __shared__ int cnt[kMaxLevel + 1], offs[kMaxLevel + 1], total;
+  if (threadIdx.x == 0) {
+    int tot = 0;
+    for (int l = 0; l <= kMaxLevel; ++l) {
+      cnt[l] = t.mlvl[2 * (kMaxLevel + 1) + l];  // cells listed per level
+      offs[l] = t.mlvl[(kMaxLevel + 1) + l];
+      tot += cnt[l];
+    }
+    total = tot;
+  }
+  __syncthreads();
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
+    const int P = listed_cell(cnt, offs, t.mlist, g);
+    const int4 *row = reinterpret_cast<const int4 *>(t.child8 + 8 * (int64_t)P);
+    const int4 r0 = row[0], r1 = row[1];
+    const uint32_t k = (r0.x != -1) + (r0.y != -1) + (r0.z != -1) + (r0.w != -1) + (r1.x != -1) +
+                       (r1.y != -1) + (r1.z != -1) + (r1.w != -1);
+    nck[P] = k;
+    ncl[g] = k;
+  }
+}
+// exclusive scan of v[0, total) in place, total = the listed cells (on device):
+// tile sums, one block scans them (and sets the record count), tiles add their prefix
+constexpr int kLTile = 4096;  // 256 threads x 16 (the tile sums fit the C-sized scan temp)
+__device__ __forceinline__ int listed_total(const TreeView &t) {
+  int tot = 0;
+  for (int l = 0; l <= kMaxLevel; ++l) tot += t.mlvl[2 * (kMaxLevel + 1) + l];
+  return tot;
+}
+__device__ __forceinline__ unsigned block_excl_256(unsigned v, unsigned *wsum, unsigned *all) {
+  const unsigned lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned x = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= (unsigned)o) incl += x;
+  }
+  if (lane == 31) wsum[w] = incl;
+  __syncthreads();
+  unsigned woff = 0, tot = 0;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+    woff += i < (int)w ? wsum[i] : 0u;
+    tot += wsum[i];
+  }
+  if (all) *all = tot;
+  __syncthreads();
+  return woff + incl - v;
+}
+__global__ void __launch_bounds__(256) k_scan_list_tiles(const TreeView t, const uint32_t *__restrict__ v,
+                                                         uint32_t *__restrict__ tsum) {
+  if (tree_overflowed(t)) return;
+  __shared__ unsigned wsum[8];
+  const int64_t total = listed_total(t), ntiles = (total + kLTile - 1) / kLTile;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    unsigned sum = 0;
+    for (int k = 0; k < kLTile / 256; ++k) {
+      const int64_t i = tile * kLTile + k * 256 + threadIdx.x;
+      if (i < total) sum += v[i];
+    }
+    unsigned all;
+    block_excl_256(sum, wsum, &all);
+    if (threadIdx.x == 0) tsum[tile] = all;
+  }
+}
+__global__ void __launch_bounds__(1024) k_scan_list_top(const TreeView t, uint32_t *__restrict__ tsum,
+                                                        int *__restrict__ dCp) {
+  if (tree_overflowed(t)) return;
+  __shared__ unsigned wsum[32];
+  const int64_t total = listed_total(t), ntiles = (total + kLTile - 1) / kLTile;
+  const int64_t per = (ntiles + 1023) / 1024;
+  const int64_t b = per * threadIdx.x, e = b + per < ntiles ? b + per : ntiles;
+  unsigned run = 0;
+  for (int64_t i = b; i < e; ++i) run += tsum[i];
+  const unsigned lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned incl = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned x = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= (unsigned)o) incl += x;
+  }
+  if (lane == 31) wsum[w] = incl;
+  __syncthreads();
+  unsigned woff = 0, all = 0;
+  for (int i = 0; i < 32; ++i) {
+    woff += i < (int)w ? wsum[i] : 0u;
+    all += wsum[i];
+  }
+  unsigned ex = woff + incl - run;
+  for (int64_t i = b; i < e; ++i) {
+    const unsigned x = tsum[i];
+    tsum[i] = ex;
+    ex += x;
+  }
+  if (threadIdx.x == 0) *dCp = 1 + (int)all;  // the root and every listed cell's children
+}
+__global__ void __launch_bounds__(256) k_scan_list_down(const TreeView t, uint32_t *__restrict__ v,
+                                                        const uint32_t *__restrict__ tsum) {
+  if (tree_overflowed(t)) return;
+  __shared__ unsigned wsum[8];
+  const int64_t total = listed_total(t), ntiles = (total + kLTile - 1) / kLTile;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t i0 = tile * kLTile + (int64_t)threadIdx.x * (kLTile / 256);
+    unsigned x[kLTile / 256], sum = 0;
+#pragma unroll
+    for (int k = 0; k < kLTile / 256; ++k) {
+      x[k] = i0 + k < total ? v[i0 + k] : 0u;
+      sum += x[k];
+    }
+    unsigned run = tsum[tile] + block_excl_256(sum, wsum, nullptr);
+#pragma unroll
+    for (int k = 0; k < kLTile / 256; ++k) {
+      if (i0 + k < total) v[i0 + k] = run;
+      run += x[k];
+    }
+  }
+}
+__global__ void k_base_list(TreeView t, const uint32_t *__restrict__ ncl, uint32_t *__restrict__ base) {
+  if (tree_overflowed(t)) return;
+  __shared__ int cnt[kMaxLevel + 1], offs[kMaxLevel + 1], total;
+  if (threadIdx.x == 0) {
+    int tot = 0;
+    for (int l = 0; l <= kMaxLevel; ++l) {
+      cnt[l] = t.mlvl[2 * (kMaxLevel + 1) + l];
+      offs[l] = t.mlvl[(kMaxLevel + 1) + l];
+      tot += cnt[l];
+    }
+    total = tot;
+  }
+  __syncthreads();
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x)
+    base[listed_cell(cnt, offs, t.mlist, g)] = ncl[g];
+}
+
 void launch_walk_tree(const TreeView &t, const double *dR, double theta, int leaf,
                       uint32_t *smask, uint32_t *nck, uint32_t *base, void *scan_tmp,
                       size_t scan_bytes, WalkNode *out, int *dCp, cudaStream_t s,
                       const uint8_t *force, int *rec_of_cell, int *wparent) {
   const int g = grid_for(t.C, 256);
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  if (!force && t.mclass && t.mleaf == leaf && t.mlvl && !rec_of_cell && !wparent) {  // walk-only tree
+    uint32_t *ncl = smask;  // scratch (>= C entries), unused on this path
+    uint32_t *tsum = static_cast<uint32_t *>(scan_tmp);  // (>= C / 4096 tile sums)
+    k_nchild_list<<<sms * 4, 256, 0, s>>>(t, nck, ncl);
+    k_scan_list_tiles<<<sms * 4, 256, 0, s>>>(t, ncl, tsum);
+    k_scan_list_top<<<1, 1024, 0, s>>>(t, tsum, dCp);
+    k_scan_list_down<<<sms * 4, 256, 0, s>>>(t, ncl, tsum);
+    k_base_list<<<sms * 4, 256, 0, s>>>(t, ncl, base);
+    k_compact_parents<<<sms * 8, 256, 0, s>>>(t, dR, theta, leaf, nck, base, out, nullptr);
+    return;
+  }
   if (!force) {  // children counted and ranked from the child8 rows: no slot-mask pass
     k_nchild_rows<<<g, 256, 0, s>>>(t, leaf, nck);
     exclusive_scan_u32(scan_tmp, scan_bytes, nck, base, t.C, s);
-    if (t.mclass && t.mleaf == leaf && t.mlvl && !rec_of_cell && !wparent) {  // walk-only tree
-      static int sms = 0;
-      if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      }
-      k_compact_parents<<<sms * 8, 256, 0, s>>>(t, dR, theta, leaf, nck, base, out, dCp);
-      return;
-    }
     k_compact<<<g, 256, 0, s>>>(t, dR, theta, leaf, force, nullptr, nck, base, out, dCp, rec_of_cell, wparent);
     return;
   }
