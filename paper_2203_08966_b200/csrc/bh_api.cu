@@ -628,7 +628,7 @@ int sim_walk(bh_handle *h, double theta, double eps, int leaf, int64_t begin, in
     const uint32_t *perm = nullptr;  // warps of Hilbert-ordered targets (bh_walk.cu)
     if (walk_hilbert_enabled() && nt > 64) {
       BH_CUDA(h->hperm.ensure(sizeof(uint32_t) * (nt + 1)));
-      launch_hilbert_chunks(h->pos.as<float4>() + begin, nt, h->dR, h->hperm.as<uint32_t>(), s);
+      launch_hilbert_chunks(h->keys2.as<uint64_t>() + begin, nt, h->hperm.as<uint32_t>(), s);  // the tree's keys
       perm = h->hperm.as<uint32_t>();
       h->launches += 1;
     }

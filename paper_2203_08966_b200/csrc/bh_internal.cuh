@@ -229,9 +229,10 @@ void launch_walk_f32(const WalkNode *T, int64_t nrec_max, const float4 *bodies, 
                      int tstride, const uint32_t *tperm, int nt, float e2, int leaf, float *acc, int astride,
                      int64_t *work64, int *work32, DeviceFlags *f, cudaStream_t s,
                      const W9Peers *peers = nullptr);
-// Hilbert order of the targets inside each chunk of 4096 (perm: chunk-local
-// permutation of [0, nt), for the walk's tperm); BH_WALK_HILBERT=0 disables
-void launch_hilbert_chunks(const float4 *pos, int64_t nt, const double *dR, uint32_t *perm, cudaStream_t s);
+// Hilbert order of the targets inside each chunk of 4096, from their sorted
+// Morton keys (perm: chunk-local permutation of [0, nt), for the walk's
+// tperm); BH_WALK_HILBERT=0 disables
+void launch_hilbert_chunks(const uint64_t *mkeys, int64_t nt, uint32_t *perm, cudaStream_t s);
 bool walk_hilbert_enabled();
 // deferred walk (LET overlap): pass A appends (target chunk, record, m0, m1) to
 // out[cap] for records flagged in d.w; pass B (resume) walks in[nin] with

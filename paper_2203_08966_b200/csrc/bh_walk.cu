@@ -1655,90 +1655,120 @@ void launch_walk_f32(const WalkNode *T, int64_t nrec_max, const float4 *bodies, 
 // (CPU model, tools/order_sim.py: -3.5% pc evaluations, -11% mixed cells).
 // The interaction sets are unchanged; only the grouping of targets into warps
 // (and so the fp32 summation order) moves.
-#ifndef BH_HIL_CHUNK
-#define BH_HIL_CHUNK 4096
-#endif
-constexpr int kHilChunk = BH_HIL_CHUNK;
-constexpr int kHilThreads = kHilChunk >= 8192 ? 1024 : 512;
-__device__ __forceinline__ uint64_t hil_spread(uint64_t v) {  // 21 bits -> every third bit
-  v &= 0x1fffffull;
-  v = (v | v << 32) & 0x1f00000000ffffull;
-  v = (v | v << 16) & 0x1f0000ff0000ffull;
-  v = (v | v << 8) & 0x100f00f00f00f00full;
-  v = (v | v << 4) & 0x10c30c30c30c30c3ull;
-  v = (v | v << 2) & 0x1249249249249249ull;
-  return v;
-}
-// Skilling's transpose: Hilbert index of three 21-bit coordinates
-__device__ __forceinline__ uint64_t hilbert63(uint32_t x, uint32_t y, uint32_t z) {
-  uint32_t X0 = x, X1 = y, X2 = z;
-  for (uint32_t Q = 1u << 20; Q > 1u; Q >>= 1) {
-    const uint32_t P = Q - 1u;
-    if (X0 & Q) X0 ^= P;
-    if (X1 & Q) X0 ^= P;
-    else { const uint32_t t = (X0 ^ X1) & P; X0 ^= t; X1 ^= t; }
-    if (X2 & Q) X0 ^= P;
-    else { const uint32_t t = (X0 ^ X2) & P; X0 ^= t; X2 ^= t; }
-  }
-  X1 ^= X0;
-  X2 ^= X1;
-  uint32_t t = 0;
-  for (uint32_t Q = 1u << 20; Q > 1u; Q >>= 1)
-    if (X2 & Q) t ^= Q - 1u;
-  X0 ^= t; X1 ^= t; X2 ^= t;
-  return (hil_spread(X0) << 2) | (hil_spread(X1) << 1) | hil_spread(X2);
-}
-__global__ void __launch_bounds__(kHilThreads) k_hilbert_chunks(const float4 *__restrict__ pos, int nt,
-                                                                const double *__restrict__ dR,
+// The curve as a 24-state machine over the Morton digits (octant -> Hilbert
+// digit, next state), derived from Skilling's transpose and checked against it
+// by tools/hilbert_table.py; one combined byte per (state, octant).
+__constant__ uint8_t kHilDigit[24][8] = {{0, 1, 3, 2, 7, 6, 4, 5}, {0, 7, 1, 6, 3, 4, 2, 5}, {0, 3, 7, 4, 1, 2, 6, 5}, {0, 1, 7, 6, 3, 2, 4, 5}, {6, 5, 7, 4, 1, 2, 0, 3}, {6, 1, 7, 0, 5, 2, 4, 3}, {4, 7, 3, 0, 5, 6, 2, 1}, {2, 1, 3, 0, 5, 6, 4, 7}, {6, 7, 5, 4, 1, 0, 2, 3}, {6, 7, 1, 0, 5, 4, 2, 3}, {0, 7, 3, 4, 1, 6, 2, 5}, {0, 3, 1, 2, 7, 4, 6, 5}, {6, 5, 1, 2, 7, 4, 0, 3}, {4, 7, 5, 6, 3, 0, 2, 1}, {2, 1, 5, 6, 3, 0, 4, 7}, {6, 1, 5, 2, 7, 0, 4, 3}, {4, 3, 7, 0, 5, 2, 6, 1}, {4, 5, 7, 6, 3, 2, 0, 1}, {2, 5, 1, 6, 3, 4, 0, 7}, {2, 3, 1, 0, 5, 4, 6, 7}, {4, 3, 5, 2, 7, 0, 6, 1}, {4, 5, 3, 2, 7, 6, 0, 1}, {2, 5, 3, 4, 1, 6, 0, 7}, {2, 3, 5, 4, 1, 0, 6, 7}};
+__constant__ uint8_t kHilNext[24][8] = {{1, 3, 15, 0, 20, 21, 10, 0}, {2, 6, 11, 13, 9, 3, 1, 1}, {0, 4, 17, 11, 10, 2, 16, 2}, {10, 0, 16, 17, 5, 3, 1, 3}, {5, 4, 3, 12, 22, 4, 21, 2}, {4, 7, 2, 6, 5, 5, 9, 3}, {7, 8, 13, 19, 6, 10, 6, 16}, {7, 5, 14, 9, 7, 22, 6, 23}, {9, 1, 8, 15, 23, 20, 8, 10}, {8, 10, 19, 16, 9, 5, 9, 1}, {11, 13, 8, 0, 2, 6, 10, 10}, {3, 12, 1, 11, 21, 2, 20, 11}, {15, 12, 18, 12, 0, 4, 17, 11}, {14, 9, 13, 1, 6, 23, 13, 20}, {14, 15, 14, 18, 7, 8, 13, 19}, {12, 14, 15, 15, 11, 13, 8, 0}, {19, 17, 4, 7, 16, 16, 2, 6}, {18, 17, 5, 3, 16, 17, 22, 21}, {18, 18, 12, 14, 19, 17, 4, 7}, {19, 18, 9, 5, 19, 16, 23, 22}, {23, 21, 20, 20, 12, 14, 11, 13}, {22, 21, 20, 21, 15, 0, 18, 17}, {22, 22, 23, 21, 4, 7, 12, 14}, {23, 22, 23, 20, 8, 15, 19, 18}};
+
+// One block of 1024 threads per chunk of 4096 targets, four per thread: the
+// Hilbert index from the tree's Morton key (21 table steps), 20 bits of it
+// below the chunk's common prefix and the 12-bit chunk position packed in one
+// word, sorted by a bitonic network (in-thread for strides >= 1024, shared
+// memory for 32..512, shuffles below).  The order only has to preserve
+// locality, so the truncated keys are enough.
+constexpr int kHilChunk = 4096;
+constexpr int kHilThreads = 1024;
+constexpr int kHilPer = kHilChunk / kHilThreads;
+__global__ void __launch_bounds__(kHilThreads) k_hilbert_chunks(const uint64_t *__restrict__ mkeys, int nt,
                                                                 uint32_t *__restrict__ perm) {
-  extern __shared__ __align__(16) unsigned char hil_smem[];
-  uint64_t *key = reinterpret_cast<uint64_t *>(hil_smem);
-  uint32_t *idx = reinterpret_cast<uint32_t *>(key + kHilChunk);
-  const int64_t c0 = (int64_t)blockIdx.x * kHilChunk;
-  const int cnt = (int)(nt - c0 < kHilChunk ? nt - c0 : kHilChunk);
-  const double R = *dR;
-  const float inv = (float)((double)(1 << 21) / (2.0 * R)), fR = (float)R;
-  for (int e = threadIdx.x; e < kHilChunk; e += kHilThreads) {
-    uint64_t k = ~0ull;
-    if (e < cnt) {
-      const float4 p = pos[c0 + e];
-      const auto q = [&](float v) {
-        const float f = floorf((v + fR) * inv);
-        return (uint32_t)fminf(fmaxf(f, 0.f), 2097151.f);
-      };
-      k = hilbert63(q(p.x), q(p.y), q(p.z));
-    }
-    key[e] = k;
-    idx[e] = (uint32_t)e;
-  }
+  __shared__ uint32_t sv[kHilChunk];
+  __shared__ uint8_t tab[24 * 8];
+  __shared__ uint64_t smin[32], smax[32];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (tid < 24 * 8) tab[tid] = (uint8_t)(kHilDigit[tid >> 3][tid & 7] << 5 | kHilNext[tid >> 3][tid & 7]);
   __syncthreads();
-  for (int k = 2; k <= kHilChunk; k <<= 1) {  // bitonic sort of (key, idx) by key
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < kHilChunk; i += kHilThreads) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
-          const uint64_t a = key[i], b = key[ixj];
-          if ((a > b) == ((i & k) == 0)) {
-            key[i] = b; key[ixj] = a;
-            const uint32_t t = idx[i]; idx[i] = idx[ixj]; idx[ixj] = t;
-          }
-        }
+  const int64_t c0 = (int64_t)blockIdx.x * kHilChunk;
+  uint64_t h[kHilPer];
+  uint64_t mn = ~0ull, mx = 0ull;
+#pragma unroll
+  for (int r = 0; r < kHilPer; ++r) {
+    const int e = tid + kHilThreads * r;
+    h[r] = 0;
+    if (c0 + e < nt) {
+      const uint64_t m = mkeys[c0 + e];
+      uint64_t k = 0;
+      int st = 0;
+#pragma unroll
+      for (int l = 0; l < kMortonBits; ++l) {
+        const uint8_t v = tab[st * 8 + (int)((m >> (3 * (kMortonBits - 1 - l))) & 7)];
+        k = k << 3 | (v >> 5);
+        st = v & 31;
       }
-      __syncthreads();
+      h[r] = k;
+      mn = k < mn ? k : mn;
+      mx = k > mx ? k : mx;
     }
   }
-  for (int e = threadIdx.x; e < cnt; e += kHilThreads) perm[c0 + e] = (uint32_t)c0 + idx[e];
+  // the chunk's key range: the bits below its common prefix order it
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const uint64_t a = __shfl_xor_sync(0xffffffffu, mn, o), b = __shfl_xor_sync(0xffffffffu, mx, o);
+    mn = a < mn ? a : mn;
+    mx = b > mx ? b : mx;
+  }
+  if (lane == 0) { smin[w] = mn; smax[w] = mx; }
+  __syncthreads();
+  mn = smin[0];
+  mx = smax[0];
+  for (int i = 1; i < kHilThreads / 32; ++i) {
+    mn = smin[i] < mn ? smin[i] : mn;
+    mx = smax[i] > mx ? smax[i] : mx;
+  }
+  const uint64_t span = mx - mn;  // (every chunk holds a target: mx >= mn)
+  const int top = span ? 63 - __clzll((long long)span) : 0;
+  const int shift = top > 19 ? top - 19 : 0;
+  uint32_t v[kHilPer];
+#pragma unroll
+  for (int r = 0; r < kHilPer; ++r) {
+    const int e = tid + kHilThreads * r;
+    v[r] = c0 + e < nt ? ((uint32_t)((h[r] - mn) >> shift) << 12) | (uint32_t)e : 0xffffffffu;
+  }
+  for (int k = 2; k <= kHilChunk; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= kHilThreads) {  // partners in this thread's registers
+        const int rj = j / kHilThreads;
+#pragma unroll
+        for (int r = 0; r < kHilPer; ++r) {
+          if (r & rj) continue;
+          const int e = tid + kHilThreads * r;
+          const bool up = (e & k) == 0;
+          const uint32_t a = v[r], b = v[r | rj];
+          v[r] = up ? min(a, b) : max(a, b);
+          v[r | rj] = up ? max(a, b) : min(a, b);
+        }
+        continue;
+      }
+      uint32_t p[kHilPer];
+      if (j >= 32) {
+#pragma unroll
+        for (int r = 0; r < kHilPer; ++r) sv[tid + kHilThreads * r] = v[r];
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < kHilPer; ++r) p[r] = sv[(tid ^ j) + kHilThreads * r];
+        __syncthreads();
+      } else {
+#pragma unroll
+        for (int r = 0; r < kHilPer; ++r) p[r] = __shfl_xor_sync(0xffffffffu, v[r], j);
+      }
+#pragma unroll
+      for (int r = 0; r < kHilPer; ++r) {
+        const int e = tid + kHilThreads * r;
+        const bool up = (e & k) == 0, lower = (e & j) == 0;
+        v[r] = (lower == up) ? min(v[r], p[r]) : max(v[r], p[r]);
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < kHilPer; ++r) {
+    const int e = tid + kHilThreads * r;
+    if (c0 + e < nt) perm[c0 + e] = (uint32_t)c0 + (v[r] & (kHilChunk - 1));
+  }
 }
 
-void launch_hilbert_chunks(const float4 *pos, int64_t nt, const double *dR, uint32_t *perm, cudaStream_t s) {
+void launch_hilbert_chunks(const uint64_t *mkeys, int64_t nt, uint32_t *perm, cudaStream_t s) {
   if (nt <= 0) return;
-  const int smem = kHilChunk * (int)(sizeof(uint64_t) + sizeof(uint32_t));
-  static bool init = false;
-  if (!init) {
-    cudaFuncSetAttribute(k_hilbert_chunks, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    init = true;
-  }
-  k_hilbert_chunks<<<(unsigned)((nt + kHilChunk - 1) / kHilChunk), kHilThreads, smem, s>>>(pos, (int)nt, dR, perm);
+  k_hilbert_chunks<<<(unsigned)((nt + kHilChunk - 1) / kHilChunk), kHilThreads, 0, s>>>(mkeys, (int)nt, perm);
 }
 
 bool walk_hilbert_enabled() {  // BH_WALK_HILBERT=0: Morton-consecutive warps
