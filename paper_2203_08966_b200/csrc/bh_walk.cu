@@ -1667,10 +1667,16 @@ __constant__ uint8_t kHilNext[24][8] = {{1, 3, 15, 0, 20, 21, 10, 0}, {2, 6, 11,
 // word, sorted by a bitonic network (in-thread for strides >= 1024, shared
 // memory for 32..512, shuffles below).  The order only has to preserve
 // locality, so the truncated keys are enough.
+#ifndef BH_HIL_RADIX
+#define BH_HIL_RADIX 1  // 1: 4-pass stable radix, 2: one counting pass on 12 bits (cheaper, loses order: slower walk), 0: bitonic
+#endif
 constexpr int kHilChunk = 4096;
 constexpr int kHilThreads = 1024;
 constexpr int kHilPer = kHilChunk / kHilThreads;
-__global__ void __launch_bounds__(kHilThreads) k_hilbert_chunks(const uint64_t *__restrict__ mkeys, int nt,
+#ifndef BH_HIL_MINB
+#define BH_HIL_MINB 2
+#endif
+__global__ void __launch_bounds__(kHilThreads, BH_HIL_MINB) k_hilbert_chunks(const uint64_t *__restrict__ mkeys, int nt,
                                                                 uint32_t *__restrict__ perm) {
   __shared__ uint32_t sv[kHilChunk];
   __shared__ uint8_t tab[24 * 8];
@@ -1683,7 +1689,7 @@ __global__ void __launch_bounds__(kHilThreads) k_hilbert_chunks(const uint64_t *
   uint64_t mn = ~0ull, mx = 0ull;
 #pragma unroll
   for (int r = 0; r < kHilPer; ++r) {
-    const int e = tid + kHilThreads * r;
+    const int e = BH_HIL_RADIX ? w * 128 + 32 * r + lane : tid + kHilThreads * r;  // element of item r
     h[r] = 0;
     if (c0 + e < nt) {
       const uint64_t m = mkeys[c0 + e];
@@ -1719,6 +1725,112 @@ __global__ void __launch_bounds__(kHilThreads) k_hilbert_chunks(const uint64_t *
   const int top = span ? 63 - __clzll((long long)span) : 0;
   const int shift = top > 19 ? top - 19 : 0;
   uint32_t v[kHilPer];
+#if BH_HIL_RADIX == 2
+  // one counting pass on the top 12 bits below the common prefix (4096 buckets
+  // for 4096 targets: a bucket is a tiny region, its internal order is free)
+  {
+    const int sh12 = top > 11 ? top - 11 : 0;
+    for (int b = tid; b < kHilChunk; b += kHilThreads) sv[b] = 0u;
+    __syncthreads();
+    unsigned bk[kHilPer], rk[kHilPer];
+#pragma unroll
+    for (int r = 0; r < kHilPer; ++r) {
+      const int e = w * 128 + 32 * r + lane;
+      bk[r] = c0 + e < nt ? (unsigned)((h[r] - mn) >> sh12) : 0xffffffffu;
+      rk[r] = bk[r] != 0xffffffffu ? atomicAdd(&sv[bk[r]], 1u) : 0u;
+    }
+    __syncthreads();
+    // exclusive scan of the 4096 bucket counts: 4 consecutive per thread
+    unsigned c[kHilPer], run = 0;
+#pragma unroll
+    for (int q = 0; q < kHilPer; ++q) { c[q] = sv[tid * kHilPer + q]; run += c[q]; }
+    unsigned incl = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned x = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= (unsigned)o) incl += x;
+    }
+    __shared__ unsigned wsum2[32];
+    if (lane == 31) wsum2[w] = incl;
+    __syncthreads();
+    unsigned woff = 0;
+    if (lane < (unsigned)w) woff = wsum2[lane];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) woff += __shfl_xor_sync(0xffffffffu, woff, o);
+    unsigned ex = woff + incl - run;
+#pragma unroll
+    for (int q = 0; q < kHilPer; ++q) { sv[tid * kHilPer + q] = ex; ex += c[q]; }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kHilPer; ++r) {
+      const int e = w * 128 + 32 * r + lane;
+      if (c0 + e < nt) perm[c0 + sv[bk[r]] + rk[r]] = (uint32_t)(c0 + e);
+    }
+    return;
+  }
+#elif BH_HIL_RADIX
+  // stable LSD radix sort of the 20 key bits, 4 passes of 5 bits; element
+  // w*128 + 32 r + lane is item r of lane `lane` in warp w (ranks from ballots)
+  __shared__ unsigned wh[32][33];  // per warp: digit counts, then offsets
+  __shared__ unsigned wtot[32];
+#pragma unroll
+  for (int r = 0; r < kHilPer; ++r) {
+    const int e = w * 128 + 32 * r + lane;
+    v[r] = c0 + e < nt ? ((uint32_t)((h[r] - mn) >> shift) << 12) | (uint32_t)e : 0xffffffffu;
+  }
+  const unsigned lt = (1u << lane) - 1u;
+  for (int pass = 0; pass < 4; ++pass) {
+    const int sh = 12 + 5 * pass;
+    wh[w][lane] = 0u;
+    __syncwarp();
+    unsigned rk[kHilPer];
+#pragma unroll
+    for (int r = 0; r < kHilPer; ++r) {
+      const unsigned d = (v[r] >> sh) & 31u;
+      unsigned peers = 0xffffffffu;
+#pragma unroll
+      for (int b = 0; b < 5; ++b) {
+        const unsigned bb = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+        peers &= ((d >> b) & 1u) ? bb : ~bb;
+      }
+      const unsigned base = wh[w][d];
+      __syncwarp();
+      if (lane == 31u - __clz(peers)) wh[w][d] = base + __popc(peers);
+      __syncwarp();
+      rk[r] = base + __popc(peers & lt);
+    }
+    __syncthreads();
+    // exclusive offsets in (digit, warp) order: thread (d = tid / 32, w' = tid % 32)
+    {
+      const int d = tid >> 5, ww = tid & 31;
+      const unsigned c = wh[ww][d];
+      unsigned incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned x = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= (unsigned)o) incl += x;
+      }
+      if (lane == 31) wtot[d] = incl;
+      __syncthreads();
+      unsigned before = 0;
+      for (int q = 0; q < d; ++q) before += wtot[q];
+      wh[ww][d] = before + incl - c;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kHilPer; ++r) sv[wh[w][(v[r] >> sh) & 31u] + rk[r]] = v[r];
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kHilPer; ++r) v[r] = sv[w * 128 + 32 * r + lane];
+    __syncthreads();
+  }
+#pragma unroll
+  for (int r = 0; r < kHilPer; ++r) {
+    const int e = w * 128 + 32 * r + lane;
+    if (c0 + e < nt) perm[c0 + e] = (uint32_t)c0 + (v[r] & (kHilChunk - 1));
+  }
+  return;
+#endif
 #pragma unroll
   for (int r = 0; r < kHilPer; ++r) {
     const int e = tid + kHilThreads * r;
