@@ -624,14 +624,16 @@ int sim_walk(bh_handle *h, double theta, double eps, int leaf, int64_t begin, in
     peers.acc[r] = reinterpret_cast<float *>(static_cast<char *>(h->peer_acc[r]) + row * begin);
     peers.work[r] = static_cast<int *>(h->peer_work[r]) + begin;
   }
+  // warps of Hilbert-ordered targets (bh_walk.cu): tighter target groups, same
+  // per-target interaction sets and (fp64) the same per-target summation order
+  const uint32_t *perm = nullptr;
+  if (walk_hilbert_enabled() && nt > 64) {
+    BH_CUDA(h->hperm.ensure(sizeof(uint32_t) * (nt + 1)));
+    launch_hilbert_chunks(h->keys2.as<uint64_t>() + begin, nt, h->hperm.as<uint32_t>(), s);  // the tree's keys
+    perm = h->hperm.as<uint32_t>();
+    h->launches += 1;
+  }
   if (f32) {
-    const uint32_t *perm = nullptr;  // warps of Hilbert-ordered targets (bh_walk.cu)
-    if (walk_hilbert_enabled() && nt > 64) {
-      BH_CUDA(h->hperm.ensure(sizeof(uint32_t) * (nt + 1)));
-      launch_hilbert_chunks(h->keys2.as<uint64_t>() + begin, nt, h->hperm.as<uint32_t>(), s);  // the tree's keys
-      perm = h->hperm.as<uint32_t>();
-      h->launches += 1;
-    }
     launch_walk_f32(h->wnodes.as<WalkNode>(), walk_records_bound(h), h->pos.as<float4>(),
                     h->pos.as<float>() + 4 * begin, 4, perm, (int)nt, (float)(eps * eps), leaf,
                     h->acc.as<float>() + 4 * begin, 4, nullptr, w32, h->flags, s, h->npeers ? &peers : nullptr);
@@ -639,7 +641,7 @@ int sim_walk(bh_handle *h, double theta, double eps, int leaf, int64_t begin, in
     WalkParams P;
     fill_walk_params(h, P, nt, theta, eps, leaf);
     launch_walk_f64(P, h->cm64.as<double4>(), h->q64.as<double>(), h->link.as<int4>(),
-                    h->pos.as<double4>(), h->pos.as<double>() + 4 * begin, 4, nullptr,
+                    h->pos.as<double4>(), h->pos.as<double>() + 4 * begin, 4, perm,
                     h->acc.as<double>() + 4 * begin, 4, nullptr, w32, h->flags, s);
     if (h->npeers) launch_peer_scatter(h->acc.as<double>() + 4 * begin, row, w32, nt, peers, s);
   }
