@@ -1,9 +1,10 @@
 """The fp32 walk schedules give the same per-target interaction sets.
 
 The default traversal (k_walk9, group-classified) is checked against the
-masked-stack walk it replaced (k_walk, BH_WALK_V4=1) and against itself with
+masked-stack walk it replaced (k_walk, BH_WALK_V4=1), against itself with
 every batch forced to a single sibling set (BH_W9_FULL=0, the DFS mode whose
-depth bound sizes its frontier).  Per-body work (pp + 2 pc) must be identical;
+depth bound sizes its frontier), and against itself with Morton-consecutive
+warps instead of the Hilbert target order (BH_WALK_HILBERT=0).  Per-body work (pp + 2 pc) must be identical;
 accelerations differ only by fp32 summation order.  The schedule is chosen once
 per process, so each runs in a subprocess.
 """
@@ -68,9 +69,11 @@ def test_walk_schedules_same_interaction_sets(tmp_path):
     base = _run(tmp_path, "v9", {"BH_WALK_V4": "0"})
     dfs = _run(tmp_path, "v9dfs", {"BH_WALK_V4": "0", "BH_W9_FULL": "0"})
     v4 = _run(tmp_path, "v4", {"BH_WALK_V4": "1"})
+    # Morton-consecutive warps instead of the Hilbert target order (bh_walk.cu)
+    morton = _run(tmp_path, "v9morton", {"BH_WALK_V4": "0", "BH_WALK_HILBERT": "0"})
     report = {}
     for name, (a, w) in base.items():
-        for other_name, other in (("dfs", dfs), ("v4", v4)):
+        for other_name, other in (("dfs", dfs), ("v4", v4), ("morton", morton)):
             a2, w2 = other[name]
             assert np.array_equal(w, w2), f"{name}: work differs from {other_name}"
             err = float(np.linalg.norm(a - a2) / np.linalg.norm(a2))
