@@ -338,7 +338,10 @@ __global__ void __launch_bounds__(256) k_scan_list_tiles(const TreeView t, const
 }
 __global__ void __launch_bounds__(1024) k_scan_list_top(const TreeView t, uint32_t *__restrict__ tsum,
                                                         int *__restrict__ dCp) {
-  if (tree_overflowed(t)) return;
+  if (tree_overflowed(t)) {  // the build overflowed (redone): one empty root record
+    if (threadIdx.x == 0) *dCp = 1;
+    return;
+  }
   __shared__ unsigned wsum[32];
   const int64_t total = listed_total(t), ntiles = (total + kLTile - 1) / kLTile;
   const int64_t per = (ntiles + 1023) / 1024;
