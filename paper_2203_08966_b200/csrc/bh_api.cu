@@ -1677,6 +1677,16 @@ int bh_sim_walk_records(bh_handle *h, void *d_out, int64_t *n_out, void *stream)
   return BH_OK;
 }
 
+// The walk's Hilbert target order for caller target arrays (the distributed
+// walk): the same deterministic permutation for pass A and pass B
+static const uint32_t *caller_target_order(bh_handle *h, const float *d_targets4, int64_t nt, cudaStream_t s) {
+  if (!walk_hilbert_enabled() || nt <= 64) return nullptr;
+  if (h->hperm.ensure(sizeof(uint32_t) * (nt + 1)) != cudaSuccess) return nullptr;
+  launch_hilbert_chunks_pos(reinterpret_cast<const float4 *>(d_targets4), nt, h->dR, h->hperm.as<uint32_t>(), s);
+  h->launches += 1;
+  return h->hperm.as<uint32_t>();
+}
+
 // The fp32 walk over a caller-assembled record array (layout of WalkNode in
 // bh_walk.cu; record 0 is the root) and a caller body array (bucket bodies).
 int bh_walk_records_f32(bh_handle *h, const void *d_records, int64_t nrec, const float *d_bodies4,
@@ -1687,8 +1697,9 @@ int bh_walk_records_f32(bh_handle *h, const void *d_records, int64_t nrec, const
   cudaStream_t s = S(stream);
   BH_TRY(reset_counters(h, s));
   h->tbegin(BH_PHASE_WALK, s);
+  const uint32_t *perm = caller_target_order(h, d_targets4, nt, s);
   launch_walk_f32(static_cast<const WalkNode *>(d_records), nrec, reinterpret_cast<const float4 *>(d_bodies4),
-                  d_targets4, 4, nullptr, (int)nt, (float)(eps * eps), leaf_size, d_acc4, 4, nullptr,
+                  d_targets4, 4, perm, (int)nt, (float)(eps * eps), leaf_size, d_acc4, 4, nullptr,
                   d_work, h->flags, s);
   h->tend(s);
   h->launches += 1;
@@ -1713,8 +1724,10 @@ int bh_walk_records_defer_f32(bh_handle *h, const void *d_records, int64_t nrec,
   dfr.count = d_count;
   dfr.cap = (int)std::min<int64_t>(cap, 0x7fffffff);
   h->tbegin(BH_PHASE_WALK, s);
+  const uint32_t *perm = caller_target_order(h, d_targets4, nt, s);
   launch_walk_defer_f32(static_cast<const WalkNode *>(d_records), nrec, reinterpret_cast<const float4 *>(d_bodies4),
-                        d_targets4, (int)nt, (float)(eps * eps), leaf_size, d_acc4, d_work, h->flags, dfr, false, s);
+                        d_targets4, (int)nt, (float)(eps * eps), leaf_size, d_acc4, d_work, h->flags, dfr, false, s,
+                        perm);
   h->tend(s);
   h->launches += 1;
   BH_LAUNCHED();
@@ -1737,8 +1750,10 @@ int bh_walk_records_resume_f32(bh_handle *h, const void *d_records, int64_t nrec
   dfr.nin = (int)n_entries;
   dfr.fcnc = reinterpret_cast<const int2 *>(d_fcnc);
   h->tbegin(BH_PHASE_WALK, s);
+  const uint32_t *perm = caller_target_order(h, d_targets4, nt, s);  // pass A's order (deterministic)
   launch_walk_defer_f32(static_cast<const WalkNode *>(d_records), nrec, reinterpret_cast<const float4 *>(d_bodies4),
-                        d_targets4, (int)nt, (float)(eps * eps), leaf_size, d_acc4, d_work, h->flags, dfr, true, s);
+                        d_targets4, (int)nt, (float)(eps * eps), leaf_size, d_acc4, d_work, h->flags, dfr, true, s,
+                        perm);
   h->tend(s);
   h->launches += 1;
   BH_LAUNCHED();

@@ -233,6 +233,8 @@ void launch_walk_f32(const WalkNode *T, int64_t nrec_max, const float4 *bodies, 
 // Morton keys (perm: chunk-local permutation of [0, nt), for the walk's
 // tperm); BH_WALK_HILBERT=0 disables
 void launch_hilbert_chunks(const uint64_t *mkeys, int64_t nt, uint32_t *perm, cudaStream_t s);
+// the same from target positions (fp32 quantisation with the handle's R)
+void launch_hilbert_chunks_pos(const float4 *pos, int64_t nt, const double *dR, uint32_t *perm, cudaStream_t s);
 bool walk_hilbert_enabled();
 // deferred walk (LET overlap): pass A appends (target chunk, record, m0, m1) to
 // out[cap] for records flagged in d.w; pass B (resume) walks in[nin] with
@@ -247,7 +249,8 @@ struct DeferArgs {
 };
 void launch_walk_defer_f32(const WalkNode *T, int64_t nrec_max, const float4 *bodies, const float *targets, int nt,
                            float e2, int leaf, float *acc, int *work32, DeviceFlags *f, const DeferArgs &dfr,
-                           bool resume, cudaStream_t s);
+                           bool resume, cudaStream_t s,
+                           const uint32_t *tperm = nullptr);
 void launch_walk_f64(const WalkParams &p, const double4 *cm64, const double *q64,
                      const int4 *link, const double4 *bodies, const double *targets,
                      int tstride, const uint32_t *tperm, double *acc, int astride,

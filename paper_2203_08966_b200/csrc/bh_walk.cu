@@ -1679,8 +1679,27 @@ constexpr int kHilPer = kHilChunk / kHilThreads;
 #ifndef BH_HIL_MINB
 #define BH_HIL_MINB 2
 #endif
+__device__ __forceinline__ uint64_t hil_spread(uint64_t v) {  // 21 bits -> every third bit
+  v &= 0x1fffffull;
+  v = (v | v << 32) & 0x1f00000000ffffull;
+  v = (v | v << 16) & 0x1f0000ff0000ffull;
+  v = (v | v << 8) & 0x100f00f00f00f00full;
+  v = (v | v << 4) & 0x10c30c30c30c30c3ull;
+  v = (v | v << 2) & 0x1249249249249249ull;
+  return v;
+}
+// Morton key of a target from its position (targets without tree keys: the
+// distributed walk's caller arrays); only the order matters, fp32 quantisation
+__device__ __forceinline__ uint64_t morton_of_pos(const float4 p, const double *dR) {
+  const double R = *dR;
+  const float inv = (float)((double)(1 << 21) / (2.0 * R)), fR = (float)R;
+  const auto q = [&](float v) { return (uint64_t)fminf(fmaxf(floorf((v + fR) * inv), 0.f), 2097151.f); };
+  return hil_spread(q(p.x)) << 2 | hil_spread(q(p.y)) << 1 | hil_spread(q(p.z));
+}
 __global__ void __launch_bounds__(kHilThreads, BH_HIL_MINB) k_hilbert_chunks(const uint64_t *__restrict__ mkeys, int nt,
-                                                                uint32_t *__restrict__ perm) {
+                                                                uint32_t *__restrict__ perm,
+                                                                const float4 *__restrict__ pos = nullptr,
+                                                                const double *__restrict__ dR = nullptr) {
   __shared__ uint32_t sv[kHilChunk];
   __shared__ uint8_t tab[24 * 8];
   __shared__ uint64_t smin[32], smax[32];
@@ -1695,7 +1714,7 @@ __global__ void __launch_bounds__(kHilThreads, BH_HIL_MINB) k_hilbert_chunks(con
     const int e = BH_HIL_RADIX ? w * 128 + 32 * r + lane : tid + kHilThreads * r;  // element of item r
     h[r] = 0;
     if (c0 + e < nt) {
-      const uint64_t m = mkeys[c0 + e];
+      const uint64_t m = mkeys ? mkeys[c0 + e] : morton_of_pos(pos[c0 + e], dR);
       uint64_t k = 0;
       int st = 0;
 #pragma unroll
@@ -1885,6 +1904,11 @@ void launch_hilbert_chunks(const uint64_t *mkeys, int64_t nt, uint32_t *perm, cu
   if (nt <= 0) return;
   k_hilbert_chunks<<<(unsigned)((nt + kHilChunk - 1) / kHilChunk), kHilThreads, 0, s>>>(mkeys, (int)nt, perm);
 }
+void launch_hilbert_chunks_pos(const float4 *pos, int64_t nt, const double *dR, uint32_t *perm, cudaStream_t s) {
+  if (nt <= 0) return;
+  k_hilbert_chunks<<<(unsigned)((nt + kHilChunk - 1) / kHilChunk), kHilThreads, 0, s>>>(nullptr, (int)nt, perm,
+                                                                                       pos, dR);
+}
 
 bool walk_hilbert_enabled() {  // BH_WALK_HILBERT=0: Morton-consecutive warps
   static int on = -1;
@@ -1919,20 +1943,20 @@ void launch_peer_scatter(const void *acc, size_t row_bytes, const int *work, int
 
 void launch_walk_defer_f32(const WalkNode *T, int64_t nrec_max, const float4 *bodies, const float *targets, int nt,
                            float e2, int leaf, float *acc, int *work32, DeviceFlags *f, const DeferArgs &dfr,
-                           bool resume, cudaStream_t s) {
+                           bool resume, cudaStream_t s, const uint32_t *tperm) {
   if (nt <= 0) return;
   if (walk9_enabled() && nrec_max < (int64_t(1) << kW9NcShift)) {
     if (resume)
-      launch_walk9_mode<kWalkResume>(T, bodies, targets, 4, nullptr, nt, e2, leaf, acc, 4, nullptr, work32, f, dfr,
+      launch_walk9_mode<kWalkResume>(T, bodies, targets, 4, tperm, nt, e2, leaf, acc, 4, nullptr, work32, f, dfr,
                                      s);
     else
-      launch_walk9_mode<kWalkDefer>(T, bodies, targets, 4, nullptr, nt, e2, leaf, acc, 4, nullptr, work32, f, dfr, s);
+      launch_walk9_mode<kWalkDefer>(T, bodies, targets, 4, tperm, nt, e2, leaf, acc, 4, nullptr, work32, f, dfr, s);
     return;
   }
   if (resume)
-    launch_walk_mode<kWalkResume>(T, bodies, targets, 4, nullptr, nt, e2, leaf, acc, 4, nullptr, work32, f, dfr, s);
+    launch_walk_mode<kWalkResume>(T, bodies, targets, 4, tperm, nt, e2, leaf, acc, 4, nullptr, work32, f, dfr, s);
   else
-    launch_walk_mode<kWalkDefer>(T, bodies, targets, 4, nullptr, nt, e2, leaf, acc, 4, nullptr, work32, f, dfr, s);
+    launch_walk_mode<kWalkDefer>(T, bodies, targets, 4, tperm, nt, e2, leaf, acc, 4, nullptr, work32, f, dfr, s);
 }
 
 }  // namespace bh
