@@ -218,6 +218,9 @@ def run_ours(args, cfg) -> dict | None:
     backend = os.environ.get("BH_DIST_BACKEND", "nccl")
     if os.environ.get("BH_SHARE_GPU") == "1":
         local = 0
+    elif local >= torch.cuda.device_count():
+        raise SystemExit(f"rank {rank}: --gpus {ws} needs {ws} visible GPUs, found {torch.cuda.device_count()} "
+                         "(BH_SHARE_GPU=1 BH_DIST_BACKEND=gloo runs the ranks on one GPU as a smoke test)")
     torch.cuda.set_device(local)
     if ws > 1:
         if backend == "nccl":
