@@ -37,7 +37,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-AUTO_DISTRIBUTED_N = 5_000_000  # --decomp auto: distributed build from this many bodies
+AUTO_DISTRIBUTED_N = 30_000_000  # --decomp auto: distributed build from this many bodies
 
 CONFIGS = {
     "cfg1": dict(n=100_000, seed=1, theta=0.5, eps=1e-3, leaf=16, dt=1e-3, kind="plummer"),

@@ -43,7 +43,7 @@ ALGORITHM_NAMES = {  # simulation.py:64-73
 
 LEAF_MODES = ("reference", "bucket")
 DECOMPOSITIONS = ("auto", "replicated", "distributed")
-AUTO_DISTRIBUTED_N = 5_000_000
+AUTO_DISTRIBUTED_N = 30_000_000  # replicated below ("Which scheme runs")
 
 
 @dataclass(frozen=True)
