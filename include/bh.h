@@ -106,6 +106,11 @@ int bh_build_f32(bh_handle *h, const float *d_pos4_sorted, int64_t n, const doub
 int bh_build_f64(bh_handle *h, const double *d_pos3_sorted, const double *d_mass_sorted,
                  int64_t n, const double *d_R, void *stream);
 int bh_tree_size(bh_handle *h, int64_t *n_cells);
+/* Sync-free variant for multi-rank steps: d_out[0] = 1 if the last sync-free
+ * build fits its cell capacity, else 0 (call bh_tree_size to grow the capacity
+ * and build again).  Lets a caller fold the check into one host read with its
+ * own device values (the replicated step reads it with its costzones cuts). */
+int bh_sim_tree_fits_dev(bh_handle *h, int32_t *d_out, void *stream);
 /* Bucket-mode extension: bodies with identical Morton keys share
  * one level-21 cell that is resolved body by body, instead of the reference's
  * "tree resolution" error (hashed.py:477-482).  Off by default for

@@ -33,7 +33,7 @@ BH_FP64 = 1
 EXPORTS = (
     "bh_create", "bh_destroy", "bh_last_error", "bh_version", "bh_check",
     "bh_bounds_f32", "bh_bounds_f64", "bh_morton_f32", "bh_morton_f64", "bh_sort", "bh_scan_u32",
-    "bh_build_f32", "bh_build_f64", "bh_tree_size", "bh_set_allow_duplicates", "bh_export_tree",
+    "bh_build_f32", "bh_build_f64", "bh_tree_size", "bh_sim_tree_fits_dev", "bh_set_allow_duplicates", "bh_export_tree",
     "bh_traverse_f32", "bh_traverse_f64", "bh_kick_f32", "bh_drift_f32",
     "bh_kick_f64", "bh_drift_f64", "bh_direct_f64", "bh_potential_f64",
     "bh_sim_load", "bh_sim_forces", "bh_sim_step", "bh_sim_store", "bh_stats_get",
@@ -91,6 +91,7 @@ def _declare(L: ctypes.CDLL) -> None:
         "bh_build_f32": ([P, P, I64, P, P], I),
         "bh_build_f64": ([P, P, P, I64, P, P], I),
         "bh_tree_size": ([P, ctypes.POINTER(I64)], I),
+        "bh_sim_tree_fits_dev": ([P, P, P], I),
         "bh_set_allow_duplicates": ([P, I], I),
         "bh_export_tree": ([P] + [P] * 9 + [P], I),
         "bh_traverse_f32": ([P, P, I64, D, D, I, P, P, P], I),

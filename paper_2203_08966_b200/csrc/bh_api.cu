@@ -902,6 +902,24 @@ int bh_tree_size(bh_handle *h, int64_t *n_cells) {
   return BH_OK;
 }
 
+__global__ void k_tree_fits(const int *dC, int64_t cap, int32_t *out) { out[0] = *dC <= cap ? 1 : 0; }
+
+int bh_sim_tree_fits_dev(bh_handle *h, int32_t *d_out, void *stream) {
+  if (!h || !d_out) return fail(BH_BAD_ARG, "bh_sim_tree_fits_dev: bad args");
+  if (h->tree_n < 0) return fail(BH_NO_TREE, "no tree has been built");
+  cudaStream_t s = S(stream);
+  if (!h->async_tree) {
+    const int32_t one = 1;
+    BH_CUDA(cudaMemcpyAsync(d_out, &one, sizeof(one), cudaMemcpyHostToDevice, s));
+    BH_CUDA(cudaStreamSynchronize(s));  // (the host source is on the stack)
+    return BH_OK;
+  }
+  k_tree_fits<<<1, 1, 0, s>>>(h->dCtrue, h->C, d_out);
+  h->launches += 1;
+  BH_LAUNCHED();
+  return BH_OK;
+}
+
 int bh_export_tree(bh_handle *h, uint64_t *d_key, int8_t *d_level, double *d_centre,
                    double *d_side, double *d_mass, double *d_com, double *d_quad,
                    int64_t *d_count, int32_t *d_children, void *stream) {

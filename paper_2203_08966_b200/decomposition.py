@@ -60,18 +60,27 @@ def costzones(works, zones: int) -> np.ndarray:
     return np.concatenate(([0], cuts, [n])).astype(np.int64)
 
 
-def costzones_device(works: torch.Tensor, zones: int) -> list[int]:
-    """``costzones`` on a device work array (same rule, integer-exact: the
-    zone targets k*total/zones are compared as prefix*zones >= k*total)."""
+def costzones_cuts(works: torch.Tensor, zones: int) -> torch.Tensor:
+    """``costzones`` on a device work array, left on the device: the zones+1
+    boundaries [0, c_1, ..., n] as an int64 tensor (same rule, integer-exact:
+    the zone targets k*total/zones are compared as prefix*zones >= k*total)."""
     n = works.shape[0]
     if zones > n:
         raise ValueError(f"cannot cut {n} bodies into {zones} zones")
+    dev = works.device
+    if n == 0:
+        return torch.zeros(zones + 1, dtype=torch.int64, device=dev)
     prefix = torch.cumsum(works.to(torch.int64), 0)
-    total = int(prefix[-1].item()) if n else 0
     scaled = prefix * zones
-    t = torch.arange(1, zones, device=works.device, dtype=torch.int64) * total
+    t = torch.arange(1, zones, device=dev, dtype=torch.int64) * prefix[-1]
     cuts = torch.searchsorted(scaled, t, side="left") + 1
-    return [0] + [int(c) for c in cuts.tolist()] + [n]
+    ends = torch.tensor([0, n], dtype=torch.int64, device=dev)
+    return torch.cat([ends[:1], cuts, ends[1:]])
+
+
+def costzones_device(works: torch.Tensor, zones: int) -> list[int]:
+    """``costzones`` on a device work array (one host read)."""
+    return [int(c) for c in costzones_cuts(works, zones).tolist()]
 
 
 # --------------------------------------------------------------- collectives
@@ -310,13 +319,26 @@ class DistributedSim:
             self.eng.sim_prepare(p.theta, p.eps, p.leaf_size, bounds_ready)
             # a build that overflowed its cell capacity is redone before any walk
             # (the walk would store its rows into the peers); replicas build the
-            # same tree, so every rank takes the same branch
-            if not hasattr(self.eng, "sim_tree_fits") or self.eng.sim_tree_fits():
+            # same tree, so every rank takes the same branch.  The capacity check
+            # and this step's costzones cuts come back in ONE host read.
+            if hasattr(self.eng, "sim_tree_fits_dev"):
+                _, _, prev = self._bufs()
+                self.eng.sim_export(_lib.BH_SIM_PREV_WORK, 0, self.n, prev)
+                if getattr(self, "_fit", None) is None:
+                    self._fit = torch.zeros(1, dtype=torch.int32, device=self.eng.device)
+                self.eng.sim_tree_fits_dev(self._fit)
+                host = torch.cat([self._fit.to(torch.int64), costzones_cuts(prev, self.comm.size)]).tolist()
+                if host[0]:
+                    self.zones = [int(c) for c in host[1:]]
+                    break
+                self.eng.sim_tree_fits()  # overflowed: grow the capacity, build again
+            elif not hasattr(self.eng, "sim_tree_fits") or self.eng.sim_tree_fits():
+                self._zone()
                 break
             bounds_ready = False
         else:
             raise RuntimeError("tree cell capacity kept overflowing")
-        b, e = self._zone()
+        b, e = self.zones[self.comm.rank], self.zones[self.comm.rank + 1]
         if getattr(self, "p2p", False):
             self.comm.stream_barrier()  # every rank is done reading its acc (the kick)
             self.eng.sim_walk_range(p.theta, p.eps, p.leaf_size, b, e, record_work)  # + peers' rows
@@ -365,8 +387,8 @@ class DistributedSim:
             self.eng.sim_begin_step(self.p.dt)
             self._forces(record_work=True, bounds_ready=True)
             self.eng.sim_end_step(self.p.dt)
-            if hasattr(self.eng, "check"):
-                self.eng.check()  # latched device errors (incl. tree-capacity overflow)
+        if hasattr(self.eng, "check"):
+            self.eng.check()  # latched device errors, once per call (capacity: checked per step above)
 
     def store(self, pos=None, vel=None, acc=None, work=None) -> None:
         self.eng.sim_store(pos, vel, acc, work)

@@ -234,6 +234,12 @@ class Engine:
         check(self._L.bh_sim_prepare(self._h, float(theta), float(eps), int(leaf_size),
                                      int(bool(bounds_ready)), self.stream))
 
+    def sim_tree_fits_dev(self, out: torch.Tensor) -> None:
+        """Sync-free: out[0] (int32, device) = 1 if the last sync-free build fit
+        its cell capacity, else 0 (then ``sim_tree_fits`` grows it)."""
+        assert out.dtype == torch.int32 and out.is_cuda
+        check(self._L.bh_sim_tree_fits_dev(self._h, ctypes.c_void_p(out.data_ptr()), self.stream))
+
     def sim_tree_fits(self) -> bool:
         """After sim_prepare: False if the sync-free build overflowed its cell
         capacity (the capacity is grown; prepare again).  One host sync."""
