@@ -936,6 +936,9 @@ constexpr int kW9NcShift = 28;  // frontier entry: first_child | nchild << 28, u
 #ifndef BH_W9_PPPACK
 #define BH_W9_PPPACK 1  // pp drain: buckets with disjoint lane sets share a pass (see flush_pp)
 #endif
+#ifndef BH_W9_PPPIPE
+#define BH_W9_PPPIPE 0  // 1, 2: pp passes load the next (two) pair(s) of bodies first (measured 3-4% slower)
+#endif
 #ifndef BH_W9_PPSORT
 #define BH_W9_PPSORT 0  // pp drain: pack the buckets longest first (CPU model: 0.64 -> 0.55 of the broadcast iterations)
 #endif
@@ -1251,12 +1254,35 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
           u0 = (unsigned)en.z & bit;
           u1 = (unsigned)en.w & bit;
         }
+#if BH_W9_PPPIPE == 2
+        const float4 *bp = bodies + lo;  // two pairs ahead
+        float4 c0 = bp[0], c1 = bp[1 < cnt ? 1 : 0], n0 = bp[2 < cnt ? 2 : 0], n1 = bp[3 < cnt ? 3 : 0];
+        for (int j = 0; j < len; j += 2) {
+          const float4 m0 = bp[j + 4 < cnt ? j + 4 : 0], m1 = bp[j + 5 < cnt ? j + 5 : 0];
+          pp_body(c0, u0 && j < cnt, u1 && j < cnt);
+          pp_body(c1, u0 && j + 1 < cnt && j + 1 < len, u1 && j + 1 < cnt && j + 1 < len);
+          c0 = n0; c1 = n1; n0 = m0; n1 = m1;
+        }
+#elif BH_W9_PPPIPE
+        // software-pipelined: the next pair of bodies is loaded before the
+        // current pair is evaluated (the loop was bound by the load latency)
+        const float4 *bp = bodies + lo;
+        float4 c0 = bp[0 < cnt ? 0 : 0], c1 = bp[1 < cnt ? 1 : 0];
+        for (int j = 0; j < len; j += 2) {
+          const float4 n0 = bp[j + 2 < cnt ? j + 2 : 0], n1 = bp[j + 3 < cnt ? j + 3 : 0];
+          pp_body(c0, u0 && j < cnt, u1 && j < cnt);
+          pp_body(c1, u0 && j + 1 < cnt && j + 1 < len, u1 && j + 1 < cnt && j + 1 < len);
+          c0 = n0;
+          c1 = n1;
+        }
+#else
 #pragma unroll(kBucketUnroll)
         for (int j = 0; j < len; ++j) {
           const bool v = j < cnt;
           const float4 bb = bodies[v ? lo + j : lo];
           pp_body(bb, u0 && v, u1 && v);
         }
+#endif
       }
       __syncwarp();
       k0 = k;
