@@ -1410,7 +1410,10 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
     if (BH_W9_CHECK && (sp + __popc(bfr) + __popc(bmx) > kW9Fcap ||
         gsp + sp + __popc(bfr) + __popc(bmx) > kW9Frontier || npc + __popc(bpc) > kW9List ||
         npp + __popc(bpp) + __popc(bmx) > kW9PpList)) {
-      if (lane == 0) atomicOr(&f->bits, FLAG_WALK_BOUNDS);
+      if (lane == 0) {
+        atomicOr(&f->bits, FLAG_WALK_BOUNDS);
+        if (slot >= 0) atomicAnd(spl.bits + (slot >> 5), ~(1u << (slot & 31)));  // never leak a spill slot
+      }
       return;
     }
     if (to_pp) S.pp[npp + __popc(bpp & lt)] = d.y == 1 ? make_int4(cell, 0, (int)m0, (int)m1)
