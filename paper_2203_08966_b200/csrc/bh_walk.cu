@@ -1527,16 +1527,22 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
       if (work64) atomicAdd((unsigned long long *)(work64 + s1), (unsigned long long)(pp1 + 2 * pc1));
     }
   } else {
+    // rows of 4 floats (the resident layout): one 16-byte store per row, so a
+    // peer's row travels as one NVLink write (w = 0; nothing reads it)
+    const bool row4 = astride == 4;
+    const float4 r0 = make_float4(AX.x, AY.x, AZ.x, 0.f), r1 = make_float4(AX.y, AY.y, AZ.y, 0.f);
     if (v0) {
       float *o = acc + s0 * astride;
-      o[0] = AX.x; o[1] = AY.x; o[2] = AZ.x;
+      if (row4) *reinterpret_cast<float4 *>(o) = r0;
+      else { o[0] = AX.x; o[1] = AY.x; o[2] = AZ.x; }
       const int w = pp0 + 2 * pc0;  // WORK_PP, WORK_PC (octree.py:23-25)
       if (work64) work64[s0] = w;
       if (work32) work32[s0] = w;
     }
     if (v1) {
       float *o = acc + s1 * astride;
-      o[0] = AX.y; o[1] = AY.y; o[2] = AZ.y;
+      if (row4) *reinterpret_cast<float4 *>(o) = r1;
+      else { o[0] = AX.y; o[1] = AY.y; o[2] = AZ.y; }
       const int w = pp1 + 2 * pc1;
       if (work64) work64[s1] = w;
       if (work32) work32[s1] = w;
@@ -1548,12 +1554,14 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
       if (r >= peers.n) break;
       if (v0) {
         float *o = peers.acc[r] + s0 * astride;
-        o[0] = AX.x; o[1] = AY.x; o[2] = AZ.x;
+        if (row4) *reinterpret_cast<float4 *>(o) = r0;
+        else { o[0] = AX.x; o[1] = AY.x; o[2] = AZ.x; }
         if (work32 && peers.work[r]) peers.work[r][s0] = pp0 + 2 * pc0;
       }
       if (v1) {
         float *o = peers.acc[r] + s1 * astride;
-        o[0] = AX.y; o[1] = AY.y; o[2] = AZ.y;
+        if (row4) *reinterpret_cast<float4 *>(o) = r1;
+        else { o[0] = AX.y; o[1] = AY.y; o[2] = AZ.y; }
         if (work32 && peers.work[r]) peers.work[r][s1] = pp1 + 2 * pc1;
       }
     }
