@@ -425,13 +425,25 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit_mark(TreeView t, const fl
       }
     }
   }
-  // densely list the creators (one atomic per warp)
+  // densely list the creators: one global atomic per block (one per warp was
+  // ~300K same-address atomics at 1e7 bodies, serialised in L2)
+  __shared__ int wcnt[kEmitThreads / 32];
+  __shared__ int bbase;
   const unsigned m = __ballot_sync(0xffffffffu, creator);
-  const unsigned lane = threadIdx.x & 31;
-  int wbase = 0;
-  if (lane == 0 && m) wbase = atomicAdd(ncreators, __popc(m));
-  wbase = __shfl_sync(0xffffffffu, wbase, 0);
-  if (creator) creators[wbase + __popc(m & ((1u << lane) - 1u))] = (int)i;
+  const unsigned lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) wcnt[w] = __popc(m);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int tot = 0;
+    for (int q = 0; q < kEmitThreads / 32; ++q) {
+      const int c = wcnt[q];
+      wcnt[q] = tot;
+      tot += c;
+    }
+    bbase = tot ? atomicAdd(ncreators, tot) : 0;
+  }
+  __syncthreads();
+  if (creator) creators[bbase + wcnt[w] + __popc(m & ((1u << lane) - 1u))] = (int)i;
 }
 
 __global__ void __launch_bounds__(128) k_emit_create(TreeView t, const float4 *__restrict__ bod32,
