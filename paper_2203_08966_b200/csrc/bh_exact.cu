@@ -406,13 +406,15 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit_mark(TreeView t, const fl
         t.cm64[0] = make_double4(v.x, v.y, v.z, v.w);
       }
     }
-    const int lp = i > 0 ? t.lcp[i - 1] : -1;
-    const int ln = i + 1 < n ? t.lcp[i] : -1;
+    // lcp with the neighbours from the staged keys (= t.lcp, hashed.py:376-388)
+    const int lp = i > 0 ? lcp_of(ks[li - 1], ks[li]) : -1;
+    const int ln = i + 1 < n ? lcp_of(ks[li], ks[li + 1]) : -1;
     int depth = min((lp > ln ? lp : ln) + 1, kMaxLevel);
     if (i == 0 && t.bnd_prev >= 0) depth = max(depth, min(t.bnd_prev + 1, kMaxLevel));
     if (i == n - 1 && t.bnd_next >= 0) depth = max(depth, min(t.bnd_next + 1, kMaxLevel));
     const int start = i > 0 ? lp : 0;
     int maxw = -1;
+#pragma unroll 4
     for (int a = li - L; a <= li; ++a) maxw = max(maxw, (int)ws[a]);
     creator = n > 1 && (start == 0 || start <= maxw);
     if (creator) {  // the rows of the opened cells this body creates: all slots absent
