@@ -298,6 +298,12 @@ int bh_timing_get(bh_handle *h, double *ms_out, int nphases);
 /* FP32 FFMA throughput microbenchmark (the roofline denominator for the walk):
  * runs a dependent-chain-free FFMA loop on every SM, returns TFLOP/s. */
 int bh_ffma_peak(bh_handle *h, double *tflops_out, void *stream);
+/* Page-lock (pin) a caller's host array in place so that copies to and from it
+ * run at full PCIe rate (the reference's numpy Bodies arrays, integrator.py:47-58
+ * through TreeForces); bh_host_unregister undoes it.  Thin wrappers of
+ * cudaHostRegister / cudaHostUnregister. */
+int bh_host_register(void *p, int64_t bytes);
+int bh_host_unregister(void *p);
 /* The same loop in fp64 (DFMA): the roofline denominator of the fp64 walk. */
 int bh_dfma_peak(bh_handle *h, double *tflops_out, void *stream);
 

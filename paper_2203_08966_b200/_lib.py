@@ -44,7 +44,7 @@ EXPORTS = (
     "bh_sim_build_local", "bh_sim_branch_export", "bh_sim_walk_records", "bh_walk_records_f32",
     "bh_sim_let", "bh_sim_let_pack", "bh_sim_target_boxes", "bh_sim_step_host",
     "bh_walk_records_defer_f32", "bh_walk_records_resume_f32",
-    "bh_timing_enable", "bh_timing_reset", "bh_timing_get", "bh_ffma_peak", "bh_dfma_peak",
+    "bh_timing_enable", "bh_timing_reset", "bh_timing_get", "bh_ffma_peak", "bh_dfma_peak", "bh_host_register", "bh_host_unregister",
     "bh_ic_plummer", "bh_host_potential_pairs", "bh_top_tree",
 )
 BH_SIM_ACC, BH_SIM_WORK, BH_SIM_PREV_WORK, BH_SIM_POS, BH_SIM_VEL, BH_SIM_ID, BH_SIM_KEYS = range(7)
@@ -137,6 +137,8 @@ def _declare(L: ctypes.CDLL) -> None:
         "bh_timing_reset": ([P], I),
         "bh_timing_get": ([P, ctypes.POINTER(D), I], I),
         "bh_ffma_peak": ([P, ctypes.POINTER(D), P], I),
+        "bh_host_register": ([P, I64], I),
+        "bh_host_unregister": ([P], I),
         "bh_dfma_peak": ([P, ctypes.POINTER(D), P], I),
         "bh_ic_plummer": ([P, I64, I64, D, P, P, ctypes.POINTER(I64)], I64),
         "bh_host_potential_pairs": ([P, P, I64, D], D),

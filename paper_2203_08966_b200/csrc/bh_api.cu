@@ -1938,6 +1938,17 @@ static int fma_peak(bh_handle *h, bool fp64, double *tflops_out, void *stream) {
   *tflops_out = flops / (ms * 1e-3) / 1e12;
   return BH_OK;
 }
+int bh_host_register(void *p, int64_t bytes) {
+  if (!p || bytes <= 0) return fail(BH_BAD_ARG, "bh_host_register: bad args");
+  BH_CUDA(cudaHostRegister(p, (size_t)bytes, cudaHostRegisterDefault));
+  return BH_OK;
+}
+int bh_host_unregister(void *p) {
+  if (!p) return fail(BH_BAD_ARG, "bh_host_unregister: bad args");
+  BH_CUDA(cudaHostUnregister(p));
+  return BH_OK;
+}
+
 int bh_ffma_peak(bh_handle *h, double *tflops_out, void *stream) {
   if (!h || !tflops_out) return fail(BH_BAD_ARG, "bh_ffma_peak: bad args");
   return fma_peak(h, false, tflops_out, stream);
