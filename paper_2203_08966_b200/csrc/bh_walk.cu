@@ -1565,6 +1565,9 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
         if (work32 && peers.work[r]) peers.work[r][s1] = pp1 + 2 * pc1;
       }
     }
+    // the peers read these rows after the stream barrier that follows this
+    // kernel: make the remote stores visible system-wide first
+    if (peers.n > 0) __threadfence_system();
   }
   if (slot >= 0 && lane == 0) atomicAnd(spl.bits + (slot >> 5), ~(1u << (slot & 31)));
   const unsigned spp = __reduce_add_sync(FULL, (unsigned)(pp0 + pp1));
@@ -1961,10 +1964,12 @@ bool walk_hilbert_enabled() {  // BH_WALK_HILBERT=0: Morton-consecutive warps
 __global__ void k_peer_scatter(const int4 *__restrict__ src, int64_t n16, int4 *__restrict__ dst) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += (int64_t)gridDim.x * blockDim.x)
     dst[i] = src[i];
+  __threadfence_system();  // visible to the peer before the barrier that follows
 }
 __global__ void k_peer_scatter_i32(const int *__restrict__ src, int64_t n, int *__restrict__ dst) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     dst[i] = src[i];
+  __threadfence_system();
 }
 void launch_peer_scatter(const void *acc, size_t row_bytes, const int *work, int64_t nt, const W9Peers &p,
                          cudaStream_t s) {
