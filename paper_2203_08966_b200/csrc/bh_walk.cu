@@ -40,6 +40,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstddef>
 #include <cstdlib>
 #include <cooperative_groups.h>
 
@@ -928,6 +929,17 @@ constexpr int kW9Block = BH_W9_BLOCK;
 #define BH_W9_PCUNROLL 4
 #endif
 constexpr int kW9PcUnroll = BH_W9_PCUNROLL;
+#ifndef BH_W9_HALVES
+#define BH_W9_HALVES 0  // 1: lane l holds targets (l, l + 32) instead of (2l, 2l + 1); see k_walk9 (measured 1% slower)
+#endif
+#ifndef BH_W9_PPSTAGE
+#define BH_W9_PPSTAGE 0  // 1: pp drain with each pass's bucket bodies staged in shared memory by cp.async.bulk (measured 1% slower)
+#endif
+#ifndef BH_W9_PPUNROLL
+#define BH_W9_PPUNROLL 4  // staged pp passes: body loop unroll (the bodies are LDS reads)
+#endif
+constexpr int kW9PpUnroll = BH_W9_PPUNROLL;
+constexpr int kW9StageF4 = 128;  // BH_W9_PPSTAGE: bodies per staging buffer (2 KB)
 constexpr int kW9NcShift = 28;  // frontier entry: first_child | nchild << 28, unsigned (records < 2^28)
 
 #ifndef BH_W9_PC30
@@ -942,9 +954,6 @@ constexpr int kW9NcShift = 28;  // frontier entry: first_child | nchild << 28, u
 #ifndef BH_W9_PPSORT
 #define BH_W9_PPSORT 0  // pp drain: pack the buckets longest first (CPU model: 0.64 -> 0.55 of the broadcast iterations)
 #endif
-#ifndef BH_W9_BULK
-#define BH_W9_BULK 0  // 1: accepted records reach shared memory by cp.async.bulk (mbarrier-completed)
-#endif
 #ifdef BH_W9_STATS
 // diagnostics (-DBH_W9_STATS): per-warp schedule counters summed over the launch
 //  0 batches  1 cells classified  2 mixed  3 mixed with an accepting target
@@ -952,6 +961,8 @@ constexpr int kW9NcShift = 28;  // frontier entry: first_child | nchild << 28, u
 //  8 pp bucket entries  9 pp passes  10 pass body iterations  11 bucket (target, body) slots used
 //  12 frontier pushes (certain-open)  13 pc flushes  14 pp flushes  15 mixed opened (pushed / bucket)
 //  16 mixed accepting target bits  17 bucket entries' mask bits
+//  18 pc entries of one half (scalar drain)  19 mixed cells accepted by one half only
+//  20 pp passes of one half  21 their body iterations
 __device__ unsigned long long g_w9_stats[64];  // [32, 64): histogram of the warp's peak frontier depth / 10
 extern "C" int bh_debug_w9_stats(unsigned long long *out, int reset) {
   int e = (int)cudaMemcpyFromSymbol(out, g_w9_stats, sizeof(g_w9_stats));
@@ -966,9 +977,8 @@ extern "C" int bh_debug_w9_stats(unsigned long long *out, int reset) {
 #define W9S(i, v) ((void)0)
 #endif
 
-// cp.async.bulk (the bulk-copy / TMA engine) of one 48-byte record prefix into
-// shared memory, completing on a per-warp mbarrier.  The barrier expects one
-// arrival per phase (the flush) plus the bytes each copy announces.
+// cp.async.bulk (the bulk-copy / TMA engine) into shared memory, completing on
+// a per-warp mbarrier (BH_W9_PPSTAGE).
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -976,39 +986,38 @@ __device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
-__device__ __forceinline__ void bulk_copy_48(void *dst, const void *src, uint64_t *bar) {
-  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], 48;" ::"r"(smem_u32(bar)) : "memory");
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// one bulk copy (the TMA engine; SASS UBLKCP) of `bytes` (a multiple of 16, both
+// addresses 16-byte aligned) into shared memory, completing bytes on `bar`
+__device__ __forceinline__ void bulk_copy(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
   asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 48, [%2];" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(smem_u32(bar))
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
-// the flush: one arrival completes the phase once every announced byte landed
-__device__ __forceinline__ void mbar_arrive_wait(uint64_t *bar, unsigned &phase, bool arrive) {
-  if (arrive) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+// the phase's one arrival, announcing the bytes its copies will complete
+__device__ __forceinline__ void mbar_arrive_expect(uint64_t *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
   uint32_t done = 0;
   while (!done) {
     asm volatile(
         "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
         : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(phase)
+        : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
   }
-  phase ^= 1u;
 }
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // Per-warp shared memory (~7.4 KB).  Masks ride in record words the drains do
 // not read: a.w (mac2) and b.z (the duplicate qxy) of a staged pc record, b.z
-// and d.w (level) of a staged mixed record.  (BH_W9_BULK: the pc records are
-// bulk copies of the global records, so their masks sit in pcm.)
+// and d.w (level) of a staged mixed record.  The pc list has two ends: entries
+// with targets in both halves of the warp (mask0 and mask1 non-zero) fill it
+// from the bottom, entries of one half only from the top (see flush_pc).
 struct W9Warp {
   int fc[kW9Fcap];         // frontier (top): first_child | nchild << kW9NcShift
   uint2 fm[kW9Fcap];       //                 (mask0, mask1)
-#if BH_W9_BULK
-  uint64_t bar;            // completes the bulk copies of one flush
-  uint2 pcm[kW9List];      // masks of the staged pc records
-#endif
   float4 pcr[kW9List][3];  // accepted cells: a (mask0 in .w), b (mask1 in .z), c
   int4 pp[kW9PpList];      // pp: (lo, count, mask0, mask1) or a leaf record (cell, 0, ...)
 #if BH_W9_PPSORT
@@ -1021,7 +1030,18 @@ struct W9Warp {
     };
     uint8_t psel[32][32];  // pp drain (after the batch): entry + 1 of each lane in each pass
   };
+#if BH_W9_PPSTAGE
+  // pp drain: two staging buffers of kW9StageF4 bodies, one pass each.  Buffer 0
+  // is the (drained) pc list; buffer 1 the second half of the union above plus
+  // stg1 (which must follow it directly).
+  float4 stg1[kW9StageF4 - 64];
+  uint64_t sbar[2];        // one mbarrier per buffer
+#endif
 };
+#if BH_W9_PPSTAGE
+static_assert(sizeof(float4) * 3 * kW9List >= sizeof(float4) * kW9StageF4, "staging buffer 0 is the pc list");
+static_assert(offsetof(W9Warp, stg1) == offsetof(W9Warp, psel) + 2048, "staging buffer 1 spans the union's tail and stg1");
+#endif
 
 __device__ __forceinline__ float w9_shfl_min(float v) {
 #pragma unroll
@@ -1057,7 +1077,18 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
     entry = dfr.in[gwarp];
   }
   const int64_t warp = MODE == kWalkResume ? (int64_t)entry.x : gwarp;
+#if BH_W9_HALVES
+  // lane l holds targets l and l + 32 of the warp's 64: the .x and .y halves of
+  // the packed math are then the two spatial halves of the group (targets are
+  // in curve order), and 17% of the pc entries (6% with the interleaved
+  // mapping) are reached by targets of one half only and run as scalar FFMA.
+  // But sets of neighbouring targets then occupy twice the lanes, so the pp
+  // drain packs fewer buckets per pass (+20% body iterations at cfg3): 1% slower
+  // overall, off.
+  const int64_t t0 = warp * 64 + lane, t1 = t0 + 32;
+#else
   const int64_t t0 = warp * 64 + 2 * lane, t1 = t0 + 1;
+#endif
   const bool v0 = t0 < nt, v1 = t1 < nt;
   const int64_t s0 = v0 ? (tperm ? (int64_t)tperm[t0] : t0) : 0;
   const int64_t s1 = v1 ? (tperm ? (int64_t)tperm[t1] : t1) : 0;
@@ -1078,10 +1109,10 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
   const unsigned bit = 1u << lane;
   const unsigned lt = bit - 1u;
 
-  int sp = 1, npc = 0, npp = 0;
+  int sp = 1, npf = 0, nph = 0, npp = 0;  // pc entries (both halves / one half), pp entries
   int gsp = 0, slot = -1;  // spilled entries, spill slot (warp-uniform)
 #ifdef BH_W9_STATS
-  unsigned long long st[18] = {};
+  unsigned long long st[24] = {};
   int spmax = 0;
 #endif
   if (MODE == kWalkResume) {  // the deferred record's subtree, for the targets that opened it
@@ -1099,33 +1130,54 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
       S.fm[0] = make_uint2(m0, m1);
     }
   }
-#if BH_W9_BULK
-  unsigned bphase = 0;
-  if (lane == 0) mbar_init(&S.bar, 1);
+#if BH_W9_PPSTAGE
+  unsigned sphase = 0;  // bit b: the parity buffer b's barrier completes next
+  if (BUCKET && lane == 0) {
+    mbar_init(&S.sbar[0], 1);
+    mbar_init(&S.sbar[1], 1);
+  }
 #endif
   __syncwarp();
 
-  // dense pc over the list (the FP32-pipe work)
-  auto flush_pc = [&](int n) {
-    W9S(13, n > 0); W9S(4, n);
+  // one target's share of a pc entry: the scalar twin of the packed evaluation below
+  auto pc_tail = [&](const float4 b, const float4 q, bool u, float dx, float dy, float dz, float d2, float &ax,
+                     float &ay, float &az, int &cnt) {
+    const float r = u ? rsqrtf(d2) : 0.f;
+    const float r2 = __fmul_rn(r, r);
+    const float qx = __fmaf_rn(q.x, dz, __fmaf_rn(b.y, dy, __fmul_rn(b.x, dx)));
+    const float qy = __fmaf_rn(q.y, dz, __fmaf_rn(b.w, dy, __fmul_rn(b.y, dx)));
+    const float qz = __fmaf_rn(q.w, dz, __fmaf_rn(q.y, dy, __fmul_rn(q.x, dx)));
+    const float rqr = __fmaf_rn(dz, qz, __fmaf_rn(dy, qy, __fmul_rn(dx, qx)));
+    const float r5 = __fmul_rn(__fmul_rn(r2, r2), r);
+    const float v = __fmaf_rn(__fmul_rn(rqr, r2), -2.5f, __fmul_rn(-q.z, d2));
+    ax = __fmaf_rn(r5, __fmaf_rn(dx, v, qx), ax);
+    ay = __fmaf_rn(r5, __fmaf_rn(dy, v, qy), ay);
+    az = __fmaf_rn(r5, __fmaf_rn(dz, v, qz), az);
+    cnt += u;
+  };
+  auto pc_one = [&](const float4 a, const float4 b, const float4 q, bool u, float x, float y, float z, float &ax,
+                    float &ay, float &az, int &cnt) {
+    const float dx = __fadd_rn(x, a.x), dy = __fadd_rn(y, a.y), dz = __fadd_rn(z, a.z);
+    pc_tail(b, q, u, dx, dy, dz, __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx))), ax, ay, az, cnt);
+  };
+  // dense pc over the list (the FP32-pipe work): the entries [0, n) packed, two
+  // targets per lane; the nh one-half entries at the list's top as scalar FFMA
+  // on the half their targets are in
+  auto flush_pc = [&](int n, int nh) {
+    W9S(13, n + nh > 0); W9S(4, n + nh);
 #ifdef BH_W9_STATS
     for (int k = 0; k < n; ++k)
       W9S(5, __popc((unsigned)__float_as_int(S.pcr[k][0].w)) + __popc((unsigned)__float_as_int(S.pcr[k][1].z)));
-#endif
-#if BH_W9_BULK
-    mbar_arrive_wait(&S.bar, bphase, lane == 0);  // the staged records have landed
+    for (int k = kW9List - nh; k < kW9List; ++k)
+      W9S(5, __popc((unsigned)__float_as_int(S.pcr[k][0].w)) + __popc((unsigned)__float_as_int(S.pcr[k][1].z)));
+    W9S(18, nh);
 #endif
 #pragma unroll(kW9PcUnroll)
     for (int k = 0; k < n; ++k) {
       const float4 a = S.pcr[k][0];
       const float4 b = S.pcr[k][1];
       const float4 q = S.pcr[k][2];
-#if BH_W9_BULK
-      const uint2 mk = S.pcm[k];
-      const bool u0 = mk.x & bit, u1 = mk.y & bit;
-#else
       const bool u0 = (unsigned)__float_as_int(a.w) & bit, u1 = (unsigned)__float_as_int(b.z) & bit;
-#endif
       const float2 DX = __fadd2_rn(X, f2(a.x));
       const float2 DY = __fadd2_rn(Y, f2(a.y));
       const float2 DZ = __fadd2_rn(Z, f2(a.z));
@@ -1153,10 +1205,15 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
 #endif
       pc0 += u0; pc1 += u1;
     }
-#if BH_W9_BULK
-    __syncwarp();
-    fence_proxy_async();  // these reads precede the next bulk writes into the list
-#endif
+#pragma unroll 2
+    for (int k = kW9List - nh; k < kW9List; ++k) {
+      const float4 a = S.pcr[k][0];
+      const float4 b = S.pcr[k][1];
+      const float4 q = S.pcr[k][2];
+      const unsigned mk0 = (unsigned)__float_as_int(a.w), mk1 = (unsigned)__float_as_int(b.z);
+      if (mk0) pc_one(a, b, q, mk0 & bit, X.x, Y.x, Z.x, AX.x, AY.x, AZ.x, pc0);  // warp-uniform
+      else pc_one(a, b, q, mk1 & bit, X.y, Y.y, Z.y, AX.y, AY.y, AZ.y, pc1);
+    }
   };
   // dense pp over the bodies of the listed leaves / buckets (self skipped by r2 > 0)
   auto pp_body = [&](const float4 bb, bool u0, bool u1) {
@@ -1173,8 +1230,117 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
     AZ = __ffma2_rn(Sc, EZ, AZ);
     pp0 += m0; pp1 += m1;
   };
+  auto pp_one = [&](const float4 bb, bool u, float x, float y, float z, float &ax, float &ay, float &az, int &cnt) {
+    const float ex = __fsub_rn(x, bb.x), ey = __fsub_rn(y, bb.y), ez = __fsub_rn(z, bb.z);
+    const float q2 = __fmaf_rn(ez, ez, __fmaf_rn(ey, ey, __fmul_rn(ex, ex)));
+    const bool m = u && q2 > 0.f;
+    const float r = m ? rsqrtf(__fadd_rn(q2, e2)) : 0.f;
+    const float sc = __fmul_rn(__fmul_rn(r, r), __fmul_rn(r, -bb.w));
+    ax = __fmaf_rn(sc, ex, ax);
+    ay = __fmaf_rn(sc, ey, ay);
+    az = __fmaf_rn(sc, ez, az);
+    cnt += m;
+  };
   auto flush_pp = [&](int n) {
-#if BH_W9_PPPACK
+#if BH_W9_PPSTAGE
+    // As the packed drain below (buckets with disjoint lane sets share a pass),
+    // and the bodies of a pass reach shared memory by bulk copies (the TMA
+    // engine), one per bucket, issued a pass ahead into the other of two
+    // staging buffers: the body loop reads shared memory instead of waiting on
+    // a global load per cache line.  A pass holds at most kW9StageF4 bodies.
+    // The pc list is empty here (buffer 0 is its storage).  Lane p keeps pass
+    // p's used lanes, length and staged bodies; a packed entry's .y becomes
+    // count | buffer offset << 8.
+    W9S(14, n > 0);
+    int k0 = 0;
+    while (k0 < n) {
+      unsigned used = 0u;
+      int plen = 0, pf4 = 0, npass = 0, k = k0;
+      for (; k < n; ++k) {
+        const int4 en = S.pp[k];
+        const bool u0 = (unsigned)en.z & bit, u1 = (unsigned)en.w & bit;
+        if (en.y == 0) {  // leaf record: its com and mass are the body (a LET leaf has no body index here)
+          W9S(6, 1); W9S(7, __popc((unsigned)en.z) + __popc((unsigned)en.w));
+          const WalkNode *nd = T + en.x;
+          const float4 a = nd->a;
+          pp_body(make_float4(-a.x, -a.y, -a.z, nd->c.z), u0, u1);
+          continue;
+        }
+        if (!BUCKET) continue;
+        if (en.y > kW9StageF4) {  // a run of equal keys longer than a buffer: straight from global memory
+#pragma unroll(kBucketUnroll)
+          for (int j = en.x; j < en.x + en.y; ++j) pp_body(bodies[j], u0, u1);
+          continue;
+        }
+        W9S(8, 1); W9S(17, __popc((unsigned)en.z) + __popc((unsigned)en.w));
+        W9S(11, (unsigned long long)en.y * (__popc((unsigned)en.z) + __popc((unsigned)en.w)));
+        const unsigned lm = (unsigned)en.z | (unsigned)en.w;
+        // (a bucket every lane reads shares a pass with nothing: no search)
+        const unsigned fit = lm == FULL ? 0u :
+            __ballot_sync(FULL, (int)lane < npass && (used & lm) == 0u && pf4 + en.y <= kW9StageF4);
+        int p;
+        if (fit) {
+          p = __ffs(fit) - 1;
+        } else {
+          if (npass == 32) break;  // run these passes, then pack the rest
+          p = npass++;
+          S.psel[p][lane] = 0;
+        }
+        const int off = __shfl_sync(FULL, pf4, p);
+        if ((int)lane == p) {
+          used |= lm;
+          plen = max(plen, en.y);
+          pf4 += en.y;
+        }
+        if (lane == 0) S.pp[k].y = en.y | off << 8;
+        if ((lm >> lane) & 1u) S.psel[p][lane] = (uint8_t)(k + 1);
+      }
+      W9S(9, npass);
+      if (BUCKET && npass > 0) {
+        auto stage = [&](int b) { return b ? reinterpret_cast<float4 *>(&S.psel[0][0]) + 64 : &S.pcr[0][0]; };
+        // the bulk copies of pass p: the first lane of each bucket copies it
+        auto issue = [&](int p) {
+          __syncwarp();
+          fence_proxy_async();  // the buffer's earlier reads and writes precede the copies
+          const int e = (int)S.psel[p][lane] - 1;
+          uint64_t *bar = &S.sbar[p & 1];
+          if (e >= 0) {
+            const int4 en = S.pp[e];
+            if ((((unsigned)en.z | (unsigned)en.w) & lt) == 0u)
+              bulk_copy(stage(p & 1) + (en.y >> 8), bodies + en.x, (unsigned)(en.y & 255) * 16u, bar);
+          }
+          const int tot = __shfl_sync(FULL, pf4, p);
+          if (lane == 0) mbar_arrive_expect(bar, (unsigned)tot * 16u);
+        };
+        issue(0);
+        for (int p = 0; p < npass; ++p) {
+          if (p + 1 < npass) issue(p + 1);
+          const int len = __shfl_sync(FULL, plen, p);
+          W9S(10, len);
+          const int e = (int)S.psel[p][lane] - 1;
+          const float4 *sb = stage(p & 1);
+          int cnt = 0;
+          bool u0 = false, u1 = false;
+          if (e >= 0) {
+            const int4 en = S.pp[e];
+            sb += en.y >> 8;
+            cnt = en.y & 255;
+            u0 = (unsigned)en.z & bit;
+            u1 = (unsigned)en.w & bit;
+          }
+          mbar_wait(&S.sbar[p & 1], sphase >> (p & 1) & 1u);
+          sphase ^= 1u << (p & 1);
+#pragma unroll(kW9PpUnroll)
+          for (int j = 0; j < len; ++j) {
+            const bool v = j < cnt;
+            pp_body(sb[v ? j : 0], u0 && v, u1 && v);
+          }
+        }
+      }
+      __syncwarp();
+      k0 = k;
+    }
+#elif BH_W9_PPPACK
     // Leaf records one at a time (their body is the record); buckets packed:
     // greedy first-fit of the listed buckets into passes whose lane sets
     // (targets 2l, 2l+1 <-> lane l) do not overlap, so one pass over the
@@ -1224,7 +1390,7 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
         W9S(8, 1); W9S(17, __popc((unsigned)en.z) + __popc((unsigned)en.w));
         W9S(11, (unsigned long long)en.y * (__popc((unsigned)en.z) + __popc((unsigned)en.w)));
         const unsigned lm = (unsigned)en.z | (unsigned)en.w;
-        const unsigned fit = __ballot_sync(FULL, (int)lane < npass && (used & lm) == 0u);
+        const unsigned fit = lm == FULL ? 0u : __ballot_sync(FULL, (int)lane < npass && (used & lm) == 0u);
         int p;
         if (fit) {
           p = __ffs(fit) - 1;
@@ -1276,11 +1442,29 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
           c1 = n1;
         }
 #else
+        // a pass whose buckets are read by targets of one half only: scalar
+        const bool hx = __any_sync(FULL, u0), hy = __any_sync(FULL, u1);
+        if (hx && hy) {
 #pragma unroll(kBucketUnroll)
-        for (int j = 0; j < len; ++j) {
-          const bool v = j < cnt;
-          const float4 bb = bodies[v ? lo + j : lo];
-          pp_body(bb, u0 && v, u1 && v);
+          for (int j = 0; j < len; ++j) {
+            const bool v = j < cnt;
+            const float4 bb = bodies[v ? lo + j : lo];
+            pp_body(bb, u0 && v, u1 && v);
+          }
+        } else if (hx) {
+          W9S(20, 1); W9S(21, len);
+#pragma unroll(kBucketUnroll)
+          for (int j = 0; j < len; ++j) {
+            const bool v = j < cnt;
+            pp_one(bodies[v ? lo + j : lo], u0 && v, X.x, Y.x, Z.x, AX.x, AY.x, AZ.x, pp0);
+          }
+        } else {
+          W9S(20, 1); W9S(21, len);
+#pragma unroll(kBucketUnroll)
+          for (int j = 0; j < len; ++j) {
+            const bool v = j < cnt;
+            pp_one(bodies[v ? lo + j : lo], u1 && v, X.y, Y.y, Z.y, AX.y, AY.y, AZ.y, pp1);
+          }
         }
 #endif
       }
@@ -1408,7 +1592,7 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
     // construction; checked anyway (warp-uniform) so a violation is loud, not a
     // shared-memory overrun
     if (BH_W9_CHECK && (sp + __popc(bfr) + __popc(bmx) > kW9Fcap ||
-        gsp + sp + __popc(bfr) + __popc(bmx) > kW9Frontier || npc + __popc(bpc) > kW9List ||
+        gsp + sp + __popc(bfr) + __popc(bmx) > kW9Frontier || npf + nph + __popc(bpc) > kW9List ||
         npp + __popc(bpp) + __popc(bmx) > kW9PpList)) {
       if (lane == 0) {
         atomicOr(&f->bits, FLAG_WALK_BOUNDS);
@@ -1418,18 +1602,16 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
     }
     if (to_pp) S.pp[npp + __popc(bpp & lt)] = d.y == 1 ? make_int4(cell, 0, (int)m0, (int)m1)
                                                    : make_int4(d.x, d.y, (int)m0, (int)m1);
+    // accepted by the targets of one half only: the list's top end (scalar drain)
+    const unsigned bph = __ballot_sync(FULL, to_pc && (m0 == 0u || m1 == 0u));
     if (to_pc) {
-      const int slot = npc + __popc(bpc & lt);
-#if BH_W9_BULK
-      S.pcm[slot] = make_uint2(m0, m1);
-      bulk_copy_48(&S.pcr[slot][0], T + cell, &S.bar);
-#else
+      const bool hf = m0 == 0u || m1 == 0u;
+      const int slot = hf ? kW9List - 1 - nph - __popc(bph & lt) : npf + __popc(bpc & ~bph & lt);
       float4 b = T[cell].b;
       b.z = __int_as_float((int)m1);
       S.pcr[slot][0] = make_float4(a.x, a.y, a.z, __int_as_float((int)m0));
       S.pcr[slot][1] = b;
       S.pcr[slot][2] = T[cell].c;
-#endif
     }
     if (to_fr) {
       const int slot = sp + __popc(bfr & lt);
@@ -1448,7 +1630,8 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
       S.mxd[slot] = make_int4(dfr_rec ? cell : d.x, d.y, dfr_rec ? -1 : d.z, (int)m1);
     }
     npp += __popc(bpp);
-    npc += __popc(bpc);
+    npf += __popc(bpc & ~bph);
+    nph += __popc(bph);
     sp += __popc(bfr);
     const int nmx = __popc(bmx);
     W9S(0, 1); W9S(1, ncell); W9S(2, nmx); W9S(12, __popc(bfr));
@@ -1469,7 +1652,12 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
       const float2 DZ = __fadd2_rn(Z, f2(a.z));
       const float2 D2 = __ffma2_rn(DZ, DZ, __ffma2_rn(DY, DY, __fmul2_rn(DX, DX)));
       const bool c0 = in0 && D2.x > a.w, c1 = in1 && D2.y > a.w;  // MAC (flattree.py:295)
-      if (__any_sync(FULL, c0 || c1)) {
+      const bool any0 = __any_sync(FULL, c0), any1 = __any_sync(FULL, c1);
+      if (any0 != any1) {  // accepted by targets of one half only: scalar
+        W9S(3, 1); W9S(19, 1); W9S(16, __popc(__ballot_sync(FULL, c0)) + __popc(__ballot_sync(FULL, c1)));
+        if (any0) pc_tail(b, q, c0, DX.x, DY.x, DZ.x, D2.x, AX.x, AY.x, AZ.x, pc0);
+        else pc_tail(b, q, c1, DX.y, DY.y, DZ.y, D2.y, AX.y, AY.y, AZ.y, pc1);
+      } else if (any0) {
         W9S(3, 1); W9S(16, __popc(__ballot_sync(FULL, c0)) + __popc(__ballot_sync(FULL, c1)));
         const float2 R = f2(c0 ? rsqrtf(D2.x) : 0.f, c1 ? rsqrtf(D2.y) : 0.f);
         const float2 R2 = __fmul2_rn(R, R);
@@ -1505,11 +1693,16 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
       }
     }
     __syncwarp();
-    if (npc >= kW9Flush) { flush_pc(npc); npc = 0; }
+#if BH_W9_PPSTAGE
+    // the staged pp drain borrows the pc list's storage: drain that first
+    if (npf + nph >= kW9Flush || npp >= kW9PpFlush) { flush_pc(npf, nph); npf = nph = 0; }
+#else
+    if (npf + nph >= kW9Flush) { flush_pc(npf, nph); npf = nph = 0; }
+#endif
     if (npp >= kW9PpFlush) { flush_pp(npp); npp = 0; }
     __syncwarp();
   }
-  flush_pc(npc);
+  flush_pc(npf, nph);
   flush_pp(npp);
 
   if (MODE == kWalkResume) {  // add to pass A's results (several entries may share a target)
@@ -1576,7 +1769,7 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
     atomicAdd(&f->pp, (unsigned long long)spp);
     atomicAdd(&f->pc, (unsigned long long)spc);
 #ifdef BH_W9_STATS
-    for (int i = 0; i < 18; ++i) atomicAdd(&g_w9_stats[i], st[i]);
+    for (int i = 0; i < 24; ++i) atomicAdd(&g_w9_stats[i], st[i]);
     atomicAdd(&g_w9_stats[32 + min(31, spmax / 10)], 1ull);
 #endif
   }
