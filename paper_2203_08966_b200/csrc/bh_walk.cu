@@ -951,6 +951,9 @@ constexpr int kW9NcShift = 28;  // frontier entry: first_child | nchild << 28, u
 #ifndef BH_W9_PPPIPE
 #define BH_W9_PPPIPE 0  // 1, 2: pp passes load the next (two) pair(s) of bodies first (measured 3-4% slower)
 #endif
+#ifndef BH_W9_PPPREF
+#define BH_W9_PPPREF 0  // 1: pp drain prefetches the next pass's body lines to L1 at the start of a pass (measured neutral)
+#endif
 #ifndef BH_W9_PPSORT
 #define BH_W9_PPSORT 0  // pp drain: pack the buckets longest first (CPU model: 0.64 -> 0.55 of the broadcast iterations)
 #endif
@@ -1442,6 +1445,18 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
           c1 = n1;
         }
 #else
+#if BH_W9_PPPREF
+        // the next pass's body lines are requested now (prefetch to L1: no
+        // register, no wait); the lanes of a bucket take its 128-byte lines in turn
+        if (p + 1 < npass) {
+          const int e2n = (int)S.psel[p + 1][lane] - 1;
+          if (e2n >= 0) {
+            const int4 nn = S.pp[e2n];
+            const int rk = __popc(((unsigned)nn.z | (unsigned)nn.w) & lt);  // this lane's rank in the bucket's lane set
+            if (rk * 8 < nn.y) asm volatile("prefetch.global.L1 [%0];" ::"l"(bodies + nn.x + rk * 8));
+          }
+        }
+#endif
         // a pass whose buckets are read by targets of one half only: scalar
         const bool hx = __any_sync(FULL, u0), hy = __any_sync(FULL, u1);
         if (hx && hy) {
