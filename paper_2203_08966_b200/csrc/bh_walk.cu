@@ -1013,6 +1013,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
   }
 }
 
+// c += (bits != 0) as one predicated add (the compiler's select form is two instructions)
+#ifndef BH_W9_CNTASM
+#define BH_W9_CNTASM 1
+#endif
+__device__ __forceinline__ void w9_count(int &c, unsigned bits) {
+#if BH_W9_CNTASM
+  asm("{ .reg .pred p; setp.ne.u32 p, %1, 0; @p add.s32 %0, %0, 1; }" : "+r"(c) : "r"(bits));
+#else
+  c += bits != 0u;
+#endif
+}
+
 // Per-warp shared memory (~7.4 KB).  Masks ride in record words the drains do
 // not read: a.w (mac2) and b.z (the duplicate qxy) of a staged pc record, b.z
 // and d.w (level) of a staged mixed record.  The pc list has two ends: entries
@@ -1021,7 +1033,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
 struct W9Warp {
   int fc[kW9Fcap];         // frontier (top): first_child | nchild << kW9NcShift
   uint2 fm[kW9Fcap];       //                 (mask0, mask1)
-  float4 pcr[kW9List][3];  // accepted cells: a (mask0 in .w), b (mask1 in .z), c
+  float4 pcr[kW9List][3];  // accepted cells: a (mask0 in .w), b (mask1 in .z), c with -M in .z
   int4 pp[kW9PpList];      // pp: (lo, count, mask0, mask1) or a leaf record (cell, 0, ...)
 #if BH_W9_PPSORT
   uint8_t pord[kW9PpList]; // pp drain: the entries longest bucket first
@@ -1143,8 +1155,8 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
   __syncwarp();
 
   // one target's share of a pc entry: the scalar twin of the packed evaluation below
-  auto pc_tail = [&](const float4 b, const float4 q, bool u, float dx, float dy, float dz, float d2, float &ax,
-                     float &ay, float &az, int &cnt) {
+  auto pc_tail = [&](const float4 b, const float4 q, float nm, bool u, float dx, float dy, float dz, float d2,
+                     float &ax, float &ay, float &az, int &cnt) {  // nm = -M
     const float r = u ? rsqrtf(d2) : 0.f;
     const float r2 = __fmul_rn(r, r);
     const float qx = __fmaf_rn(q.x, dz, __fmaf_rn(b.y, dy, __fmul_rn(b.x, dx)));
@@ -1152,16 +1164,17 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
     const float qz = __fmaf_rn(q.w, dz, __fmaf_rn(q.y, dy, __fmul_rn(q.x, dx)));
     const float rqr = __fmaf_rn(dz, qz, __fmaf_rn(dy, qy, __fmul_rn(dx, qx)));
     const float r5 = __fmul_rn(__fmul_rn(r2, r2), r);
-    const float v = __fmaf_rn(__fmul_rn(rqr, r2), -2.5f, __fmul_rn(-q.z, d2));
+    const float v = __fmaf_rn(__fmul_rn(rqr, r2), -2.5f, __fmul_rn(nm, d2));
     ax = __fmaf_rn(r5, __fmaf_rn(dx, v, qx), ax);
     ay = __fmaf_rn(r5, __fmaf_rn(dy, v, qy), ay);
     az = __fmaf_rn(r5, __fmaf_rn(dz, v, qz), az);
-    cnt += u;
+    if (u) ++cnt;
   };
+  // (a staged list record: q.z holds -M)
   auto pc_one = [&](const float4 a, const float4 b, const float4 q, bool u, float x, float y, float z, float &ax,
                     float &ay, float &az, int &cnt) {
     const float dx = __fadd_rn(x, a.x), dy = __fadd_rn(y, a.y), dz = __fadd_rn(z, a.z);
-    pc_tail(b, q, u, dx, dy, dz, __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx))), ax, ay, az, cnt);
+    pc_tail(b, q, q.z, u, dx, dy, dz, __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx))), ax, ay, az, cnt);
   };
   // dense pc over the list (the FP32-pipe work): the entries [0, n) packed, two
   // targets per lane; the nh one-half entries at the list's top as scalar FFMA
@@ -1180,7 +1193,8 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
       const float4 a = S.pcr[k][0];
       const float4 b = S.pcr[k][1];
       const float4 q = S.pcr[k][2];
-      const bool u0 = (unsigned)__float_as_int(a.w) & bit, u1 = (unsigned)__float_as_int(b.z) & bit;
+      const unsigned ub0 = (unsigned)__float_as_int(a.w) & bit, ub1 = (unsigned)__float_as_int(b.z) & bit;
+      const bool u0 = ub0, u1 = ub1;
       const float2 DX = __fadd2_rn(X, f2(a.x));
       const float2 DY = __fadd2_rn(Y, f2(a.y));
       const float2 DZ = __fadd2_rn(Z, f2(a.z));
@@ -1194,19 +1208,20 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
 #if BH_W9_PC30
       // -M d/r^3 + Qd/r^5 - 2.5 (dQd) d/r^7 = r^-5 (Qd + d (-M d2 - 2.5 dQd r^-2))
       const float2 R5 = __fmul2_rn(__fmul2_rn(R2, R2), R);
-      const float2 V = __ffma2_rn(__fmul2_rn(RQR, R2), f2(-2.5f), __fmul2_rn(f2(-q.z), D2));
+      const float2 V = __ffma2_rn(__fmul2_rn(RQR, R2), f2(-2.5f), __fmul2_rn(f2(q.z), D2));
       AX = __ffma2_rn(R5, __ffma2_rn(DX, V, QX), AX);
       AY = __ffma2_rn(R5, __ffma2_rn(DY, V, QY), AY);
       AZ = __ffma2_rn(R5, __ffma2_rn(DZ, V, QZ), AZ);
 #else
       const float2 R3 = __fmul2_rn(R2, R);
       const float2 R5 = __fmul2_rn(R3, R2);
-      const float2 Sc = __fmul2_rn(__ffma2_rn(__fmul2_rn(RQR, __fmul2_rn(R2, R2)), f2(-2.5f), f2(-q.z)), R3);
+      const float2 Sc = __fmul2_rn(__ffma2_rn(__fmul2_rn(RQR, __fmul2_rn(R2, R2)), f2(-2.5f), f2(q.z)), R3);
       AX = __ffma2_rn(R5, QX, __ffma2_rn(Sc, DX, AX));
       AY = __ffma2_rn(R5, QY, __ffma2_rn(Sc, DY, AY));
       AZ = __ffma2_rn(R5, QZ, __ffma2_rn(Sc, DZ, AZ));
 #endif
-      pc0 += u0; pc1 += u1;
+      w9_count(pc0, ub0);
+      w9_count(pc1, ub1);
     }
 #pragma unroll 2
     for (int k = kW9List - nh; k < kW9List; ++k) {
@@ -1231,7 +1246,8 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
     AX = __ffma2_rn(Sc, EX, AX);
     AY = __ffma2_rn(Sc, EY, AY);
     AZ = __ffma2_rn(Sc, EZ, AZ);
-    pp0 += m0; pp1 += m1;
+    if (m0) ++pp0;
+    if (m1) ++pp1;
   };
   auto pp_one = [&](const float4 bb, bool u, float x, float y, float z, float &ax, float &ay, float &az, int &cnt) {
     const float ex = __fsub_rn(x, bb.x), ey = __fsub_rn(y, bb.y), ez = __fsub_rn(z, bb.z);
@@ -1242,7 +1258,7 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
     ax = __fmaf_rn(sc, ex, ax);
     ay = __fmaf_rn(sc, ey, ay);
     az = __fmaf_rn(sc, ez, az);
-    cnt += m;
+    if (m) ++cnt;
   };
   auto flush_pp = [&](int n) {
 #if BH_W9_PPSTAGE
@@ -1626,7 +1642,9 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
       b.z = __int_as_float((int)m1);
       S.pcr[slot][0] = make_float4(a.x, a.y, a.z, __int_as_float((int)m0));
       S.pcr[slot][1] = b;
-      S.pcr[slot][2] = T[cell].c;
+      float4 cq = T[cell].c;
+      cq.z = -cq.z;  // the drains use -M
+      S.pcr[slot][2] = cq;
     }
     if (to_fr) {
       const int slot = sp + __popc(bfr & lt);
@@ -1670,8 +1688,8 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
       const bool any0 = __any_sync(FULL, c0), any1 = __any_sync(FULL, c1);
       if (any0 != any1) {  // accepted by targets of one half only: scalar
         W9S(3, 1); W9S(19, 1); W9S(16, __popc(__ballot_sync(FULL, c0)) + __popc(__ballot_sync(FULL, c1)));
-        if (any0) pc_tail(b, q, c0, DX.x, DY.x, DZ.x, D2.x, AX.x, AY.x, AZ.x, pc0);
-        else pc_tail(b, q, c1, DX.y, DY.y, DZ.y, D2.y, AX.y, AY.y, AZ.y, pc1);
+        if (any0) pc_tail(b, q, -q.z, c0, DX.x, DY.x, DZ.x, D2.x, AX.x, AY.x, AZ.x, pc0);
+        else pc_tail(b, q, -q.z, c1, DX.y, DY.y, DZ.y, D2.y, AX.y, AY.y, AZ.y, pc1);
       } else if (any0) {
         W9S(3, 1); W9S(16, __popc(__ballot_sync(FULL, c0)) + __popc(__ballot_sync(FULL, c1)));
         const float2 R = f2(c0 ? rsqrtf(D2.x) : 0.f, c1 ? rsqrtf(D2.y) : 0.f);
@@ -1686,7 +1704,8 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
         AX = __ffma2_rn(R5, QX, __ffma2_rn(Sc, DX, AX));
         AY = __ffma2_rn(R5, QY, __ffma2_rn(Sc, DY, AY));
         AZ = __ffma2_rn(R5, QZ, __ffma2_rn(Sc, DZ, AZ));
-        pc0 += c0; pc1 += c1;
+        if (c0) ++pc0;
+        if (c1) ++pc1;
       }
       const unsigned o0 = __ballot_sync(FULL, in0 && !c0), o1 = __ballot_sync(FULL, in1 && !c1);
       if ((o0 | o1) == 0u) continue;
