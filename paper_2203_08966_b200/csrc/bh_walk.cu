@@ -1155,9 +1155,9 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
   __syncwarp();
 
   // one target's share of a pc entry: the scalar twin of the packed evaluation below
-  auto pc_tail = [&](const float4 b, const float4 q, float nm, bool u, float dx, float dy, float dz, float d2,
-                     float &ax, float &ay, float &az, int &cnt) {  // nm = -M
-    const float r = u ? rsqrtf(d2) : 0.f;
+  auto pc_tail = [&](const float4 b, const float4 q, float nm, unsigned ub, float dx, float dy, float dz, float d2,
+                     float &ax, float &ay, float &az, int &cnt) {  // nm = -M, ub != 0: the lane's target takes part
+    const float r = ub ? rsqrtf(d2) : 0.f;
     const float r2 = __fmul_rn(r, r);
     const float qx = __fmaf_rn(q.x, dz, __fmaf_rn(b.y, dy, __fmul_rn(b.x, dx)));
     const float qy = __fmaf_rn(q.y, dz, __fmaf_rn(b.w, dy, __fmul_rn(b.y, dx)));
@@ -1168,10 +1168,10 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
     ax = __fmaf_rn(r5, __fmaf_rn(dx, v, qx), ax);
     ay = __fmaf_rn(r5, __fmaf_rn(dy, v, qy), ay);
     az = __fmaf_rn(r5, __fmaf_rn(dz, v, qz), az);
-    if (u) ++cnt;
+    w9_count(cnt, ub);
   };
   // (a staged list record: q.z holds -M)
-  auto pc_one = [&](const float4 a, const float4 b, const float4 q, bool u, float x, float y, float z, float &ax,
+  auto pc_one = [&](const float4 a, const float4 b, const float4 q, unsigned u, float x, float y, float z, float &ax,
                     float &ay, float &az, int &cnt) {
     const float dx = __fadd_rn(x, a.x), dy = __fadd_rn(y, a.y), dz = __fadd_rn(z, a.z);
     pc_tail(b, q, q.z, u, dx, dy, dz, __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx))), ax, ay, az, cnt);
@@ -1679,35 +1679,36 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
       const float4 b = S.mxr[k][1];
       const float4 q = S.mxr[k][2];
       const int4 dd = S.mxd[k];
-      const bool in0 = (unsigned)__float_as_int(b.z) & bit, in1 = (unsigned)dd.w & bit;
+      const unsigned mb0 = (unsigned)__float_as_int(b.z), mb1 = (unsigned)dd.w;  // the targets that reached the cell
       const float2 DX = __fadd2_rn(X, f2(a.x));
       const float2 DY = __fadd2_rn(Y, f2(a.y));
       const float2 DZ = __fadd2_rn(Z, f2(a.z));
       const float2 D2 = __ffma2_rn(DZ, DZ, __ffma2_rn(DY, DY, __fmul2_rn(DX, DX)));
-      const bool c0 = in0 && D2.x > a.w, c1 = in1 && D2.y > a.w;  // MAC (flattree.py:295)
-      const bool any0 = __any_sync(FULL, c0), any1 = __any_sync(FULL, c1);
-      if (any0 != any1) {  // accepted by targets of one half only: scalar
-        W9S(3, 1); W9S(19, 1); W9S(16, __popc(__ballot_sync(FULL, c0)) + __popc(__ballot_sync(FULL, c1)));
-        if (any0) pc_tail(b, q, -q.z, c0, DX.x, DY.x, DZ.x, D2.x, AX.x, AY.x, AZ.x, pc0);
-        else pc_tail(b, q, -q.z, c1, DX.y, DY.y, DZ.y, D2.y, AX.y, AY.y, AZ.y, pc1);
-      } else if (any0) {
-        W9S(3, 1); W9S(16, __popc(__ballot_sync(FULL, c0)) + __popc(__ballot_sync(FULL, c1)));
+      const bool c0 = (mb0 & bit) && D2.x > a.w, c1 = (mb1 & bit) && D2.y > a.w;  // MAC (flattree.py:295)
+      const unsigned A0 = __ballot_sync(FULL, c0), A1 = __ballot_sync(FULL, c1);  // the accepting targets
+      if (A0 && A1) {
+        W9S(3, 1); W9S(16, __popc(A0) + __popc(A1));
         const float2 R = f2(c0 ? rsqrtf(D2.x) : 0.f, c1 ? rsqrtf(D2.y) : 0.f);
         const float2 R2 = __fmul2_rn(R, R);
-        const float2 R3 = __fmul2_rn(R2, R);
-        const float2 R5 = __fmul2_rn(R3, R2);
         const float2 QX = __ffma2_rn(f2(q.x), DZ, __ffma2_rn(f2(b.y), DY, __fmul2_rn(f2(b.x), DX)));
         const float2 QY = __ffma2_rn(f2(q.y), DZ, __ffma2_rn(f2(b.w), DY, __fmul2_rn(f2(b.y), DX)));
         const float2 QZ = __ffma2_rn(f2(q.w), DZ, __ffma2_rn(f2(q.y), DY, __fmul2_rn(f2(q.x), DX)));
         const float2 RQR = __ffma2_rn(DZ, QZ, __ffma2_rn(DY, QY, __fmul2_rn(DX, QX)));
-        const float2 Sc = __fmul2_rn(__ffma2_rn(__fmul2_rn(RQR, __fmul2_rn(R2, R2)), f2(-2.5f), f2(-q.z)), R3);
-        AX = __ffma2_rn(R5, QX, __ffma2_rn(Sc, DX, AX));
-        AY = __ffma2_rn(R5, QY, __ffma2_rn(Sc, DY, AY));
-        AZ = __ffma2_rn(R5, QZ, __ffma2_rn(Sc, DZ, AZ));
-        if (c0) ++pc0;
-        if (c1) ++pc1;
+        const float2 R5 = __fmul2_rn(__fmul2_rn(R2, R2), R);  // the 30-op form of flush_pc
+        const float2 V = __ffma2_rn(__fmul2_rn(RQR, R2), f2(-2.5f), __fmul2_rn(f2(-q.z), D2));
+        AX = __ffma2_rn(R5, __ffma2_rn(DX, V, QX), AX);
+        AY = __ffma2_rn(R5, __ffma2_rn(DY, V, QY), AY);
+        AZ = __ffma2_rn(R5, __ffma2_rn(DZ, V, QZ), AZ);
+        w9_count(pc0, A0 & bit);
+        w9_count(pc1, A1 & bit);
+      } else if (A0) {  // accepted by targets of one half only: scalar
+        W9S(3, 1); W9S(19, 1); W9S(16, __popc(A0));
+        pc_tail(b, q, -q.z, A0 & bit, DX.x, DY.x, DZ.x, D2.x, AX.x, AY.x, AZ.x, pc0);
+      } else if (A1) {
+        W9S(3, 1); W9S(19, 1); W9S(16, __popc(A1));
+        pc_tail(b, q, -q.z, A1 & bit, DX.y, DY.y, DZ.y, D2.y, AX.y, AY.y, AZ.y, pc1);
       }
-      const unsigned o0 = __ballot_sync(FULL, in0 && !c0), o1 = __ballot_sync(FULL, in1 && !c1);
+      const unsigned o0 = mb0 & ~A0, o1 = mb1 & ~A1;  // the targets that open it
       if ((o0 | o1) == 0u) continue;
       W9S(15, 1);
       if (dd.z > 0) {
