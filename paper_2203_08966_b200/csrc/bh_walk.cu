@@ -1234,15 +1234,16 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
     }
   };
   // dense pp over the bodies of the listed leaves / buckets (self skipped by r2 > 0)
+  // (E = body - target and +m: the same bits as (target - body) and -m, one negation fewer)
   auto pp_body = [&](const float4 bb, bool u0, bool u1) {
-    const float2 EX = __ffma2_rn(f2(bb.x), f2(-1.f), X);
-    const float2 EY = __ffma2_rn(f2(bb.y), f2(-1.f), Y);
-    const float2 EZ = __ffma2_rn(f2(bb.z), f2(-1.f), Z);
+    const float2 EX = __ffma2_rn(X, f2(-1.f), f2(bb.x));
+    const float2 EY = __ffma2_rn(Y, f2(-1.f), f2(bb.y));
+    const float2 EZ = __ffma2_rn(Z, f2(-1.f), f2(bb.z));
     const float2 Q2 = __ffma2_rn(EZ, EZ, __ffma2_rn(EY, EY, __fmul2_rn(EX, EX)));
     const bool m0 = u0 && Q2.x > 0.f, m1 = u1 && Q2.y > 0.f;
     const float2 W = __fadd2_rn(Q2, E2);
     const float2 R = f2(m0 ? rsqrtf(W.x) : 0.f, m1 ? rsqrtf(W.y) : 0.f);
-    const float2 Sc = __fmul2_rn(__fmul2_rn(R, R), __fmul2_rn(R, f2(-bb.w)));
+    const float2 Sc = __fmul2_rn(__fmul2_rn(R, R), __fmul2_rn(R, f2(bb.w)));
     AX = __ffma2_rn(Sc, EX, AX);
     AY = __ffma2_rn(Sc, EY, AY);
     AZ = __ffma2_rn(Sc, EZ, AZ);
@@ -1250,11 +1251,11 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
     if (m1) ++pp1;
   };
   auto pp_one = [&](const float4 bb, bool u, float x, float y, float z, float &ax, float &ay, float &az, int &cnt) {
-    const float ex = __fsub_rn(x, bb.x), ey = __fsub_rn(y, bb.y), ez = __fsub_rn(z, bb.z);
+    const float ex = __fsub_rn(bb.x, x), ey = __fsub_rn(bb.y, y), ez = __fsub_rn(bb.z, z);
     const float q2 = __fmaf_rn(ez, ez, __fmaf_rn(ey, ey, __fmul_rn(ex, ex)));
     const bool m = u && q2 > 0.f;
     const float r = m ? rsqrtf(__fadd_rn(q2, e2)) : 0.f;
-    const float sc = __fmul_rn(__fmul_rn(r, r), __fmul_rn(r, -bb.w));
+    const float sc = __fmul_rn(__fmul_rn(r, r), __fmul_rn(r, bb.w));
     ax = __fmaf_rn(sc, ex, ax);
     ay = __fmaf_rn(sc, ey, ay);
     az = __fmaf_rn(sc, ez, az);
@@ -1475,26 +1476,28 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
 #endif
         // a pass whose buckets are read by targets of one half only: scalar
         const bool hx = __any_sync(FULL, u0), hy = __any_sync(FULL, u1);
+        // (a lane past its bucket's end re-reads the last body, masked: c0 = c1 = 0 without a bucket)
+        const int ilast = lo + max(cnt - 1, 0), c0 = u0 ? cnt : 0, c1 = u1 ? cnt : 0;
+        int ib = lo;
         if (hx && hy) {
 #pragma unroll(kBucketUnroll)
           for (int j = 0; j < len; ++j) {
-            const bool v = j < cnt;
-            const float4 bb = bodies[v ? lo + j : lo];
-            pp_body(bb, u0 && v, u1 && v);
+            pp_body(bodies[ib], j < c0, j < c1);
+            ib = min(ib + 1, ilast);
           }
         } else if (hx) {
           W9S(20, 1); W9S(21, len);
 #pragma unroll(kBucketUnroll)
           for (int j = 0; j < len; ++j) {
-            const bool v = j < cnt;
-            pp_one(bodies[v ? lo + j : lo], u0 && v, X.x, Y.x, Z.x, AX.x, AY.x, AZ.x, pp0);
+            pp_one(bodies[ib], j < c0, X.x, Y.x, Z.x, AX.x, AY.x, AZ.x, pp0);
+            ib = min(ib + 1, ilast);
           }
         } else {
           W9S(20, 1); W9S(21, len);
 #pragma unroll(kBucketUnroll)
           for (int j = 0; j < len; ++j) {
-            const bool v = j < cnt;
-            pp_one(bodies[v ? lo + j : lo], u1 && v, X.y, Y.y, Z.y, AX.y, AY.y, AZ.y, pp1);
+            pp_one(bodies[ib], j < c1, X.y, Y.y, Z.y, AX.y, AY.y, AZ.y, pp1);
+            ib = min(ib + 1, ilast);
           }
         }
 #endif

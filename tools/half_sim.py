@@ -96,3 +96,7 @@ def pp_cost_slots(grp, K):
 
 t_ = sum(pp_cost_slots(grp, 64) for grp in pp)
 print(f"pp packed K=64 on 64 target slots: {t_ / base:.3f} of broadcast body iterations")
+
+full = sum(e.all() for g in pc_cert for e in g)
+tot_ = sum(len(g) for g in pc_cert)
+print(f"pc certain entries with a full mask: {full / tot_:.3f}")
