@@ -942,9 +942,6 @@ constexpr int kW9PpUnroll = BH_W9_PPUNROLL;
 constexpr int kW9StageF4 = 128;  // BH_W9_PPSTAGE: bodies per staging buffer (2 KB)
 constexpr int kW9NcShift = 28;  // frontier entry: first_child | nchild << 28, unsigned (records < 2^28)
 
-#ifndef BH_W9_PC30
-#define BH_W9_PC30 1  // pc: a += R5 (Qd + d (-M d2 - 2.5 dQd R2)): 30 packed FP ops instead of 31
-#endif
 #ifndef BH_W9_PPPACK
 #define BH_W9_PPPACK 1  // pp drain: buckets with disjoint lane sets share a pass (see flush_pp)
 #endif
@@ -964,7 +961,7 @@ constexpr int kW9NcShift = 28;  // frontier entry: first_child | nchild << 28, u
 //  8 pp bucket entries  9 pp passes  10 pass body iterations  11 bucket (target, body) slots used
 //  12 frontier pushes (certain-open)  13 pc flushes  14 pp flushes  15 mixed opened (pushed / bucket)
 //  16 mixed accepting target bits  17 bucket entries' mask bits
-//  18 pc entries of one half (scalar drain)  19 mixed cells accepted by one half only
+//  18 pc entries with full masks (unmasked drain)  19 mixed cells accepted by one half only
 //  20 pp passes of one half  21 their body iterations
 __device__ unsigned long long g_w9_stats[64];  // [32, 64): histogram of the warp's peak frontier depth / 10
 extern "C" int bh_debug_w9_stats(unsigned long long *out, int reset) {
@@ -1028,8 +1025,8 @@ __device__ __forceinline__ void w9_count(int &c, unsigned bits) {
 // Per-warp shared memory (~7.4 KB).  Masks ride in record words the drains do
 // not read: a.w (mac2) and b.z (the duplicate qxy) of a staged pc record, b.z
 // and d.w (level) of a staged mixed record.  The pc list has two ends: entries
-// with targets in both halves of the warp (mask0 and mask1 non-zero) fill it
-// from the bottom, entries of one half only from the top (see flush_pc).
+// that every target of the warp reached (both masks full) fill it from the
+// bottom, masked entries from the top (see flush_pc).
 struct W9Warp {
   int fc[kW9Fcap];         // frontier (top): first_child | nchild << kW9NcShift
   uint2 fm[kW9Fcap];       //                 (mask0, mask1)
@@ -1124,7 +1121,7 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
   const unsigned bit = 1u << lane;
   const unsigned lt = bit - 1u;
 
-  int sp = 1, npf = 0, nph = 0, npp = 0;  // pc entries (both halves / one half), pp entries
+  int sp = 1, npf = 0, nph = 0, npp = 0;  // pc entries (every target / masked), pp entries
   int gsp = 0, slot = -1;  // spilled entries, spill slot (warp-uniform)
 #ifdef BH_W9_STATS
   unsigned long long st[24] = {};
@@ -1170,67 +1167,56 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
     az = __fmaf_rn(r5, __fmaf_rn(dz, v, qz), az);
     w9_count(cnt, ub);
   };
-  // (a staged list record: q.z holds -M)
-  auto pc_one = [&](const float4 a, const float4 b, const float4 q, unsigned u, float x, float y, float z, float &ax,
-                    float &ay, float &az, int &cnt) {
-    const float dx = __fadd_rn(x, a.x), dy = __fadd_rn(y, a.y), dz = __fadd_rn(z, a.z);
-    pc_tail(b, q, q.z, u, dx, dy, dz, __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx))), ax, ay, az, cnt);
+  // dense pc over the list (the FP32-pipe work), two targets per lane: the nf
+  // entries at the bottom are reached by every target of the warp (no masks,
+  // counted once per flush), the nm entries at the list's top carry masks
+  auto pc_eval = [&](const float4 a, const float4 b, const float4 q, const float2 R, const float2 DX, const float2 DY,
+                     const float2 DZ, const float2 D2) {
+    const float2 R2 = __fmul2_rn(R, R);
+    const float2 QX = __ffma2_rn(f2(q.x), DZ, __ffma2_rn(f2(b.y), DY, __fmul2_rn(f2(b.x), DX)));
+    const float2 QY = __ffma2_rn(f2(q.y), DZ, __ffma2_rn(f2(b.w), DY, __fmul2_rn(f2(b.y), DX)));
+    const float2 QZ = __ffma2_rn(f2(q.w), DZ, __ffma2_rn(f2(q.y), DY, __fmul2_rn(f2(q.x), DX)));
+    const float2 RQR = __ffma2_rn(DZ, QZ, __ffma2_rn(DY, QY, __fmul2_rn(DX, QX)));
+    // -M d/r^3 + Qd/r^5 - 2.5 (dQd) d/r^7 = r^-5 (Qd + d (-M d2 - 2.5 dQd r^-2)): 30 packed ops (q.z = -M)
+    const float2 R5 = __fmul2_rn(__fmul2_rn(R2, R2), R);
+    const float2 V = __ffma2_rn(__fmul2_rn(RQR, R2), f2(-2.5f), __fmul2_rn(f2(q.z), D2));
+    AX = __ffma2_rn(R5, __ffma2_rn(DX, V, QX), AX);
+    AY = __ffma2_rn(R5, __ffma2_rn(DY, V, QY), AY);
+    AZ = __ffma2_rn(R5, __ffma2_rn(DZ, V, QZ), AZ);
   };
-  // dense pc over the list (the FP32-pipe work): the entries [0, n) packed, two
-  // targets per lane; the nh one-half entries at the list's top as scalar FFMA
-  // on the half their targets are in
-  auto flush_pc = [&](int n, int nh) {
-    W9S(13, n + nh > 0); W9S(4, n + nh);
+  auto flush_pc = [&](int nf, int nm) {
+    W9S(13, nf + nm > 0); W9S(4, nf + nm); W9S(18, nf);
 #ifdef BH_W9_STATS
-    for (int k = 0; k < n; ++k)
+    W9S(5, 64ull * nf);
+    for (int k = kW9List - nm; k < kW9List; ++k)
       W9S(5, __popc((unsigned)__float_as_int(S.pcr[k][0].w)) + __popc((unsigned)__float_as_int(S.pcr[k][1].z)));
-    for (int k = kW9List - nh; k < kW9List; ++k)
-      W9S(5, __popc((unsigned)__float_as_int(S.pcr[k][0].w)) + __popc((unsigned)__float_as_int(S.pcr[k][1].z)));
-    W9S(18, nh);
 #endif
 #pragma unroll(kW9PcUnroll)
-    for (int k = 0; k < n; ++k) {
+    for (int k = 0; k < nf; ++k) {
       const float4 a = S.pcr[k][0];
       const float4 b = S.pcr[k][1];
       const float4 q = S.pcr[k][2];
-      const unsigned ub0 = (unsigned)__float_as_int(a.w) & bit, ub1 = (unsigned)__float_as_int(b.z) & bit;
-      const bool u0 = ub0, u1 = ub1;
       const float2 DX = __fadd2_rn(X, f2(a.x));
       const float2 DY = __fadd2_rn(Y, f2(a.y));
       const float2 DZ = __fadd2_rn(Z, f2(a.z));
       const float2 D2 = __ffma2_rn(DZ, DZ, __ffma2_rn(DY, DY, __fmul2_rn(DX, DX)));
-      const float2 R = f2(u0 ? rsqrtf(D2.x) : 0.f, u1 ? rsqrtf(D2.y) : 0.f);
-      const float2 R2 = __fmul2_rn(R, R);
-      const float2 QX = __ffma2_rn(f2(q.x), DZ, __ffma2_rn(f2(b.y), DY, __fmul2_rn(f2(b.x), DX)));
-      const float2 QY = __ffma2_rn(f2(q.y), DZ, __ffma2_rn(f2(b.w), DY, __fmul2_rn(f2(b.y), DX)));
-      const float2 QZ = __ffma2_rn(f2(q.w), DZ, __ffma2_rn(f2(q.y), DY, __fmul2_rn(f2(q.x), DX)));
-      const float2 RQR = __ffma2_rn(DZ, QZ, __ffma2_rn(DY, QY, __fmul2_rn(DX, QX)));
-#if BH_W9_PC30
-      // -M d/r^3 + Qd/r^5 - 2.5 (dQd) d/r^7 = r^-5 (Qd + d (-M d2 - 2.5 dQd r^-2))
-      const float2 R5 = __fmul2_rn(__fmul2_rn(R2, R2), R);
-      const float2 V = __ffma2_rn(__fmul2_rn(RQR, R2), f2(-2.5f), __fmul2_rn(f2(q.z), D2));
-      AX = __ffma2_rn(R5, __ffma2_rn(DX, V, QX), AX);
-      AY = __ffma2_rn(R5, __ffma2_rn(DY, V, QY), AY);
-      AZ = __ffma2_rn(R5, __ffma2_rn(DZ, V, QZ), AZ);
-#else
-      const float2 R3 = __fmul2_rn(R2, R);
-      const float2 R5 = __fmul2_rn(R3, R2);
-      const float2 Sc = __fmul2_rn(__ffma2_rn(__fmul2_rn(RQR, __fmul2_rn(R2, R2)), f2(-2.5f), f2(q.z)), R3);
-      AX = __ffma2_rn(R5, QX, __ffma2_rn(Sc, DX, AX));
-      AY = __ffma2_rn(R5, QY, __ffma2_rn(Sc, DY, AY));
-      AZ = __ffma2_rn(R5, QZ, __ffma2_rn(Sc, DZ, AZ));
-#endif
-      w9_count(pc0, ub0);
-      w9_count(pc1, ub1);
+      pc_eval(a, b, q, f2(rsqrtf(D2.x), rsqrtf(D2.y)), DX, DY, DZ, D2);
     }
-#pragma unroll 2
-    for (int k = kW9List - nh; k < kW9List; ++k) {
+    pc0 += nf;
+    pc1 += nf;
+#pragma unroll(kW9PcUnroll)
+    for (int k = kW9List - nm; k < kW9List; ++k) {
       const float4 a = S.pcr[k][0];
       const float4 b = S.pcr[k][1];
       const float4 q = S.pcr[k][2];
-      const unsigned mk0 = (unsigned)__float_as_int(a.w), mk1 = (unsigned)__float_as_int(b.z);
-      if (mk0) pc_one(a, b, q, mk0 & bit, X.x, Y.x, Z.x, AX.x, AY.x, AZ.x, pc0);  // warp-uniform
-      else pc_one(a, b, q, mk1 & bit, X.y, Y.y, Z.y, AX.y, AY.y, AZ.y, pc1);
+      const unsigned ub0 = (unsigned)__float_as_int(a.w) & bit, ub1 = (unsigned)__float_as_int(b.z) & bit;
+      const float2 DX = __fadd2_rn(X, f2(a.x));
+      const float2 DY = __fadd2_rn(Y, f2(a.y));
+      const float2 DZ = __fadd2_rn(Z, f2(a.z));
+      const float2 D2 = __ffma2_rn(DZ, DZ, __ffma2_rn(DY, DY, __fmul2_rn(DX, DX)));
+      pc_eval(a, b, q, f2(ub0 ? rsqrtf(D2.x) : 0.f, ub1 ? rsqrtf(D2.y) : 0.f), DX, DY, DZ, D2);
+      w9_count(pc0, ub0);
+      w9_count(pc1, ub1);
     }
   };
   // dense pp over the bodies of the listed leaves / buckets (self skipped by r2 > 0)
@@ -1636,10 +1622,10 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
     }
     if (to_pp) S.pp[npp + __popc(bpp & lt)] = d.y == 1 ? make_int4(cell, 0, (int)m0, (int)m1)
                                                    : make_int4(d.x, d.y, (int)m0, (int)m1);
-    // accepted by the targets of one half only: the list's top end (scalar drain)
-    const unsigned bph = __ballot_sync(FULL, to_pc && (m0 == 0u || m1 == 0u));
+    // accepted cells that only some of the warp's targets reached: the list's top end (masked drain)
+    const unsigned bph = __ballot_sync(FULL, to_pc && (m0 & m1) != FULL);
     if (to_pc) {
-      const bool hf = m0 == 0u || m1 == 0u;
+      const bool hf = (m0 & m1) != FULL;
       const int slot = hf ? kW9List - 1 - nph - __popc(bph & lt) : npf + __popc(bpc & ~bph & lt);
       float4 b = T[cell].b;
       b.z = __int_as_float((int)m1);

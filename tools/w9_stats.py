@@ -25,7 +25,7 @@ L.bh_debug_w9_stats(h, 1)
 st = eng.stats()
 names = ["batches", "cells", "mixed", "mixed_acc", "pc_entries", "pc_bits", "leaf_entries", "leaf_bits",
          "bucket_entries", "passes", "pass_iters", "bucket_slots_used", "frontier_push", "pc_flushes",
-         "pp_flushes", "mixed_opened", "mixed_acc_bits", "bucket_bits", "pc_half_entries", "mixed_half_acc",
+         "pp_flushes", "mixed_opened", "mixed_acc_bits", "bucket_bits", "pc_full_entries", "mixed_half_acc",
          "half_passes", "half_pass_iters"]
 d = {k: int(h[i]) for i, k in enumerate(names)}
 n = len(b)
