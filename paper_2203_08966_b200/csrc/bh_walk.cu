@@ -912,7 +912,7 @@ struct W9Spill {
 #define BH_W9_FLUSH 20
 #endif
 #ifndef BH_W9_PPFLUSH
-#define BH_W9_PPFLUSH 64
+#define BH_W9_PPFLUSH 128
 #endif
 constexpr int kW9Flush = BH_W9_FLUSH;      // the pc list is drained at >= kW9Flush entries
 constexpr int kW9List = kW9Flush + 32;     // a batch adds <= 32
