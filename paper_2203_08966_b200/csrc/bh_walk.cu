@@ -871,7 +871,9 @@ __global__ void __launch_bounds__(kWalkBlock, BH_WALK_MINB) k_walk(
 // fails it is opened by every target (certain-open); only the rest (mixed)
 // need the per-target test.  Cells are classified 32 at a time, one per lane,
 // taken from a frontier of (first_child, nchild, mask0, mask1) entries:
-//   certain-accept -> pc list (the record, masks)      evaluated densely
+//   certain-accept -> pc list (the record, masks)      evaluated densely; cells that
+//            every target of the warp reached (about half) are listed apart and
+//            drained with no masks, predicates or per-entry counters
 //   leaf / certain-open bucket -> pp list (lo, count | cell, 0 for a leaf, masks)
 //   certain-open internal -> frontier entry (its children, same masks)
 //   mixed -> per-target MAC, warp-uniform (as k_walk): pc for the accepting
