@@ -1039,7 +1039,7 @@ struct W9Warp {
 #endif
   union {
     struct {
-      float4 mxr[32][3];   // mixed cells of the batch: a, b (mask0 in .z), c
+      float4 mxr[32][3];   // mixed cells of the batch: a, b (mask0 in .z), c with -M in .z
       int4 mxd[32];        //                           d (mask1 in .w)
     };
     uint8_t psel[32][32];  // pp drain (after the batch): entry + 1 of each lane in each pass
@@ -1648,7 +1648,9 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
       b.z = __int_as_float((int)m0);
       S.mxr[slot][0] = a;
       S.mxr[slot][1] = b;
-      S.mxr[slot][2] = T[cell].c;
+      float4 cq = T[cell].c;
+      cq.z = -cq.z;  // -M, as in the pc list
+      S.mxr[slot][2] = cq;
       // a deferrable record (pass A) keeps its index, flagged by nchild = -1
       const bool dfr_rec = MODE == kWalkDefer && d.z == 0 && (d.w & kDeferBit);
       S.mxd[slot] = make_int4(dfr_rec ? cell : d.x, d.y, dfr_rec ? -1 : d.z, (int)m1);
@@ -1686,7 +1688,7 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
         const float2 QZ = __ffma2_rn(f2(q.w), DZ, __ffma2_rn(f2(q.y), DY, __fmul2_rn(f2(q.x), DX)));
         const float2 RQR = __ffma2_rn(DZ, QZ, __ffma2_rn(DY, QY, __fmul2_rn(DX, QX)));
         const float2 R5 = __fmul2_rn(__fmul2_rn(R2, R2), R);  // the 30-op form of flush_pc
-        const float2 V = __ffma2_rn(__fmul2_rn(RQR, R2), f2(-2.5f), __fmul2_rn(f2(-q.z), D2));
+        const float2 V = __ffma2_rn(__fmul2_rn(RQR, R2), f2(-2.5f), __fmul2_rn(f2(q.z), D2));
         AX = __ffma2_rn(R5, __ffma2_rn(DX, V, QX), AX);
         AY = __ffma2_rn(R5, __ffma2_rn(DY, V, QY), AY);
         AZ = __ffma2_rn(R5, __ffma2_rn(DZ, V, QZ), AZ);
@@ -1694,10 +1696,10 @@ __global__ void __launch_bounds__(kW9Block, BH_W9_MINB) k_walk9(
         w9_count(pc1, A1 & bit);
       } else if (A0) {  // accepted by targets of one half only: scalar
         W9S(3, 1); W9S(19, 1); W9S(16, __popc(A0));
-        pc_tail(b, q, -q.z, A0 & bit, DX.x, DY.x, DZ.x, D2.x, AX.x, AY.x, AZ.x, pc0);
+        pc_tail(b, q, q.z, A0 & bit, DX.x, DY.x, DZ.x, D2.x, AX.x, AY.x, AZ.x, pc0);
       } else if (A1) {
         W9S(3, 1); W9S(19, 1); W9S(16, __popc(A1));
-        pc_tail(b, q, -q.z, A1 & bit, DX.y, DY.y, DZ.y, D2.y, AX.y, AY.y, AZ.y, pc1);
+        pc_tail(b, q, q.z, A1 & bit, DX.y, DY.y, DZ.y, D2.y, AX.y, AY.y, AZ.y, pc1);
       }
       const unsigned o0 = mb0 & ~A0, o1 = mb1 & ~A1;  // the targets that open it
       if ((o0 | o1) == 0u) continue;
