@@ -242,6 +242,9 @@ __device__ __forceinline__ unsigned block_excl_scan(unsigned v, unsigned *wsum, 
   return woff + incl - v;
 }
 
+#ifndef BH_SORT_RANKASM
+#define BH_SORT_RANKASM 1
+#endif
 template <int MINB, bool MATCH>
 __global__ void __launch_bounds__(kSortThreads, MINB) k_sort_pass(
     const uint64_t *__restrict__ kin, const uint32_t *vin, uint64_t *__restrict__ kout,
@@ -301,8 +304,20 @@ __global__ void __launch_bounds__(kSortThreads, MINB) k_sort_pass(
     } else {
 #pragma unroll
       for (int b = 0; b < kDigitBits; ++b) {
+#if BH_SORT_RANKASM
+        // one bit test feeds the vote and the mask: 4 instructions per bit (the
+        // compiler derived the predicate twice: ~8)
+        asm("{ .reg .pred p; .reg .b32 t, m;\n"
+            "  and.b32 t, %1, %2; setp.ne.u32 p, t, 0;\n"
+            "  vote.sync.ballot.b32 t, p, 0xffffffff;\n"
+            "  selp.b32 m, 0xffffffff, 0, p;\n"
+            "  xor.b32 t, t, m; not.b32 t, t; and.b32 %0, %0, t; }"
+            : "+r"(peers)
+            : "r"(d), "r"(1u << b));
+#else
         const unsigned bb = __ballot_sync(FULL, (d >> b) & 1u);
         peers &= ((d >> b) & 1u) ? bb : ~bb;
+#endif
       }
     }
     rank[j] = peers;
