@@ -215,6 +215,19 @@ void launch_branch_export(const TreeView &t, const int *branch, int nb, const in
 // range.  The walk's epilogue stores each target's acceleration and work into
 // every peer as well as locally, so no all-reduce follows the walk.
 constexpr int kMaxPeers = 7;
+// peers &= lanes whose bit `bitmask` of d equals this lane's (one step of a
+// ballot match): one bit test feeds the vote and the mask -- 3-4 instructions,
+// where `p ? bb : ~bb` in C++ made the compiler derive the predicate twice (~8)
+__device__ __forceinline__ void match_bit(unsigned &peers, unsigned d, unsigned bitmask) {
+  asm("{ .reg .pred p; .reg .b32 t, m;\n"
+      "  and.b32 t, %1, %2; setp.ne.u32 p, t, 0;\n"
+      "  vote.sync.ballot.b32 t, p, 0xffffffff;\n"
+      "  selp.b32 m, 0xffffffff, 0, p;\n"
+      "  xor.b32 t, t, m; not.b32 t, t; and.b32 %0, %0, t; }"
+      : "+r"(peers)
+      : "r"(d), "r"(bitmask));
+}
+
 struct W9Peers {
   int n = 0;
   float *acc[kMaxPeers] = {};

@@ -305,15 +305,7 @@ __global__ void __launch_bounds__(kSortThreads, MINB) k_sort_pass(
 #pragma unroll
       for (int b = 0; b < kDigitBits; ++b) {
 #if BH_SORT_RANKASM
-        // one bit test feeds the vote and the mask: 4 instructions per bit (the
-        // compiler derived the predicate twice: ~8)
-        asm("{ .reg .pred p; .reg .b32 t, m;\n"
-            "  and.b32 t, %1, %2; setp.ne.u32 p, t, 0;\n"
-            "  vote.sync.ballot.b32 t, p, 0xffffffff;\n"
-            "  selp.b32 m, 0xffffffff, 0, p;\n"
-            "  xor.b32 t, t, m; not.b32 t, t; and.b32 %0, %0, t; }"
-            : "+r"(peers)
-            : "r"(d), "r"(1u << b));
+        match_bit(peers, d, 1u << b);  // (bh_internal.cuh)
 #else
         const unsigned bb = __ballot_sync(FULL, (d >> b) & 1u);
         peers &= ((d >> b) & 1u) ? bb : ~bb;

@@ -2072,10 +2072,7 @@ __global__ void __launch_bounds__(kHilThreads, BH_HIL_MINB) k_hilbert_chunks(con
       const unsigned d = (v[r] >> sh) & 31u;
       unsigned peers = 0xffffffffu;
 #pragma unroll
-      for (int b = 0; b < 5; ++b) {
-        const unsigned bb = __ballot_sync(0xffffffffu, (d >> b) & 1u);
-        peers &= ((d >> b) & 1u) ? bb : ~bb;
-      }
+      for (int b = 0; b < 5; ++b) match_bit(peers, d, 1u << b);
       const unsigned base = wh[w][d];
       __syncwarp();
       if (lane == 31u - __clz(peers)) wh[w][d] = base + __popc(peers);
