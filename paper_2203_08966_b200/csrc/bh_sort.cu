@@ -242,6 +242,12 @@ __device__ __forceinline__ unsigned block_excl_scan(unsigned v, unsigned *wsum, 
   return woff + incl - v;
 }
 
+#ifndef BH_SORT_FULL_LOAD
+#define BH_SORT_FULL_LOAD 0  // 1: full tiles load without bounds tests (cfg3 -1.9%, cfg4 +1.7%)
+#endif
+#ifndef BH_SORT_FULL_SCATTER
+#define BH_SORT_FULL_SCATTER 1
+#endif
 #ifndef BH_SORT_RANKASM
 #define BH_SORT_RANKASM 1
 #endif
@@ -272,6 +278,17 @@ __global__ void __launch_bounds__(kSortThreads, MINB) k_sort_pass(
 #if !BH_SORT_VIDX
   uint32_t v[kSortItems];
 #endif
+  const bool full_tile = tbase + kTile <= n;  // (block-uniform) every tile but the last: no bounds tests
+  if (BH_SORT_FULL_LOAD && full_tile) {
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+      const int64_t i = wbase + 32 * j + lane;
+      k[j] = __ldcs(kin + i);
+#if !BH_SORT_VIDX
+      v[j] = vin ? __ldcs(vin + i) : (uint32_t)i;
+#endif
+    }
+  } else
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
     const int64_t i = wbase + 32 * j + lane;
@@ -383,6 +400,19 @@ __global__ void __launch_bounds__(kSortThreads, MINB) k_sort_pass(
   __syncthreads();
 
   // ---- scatter: consecutive tile slots of one digit go to consecutive addresses
+#if !BH_SORT_VIDX
+  if (BH_SORT_FULL_SCATTER && full_tile) {
+#pragma unroll 4
+    for (int i = threadIdx.x; i < kTile; i += kSortThreads) {
+      const uint64_t key = S.keys[i];
+      const unsigned di = (unsigned)(key >> shift) & (kBins - 1);
+      const long long g = S.gdelta[di] + i;
+      kout[g] = key;
+      vout[g] = S.vals[i];
+    }
+    return;
+  }
+#endif
 #pragma unroll 4
   for (int i = threadIdx.x; i < kTile; i += kSortThreads) {
     const uint64_t key = S.keys[i];
