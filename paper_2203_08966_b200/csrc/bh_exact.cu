@@ -373,7 +373,10 @@ constexpr int kEmitHalo = 64;  // >= L
 __global__ void __launch_bounds__(kEmitThreads) k_emit_mark(TreeView t, const float4 *__restrict__ bod32,
                                                             int *__restrict__ creators, int *__restrict__ ncreators) {
   __shared__ uint64_t ks[kEmitThreads + 2 * kEmitHalo];
-  __shared__ int8_t ws[kEmitThreads + kEmitHalo];
+  // W as 16-bit values, read two at a time: the window maximum below is packed
+  // (VIMNMX3.S16x2); byte reads with their sign extensions were 4 instructions
+  // per element, 132 per body at L = 32
+  __shared__ __align__(8) int16_t ws[kEmitThreads + kEmitHalo + 2];
   const int64_t n = t.n;
   const int C = (int)tree_count(t);
   if (C > t.C) return;  // sync-free build overflowed its capacity (flagged; redone)
@@ -386,7 +389,7 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit_mark(TreeView t, const fl
   __syncthreads();
   for (int k = threadIdx.x; k < kEmitThreads + kEmitHalo; k += kEmitThreads) {
     const int64_t a = b0 - kEmitHalo + k;  // ws[k] = W(a), -1 without a full window
-    ws[k] = (int8_t)(a >= 0 && a + L < n ? lcp_of(ks[k], ks[k + L]) : -1);
+    ws[k] = (int16_t)(a >= 0 && a + L < n ? lcp_of(ks[k], ks[k + L]) : -1);
   }
   __syncthreads();
   const int64_t i = b0 + threadIdx.x;
@@ -413,9 +416,17 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit_mark(TreeView t, const fl
     if (i == 0 && t.bnd_prev >= 0) depth = max(depth, min(t.bnd_prev + 1, kMaxLevel));
     if (i == n - 1 && t.bnd_next >= 0) depth = max(depth, min(t.bnd_next + 1, kMaxLevel));
     const int start = i > 0 ? lp : 0;
-    int maxw = -1;
-#pragma unroll 4
-    for (int a = li - L; a <= li; ++a) maxw = max(maxw, (int)ws[a]);
+    // max of W over the elements [li - L, li]; -1 (0xffff) is the identity
+    const unsigned *w32 = reinterpret_cast<const unsigned *>(ws);
+    const int wlo = li - L, wa = wlo >> 1, wb = li >> 1;
+    unsigned acc = w32[wa];
+    if (wlo & 1) acc |= 0x0000ffffu;                   // element wlo - 1 is outside
+    unsigned last = w32[wb];
+    if (!(li & 1)) last |= 0xffff0000u;                // element li + 1 is outside
+    acc = wa == wb ? (acc | (last & 0xffff0000u)) : __vmaxs2(acc, last);
+    for (int q = wa + 1; q < wb; q += 2)
+      acc = __vimax3_s16x2(acc, w32[q], q + 1 < wb ? w32[q + 1] : 0xffffffffu);
+    const int maxw = max((int)(short)(acc & 0xffffu), (int)(short)(acc >> 16));
     creator = n > 1 && (start == 0 || start <= maxw);
     if (creator) {  // the rows of the opened cells this body creates: all slots absent
       const int base = 1 + (int)t.off[i];
