@@ -130,10 +130,17 @@ __device__ __forceinline__ double4 ldcg4(const double4 *p) {
 
 // hashed.py:376-388 _lcp_levels: 21 - ceil(bitlen(a ^ b) / 3)
 __device__ __forceinline__ int lcp_of(uint64_t a, uint64_t b) {
-  uint64_t x = a ^ b;
-  int bits = x ? 64 - __clzll((long long)x) : 0;
-  return kMortonBits - (bits + 2) / 3;
+  // kMortonBits - ceil(bits / 3) with bits = the position of the highest
+  // differing bit + 1, written on 32-bit halves (the 64-bit clz and the
+  // division compiled to twice the instructions): for x != 0 it is
+  // 20 - p / 3 with p the highest set bit, and p / 3 = (43 p) >> 7 for p < 64
+  const uint64_t x = a ^ b;
+  const uint32_t hi = (uint32_t)(x >> 32), lo = (uint32_t)x;
+  if (x == 0) return kMortonBits;
+  const int p = hi ? 63 - __clz((int)hi) : 31 - __clz((int)lo);
+  return kMortonBits - 1 - ((p * 43) >> 7);
 }
+static_assert(kMortonBits == 21, "lcp_of: 21 levels of 3 bits");
 
 // hashed.py:475-489: sortedness / duplicate checks, lcp, depth, cells per body.
 // newc[i] = depth[i] - start[i] with start = lcp[i-1] (0 for i = 0).
